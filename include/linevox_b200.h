@@ -1,0 +1,265 @@
+/*
+ * linevox_b200.h -- C ABI of liblinevox_b200.so, the B200 (sm_100a) drop-in for
+ * the hot path of the `linevox` reference (arXiv 1801.01155):
+ *   voxelize -> LoD -> ray-cast (+ density-grid AO / soft shadows).
+ *
+ * Conventions
+ *   - every entry point returns int: 0 = ok, nonzero = LVX_E_* (never throws);
+ *     lvx_last_error() gives a thread-local message for the last failure;
+ *   - every `*_d` / device pointer is CALLER-OWNED device memory (e.g. the
+ *     data_ptr() of a torch CUDA tensor).  The library never allocates device
+ *     memory behind the caller's back; scratch space is passed in explicitly;
+ *   - `stream` is a cudaStream_t passed as void*; all work is enqueued on it and
+ *     the call returns without synchronising unless stated otherwise;
+ *   - plain C types only: no torch / C++ types cross this boundary.
+ *
+ * Each declaration cites the reference interface it replaces
+ * (paths relative to /root/reference/pkg/src/linevox/).
+ */
+#ifndef LINEVOX_B200_H
+#define LINEVOX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LVX_OK 0
+#define LVX_E_INVALID 1   /* bad argument */
+#define LVX_E_CUDA 2      /* CUDA runtime error (see lvx_last_error) */
+#define LVX_E_NO_DEVICE 3 /* no sm_100-class device visible */
+#define LVX_E_RANGE 4     /* size exceeds a documented limit */
+
+#define LVX_ABI_VERSION 1
+
+/* mode codes: _kernels.py:43-55 */
+#define LVX_OPACITY_CONSTANT 0
+#define LVX_OPACITY_TRANSFER 1
+#define LVX_OPACITY_DISTANCE 2
+#define LVX_SHADOW_NONE 0
+#define LVX_SHADOW_HARD 1     /* not built (SURVEY 8f "next") -> LVX_E_INVALID */
+#define LVX_SHADOW_REPLINES 2 /* not built (SURVEY 8f "next") -> LVX_E_INVALID */
+#define LVX_SHADOW_CONE 3
+#define LVX_AO_NONE 0
+#define LVX_AO_HEMISPHERE 1 /* not built (SURVEY 8f "next") -> LVX_E_INVALID */
+#define LVX_AO_DENSITY 2
+#define LVX_AO_PRECOMPUTED 3
+
+/* caps that are part of the reference's observable behaviour (_kernels.py:36-38) */
+#define LVX_MAX_WINDOW_HITS 1024
+#define LVX_MAX_SEEN 256
+#define LVX_MAX_LEVELS 24
+
+int lvx_abi_version(void);
+const char *lvx_last_error(void);
+/* 0 when a compute-capability 10.x device is current; LVX_E_NO_DEVICE otherwise. */
+int lvx_device_check(void);
+
+/* ------------------------------------------------------------------------- */
+/* Voxelizer: replaces _plane_events/_clip_batch/_faces_and_bins/             */
+/* build_voxel_model/_pack_all (voxelizer.py:174-263, 358-394, 397-488).      */
+/*                                                                           */
+/* Input batch layout (what voxelizer.py:419-425 concatenates per chunk):     */
+/*   pts_d   f64 [P,3]  vertices of all curves, curve after curve             */
+/*   attrs_d f64 [P]    per-vertex attribute                                  */
+/*   curve_off_d i64 [n_curves+1]  first vertex of each curve, last = P       */
+/* The parallel unit is the polyline EDGE (vertex i -> i+1).                  */
+/* ------------------------------------------------------------------------- */
+
+/* first_d u8[P]: 1 at the first vertex of every curve (the reference's
+ * `point_curve[1:] == point_curve[:-1]` test, voxelizer.py:216). */
+int lvx_mark_curve_starts(const int64_t *curve_off_d, int64_t n_curves, int64_t n_points,
+                          uint8_t *first_d, void *stream);
+
+/* Pass 1: clip every edge, count kept chords per voxel (atomics).
+ * vox_cnt_d u32[V] must be zeroed by the caller.  dims = (rx, ry, rz). */
+int lvx_voxelize_count(const double *pts_d, const uint8_t *first_d, int64_t n_points,
+                       const int32_t dims[3], uint32_t *vox_cnt_d, void *stream);
+
+/* Device prefix sums over the V voxel counters (voxelizer.py:442-449, 462-466):
+ *   cursor_d  u32[V]  exclusive scan of the RAW counts (scatter cursors)
+ *   offsets_d u32[V]  exclusive scan of min(count,255)  (final headers)
+ *   counts_d  u8[V]   min(count,255)
+ *   totals_d  u64[2]  {raw chords, kept segments}
+ * scratch_d: lvx_scan_scratch_bytes(V) bytes. */
+size_t lvx_scan_scratch_bytes(int64_t n);
+int lvx_voxel_scan(const uint32_t *vox_cnt_d, int64_t n_voxels, uint32_t *cursor_d,
+                   uint32_t *offsets_d, uint8_t *counts_d, uint64_t *totals_d,
+                   void *scratch_d, void *stream);
+
+/* Pass 2: clip again and scatter one raw record per kept chord into its voxel's
+ * range (slot = atomicAdd(cursor[lin])).  After the call cursor_d[lin] is the END
+ * of voxel lin's raw range.  Raw record (SoA):
+ *   raw_key_d u64[S_raw]  (edge index << 16) | kept-chord ordinal inside the edge
+ *                          -- strictly increasing in (curve, chord order)
+ *   raw_q_d   u64[S_raw]  face_in | bin_in<<3 | face_out<<19 | bin_out<<22 | attr<<38
+ *   raw_lin_d u32[S_raw]  voxel linear index
+ * edge_kept_d u16[P] (nullable): kept chords ending in each edge (for seg_order).
+ * err_d i32[1]: set to 1 if an endpoint is off every face (voxelizer.py:366-368). */
+int lvx_voxelize_emit(const double *pts_d, const double *attrs_d, const uint8_t *first_d,
+                      int64_t n_points, const int32_t dims[3], int32_t n_bins,
+                      uint32_t *cursor_d, uint64_t *raw_key_d, uint64_t *raw_q_d,
+                      uint32_t *raw_lin_d, uint16_t *edge_kept_d, int32_t *err_d,
+                      void *stream);
+
+/* Pass 3: order every voxel's list by key (== the reference's stable sort by
+ * voxel, voxelizer.py:435-438), keep rank < 255, lid = rank % 32, decode
+ * endpoints to bin centres, pack.  Any output pointer except packed_d may be
+ * NULL to skip that derived cache.
+ *   packed_d u8[S*w], seg_a_d/seg_b_d f32[S,3], seg_attr_d/seg_lid_d u8[S],
+ *   seg_voxel_d i32[S,3], seg_face_in/out_d u8[S], seg_bin_in/out_d u16[S],
+ *   seg_key_d u64[S] (provenance key of each kept segment),
+ *   seg_rec_d 32-byte render records [S] (see lvx_seg_record). */
+typedef struct {
+    float ax, ay, az;
+    uint32_t meta; /* attr | lid << 8 */
+    float bx, by, bz;
+    uint32_t pad;
+} lvx_seg_record;
+
+int lvx_voxelize_compact(const uint64_t *raw_key_d, const uint64_t *raw_q_d,
+                         const uint32_t *raw_lin_d, int64_t n_raw,
+                         const uint32_t *vox_cnt_d, const uint32_t *cursor_end_d,
+                         const uint32_t *offsets_d, const int32_t dims[3], int32_t n_bins,
+                         uint8_t *packed_d, float *seg_a_d, float *seg_b_d,
+                         uint8_t *seg_attr_d, uint8_t *seg_lid_d, int32_t *seg_voxel_d,
+                         uint8_t *seg_face_in_d, uint16_t *seg_bin_in_d,
+                         uint8_t *seg_face_out_d, uint16_t *seg_bin_out_d,
+                         uint64_t *seg_key_d, lvx_seg_record *seg_rec_d, void *stream);
+
+/* Generic exclusive scan u16 -> u32 (edge_kept -> edge_base), same scratch rule. */
+int lvx_scan_u16(const uint16_t *in_d, int64_t n, uint32_t *out_d, void *scratch_d,
+                 void *stream);
+
+/* seg_curve / seg_order (voxelizer.py:254-262, 486-487) from provenance keys. */
+int lvx_provenance(const uint64_t *seg_key_d, int64_t n_seg, const uint32_t *edge_base_d,
+                   const int64_t *curve_off_d, int64_t n_curves, int32_t *seg_curve_d,
+                   int32_t *seg_order_d, void *stream);
+
+/* Rebuild the 32-byte render records from the reference-layout caches (used when
+ * a model arrives from host arrays, e.g. a decoded .vxl). */
+int lvx_build_seg_records(const float *seg_a_d, const float *seg_b_d,
+                          const uint8_t *seg_attr_d, const uint8_t *seg_lid_d, int64_t n_seg,
+                          lvx_seg_record *seg_rec_d, void *stream);
+
+/* ------------------------------------------------------------------------- */
+/* LoD: compute_density_level0 (lod.py:82-94), _coarsen/build_octree          */
+/* (lod.py:97-119), _occupancy_dilated (raycast.py:351-366).                  */
+/* ------------------------------------------------------------------------- */
+
+int lvx_density_l0(const uint8_t *counts_d, const uint32_t *offsets_d,
+                   const lvx_seg_record *seg_rec_d, const float *table_d, int64_t n_voxels,
+                   float *level0_d, void *stream);
+
+/* Host helper: level offsets/dims of the flat octree buffer (_octree_args,
+ * raycast.py:369-388).  off[n_levels+1], ldims[n_levels*3] as (dx,dy,dz). */
+int lvx_octree_layout(const int32_t dims[3], int64_t *off, int64_t *ldims, int32_t *n_levels);
+
+/* Fills levels 1.. of flat_d (level 0 already at offset 0) with the 2x2x2 means. */
+int lvx_build_octree(float *flat_d, const int32_t dims[3], void *stream);
+
+int lvx_occupancy_dilate(const uint8_t *counts_d, const int32_t dims[3], uint8_t *occ_d,
+                         void *stream);
+
+/* ------------------------------------------------------------------------- */
+/* Ray-caster: render_rows + stream_hit + dda_collect + tube/sphere + sort     */
+/* (_kernels.py:76-341, 625-923) and the density-grid secondary rays           */
+/* (cone_blocking :386-422, ao_density_point :592-605, trilinear :346-383).    */
+/* ------------------------------------------------------------------------- */
+
+typedef struct {
+    double o[3], r[3], u[3], f[3]; /* position, right, up, forward: _camera_args raycast.py:335-341 */
+    double tan_half, aspect;
+    int32_t width, height;
+} lvx_camera;
+
+typedef struct {
+    int32_t rx, ry, rz;
+    int32_t _pad;
+    const uint8_t *counts_d;
+    const uint32_t *offsets_d;
+    const lvx_seg_record *seg_rec_d;
+    const float *table_d;      /* f32[256,4] */
+    const uint8_t *occ_d;      /* u8[(rz+2)(ry+2)(rx+2)] */
+} lvx_model;
+
+typedef struct {
+    double tube_r, base_alpha, tau;
+    double ka, kd, ks, shininess;
+    double light[3];
+    double bg[4];
+    int32_t opacity_mode, neighbor, joints, headlight;
+    int32_t shadow_mode, ao_mode, ao_n_rays, _pad;
+    double ao_radius;
+} lvx_params;
+
+typedef struct {
+    const float *oct_flat_d;           /* flat octree (nullable when unused) */
+    int64_t oct_off[LVX_MAX_LEVELS + 1];
+    int64_t oct_dims[LVX_MAX_LEVELS * 3];
+    int32_t n_levels, _pad;
+    const float *ao_flat_d;            /* baked AO field f32[V] (nullable) */
+    const double *ao_dirs_d;           /* f64[ao_n_rays,3] hemisphere lattice (nullable) */
+} lvx_lod;
+
+/* Screen partition for multi-GPU: the image is cut into tile_w x tile_h pixel
+ * tiles numbered row-major; this call renders tiles tile_first, tile_first +
+ * tile_step, ...  With compact != 0 the output is the rank's tiles back to back
+ * ([n_my_tiles, tile_h, tile_w, 4] f32, the NCCL send buffer); otherwise pixels
+ * are written in place into the full (H, W, 4) image. */
+typedef struct {
+    int32_t tile_w, tile_h, tile_first, tile_step, compact, _pad;
+} lvx_tiling;
+
+/* img_d f32, row_stats_d i64[H,3] (steps, tests, overflow; caller zeroes it),
+ * hitbuf_d: per-thread hit scratch, lvx_render_scratch_bytes() bytes. */
+size_t lvx_render_scratch_bytes(const lvx_camera *cam, const lvx_tiling *tiling);
+int lvx_render(const lvx_camera *cam, const lvx_model *model, const lvx_params *params,
+               const lvx_lod *lod, const lvx_tiling *tiling, float *img_d,
+               int64_t *row_stats_d, void *scratch_d, void *stream);
+
+/* Scatter compact tiles (any rank's send buffer) into the full image. */
+int lvx_untile(const float *tiles_d, const lvx_tiling *tiling, int32_t width, int32_t height,
+               float *img_d, void *stream);
+
+/* ------------------------------------------------------------------------- */
+/* AO bake: precompute_ao_kernel (_kernels.py:608-620) + the clip/cast of      */
+/* precompute_voxel_ao (illumination.py:193-214).                              */
+/* ------------------------------------------------------------------------- */
+
+/* Host: Fibonacci lattice (fibonacci_dir, _kernels.py:541-552) with libm cos/sin. */
+int lvx_fibonacci_dirs(int32_t n, int32_t hemisphere, double jitter, double *out_host);
+
+int lvx_ao_bake(const uint8_t *counts_d, const int32_t dims[3], int32_t n_rays,
+                double radius, double step, const double *dirs_d, const float *level0_d,
+                float *ao_d, void *stream);
+
+/* ------------------------------------------------------------------------- */
+/* Point probes (the Python-level reference ops used by the parity tests):     */
+/* traverse_voxels raycast.py:170-181, intersect_ray_tube/sphere :184-213,     */
+/* cone_soft_shadow / ao_density_rays / sample_ao illumination.py:142-225.     */
+/* ------------------------------------------------------------------------- */
+
+/* windows of one ray: out_vox_d i64[cap,3], out_t_d f64[cap,2], n_d i64[1] */
+int lvx_probe_dda(const double o[3], const double d[3], const int32_t dims[3], int32_t pad,
+                  int64_t cap, int64_t *out_vox_d, double *out_t_d, int64_t *n_d, void *stream);
+/* n queries; rays_d f64[n,6] (o,d); a_d,b_d f32[n,3] (f32_axis=1: the frame-kernel
+ * specialisation) or f64[n,3] (f32_axis=0); out_d f64[n,6] = hit,t_in,t_out,normal */
+int lvx_probe_tube(const double *rays_d, const void *a_d, const void *b_d, double radius,
+                   int32_t f32_axis, int64_t n, double *out_d, void *stream);
+int lvx_probe_sphere(const double *rays_d, const double *c_d, double radius, int64_t n,
+                     double *out_d, void *stream);
+int lvx_probe_trilinear(const float *flat_d, int64_t off, const int64_t ldims[3], double scale,
+                        const double *pts_d, int64_t n, double *out_d, void *stream);
+int lvx_probe_cone(const lvx_lod *lod, const double *pts_d, const double light[3],
+                   double eps, int64_t n, double *out_d, void *stream);
+int lvx_probe_ao_density(const lvx_lod *lod, const double *pts_d, const double *normals_d,
+                         int32_t n_rays, double radius, double step, const double *dirs_d,
+                         int64_t n, double *out_d, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LINEVOX_B200_H */

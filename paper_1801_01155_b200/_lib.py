@@ -1,0 +1,147 @@
+"""ctypes binding of liblinevox_b200.so (the C ABI in include/linevox_b200.h).
+
+There is no CPU fallback: if the shared library is missing, or no sm_100-class
+device is visible when a compute entry point is called, this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblinevox_b200.so")
+
+MAX_LEVELS = 24
+
+
+class LvxError(RuntimeError):
+    """A C-ABI call returned a nonzero status."""
+
+
+class Camera(C.Structure):
+    _fields_ = [("o", C.c_double * 3), ("r", C.c_double * 3), ("u", C.c_double * 3),
+                ("f", C.c_double * 3), ("tan_half", C.c_double), ("aspect", C.c_double),
+                ("width", C.c_int32), ("height", C.c_int32)]
+
+
+class Model(C.Structure):
+    _fields_ = [("rx", C.c_int32), ("ry", C.c_int32), ("rz", C.c_int32), ("_pad", C.c_int32),
+                ("counts_d", C.c_void_p), ("offsets_d", C.c_void_p), ("seg_rec_d", C.c_void_p),
+                ("table_d", C.c_void_p), ("occ_d", C.c_void_p)]
+
+
+class Params(C.Structure):
+    _fields_ = [("tube_r", C.c_double), ("base_alpha", C.c_double), ("tau", C.c_double),
+                ("ka", C.c_double), ("kd", C.c_double), ("ks", C.c_double),
+                ("shininess", C.c_double), ("light", C.c_double * 3), ("bg", C.c_double * 4),
+                ("opacity_mode", C.c_int32), ("neighbor", C.c_int32), ("joints", C.c_int32),
+                ("headlight", C.c_int32), ("shadow_mode", C.c_int32), ("ao_mode", C.c_int32),
+                ("ao_n_rays", C.c_int32), ("_pad", C.c_int32), ("ao_radius", C.c_double)]
+
+
+class Lod(C.Structure):
+    _fields_ = [("oct_flat_d", C.c_void_p), ("oct_off", C.c_int64 * (MAX_LEVELS + 1)),
+                ("oct_dims", C.c_int64 * (MAX_LEVELS * 3)), ("n_levels", C.c_int32),
+                ("_pad", C.c_int32), ("ao_flat_d", C.c_void_p), ("ao_dirs_d", C.c_void_p)]
+
+
+class Tiling(C.Structure):
+    _fields_ = [("tile_w", C.c_int32), ("tile_h", C.c_int32), ("tile_first", C.c_int32),
+                ("tile_step", C.c_int32), ("compact", C.c_int32), ("_pad", C.c_int32)]
+
+
+# every symbol include/linevox_b200.h declares (tests check the library exports all)
+SYMBOLS = [
+    "lvx_abi_version", "lvx_last_error", "lvx_device_check",
+    "lvx_mark_curve_starts", "lvx_voxelize_count", "lvx_scan_scratch_bytes", "lvx_voxel_scan",
+    "lvx_voxelize_emit", "lvx_voxelize_compact", "lvx_scan_u16", "lvx_provenance",
+    "lvx_build_seg_records", "lvx_density_l0", "lvx_octree_layout", "lvx_build_octree",
+    "lvx_occupancy_dilate", "lvx_render_scratch_bytes", "lvx_render", "lvx_untile",
+    "lvx_fibonacci_dirs", "lvx_ao_bake", "lvx_probe_dda", "lvx_probe_tube", "lvx_probe_sphere",
+    "lvx_probe_trilinear", "lvx_probe_cone", "lvx_probe_ao_density",
+]
+
+_lib = None
+
+
+def lib():
+    """The loaded library.  Raises if it was never built (no silent fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                "g.build()'` (nvcc, sm_100a).  This package has no CPU fallback.")
+        L = C.CDLL(LIB_PATH)
+        L.lvx_last_error.restype = C.c_char_p
+        L.lvx_scan_scratch_bytes.restype = C.c_size_t
+        L.lvx_scan_scratch_bytes.argtypes = [C.c_int64]
+        L.lvx_render_scratch_bytes.restype = C.c_size_t
+        for name in SYMBOLS:
+            fn = getattr(L, name)
+            if name not in ("lvx_last_error", "lvx_scan_scratch_bytes", "lvx_render_scratch_bytes"):
+                fn.restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        msg = lib().lvx_last_error().decode("utf-8", "replace")
+        if rc == 1:
+            raise ValueError(msg)
+        raise LvxError(f"liblinevox_b200 error {rc}: {msg}")
+
+
+_device_ok = False
+
+
+def require_device():
+    """torch CUDA device + sm_100 check; called at the top of every compute path."""
+    global _device_ok
+    import torch
+    if not _device_ok:
+        if not torch.cuda.is_available():
+            raise LvxError("no CUDA device: paper_1801_01155_b200 runs on B200 (sm_100a) only "
+                           "and has no CPU fallback")
+        torch.cuda.init()
+        check(lib().lvx_device_check())
+        _device_ok = True
+    return torch
+
+
+def stream_ptr():
+    import torch
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t):
+    """Device pointer of a torch tensor (None -> NULL)."""
+    if t is None:
+        return C.c_void_p(0)
+    return C.c_void_p(t.data_ptr())
+
+
+def i32x3(v):
+    return (C.c_int32 * 3)(int(v[0]), int(v[1]), int(v[2]))
+
+
+def f64x3(v):
+    return (C.c_double * 3)(float(v[0]), float(v[1]), float(v[2]))
+
+
+def to_device(a: np.ndarray, dtype=None):
+    """Host numpy -> device tensor on the current stream (pinned staging is the
+    caller's business; numpy memory is pageable)."""
+    torch = require_device()
+    a = np.ascontiguousarray(a, dtype=dtype)
+    return torch.from_numpy(a).to("cuda", non_blocking=False)
+
+
+def fibonacci_dirs(n: int, hemisphere: int, jitter: float = 0.0) -> np.ndarray:
+    out = np.empty((int(n), 3), dtype=np.float64)
+    check(lib().lvx_fibonacci_dirs(C.c_int32(int(n)), C.c_int32(int(hemisphere)),
+                                   C.c_double(float(jitter)), out.ctypes.data_as(C.c_void_p)))
+    return out

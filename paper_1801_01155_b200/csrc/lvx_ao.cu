@@ -1,0 +1,228 @@
+// AO bake and point probes for sm_100a.
+//
+//   precompute_ao_kernel / precompute_voxel_ao   _kernels.py:608-620, illumination.py:193-214
+//   probes: traverse_voxels raycast.py:170-181, intersect_ray_tube/sphere :184-213,
+//           cone_soft_shadow / ao_density_rays / sample_ao illumination.py:142-225
+#include <math_constants.h>
+
+#include "lvx_geom.cuh"
+
+namespace {
+
+// One thread per voxel.  Occupied voxels integrate n_rays full-sphere density rays
+// from the voxel centre (normal (0,0,1)); rays are summed in lattice order in
+// float64, the mean is clipped to [0,1] and cast to float32.  The direction lattice
+// is staged in shared memory (n_rays * 24 bytes).
+__global__ void __launch_bounds__(128)
+ao_bake_kernel(const u8 *__restrict__ counts, int rx, int ry, int rz, int n_rays, double radius,
+               double step, const double *__restrict__ dirs, const float *__restrict__ l0,
+               float *__restrict__ out) {
+    extern __shared__ double s_dirs[];
+    for (int k = threadIdx.x; k < 3 * n_rays; k += blockDim.x) s_dirs[k] = dirs[k];
+    __syncthreads();
+    // 4x4x8 voxel bricks per block keep a warp's samples inside a few cache lines
+    const int bx = blockIdx.x * 4, by = blockIdx.y * 4, bz = blockIdx.z * 8;
+    const int x = bx + (threadIdx.x & 3), y = by + ((threadIdx.x >> 2) & 3), z = bz + (threadIdx.x >> 4);
+    if (x >= rx || y >= ry || z >= rz) return;
+    const i64 lin = x + (i64)rx * (y + (i64)ry * z);
+    float res = 0.0f;
+    if (counts[lin] != 0) {
+        double v = lvx_ao_density_point((double)x + 0.5, (double)y + 0.5, (double)z + 0.5, 0.0, 0.0,
+                                        1.0, n_rays, radius, step, s_dirs, l0, rx, ry, rz);
+        v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+        res = (float)v;
+    }
+    out[lin] = res;
+}
+
+__global__ void probe_dda_kernel(double ox, double oy, double oz, double dx, double dy, double dz,
+                                 int rx, int ry, int rz, int pad, i64 cap, i64 *out_vox,
+                                 double *out_t, i64 *n_out) {
+    LvxDda dda;
+    dda.init(ox, oy, oz, dx, dy, dz, rx, ry, rz, pad);
+    i64 n = 0;
+    int wx, wy, wz;
+    double t0, t1;
+    while (dda.next(wx, wy, wz, t0, t1)) {
+        if (n < cap) {
+            out_vox[3 * n] = wx;
+            out_vox[3 * n + 1] = wy;
+            out_vox[3 * n + 2] = wz;
+            out_t[2 * n] = t0;
+            out_t[2 * n + 1] = t1;
+            n += 1;
+        }
+    }
+    *n_out = n;
+}
+
+__device__ __forceinline__ void store_hit(double *o, bool hit, const LvxHit &h) {
+    o[0] = hit ? 1.0 : 0.0;
+    o[1] = hit ? h.t_in : 0.0;
+    o[2] = hit ? h.t_out : 0.0;
+    o[3] = hit ? h.nx : 0.0;
+    o[4] = hit ? h.ny : 0.0;
+    o[5] = hit ? h.nz : 0.0;
+}
+
+__global__ void probe_tube_kernel(const double *__restrict__ rays, const void *a_, const void *b_,
+                                  double r, int f32_axis, i64 n, double *__restrict__ out) {
+    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double *q = rays + 6 * i;
+    LvxHit h;
+    bool hit;
+    if (f32_axis) {
+        const float *a = (const float *)a_ + 3 * i, *b = (const float *)b_ + 3 * i;
+        hit = lvx_tube_f32axis(q[0], q[1], q[2], q[3], q[4], q[5], a[0], a[1], a[2], b[0], b[1], b[2], r, h);
+    } else {
+        const double *a = (const double *)a_ + 3 * i, *b = (const double *)b_ + 3 * i;
+        hit = lvx_tube_f64(q[0], q[1], q[2], q[3], q[4], q[5], a[0], a[1], a[2], b[0], b[1], b[2], r, h);
+    }
+    store_hit(out + 6 * i, hit, h);
+}
+
+__global__ void probe_sphere_kernel(const double *__restrict__ rays, const double *__restrict__ c,
+                                    double r, i64 n, double *__restrict__ out) {
+    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double *q = rays + 6 * i;
+    LvxHit h;
+    const bool hit = lvx_sphere<true>(q[0], q[1], q[2], q[3], q[4], q[5], c[3 * i], c[3 * i + 1],
+                                      c[3 * i + 2], r, h);
+    store_hit(out + 6 * i, hit, h);
+}
+
+__global__ void probe_trilinear_kernel(const float *__restrict__ flat, i64 off, int ldx, int ldy,
+                                       int ldz, double scale, const double *__restrict__ pts, i64 n,
+                                       double *__restrict__ out) {
+    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    out[i] = lvx_trilinear(flat, off, ldx, ldy, ldz, scale, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+}
+
+__global__ void probe_cone_kernel(const LvxOctree oc, const double *__restrict__ pts, double lx,
+                                  double ly, double lz, double eps, i64 n, double *__restrict__ out) {
+    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    out[i] = lvx_cone_blocking(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], lx, ly, lz, oc,
+                               (double)oc.dims[0], (double)oc.dims[1], (double)oc.dims[2], eps);
+}
+
+__global__ void probe_ao_kernel(const LvxOctree oc, const double *__restrict__ pts,
+                                const double *__restrict__ nrm, int n_rays, double radius,
+                                double step, const double *__restrict__ dirs, i64 n,
+                                double *__restrict__ out) {
+    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    out[i] = lvx_ao_density_point(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], nrm[3 * i],
+                                  nrm[3 * i + 1], nrm[3 * i + 2], n_rays, radius, step, dirs,
+                                  oc.flat, oc.dims[0], oc.dims[1], oc.dims[2]);
+}
+
+int fill_octree(LvxOctree &oc, const lvx_lod *lod) {
+    LVX_REQUIRE(lod && lod->oct_flat_d && lod->n_levels >= 1 && lod->n_levels <= LVX_MAX_LEVELS,
+                "a density octree is required");
+    memset(&oc, 0, sizeof(oc));
+    oc.flat = lod->oct_flat_d;
+    oc.n_levels = lod->n_levels;
+    for (int l = 0; l <= lod->n_levels; ++l) oc.off[l] = lod->oct_off[l];
+    for (int l = 0; l < lod->n_levels * 3; ++l) oc.dims[l] = (int)lod->oct_dims[l];
+    return LVX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lvx_ao_bake(const uint8_t *counts_d, const int32_t dims[3], int32_t n_rays, double radius,
+                double step, const double *dirs_d, const float *level0_d, float *ao_d,
+                void *stream) {
+    LVX_REQUIRE(counts_d && dims && dirs_d && level0_d && ao_d, "null argument");
+    LVX_REQUIRE(dims[0] >= 1 && dims[1] >= 1 && dims[2] >= 1, "grid dims must be >= 1");
+    LVX_REQUIRE(n_rays >= 1 && n_rays <= 8192, "n_rays must be in [1, 8192], got %d", n_rays);
+    LVX_REQUIRE(radius > 0.0 && step > 0.0, "radius and step must be positive");
+    dim3 grid((unsigned)lvx_ceil_div(dims[0], 4), (unsigned)lvx_ceil_div(dims[1], 4),
+              (unsigned)lvx_ceil_div(dims[2], 8));
+    const size_t smem = (size_t)n_rays * 3 * sizeof(double);
+    if (smem > 48 * 1024)
+        LVX_CUDA_CHECK(cudaFuncSetAttribute(ao_bake_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)smem));
+    ao_bake_kernel<<<grid, 128, smem, (cudaStream_t)stream>>>(counts_d, dims[0], dims[1], dims[2],
+                                                             n_rays, radius, step, dirs_d, level0_d,
+                                                             ao_d);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_probe_dda(const double o[3], const double d[3], const int32_t dims[3], int32_t pad,
+                  int64_t cap, int64_t *out_vox_d, double *out_t_d, int64_t *n_d, void *stream) {
+    LVX_REQUIRE(o && d && dims && out_vox_d && out_t_d && n_d && cap >= 0 && pad >= 0, "bad arguments");
+    probe_dda_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(o[0], o[1], o[2], d[0], d[1], d[2], dims[0],
+                                                       dims[1], dims[2], pad, cap, out_vox_d,
+                                                       out_t_d, n_d);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_probe_tube(const double *rays_d, const void *a_d, const void *b_d, double radius,
+                   int32_t f32_axis, int64_t n, double *out_d, void *stream) {
+    LVX_REQUIRE(n >= 0, "bad arguments");
+    if (n == 0) return LVX_OK;
+    LVX_REQUIRE(rays_d && a_d && b_d && out_d, "null argument");
+    probe_tube_kernel<<<(unsigned)lvx_ceil_div(n, 128), 128, 0, (cudaStream_t)stream>>>(
+        rays_d, a_d, b_d, radius, f32_axis, n, out_d);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_probe_sphere(const double *rays_d, const double *c_d, double radius, int64_t n,
+                     double *out_d, void *stream) {
+    LVX_REQUIRE(n >= 0, "bad arguments");
+    if (n == 0) return LVX_OK;
+    LVX_REQUIRE(rays_d && c_d && out_d, "null argument");
+    probe_sphere_kernel<<<(unsigned)lvx_ceil_div(n, 128), 128, 0, (cudaStream_t)stream>>>(
+        rays_d, c_d, radius, n, out_d);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_probe_trilinear(const float *flat_d, int64_t off, const int64_t ldims[3], double scale,
+                        const double *pts_d, int64_t n, double *out_d, void *stream) {
+    LVX_REQUIRE(n >= 0 && ldims, "bad arguments");
+    if (n == 0) return LVX_OK;
+    LVX_REQUIRE(flat_d && pts_d && out_d, "null argument");
+    probe_trilinear_kernel<<<(unsigned)lvx_ceil_div(n, 128), 128, 0, (cudaStream_t)stream>>>(
+        flat_d, off, (int)ldims[0], (int)ldims[1], (int)ldims[2], scale, pts_d, n, out_d);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_probe_cone(const lvx_lod *lod, const double *pts_d, const double light[3], double eps,
+                   int64_t n, double *out_d, void *stream) {
+    LvxOctree oc;
+    if (int rc = fill_octree(oc, lod)) return rc;
+    LVX_REQUIRE(n >= 0 && light, "bad arguments");
+    if (n == 0) return LVX_OK;
+    LVX_REQUIRE(pts_d && out_d, "null argument");
+    probe_cone_kernel<<<(unsigned)lvx_ceil_div(n, 128), 128, 0, (cudaStream_t)stream>>>(
+        oc, pts_d, light[0], light[1], light[2], eps, n, out_d);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_probe_ao_density(const lvx_lod *lod, const double *pts_d, const double *normals_d,
+                         int32_t n_rays, double radius, double step, const double *dirs_d,
+                         int64_t n, double *out_d, void *stream) {
+    LvxOctree oc;
+    if (int rc = fill_octree(oc, lod)) return rc;
+    LVX_REQUIRE(n >= 0 && n_rays >= 1, "bad arguments");
+    if (n == 0) return LVX_OK;
+    LVX_REQUIRE(pts_d && normals_d && dirs_d && out_d, "null argument");
+    probe_ao_kernel<<<(unsigned)lvx_ceil_div(n, 64), 64, 0, (cudaStream_t)stream>>>(
+        oc, pts_d, normals_d, n_rays, radius, step, dirs_d, n, out_d);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,47 @@
+// Shared host/device helpers for liblinevox_b200.so (sm_100a only).
+//
+// Arithmetic contract: the reference is IEEE float64 (and a few float32 islands)
+// with NO fused multiply-add.  Every translation unit is compiled with
+// -fmad=false so `a*b+c` stays two roundings; f32 divide/sqrt keep the default
+// IEEE-exact (-prec-div/-prec-sqrt) code paths.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/linevox_b200.h"
+
+typedef int64_t i64;
+typedef uint8_t u8;
+typedef uint16_t u16;
+typedef uint32_t u32;
+typedef uint64_t u64;
+
+void lvx_set_error(const char *fmt, ...);
+
+#define LVX_CUDA_CHECK(expr)                                                            \
+    do {                                                                                \
+        cudaError_t _e = (expr);                                                        \
+        if (_e != cudaSuccess) {                                                        \
+            lvx_set_error("%s:%d: %s -> %s", __FILE__, __LINE__, #expr,                 \
+                          cudaGetErrorString(_e));                                      \
+            return LVX_E_CUDA;                                                          \
+        }                                                                               \
+    } while (0)
+
+#define LVX_LAUNCH_CHECK() LVX_CUDA_CHECK(cudaGetLastError())
+
+#define LVX_REQUIRE(cond, ...)                                                          \
+    do {                                                                                \
+        if (!(cond)) {                                                                  \
+            lvx_set_error(__VA_ARGS__);                                                 \
+            return LVX_E_INVALID;                                                       \
+        }                                                                               \
+    } while (0)
+
+static inline i64 lvx_ceil_div(i64 a, i64 b) { return (a + b - 1) / b; }
+
+// number of SMs of the current device (148 on B200); grids of persistent-style
+// kernels are sized as a multiple of it
+int lvx_sm_count();

@@ -1,0 +1,447 @@
+// Device-side geometry shared by the ray-caster, the AO bake and the point probes.
+// Each function restates one numba kernel of the reference (_kernels.py) in IEEE
+// float64 without FMA contraction (the TU is compiled with -fmad=false).
+#pragma once
+#include "lvx_common.cuh"
+
+struct LvxHit {
+    double t_in, t_out, nx, ny, nz;
+};
+
+// intersect_tube_raw, _kernels.py:76-134, in the specialisation the frame kernels
+// compile to: the endpoints arrive as float32, numba's float(f32) does not widen,
+// so axis, length and normalisation run in float32.
+__device__ __forceinline__ bool lvx_tube_f32axis(double ox, double oy, double oz, double dx,
+                                                 double dy, double dz, float ax, float ay,
+                                                 float az, float bx, float by, float bz, double r,
+                                                 LvxHit &h) {
+    float ux = bx - ax, uy = by - ay, uz = bz - az;
+    const float length = sqrtf(ux * ux + uy * uy + uz * uz);
+    if ((double)length < 1e-12) return false;
+    ux = ux / length;
+    uy = uy / length;
+    uz = uz / length;
+    const double Ux = (double)ux, Uy = (double)uy, Uz = (double)uz, L = (double)length;
+    const double mx = ox - (double)ax, my = oy - (double)ay, mz = oz - (double)az;
+    const double du = dx * Ux + dy * Uy + dz * Uz;
+    const double mu = mx * Ux + my * Uy + mz * Uz;
+    const double nx_ = dx - du * Ux, ny_ = dy - du * Uy, nz_ = dz - du * Uz;
+    const double qx = mx - mu * Ux, qy = my - mu * Uy, qz = mz - mu * Uz;
+    const double a = nx_ * nx_ + ny_ * ny_ + nz_ * nz_;
+    const double c = qx * qx + qy * qy + qz * qz - r * r;
+    double t0, t1;
+    if (a < 1e-14) {
+        if (c > 0.0) return false;
+        t0 = -CUDART_INF;
+        t1 = CUDART_INF;
+    } else {
+        const double b = 2.0 * (nx_ * qx + ny_ * qy + nz_ * qz);
+        const double disc = b * b - 4.0 * a * c;
+        if (disc < 0.0) return false;
+        const double sq = sqrt(disc);
+        t0 = (-b - sq) / (2.0 * a);
+        t1 = (-b + sq) / (2.0 * a);
+    }
+    if (du == 0.0) {
+        if (mu < 0.0 || mu > L) return false;
+    } else {
+        double s0 = (0.0 - mu) / du;
+        double s1 = (L - mu) / du;
+        if (s0 > s1) {
+            const double t = s0;
+            s0 = s1;
+            s1 = t;
+        }
+        if (s0 > t0) t0 = s0;
+        if (s1 < t1) t1 = s1;
+    }
+    if (t1 < t0 || t1 < 0.0) return false;
+    const double t_in = t0 > 0.0 ? t0 : 0.0;
+    const double px = ox + t_in * dx, py = oy + t_in * dy, pz = oz + t_in * dz;
+    const double wx = px - (double)ax, wy = py - (double)ay, wz = pz - (double)az;
+    const double wu = wx * Ux + wy * Uy + wz * Uz;
+    double rx = wx - wu * Ux, ry = wy - wu * Uy, rz = wz - wu * Uz;
+    const double rn = sqrt(rx * rx + ry * ry + rz * rz);
+    if (rn < 1e-12) {
+        rx = -dx;
+        ry = -dy;
+        rz = -dz;
+    } else {
+        rx = rx / rn;
+        ry = ry / rn;
+        rz = rz / rn;
+    }
+    h.t_in = t_in;
+    h.t_out = t1;
+    h.nx = rx;
+    h.ny = ry;
+    h.nz = rz;
+    return true;
+}
+
+// The all-float64 specialisation reached through the Python-level
+// intersect_ray_tube (raycast.py:184-200).
+__device__ __forceinline__ bool lvx_tube_f64(double ox, double oy, double oz, double dx, double dy,
+                                             double dz, double ax, double ay, double az, double bx,
+                                             double by, double bz, double r, LvxHit &h) {
+    double ux = bx - ax, uy = by - ay, uz = bz - az;
+    const double length = sqrt(ux * ux + uy * uy + uz * uz);
+    if (length < 1e-12) return false;
+    ux = ux / length;
+    uy = uy / length;
+    uz = uz / length;
+    const double mx = ox - ax, my = oy - ay, mz = oz - az;
+    const double du = dx * ux + dy * uy + dz * uz;
+    const double mu = mx * ux + my * uy + mz * uz;
+    const double nx_ = dx - du * ux, ny_ = dy - du * uy, nz_ = dz - du * uz;
+    const double qx = mx - mu * ux, qy = my - mu * uy, qz = mz - mu * uz;
+    const double a = nx_ * nx_ + ny_ * ny_ + nz_ * nz_;
+    const double c = qx * qx + qy * qy + qz * qz - r * r;
+    double t0, t1;
+    if (a < 1e-14) {
+        if (c > 0.0) return false;
+        t0 = -CUDART_INF;
+        t1 = CUDART_INF;
+    } else {
+        const double b = 2.0 * (nx_ * qx + ny_ * qy + nz_ * qz);
+        const double disc = b * b - 4.0 * a * c;
+        if (disc < 0.0) return false;
+        const double sq = sqrt(disc);
+        t0 = (-b - sq) / (2.0 * a);
+        t1 = (-b + sq) / (2.0 * a);
+    }
+    if (du == 0.0) {
+        if (mu < 0.0 || mu > length) return false;
+    } else {
+        double s0 = (0.0 - mu) / du;
+        double s1 = (length - mu) / du;
+        if (s0 > s1) {
+            const double t = s0;
+            s0 = s1;
+            s1 = t;
+        }
+        if (s0 > t0) t0 = s0;
+        if (s1 < t1) t1 = s1;
+    }
+    if (t1 < t0 || t1 < 0.0) return false;
+    const double t_in = t0 > 0.0 ? t0 : 0.0;
+    const double px = ox + t_in * dx, py = oy + t_in * dy, pz = oz + t_in * dz;
+    const double wx = px - ax, wy = py - ay, wz = pz - az;
+    const double wu = wx * ux + wy * uy + wz * uz;
+    double rx = wx - wu * ux, ry = wy - wu * uy, rz = wz - wu * uz;
+    const double rn = sqrt(rx * rx + ry * ry + rz * rz);
+    if (rn < 1e-12) {
+        rx = -dx;
+        ry = -dy;
+        rz = -dz;
+    } else {
+        rx = rx / rn;
+        ry = ry / rn;
+        rz = rz / rn;
+    }
+    h.t_in = t_in;
+    h.t_out = t1;
+    h.nx = rx;
+    h.ny = ry;
+    h.nz = rz;
+    return true;
+}
+
+// intersect_sphere_raw, _kernels.py:137-159.  WANT_NORMAL=false stops after t_in
+// (the ownership test needs nothing else).
+template <bool WANT_NORMAL>
+__device__ __forceinline__ bool lvx_sphere(double ox, double oy, double oz, double dx, double dy,
+                                           double dz, double cx, double cy, double cz, double r,
+                                           LvxHit &h) {
+    const double mx = ox - cx, my = oy - cy, mz = oz - cz;
+    const double b = 2.0 * (dx * mx + dy * my + dz * mz);
+    const double c = mx * mx + my * my + mz * mz - r * r;
+    const double disc = b * b - 4.0 * c;
+    if (disc < 0.0) return false;
+    const double sq = sqrt(disc);
+    const double t0 = (-b - sq) / 2.0;
+    const double t1 = (-b + sq) / 2.0;
+    if (t1 < 0.0) return false;
+    const double t_in = t0 > 0.0 ? t0 : 0.0;
+    h.t_in = t_in;
+    h.t_out = t1;
+    if (WANT_NORMAL) {
+        const double px = ox + t_in * dx, py = oy + t_in * dy, pz = oz + t_in * dz;
+        double nx_ = px - cx, ny_ = py - cy, nz_ = pz - cz;
+        const double nn = sqrt(nx_ * nx_ + ny_ * ny_ + nz_ * nz_);
+        if (nn < 1e-12) {
+            nx_ = -dx;
+            ny_ = -dy;
+            nz_ = -dz;
+        } else {
+            nx_ = nx_ / nn;
+            ny_ = ny_ / nn;
+            nz_ = nz_ / nn;
+        }
+        h.nx = nx_;
+        h.ny = ny_;
+        h.nz = nz_;
+    }
+    return true;
+}
+
+// dda_collect, _kernels.py:164-256, as an incremental walker: init() does the slab
+// clip and the start voxel, next() yields one [t0,t1) window at a time in the
+// reference's order (zero-length visits dropped, ties x<=y<=z, tmax accumulated by
+// repeated addition exactly like the reference).
+struct LvxDda {
+    double t_cur, t_exit;
+    double tmax_x, tmax_y, tmax_z, tdel_x, tdel_y, tdel_z;
+    int ix, iy, iz, step_x, step_y, step_z;
+    int ilo, ihx, ihy, ihz;
+    bool alive;
+
+    __device__ __forceinline__ void init(double ox, double oy, double oz, double dx, double dy,
+                                         double dz, int rx, int ry, int rz, int pad) {
+        alive = false;
+        double t_enter = -CUDART_INF;
+        t_exit = CUDART_INF;
+        const double lo = -(double)pad;
+        const double o[3] = {ox, oy, oz}, d[3] = {dx, dy, dz};
+        const double hi[3] = {(double)(rx + pad), (double)(ry + pad), (double)(rz + pad)};
+#pragma unroll
+        for (int axis = 0; axis < 3; ++axis) {
+            if (d[axis] == 0.0) {
+                if (o[axis] < lo || o[axis] >= hi[axis]) return;
+            } else {
+                double ta = (lo - o[axis]) / d[axis];
+                double tb = (hi[axis] - o[axis]) / d[axis];
+                if (ta > tb) {
+                    const double t = ta;
+                    ta = tb;
+                    tb = t;
+                }
+                if (ta > t_enter) t_enter = ta;
+                if (tb < t_exit) t_exit = tb;
+            }
+        }
+        if (t_enter < 0.0) t_enter = 0.0;
+        if (t_exit <= t_enter) return;
+        const double px = ox + t_enter * dx, py = oy + t_enter * dy, pz = oz + t_enter * dz;
+        ilo = -pad;
+        ihx = rx + pad - 1;
+        ihy = ry + pad - 1;
+        ihz = rz + pad - 1;
+        // the clamp keeps huge floors from overflowing the int conversion
+        const double fx = floor(px), fy = floor(py), fz = floor(pz);
+        ix = fx < (double)ilo ? ilo : (fx > (double)ihx ? ihx : (int)fx);
+        iy = fy < (double)ilo ? ilo : (fy > (double)ihy ? ihy : (int)fy);
+        iz = fz < (double)ilo ? ilo : (fz > (double)ihz ? ihz : (int)fz);
+        step_x = dx > 0.0 ? 1 : (dx < 0.0 ? -1 : 0);
+        step_y = dy > 0.0 ? 1 : (dy < 0.0 ? -1 : 0);
+        step_z = dz > 0.0 ? 1 : (dz < 0.0 ? -1 : 0);
+        const double big = CUDART_INF;
+        tmax_x = step_x != 0 ? ((double)(ix + (step_x > 0 ? 1 : 0)) - ox) / dx : big;
+        tmax_y = step_y != 0 ? ((double)(iy + (step_y > 0 ? 1 : 0)) - oy) / dy : big;
+        tmax_z = step_z != 0 ? ((double)(iz + (step_z > 0 ? 1 : 0)) - oz) / dz : big;
+        tdel_x = step_x != 0 ? fabs(1.0 / dx) : big;
+        tdel_y = step_y != 0 ? fabs(1.0 / dy) : big;
+        tdel_z = step_z != 0 ? fabs(1.0 / dz) : big;
+        t_cur = t_enter;
+        alive = t_cur < t_exit;
+    }
+
+    // Advances to the next non-empty window; returns false when the walk is over.
+    __device__ __forceinline__ bool next(int &wx, int &wy, int &wz, double &t0, double &t1) {
+        while (alive) {
+            double t_next;
+            int axis;
+            if (tmax_x <= tmax_y && tmax_x <= tmax_z) {
+                t_next = tmax_x;
+                axis = 0;
+            } else if (tmax_y <= tmax_z) {
+                t_next = tmax_y;
+                axis = 1;
+            } else {
+                t_next = tmax_z;
+                axis = 2;
+            }
+            const double te = t_next < t_exit ? t_next : t_exit;
+            const bool emit = te > t_cur;
+            wx = ix;
+            wy = iy;
+            wz = iz;
+            t0 = t_cur;
+            t1 = te;
+            t_cur = te;
+            if (axis == 0) {
+                ix += step_x;
+                tmax_x += tdel_x;
+                if (ix < ilo || ix > ihx) alive = false;
+            } else if (axis == 1) {
+                iy += step_y;
+                tmax_y += tdel_y;
+                if (iy < ilo || iy > ihy) alive = false;
+            } else {
+                iz += step_z;
+                tmax_z += tdel_z;
+                if (iz < ilo || iz > ihz) alive = false;
+            }
+            if (!(t_cur < t_exit)) alive = false;
+            if (emit) return true;
+        }
+        return false;
+    }
+};
+
+// sample_field_trilinear, _kernels.py:346-383
+__device__ __forceinline__ double lvx_trilinear(const float *__restrict__ flat, i64 off, int ldx,
+                                                int ldy, int ldz, double scale, double x, double y,
+                                                double z) {
+    const double qx = x / scale - 0.5, qy = y / scale - 0.5, qz = z / scale - 0.5;
+    const double flx = floor(qx), fly = floor(qy), flz = floor(qz);
+    const double fx = qx - flx, fy = qy - fly, fz = qz - flz;
+    // clamp in floating point first so far-away queries cannot overflow the int cast
+    const double hx = (double)(ldx - 1), hy = (double)(ldy - 1), hz = (double)(ldz - 1);
+    const int x0 = (int)fmin(fmax(flx, 0.0), hx), x1 = (int)fmin(fmax(flx + 1.0, 0.0), hx);
+    const int y0 = (int)fmin(fmax(fly, 0.0), hy), y1 = (int)fmin(fmax(fly + 1.0, 0.0), hy);
+    const int z0 = (int)fmin(fmax(flz, 0.0), hz), z1 = (int)fmin(fmax(flz + 1.0, 0.0), hz);
+    const i64 sy = ldx, sz = (i64)ldx * ldy;
+    const float *f = flat + off;
+    const double v000 = (double)__ldg(f + z0 * sz + y0 * sy + x0), v001 = (double)__ldg(f + z0 * sz + y0 * sy + x1);
+    const double v010 = (double)__ldg(f + z0 * sz + y1 * sy + x0), v011 = (double)__ldg(f + z0 * sz + y1 * sy + x1);
+    const double v100 = (double)__ldg(f + z1 * sz + y0 * sy + x0), v101 = (double)__ldg(f + z1 * sz + y0 * sy + x1);
+    const double v110 = (double)__ldg(f + z1 * sz + y1 * sy + x0), v111 = (double)__ldg(f + z1 * sz + y1 * sy + x1);
+    const double c00 = v000 * (1.0 - fx) + v001 * fx;
+    const double c01 = v010 * (1.0 - fx) + v011 * fx;
+    const double c10 = v100 * (1.0 - fx) + v101 * fx;
+    const double c11 = v110 * (1.0 - fx) + v111 * fx;
+    const double c0 = c00 * (1.0 - fy) + c01 * fy;
+    const double c1 = c10 * (1.0 - fy) + c11 * fy;
+    return c0 * (1.0 - fz) + c1 * fz;
+}
+
+// Octree view passed by value to kernels (from lvx_lod).
+struct LvxOctree {
+    const float *flat;
+    i64 off[LVX_MAX_LEVELS + 1];
+    int dims[LVX_MAX_LEVELS * 3];
+    int n_levels;
+};
+
+// cone_blocking, _kernels.py:386-422.  The reference picks the level with
+// floor(log2(width)); width is max(t,1) with t = 0.5 + sum of powers of two, so
+// the value equals the binary exponent of width exactly (no libm call needed).
+__device__ __forceinline__ double lvx_cone_blocking(double px, double py, double pz, double lx,
+                                                    double ly, double lz, const LvxOctree &oc,
+                                                    double gx, double gy, double gz, double eps_T) {
+    double t_cur = 0.5, T = 1.0;
+    const double max_d = sqrt(gx * gx + gy * gy + gz * gz);
+    while (t_cur < max_d) {
+        const double x = px + t_cur * lx, y = py + t_cur * ly, z = pz + t_cur * lz;
+        if (x < 0.0 || y < 0.0 || z < 0.0 || x > gx || y > gy || z > gz) break;
+        const double width = t_cur < 1.0 ? 1.0 : t_cur;
+        int level = ilogb(width);
+        if (level < 0) level = 0;
+        if (level > oc.n_levels - 1) level = oc.n_levels - 1;
+        const double step = (double)((i64)1 << level);
+        const double rho = lvx_trilinear(oc.flat, oc.off[level], oc.dims[3 * level],
+                                         oc.dims[3 * level + 1], oc.dims[3 * level + 2], step, x, y, z);
+        double ext = 1.0 - rho * step;
+        if (ext < 0.0) ext = 0.0;
+        T *= ext;
+        if (T <= eps_T) {
+            T = 0.0;
+            break;
+        }
+        t_cur += step;
+    }
+    return 1.0 - T;
+}
+
+// density_ray_blocking, _kernels.py:425-445 (level 0 only)
+__device__ __forceinline__ double lvx_density_ray(double px, double py, double pz, double dx,
+                                                  double dy, double dz, const float *__restrict__ l0,
+                                                  int gxi, int gyi, int gzi, double radius,
+                                                  double step) {
+    const double gx = (double)gxi, gy = (double)gyi, gz = (double)gzi;
+    double acc = 0.0, t_cur = step;
+    while (t_cur <= radius) {
+        const double x = px + t_cur * dx, y = py + t_cur * dy, z = pz + t_cur * dz;
+        if (x < 0.0 || y < 0.0 || z < 0.0 || x > gx || y > gy || z > gz) break;
+        acc += lvx_trilinear(l0, 0, gxi, gyi, gzi, 1.0, x, y, z) * step;
+        if (acc >= 1.0) return 1.0;
+        t_cur += step;
+    }
+    return acc < 1.0 ? acc : 1.0;
+}
+
+// orient_frame, _kernels.py:555-569
+__device__ __forceinline__ void lvx_orient_frame(double nx, double ny, double nz, double t[3],
+                                                 double b[3]) {
+    double tx, ty, tz;
+    if (fabs(nx) > 0.9) {
+        tx = 0.0;
+        ty = 1.0;
+        tz = 0.0;
+    } else {
+        tx = 1.0;
+        ty = 0.0;
+        tz = 0.0;
+    }
+    const double d = tx * nx + ty * ny + tz * nz;
+    tx = tx - d * nx;
+    ty = ty - d * ny;
+    tz = tz - d * nz;
+    const double tn = sqrt(tx * tx + ty * ty + tz * tz);
+    tx = tx / tn;
+    ty = ty / tn;
+    tz = tz / tn;
+    t[0] = tx;
+    t[1] = ty;
+    t[2] = tz;
+    b[0] = ny * tz - nz * ty;
+    b[1] = nz * tx - nx * tz;
+    b[2] = nx * ty - ny * tx;
+}
+
+// ao_density_point, _kernels.py:592-605.  `dirs` is the host-built Fibonacci
+// lattice (fibonacci_dir with libm cos/sin, bit-identical to the reference).
+__device__ __forceinline__ double lvx_ao_density_point(double px, double py, double pz, double nx,
+                                                       double ny, double nz, int n_rays,
+                                                       double radius, double step,
+                                                       const double *__restrict__ dirs,
+                                                       const float *__restrict__ l0, int gx, int gy,
+                                                       int gz) {
+    double total = 0.0, t[3], b[3];
+    lvx_orient_frame(nx, ny, nz, t, b);
+    for (int i = 0; i < n_rays; ++i) {
+        const double lx = dirs[3 * i], ly = dirs[3 * i + 1], lz = dirs[3 * i + 2];
+        const double dx = lx * t[0] + ly * b[0] + lz * nx;
+        const double dy = lx * t[1] + ly * b[1] + lz * ny;
+        const double dz = lx * t[2] + ly * b[2] + lz * nz;
+        total += lvx_density_ray(px, py, pz, dx, dy, dz, l0, gx, gy, gz, radius, step);
+    }
+    return total / (double)n_rays;
+}
+
+// shade_scalar, _kernels.py:316-329
+__device__ __forceinline__ double lvx_shade(double nx, double ny, double nz, double lx, double ly,
+                                            double lz, double vx, double vy, double vz, double ka,
+                                            double kd, double ks, double shininess) {
+    double ndl = nx * lx + ny * ly + nz * lz;
+    if (ndl < 0.0) ndl = 0.0;
+    const double hx = lx + vx, hy = ly + vy, hz = lz + vz;
+    const double hn = sqrt(hx * hx + hy * hy + hz * hz);
+    double spec = 0.0;
+    if (hn > 1e-12) {
+        const double ndh = (nx * hx + ny * hy + nz * hz) / hn;
+        if (ndh > 0.0) spec = pow(ndh, shininess);
+    }
+    return ka + kd * ndl + ks * spec;
+}
+
+// _alpha_of, _kernels.py:332-341
+__device__ __forceinline__ double lvx_alpha_of(int mode, double base_alpha, double table_alpha,
+                                               double t_in, double t_out) {
+    if (mode == LVX_OPACITY_CONSTANT) return base_alpha;
+    if (mode == LVX_OPACITY_TRANSFER) return table_alpha;
+    double span = t_out - t_in;
+    if (span < 0.0) span = 0.0;
+    return 1.0 - pow(1.0 - base_alpha, span);
+}

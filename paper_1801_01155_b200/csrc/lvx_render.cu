@@ -1,0 +1,460 @@
+// Ray-caster for sm_100a: one thread per pixel in warp-coherent 8x4 pixel tiles,
+// incremental 3D-DDA, per-window gather over the voxel's (or 27 voxels') segment
+// records with 2 x 16-byte loads per segment, exact float64 tube / joint-sphere
+// tests, ordered insertion of the owned hits, front-to-back compositing with the
+// reference's de-duplication rules and early ray termination.
+//
+//   render_rows   _kernels.py:735-923     stream_hit   _kernels.py:650-730
+//   dda_collect   _kernels.py:164-256     _hit_before  _kernels.py:261-270
+//   _seen_check_and_mark / _sphere_seen   _kernels.py:625-647
+//
+// The reference buffers all windows of a ray and up to 1024 hits of a window with
+// their normals, then insertion-sorts.  Here windows are produced incrementally and
+// a hit is stored as (t_in, voxel, segment, lid/kind/ordinal) only -- 20 bytes -- in
+// a sorted per-thread buffer; t_out and the normal are recomputed (bit-identically)
+// for the few hits that are actually composited.  A window with more owned hits
+// than the buffer holds is finished by extra gather passes that continue after the
+// last composited key, so the composited sequence is the reference's total order
+// (t_in, home voxel, lid, kind, gather order) in every case.
+#include <math_constants.h>
+
+#include "lvx_geom.cuh"
+
+namespace {
+
+constexpr int kHitCap = 64;       // sorted per-thread hit buffer (entries)
+constexpr int kWarpsPerBlock = 4;
+
+struct RenderArgs {
+    lvx_camera cam;
+    lvx_params p;
+    int rx, ry, rz;
+    const u8 *counts;
+    const u32 *offsets;
+    const lvx_seg_record *rec;
+    const float *table;
+    const u8 *occ;
+    LvxOctree oc;
+    const float *ao_flat;
+    const double *ao_dirs;
+    lvx_tiling tl;
+    int tiles_x, n_my_tiles;
+    float *img;
+    unsigned long long *row_stats;
+};
+
+struct HitKey {
+    double t;
+    u32 lin;
+    u32 meta;  // lid (5 bits) | kind3 << 5 (0 tube, 1 sphere A, 2 sphere B) | ordinal << 8
+};
+
+__device__ __forceinline__ u32 meta_lid(u32 m) { return m & 31u; }
+__device__ __forceinline__ u32 meta_kind3(u32 m) { return (m >> 5) & 3u; }
+__device__ __forceinline__ u32 meta_ord(u32 m) { return m >> 8; }
+
+// _hit_before (_kernels.py:261-270) extended by the gather ordinal, which is what a
+// stable insertion sort resolves remaining ties with.
+__device__ __forceinline__ bool key_before(double ta, u32 la, u32 ma, double tb, u32 lb, u32 mb) {
+    if (ta != tb) return ta < tb;
+    if (la != lb) return la < lb;
+    const u32 lida = meta_lid(ma), lidb = meta_lid(mb);
+    if (lida != lidb) return lida < lidb;
+    const u32 ka = meta_kind3(ma) ? 1u : 0u, kb = meta_kind3(mb) ? 1u : 0u;
+    if (ka != kb) return ka < kb;
+    return meta_ord(ma) < meta_ord(mb);
+}
+
+struct PixelState {
+    double acc[4];
+    int n_seen, n_sph;
+    u32 seen_key[LVX_MAX_SEEN];
+    u32 seen_mask[LVX_MAX_SEEN];
+    float sph[LVX_MAX_SEEN][3];
+};
+
+// stream_hit, _kernels.py:650-730.  Returns the accumulated alpha.
+__device__ double stream_hit(PixelState &S, const RenderArgs &A, double ox, double oy, double oz,
+                             double ddx, double ddy, double ddz, const LvxHit &h, u32 lin, u32 lid,
+                             u32 attr, bool is_sphere, float cx, float cy, float cz) {
+    if (is_sphere) {
+        for (int i = 0; i < S.n_sph; ++i)
+            if (S.sph[i][0] == cx && S.sph[i][1] == cy && S.sph[i][2] == cz) return S.acc[3];
+    }
+    {
+        const u32 bit = 1u << lid;
+        bool found = false;
+        for (int i = 0; i < S.n_seen; ++i) {
+            if (S.seen_key[i] == lin) {
+                if (S.seen_mask[i] & bit) return S.acc[3];
+                S.seen_mask[i] |= bit;
+                found = true;
+                break;
+            }
+        }
+        if (!found && S.n_seen < LVX_MAX_SEEN) {
+            S.seen_key[S.n_seen] = lin;
+            S.seen_mask[S.n_seen] = bit;
+            S.n_seen += 1;
+        }
+    }
+    const lvx_params &p = A.p;
+    const double gx = (double)A.rx, gy = (double)A.ry, gz = (double)A.rz;
+    const double px = ox + h.t_in * ddx, py = oy + h.t_in * ddy, pz = oz + h.t_in * ddz;
+    double shadow_term = 0.0;
+    if (p.shadow_mode == LVX_SHADOW_CONE)
+        shadow_term = lvx_cone_blocking(px, py, pz, p.light[0], p.light[1], p.light[2], A.oc, gx,
+                                        gy, gz, 0.01);
+    double ao_term = 0.0;
+    if (p.ao_mode == LVX_AO_PRECOMPUTED) {
+        ao_term = lvx_trilinear(A.ao_flat, 0, A.rx, A.ry, A.rz, 1.0, px, py, pz);
+        if (ao_term > 1.0) ao_term = 1.0;
+        if (ao_term < 0.0) ao_term = 0.0;
+    } else if (p.ao_mode == LVX_AO_DENSITY) {
+        ao_term = lvx_ao_density_point(px, py, pz, h.nx, h.ny, h.nz, p.ao_n_rays, p.ao_radius, 1.0,
+                                       A.ao_dirs, A.oc.flat, A.rx, A.ry, A.rz);
+    }
+    const float4 col = __ldg(reinterpret_cast<const float4 *>(A.table) + attr);
+    const double alpha = lvx_alpha_of(p.opacity_mode, p.base_alpha, (double)col.w, h.t_in, h.t_out);
+    double lgx, lgy, lgz;
+    if (p.headlight != 0) {
+        lgx = -ddx;
+        lgy = -ddy;
+        lgz = -ddz;
+    } else {
+        lgx = p.light[0];
+        lgy = p.light[1];
+        lgz = p.light[2];
+    }
+    double scale = lvx_shade(h.nx, h.ny, h.nz, lgx, lgy, lgz, -ddx, -ddy, -ddz,
+                             p.ka * (1.0 - ao_term), p.kd, p.ks, p.shininess);
+    scale *= 1.0 - shadow_term;
+    const double trans = 1.0 - S.acc[3];
+    const double w = trans * alpha;
+    S.acc[0] += w * scale * (double)col.x;
+    S.acc[1] += w * scale * (double)col.y;
+    S.acc[2] += w * scale * (double)col.z;
+    S.acc[3] += w;
+    if (is_sphere && S.n_sph < LVX_MAX_SEEN) {
+        S.sph[S.n_sph][0] = cx;
+        S.sph[S.n_sph][1] = cy;
+        S.sph[S.n_sph][2] = cz;
+        S.n_sph += 1;
+    }
+    return S.acc[3];
+}
+
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+render_kernel(const RenderArgs A) {
+    const int lane = threadIdx.x & 31;
+    const i64 gw = (i64)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    const int wpt_x = A.tl.tile_w >> 3, wpt_y = A.tl.tile_h >> 2;
+    const int warps_per_tile = wpt_x * wpt_y;
+    const i64 k = gw / warps_per_tile;  // index into this rank's tile list
+    const int wi = (int)(gw % warps_per_tile);
+    const bool tile_ok = k < A.n_my_tiles;
+    const i64 tile = (i64)A.tl.tile_first + k * A.tl.tile_step;
+    const int tx = (int)(tile % A.tiles_x), ty = (int)(tile / A.tiles_x);
+    const int lx = (wi % wpt_x) * 8 + (lane & 7), ly = (wi / wpt_x) * 4 + (lane >> 3);
+    const int x = tx * A.tl.tile_w + lx, y = ty * A.tl.tile_h + ly;
+    const int W = A.cam.width, H = A.cam.height;
+    const bool active = tile_ok && x < W && y < H;
+
+    unsigned long long steps = 0, tests = 0, overflow = 0;
+    if (active) {
+        const lvx_params &p = A.p;
+        // primary ray, _kernels.py:769-776
+        const double ndc_x = (((double)x + 0.5) / (double)W * 2.0 - 1.0) * A.cam.tan_half * A.cam.aspect;
+        const double ndc_y = (1.0 - ((double)y + 0.5) / (double)H * 2.0) * A.cam.tan_half;
+        double ddx = A.cam.f[0] + ndc_x * A.cam.r[0] + ndc_y * A.cam.u[0];
+        double ddy = A.cam.f[1] + ndc_x * A.cam.r[1] + ndc_y * A.cam.u[1];
+        double ddz = A.cam.f[2] + ndc_x * A.cam.r[2] + ndc_y * A.cam.u[2];
+        const double dn = sqrt(ddx * ddx + ddy * ddy + ddz * ddz);
+        ddx = ddx / dn;
+        ddy = ddy / dn;
+        ddz = ddz / dn;
+        const double ox = A.cam.o[0], oy = A.cam.o[1], oz = A.cam.o[2];
+        const int rx = A.rx, ry = A.ry, rz = A.rz;
+        const bool neighbor = p.neighbor != 0, joints = p.joints != 0;
+        const double tube_r = p.tube_r;
+
+        PixelState S;
+        S.acc[0] = S.acc[1] = S.acc[2] = S.acc[3] = 0.0;
+        S.n_seen = 0;
+        S.n_sph = 0;
+        double h_t[kHitCap];
+        u32 h_lin[kHitCap], h_seg[kHitCap], h_meta[kHitCap];
+
+        LvxDda dda;
+        dda.init(ox, oy, oz, ddx, ddy, ddz, rx, ry, rz, neighbor ? 1 : 0);
+        bool done = false;
+        int wx, wy, wz;
+        double t0, t1;
+        while (dda.next(wx, wy, wz, t0, t1)) {
+            steps += 1;  // the reference counts every window of the full walk (:785-786)
+            if (done) continue;
+            if (neighbor) {
+                if (A.occ[((i64)(wz + 1) * (ry + 2) + (wy + 1)) * (rx + 2) + (wx + 1)] == 0) continue;
+            } else {
+                if (A.counts[wx + (i64)rx * (wy + (i64)ry * wz)] == 0) continue;
+            }
+            const int span = neighbor ? 1 : 0;
+            // continuation key for windows that overflow the sorted buffer
+            bool have_last = false;
+            double last_t = 0.0;
+            u32 last_lin = 0, last_meta = 0;
+            bool first_pass = true;
+            for (;;) {
+                int nh = 0;
+                bool spilled = false;
+                u32 ord = 0;  // gather ordinal of the next owned hit
+                for (int nz_ = wz - span; nz_ <= wz + span; ++nz_) {
+                    if (nz_ < 0 || nz_ >= rz) continue;
+                    for (int ny_ = wy - span; ny_ <= wy + span; ++ny_) {
+                        if (ny_ < 0 || ny_ >= ry) continue;
+                        for (int nx_ = wx - span; nx_ <= wx + span; ++nx_) {
+                            if (nx_ < 0 || nx_ >= rx) continue;
+                            const u32 lin = (u32)(nx_ + rx * (ny_ + ry * nz_));
+                            const u32 cnt = A.counts[lin];
+                            if (cnt == 0) continue;
+                            const u32 base = A.offsets[lin];
+                            for (u32 s = 0; s < cnt; ++s) {
+                                const u32 i = base + s;
+                                const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + i));
+                                const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + i) + 1);
+                                const u32 lid = (__float_as_uint(ra.w) >> 8) & 31u;
+                                if (first_pass) tests += joints ? 3 : 1;
+#pragma unroll
+                                for (int kind3 = 0; kind3 < 3; ++kind3) {
+                                    if (kind3 > 0 && !joints) break;
+                                    LvxHit h;
+                                    bool hit;
+                                    if (kind3 == 0)
+                                        hit = lvx_tube_f32axis(ox, oy, oz, ddx, ddy, ddz, ra.x, ra.y,
+                                                               ra.z, rb.x, rb.y, rb.z, tube_r, h);
+                                    else if (kind3 == 1)
+                                        hit = lvx_sphere<false>(ox, oy, oz, ddx, ddy, ddz, (double)ra.x,
+                                                                (double)ra.y, (double)ra.z, tube_r, h);
+                                    else
+                                        hit = lvx_sphere<false>(ox, oy, oz, ddx, ddy, ddz, (double)rb.x,
+                                                                (double)rb.y, (double)rb.z, tube_r, h);
+                                    if (!(hit && t0 <= h.t_in && h.t_in < t1)) continue;  // ownership
+                                    const u32 my_ord = ord++;
+                                    if (my_ord >= (u32)LVX_MAX_WINDOW_HITS) {
+                                        // the reference drops hits past its 1024-entry window buffer
+                                        if (first_pass) overflow += 1;
+                                        continue;
+                                    }
+                                    const u32 meta = lid | ((u32)kind3 << 5) | (my_ord << 8);
+                                    if (have_last &&
+                                        !key_before(last_t, last_lin, last_meta, h.t_in, lin, meta))
+                                        continue;  // composited in an earlier pass
+                                    int pos;
+                                    if (nh < kHitCap) {
+                                        pos = nh++;
+                                    } else {
+                                        spilled = true;
+                                        if (!key_before(h.t_in, lin, meta, h_t[kHitCap - 1],
+                                                        h_lin[kHitCap - 1], h_meta[kHitCap - 1]))
+                                            continue;
+                                        pos = kHitCap - 1;
+                                    }
+                                    while (pos > 0 && key_before(h.t_in, lin, meta, h_t[pos - 1],
+                                                                 h_lin[pos - 1], h_meta[pos - 1])) {
+                                        h_t[pos] = h_t[pos - 1];
+                                        h_lin[pos] = h_lin[pos - 1];
+                                        h_seg[pos] = h_seg[pos - 1];
+                                        h_meta[pos] = h_meta[pos - 1];
+                                        --pos;
+                                    }
+                                    h_t[pos] = h.t_in;
+                                    h_lin[pos] = lin;
+                                    h_seg[pos] = i;
+                                    h_meta[pos] = meta;
+                                }
+                            }
+                        }
+                    }
+                }
+                // composite in order, _kernels.py:898-914
+                for (int q = 0; q < nh; ++q) {
+                    const u32 i = h_seg[q], meta = h_meta[q];
+                    const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + i));
+                    const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + i) + 1);
+                    const u32 kind3 = meta_kind3(meta);
+                    LvxHit h;
+                    float cx = 0.0f, cy = 0.0f, cz = 0.0f;
+                    if (kind3 == 0) {
+                        lvx_tube_f32axis(ox, oy, oz, ddx, ddy, ddz, ra.x, ra.y, ra.z, rb.x, rb.y, rb.z,
+                                         tube_r, h);
+                    } else {
+                        cx = kind3 == 1 ? ra.x : rb.x;
+                        cy = kind3 == 1 ? ra.y : rb.y;
+                        cz = kind3 == 1 ? ra.z : rb.z;
+                        lvx_sphere<true>(ox, oy, oz, ddx, ddy, ddz, (double)cx, (double)cy, (double)cz,
+                                         tube_r, h);
+                    }
+                    const double a_now =
+                        stream_hit(S, A, ox, oy, oz, ddx, ddy, ddz, h, h_lin[q], meta_lid(meta),
+                                   __float_as_uint(ra.w) & 0xFFu, kind3 != 0, cx, cy, cz);
+                    if (a_now >= p.tau) {
+                        done = true;
+                        break;
+                    }
+                }
+                if (done || !spilled) break;
+                have_last = true;
+                last_t = h_t[kHitCap - 1];
+                last_lin = h_lin[kHitCap - 1];
+                last_meta = h_meta[kHitCap - 1];
+                first_pass = false;
+            }
+        }
+
+        // _kernels.py:916-920
+        const double a = S.acc[3];
+        float4 outp;
+        outp.x = (float)(S.acc[0] + (1.0 - a) * p.bg[3] * p.bg[0]);
+        outp.y = (float)(S.acc[1] + (1.0 - a) * p.bg[3] * p.bg[1]);
+        outp.z = (float)(S.acc[2] + (1.0 - a) * p.bg[3] * p.bg[2]);
+        outp.w = (float)(a + (1.0 - a) * p.bg[3]);
+        i64 o;
+        if (A.tl.compact) o = ((k * A.tl.tile_h + ly) * (i64)A.tl.tile_w + lx);
+        else o = (i64)y * W + x;
+        reinterpret_cast<float4 *>(A.img)[o] = outp;
+    }
+
+    // per-row counters: reduce over the 8 lanes that share an image row
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+        steps += __shfl_xor_sync(0xFFFFFFFFu, steps, o);
+        tests += __shfl_xor_sync(0xFFFFFFFFu, tests, o);
+        overflow += __shfl_xor_sync(0xFFFFFFFFu, overflow, o);
+    }
+    if ((lane & 7) == 0 && tile_ok && y < H) {
+        if (steps) atomicAdd(A.row_stats + 3 * (i64)y, steps);
+        if (tests) atomicAdd(A.row_stats + 3 * (i64)y + 1, tests);
+        if (overflow) atomicAdd(A.row_stats + 3 * (i64)y + 2, overflow);
+    }
+}
+
+__global__ void __launch_bounds__(256)
+untile_kernel(const float4 *__restrict__ tiles, lvx_tiling tl, int tiles_x, i64 n_tiles_mine, int W,
+              int H, float4 *__restrict__ img) {
+    const i64 idx = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    const i64 per_tile = (i64)tl.tile_w * tl.tile_h;
+    if (idx >= n_tiles_mine * per_tile) return;
+    const i64 k = idx / per_tile;
+    const int r = (int)(idx % per_tile), lx = r % tl.tile_w, ly = r / tl.tile_w;
+    const i64 tile = (i64)tl.tile_first + k * tl.tile_step;
+    const int x = (int)(tile % tiles_x) * tl.tile_w + lx, y = (int)(tile / tiles_x) * tl.tile_h + ly;
+    if (x < W && y < H) img[(i64)y * W + x] = tiles[idx];
+}
+
+int check_tiling(const lvx_tiling *t) {
+    LVX_REQUIRE(t && t->tile_w >= 8 && t->tile_h >= 4 && (t->tile_w % 8) == 0 &&
+                    (t->tile_h % 4) == 0 && t->tile_step >= 1 && t->tile_first >= 0 &&
+                    t->tile_first < t->tile_step,
+                "tiling: tile_w %% 8 == 0, tile_h %% 4 == 0, 0 <= tile_first < tile_step required");
+    return LVX_OK;
+}
+
+i64 my_tile_count(const lvx_tiling *t, int W, int H, int *tiles_x_out) {
+    const i64 tiles_x = lvx_ceil_div(W, t->tile_w), tiles_y = lvx_ceil_div(H, t->tile_h);
+    const i64 total = tiles_x * tiles_y;
+    if (tiles_x_out) *tiles_x_out = (int)tiles_x;
+    if (t->tile_first >= total) return 0;
+    return (total - t->tile_first + t->tile_step - 1) / t->tile_step;
+}
+
+void fill_octree(LvxOctree &oc, const lvx_lod *lod) {
+    memset(&oc, 0, sizeof(oc));
+    if (!lod) return;
+    oc.flat = lod->oct_flat_d;
+    oc.n_levels = lod->n_levels;
+    for (int l = 0; l <= lod->n_levels && l <= LVX_MAX_LEVELS; ++l) oc.off[l] = lod->oct_off[l];
+    for (int l = 0; l < lod->n_levels * 3 && l < LVX_MAX_LEVELS * 3; ++l)
+        oc.dims[l] = (int)lod->oct_dims[l];
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t lvx_render_scratch_bytes(const lvx_camera *, const lvx_tiling *) {
+    // the per-thread hit buffer and de-duplication tables live in local memory;
+    // no caller-provided scratch is needed in this ABI version
+    return 0;
+}
+
+int lvx_render(const lvx_camera *cam, const lvx_model *model, const lvx_params *params,
+               const lvx_lod *lod, const lvx_tiling *tiling, float *img_d, int64_t *row_stats_d,
+               void *scratch_d, void *stream) {
+    (void)scratch_d;
+    LVX_REQUIRE(cam && model && params && img_d && row_stats_d, "null argument");
+    LVX_REQUIRE(cam->width >= 1 && cam->height >= 1, "image dims must be >= 1");
+    if (int rc = check_tiling(tiling)) return rc;
+    LVX_REQUIRE(model->rx >= 1 && model->ry >= 1 && model->rz >= 1 && model->counts_d &&
+                    model->offsets_d && model->table_d,
+                "bad model");
+    LVX_REQUIRE((i64)model->rx * model->ry * model->rz < ((i64)1 << 31), "grid too large to render");
+    LVX_REQUIRE(!params->neighbor || model->occ_d, "neighbour mode needs the dilated occupancy map");
+    LVX_REQUIRE(params->opacity_mode >= 0 && params->opacity_mode <= 2, "bad opacity mode");
+    LVX_REQUIRE(params->shadow_mode == LVX_SHADOW_NONE || params->shadow_mode == LVX_SHADOW_CONE,
+                "shadow_mode %d is not built in this library (none/cone only)", params->shadow_mode);
+    LVX_REQUIRE(params->ao_mode == LVX_AO_NONE || params->ao_mode == LVX_AO_DENSITY ||
+                    params->ao_mode == LVX_AO_PRECOMPUTED,
+                "ao_mode %d is not built in this library (none/density-rays/precomputed only)",
+                params->ao_mode);
+    const bool need_oct = params->shadow_mode == LVX_SHADOW_CONE || params->ao_mode == LVX_AO_DENSITY;
+    LVX_REQUIRE(!need_oct || (lod && lod->oct_flat_d && lod->n_levels >= 1 &&
+                              lod->n_levels <= LVX_MAX_LEVELS),
+                "cone shadows / density-rays AO need a density octree");
+    LVX_REQUIRE(params->ao_mode != LVX_AO_PRECOMPUTED || (lod && lod->ao_flat_d),
+                "precomputed AO requested but no AO field given");
+    LVX_REQUIRE(params->ao_mode != LVX_AO_DENSITY || (lod->ao_dirs_d && params->ao_n_rays >= 1),
+                "density-rays AO needs the direction lattice");
+
+    RenderArgs A;
+    memset(&A, 0, sizeof(A));
+    A.cam = *cam;
+    A.p = *params;
+    A.rx = model->rx;
+    A.ry = model->ry;
+    A.rz = model->rz;
+    A.counts = model->counts_d;
+    A.offsets = model->offsets_d;
+    A.rec = model->seg_rec_d;
+    A.table = model->table_d;
+    A.occ = model->occ_d;
+    fill_octree(A.oc, lod);
+    A.ao_flat = lod ? lod->ao_flat_d : nullptr;
+    A.ao_dirs = lod ? lod->ao_dirs_d : nullptr;
+    A.tl = *tiling;
+    A.n_my_tiles = (int)my_tile_count(tiling, cam->width, cam->height, &A.tiles_x);
+    A.img = img_d;
+    A.row_stats = reinterpret_cast<unsigned long long *>(row_stats_d);
+    if (A.n_my_tiles == 0) return LVX_OK;
+    const i64 warps = (i64)A.n_my_tiles * (tiling->tile_w / 8) * (tiling->tile_h / 4);
+    const i64 blocks = lvx_ceil_div(warps, kWarpsPerBlock);
+    render_kernel<<<(unsigned)blocks, kWarpsPerBlock * 32, 0, (cudaStream_t)stream>>>(A);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_untile(const float *tiles_d, const lvx_tiling *tiling, int32_t width, int32_t height,
+               float *img_d, void *stream) {
+    LVX_REQUIRE(tiles_d && img_d && width >= 1 && height >= 1, "bad arguments");
+    if (int rc = check_tiling(tiling)) return rc;
+    int tiles_x = 0;
+    const i64 n = my_tile_count(tiling, width, height, &tiles_x);
+    if (n == 0) return LVX_OK;
+    const i64 px = n * tiling->tile_w * tiling->tile_h;
+    untile_kernel<<<(unsigned)lvx_ceil_div(px, 256), 256, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<const float4 *>(tiles_d), *tiling, tiles_x, n, width, height,
+        reinterpret_cast<float4 *>(img_d));
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,706 @@
+// Voxelizer for sm_100a: edge-parallel clip -> per-voxel counting (atomics) ->
+// device prefix sums -> scatter -> per-voxel key ranking -> pack.
+//
+// Restates, bit for bit, the reference's numpy pipeline
+//   _plane_events / _clip_batch   voxelizer.py:174-263
+//   _faces_and_bins               voxelizer.py:358-380
+//   build_voxel_model             voxelizer.py:397-488
+//   _pack_all / _field_layout     voxelizer.py:79-89, 383-394
+// The reference sorts all plane-crossing events of a batch (lexsort by edge, s)
+// and pairs consecutive events of a curve into chords.  Here every polyline edge
+// is one thread: it merges its own x/y/z crossings in the same order (ascending
+// s, ties x<y<z), and fetches the one event it cannot produce itself -- the last
+// crossing of the nearest earlier edge of the same curve -- by a short look-back.
+#include "lvx_common.cuh"
+
+namespace {
+
+constexpr double kMinChord = 1e-9;  // voxelizer.py:37
+constexpr double kFaceEps = 1e-9;   // voxelizer.py:361
+constexpr int kClipThreads = 256;
+
+struct Event {
+    double pos[3];
+    double attr;
+    double k;
+    int ax;
+    bool up;
+};
+
+__device__ __forceinline__ double clip01(double s) {
+    // np.clip(s, 0, 1), voxelizer.py:200
+    s = s < 0.0 ? 0.0 : s;
+    s = s > 1.0 ? 1.0 : s;
+    return s;
+}
+
+// Per-axis crossing bookkeeping of one edge (voxelizer.py:185-200).
+struct EdgeAxes {
+    double x0[3], d[3], f0[3];
+    int cnt[3];
+    bool up[3];
+
+    __device__ __forceinline__ void init(const double a0[3], const double a1[3]) {
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            x0[ax] = a0[ax];
+            d[ax] = a1[ax] - a0[ax];
+            f0[ax] = floor(a0[ax]);
+            double f1 = floor(a1[ax]);
+            up[ax] = d[ax] > 0.0;
+            double c = up[ax] ? f1 - f0[ax] : f0[ax] - f1;
+            long long ci = (long long)c;
+            cnt[ax] = ci < 0 ? 0 : (int)ci;
+        }
+    }
+    __device__ __forceinline__ int total() const { return cnt[0] + cnt[1] + cnt[2]; }
+    __device__ __forceinline__ double plane(int ax, int j) const {
+        return up[ax] ? f0[ax] + 1.0 + (double)j : f0[ax] - (double)j;
+    }
+    __device__ __forceinline__ double param(int ax, double k) const {
+        return clip01((k - x0[ax]) / d[ax]);
+    }
+};
+
+__device__ __forceinline__ void make_event(Event &ev, const EdgeAxes &E, const double a0[3],
+                                           double att0, double att1, bool want_attr, int ax,
+                                           double k, double s) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) ev.pos[c] = a0[c] + s * E.d[c];  // voxelizer.py:228
+    ev.pos[ax] = k;                                              // :229 crossing axis exact
+    ev.attr = want_attr ? att0 + s * (att1 - att0) : 0.0;        // :230
+    ev.k = k;
+    ev.ax = ax;
+    ev.up = E.up[ax];
+}
+
+// Last crossing (in the reference's sorted order) of the nearest earlier edge of
+// the same curve that has any crossing.  Returns false at the curve start.
+template <bool WANT_ATTR>
+__device__ bool lookback_event(const double *__restrict__ pts, const double *__restrict__ attrs,
+                               const u8 *__restrict__ first, i64 i, Event &ev) {
+    i64 ip = i;
+    while (!first[ip]) {
+        ip -= 1;
+        double a0[3], a1[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            a0[c] = pts[3 * ip + c];
+            a1[c] = pts[3 * (ip + 1) + c];
+        }
+        EdgeAxes E;
+        E.init(a0, a1);
+        if (E.total() == 0) continue;
+        int best = -1;
+        double bs = 0.0, bk = 0.0;
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            if (E.cnt[ax] == 0) continue;
+            double k = E.plane(ax, E.cnt[ax] - 1);
+            double s = E.param(ax, k);
+            if (best < 0 || s >= bs) {  // ties: the higher axis sorts last
+                best = ax;
+                bs = s;
+                bk = k;
+            }
+        }
+        double att0 = 0.0, att1 = 0.0;
+        if (WANT_ATTR) {
+            att0 = attrs[ip];
+            att1 = attrs[ip + 1];
+        }
+        make_event(ev, E, a0, att0, att1, WANT_ATTR, best, bk, bs);
+        return true;
+    }
+    return false;
+}
+
+// Chord voxel + keep test, voxelizer.py:242-250.  Returns the linear voxel index
+// or -1 when the chord is dropped.
+__device__ __forceinline__ i64 chord_voxel(const Event &a, const Event &b, int rx, int ry, int rz,
+                                           long long vox[3]) {
+    double m = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        double mid = 0.5 * (a.pos[c] + b.pos[c]);
+        vox[c] = (long long)floor(mid);
+        double dd = fabs(b.pos[c] - a.pos[c]);
+        m = dd > m ? dd : m;
+    }
+    long long vo = (long long)(b.up ? b.k - 1.0 : b.k);
+    long long vi = (long long)(a.up ? a.k : a.k - 1.0);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        if (c == b.ax) vox[c] = vo;
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        if (c == a.ax) vox[c] = vi;
+    }
+    if (!(m > kMinChord)) return -1;
+    if (vox[0] < 0 || vox[0] >= rx || vox[1] < 0 || vox[1] >= ry || vox[2] < 0 || vox[2] >= rz)
+        return -1;
+    return vox[0] + (i64)rx * (vox[1] + (i64)ry * vox[2]);
+}
+
+// _faces_and_bins, voxelizer.py:358-380.  Returns face | code << 3, or ~0 when off
+// every face.
+__device__ __forceinline__ u32 face_and_bin(const double p[3], const long long vox[3], int n) {
+    double local[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) local[c] = p[c] - (double)vox[c];
+    int f = -1;
+#pragma unroll
+    for (int ax = 2; ax >= 0; --ax) {  // lowest face id wins: scan downward, overwrite
+        if (local[ax] >= 1.0 - kFaceEps) f = 2 * ax + 1;
+        if (local[ax] <= kFaceEps) f = 2 * ax;
+    }
+    if (f < 0) return 0xFFFFFFFFu;
+    int axis = f >> 1;
+    double u = axis == 0 ? local[1] : local[0];
+    double v = axis == 2 ? local[1] : local[2];
+    long long bu = (long long)floor(u * (double)n);
+    long long bv = (long long)floor(v * (double)n);
+    bu = bu < 0 ? 0 : (bu > n - 1 ? n - 1 : bu);
+    bv = bv < 0 ? 0 : (bv > n - 1 ? n - 1 : bv);
+    return (u32)f | ((u32)(bu + (long long)n * bv) << 3);
+}
+
+// One thread per polyline edge.  EMIT=false: count chords per voxel.  EMIT=true:
+// scatter raw records through the per-voxel cursors.
+template <bool EMIT>
+__global__ void __launch_bounds__(kClipThreads)
+clip_kernel(const double *__restrict__ pts, const double *__restrict__ attrs,
+            const u8 *__restrict__ first, i64 n_points, int rx, int ry, int rz, int n_bins,
+            u32 *__restrict__ vox_cnt_or_cursor, u64 *__restrict__ raw_key,
+            u64 *__restrict__ raw_q, u32 *__restrict__ raw_lin, u16 *__restrict__ edge_kept,
+            int *__restrict__ err) {
+    __shared__ double s_pts[(kClipThreads + 1) * 3];
+    const i64 base = (i64)blockIdx.x * kClipThreads;
+    // coalesced staging of this block's kClipThreads+1 vertices
+    {
+        const i64 lo = base * 3;
+        const i64 hi = min((base + kClipThreads + 1) * 3, n_points * 3);
+        for (i64 k = lo + threadIdx.x; k < hi; k += kClipThreads) s_pts[k - lo] = pts[k];
+    }
+    __syncthreads();
+    const i64 i = base + threadIdx.x;
+    if (i >= n_points) return;
+    int kept = 0;
+    if (i + 1 < n_points && !first[i + 1]) {
+        double a0[3], a1[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            a0[c] = s_pts[3 * threadIdx.x + c];
+            a1[c] = s_pts[3 * (threadIdx.x + 1) + c];
+        }
+        EdgeAxes E;
+        E.init(a0, a1);
+        if (E.total() > 0) {
+            double att0 = 0.0, att1 = 0.0;
+            if (EMIT) {
+                att0 = attrs[i];
+                att1 = attrs[i + 1];
+            }
+            Event prev, ev;
+            bool have_prev = lookback_event<EMIT>(pts, attrs, first, i, prev);
+            int j[3] = {0, 0, 0};
+            double s_next[3], k_next[3];
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) {
+                k_next[ax] = E.plane(ax, 0);
+                s_next[ax] = E.cnt[ax] > 0 ? E.param(ax, k_next[ax]) : 2.0;
+            }
+            const int total = E.total();
+            for (int n = 0; n < total; ++n) {
+                // smallest s first; ties resolve x<y<z (stable lexsort, voxelizer.py:224)
+                int best = 0;
+                double bs = s_next[0];
+                if (s_next[1] < bs) {
+                    best = 1;
+                    bs = s_next[1];
+                }
+                if (s_next[2] < bs) {
+                    best = 2;
+                    bs = s_next[2];
+                }
+                double bk = best == 0 ? k_next[0] : (best == 1 ? k_next[1] : k_next[2]);
+                make_event(ev, E, a0, att0, att1, EMIT, best, bk, bs);
+                if (have_prev) {
+                    long long vox[3];
+                    i64 lin = chord_voxel(prev, ev, rx, ry, rz, vox);
+                    if (lin >= 0) {
+                        if (!EMIT) {
+                            atomicAdd(&vox_cnt_or_cursor[lin], 1u);
+                        } else {
+                            // voxelizer.py:439 -- rint is round-half-even
+                            double av = rint(255.0 * 0.5 * (prev.attr + ev.attr));
+                            av = av < 0.0 ? 0.0 : (av > 255.0 ? 255.0 : av);
+                            u32 fin = face_and_bin(prev.pos, vox, n_bins);
+                            u32 fout = face_and_bin(ev.pos, vox, n_bins);
+                            if (fin == 0xFFFFFFFFu || fout == 0xFFFFFFFFu) {
+                                *err = 1;
+                                fin = fout = 0;
+                            }
+                            u64 q = (u64)fin | ((u64)fout << 19) | ((u64)(u32)av << 38);
+                            u32 slot = atomicAdd(&vox_cnt_or_cursor[lin], 1u);
+                            raw_key[slot] = ((u64)i << 16) | (u64)kept;
+                            raw_q[slot] = q;
+                            raw_lin[slot] = (u32)lin;
+                        }
+                        kept += 1;
+                    }
+                }
+                prev = ev;
+                have_prev = true;
+                // advance the axis that fired
+#pragma unroll
+                for (int ax = 0; ax < 3; ++ax) {
+                    if (ax == best) {
+                        j[ax] += 1;
+                        if (j[ax] < E.cnt[ax]) {
+                            k_next[ax] = E.plane(ax, j[ax]);
+                            s_next[ax] = E.param(ax, k_next[ax]);
+                        } else {
+                            s_next[ax] = 2.0;  // exhausted (valid s are clipped to <= 1)
+                        }
+                    }
+                }
+            }
+        }
+    }
+    if (EMIT && edge_kept) edge_kept[i] = (u16)kept;
+}
+
+__global__ void mark_starts_kernel(const i64 *__restrict__ curve_off, i64 n_curves,
+                                   u8 *__restrict__ first) {
+    i64 c = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < n_curves) first[curve_off[c]] = 1;
+}
+
+// ---------------------------------------------------------------------------
+// Device prefix sums (three-phase: tile sums, scan of tile sums, tile rescan).
+// ---------------------------------------------------------------------------
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+// Block-wide exclusive scan of one u32 per thread; returns the thread's exclusive
+// prefix and leaves the block total in *total.
+__device__ __forceinline__ u32 block_exclusive_scan(u32 v, u32 *s_warp, u32 *total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    u32 inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        u32 t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        u32 w = lane < (kScanThreads / 32) ? s_warp[lane] : 0;
+        u32 winc = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            u32 t = __shfl_up_sync(0xFFFFFFFFu, winc, o);
+            if (lane >= o) winc += t;
+        }
+        if (lane < (kScanThreads / 32)) s_warp[lane] = winc - w;
+        if (lane == (kScanThreads / 32) - 1) s_warp[kScanThreads / 32] = winc;
+    }
+    __syncthreads();
+    u32 res = s_warp[warp] + inc - v;
+    *total = s_warp[kScanThreads / 32];
+    __syncthreads();
+    return res;
+}
+
+template <typename T>
+__device__ __forceinline__ u32 load_count(const T *in, i64 idx, i64 n) {
+    return idx < n ? (u32)in[idx] : 0u;
+}
+
+// phase 1: per-tile sums of raw and capped counts
+template <typename T, bool CAP>
+__global__ void __launch_bounds__(kScanThreads)
+scan_tile_sums(const T *__restrict__ in, i64 n, u64 *__restrict__ partial) {
+    __shared__ u32 s_warp[kScanThreads / 32 + 1];
+    const i64 t0 = (i64)blockIdx.x * kScanTile + (i64)threadIdx.x * kScanItems;
+    u32 raw = 0, cap = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        u32 v = load_count(in, t0 + k, n);
+        raw += v;
+        cap += CAP ? (v > 255u ? 255u : v) : 0u;
+    }
+    u32 total;
+    block_exclusive_scan(raw, s_warp, &total);
+    if (threadIdx.x == 0) partial[2 * (i64)blockIdx.x] = total;
+    if (CAP) {
+        block_exclusive_scan(cap, s_warp, &total);
+        if (threadIdx.x == 0) partial[2 * (i64)blockIdx.x + 1] = total;
+    } else if (threadIdx.x == 0) {
+        partial[2 * (i64)blockIdx.x + 1] = 0;
+    }
+}
+
+// phase 2: one block turns the tile sums into exclusive prefixes (u64) in place
+__global__ void __launch_bounds__(1024) scan_partials(u64 *partial, i64 n_tiles, u64 *totals) {
+    __shared__ u64 s_a[1024], s_b[1024];
+    u64 run_a = 0, run_b = 0;
+    for (i64 base = 0; base < n_tiles; base += 1024) {
+        i64 idx = base + threadIdx.x;
+        u64 a = idx < n_tiles ? partial[2 * idx] : 0, b = idx < n_tiles ? partial[2 * idx + 1] : 0;
+        s_a[threadIdx.x] = a;
+        s_b[threadIdx.x] = b;
+        __syncthreads();
+        for (int o = 1; o < 1024; o <<= 1) {
+            u64 ta = threadIdx.x >= o ? s_a[threadIdx.x - o] : 0;
+            u64 tb = threadIdx.x >= o ? s_b[threadIdx.x - o] : 0;
+            __syncthreads();
+            s_a[threadIdx.x] += ta;
+            s_b[threadIdx.x] += tb;
+            __syncthreads();
+        }
+        if (idx < n_tiles) {
+            partial[2 * idx] = run_a + s_a[threadIdx.x] - a;
+            partial[2 * idx + 1] = run_b + s_b[threadIdx.x] - b;
+        }
+        run_a += s_a[1023];
+        run_b += s_b[1023];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && totals) {
+        totals[0] = run_a;
+        totals[1] = run_b;
+    }
+}
+
+// phase 3: rescan each tile with its prefix and write the outputs
+template <typename T, bool CAP>
+__global__ void __launch_bounds__(kScanThreads)
+scan_write(const T *__restrict__ in, i64 n, const u64 *__restrict__ partial,
+           u32 *__restrict__ out_raw, u32 *__restrict__ out_cap, u8 *__restrict__ out_counts) {
+    __shared__ u32 s_warp[kScanThreads / 32 + 1];
+    const i64 t0 = (i64)blockIdx.x * kScanTile + (i64)threadIdx.x * kScanItems;
+    u32 v[kScanItems];
+    u32 raw = 0, cap = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        v[k] = load_count(in, t0 + k, n);
+        raw += v[k];
+        cap += CAP ? (v[k] > 255u ? 255u : v[k]) : 0u;
+    }
+    u32 total;
+    u32 pr = block_exclusive_scan(raw, s_warp, &total) + (u32)partial[2 * (i64)blockIdx.x];
+    u32 pc = 0;
+    if (CAP) pc = block_exclusive_scan(cap, s_warp, &total) + (u32)partial[2 * (i64)blockIdx.x + 1];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        i64 idx = t0 + k;
+        if (idx < n) {
+            out_raw[idx] = pr;
+            if (CAP) {
+                u32 c = v[k] > 255u ? 255u : v[k];
+                out_cap[idx] = pc;
+                out_counts[idx] = (u8)c;
+                pc += c;
+            }
+        }
+        pr += v[k];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Compaction: rank every raw record inside its voxel by key, apply the 255 cap,
+// assign lid, decode bin centres, pack.  One thread per raw record.
+// ---------------------------------------------------------------------------
+
+struct CompactOut {
+    u8 *packed;
+    float *seg_a, *seg_b;
+    u8 *seg_attr, *seg_lid;
+    int32_t *seg_voxel;
+    u8 *face_in, *face_out;
+    u16 *bin_in, *bin_out;
+    u64 *seg_key;
+    lvx_seg_record *seg_rec;
+};
+
+__device__ __forceinline__ void decode_point(u32 face, u32 code, int n, int lb, int vx, int vy,
+                                             int vz, float out[3]) {
+    // bin centre + voxel, cast to f32 (voxelizer.py:376-380, 477-478)
+    const int bu = (int)(code & (u32)(n - 1)), bv = (int)(code >> lb);
+    const double cu = ((double)bu + 0.5) / (double)n, cv = ((double)bv + 0.5) / (double)n;
+    const int axis = (int)(face >> 1);
+    double q[3];
+    q[0] = axis == 0 ? (double)(face & 1) : cu;
+    q[1] = axis == 1 ? (double)(face & 1) : (axis == 0 ? cu : cv);
+    q[2] = axis == 2 ? (double)(face & 1) : cv;
+    out[0] = (float)(q[0] + (double)vx);
+    out[1] = (float)(q[1] + (double)vy);
+    out[2] = (float)(q[2] + (double)vz);
+}
+
+__global__ void __launch_bounds__(256)
+compact_kernel(const u64 *__restrict__ raw_key, const u64 *__restrict__ raw_q,
+               const u32 *__restrict__ raw_lin, i64 n_raw, const u32 *__restrict__ vox_cnt,
+               const u32 *__restrict__ cursor_end, const u32 *__restrict__ offsets, int rx, int ry,
+               int n_bins, int lb, int width, CompactOut o) {
+    const i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_raw) return;
+    const u32 lin = raw_lin[r];
+    const u32 n = vox_cnt[lin];
+    const u64 key = raw_key[r];
+    u32 rank = 0;
+    if (n > 1) {
+        const u32 end = cursor_end[lin];
+        for (u32 k = end - n; k < end; ++k) rank += raw_key[k] < key ? 1u : 0u;
+    }
+    if (rank >= 255u) return;  // voxelizer.py:442-448 keep the first 255 in curve order
+    const i64 dst = (i64)offsets[lin] + rank;
+    const u64 q = raw_q[r];
+    const u32 fi = (u32)(q & 7u), bi = (u32)((q >> 3) & 0xFFFFu);
+    const u32 fo = (u32)((q >> 19) & 7u), bo = (u32)((q >> 22) & 0xFFFFu);
+    const u32 attr = (u32)((q >> 38) & 0xFFu);
+    const u32 lid = rank & 31u;  // voxelizer.py:449
+    const int vx = (int)(lin % (u32)rx), vy = (int)((lin / (u32)rx) % (u32)ry),
+              vz = (int)(lin / ((u32)rx * (u32)ry));
+    float a[3], b[3];
+    decode_point(fi, bi, n_bins, lb, vx, vy, vz, a);
+    decode_point(fo, bo, n_bins, lb, vx, vy, vz, b);
+    // _field_layout / _pack_all, voxelizer.py:79-89, 383-394 (LSB first)
+    const int bb = 2 * lb;
+    const u64 value = (u64)fi | ((u64)bi << 3) | ((u64)fo << (3 + bb)) | ((u64)bo << (6 + bb)) |
+                      ((u64)attr << (6 + 2 * bb)) | ((u64)lid << (14 + 2 * bb));
+    u8 *pk = o.packed + dst * width;
+    for (int k = 0; k < width; ++k) pk[k] = (u8)(value >> (8 * k));
+    if (o.seg_a) {
+        o.seg_a[3 * dst] = a[0];
+        o.seg_a[3 * dst + 1] = a[1];
+        o.seg_a[3 * dst + 2] = a[2];
+    }
+    if (o.seg_b) {
+        o.seg_b[3 * dst] = b[0];
+        o.seg_b[3 * dst + 1] = b[1];
+        o.seg_b[3 * dst + 2] = b[2];
+    }
+    if (o.seg_attr) o.seg_attr[dst] = (u8)attr;
+    if (o.seg_lid) o.seg_lid[dst] = (u8)lid;
+    if (o.seg_voxel) {
+        o.seg_voxel[3 * dst] = vx;
+        o.seg_voxel[3 * dst + 1] = vy;
+        o.seg_voxel[3 * dst + 2] = vz;
+    }
+    if (o.face_in) o.face_in[dst] = (u8)fi;
+    if (o.face_out) o.face_out[dst] = (u8)fo;
+    if (o.bin_in) o.bin_in[dst] = (u16)bi;
+    if (o.bin_out) o.bin_out[dst] = (u16)bo;
+    if (o.seg_key) o.seg_key[dst] = key;
+    if (o.seg_rec) {
+        float4 *rec = reinterpret_cast<float4 *>(o.seg_rec + dst);
+        rec[0] = make_float4(a[0], a[1], a[2], __uint_as_float(attr | (lid << 8)));
+        rec[1] = make_float4(b[0], b[1], b[2], 0.0f);
+    }
+}
+
+__global__ void __launch_bounds__(256)
+provenance_kernel(const u64 *__restrict__ seg_key, i64 n_seg, const u32 *__restrict__ edge_base,
+                  const i64 *__restrict__ curve_off, i64 n_curves, int32_t *__restrict__ seg_curve,
+                  int32_t *__restrict__ seg_order) {
+    const i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n_seg) return;
+    const u64 key = seg_key[s];
+    const i64 e = (i64)(key >> 16);
+    const u32 jk = (u32)(key & 0xFFFFu);
+    // curve = last c with curve_off[c] <= e
+    i64 lo = 0, hi = n_curves;  // invariant: curve_off[lo] <= e < curve_off[hi]
+    while (hi - lo > 1) {
+        i64 mid = (lo + hi) >> 1;
+        if (curve_off[mid] <= e) lo = mid;
+        else hi = mid;
+    }
+    seg_curve[s] = (int32_t)lo;
+    // chord index inside the curve after filtering (voxelizer.py:254-262)
+    seg_order[s] = (int32_t)(edge_base[e] + jk - edge_base[curve_off[lo]]);
+}
+
+__global__ void __launch_bounds__(256)
+seg_records_kernel(const float *__restrict__ seg_a, const float *__restrict__ seg_b,
+                   const u8 *__restrict__ seg_attr, const u8 *__restrict__ seg_lid, i64 n,
+                   lvx_seg_record *__restrict__ rec) {
+    const i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    float4 *r = reinterpret_cast<float4 *>(rec + s);
+    u32 meta = (u32)seg_attr[s] | ((u32)seg_lid[s] << 8);
+    r[0] = make_float4(seg_a[3 * s], seg_a[3 * s + 1], seg_a[3 * s + 2], __uint_as_float(meta));
+    r[1] = make_float4(seg_b[3 * s], seg_b[3 * s + 1], seg_b[3 * s + 2], 0.0f);
+}
+
+int ilog2i(int n) {
+    int lb = 0;
+    while ((1 << (lb + 1)) <= n) ++lb;
+    return lb;
+}
+
+int check_dims(const int32_t dims[3]) {
+    LVX_REQUIRE(dims && dims[0] >= 1 && dims[1] >= 1 && dims[2] >= 1, "grid dims must be >= 1");
+    const i64 V = (i64)dims[0] * dims[1] * dims[2];
+    if (V >= ((i64)1 << 32) || (i64)dims[0] + dims[1] + dims[2] > 65000) {
+        lvx_set_error("grid %dx%dx%d exceeds the 2^32-voxel / 65000-plane limits", dims[0],
+                      dims[1], dims[2]);
+        return LVX_E_RANGE;
+    }
+    return LVX_OK;
+}
+
+int check_bins(int n) {
+    LVX_REQUIRE(n >= 2 && n <= 256 && (n & (n - 1)) == 0,
+                "bin resolution must be a power of two in [2,256], got %d", n);
+    return LVX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lvx_mark_curve_starts(const int64_t *curve_off_d, int64_t n_curves, int64_t n_points,
+                          uint8_t *first_d, void *stream) {
+    LVX_REQUIRE(curve_off_d && first_d && n_curves >= 0 && n_points >= 0, "bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_points == 0) return LVX_OK;
+    LVX_CUDA_CHECK(cudaMemsetAsync(first_d, 0, (size_t)n_points, st));
+    if (n_curves > 0) {
+        mark_starts_kernel<<<(unsigned)lvx_ceil_div(n_curves, 256), 256, 0, st>>>(curve_off_d,
+                                                                                 n_curves, first_d);
+        LVX_LAUNCH_CHECK();
+    }
+    return LVX_OK;
+}
+
+int lvx_voxelize_count(const double *pts_d, const uint8_t *first_d, int64_t n_points,
+                       const int32_t dims[3], uint32_t *vox_cnt_d, void *stream) {
+    if (int rc = check_dims(dims)) return rc;
+    LVX_REQUIRE(vox_cnt_d && n_points >= 0, "bad arguments");
+    if (n_points < 2) return LVX_OK;
+    LVX_REQUIRE(pts_d && first_d, "null input");
+    LVX_REQUIRE(n_points < ((i64)1 << 47), "too many vertices");
+    clip_kernel<false><<<(unsigned)lvx_ceil_div(n_points, kClipThreads), kClipThreads, 0,
+                         (cudaStream_t)stream>>>(pts_d, nullptr, first_d, n_points, dims[0],
+                                                 dims[1], dims[2], 0, vox_cnt_d, nullptr, nullptr,
+                                                 nullptr, nullptr, nullptr);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+size_t lvx_scan_scratch_bytes(int64_t n) {
+    return (size_t)(lvx_ceil_div(n > 0 ? n : 1, kScanTile) * 2 * sizeof(u64));
+}
+
+int lvx_voxel_scan(const uint32_t *vox_cnt_d, int64_t n_voxels, uint32_t *cursor_d,
+                   uint32_t *offsets_d, uint8_t *counts_d, uint64_t *totals_d, void *scratch_d,
+                   void *stream) {
+    LVX_REQUIRE(vox_cnt_d && cursor_d && offsets_d && counts_d && totals_d && scratch_d &&
+                    n_voxels > 0,
+                "bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    const i64 tiles = lvx_ceil_div(n_voxels, kScanTile);
+    u64 *partial = (u64 *)scratch_d;
+    scan_tile_sums<u32, true><<<(unsigned)tiles, kScanThreads, 0, st>>>(vox_cnt_d, n_voxels, partial);
+    LVX_LAUNCH_CHECK();
+    scan_partials<<<1, 1024, 0, st>>>(partial, tiles, totals_d);
+    LVX_LAUNCH_CHECK();
+    scan_write<u32, true><<<(unsigned)tiles, kScanThreads, 0, st>>>(vox_cnt_d, n_voxels, partial,
+                                                                   cursor_d, offsets_d, counts_d);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_scan_u16(const uint16_t *in_d, int64_t n, uint32_t *out_d, void *scratch_d, void *stream) {
+    LVX_REQUIRE(in_d && out_d && scratch_d && n > 0, "bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    const i64 tiles = lvx_ceil_div(n, kScanTile);
+    u64 *partial = (u64 *)scratch_d;
+    scan_tile_sums<u16, false><<<(unsigned)tiles, kScanThreads, 0, st>>>(in_d, n, partial);
+    LVX_LAUNCH_CHECK();
+    scan_partials<<<1, 1024, 0, st>>>(partial, tiles, nullptr);
+    LVX_LAUNCH_CHECK();
+    scan_write<u16, false><<<(unsigned)tiles, kScanThreads, 0, st>>>(in_d, n, partial, out_d,
+                                                                    nullptr, nullptr);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_voxelize_emit(const double *pts_d, const double *attrs_d, const uint8_t *first_d,
+                      int64_t n_points, const int32_t dims[3], int32_t n_bins, uint32_t *cursor_d,
+                      uint64_t *raw_key_d, uint64_t *raw_q_d, uint32_t *raw_lin_d,
+                      uint16_t *edge_kept_d, int32_t *err_d, void *stream) {
+    if (int rc = check_dims(dims)) return rc;
+    if (int rc = check_bins(n_bins)) return rc;
+    LVX_REQUIRE(cursor_d && err_d && n_points >= 0, "bad arguments");
+    if (n_points < 2) {
+        if (edge_kept_d && n_points > 0)
+            LVX_CUDA_CHECK(cudaMemsetAsync(edge_kept_d, 0, (size_t)n_points * 2, (cudaStream_t)stream));
+        return LVX_OK;
+    }
+    LVX_REQUIRE(pts_d && attrs_d && first_d && raw_key_d && raw_q_d && raw_lin_d, "null input");
+    clip_kernel<true><<<(unsigned)lvx_ceil_div(n_points, kClipThreads), kClipThreads, 0,
+                        (cudaStream_t)stream>>>(pts_d, attrs_d, first_d, n_points, dims[0], dims[1],
+                                                dims[2], n_bins, cursor_d, raw_key_d, raw_q_d,
+                                                raw_lin_d, edge_kept_d, err_d);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_voxelize_compact(const uint64_t *raw_key_d, const uint64_t *raw_q_d,
+                         const uint32_t *raw_lin_d, int64_t n_raw, const uint32_t *vox_cnt_d,
+                         const uint32_t *cursor_end_d, const uint32_t *offsets_d,
+                         const int32_t dims[3], int32_t n_bins, uint8_t *packed_d, float *seg_a_d,
+                         float *seg_b_d, uint8_t *seg_attr_d, uint8_t *seg_lid_d,
+                         int32_t *seg_voxel_d, uint8_t *seg_face_in_d, uint16_t *seg_bin_in_d,
+                         uint8_t *seg_face_out_d, uint16_t *seg_bin_out_d, uint64_t *seg_key_d,
+                         lvx_seg_record *seg_rec_d, void *stream) {
+    if (int rc = check_dims(dims)) return rc;
+    if (int rc = check_bins(n_bins)) return rc;
+    LVX_REQUIRE(n_raw >= 0, "bad arguments");
+    if (n_raw == 0) return LVX_OK;
+    LVX_REQUIRE(raw_key_d && raw_q_d && raw_lin_d && vox_cnt_d && cursor_end_d && offsets_d &&
+                    packed_d,
+                "null input");
+    const int lb = ilog2i(n_bins);
+    const int width = (2 * (3 + 2 * lb) + 8 + 5 + 7) / 8;  // record_width, voxelizer.py:70-76
+    CompactOut o = {packed_d,      seg_a_d,        seg_b_d,      seg_attr_d, seg_lid_d, seg_voxel_d,
+                    seg_face_in_d, seg_face_out_d, seg_bin_in_d, seg_bin_out_d, seg_key_d, seg_rec_d};
+    compact_kernel<<<(unsigned)lvx_ceil_div(n_raw, 256), 256, 0, (cudaStream_t)stream>>>(
+        raw_key_d, raw_q_d, raw_lin_d, n_raw, vox_cnt_d, cursor_end_d, offsets_d, dims[0], dims[1],
+        n_bins, lb, width, o);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_provenance(const uint64_t *seg_key_d, int64_t n_seg, const uint32_t *edge_base_d,
+                   const int64_t *curve_off_d, int64_t n_curves, int32_t *seg_curve_d,
+                   int32_t *seg_order_d, void *stream) {
+    LVX_REQUIRE(n_seg >= 0 && n_curves >= 0, "bad arguments");
+    if (n_seg == 0) return LVX_OK;
+    LVX_REQUIRE(seg_key_d && edge_base_d && curve_off_d && seg_curve_d && seg_order_d, "null input");
+    provenance_kernel<<<(unsigned)lvx_ceil_div(n_seg, 256), 256, 0, (cudaStream_t)stream>>>(
+        seg_key_d, n_seg, edge_base_d, curve_off_d, n_curves, seg_curve_d, seg_order_d);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_build_seg_records(const float *seg_a_d, const float *seg_b_d, const uint8_t *seg_attr_d,
+                          const uint8_t *seg_lid_d, int64_t n_seg, lvx_seg_record *seg_rec_d,
+                          void *stream) {
+    LVX_REQUIRE(n_seg >= 0, "bad arguments");
+    if (n_seg == 0) return LVX_OK;
+    LVX_REQUIRE(seg_a_d && seg_b_d && seg_attr_d && seg_lid_d && seg_rec_d, "null input");
+    seg_records_kernel<<<(unsigned)lvx_ceil_div(n_seg, 256), 256, 0, (cudaStream_t)stream>>>(
+        seg_a_d, seg_b_d, seg_attr_d, seg_lid_d, n_seg, seg_rec_d);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+}  // extern "C"
