@@ -137,6 +137,12 @@ def to_device(a: np.ndarray, dtype=None):
     caller's business; numpy memory is pageable)."""
     torch = require_device()
     a = np.ascontiguousarray(a, dtype=dtype)
+    if a.dtype == np.uint32:  # torch's unsigned support is partial: ship the bit pattern
+        a = a.view(np.int32)
+    elif a.dtype == np.uint16:
+        a = a.view(np.int16)
+    elif a.dtype == np.uint64:
+        a = a.view(np.int64)
     return torch.from_numpy(a).to("cuda", non_blocking=False)
 
 

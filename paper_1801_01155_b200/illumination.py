@@ -1,0 +1,218 @@
+"""Density-grid secondary rays: cone soft shadows, density-ray ambient occlusion,
+the per-voxel AO bake and its trilinear lookup (illumination.py:142-225 and
+_kernels.py:346-445, 541-620 of the reference), evaluated on the GPU.
+
+    lvx_ao_bake           <- precompute_voxel_ao / precompute_ao_kernel
+    lvx_probe_cone        <- cone_soft_shadow
+    lvx_probe_ao_density  <- ao_density_rays
+    lvx_probe_trilinear   <- sample_ao / DensityOctree.sample
+
+The geometry-based secondary rays of the reference (`hard_shadow`,
+`replines_shadow`, `ao_hemisphere_geometry`) are outside the accelerated path
+ and raise NotImplementedError here.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .lod import DensityOctree
+from .voxelizer import VoxelModel
+
+_AO_MODES = ("hemisphere-geometry", "density-rays", "precomputed")
+
+__all__ = ["AOField", "AOParams", "ao_density_rays", "ao_hemisphere_geometry", "cone_soft_shadow",
+           "hard_shadow", "precompute_voxel_ao", "replines_shadow", "sample_ao"]
+
+
+@dataclass
+class AOParams:
+    """Sampling budget for ambient occlusion: `radius` of influence in voxel units,
+    march `step` for the density integration (illumination.py:35-57)."""
+
+    n_rays: int = 100
+    radius: float = 15.0
+    step: float = 1.0
+    mode: str = "hemisphere-geometry"
+
+    def __post_init__(self):
+        if self.n_rays < 1:
+            raise ValueError(f"n_rays must be at least 1, got {self.n_rays}")
+        if not self.radius > 0:
+            raise ValueError(f"radius must be positive, got {self.radius}")
+        if not self.step > 0:
+            raise ValueError(f"step must be positive, got {self.step}")
+        if self.mode not in _AO_MODES:
+            raise ValueError(f"unknown AO mode {self.mode!r}; pick one of {sorted(_AO_MODES)}")
+
+
+class AOField:
+    """Dense per-voxel occlusion in [0,1], shaped (rz, ry, rx) (illumination.py:60-78).
+    A field baked on the GPU stays there; `values` downloads it on first access."""
+
+    def __init__(self, values=None, *, _dev=None, _shape=None):
+        self._dev = _dev
+        self._values = None
+        if values is not None:
+            v = np.asarray(values, dtype=np.float32)
+            if v.ndim != 3:
+                raise ValueError(f"expected a 3D field, got shape {v.shape}")
+            self._values = v
+            self._shape = v.shape
+        elif _dev is not None:
+            self._shape = tuple(int(s) for s in _shape)
+        else:
+            raise ValueError("expected a 3D field")
+
+    @property
+    def values(self) -> np.ndarray:
+        if self._values is None:
+            self._values = self._dev.cpu().numpy().reshape(self._shape)
+        return self._values
+
+    @property
+    def shape(self):
+        return self._shape
+
+    def flat_device(self):
+        if self._dev is None:
+            self._dev = _lib.to_device(np.ascontiguousarray(self._values.reshape(-1)))
+        return self._dev
+
+
+def _unit(v, what: str) -> np.ndarray:
+    v = np.asarray(v, dtype=np.float64)
+    n = float(np.linalg.norm(v))
+    if n == 0.0:
+        raise ValueError(f"{what} must be a nonzero vector")
+    return v / n
+
+
+_DIRS_CACHE = {}
+
+
+def fibonacci_dirs_device(n_rays: int, hemisphere: int):
+    """Direction lattice of fibonacci_dir (_kernels.py:541-552), built once on the
+    host with libm cos/sin (bit-identical to the reference) and kept on the GPU."""
+    key = (int(n_rays), int(hemisphere))
+    d = _DIRS_CACHE.get(key)
+    if d is None:
+        d = _lib.to_device(_lib.fibonacci_dirs(n_rays, hemisphere))
+        _DIRS_CACHE[key] = d
+    return d
+
+
+def _probe_trilinear(flat_d, off: int, ldims, scale: float, pts: np.ndarray) -> np.ndarray:
+    torch = _lib.require_device()
+    pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+    n = pts.shape[0]
+    pts_d = _lib.to_device(pts)
+    out = torch.empty(max(n, 1), dtype=torch.float64, device="cuda")
+    ld = (C.c_int64 * 3)(int(ldims[0]), int(ldims[1]), int(ldims[2]))
+    _lib.check(_lib.lib().lvx_probe_trilinear(_lib.ptr(flat_d), C.c_int64(off), ld, C.c_double(scale),
+                                              _lib.ptr(pts_d), C.c_int64(n), _lib.ptr(out),
+                                              _lib.stream_ptr()))
+    return out[:n].cpu().numpy()
+
+
+def cone_soft_shadow(point, light_direction, octree: DensityOctree, eps: float = 0.01):
+    """Blocking in [0,1] from marching the density pyramid toward the light
+    (illumination.py:142-155 -> cone_blocking _kernels.py:386-422).  `point` may be
+    one point or an (n,3) batch (returns a float or an array accordingly)."""
+    torch = _lib.require_device()
+    pts = np.asarray(point, dtype=np.float64)
+    single = pts.ndim == 1
+    pts = np.ascontiguousarray(pts.reshape(-1, 3))
+    d = _unit(light_direction, "light direction")
+    n = pts.shape[0]
+    lod = octree.lod_struct()
+    out = torch.empty(max(n, 1), dtype=torch.float64, device="cuda")
+    pts_d = _lib.to_device(pts)
+    _lib.check(_lib.lib().lvx_probe_cone(C.byref(lod), _lib.ptr(pts_d), _lib.f64x3(d),
+                                         C.c_double(float(eps)), C.c_int64(n), _lib.ptr(out),
+                                         _lib.stream_ptr()))
+    res = out[:n].cpu().numpy()
+    return float(res[0]) if single else res
+
+
+def ao_density_rays(point, normal, octree: DensityOctree, params: Optional[AOParams] = None):
+    """Mean per-ray blocking over deterministic hemisphere rays about the normal,
+    each integrating the fine density field until it saturates, leaves the
+    radius of influence or exits the grid (illumination.py:176-190)."""
+    if params is None:
+        params = AOParams()
+    torch = _lib.require_device()
+    pts = np.asarray(point, dtype=np.float64)
+    single = pts.ndim == 1
+    pts = np.ascontiguousarray(pts.reshape(-1, 3))
+    nrm = np.asarray(normal, dtype=np.float64).reshape(-1, 3)
+    nrm = np.stack([_unit(v, "normal") for v in nrm])
+    if nrm.shape[0] == 1 and pts.shape[0] > 1:
+        nrm = np.repeat(nrm, pts.shape[0], axis=0)
+    n = pts.shape[0]
+    lod = octree.lod_struct()
+    dirs = fibonacci_dirs_device(params.n_rays, 1)
+    out = torch.empty(max(n, 1), dtype=torch.float64, device="cuda")
+    pts_d, nrm_d = _lib.to_device(pts), _lib.to_device(np.ascontiguousarray(nrm))
+    _lib.check(_lib.lib().lvx_probe_ao_density(
+        C.byref(lod), _lib.ptr(pts_d), _lib.ptr(nrm_d), C.c_int32(int(params.n_rays)),
+        C.c_double(float(params.radius)), C.c_double(float(params.step)), _lib.ptr(dirs),
+        C.c_int64(n), _lib.ptr(out), _lib.stream_ptr()))
+    res = out[:n].cpu().numpy()
+    return float(res[0]) if single else res
+
+
+def ao_bake_device(model: VoxelModel, octree: DensityOctree, params: AOParams):
+    """The bake kernel on device-resident inputs; returns the f32[V] device tensor."""
+    torch = _lib.require_device()
+    dirs = fibonacci_dirs_device(params.n_rays, 0)
+    out = torch.empty(model.voxel_count, dtype=torch.float32, device="cuda")
+    _lib.check(_lib.lib().lvx_ao_bake(
+        _lib.ptr(model.dev("counts")), _lib.i32x3(model.spec.dims), C.c_int32(int(params.n_rays)),
+        C.c_double(float(params.radius)), C.c_double(float(params.step)), _lib.ptr(dirs),
+        _lib.ptr(octree.flat_device()), _lib.ptr(out), _lib.stream_ptr()))
+    return out
+
+
+def precompute_voxel_ao(model: VoxelModel, octree: DensityOctree, params: Optional[AOParams] = None,
+                        workers: int = 1) -> AOField:
+    """Full-sphere density-ray occlusion at every occupied voxel centre; defaults
+    to 100 rays within 5 voxels at step 1 (illumination.py:193-214).  Unoccupied
+    voxels keep 0.  `workers` is accepted for signature compatibility."""
+    if params is None:
+        params = AOParams(n_rays=100, radius=5.0, step=1.0)
+    rx, ry, rz = model.spec.dims
+    if tuple(octree.dims(0)) != (rx, ry, rz):
+        raise ValueError("octree level 0 does not match the model grid")
+    out = ao_bake_device(model, octree, params)
+    return AOField(_dev=out, _shape=(rz, ry, rx))
+
+
+def sample_ao(field: AOField, point, normal=None):
+    """Trilinear lookup of the baked field at a grid-space point, clamped to [0,1];
+    the normal is accepted for interface parity and ignored (illumination.py:217-225)."""
+    pts = np.asarray(point, dtype=np.float64)
+    single = pts.ndim == 1
+    rz, ry, rx = field.shape
+    v = _probe_trilinear(field.flat_device(), 0, (rx, ry, rz), 1.0, pts.reshape(-1, 3))
+    v = np.minimum(1.0, np.maximum(0.0, v))
+    return float(v[0]) if single else v
+
+
+def _not_built(name):
+    def fn(*args, **kwargs):
+        raise NotImplementedError(
+            f"{name} traces secondary rays against the segment geometry; only the "
+            "density-grid secondary rays (cone_soft_shadow, ao_density_rays, "
+            "precompute_voxel_ao) are part of the accelerated path")
+    fn.__name__ = name
+    return fn
+
+
+hard_shadow = _not_built("hard_shadow")
+replines_shadow = _not_built("replines_shadow")
+ao_hemisphere_geometry = _not_built("ao_hemisphere_geometry")

@@ -1,0 +1,140 @@
+"""LoD construction: level-0 density and its 2x2x2 mip chain (lod.py:82-119 of the
+reference) on the GPU.
+
+    lvx_density_l0    <- compute_density_level0   lod.py:82-94
+    lvx_build_octree  <- _coarsen / build_octree  lod.py:97-119
+
+Fields are indexed [z, y, x]; flattened C order equals the voxel linear index
+x + rx*(y + ry*z).  `DensityOctree` keeps the whole pyramid in ONE flat device
+buffer (the layout `_octree_args`, raycast.py:369-388, marshals for the render
+kernel); `levels` are numpy views downloaded on first access.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .voxelizer import VoxelModel
+
+
+def octree_layout(dims):
+    """(offsets i64[L+1], level dims i64[L,3] as dx,dy,dz, L) of the flat pyramid."""
+    off = (C.c_int64 * (_lib.MAX_LEVELS + 1))()
+    ld = (C.c_int64 * (_lib.MAX_LEVELS * 3))()
+    n = C.c_int32(0)
+    _lib.check(_lib.lib().lvx_octree_layout(_lib.i32x3(dims), off, ld, C.byref(n)))
+    L = n.value
+    return (np.asarray(off[:L + 1], dtype=np.int64),
+            np.asarray(ld[:3 * L], dtype=np.int64).reshape(L, 3), L)
+
+
+class DensityOctree:
+    """Dense density fields, level 0 at grid resolution, every level half the
+    previous per axis (rounded up) down to 1x1x1 (lod.py:27-58)."""
+
+    def __init__(self, levels=None, *, _flat_dev=None, _dims=None):
+        if levels is None and _flat_dev is None:
+            raise ValueError("need levels")
+        self._levels = None if levels is None else [np.asarray(l, dtype=np.float32) for l in levels]
+        self._flat_dev = _flat_dev
+        if _dims is None:
+            dz, dy, dx = self._levels[0].shape
+            _dims = (dx, dy, dz)
+        self._dims0 = tuple(int(d) for d in _dims)
+        self._off, self._ldims, self._n = octree_layout(self._dims0)
+        if self._levels is not None and len(self._levels) != self._n:
+            raise ValueError(f"expected {self._n} levels for grid {self._dims0}, got {len(self._levels)}")
+
+    @property
+    def levels(self) -> list:
+        if self._levels is None:
+            flat = self._flat_dev.cpu().numpy()
+            self._levels = [flat[self._off[l]:self._off[l + 1]].reshape(
+                int(self._ldims[l, 2]), int(self._ldims[l, 1]), int(self._ldims[l, 0]))
+                for l in range(self._n)]
+        return self._levels
+
+    @property
+    def n_levels(self) -> int:
+        return self._n
+
+    def dims(self, level: int):
+        dx, dy, dz = (int(v) for v in self._ldims[level])
+        return dx, dy, dz
+
+    def flat_device(self):
+        """The flat f32 pyramid on the GPU (uploaded from `levels` if it was built on the host)."""
+        if self._flat_dev is None:
+            flat = np.concatenate([np.ascontiguousarray(l, dtype=np.float32).reshape(-1)
+                                   for l in self._levels])
+            self._flat_dev = _lib.to_device(flat)
+        return self._flat_dev
+
+    def lod_struct(self, ao_flat_d=None, ao_dirs_d=None) -> "_lib.Lod":
+        s = _lib.Lod()
+        s.oct_flat_d = self.flat_device().data_ptr()
+        for i, v in enumerate(self._off):
+            s.oct_off[i] = int(v)
+        for i, v in enumerate(self._ldims.reshape(-1)):
+            s.oct_dims[i] = int(v)
+        s.n_levels = self._n
+        s.ao_flat_d = ao_flat_d.data_ptr() if ao_flat_d is not None else None
+        s.ao_dirs_d = ao_dirs_d.data_ptr() if ao_dirs_d is not None else None
+        return s
+
+    def sample(self, point, level: int) -> float:
+        """Trilinear sample at a grid-space point: cell centres carry the values and
+        queries clamp to the field edge (lod.py:42-58).  Evaluated by the device
+        probe so it is the same arithmetic the kernels use."""
+        from .illumination import _probe_trilinear
+        dx, dy, dz = self.dims(level)
+        return float(_probe_trilinear(self.flat_device(), int(self._off[level]), (dx, dy, dz),
+                                      float(1 << level), np.asarray(point, dtype=np.float64)[None])[0])
+
+
+def density_level0_device(model: VoxelModel):
+    """Level-0 density as a device tensor f32[V] (no host copy)."""
+    torch = _lib.require_device()
+    counts_d, offsets_d, rec_d, table_d, _ = model.device_view(need_occ=False)
+    V = model.voxel_count
+    out = torch.empty(V, dtype=torch.float32, device="cuda")
+    _lib.check(_lib.lib().lvx_density_l0(_lib.ptr(counts_d), _lib.ptr(offsets_d), _lib.ptr(rec_d),
+                                         _lib.ptr(table_d), C.c_int64(V), _lib.ptr(out),
+                                         _lib.stream_ptr()))
+    return out
+
+
+def compute_density_level0(model: VoxelModel) -> np.ndarray:
+    """Per-voxel sum of segment length times transfer-table opacity, (rz, ry, rx) f32."""
+    dx, dy, dz = model.spec.dims
+    _lib.require_device()
+    if model.segment_count == 0:
+        return np.zeros((dz, dy, dx), dtype=np.float32)
+    return density_level0_device(model).cpu().numpy().reshape(dz, dy, dx)
+
+
+def _octree_from_level0_device(level0_d, dims) -> DensityOctree:
+    torch = _lib.require_device()
+    off, _, _ = octree_layout(dims)
+    flat = torch.empty(int(off[-1]), dtype=torch.float32, device="cuda")
+    flat[:int(off[1])].copy_(level0_d.reshape(-1))
+    _lib.check(_lib.lib().lvx_build_octree(_lib.ptr(flat), _lib.i32x3(dims), _lib.stream_ptr()))
+    return DensityOctree(_flat_dev=flat, _dims=dims)
+
+
+def build_octree(level0: np.ndarray) -> DensityOctree:
+    """Mip chain of a (rz, ry, rx) field down to 1x1x1 (lod.py:113-119)."""
+    level0 = np.asarray(level0)
+    if level0.ndim != 3 or level0.size == 0:
+        raise ValueError(f"need a non-empty 3D field, got shape {level0.shape}")
+    _lib.require_device()
+    dz, dy, dx = level0.shape
+    l0 = _lib.to_device(np.ascontiguousarray(level0, dtype=np.float32).reshape(-1))
+    return _octree_from_level0_device(l0, (dx, dy, dz))
+
+
+def build_lod(model: VoxelModel) -> DensityOctree:
+    """compute_density_level0 + build_octree without leaving the GPU."""
+    return _octree_from_level0_device(density_level0_device(model), model.spec.dims)

@@ -1,0 +1,406 @@
+"""Per-pixel ray casting over the two-level voxel model: the reference's
+`render_frame` (raycast.py:468-521) with `render_rows` (_kernels.py:735-923)
+replaced by the sm_100a kernel behind `lvx_render`.
+
+Host-side ray setup (camera basis, tan(fov/2), light normalisation) is the same
+float64 numpy arithmetic as the reference (raycast.py:63-76, 335-341, 427-433), so
+the kernel receives bit-identical camera arguments.
+
+The small reference operations `traverse_voxels`, `intersect_ray_tube` and
+`intersect_ray_sphere` run through the device probes so tests exercise the same
+device functions the frame kernel is built from.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from .lod import DensityOctree, build_lod
+from .voxelizer import VoxelModel
+
+_OPACITY_MODES = {"constant": 0, "transfer": 1, "distance-scaled": 2}
+_SHADOW_MODES = {"none": 0, "hard": 1, "replines": 2, "cone": 3}
+_AO_MODES = {"none": 0, "hemisphere-geometry": 1, "density-rays": 2, "precomputed": 3}
+
+TILE_W, TILE_H = 8, 4  # one warp = one 8x4 pixel tile
+
+
+@dataclass
+class Camera:
+    """Pinhole camera in grid-local units; fov is vertical, in degrees (raycast.py:40-87)."""
+
+    position: Sequence[float]
+    target: Sequence[float]
+    up: Sequence[float] = (0.0, 0.0, 1.0)
+    fov: float = 45.0
+    width: int = 640
+    height: int = 360
+
+    def __post_init__(self):
+        self.position = np.asarray(self.position, dtype=np.float64)
+        self.target = np.asarray(self.target, dtype=np.float64)
+        self.up = np.asarray(self.up, dtype=np.float64)
+        if self.position.shape != (3,) or self.target.shape != (3,) or self.up.shape != (3,):
+            raise ValueError("camera vectors must have 3 components")
+        if not 0.0 < self.fov < 180.0:
+            raise ValueError("fov must be in (0, 180) degrees")
+        if self.width < 1 or self.height < 1:
+            raise ValueError("image dims must be >= 1")
+        self.basis()
+
+    def basis(self):
+        """Right/up/forward unit vectors of the view frame."""
+        fwd = self.target - self.position
+        fn = np.linalg.norm(fwd)
+        if fn < 1e-12:
+            raise ValueError("camera position and target coincide")
+        fwd = fwd / fn
+        right = np.cross(fwd, self.up)
+        rn = np.linalg.norm(right)
+        if rn < 1e-9:
+            raise ValueError("up vector is parallel to the view direction")
+        right = right / rn
+        up = np.cross(right, fwd)
+        return right, up, fwd
+
+    def ray(self, x: int, y: int):
+        """Primary ray through the centre of pixel (x, y); y runs downward."""
+        right, up, fwd = self.basis()
+        tan_half = np.tan(np.radians(self.fov) * 0.5)
+        aspect = self.width / self.height
+        ndc_x = ((x + 0.5) / self.width * 2.0 - 1.0) * tan_half * aspect
+        ndc_y = (1.0 - (y + 0.5) / self.height * 2.0) * tan_half
+        d = fwd + ndc_x * right + ndc_y * up
+        d = d / np.linalg.norm(d)
+        return self.position.copy(), d
+
+
+@dataclass
+class RenderParams:
+    """raycast.py:90-129 (same fields, defaults and validation)."""
+
+    tube_radius: float = 0.3
+    opacity_mode: str = "constant"
+    base_opacity: float = 1.0
+    tau: float = 0.95
+    neighbor_mode: str = "auto"
+    shadow_mode: str = "none"
+    ao_mode: str = "none"
+    background: Sequence[float] = (0.0, 0.0, 0.0, 1.0)
+    joint_spheres: bool = True
+    light_dir: Optional[Sequence[float]] = None  # headlight unless a direction is given
+    ambient: float = 0.2
+    diffuse: float = 0.7
+    specular: float = 0.3
+    shininess: float = 32.0
+    ao_rays: int = 25
+    ao_radius: float = 15.0
+    shadow_rep_level: int = 2
+
+    def __post_init__(self):
+        if not 0.0 < self.tube_radius <= 0.5:
+            raise ValueError("tube_radius must be in (0, 0.5] voxel units")
+        if self.opacity_mode not in _OPACITY_MODES:
+            raise ValueError("opacity_mode must be one of %s" % sorted(_OPACITY_MODES))
+        if not 0.0 < self.base_opacity <= 1.0:
+            raise ValueError("base_opacity must be in (0, 1]")
+        if not 0.0 < self.tau <= 1.0:
+            raise ValueError("tau must be in (0, 1]")
+        if self.neighbor_mode not in ("off", "on", "auto"):
+            raise ValueError("neighbor_mode must be off, on or auto")
+        if self.shadow_mode not in _SHADOW_MODES:
+            raise ValueError("shadow_mode must be one of %s" % sorted(_SHADOW_MODES))
+        if self.ao_mode not in _AO_MODES:
+            raise ValueError("ao_mode must be one of %s" % sorted(_AO_MODES))
+        bg = np.asarray(self.background, dtype=np.float64)
+        if bg.shape != (4,):
+            raise ValueError("background must be RGBA")
+        self.background = bg
+
+
+@dataclass
+class HitRecord:
+    t_in: float
+    t_out: float
+    normal: np.ndarray
+    voxel: Optional[tuple] = None
+    local_line_id: int = 0
+    attr_index: int = 0
+    kind: str = "tube"
+
+
+@dataclass
+class Frame:
+    image: np.ndarray  # (H, W, 4) float32, premultiplied RGBA in [0,1]
+    stats: dict = field(default_factory=dict)
+
+    @property
+    def width(self) -> int:
+        return self.image.shape[1]
+
+    @property
+    def height(self) -> int:
+        return self.image.shape[0]
+
+    def to_rgba8(self) -> np.ndarray:
+        return np.clip(np.rint(self.image * 255.0), 0, 255).astype(np.uint8)
+
+
+# --- point probes -----------------------------------------------------------------
+
+def _as_ray(ray):
+    origin, direction = ray
+    o = np.asarray(origin, dtype=np.float64)
+    d = np.asarray(direction, dtype=np.float64)
+    n = np.linalg.norm(d)
+    if n == 0.0:
+        raise ValueError("ray direction must be non-zero")
+    return o, d / n
+
+
+def traverse_voxels(ray, spec, pad: int = 0):
+    """Ordered (voxel, t_enter, t_exit) triples of the DDA walk (raycast.py:170-181)."""
+    torch = _lib.require_device()
+    o, d = _as_ray(ray)
+    dims = tuple(int(v) for v in getattr(spec, "dims", spec))
+    cap = dims[0] + dims[1] + dims[2] + 6 * (pad + 2)
+    vox = torch.empty((cap, 3), dtype=torch.int64, device="cuda")
+    t = torch.empty((cap, 2), dtype=torch.float64, device="cuda")
+    n = torch.zeros(1, dtype=torch.int64, device="cuda")
+    _lib.check(_lib.lib().lvx_probe_dda(_lib.f64x3(o), _lib.f64x3(d), _lib.i32x3(dims),
+                                        C.c_int32(int(pad)), C.c_int64(cap), _lib.ptr(vox),
+                                        _lib.ptr(t), _lib.ptr(n), _lib.stream_ptr()))
+    k = int(n.item())
+    vox, t = vox[:k].cpu().numpy(), t[:k].cpu().numpy()
+    return [(tuple(int(v) for v in vox[i]), float(t[i, 0]), float(t[i, 1])) for i in range(k)]
+
+
+def probe_tubes(rays: np.ndarray, a: np.ndarray, b: np.ndarray, radius: float,
+                f32_axis: bool = False) -> np.ndarray:
+    """Batched tube test: rays (n,6) = origin|unit direction, endpoints (n,3).
+    Returns (n,6) = hit, t_in, t_out, normal.  f32_axis selects the frame-kernel
+    specialisation (float32 endpoints, float32 axis arithmetic)."""
+    torch = _lib.require_device()
+    rays = np.ascontiguousarray(rays, dtype=np.float64).reshape(-1, 6)
+    n = rays.shape[0]
+    dt = np.float32 if f32_axis else np.float64
+    a_d, b_d = _lib.to_device(np.asarray(a).reshape(-1, 3), dt), _lib.to_device(np.asarray(b).reshape(-1, 3), dt)
+    out = torch.empty((max(n, 1), 6), dtype=torch.float64, device="cuda")
+    _lib.check(_lib.lib().lvx_probe_tube(_lib.ptr(_lib.to_device(rays)), _lib.ptr(a_d), _lib.ptr(b_d),
+                                         C.c_double(float(radius)), C.c_int32(1 if f32_axis else 0),
+                                         C.c_int64(n), _lib.ptr(out), _lib.stream_ptr()))
+    return out[:n].cpu().numpy()
+
+
+def probe_spheres(rays: np.ndarray, centers: np.ndarray, radius: float) -> np.ndarray:
+    torch = _lib.require_device()
+    rays = np.ascontiguousarray(rays, dtype=np.float64).reshape(-1, 6)
+    n = rays.shape[0]
+    out = torch.empty((max(n, 1), 6), dtype=torch.float64, device="cuda")
+    _lib.check(_lib.lib().lvx_probe_sphere(
+        _lib.ptr(_lib.to_device(rays)), _lib.ptr(_lib.to_device(np.asarray(centers).reshape(-1, 3), np.float64)),
+        C.c_double(float(radius)), C.c_int64(n), _lib.ptr(out), _lib.stream_ptr()))
+    return out[:n].cpu().numpy()
+
+
+def intersect_ray_sphere(ray, center, radius: float) -> Optional[HitRecord]:
+    o, d = _as_ray(ray)
+    if radius <= 0.0:
+        raise ValueError("radius must be positive")
+    r = probe_spheres(np.concatenate([o, d])[None], np.asarray(center, dtype=np.float64)[None], radius)[0]
+    if r[0] == 0.0:
+        return None
+    return HitRecord(t_in=float(r[1]), t_out=float(r[2]), normal=r[3:6].copy(), kind="joint-sphere")
+
+
+def intersect_ray_tube(ray, a, b, radius: float) -> Optional[HitRecord]:
+    """Slab-clipped cylinder test; degenerate segments fall back to the endpoint
+    sphere (raycast.py:184-200).  All-float64 specialisation, like the reference op."""
+    o, d = _as_ray(ray)
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    if radius <= 0.0:
+        raise ValueError("radius must be positive")
+    if np.linalg.norm(b - a) < 1e-12:
+        return intersect_ray_sphere(ray, a, radius)
+    r = probe_tubes(np.concatenate([o, d])[None], a[None], b[None], radius, f32_axis=False)[0]
+    if r[0] == 0.0:
+        return None
+    return HitRecord(t_in=float(r[1]), t_out=float(r[2]), normal=r[3:6].copy(), kind="tube")
+
+
+# --- frame ---------------------------------------------------------------------------
+
+def default_camera(dims, width: int = 640, height: int = 360) -> Camera:
+    """Camera that frames the whole grid from -y, slightly elevated (raycast.py:441-448)."""
+    center = np.asarray(dims, dtype=np.float64) * 0.5
+    dist = 1.9 * float(max(dims))
+    position = center + np.array([0.0, -dist, 0.42 * dist])
+    return Camera(position=position, target=center, up=(0.0, 0.0, 1.0), fov=45.0, width=width,
+                  height=height)
+
+
+def ensure_lod(model: VoxelModel, octree: Optional[DensityOctree], replines, params: RenderParams):
+    """Build the octree the requested shadow/AO modes need (raycast.py:451-465)."""
+    if params.shadow_mode == "replines":
+        raise NotImplementedError("shadow_mode='replines' is outside the accelerated path")
+    need_octree = params.shadow_mode == "cone" or params.ao_mode == "density-rays"
+    if need_octree and octree is None:
+        octree = build_lod(model)
+    if params.ao_mode == "precomputed" and model.ao is None:
+        raise ValueError("the model carries no baked AO field; run `linevox precompute-ao` first")
+    return octree, replines
+
+
+def camera_struct(camera: Camera) -> "_lib.Camera":
+    """_camera_args (raycast.py:335-341) as the C struct."""
+    right, up, fwd = camera.basis()
+    s = _lib.Camera()
+    for i in range(3):
+        s.o[i] = float(camera.position[i])
+        s.r[i] = float(right[i])
+        s.u[i] = float(up[i])
+        s.f[i] = float(fwd[i])
+    s.tan_half = float(np.tan(np.radians(camera.fov) * 0.5))
+    s.aspect = camera.width / camera.height
+    s.width, s.height = int(camera.width), int(camera.height)
+    return s
+
+
+def resolve_neighbor(params: RenderParams, moving: bool) -> int:
+    if params.neighbor_mode == "auto":
+        return 0 if moving else 1
+    return 1 if params.neighbor_mode == "on" else 0
+
+
+def params_struct(params: RenderParams, neighbor: int) -> "_lib.Params":
+    """Mode codes + shading scalars of _illum_args / render_frame (raycast.py:405-438, 498-509)."""
+    p = _lib.Params()
+    p.tube_r = float(params.tube_radius)
+    p.base_alpha = float(params.base_opacity)
+    p.tau = float(params.tau)
+    p.ka, p.kd, p.ks = float(params.ambient), float(params.diffuse), float(params.specular)
+    p.shininess = float(params.shininess)
+    if params.light_dir is None:
+        p.headlight = 1
+        light = np.zeros(3, dtype=np.float64)
+    else:
+        p.headlight = 0
+        light = np.asarray(params.light_dir, dtype=np.float64)
+        light = light / np.linalg.norm(light)
+    bg = np.asarray(params.background, dtype=np.float64)
+    for i in range(3):
+        p.light[i] = float(light[i])
+    for i in range(4):
+        p.bg[i] = float(bg[i])
+    p.opacity_mode = _OPACITY_MODES[params.opacity_mode]
+    p.neighbor = int(neighbor)
+    p.joints = 1 if params.joint_spheres else 0
+    p.shadow_mode = _SHADOW_MODES[params.shadow_mode]
+    p.ao_mode = _AO_MODES[params.ao_mode]
+    p.ao_n_rays = int(params.ao_rays)
+    p.ao_radius = float(params.ao_radius)
+    return p
+
+
+def check_modes(params: RenderParams, model: VoxelModel, octree):
+    """The error behaviour of _illum_args (raycast.py:414-421), plus the modes this
+    build does not accelerate."""
+    if params.shadow_mode in ("hard", "replines"):
+        raise NotImplementedError(f"shadow_mode={params.shadow_mode!r} traces geometry secondary "
+                                  "rays and is outside the accelerated path (none/cone only)")
+    if params.ao_mode == "hemisphere-geometry":
+        raise NotImplementedError("ao_mode='hemisphere-geometry' is outside the accelerated path "
+                                  "(none/density-rays/precomputed only)")
+    if params.shadow_mode == "cone" and octree is None:
+        raise ValueError("cone shadows need a density octree")
+    if params.ao_mode == "density-rays" and octree is None:
+        raise ValueError("density-rays AO needs a density octree")
+    if params.ao_mode == "precomputed" and getattr(model, "ao", None) is None:
+        raise ValueError("precomputed AO requested but the model carries none")
+
+
+class FramePlan:
+    """Everything `lvx_render` needs for one (camera, model, params) triple, resolved
+    once: C structs plus the device tensors they point into (kept alive here)."""
+
+    def __init__(self, camera: Camera, model: VoxelModel, octree: Optional[DensityOctree],
+                 params: RenderParams, neighbor: int, tile_first: int = 0, tile_step: int = 1,
+                 compact: bool = False, tile_w: int = TILE_W, tile_h: int = TILE_H):
+        from .illumination import fibonacci_dirs_device
+        check_modes(params, model, octree)
+        self.cam = camera_struct(camera)
+        self.par = params_struct(params, neighbor)
+        counts_d, offsets_d, rec_d, table_d, occ_d = model.device_view(need_occ=bool(neighbor))
+        m = _lib.Model()
+        m.rx, m.ry, m.rz = model.spec.dims
+        m.counts_d, m.offsets_d = counts_d.data_ptr(), offsets_d.data_ptr()
+        m.seg_rec_d, m.table_d = rec_d.data_ptr(), table_d.data_ptr()
+        m.occ_d = occ_d.data_ptr() if occ_d is not None else None
+        self.mdl = m
+        ao_d = model.ao_device() if params.ao_mode == "precomputed" else None
+        dirs_d = fibonacci_dirs_device(params.ao_rays, 1) if params.ao_mode == "density-rays" else None
+        if octree is not None:
+            self.lod = octree.lod_struct(ao_d, dirs_d)
+        else:
+            self.lod = _lib.Lod()
+            self.lod.n_levels = 0
+            self.lod.ao_flat_d = ao_d.data_ptr() if ao_d is not None else None
+        t = _lib.Tiling()
+        t.tile_w, t.tile_h = tile_w, tile_h
+        t.tile_first, t.tile_step, t.compact = int(tile_first), int(tile_step), 1 if compact else 0
+        self.til = t
+        self._keep = (counts_d, offsets_d, rec_d, table_d, occ_d, ao_d, dirs_d, octree, model)
+        self.width, self.height = int(camera.width), int(camera.height)
+
+    def n_my_tiles(self) -> int:
+        tx = -(-self.width // self.til.tile_w)
+        ty = -(-self.height // self.til.tile_h)
+        total = tx * ty
+        if self.til.tile_first >= total:
+            return 0
+        return (total - self.til.tile_first + self.til.tile_step - 1) // self.til.tile_step
+
+    def launch(self, img_d, row_stats_d):
+        """Enqueue the frame kernel on the current stream (row_stats_d must be zeroed)."""
+        _lib.check(_lib.lib().lvx_render(C.byref(self.cam), C.byref(self.mdl), C.byref(self.par),
+                                         C.byref(self.lod), C.byref(self.til), _lib.ptr(img_d),
+                                         _lib.ptr(row_stats_d), None, _lib.stream_ptr()))
+
+
+def render_frame(camera: Camera, model: VoxelModel, octree: Optional[DensityOctree] = None,
+                 replines=None, params: Optional[RenderParams] = None, workers: int = 1,
+                 moving: bool = False) -> Frame:
+    """Render one frame (raycast.py:468-521).  neighbor_mode=auto resolves to off
+    while `moving` and on otherwise.  `workers` is accepted for signature
+    compatibility; `stats["workers"]` reports the number of GPUs used (1)."""
+    if params is None:
+        params = RenderParams()
+    torch = _lib.require_device()
+    neighbor = resolve_neighbor(params, moving)
+    plan = FramePlan(camera, model, octree, params, neighbor)
+    H, W = camera.height, camera.width
+    img_d = torch.empty((H, W, 4), dtype=torch.float32, device="cuda")
+    stats_d = torch.zeros((H, 3), dtype=torch.int64, device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    plan.launch(img_d, stats_d)
+    e1.record()
+    img = torch.empty((H, W, 4), dtype=torch.float32, pin_memory=True)
+    img.copy_(img_d, non_blocking=True)
+    tot = stats_d.sum(dim=0).cpu()  # synchronises
+    torch.cuda.current_stream().synchronize()
+    stats = {
+        "rays": W * H,
+        "voxel_steps": int(tot[0]),
+        "intersection_tests": int(tot[1]),
+        "ms": float(e0.elapsed_time(e1)),
+        "workers": 1,
+        "window_overflow": int(tot[2]),
+        "neighbor": bool(neighbor),
+    }
+    return Frame(image=img.numpy(), stats=stats)

@@ -1,0 +1,429 @@
+"""Voxelizer front end: the reference's `build_voxel_model` (voxelizer.py:397-488)
+with the clip / quantize / sort / pack pipeline running as sm_100a kernels.
+
+The device pipeline (include/linevox_b200.h):
+
+    lvx_mark_curve_starts -> lvx_voxelize_count -> lvx_voxel_scan
+        -> lvx_voxelize_emit -> lvx_voxelize_compact -> lvx_scan_u16 + lvx_provenance
+
+`VoxelModel` keeps the reference's field names.  Arrays live on the GPU; the
+numpy views the reference exposes (`model.counts`, `model.packed`, `model.seg_a`,
+...) are downloaded on first access and cached.  Assigning a new array to one of
+those attributes replaces it and drops the stale device mirror; arrays mutated
+*in place* need an explicit `model.invalidate_device()`.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .scene_io import CurveSet, GridSpec
+
+_FACE_BITS, _ATTR_BITS, _LID_BITS = 3, 8, 5
+
+# name -> (numpy dtype, trailing shape)
+_ARRAY_FIELDS = {
+    "counts": (np.uint8, ()), "offsets": (np.uint32, ()), "packed": (np.uint8, ()),
+    "seg_voxel": (np.int32, (3,)), "seg_a": (np.float32, (3,)), "seg_b": (np.float32, (3,)),
+    "seg_attr": (np.uint8, ()), "seg_lid": (np.uint8, ()),
+    "seg_face_in": (np.uint8, ()), "seg_bin_in": (np.uint16, ()),
+    "seg_face_out": (np.uint8, ()), "seg_bin_out": (np.uint16, ()),
+    "seg_curve": (np.int32, ()), "seg_order": (np.int32, ()),
+}
+# device mirrors that feed the render kernels
+_RENDER_INPUTS = ("counts", "offsets", "seg_a", "seg_b", "seg_attr", "seg_lid")
+
+
+def _check_bins(n_bins: int) -> int:
+    n = int(n_bins)
+    if n < 2 or n > 256 or (n & (n - 1)) != 0:
+        raise ValueError(f"bin resolution must be a power of two in [2,256], got {n_bins}")
+    return n
+
+
+def record_width(n_bins: int) -> int:
+    """Bytes per packed record: ceil((2*(3 + 2*log2 N) + 8 + 5) / 8) (voxelizer.py:70-76)."""
+    n = _check_bins(n_bins)
+    lb = n.bit_length() - 1
+    return (2 * (_FACE_BITS + 2 * lb) + _ATTR_BITS + _LID_BITS + 7) // 8
+
+
+def unpack_records(packed: np.ndarray, n_bins: int) -> dict:
+    """Host-side decode of packed records into their six fields (the layout of
+    voxelizer.py:79-89, LSB first).  Used by tests and by callers that want to
+    inspect a model without the per-segment caches."""
+    n = _check_bins(n_bins)
+    w = record_width(n)
+    lb = n.bit_length() - 1
+    bb = 2 * lb
+    raw = np.ascontiguousarray(packed, dtype=np.uint8).reshape(-1, w)
+    value = np.zeros(raw.shape[0], dtype=np.uint64)
+    for k in range(w):
+        value |= raw[:, k].astype(np.uint64) << np.uint64(8 * k)
+    mask = np.uint64((1 << bb) - 1)
+
+    def field(shift, m):
+        return (value >> np.uint64(shift)) & np.uint64(m)
+
+    return {
+        "face_in": field(0, 7).astype(np.uint8),
+        "bin_in": (field(3, int(mask))).astype(np.uint16),
+        "face_out": field(3 + bb, 7).astype(np.uint8),
+        "bin_out": field(6 + bb, int(mask)).astype(np.uint16),
+        "attr": field(6 + 2 * bb, 0xFF).astype(np.uint8),
+        "lid": field(14 + 2 * bb, 0x1F).astype(np.uint8),
+    }
+
+
+def default_transfer_table() -> np.ndarray:
+    """Blue-grey-red ramp, opacity 1 (voxelizer.py:292-303)."""
+    t = np.linspace(0.0, 1.0, 256)
+    cold = np.array([0.231, 0.299, 0.754])
+    mid = np.array([0.865, 0.865, 0.865])
+    warm = np.array([0.706, 0.016, 0.150])
+    table = np.empty((256, 4), dtype=np.float32)
+    lo = t < 0.5
+    table[lo, :3] = cold + (t[lo, None] * 2.0) * (mid - cold)
+    table[~lo, :3] = mid + ((t[~lo, None] - 0.5) * 2.0) * (warm - mid)
+    table[:, 3] = 1.0
+    return table
+
+
+def _array_property(name):
+    def get(self):
+        return self._get_array(name)
+
+    def set_(self, value):
+        self._set_array(name, value)
+
+    return property(get, set_)
+
+
+class VoxelModel:
+    """Compact voxel encoding (`counts`, `offsets`, `packed`: 5V + width*S bytes)
+    plus the per-segment caches of the reference's VoxelModel (voxelizer.py:306-355).
+
+    Every array argument may be a numpy array (a model that arrives from the
+    host, e.g. decoded from a .vxl file) or a torch CUDA tensor (a model built
+    on the device)."""
+
+    def __init__(self, spec: GridSpec, counts, offsets, packed, transfer_table, seg_voxel=None,
+                 seg_a=None, seg_b=None, seg_attr=None, seg_lid=None, seg_face_in=None,
+                 seg_bin_in=None, seg_face_out=None, seg_bin_out=None, dropped_overflow: int = 0,
+                 seg_curve=None, seg_order=None, ao=None):
+        self.spec = spec
+        self.transfer_table = np.asarray(transfer_table, dtype=np.float32)
+        self.dropped_overflow = int(dropped_overflow)
+        self._host = {}
+        self._dev = {}
+        self._derived = {}  # seg_rec, occ, table: device-only render inputs
+        self._ao = None
+        for name, value in (("counts", counts), ("offsets", offsets), ("packed", packed),
+                            ("seg_voxel", seg_voxel), ("seg_a", seg_a), ("seg_b", seg_b),
+                            ("seg_attr", seg_attr), ("seg_lid", seg_lid),
+                            ("seg_face_in", seg_face_in), ("seg_bin_in", seg_bin_in),
+                            ("seg_face_out", seg_face_out), ("seg_bin_out", seg_bin_out),
+                            ("seg_curve", seg_curve), ("seg_order", seg_order)):
+            if value is not None:
+                self._set_array(name, value)
+        self.ao = ao
+
+    # -- array storage ----------------------------------------------------------
+    def _set_array(self, name, value):
+        if value is None:
+            self._host.pop(name, None)
+            self._dev.pop(name, None)
+        elif isinstance(value, np.ndarray) or not hasattr(value, "data_ptr"):
+            dt, tail = _ARRAY_FIELDS[name]
+            arr = np.ascontiguousarray(value, dtype=dt)
+            if tail:
+                arr = arr.reshape((-1,) + tail)
+            self._host[name] = arr
+            self._dev.pop(name, None)
+        else:
+            self._dev[name] = value
+            self._host.pop(name, None)
+        if name in _RENDER_INPUTS:
+            self._derived.clear()
+            self.__dict__.pop("_occ_dilated", None)
+
+    def _get_array(self, name):
+        h = self._host.get(name)
+        if h is None:
+            d = self._dev.get(name)
+            if d is None:
+                if name in ("seg_curve", "seg_order"):
+                    return None  # optional in the reference too
+                raise AttributeError(f"model carries no {name}")
+            h = d.cpu().numpy()
+            dt = np.dtype(_ARRAY_FIELDS[name][0])
+            if h.dtype != dt:  # u16/u32 travel as same-width signed torch tensors
+                h = h.view(dt)
+            self._host[name] = h
+        return h
+
+    counts = _array_property("counts")
+    offsets = _array_property("offsets")
+    packed = _array_property("packed")
+    seg_voxel = _array_property("seg_voxel")
+    seg_a = _array_property("seg_a")
+    seg_b = _array_property("seg_b")
+    seg_attr = _array_property("seg_attr")
+    seg_lid = _array_property("seg_lid")
+    seg_face_in = _array_property("seg_face_in")
+    seg_bin_in = _array_property("seg_bin_in")
+    seg_face_out = _array_property("seg_face_out")
+    seg_bin_out = _array_property("seg_bin_out")
+    seg_curve = _array_property("seg_curve")
+    seg_order = _array_property("seg_order")
+
+    @property
+    def ao(self):
+        """Optional baked occlusion, (rz, ry, rx) float32 (voxelizer.py:334-335).
+        Accepts an ndarray or an AOField; a field baked on the GPU is not copied
+        to the host until someone reads this attribute."""
+        a = self._ao
+        if a is not None and not isinstance(a, np.ndarray):
+            return a.values
+        return a
+
+    @ao.setter
+    def ao(self, value):
+        self._derived.pop("ao", None)
+        if value is None or hasattr(value, "flat_device"):
+            self._ao = value
+        else:
+            self._ao = np.asarray(value, dtype=np.float32)
+
+    def invalidate_device(self):
+        """Forget every device mirror of arrays that also exist on the host (call
+        after mutating a host array in place)."""
+        for name in list(self._dev):
+            if name in self._host:
+                del self._dev[name]
+        self._derived.clear()
+        self.__dict__.pop("_occ_dilated", None)
+
+    def dev(self, name):
+        """Device tensor of one array field (uploaded from the host copy if needed)."""
+        d = self._dev.get(name)
+        if d is None:
+            d = _lib.to_device(self._get_array(name))
+            self._dev[name] = d
+        return d
+
+    # -- reference properties -----------------------------------------------------
+    @property
+    def voxel_count(self) -> int:
+        return self.spec.voxel_count
+
+    @property
+    def segment_count(self) -> int:
+        for store in (self._host, self._dev):
+            a = store.get("seg_attr")
+            if a is not None:
+                return int(a.shape[0])
+        p = self._host.get("packed")
+        if p is None:
+            p = self._dev["packed"]
+        return int(p.shape[0]) // self.record_width
+
+    @property
+    def record_width(self) -> int:
+        return record_width(self.spec.bins_per_axis)
+
+    @property
+    def memory_bytes(self) -> int:
+        return 5 * self.voxel_count + self.record_width * self.segment_count
+
+    def linear_index(self, voxel) -> int:
+        dx, dy, _ = self.spec.dims
+        return int(voxel[0] + dx * (voxel[1] + dy * voxel[2]))
+
+    # -- device-side render inputs --------------------------------------------------
+    def device_view(self, need_occ: bool = True):
+        """(counts_d, offsets_d, seg_rec_d, table_d, occ_d) -- the lvx_model fields."""
+        torch = _lib.require_device()
+        L = _lib.lib()
+        st = _lib.stream_ptr()
+        d = self._derived
+        S = self.segment_count
+        if "seg_rec" not in d:
+            rec = torch.empty((max(S, 1), 8), dtype=torch.float32, device="cuda")
+            if S:
+                _lib.check(L.lvx_build_seg_records(
+                    _lib.ptr(self.dev("seg_a")), _lib.ptr(self.dev("seg_b")),
+                    _lib.ptr(self.dev("seg_attr")), _lib.ptr(self.dev("seg_lid")),
+                    C.c_int64(S), _lib.ptr(rec), st))
+            d["seg_rec"] = rec
+        if "table" not in d or d.get("table_src") is not self.transfer_table:
+            d["table"] = _lib.to_device(np.ascontiguousarray(self.transfer_table, dtype=np.float32))
+            d["table_src"] = self.transfer_table
+        if need_occ and "occ" not in d:
+            rx, ry, rz = self.spec.dims
+            occ = torch.empty((rx + 2) * (ry + 2) * (rz + 2), dtype=torch.uint8, device="cuda")
+            _lib.check(L.lvx_occupancy_dilate(_lib.ptr(self.dev("counts")), _lib.i32x3(self.spec.dims),
+                                              _lib.ptr(occ), st))
+            d["occ"] = occ
+        return (self.dev("counts"), self.dev("offsets"), d["seg_rec"], d["table"], d.get("occ"))
+
+    def ao_device(self):
+        """Flat f32[V] device tensor of the baked AO field, or None."""
+        a = self._ao
+        if a is None:
+            return None
+        if not isinstance(a, np.ndarray):
+            return a.flat_device()
+        d = self._derived
+        if "ao" not in d:
+            d["ao"] = _lib.to_device(np.ascontiguousarray(a.reshape(-1), dtype=np.float32))
+        return d["ao"]
+
+
+# ---------------------------------------------------------------------------------
+
+def voxelize_device(pts_d, attrs_d, off_d, n_curves: int, spec: GridSpec, *, caches: bool = True,
+                    provenance: bool = True, memory_budget: Optional[int] = None):
+    """Run the device pipeline on vertex arrays that already live on the GPU.
+
+    pts_d f64[P,3], attrs_d f64[P], off_d i64[n_curves+1].  Returns a dict of
+    device tensors plus `dropped` and `n_segments`.  This is the kernel-only path
+    bench.py times; `build_voxel_model` wraps it with the host<->device copies."""
+    torch = _lib.require_device()
+    L = _lib.lib()
+    st = _lib.stream_ptr()
+    n_bins = spec.bins_per_axis
+    dims = _lib.i32x3(spec.dims)
+    V = spec.voxel_count
+    P = int(pts_d.shape[0])
+    w = record_width(n_bins)
+    dev = "cuda"
+
+    first = torch.empty(max(P, 1), dtype=torch.uint8, device=dev)
+    _lib.check(L.lvx_mark_curve_starts(_lib.ptr(off_d), C.c_int64(n_curves), C.c_int64(P),
+                                       _lib.ptr(first), st))
+    vox_cnt = torch.zeros(V, dtype=torch.int32, device=dev)
+    _lib.check(L.lvx_voxelize_count(_lib.ptr(pts_d), _lib.ptr(first), C.c_int64(P), dims,
+                                    _lib.ptr(vox_cnt), st))
+    cursor = torch.empty(V, dtype=torch.int32, device=dev)
+    offsets = torch.empty(V, dtype=torch.int32, device=dev)  # u32 bit pattern
+    counts = torch.empty(V, dtype=torch.uint8, device=dev)
+    totals = torch.zeros(2, dtype=torch.int64, device=dev)
+    scratch = torch.empty(max(int(L.lvx_scan_scratch_bytes(C.c_int64(max(V, P)))), 16),
+                          dtype=torch.uint8, device=dev)
+    _lib.check(L.lvx_voxel_scan(_lib.ptr(vox_cnt), C.c_int64(V), _lib.ptr(cursor), _lib.ptr(offsets),
+                                _lib.ptr(counts), _lib.ptr(totals), _lib.ptr(scratch), st))
+    n_raw, S = (int(x) for x in totals.cpu().tolist())  # the one sync: sizes the outputs
+    if n_raw >= 2 ** 32:
+        raise MemoryError(f"{n_raw} chords exceed the 32-bit offsets of the voxel headers")
+    total_bytes = 5 * V + w * S
+    if memory_budget is not None and total_bytes > memory_budget:
+        raise MemoryError(f"model needs {total_bytes} bytes (5*{V} + {w}*{S}), "
+                          f"budget is {memory_budget}")
+
+    raw_key = torch.empty(max(n_raw, 1), dtype=torch.int64, device=dev)
+    raw_q = torch.empty(max(n_raw, 1), dtype=torch.int64, device=dev)
+    raw_lin = torch.empty(max(n_raw, 1), dtype=torch.int32, device=dev)
+    edge_kept = torch.empty(max(P, 1), dtype=torch.int16, device=dev) if provenance else None
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    _lib.check(L.lvx_voxelize_emit(_lib.ptr(pts_d), _lib.ptr(attrs_d), _lib.ptr(first), C.c_int64(P),
+                                   dims, C.c_int32(n_bins), _lib.ptr(cursor), _lib.ptr(raw_key),
+                                   _lib.ptr(raw_q), _lib.ptr(raw_lin), _lib.ptr(edge_kept),
+                                   _lib.ptr(err), st))
+    m = max(S, 1)
+    out = {
+        "counts": counts, "offsets": offsets,
+        "packed": torch.empty(m * w, dtype=torch.uint8, device=dev),
+        "seg_rec": torch.empty((m, 8), dtype=torch.float32, device=dev),
+    }
+    if caches:
+        out.update(
+            seg_a=torch.empty((m, 3), dtype=torch.float32, device=dev),
+            seg_b=torch.empty((m, 3), dtype=torch.float32, device=dev),
+            seg_attr=torch.empty(m, dtype=torch.uint8, device=dev),
+            seg_lid=torch.empty(m, dtype=torch.uint8, device=dev),
+            seg_voxel=torch.empty((m, 3), dtype=torch.int32, device=dev),
+            seg_face_in=torch.empty(m, dtype=torch.uint8, device=dev),
+            seg_bin_in=torch.empty(m, dtype=torch.int16, device=dev),
+            seg_face_out=torch.empty(m, dtype=torch.uint8, device=dev),
+            seg_bin_out=torch.empty(m, dtype=torch.int16, device=dev))
+    seg_key = torch.empty(m, dtype=torch.int64, device=dev) if provenance else None
+    g = out.get
+    _lib.check(L.lvx_voxelize_compact(
+        _lib.ptr(raw_key), _lib.ptr(raw_q), _lib.ptr(raw_lin), C.c_int64(n_raw), _lib.ptr(vox_cnt),
+        _lib.ptr(cursor), _lib.ptr(offsets), dims, C.c_int32(n_bins), _lib.ptr(out["packed"]),
+        _lib.ptr(g("seg_a")), _lib.ptr(g("seg_b")), _lib.ptr(g("seg_attr")), _lib.ptr(g("seg_lid")),
+        _lib.ptr(g("seg_voxel")), _lib.ptr(g("seg_face_in")), _lib.ptr(g("seg_bin_in")),
+        _lib.ptr(g("seg_face_out")), _lib.ptr(g("seg_bin_out")), _lib.ptr(seg_key),
+        _lib.ptr(out["seg_rec"]), st))
+    if provenance:
+        seg_curve = torch.empty(m, dtype=torch.int32, device=dev)
+        seg_order = torch.empty(m, dtype=torch.int32, device=dev)
+        if S:
+            edge_base = torch.empty(P, dtype=torch.int32, device=dev)
+            _lib.check(L.lvx_scan_u16(_lib.ptr(edge_kept), C.c_int64(P), _lib.ptr(edge_base),
+                                      _lib.ptr(scratch), st))
+            _lib.check(L.lvx_provenance(_lib.ptr(seg_key), C.c_int64(S), _lib.ptr(edge_base),
+                                        _lib.ptr(off_d), C.c_int64(n_curves), _lib.ptr(seg_curve),
+                                        _lib.ptr(seg_order), st))
+        out["seg_curve"], out["seg_order"] = seg_curve, seg_order
+    # trim the >=1 padding of empty models
+    for k in list(out):
+        if k in ("counts", "offsets"):
+            continue
+        out[k] = out[k][:S * w] if k == "packed" else out[k][:S]
+    out["n_segments"] = S
+    out["dropped"] = n_raw - S
+    out["err"] = err
+    return out
+
+
+def build_voxel_model(curves: CurveSet, spec: GridSpec, transfer_table=None, workers: int = 1,
+                      memory_budget: Optional[int] = None) -> VoxelModel:
+    """Clip, quantize, pack and compact a whole curve set (voxelizer.py:397-488).
+
+    `workers` is accepted for signature compatibility: the reference's output
+    does not depend on it (voxelizer.py:401-403) and the device pipeline has no
+    use for it.  Voxels crossed by more than 255 chords keep the first 255 in
+    curve order; the rest are counted in `dropped_overflow`."""
+    if transfer_table is None:
+        transfer_table = default_transfer_table()
+    transfer_table = np.asarray(transfer_table, dtype=np.float32)
+    if transfer_table.shape != (256, 4):
+        raise ValueError(f"transfer table must be (256,4), got {transfer_table.shape}")
+    _lib.require_device()
+    pts, attrs, off = curves.flat()
+    pts_d = _lib.to_device(pts, np.float64)
+    attrs_d = _lib.to_device(attrs, np.float64)
+    off_d = _lib.to_device(off, np.int64)
+    out = voxelize_device(pts_d, attrs_d, off_d, int(off.size - 1), spec,
+                          memory_budget=memory_budget)
+    if int(out["err"].item()) != 0:
+        # voxelizer.py:366-368
+        raise AssertionError("chord endpoint off every face")
+    model = VoxelModel(
+        spec=spec, counts=out["counts"], offsets=out["offsets"], packed=out["packed"],
+        transfer_table=transfer_table, seg_voxel=out["seg_voxel"], seg_a=out["seg_a"],
+        seg_b=out["seg_b"], seg_attr=out["seg_attr"], seg_lid=out["seg_lid"],
+        seg_face_in=out["seg_face_in"], seg_bin_in=out["seg_bin_in"],
+        seg_face_out=out["seg_face_out"], seg_bin_out=out["seg_bin_out"],
+        dropped_overflow=out["dropped"], seg_curve=out["seg_curve"], seg_order=out["seg_order"])
+    model._derived["seg_rec"] = out["seg_rec"]
+    return model
+
+
+def count_duplicates(model: VoxelModel) -> float:
+    """Fraction of segments whose (voxel, faces, bins) repeat an earlier record
+    (voxelizer.py:491-509)."""
+    s = model.segment_count
+    if s == 0:
+        return 0.0
+    dx, dy, _ = model.spec.dims
+    v = model.seg_voxel.astype(np.int64)
+    lin = v[:, 0] + dx * (v[:, 1] + dy * v[:, 2])
+    rows = np.stack([lin, model.seg_face_in.astype(np.int64), model.seg_bin_in.astype(np.int64),
+                     model.seg_face_out.astype(np.int64), model.seg_bin_out.astype(np.int64)], axis=1)
+    return float(s - np.unique(rows, axis=0).shape[0]) / float(s)
