@@ -129,6 +129,16 @@ int lvx_voxelize_compact(const uint64_t *raw_key_d, const uint64_t *raw_q_d,
                          uint8_t *seg_face_out_d, uint16_t *seg_bin_out_d,
                          uint64_t *seg_key_d, lvx_seg_record *seg_rec_d, void *stream);
 
+/* Multi-GPU merge (voxelization sharded by line ID): raw records
+ * all-gathered from every rank are scattered into one voxel-grouped array through
+ * the GLOBAL per-voxel cursors (exclusive scan of the summed counts); afterwards
+ * cursor_d[lin] is the end of voxel lin's range, ready for lvx_voxelize_compact.
+ * This stands where the reference's single stable argsort over all chords does
+ * (voxelizer.py:435-438). */
+int lvx_raw_regroup(const uint64_t *in_key_d, const uint64_t *in_q_d, const uint32_t *in_lin_d,
+                    int64_t n_raw, uint32_t *cursor_d, uint64_t *out_key_d, uint64_t *out_q_d,
+                    uint32_t *out_lin_d, void *stream);
+
 /* Generic exclusive scan u16 -> u32 (edge_kept -> edge_base), same scratch rule. */
 int lvx_scan_u16(const uint16_t *in_d, int64_t n, uint32_t *out_d, void *scratch_d,
                  void *stream);
@@ -219,6 +229,16 @@ size_t lvx_render_scratch_bytes(const lvx_camera *cam, const lvx_tiling *tiling)
 int lvx_render(const lvx_camera *cam, const lvx_model *model, const lvx_params *params,
                const lvx_lod *lod, const lvx_tiling *tiling, float *img_d,
                int64_t *row_stats_d, void *scratch_d, void *stream);
+
+/* Measurement aid (bench.py roofline): the same frame, additionally setting bit v of
+ * voxel_bits_d (u32[ceil(V/32)], caller-zeroed) for every voxel whose header the
+ * reference's gather would read (`counts[lin]`, _kernels.py:817-820): the window's
+ * voxel and, in neighbour mode, its 26 in-grid neighbours, for every non-skipped
+ * window up to early termination.  Distinct voxels / their segments give the
+ * unique-bytes-touched figure of SURVEY.md 8(d). */
+int lvx_render_footprint(const lvx_camera *cam, const lvx_model *model, const lvx_params *params,
+                         const lvx_lod *lod, const lvx_tiling *tiling, float *img_d,
+                         int64_t *row_stats_d, uint32_t *voxel_bits_d, void *stream);
 
 /* Scatter compact tiles (any rank's send buffer) into the full image. */
 int lvx_untile(const float *tiles_d, const lvx_tiling *tiling, int32_t width, int32_t height,

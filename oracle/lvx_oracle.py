@@ -318,7 +318,7 @@ def render(camera: dict, model, levels=None, *, tube_radius=0.3, opacity_mode="c
            rows=None):
     """render_frame (raycast.py:468-521): returns (image (H,W,4) f32, stats dict).
 
-    `rows=(y0, y1)` renders only that row band (used for bounded CPU timing)."""
+    `rows=(y0, y1[, step])` renders only rows y0, y0+step, ... < y1 (bounded CPU timing)."""
     cam = camera_args(**camera)
     W, H = cam[6], cam[7]
     rx, ry, rz = model.dims
@@ -332,17 +332,23 @@ def render(camera: dict, model, levels=None, *, tube_radius=0.3, opacity_mode="c
                if ao is not None else np.zeros(1, np.float32))
     if AO_MODES[ao_mode] == 3 and ao is None:
         raise ValueError("precomputed AO requested but the model carries none")
-    occ = occupancy_dilated(model)
+    occ = getattr(model, "_occ_cache", None)
+    if occ is None:
+        occ = occupancy_dilated(model)
+        try:
+            model._occ_cache = occ
+        except AttributeError:
+            pass
     img = np.zeros((H, W, 4), np.float32)
     stats = np.zeros((H, 3), np.int64)
-    y0, y1 = (0, H) if rows is None else rows
+    y0, y1, ystep = (0, H, 1) if rows is None else (tuple(rows) + (1,))[:3]
     bg = _f64(background)
     table = np.ascontiguousarray(model.transfer_table, dtype=np.float32)
     seg_a = np.ascontiguousarray(model.seg_a, dtype=np.float32)
     seg_b = np.ascontiguousarray(model.seg_b, dtype=np.float32)
     rc = lib().lvo_render_rows(
         _p(cam[0]), _p(cam[1]), _p(cam[2]), _p(cam[3]), C.c_double(cam[4]), C.c_double(cam[5]),
-        C.c_int64(W), C.c_int64(H), C.c_int64(y0), C.c_int64(y1), C.c_int64(rx), C.c_int64(ry),
+        C.c_int64(W), C.c_int64(H), C.c_int64(y0), C.c_int64(y1), C.c_int64(max(1, ystep)), C.c_int64(rx), C.c_int64(ry),
         C.c_int64(rz), _p(model.counts), _p(model.offsets), _p(seg_a), _p(seg_b),
         _p(model.seg_attr), _p(model.seg_lid), _p(table), _p(occ), C.c_double(tube_radius),
         C.c_int64(OPACITY_MODES[opacity_mode]), C.c_double(base_opacity), C.c_double(tau),

@@ -41,6 +41,7 @@ struct RenderArgs {
     int tiles_x, n_my_tiles;
     float *img;
     unsigned long long *row_stats;
+    u32 *footprint;  // instrumentation pass only: bitmap of voxels whose header was read
 };
 
 struct HitKey {
@@ -144,6 +145,7 @@ __device__ double stream_hit(PixelState &S, const RenderArgs &A, double ox, doub
     return S.acc[3];
 }
 
+template <bool FOOTPRINT>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 render_kernel(const RenderArgs A) {
     const int lane = threadIdx.x & 31;
@@ -216,6 +218,7 @@ render_kernel(const RenderArgs A) {
                             if (nx_ < 0 || nx_ >= rx) continue;
                             const u32 lin = (u32)(nx_ + rx * (ny_ + ry * nz_));
                             const u32 cnt = A.counts[lin];
+                            if (FOOTPRINT && first_pass) atomicOr(&A.footprint[lin >> 5], 1u << (lin & 31u));
                             if (cnt == 0) continue;
                             const u32 base = A.offsets[lin];
                             for (u32 s = 0; s < cnt; ++s) {
@@ -387,10 +390,9 @@ size_t lvx_render_scratch_bytes(const lvx_camera *, const lvx_tiling *) {
     return 0;
 }
 
-int lvx_render(const lvx_camera *cam, const lvx_model *model, const lvx_params *params,
-               const lvx_lod *lod, const lvx_tiling *tiling, float *img_d, int64_t *row_stats_d,
-               void *scratch_d, void *stream) {
-    (void)scratch_d;
+static int render_impl(const lvx_camera *cam, const lvx_model *model, const lvx_params *params,
+                       const lvx_lod *lod, const lvx_tiling *tiling, float *img_d,
+                       int64_t *row_stats_d, uint32_t *footprint_d, void *stream) {
     LVX_REQUIRE(cam && model && params && img_d && row_stats_d, "null argument");
     LVX_REQUIRE(cam->width >= 1 && cam->height >= 1, "image dims must be >= 1");
     if (int rc = check_tiling(tiling)) return rc;
@@ -437,9 +439,27 @@ int lvx_render(const lvx_camera *cam, const lvx_model *model, const lvx_params *
     if (A.n_my_tiles == 0) return LVX_OK;
     const i64 warps = (i64)A.n_my_tiles * (tiling->tile_w / 8) * (tiling->tile_h / 4);
     const i64 blocks = lvx_ceil_div(warps, kWarpsPerBlock);
-    render_kernel<<<(unsigned)blocks, kWarpsPerBlock * 32, 0, (cudaStream_t)stream>>>(A);
+    A.footprint = footprint_d;
+    if (footprint_d)
+        render_kernel<true><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, (cudaStream_t)stream>>>(A);
+    else
+        render_kernel<false><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, (cudaStream_t)stream>>>(A);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
+}
+
+int lvx_render(const lvx_camera *cam, const lvx_model *model, const lvx_params *params,
+               const lvx_lod *lod, const lvx_tiling *tiling, float *img_d, int64_t *row_stats_d,
+               void *scratch_d, void *stream) {
+    (void)scratch_d;
+    return render_impl(cam, model, params, lod, tiling, img_d, row_stats_d, nullptr, stream);
+}
+
+int lvx_render_footprint(const lvx_camera *cam, const lvx_model *model, const lvx_params *params,
+                         const lvx_lod *lod, const lvx_tiling *tiling, float *img_d,
+                         int64_t *row_stats_d, uint32_t *voxel_bits_d, void *stream) {
+    LVX_REQUIRE(voxel_bits_d, "null footprint bitmap");
+    return render_impl(cam, model, params, lod, tiling, img_d, row_stats_d, voxel_bits_d, stream);
 }
 
 int lvx_untile(const float *tiles_d, const lvx_tiling *tiling, int32_t width, int32_t height,

@@ -538,6 +538,23 @@ seg_records_kernel(const float *__restrict__ seg_a, const float *__restrict__ se
     r[1] = make_float4(seg_b[3 * s], seg_b[3 * s + 1], seg_b[3 * s + 2], 0.0f);
 }
 
+// Multi-GPU merge: raw records gathered from all ranks (each rank's block is grouped
+// by voxel, but the blocks are not interleaved) are scattered into one voxel-grouped
+// array through the global per-voxel cursors.  Order inside a voxel is restored by
+// the key ranking of compact_kernel.
+__global__ void __launch_bounds__(256)
+regroup_kernel(const u64 *__restrict__ in_key, const u64 *__restrict__ in_q,
+               const u32 *__restrict__ in_lin, i64 n, u32 *__restrict__ cursor,
+               u64 *__restrict__ out_key, u64 *__restrict__ out_q, u32 *__restrict__ out_lin) {
+    const i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const u32 lin = in_lin[r];
+    const u32 slot = atomicAdd(&cursor[lin], 1u);
+    out_key[slot] = in_key[r];
+    out_q[slot] = in_q[r];
+    out_lin[slot] = lin;
+}
+
 int ilog2i(int n) {
     int lb = 0;
     while ((1 << (lb + 1)) <= n) ++lb;
@@ -675,6 +692,19 @@ int lvx_voxelize_compact(const uint64_t *raw_key_d, const uint64_t *raw_q_d,
     compact_kernel<<<(unsigned)lvx_ceil_div(n_raw, 256), 256, 0, (cudaStream_t)stream>>>(
         raw_key_d, raw_q_d, raw_lin_d, n_raw, vox_cnt_d, cursor_end_d, offsets_d, dims[0], dims[1],
         n_bins, lb, width, o);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_raw_regroup(const uint64_t *in_key_d, const uint64_t *in_q_d, const uint32_t *in_lin_d,
+                    int64_t n_raw, uint32_t *cursor_d, uint64_t *out_key_d, uint64_t *out_q_d,
+                    uint32_t *out_lin_d, void *stream) {
+    LVX_REQUIRE(n_raw >= 0, "bad arguments");
+    if (n_raw == 0) return LVX_OK;
+    LVX_REQUIRE(in_key_d && in_q_d && in_lin_d && cursor_d && out_key_d && out_q_d && out_lin_d,
+                "null input");
+    regroup_kernel<<<(unsigned)lvx_ceil_div(n_raw, 256), 256, 0, (cudaStream_t)stream>>>(
+        in_key_d, in_q_d, in_lin_d, n_raw, cursor_d, out_key_d, out_q_d, out_lin_d);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }

@@ -372,6 +372,14 @@ class FramePlan:
                                          _lib.ptr(row_stats_d), None, _lib.stream_ptr()))
 
 
+    def launch_footprint(self, img_d, row_stats_d, voxel_bits_d):
+        """Instrumented frame (bench.py): also marks every voxel whose header is read."""
+        _lib.check(_lib.lib().lvx_render_footprint(
+            C.byref(self.cam), C.byref(self.mdl), C.byref(self.par), C.byref(self.lod),
+            C.byref(self.til), _lib.ptr(img_d), _lib.ptr(row_stats_d), _lib.ptr(voxel_bits_d),
+            _lib.stream_ptr()))
+
+
 def render_frame(camera: Camera, model: VoxelModel, octree: Optional[DensityOctree] = None,
                  replines=None, params: Optional[RenderParams] = None, workers: int = 1,
                  moving: bool = False) -> Frame:

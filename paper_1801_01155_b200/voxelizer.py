@@ -285,55 +285,68 @@ class VoxelModel:
 
 # ---------------------------------------------------------------------------------
 
-def voxelize_device(pts_d, attrs_d, off_d, n_curves: int, spec: GridSpec, *, caches: bool = True,
-                    provenance: bool = True, memory_budget: Optional[int] = None):
-    """Run the device pipeline on vertex arrays that already live on the GPU.
+def _scratch(n):
+    import torch
+    nbytes = int(_lib.lib().lvx_scan_scratch_bytes(C.c_int64(max(int(n), 1))))
+    return torch.empty(max(nbytes, 16), dtype=torch.uint8, device="cuda")
 
-    pts_d f64[P,3], attrs_d f64[P], off_d i64[n_curves+1].  Returns a dict of
-    device tensors plus `dropped` and `n_segments`.  This is the kernel-only path
-    bench.py times; `build_voxel_model` wraps it with the host<->device copies."""
+
+def stage_count(pts_d, off_d, n_curves: int, spec: GridSpec):
+    """mark curve starts + pass 1 (chords per voxel).  Returns (first u8[P], vox_cnt u32[V])."""
     torch = _lib.require_device()
-    L = _lib.lib()
-    st = _lib.stream_ptr()
-    n_bins = spec.bins_per_axis
-    dims = _lib.i32x3(spec.dims)
-    V = spec.voxel_count
+    L, st = _lib.lib(), _lib.stream_ptr()
     P = int(pts_d.shape[0])
-    w = record_width(n_bins)
-    dev = "cuda"
-
-    first = torch.empty(max(P, 1), dtype=torch.uint8, device=dev)
+    first = torch.empty(max(P, 1), dtype=torch.uint8, device="cuda")
     _lib.check(L.lvx_mark_curve_starts(_lib.ptr(off_d), C.c_int64(n_curves), C.c_int64(P),
                                        _lib.ptr(first), st))
-    vox_cnt = torch.zeros(V, dtype=torch.int32, device=dev)
-    _lib.check(L.lvx_voxelize_count(_lib.ptr(pts_d), _lib.ptr(first), C.c_int64(P), dims,
-                                    _lib.ptr(vox_cnt), st))
-    cursor = torch.empty(V, dtype=torch.int32, device=dev)
-    offsets = torch.empty(V, dtype=torch.int32, device=dev)  # u32 bit pattern
-    counts = torch.empty(V, dtype=torch.uint8, device=dev)
-    totals = torch.zeros(2, dtype=torch.int64, device=dev)
-    scratch = torch.empty(max(int(L.lvx_scan_scratch_bytes(C.c_int64(max(V, P)))), 16),
-                          dtype=torch.uint8, device=dev)
-    _lib.check(L.lvx_voxel_scan(_lib.ptr(vox_cnt), C.c_int64(V), _lib.ptr(cursor), _lib.ptr(offsets),
-                                _lib.ptr(counts), _lib.ptr(totals), _lib.ptr(scratch), st))
-    n_raw, S = (int(x) for x in totals.cpu().tolist())  # the one sync: sizes the outputs
+    vox_cnt = torch.zeros(spec.voxel_count, dtype=torch.int32, device="cuda")
+    _lib.check(L.lvx_voxelize_count(_lib.ptr(pts_d), _lib.ptr(first), C.c_int64(P),
+                                    _lib.i32x3(spec.dims), _lib.ptr(vox_cnt), st))
+    return first, vox_cnt
+
+
+def stage_scan(vox_cnt):
+    """Prefix sums over the voxel counters.  Returns (cursor, offsets, counts, n_raw, S);
+    reading the two totals is the pipeline's one host synchronisation (it sizes the outputs)."""
+    torch = _lib.require_device()
+    V = int(vox_cnt.shape[0])
+    cursor = torch.empty(V, dtype=torch.int32, device="cuda")
+    offsets = torch.empty(V, dtype=torch.int32, device="cuda")  # u32 bit pattern
+    counts = torch.empty(V, dtype=torch.uint8, device="cuda")
+    totals = torch.zeros(2, dtype=torch.int64, device="cuda")
+    _lib.check(_lib.lib().lvx_voxel_scan(_lib.ptr(vox_cnt), C.c_int64(V), _lib.ptr(cursor),
+                                         _lib.ptr(offsets), _lib.ptr(counts), _lib.ptr(totals),
+                                         _lib.ptr(_scratch(V)), _lib.stream_ptr()))
+    n_raw, S = (int(x) for x in totals.cpu().tolist())
     if n_raw >= 2 ** 32:
         raise MemoryError(f"{n_raw} chords exceed the 32-bit offsets of the voxel headers")
-    total_bytes = 5 * V + w * S
-    if memory_budget is not None and total_bytes > memory_budget:
-        raise MemoryError(f"model needs {total_bytes} bytes (5*{V} + {w}*{S}), "
-                          f"budget is {memory_budget}")
+    return cursor, offsets, counts, n_raw, S
 
-    raw_key = torch.empty(max(n_raw, 1), dtype=torch.int64, device=dev)
-    raw_q = torch.empty(max(n_raw, 1), dtype=torch.int64, device=dev)
-    raw_lin = torch.empty(max(n_raw, 1), dtype=torch.int32, device=dev)
-    edge_kept = torch.empty(max(P, 1), dtype=torch.int16, device=dev) if provenance else None
-    err = torch.zeros(1, dtype=torch.int32, device=dev)
-    _lib.check(L.lvx_voxelize_emit(_lib.ptr(pts_d), _lib.ptr(attrs_d), _lib.ptr(first), C.c_int64(P),
-                                   dims, C.c_int32(n_bins), _lib.ptr(cursor), _lib.ptr(raw_key),
-                                   _lib.ptr(raw_q), _lib.ptr(raw_lin), _lib.ptr(edge_kept),
-                                   _lib.ptr(err), st))
+
+def stage_emit(pts_d, attrs_d, first, spec: GridSpec, cursor, n_raw: int, want_edge_kept: bool):
+    """Pass 2: clip again and scatter raw records through the cursors (which end up
+    pointing at the END of every voxel's range)."""
+    torch = _lib.require_device()
+    P = int(pts_d.shape[0])
+    raw_key = torch.empty(max(n_raw, 1), dtype=torch.int64, device="cuda")
+    raw_q = torch.empty(max(n_raw, 1), dtype=torch.int64, device="cuda")
+    raw_lin = torch.empty(max(n_raw, 1), dtype=torch.int32, device="cuda")
+    edge_kept = torch.empty(max(P, 1), dtype=torch.int16, device="cuda") if want_edge_kept else None
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.check(_lib.lib().lvx_voxelize_emit(
+        _lib.ptr(pts_d), _lib.ptr(attrs_d), _lib.ptr(first), C.c_int64(P), _lib.i32x3(spec.dims),
+        C.c_int32(spec.bins_per_axis), _lib.ptr(cursor), _lib.ptr(raw_key), _lib.ptr(raw_q),
+        _lib.ptr(raw_lin), _lib.ptr(edge_kept), _lib.ptr(err), _lib.stream_ptr()))
+    return raw_key, raw_q, raw_lin, edge_kept, err
+
+
+def stage_compact(raw_key, raw_q, raw_lin, n_raw: int, vox_cnt, cursor_end, offsets, counts,
+                  spec: GridSpec, S: int, caches: bool, want_keys: bool):
+    """Pass 3: per-voxel ordering by key, 255 cap, lid, decode, pack."""
+    torch = _lib.require_device()
+    w = record_width(spec.bins_per_axis)
     m = max(S, 1)
+    dev = "cuda"
     out = {
         "counts": counts, "offsets": offsets,
         "packed": torch.empty(m * w, dtype=torch.uint8, device=dev),
@@ -350,35 +363,94 @@ def voxelize_device(pts_d, attrs_d, off_d, n_curves: int, spec: GridSpec, *, cac
             seg_bin_in=torch.empty(m, dtype=torch.int16, device=dev),
             seg_face_out=torch.empty(m, dtype=torch.uint8, device=dev),
             seg_bin_out=torch.empty(m, dtype=torch.int16, device=dev))
-    seg_key = torch.empty(m, dtype=torch.int64, device=dev) if provenance else None
+    if want_keys:
+        out["seg_key"] = torch.empty(m, dtype=torch.int64, device=dev)
     g = out.get
-    _lib.check(L.lvx_voxelize_compact(
+    _lib.check(_lib.lib().lvx_voxelize_compact(
         _lib.ptr(raw_key), _lib.ptr(raw_q), _lib.ptr(raw_lin), C.c_int64(n_raw), _lib.ptr(vox_cnt),
-        _lib.ptr(cursor), _lib.ptr(offsets), dims, C.c_int32(n_bins), _lib.ptr(out["packed"]),
-        _lib.ptr(g("seg_a")), _lib.ptr(g("seg_b")), _lib.ptr(g("seg_attr")), _lib.ptr(g("seg_lid")),
-        _lib.ptr(g("seg_voxel")), _lib.ptr(g("seg_face_in")), _lib.ptr(g("seg_bin_in")),
-        _lib.ptr(g("seg_face_out")), _lib.ptr(g("seg_bin_out")), _lib.ptr(seg_key),
-        _lib.ptr(out["seg_rec"]), st))
+        _lib.ptr(cursor_end), _lib.ptr(offsets), _lib.i32x3(spec.dims), C.c_int32(spec.bins_per_axis),
+        _lib.ptr(out["packed"]), _lib.ptr(g("seg_a")), _lib.ptr(g("seg_b")), _lib.ptr(g("seg_attr")),
+        _lib.ptr(g("seg_lid")), _lib.ptr(g("seg_voxel")), _lib.ptr(g("seg_face_in")),
+        _lib.ptr(g("seg_bin_in")), _lib.ptr(g("seg_face_out")), _lib.ptr(g("seg_bin_out")),
+        _lib.ptr(g("seg_key")), _lib.ptr(out["seg_rec"]), _lib.stream_ptr()))
+    for k in list(out):  # trim the >=1 padding of empty models
+        if k not in ("counts", "offsets"):
+            out[k] = out[k][:S * w] if k == "packed" else out[k][:S]
+    return out
+
+
+def stage_provenance(seg_key, S: int, edge_kept, off_d, n_curves: int):
+    """seg_curve / seg_order (voxelizer.py:254-262, 486-487) from the provenance keys."""
+    torch = _lib.require_device()
+    seg_curve = torch.empty(S, dtype=torch.int32, device="cuda")
+    seg_order = torch.empty(S, dtype=torch.int32, device="cuda")
+    if S:
+        P = int(edge_kept.shape[0])
+        edge_base = torch.empty(P, dtype=torch.int32, device="cuda")
+        L, st = _lib.lib(), _lib.stream_ptr()
+        _lib.check(L.lvx_scan_u16(_lib.ptr(edge_kept), C.c_int64(P), _lib.ptr(edge_base),
+                                  _lib.ptr(_scratch(P)), st))
+        _lib.check(L.lvx_provenance(_lib.ptr(seg_key), C.c_int64(S), _lib.ptr(edge_base),
+                                    _lib.ptr(off_d), C.c_int64(n_curves), _lib.ptr(seg_curve),
+                                    _lib.ptr(seg_order), st))
+    return seg_curve, seg_order
+
+
+def check_budget(spec: GridSpec, S: int, memory_budget: Optional[int]):
+    w = record_width(spec.bins_per_axis)
+    V = spec.voxel_count
+    total_bytes = 5 * V + w * S
+    if memory_budget is not None and total_bytes > memory_budget:
+        raise MemoryError(f"model needs {total_bytes} bytes (5*{V} + {w}*{S}), "
+                          f"budget is {memory_budget}")
+
+
+def voxelize_device(pts_d, attrs_d, off_d, n_curves: int, spec: GridSpec, *, caches: bool = True,
+                    provenance: bool = True, memory_budget: Optional[int] = None):
+    """Run the device pipeline on vertex arrays that already live on the GPU.
+
+    pts_d f64[P,3], attrs_d f64[P], off_d i64[n_curves+1].  Returns a dict of
+    device tensors plus `dropped` and `n_segments`.  This is the kernel-only path
+    bench.py times; `build_voxel_model` wraps it with the host<->device copies."""
+    first, vox_cnt = stage_count(pts_d, off_d, n_curves, spec)
+    cursor, offsets, counts, n_raw, S = stage_scan(vox_cnt)
+    check_budget(spec, S, memory_budget)
+    raw_key, raw_q, raw_lin, edge_kept, err = stage_emit(pts_d, attrs_d, first, spec, cursor, n_raw,
+                                                         provenance)
+    out = stage_compact(raw_key, raw_q, raw_lin, n_raw, vox_cnt, cursor, offsets, counts, spec, S,
+                        caches, provenance)
     if provenance:
-        seg_curve = torch.empty(m, dtype=torch.int32, device=dev)
-        seg_order = torch.empty(m, dtype=torch.int32, device=dev)
-        if S:
-            edge_base = torch.empty(P, dtype=torch.int32, device=dev)
-            _lib.check(L.lvx_scan_u16(_lib.ptr(edge_kept), C.c_int64(P), _lib.ptr(edge_base),
-                                      _lib.ptr(scratch), st))
-            _lib.check(L.lvx_provenance(_lib.ptr(seg_key), C.c_int64(S), _lib.ptr(edge_base),
-                                        _lib.ptr(off_d), C.c_int64(n_curves), _lib.ptr(seg_curve),
-                                        _lib.ptr(seg_order), st))
-        out["seg_curve"], out["seg_order"] = seg_curve, seg_order
-    # trim the >=1 padding of empty models
-    for k in list(out):
-        if k in ("counts", "offsets"):
-            continue
-        out[k] = out[k][:S * w] if k == "packed" else out[k][:S]
+        out["seg_curve"], out["seg_order"] = stage_provenance(out.pop("seg_key"), S, edge_kept,
+                                                              off_d, n_curves)
     out["n_segments"] = S
     out["dropped"] = n_raw - S
     out["err"] = err
     return out
+
+
+def model_from_device(out: dict, spec: GridSpec, transfer_table) -> "VoxelModel":
+    if int(out["err"].item()) != 0:
+        # voxelizer.py:366-368
+        raise AssertionError("chord endpoint off every face")
+    g = out.get
+    model = VoxelModel(
+        spec=spec, counts=out["counts"], offsets=out["offsets"], packed=out["packed"],
+        transfer_table=transfer_table, seg_voxel=g("seg_voxel"), seg_a=g("seg_a"),
+        seg_b=g("seg_b"), seg_attr=g("seg_attr"), seg_lid=g("seg_lid"),
+        seg_face_in=g("seg_face_in"), seg_bin_in=g("seg_bin_in"),
+        seg_face_out=g("seg_face_out"), seg_bin_out=g("seg_bin_out"),
+        dropped_overflow=out["dropped"], seg_curve=g("seg_curve"), seg_order=g("seg_order"))
+    model._derived["seg_rec"] = out["seg_rec"]
+    return model
+
+
+def _check_table(transfer_table):
+    if transfer_table is None:
+        transfer_table = default_transfer_table()
+    transfer_table = np.asarray(transfer_table, dtype=np.float32)
+    if transfer_table.shape != (256, 4):
+        raise ValueError(f"transfer table must be (256,4), got {transfer_table.shape}")
+    return transfer_table
 
 
 def build_voxel_model(curves: CurveSet, spec: GridSpec, transfer_table=None, workers: int = 1,
@@ -389,11 +461,7 @@ def build_voxel_model(curves: CurveSet, spec: GridSpec, transfer_table=None, wor
     does not depend on it (voxelizer.py:401-403) and the device pipeline has no
     use for it.  Voxels crossed by more than 255 chords keep the first 255 in
     curve order; the rest are counted in `dropped_overflow`."""
-    if transfer_table is None:
-        transfer_table = default_transfer_table()
-    transfer_table = np.asarray(transfer_table, dtype=np.float32)
-    if transfer_table.shape != (256, 4):
-        raise ValueError(f"transfer table must be (256,4), got {transfer_table.shape}")
+    transfer_table = _check_table(transfer_table)
     _lib.require_device()
     pts, attrs, off = curves.flat()
     pts_d = _lib.to_device(pts, np.float64)
@@ -401,18 +469,7 @@ def build_voxel_model(curves: CurveSet, spec: GridSpec, transfer_table=None, wor
     off_d = _lib.to_device(off, np.int64)
     out = voxelize_device(pts_d, attrs_d, off_d, int(off.size - 1), spec,
                           memory_budget=memory_budget)
-    if int(out["err"].item()) != 0:
-        # voxelizer.py:366-368
-        raise AssertionError("chord endpoint off every face")
-    model = VoxelModel(
-        spec=spec, counts=out["counts"], offsets=out["offsets"], packed=out["packed"],
-        transfer_table=transfer_table, seg_voxel=out["seg_voxel"], seg_a=out["seg_a"],
-        seg_b=out["seg_b"], seg_attr=out["seg_attr"], seg_lid=out["seg_lid"],
-        seg_face_in=out["seg_face_in"], seg_bin_in=out["seg_bin_in"],
-        seg_face_out=out["seg_face_out"], seg_bin_out=out["seg_bin_out"],
-        dropped_overflow=out["dropped"], seg_curve=out["seg_curve"], seg_order=out["seg_order"])
-    model._derived["seg_rec"] = out["seg_rec"]
-    return model
+    return model_from_device(out, spec, transfer_table)
 
 
 def count_duplicates(model: VoxelModel) -> float:

@@ -1,0 +1,361 @@
+"""CUDA path vs the CPU oracle on seeded inputs the oracle finishes in seconds,
+edge cases, error behaviour, and size-independent properties at the full
+BASELINE.json sizes."""
+import numpy as np
+import pytest
+
+from conftest import MODEL_FIELDS, assert_model_equal
+
+pytestmark = pytest.mark.gpu
+
+MAX_ERR = 1.0 / 255.0
+MEAN_ERR = 1e-3
+
+
+@pytest.fixture(scope="module")
+def lv():
+    import paper_1801_01155_b200 as lv
+    return lv
+
+
+@pytest.fixture(scope="module")
+def synth():
+    from paper_1801_01155_b200 import synth
+    return synth
+
+
+def both(lv, oracle, gen, dims, n_bins=32, table=None):
+    pts, attrs, off = gen
+    m = lv.build_voxel_model(lv.CurveSet.from_flat(pts, attrs, off), lv.GridSpec(dims, n_bins), table)
+    ref = oracle.build_voxel_model(pts, attrs, off, dims, n_bins, table)
+    return m, ref
+
+
+def as_dict(ref):
+    return {f: getattr(ref, f) for f in MODEL_FIELDS}
+
+
+# --- configs[0]: 1k helices x 100 pts, 64^3, 256x256 opaque -------------------------
+
+@pytest.fixture(scope="module")
+def c1(lv, oracle, synth):
+    dims = (64, 64, 64)
+    m, ref = both(lv, oracle, synth.helices(1000, 100, dims), dims)
+    return dims, m, ref
+
+
+def test_c1_voxel_model(c1):
+    dims, m, ref = c1
+    assert ref.segment_count == 263432  # SURVEY.md 8c golden count
+    assert_model_equal(m, as_dict(ref))
+
+
+def test_c1_golden_hash(c1):
+    import hashlib
+    _, m, _ = c1
+    # sha256 prefix of `packed` observed on the unmodified reference
+    assert hashlib.sha256(m.packed.tobytes()).hexdigest()[:16] == "3587d4ece308025c"
+
+
+def test_c1_lod_and_ao(lv, oracle, c1):
+    dims, m, ref = c1
+    oc = lv.build_lod(m)
+    levels = oracle.build_octree(oracle.compute_density_level0(ref))
+    assert oc.n_levels == len(levels) == 7
+    for a, b in zip(oc.levels, levels):
+        assert np.array_equal(a, b)
+    ao = lv.precompute_voxel_ao(m, oc)
+    assert np.array_equal(ao.values, oracle.precompute_voxel_ao(ref, levels, 100, 5.0, 1.0))
+
+
+@pytest.mark.parametrize("kw", [
+    dict(neighbor_mode="on"),
+    dict(neighbor_mode="off"),
+    dict(neighbor_mode="on", base_opacity=0.25),
+    dict(neighbor_mode="off", base_opacity=0.25, joint_spheres=False),
+    dict(neighbor_mode="on", base_opacity=0.25, ao_mode="precomputed", shadow_mode="cone",
+         light_dir=(0.3, 0.2, 1.0)),
+    dict(neighbor_mode="off", base_opacity=0.25, ao_mode="density-rays"),
+    dict(neighbor_mode="on", base_opacity=0.05, tau=1.0),
+], ids=lambda kw: "-".join(f"{k}={v}" for k, v in kw.items() if k != "light_dir"))
+def test_c1_frames(lv, oracle, c1, kw):
+    dims, m, ref = c1
+    oc = lv.build_lod(m)
+    levels = oracle.build_octree(oracle.compute_density_level0(ref))
+    if kw.get("ao_mode") == "precomputed":
+        m.ao = lv.precompute_voxel_ao(m, oc)
+        ref.ao = oracle.precompute_voxel_ao(ref, levels, 100, 5.0, 1.0)
+    fr = lv.render_frame(lv.default_camera(dims, 256, 256), m, oc, None, lv.RenderParams(**kw))
+    okw = dict(kw)
+    nb = okw.pop("neighbor_mode") == "on"
+    img, st = oracle.render(oracle.default_camera(dims, 256, 256), ref, levels, neighbor=nb, **okw)
+    err = np.abs(fr.image.astype(np.float64) - img.astype(np.float64))
+    assert err.max() <= MAX_ERR and err.mean() < MEAN_ERR
+    for k in ("rays", "voxel_steps", "intersection_tests", "window_overflow", "neighbor"):
+        assert fr.stats[k] == st[k], k
+    if kw == dict(neighbor_mode="on"):
+        # counters of the reference's own run of this config
+        assert fr.stats["voxel_steps"] == 2430102 and fr.stats["intersection_tests"] == 9073278
+
+
+# --- other seeded sets vs the oracle --------------------------------------------------
+
+@pytest.mark.parametrize("case", ["turbulence", "wiggles", "lattice", "cap"])
+def test_voxelize_matches_oracle(lv, oracle, synth, case):
+    if case == "turbulence":
+        dims, gen = (64, 64, 64), synth.turbulence(3000, 100, (64, 64, 64))
+    elif case == "wiggles":
+        dims, gen = (24, 20, 16), synth.wiggles(400, 60, (24, 20, 16))
+    elif case == "lattice":
+        dims, gen = (12, 10, 8), synth.lattice_adversarial(4000, 12, (12, 10, 8))
+    else:
+        dims, gen = (3, 3, 3), synth.helices(900, 30, (3, 3, 3), seed=3)
+    m, ref = both(lv, oracle, gen, dims)
+    assert_model_equal(m, as_dict(ref))
+    assert m.dropped_overflow == ref.dropped_overflow
+    if case == "cap":
+        assert m.dropped_overflow > 0 and m.counts.max() == 255
+
+
+@pytest.mark.parametrize("n_bins", [2, 4, 16, 64, 256])
+def test_bin_resolutions(lv, oracle, synth, n_bins):
+    dims = (16, 12, 10)
+    m, ref = both(lv, oracle, synth.turbulence(300, 40, dims), dims, n_bins)
+    assert_model_equal(m, as_dict(ref))
+    assert m.packed.size == lv.record_width(n_bins) * m.segment_count
+
+
+def test_ragged_and_degenerate_inputs(lv, oracle):
+    dims = (5, 4, 3)
+    curves = [
+        np.array([[0.5, 0.5, 0.5], [4.5, 3.5, 2.5]]),                       # 2 vertices, long diagonal
+        np.array([[1.2, 1.2, 1.2], [1.3, 1.4, 1.5], [1.6, 1.1, 1.9]]),      # never leaves its voxel
+        np.array([[-3.0, 1.5, 1.5], [9.0, 1.5, 1.5]]),                      # passes through from outside
+        np.array([[2.0, 2.0, 1.0], [2.0, 2.0, 1.0], [3.0, 3.0, 2.0]]),      # repeated vertex, lattice points
+        np.array([[0.5, 0.5, 0.5], [1.0, 0.5, 0.5], [0.5, 0.5, 0.5]]),      # reversal exactly on a plane
+        np.array([[-1.0, -1.0, -1.0], [-2.0, -0.5, -0.2]]),                 # entirely outside
+        np.array([[0.5, 3.999999999, 0.5], [4.9, 0.0000001, 2.99999]]),
+    ]
+    pts = np.concatenate(curves)
+    off = np.concatenate([[0], np.cumsum([len(c) for c in curves])]).astype(np.int64)
+    attrs = np.linspace(0.0, 1.0, len(pts))
+    m, ref = both(lv, oracle, (pts, attrs, off), dims, 8)
+    assert_model_equal(m, as_dict(ref))
+
+
+def test_empty_model(lv, oracle):
+    dims = (4, 4, 4)
+    pts = np.array([[1.1, 1.1, 1.1], [1.2, 1.3, 1.4]])
+    m, ref = both(lv, oracle, (pts, np.array([0.0, 1.0]), np.array([0, 2], dtype=np.int64)), dims)
+    assert m.segment_count == 0 and ref.segment_count == 0
+    assert m.packed.size == 0 and m.seg_a.shape == (0, 3) and not m.counts.any()
+    l0 = lv.compute_density_level0(m)
+    assert l0.shape == (4, 4, 4) and not l0.any()
+    oc = lv.build_octree(l0)
+    assert oc.n_levels == 3
+    bg = (0.1, 0.2, 0.3, 1.0)
+    fr = lv.render_frame(lv.default_camera(dims, 33, 17), m, None, None, lv.RenderParams(background=bg))
+    # reference tests/test_raycast.py:402-408: an empty model renders the background
+    assert np.allclose(fr.image, np.asarray(bg, np.float32)[None, None, :])
+    assert fr.stats["intersection_tests"] == 0 and fr.stats["voxel_steps"] > 0
+
+
+def test_odd_image_sizes_and_determinism(lv, oracle, synth):
+    dims = (10, 9, 7)
+    m, ref = both(lv, oracle, synth.wiggles(120, 30, dims), dims)
+    levels = oracle.build_octree(oracle.compute_density_level0(ref))
+    for (W, H) in ((1, 1), (7, 5), (37, 21), (130, 3)):
+        cam = lv.default_camera(dims, W, H)
+        fr = lv.render_frame(cam, m, None, None, lv.RenderParams(base_opacity=0.5, neighbor_mode="on"))
+        fr2 = lv.render_frame(cam, m, None, None, lv.RenderParams(base_opacity=0.5, neighbor_mode="on"),
+                              workers=8)
+        img, st = oracle.render(oracle.default_camera(dims, W, H), ref, levels, base_opacity=0.5)
+        assert np.array_equal(fr.image, fr2.image) and fr.stats["intersection_tests"] == fr2.stats["intersection_tests"]
+        assert np.abs(fr.image - img).max() <= MAX_ERR
+        assert fr.stats["voxel_steps"] == st["voxel_steps"]
+        assert fr.stats["intersection_tests"] == st["intersection_tests"]
+
+
+def test_camera_inside_grid_and_auto_neighbor(lv, oracle, synth):
+    dims = (12, 12, 12)
+    m, ref = both(lv, oracle, synth.turbulence(200, 60, dims), dims)
+    levels = oracle.build_octree(oracle.compute_density_level0(ref))
+    cam = lv.Camera(position=(6.2, 5.7, 6.1), target=(11.0, 9.0, 7.0), fov=70.0, width=64, height=40)
+    ocam = dict(position=(6.2, 5.7, 6.1), target=(11.0, 9.0, 7.0), up=(0.0, 0.0, 1.0), fov=70.0, width=64, height=40)
+    p = lv.RenderParams(base_opacity=0.3)
+    still = lv.render_frame(cam, m, None, None, p, moving=False)
+    moving = lv.render_frame(cam, m, None, None, p, moving=True)
+    assert still.stats["neighbor"] is True and moving.stats["neighbor"] is False  # tests/test_raycast.py:450-458
+    for fr, nb in ((still, True), (moving, False)):
+        img, st = oracle.render(ocam, ref, levels, base_opacity=0.3, neighbor=nb)
+        assert np.abs(fr.image - img).max() <= MAX_ERR
+        assert fr.stats["intersection_tests"] == st["intersection_tests"]
+
+
+def test_model_from_host_arrays_renders_identically(lv, synth):
+    """A model rebuilt from plain numpy arrays (e.g. decoded from a .vxl file,
+    reference tests/test_model_io.py:105-116) renders bit-identically."""
+    dims = (16, 16, 16)
+    m = lv.build_voxel_model(lv.CurveSet.from_flat(*synth.helices(50, 40, dims)), lv.GridSpec(dims))
+    host = lv.VoxelModel(spec=m.spec, counts=m.counts.copy(), offsets=m.offsets.copy(), packed=m.packed.copy(),
+                         transfer_table=m.transfer_table, seg_voxel=m.seg_voxel.copy(), seg_a=m.seg_a.copy(),
+                         seg_b=m.seg_b.copy(), seg_attr=m.seg_attr.copy(), seg_lid=m.seg_lid.copy(),
+                         seg_face_in=m.seg_face_in.copy(), seg_bin_in=m.seg_bin_in.copy(),
+                         seg_face_out=m.seg_face_out.copy(), seg_bin_out=m.seg_bin_out.copy())
+    cam = lv.default_camera(dims, 80, 60)
+    p = lv.RenderParams(base_opacity=0.4, neighbor_mode="on")
+    a, b = lv.render_frame(cam, m, None, None, p), lv.render_frame(cam, host, None, None, p)
+    assert np.array_equal(a.image, b.image) and a.stats["intersection_tests"] == b.stats["intersection_tests"]
+    assert np.array_equal(lv.compute_density_level0(m), lv.compute_density_level0(host))
+    # replacing a cache array through the attribute drops the stale device mirror
+    host.seg_attr = np.zeros_like(host.seg_attr)
+    c = lv.render_frame(cam, host, None, None, p)
+    assert not np.array_equal(c.image, b.image)
+
+
+# --- error behaviour ------------------------------------------------------
+
+def test_error_conventions(lv, synth):
+    dims = (8, 8, 8)
+    cs = lv.CurveSet.from_flat(*synth.helices(20, 30, dims))
+    with pytest.raises(ValueError, match="transfer table"):
+        lv.build_voxel_model(cs, lv.GridSpec(dims), np.zeros((10, 4), np.float32))
+    with pytest.raises(MemoryError, match=r"5\*512"):
+        lv.build_voxel_model(cs, lv.GridSpec(dims), memory_budget=1000)
+    m = lv.build_voxel_model(cs, lv.GridSpec(dims))
+    cam = lv.default_camera(dims, 16, 16)
+    with pytest.raises(ValueError, match="octree"):
+        lv.render_frame(cam, m, None, None, lv.RenderParams(shadow_mode="cone", light_dir=(0, 0, 1)))
+    with pytest.raises(ValueError, match="octree"):
+        lv.render_frame(cam, m, None, None, lv.RenderParams(ao_mode="density-rays"))
+    with pytest.raises(ValueError, match="precomputed AO"):
+        lv.render_frame(cam, m, None, None, lv.RenderParams(ao_mode="precomputed"))
+    with pytest.raises(NotImplementedError):
+        lv.render_frame(cam, m, None, None, lv.RenderParams(shadow_mode="hard", light_dir=(0, 0, 1)))
+    with pytest.raises(ValueError):
+        lv.build_octree(np.zeros((0, 2, 2), np.float32))
+
+
+# --- size-independent properties at the full BASELINE.json sizes ---------------------------
+
+def check_model_properties(lv, m):
+    counts, offsets = m.counts.astype(np.int64), m.offsets.astype(np.int64)
+    S = m.segment_count
+    assert counts.sum() == S
+    # headers are the exclusive prefix sums in scan order (tests/test_voxelizer.py:324-333)
+    assert offsets[0] == 0 and np.array_equal(offsets[1:], np.cumsum(counts)[:-1])
+    dx, dy, _ = m.spec.dims
+    v = m.seg_voxel.astype(np.int64)
+    lin = v[:, 0] + dx * (v[:, 1] + dy * v[:, 2])
+    assert np.all(np.diff(lin) >= 0)  # grouped by voxel in scan order
+    assert np.array_equal(np.bincount(lin, minlength=counts.size), counts)
+    # unpack(packed) == the cached arrays (tests/test_voxelizer.py:336-351)
+    u = lv.unpack_records(m.packed, m.spec.bins_per_axis)
+    assert np.array_equal(u["face_in"], m.seg_face_in) and np.array_equal(u["bin_in"], m.seg_bin_in)
+    assert np.array_equal(u["face_out"], m.seg_face_out) and np.array_equal(u["bin_out"], m.seg_bin_out)
+    assert np.array_equal(u["attr"], m.seg_attr) and np.array_equal(u["lid"], m.seg_lid)
+    # lid = rank inside the voxel mod 32 (voxelizer.py:442-449)
+    rank = np.arange(S) - offsets[lin]
+    assert np.array_equal(m.seg_lid, (rank % 32).astype(np.uint8))
+    # endpoints sit on a face of their own voxel, at bin centres (tests/test_voxelizer.py:354-361)
+    for pts, face in ((m.seg_a, m.seg_face_in), (m.seg_b, m.seg_face_out)):
+        local = pts.astype(np.float64) - v
+        assert local.min() >= 0.0 and local.max() <= 1.0
+        ax = (face >> 1).astype(np.int64)
+        assert np.array_equal(local[np.arange(S), ax], (face & 1).astype(np.float64))
+    # (curve, chord order) increases inside every voxel: the stable-sort order
+    key = m.seg_curve.astype(np.int64) * (1 << 32) + m.seg_order
+    same = lin[1:] == lin[:-1]
+    assert np.all(key[1:][same] > key[:-1][same])
+
+
+def test_c2_properties_and_golden_hash(lv, synth):
+    """configs[1]: 10k helices x 100 pts, 128^3.  Too slow for the oracle inside a unit
+    test at 1080p, so: structural properties, the reference's golden hash and
+    counters, run-to-run determinism."""
+    import hashlib
+    dims = (128, 128, 128)
+    cs = lv.CurveSet.from_flat(*synth.helices(10000, 100, dims))
+    m = lv.build_voxel_model(cs, lv.GridSpec(dims))
+    assert m.segment_count == 5355984
+    assert hashlib.sha256(m.packed.tobytes()).hexdigest()[:16] == "7e7d82534e9a9d10"
+    check_model_properties(lv, m)
+    m2 = lv.build_voxel_model(cs, lv.GridSpec(dims), workers=8)
+    assert np.array_equal(m.packed, m2.packed) and np.array_equal(m.seg_order, m2.seg_order)
+    oc = lv.build_lod(m)
+    # mass conservation: the mean is preserved level to level on power-of-two grids
+    tot = [float(l.astype(np.float64).mean()) for l in oc.levels]
+    assert np.allclose(tot, tot[0], rtol=1e-5)
+    cam = lv.default_camera(dims, 1920, 1080)
+    p = lv.RenderParams(base_opacity=0.25, neighbor_mode="on")
+    fr = lv.render_frame(cam, m, None, None, p)
+    # counters of the unmodified reference on this exact frame
+    assert fr.stats["voxel_steps"] == 82325274 and fr.stats["intersection_tests"] == 884660172
+    fr2 = lv.render_frame(cam, m, None, None, p)
+    assert np.array_equal(fr.image, fr2.image)
+    a = fr.image[..., 3]
+    assert a.min() >= 0.0 and a.max() <= 1.0 + 1e-6 and np.isfinite(fr.image).all()
+
+
+def test_c3_turbulence_golden_hash(lv, synth):
+    """configs[2] voxelisation: 100k turbulence lines, 256^3 (hashes from SURVEY.md 8c)."""
+    import hashlib
+    dims = (256, 256, 256)
+    m = lv.build_voxel_model(lv.CurveSet.from_flat(*synth.turbulence(100000, 100, dims)), lv.GridSpec(dims))
+    assert m.segment_count == 9683143 and m.dropped_overflow == 0
+    assert hashlib.sha256(m.packed.tobytes()).hexdigest()[:16] == "bf0cebfed11c4875"
+    assert hashlib.sha256(m.counts.tobytes()).hexdigest()[:16] == "1f3e2873ac51a76a"
+    check_model_properties(lv, m)
+
+
+def test_untile_round_trip(lv, synth):
+    """Interleaved-tile rendering (the multi-GPU screen partition) reassembles to
+    the single-pass frame bit for bit, counters included."""
+    import torch
+    from paper_1801_01155_b200 import parallel
+    dims = (16, 16, 16)
+    m = lv.build_voxel_model(lv.CurveSet.from_flat(*synth.helices(60, 40, dims)), lv.GridSpec(dims))
+    cam = lv.default_camera(dims, 150, 70)  # not a multiple of the tile size
+    p = lv.RenderParams(base_opacity=0.3, neighbor_mode="on")
+    full = lv.render_frame(cam, m, None, None, p)
+    for world in (2, 3, 8):
+        img = torch.zeros((70, 150, 4), dtype=torch.float32, device="cuda")
+        stats = torch.zeros((70, 3), dtype=torch.int64, device="cuda")
+        for rank in range(world):
+            tiles, st = parallel.render_my_tiles(cam, m, None, p, rank, world)
+            parallel.untile_into(tiles, rank, world, cam.width, cam.height, img)
+            stats += st
+        assert np.array_equal(img.cpu().numpy(), full.image), world
+        tot = stats.sum(0).tolist()
+        assert tot[0] == full.stats["voxel_steps"] and tot[1] == full.stats["intersection_tests"]
+
+
+def test_sharded_voxelization_merges_to_single_gpu_result(lv, synth):
+    """Voxelization sharded by line ID (the multi-GPU path, here with the ranks run one
+    after another on one GPU): shard -> sum counts -> concatenate records -> merge gives
+    the single-pass model byte for byte, cap-255 voxels included."""
+    import torch
+    from paper_1801_01155_b200 import _lib, parallel
+    for dims, gen, world in (((24, 20, 16), synth.wiggles(500, 40, (24, 20, 16)), 3),
+                             ((3, 3, 3), synth.helices(900, 30, (3, 3, 3), seed=3), 4)):
+        pts, attrs, off = gen
+        spec = lv.GridSpec(dims)
+        single = lv.build_voxel_model(lv.CurveSet.from_flat(pts, attrs, off), spec)
+        n_curves = off.size - 1
+        shards = []
+        for r in range(world):
+            c0, c1 = parallel.shard_range(n_curves, r, world)
+            p0, p1 = int(off[c0]), int(off[c1])
+            sh = parallel.voxelize_shard(_lib.to_device(pts[p0:p1]), _lib.to_device(attrs[p0:p1]),
+                                         _lib.to_device(off[c0:c1 + 1] - p0), c1 - c0, spec, p0)
+            sh["edge_kept"] = sh["edge_kept"][:p1 - p0]
+            shards.append(sh)
+        total = sum(s["vox_cnt"] for s in shards)
+        cat = {k: torch.cat([s[k] for s in shards]) for k in ("raw_key", "raw_q", "raw_lin", "edge_kept")}
+        out = parallel.merge_shards(spec, total, cat["raw_key"], cat["raw_q"], cat["raw_lin"],
+                                    edge_kept=cat["edge_kept"], off_d=_lib.to_device(off), n_curves=n_curves)
+        out["err"] = shards[0]["err"]
+        from paper_1801_01155_b200.voxelizer import model_from_device
+        merged = model_from_device(out, spec, single.transfer_table)
+        assert_model_equal(merged, {f: getattr(single, f) for f in MODEL_FIELDS})
+        assert merged.dropped_overflow == single.dropped_overflow
