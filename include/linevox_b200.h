@@ -116,7 +116,7 @@ typedef struct {
     float ax, ay, az;
     uint32_t meta; /* attr | lid << 8 */
     float bx, by, bz;
-    uint32_t pad;
+    float half_len; /* >= |b-a|/2 (rounded up): radius of the segment's bounding sphere */
 } lvx_seg_record;
 
 int lvx_voxelize_compact(const uint64_t *raw_key_d, const uint64_t *raw_q_d,
@@ -173,6 +173,15 @@ int lvx_build_octree(float *flat_d, const int32_t dims[3], void *stream);
 int lvx_occupancy_dilate(const uint8_t *counts_d, const int32_t dims[3], uint8_t *occ_d,
                          void *stream);
 
+/* nsum_d u16[(rz+2)(ry+2)(rx+2)]: per cell of the grid padded by one voxel, the sum
+ * of counts over the cell's in-grid 27-neighbourhood.  nsum > 0 is the dilated
+ * occupancy of _occupancy_dilated (raycast.py:351-366); the value is the number of
+ * candidate segments the reference's neighbour gather visits for a window in that
+ * cell (_kernels.py:811-821), i.e. what `intersection_tests` adds per window.  The
+ * frame kernel reads this ONE u16 per window instead of 27 headers. */
+int lvx_neighbor_sums(const uint8_t *counts_d, const int32_t dims[3], uint16_t *nsum_d,
+                      void *stream);
+
 /* ------------------------------------------------------------------------- */
 /* Ray-caster: render_rows + stream_hit + dda_collect + tube/sphere + sort     */
 /* (_kernels.py:76-341, 625-923) and the density-grid secondary rays           */
@@ -192,7 +201,7 @@ typedef struct {
     const uint32_t *offsets_d;
     const lvx_seg_record *seg_rec_d;
     const float *table_d;      /* f32[256,4] */
-    const uint8_t *occ_d;      /* u8[(rz+2)(ry+2)(rx+2)] */
+    const uint16_t *nsum_d;    /* u16[(rz+2)(ry+2)(rx+2)] from lvx_neighbor_sums (neighbour mode) */
 } lvx_model;
 
 typedef struct {

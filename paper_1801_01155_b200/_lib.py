@@ -29,7 +29,7 @@ class Camera(C.Structure):
 class Model(C.Structure):
     _fields_ = [("rx", C.c_int32), ("ry", C.c_int32), ("rz", C.c_int32), ("_pad", C.c_int32),
                 ("counts_d", C.c_void_p), ("offsets_d", C.c_void_p), ("seg_rec_d", C.c_void_p),
-                ("table_d", C.c_void_p), ("occ_d", C.c_void_p)]
+                ("table_d", C.c_void_p), ("nsum_d", C.c_void_p)]
 
 
 class Params(C.Structure):
@@ -58,7 +58,7 @@ SYMBOLS = [
     "lvx_mark_curve_starts", "lvx_voxelize_count", "lvx_scan_scratch_bytes", "lvx_voxel_scan",
     "lvx_voxelize_emit", "lvx_voxelize_compact", "lvx_raw_regroup", "lvx_scan_u16", "lvx_provenance",
     "lvx_build_seg_records", "lvx_density_l0", "lvx_octree_layout", "lvx_build_octree",
-    "lvx_occupancy_dilate", "lvx_render_scratch_bytes", "lvx_render", "lvx_render_footprint", "lvx_untile",
+    "lvx_occupancy_dilate", "lvx_neighbor_sums", "lvx_render_scratch_bytes", "lvx_render", "lvx_render_footprint", "lvx_untile",
     "lvx_fibonacci_dirs", "lvx_ao_bake", "lvx_probe_dda", "lvx_probe_tube", "lvx_probe_sphere",
     "lvx_probe_trilinear", "lvx_probe_cone", "lvx_probe_ao_density",
 ]

@@ -45,3 +45,11 @@ static inline i64 lvx_ceil_div(i64 a, i64 b) { return (a + b - 1) / b; }
 // number of SMs of the current device (148 on B200); grids of persistent-style
 // kernels are sized as a multiple of it
 int lvx_sm_count();
+
+// Upper bound of half the segment length (bounding-sphere radius about the midpoint),
+// stored in lvx_seg_record::half_len for the frame kernel's conservative pre-reject.
+__host__ __device__ __forceinline__ float lvx_half_len(float ax, float ay, float az, float bx,
+                                                       float by, float bz) {
+    const float ux = bx - ax, uy = by - ay, uz = bz - az;
+    return 0.5f * sqrtf(ux * ux + uy * uy + uz * uz) * 1.0001f + 1e-6f;
+}

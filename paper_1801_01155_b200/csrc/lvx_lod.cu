@@ -98,6 +98,25 @@ dilate_kernel(const u8 *__restrict__ counts, int rx, int ry, int rz, u8 *__restr
     occ[c] = any;
 }
 
+// One thread per cell of the padded grid: sum of `counts` over the voxel's in-grid
+// 27-neighbourhood (max 27*255 fits u16).  nsum > 0 is exactly the dilated
+// occupancy above; the value itself is the number of candidate segments the
+// reference's neighbour gather visits for a window in this cell
+// (_kernels.py:811-821), which is what its `intersection_tests` counter adds up.
+__global__ void __launch_bounds__(256)
+nsum_kernel(const u8 *__restrict__ counts, int rx, int ry, int rz, u16 *__restrict__ nsum) {
+    const i64 sx = rx + 2, sy = ry + 2, sz = rz + 2;
+    const i64 c = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= sx * sy * sz) return;
+    const int px = (int)(c % sx), py = (int)((c / sx) % sy), pz = (int)(c / (sx * sy));
+    u32 sum = 0;
+    for (int z = max(pz - 2, 0); z <= min(pz, rz - 1); ++z)
+        for (int y = max(py - 2, 0); y <= min(py, ry - 1); ++y)
+            for (int x = max(px - 2, 0); x <= min(px, rx - 1); ++x)
+                sum += counts[((i64)z * ry + y) * rx + x];
+    nsum[c] = (u16)sum;
+}
+
 }  // namespace
 
 extern "C" {
@@ -156,6 +175,17 @@ int lvx_occupancy_dilate(const uint8_t *counts_d, const int32_t dims[3], uint8_t
     const i64 cells = (i64)(dims[0] + 2) * (dims[1] + 2) * (dims[2] + 2);
     dilate_kernel<<<(unsigned)lvx_ceil_div(cells, 256), 256, 0, (cudaStream_t)stream>>>(
         counts_d, dims[0], dims[1], dims[2], occ_d);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_neighbor_sums(const uint8_t *counts_d, const int32_t dims[3], uint16_t *nsum_d,
+                      void *stream) {
+    LVX_REQUIRE(counts_d && nsum_d && dims && dims[0] >= 1 && dims[1] >= 1 && dims[2] >= 1,
+                "bad arguments");
+    const i64 cells = (i64)(dims[0] + 2) * (dims[1] + 2) * (dims[2] + 2);
+    nsum_kernel<<<(unsigned)lvx_ceil_div(cells, 256), 256, 0, (cudaStream_t)stream>>>(
+        counts_d, dims[0], dims[1], dims[2], nsum_d);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }

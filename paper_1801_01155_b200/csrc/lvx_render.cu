@@ -1,29 +1,44 @@
 // Ray-caster for sm_100a: one thread per pixel in warp-coherent 8x4 pixel tiles,
-// incremental 3D-DDA, per-window gather over the voxel's (or 27 voxels') segment
-// records with 2 x 16-byte loads per segment, exact float64 tube / joint-sphere
-// tests, ordered insertion of the owned hits, front-to-back compositing with the
-// reference's de-duplication rules and early ray termination.
+// incremental 3D-DDA, exact float64 tube / joint-sphere tests, ordered insertion of
+// the owned hits, front-to-back compositing with the reference's de-duplication
+// rules and early ray termination.
 //
 //   render_rows   _kernels.py:735-923     stream_hit   _kernels.py:650-730
 //   dda_collect   _kernels.py:164-256     _hit_before  _kernels.py:261-270
 //   _seen_check_and_mark / _sphere_seen   _kernels.py:625-647
 //
-// The reference buffers all windows of a ray and up to 1024 hits of a window with
-// their normals, then insertion-sorts.  Here windows are produced incrementally and
-// a hit is stored as (t_in, voxel, segment, lid/kind/ordinal) only -- 20 bytes -- in
-// a sorted per-thread buffer; t_out and the normal are recomputed (bit-identically)
-// for the few hits that are actually composited.  A window with more owned hits
-// than the buffer holds is finished by extra gather passes that continue after the
-// last composited key, so the composited sequence is the reference's total order
-// (t_in, home voxel, lid, kind, gather order) in every case.
+// The reference visits, for every non-empty window of a ray, all segments of the
+// window's 27-voxel neighbourhood and runs three float64 intersection tests on each
+// (~700 tests per ray on the bench scene).  A hit only counts for a window if its
+// entry parameter t_in falls inside the window ("ownership").  This kernel produces
+// the same composited sequence and the same counters with far less work:
+//
+//  * `intersection_tests` is a sum of candidate counts, so it is read from the
+//    neighbour-sum grid (one u16 per window, lvx_neighbor_sums) instead of counted;
+//  * a hit owned by a window has its entry point on the ray piece inside the window's
+//    voxel and within tube_radius of its segment, which lies in its home voxel: only
+//    neighbour voxels within tube_radius of the ray piece's bounding box can own
+//    anything (sub-box cull, a subset of the 27 in the same scan order);
+//  * per candidate, a float32 bounding-sphere test in window-local coordinates
+//    (conservative: margins orders of magnitude above float32 rounding) rejects
+//    segments that cannot be hit inside this window; survivors are queued and then
+//    run through the exact float64 tests in a second, warp-converged phase;
+//  * a hit is buffered as (t_in, voxel, segment, lid/kind/ordinal) only; t_out and
+//    the normal are recomputed (bit-identically) for hits that are composited.  A
+//    window with more owned hits than the buffer holds is finished by extra gather
+//    passes that continue after the last composited key, so the composited sequence
+//    is the reference's total order (t_in, home voxel, lid, kind, gather order).
 #include <math_constants.h>
 
 #include "lvx_geom.cuh"
 
 namespace {
 
-constexpr int kHitCap = 64;       // sorted per-thread hit buffer (entries)
+constexpr int kHitCap = 32;       // sorted per-thread hit buffer (entries)
+constexpr int kQueue = 4;         // survivors of the float32 pre-reject awaiting the exact tests
 constexpr int kWarpsPerBlock = 4;
+constexpr double kCullMargin = 1e-4;   // sub-box cull slack (float64 path, rounding ~1e-12)
+constexpr float kRejectMargin = 2e-3f; // bounding-sphere slack (float32 path, rounding ~1e-5)
 
 struct RenderArgs {
     lvx_camera cam;
@@ -33,7 +48,7 @@ struct RenderArgs {
     const u32 *offsets;
     const lvx_seg_record *rec;
     const float *table;
-    const u8 *occ;
+    const u16 *nsum;
     LvxOctree oc;
     const float *ao_flat;
     const double *ao_dirs;
@@ -41,13 +56,7 @@ struct RenderArgs {
     int tiles_x, n_my_tiles;
     float *img;
     unsigned long long *row_stats;
-    u32 *footprint;  // instrumentation pass only: bitmap of voxels whose header was read
-};
-
-struct HitKey {
-    double t;
-    u32 lin;
-    u32 meta;  // lid (5 bits) | kind3 << 5 (0 tube, 1 sphere A, 2 sphere B) | ordinal << 8
+    u32 *footprint;  // instrumentation pass only: bitmap of voxels whose header the reference reads
 };
 
 __device__ __forceinline__ u32 meta_lid(u32 m) { return m & 31u; }
@@ -75,9 +84,10 @@ struct PixelState {
 };
 
 // stream_hit, _kernels.py:650-730.  Returns the accumulated alpha.
-__device__ double stream_hit(PixelState &S, const RenderArgs &A, double ox, double oy, double oz,
-                             double ddx, double ddy, double ddz, const LvxHit &h, u32 lin, u32 lid,
-                             u32 attr, bool is_sphere, float cx, float cy, float cz) {
+__device__ __noinline__ double stream_hit(PixelState &S, const RenderArgs &A, double ox, double oy,
+                                          double oz, double ddx, double ddy, double ddz,
+                                          const LvxHit &h, u32 lin, u32 lid, u32 attr,
+                                          bool is_sphere, float cx, float cy, float cz) {
     if (is_sphere) {
         for (int i = 0; i < S.n_sph; ++i)
             if (S.sph[i][0] == cx && S.sph[i][1] == cy && S.sph[i][2] == cz) return S.acc[3];
@@ -145,6 +155,19 @@ __device__ double stream_hit(PixelState &S, const RenderArgs &A, double ox, doub
     return S.acc[3];
 }
 
+// Conservative float32 test in window-local coordinates: can a primitive whose points
+// all lie within `reach` of centre c be entered by the ray inside this window?
+//   q0    ray point at the window start, d unit direction, tlen window length
+// The entry point lies on the ray piece [0, tlen] and within `reach` of c.
+__device__ __forceinline__ bool may_enter(float cx, float cy, float cz, float q0x, float q0y,
+                                          float q0z, float dx, float dy, float dz, float tlen,
+                                          float reach) {
+    const float wx = cx - q0x, wy = cy - q0y, wz = cz - q0z;
+    const float tc = wx * dx + wy * dy + wz * dz;
+    const float d2 = (wx * wx + wy * wy + wz * wz) - tc * tc;
+    return d2 <= reach * reach && tc >= -reach && tc <= tlen + reach;
+}
+
 template <bool FOOTPRINT>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 render_kernel(const RenderArgs A) {
@@ -179,6 +202,10 @@ render_kernel(const RenderArgs A) {
         const int rx = A.rx, ry = A.ry, rz = A.rz;
         const bool neighbor = p.neighbor != 0, joints = p.joints != 0;
         const double tube_r = p.tube_r;
+        const u32 tmul = joints ? 3u : 1u;
+        const float fdx = (float)ddx, fdy = (float)ddy, fdz = (float)ddz;
+        const float reach_pt = (float)tube_r + kRejectMargin;  // joint sphere about an endpoint
+        const double cull = tube_r + kCullMargin;
 
         PixelState S;
         S.acc[0] = S.acc[1] = S.acc[2] = S.acc[3] = 0.0;
@@ -186,96 +213,173 @@ render_kernel(const RenderArgs A) {
         S.n_sph = 0;
         double h_t[kHitCap];
         u32 h_lin[kHitCap], h_seg[kHitCap], h_meta[kHitCap];
+        u32 q_seg[kQueue], q_lin[kQueue], q_mask[kQueue];
 
         LvxDda dda;
         dda.init(ox, oy, oz, ddx, ddy, ddz, rx, ry, rz, neighbor ? 1 : 0);
         bool done = false;
-        int wx, wy, wz;
-        double t0, t1;
-        while (dda.next(wx, wy, wz, t0, t1)) {
-            steps += 1;  // the reference counts every window of the full walk (:785-786)
-            if (done) continue;
-            if (neighbor) {
-                if (A.occ[((i64)(wz + 1) * (ry + 2) + (wy + 1)) * (rx + 2) + (wx + 1)] == 0) continue;
-            } else {
-                if (A.counts[wx + (i64)rx * (wy + (i64)ry * wz)] == 0) continue;
+        for (;;) {
+            // ---- phase A: walk to the next window that has candidates ---------------------
+            int wx = 0, wy = 0, wz = 0;
+            double t0 = 0.0, t1 = 0.0;
+            bool have = false;
+            while (!have && dda.next(wx, wy, wz, t0, t1)) {
+                steps += 1;  // the reference counts every window of the full walk (:785-786)
+                if (done) continue;
+                u32 n;
+                if (neighbor) n = A.nsum[((i64)(wz + 1) * (ry + 2) + (wy + 1)) * (rx + 2) + (wx + 1)];
+                else n = A.counts[wx + (i64)rx * (wy + (i64)ry * wz)];
+                if (n == 0) continue;
+                tests += (unsigned long long)n * tmul;  // _kernels.py:833,855 summed over the gather
+                have = true;
             }
-            const int span = neighbor ? 1 : 0;
+            if (!have) break;
+
+            // ---- phase B: this window -----------------------------------------------------------
+            // neighbour voxels that can own a hit: within tube_r of the ray piece's bounding box
+            const double p0x = ox + t0 * ddx, p0y = oy + t0 * ddy, p0z = oz + t0 * ddz;
+            int x0 = wx, x1 = wx, y0 = wy, y1 = wy, z0 = wz, z1 = wz;
+            if (neighbor) {
+                const double p1x = ox + t1 * ddx, p1y = oy + t1 * ddy, p1z = oz + t1 * ddz;
+                if (fmin(p0x, p1x) - cull < (double)wx) x0 = wx - 1;
+                if (fmax(p0x, p1x) + cull > (double)(wx + 1)) x1 = wx + 1;
+                if (fmin(p0y, p1y) - cull < (double)wy) y0 = wy - 1;
+                if (fmax(p0y, p1y) + cull > (double)(wy + 1)) y1 = wy + 1;
+                if (fmin(p0z, p1z) - cull < (double)wz) z0 = wz - 1;
+                if (fmax(p0z, p1z) + cull > (double)(wz + 1)) z1 = wz + 1;
+                x0 = max(x0, 0);
+                y0 = max(y0, 0);
+                z0 = max(z0, 0);
+                x1 = min(x1, rx - 1);
+                y1 = min(y1, ry - 1);
+                z1 = min(z1, rz - 1);
+                if (FOOTPRINT) {
+                    for (int nz_ = max(wz - 1, 0); nz_ <= min(wz + 1, rz - 1); ++nz_)
+                        for (int ny_ = max(wy - 1, 0); ny_ <= min(wy + 1, ry - 1); ++ny_)
+                            for (int nx_ = max(wx - 1, 0); nx_ <= min(wx + 1, rx - 1); ++nx_) {
+                                const u32 l = (u32)(nx_ + rx * (ny_ + ry * nz_));
+                                atomicOr(&A.footprint[l >> 5], 1u << (l & 31u));
+                            }
+                }
+            } else if (FOOTPRINT) {
+                const u32 l = (u32)(wx + rx * (wy + ry * wz));
+                atomicOr(&A.footprint[l >> 5], 1u << (l & 31u));
+            }
+            if (x0 > x1 || y0 > y1 || z0 > z1) continue;
+            // window-local float32 frame: origin at the window voxel's corner
+            const float q0x = (float)(p0x - (double)wx), q0y = (float)(p0y - (double)wy),
+                        q0z = (float)(p0z - (double)wz);
+            const float tlen = (float)(t1 - t0);
+            const float fwx = (float)wx, fwy = (float)wy, fwz = (float)wz;
+
             // continuation key for windows that overflow the sorted buffer
             bool have_last = false;
             double last_t = 0.0;
             u32 last_lin = 0, last_meta = 0;
-            bool first_pass = true;
-            for (;;) {
+            for (;;) {  // gather passes (one unless the hit buffer spills)
                 int nh = 0;
                 bool spilled = false;
                 u32 ord = 0;  // gather ordinal of the next owned hit
-                for (int nz_ = wz - span; nz_ <= wz + span; ++nz_) {
-                    if (nz_ < 0 || nz_ >= rz) continue;
-                    for (int ny_ = wy - span; ny_ <= wy + span; ++ny_) {
-                        if (ny_ < 0 || ny_ >= ry) continue;
-                        for (int nx_ = wx - span; nx_ <= wx + span; ++nx_) {
-                            if (nx_ < 0 || nx_ >= rx) continue;
-                            const u32 lin = (u32)(nx_ + rx * (ny_ + ry * nz_));
-                            const u32 cnt = A.counts[lin];
-                            if (FOOTPRINT && first_pass) atomicOr(&A.footprint[lin >> 5], 1u << (lin & 31u));
-                            if (cnt == 0) continue;
-                            const u32 base = A.offsets[lin];
-                            for (u32 s = 0; s < cnt; ++s) {
-                                const u32 i = base + s;
-                                const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + i));
-                                const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + i) + 1);
-                                const u32 lid = (__float_as_uint(ra.w) >> 8) & 31u;
-                                if (first_pass) tests += joints ? 3 : 1;
-#pragma unroll
-                                for (int kind3 = 0; kind3 < 3; ++kind3) {
-                                    if (kind3 > 0 && !joints) break;
-                                    LvxHit h;
-                                    bool hit;
-                                    if (kind3 == 0)
-                                        hit = lvx_tube_f32axis(ox, oy, oz, ddx, ddy, ddz, ra.x, ra.y,
-                                                               ra.z, rb.x, rb.y, rb.z, tube_r, h);
-                                    else if (kind3 == 1)
-                                        hit = lvx_sphere<false>(ox, oy, oz, ddx, ddy, ddz, (double)ra.x,
-                                                                (double)ra.y, (double)ra.z, tube_r, h);
-                                    else
-                                        hit = lvx_sphere<false>(ox, oy, oz, ddx, ddy, ddz, (double)rb.x,
-                                                                (double)rb.y, (double)rb.z, tube_r, h);
-                                    if (!(hit && t0 <= h.t_in && h.t_in < t1)) continue;  // ownership
-                                    const u32 my_ord = ord++;
-                                    if (my_ord >= (u32)LVX_MAX_WINDOW_HITS) {
-                                        // the reference drops hits past its 1024-entry window buffer
-                                        if (first_pass) overflow += 1;
-                                        continue;
+                int vx = x0 - 1, vy = y0, vz = z0;
+                u32 s = 0, cnt = 0, base = 0, lin = 0;
+                bool more = true;
+                while (more) {
+                    // -- scan: float32 pre-reject, queue the survivors ---------------------------
+                    int nq = 0;
+                    while (nq < kQueue) {
+                        if (s >= cnt) {
+                            do {  // next non-empty voxel of the sub-box, scan order z,y,x
+                                if (++vx > x1) {
+                                    vx = x0;
+                                    if (++vy > y1) {
+                                        vy = y0;
+                                        ++vz;
                                     }
-                                    const u32 meta = lid | ((u32)kind3 << 5) | (my_ord << 8);
-                                    if (have_last &&
-                                        !key_before(last_t, last_lin, last_meta, h.t_in, lin, meta))
-                                        continue;  // composited in an earlier pass
-                                    int pos;
-                                    if (nh < kHitCap) {
-                                        pos = nh++;
-                                    } else {
-                                        spilled = true;
-                                        if (!key_before(h.t_in, lin, meta, h_t[kHitCap - 1],
-                                                        h_lin[kHitCap - 1], h_meta[kHitCap - 1]))
-                                            continue;
-                                        pos = kHitCap - 1;
-                                    }
-                                    while (pos > 0 && key_before(h.t_in, lin, meta, h_t[pos - 1],
-                                                                 h_lin[pos - 1], h_meta[pos - 1])) {
-                                        h_t[pos] = h_t[pos - 1];
-                                        h_lin[pos] = h_lin[pos - 1];
-                                        h_seg[pos] = h_seg[pos - 1];
-                                        h_meta[pos] = h_meta[pos - 1];
-                                        --pos;
-                                    }
-                                    h_t[pos] = h.t_in;
-                                    h_lin[pos] = lin;
-                                    h_seg[pos] = i;
-                                    h_meta[pos] = meta;
                                 }
+                                if (vz > z1) {
+                                    more = false;
+                                    break;
+                                }
+                                lin = (u32)(vx + rx * (vy + ry * vz));
+                                cnt = A.counts[lin];
+                            } while (cnt == 0);
+                            if (!more) break;
+                            base = A.offsets[lin];
+                            s = 0;
+                        }
+                        const u32 i = base + s;
+                        s += 1;
+                        const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + i));
+                        const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + i) + 1);
+                        const float ax = ra.x - fwx, ay = ra.y - fwy, az = ra.z - fwz;
+                        const float bx = rb.x - fwx, by = rb.y - fwy, bz = rb.z - fwz;
+                        u32 mask = 0;
+                        if (may_enter(0.5f * (ax + bx), 0.5f * (ay + by), 0.5f * (az + bz), q0x, q0y, q0z,
+                                      fdx, fdy, fdz, tlen, rb.w + reach_pt))
+                            mask |= 1u;
+                        if (joints) {
+                            if (may_enter(ax, ay, az, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mask |= 2u;
+                            if (may_enter(bx, by, bz, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mask |= 4u;
+                        }
+                        if (mask) {
+                            q_seg[nq] = i;
+                            q_lin[nq] = lin;
+                            q_mask[nq] = mask;
+                            nq += 1;
+                        }
+                    }
+                    // -- drain: exact float64 tests in candidate order --------------------------------
+                    for (int qi = 0; qi < nq; ++qi) {
+                        const u32 i = q_seg[qi], qlin = q_lin[qi], mask = q_mask[qi];
+                        const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + i));
+                        const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + i) + 1);
+                        const u32 lid = (__float_as_uint(ra.w) >> 8) & 31u;
+#pragma unroll
+                        for (int kind3 = 0; kind3 < 3; ++kind3) {
+                            if (!(mask & (1u << kind3))) continue;
+                            LvxHit h;
+                            bool hit;
+                            if (kind3 == 0)
+                                hit = lvx_tube_f32axis(ox, oy, oz, ddx, ddy, ddz, ra.x, ra.y, ra.z, rb.x,
+                                                       rb.y, rb.z, tube_r, h);
+                            else if (kind3 == 1)
+                                hit = lvx_sphere<false>(ox, oy, oz, ddx, ddy, ddz, (double)ra.x, (double)ra.y,
+                                                        (double)ra.z, tube_r, h);
+                            else
+                                hit = lvx_sphere<false>(ox, oy, oz, ddx, ddy, ddz, (double)rb.x, (double)rb.y,
+                                                        (double)rb.z, tube_r, h);
+                            if (!(hit && t0 <= h.t_in && h.t_in < t1)) continue;  // ownership
+                            const u32 my_ord = ord++;
+                            if (my_ord >= (u32)LVX_MAX_WINDOW_HITS) {
+                                // the reference drops hits past its 1024-entry window buffer
+                                if (!have_last) overflow += 1;
+                                continue;
                             }
+                            const u32 meta = lid | ((u32)kind3 << 5) | (my_ord << 8);
+                            if (have_last && !key_before(last_t, last_lin, last_meta, h.t_in, qlin, meta))
+                                continue;  // composited in an earlier pass
+                            int pos;
+                            if (nh < kHitCap) {
+                                pos = nh++;
+                            } else {
+                                spilled = true;
+                                if (!key_before(h.t_in, qlin, meta, h_t[kHitCap - 1], h_lin[kHitCap - 1],
+                                                h_meta[kHitCap - 1]))
+                                    continue;
+                                pos = kHitCap - 1;
+                            }
+                            while (pos > 0 && key_before(h.t_in, qlin, meta, h_t[pos - 1], h_lin[pos - 1],
+                                                         h_meta[pos - 1])) {
+                                h_t[pos] = h_t[pos - 1];
+                                h_lin[pos] = h_lin[pos - 1];
+                                h_seg[pos] = h_seg[pos - 1];
+                                h_meta[pos] = h_meta[pos - 1];
+                                --pos;
+                            }
+                            h_t[pos] = h.t_in;
+                            h_lin[pos] = qlin;
+                            h_seg[pos] = i;
+                            h_meta[pos] = meta;
                         }
                     }
                 }
@@ -310,7 +414,6 @@ render_kernel(const RenderArgs A) {
                 last_t = h_t[kHitCap - 1];
                 last_lin = h_lin[kHitCap - 1];
                 last_meta = h_meta[kHitCap - 1];
-                first_pass = false;
             }
         }
 
@@ -400,7 +503,7 @@ static int render_impl(const lvx_camera *cam, const lvx_model *model, const lvx_
                     model->offsets_d && model->table_d,
                 "bad model");
     LVX_REQUIRE((i64)model->rx * model->ry * model->rz < ((i64)1 << 31), "grid too large to render");
-    LVX_REQUIRE(!params->neighbor || model->occ_d, "neighbour mode needs the dilated occupancy map");
+    LVX_REQUIRE(!params->neighbor || model->nsum_d, "neighbour mode needs the neighbour-sum grid (lvx_neighbor_sums)");
     LVX_REQUIRE(params->opacity_mode >= 0 && params->opacity_mode <= 2, "bad opacity mode");
     LVX_REQUIRE(params->shadow_mode == LVX_SHADOW_NONE || params->shadow_mode == LVX_SHADOW_CONE,
                 "shadow_mode %d is not built in this library (none/cone only)", params->shadow_mode);
@@ -428,7 +531,7 @@ static int render_impl(const lvx_camera *cam, const lvx_model *model, const lvx_
     A.offsets = model->offsets_d;
     A.rec = model->seg_rec_d;
     A.table = model->table_d;
-    A.occ = model->occ_d;
+    A.nsum = model->nsum_d;
     fill_octree(A.oc, lod);
     A.ao_flat = lod ? lod->ao_flat_d : nullptr;
     A.ao_dirs = lod ? lod->ao_dirs_d : nullptr;

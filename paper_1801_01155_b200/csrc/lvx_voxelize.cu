@@ -501,7 +501,7 @@ compact_kernel(const u64 *__restrict__ raw_key, const u64 *__restrict__ raw_q,
     if (o.seg_rec) {
         float4 *rec = reinterpret_cast<float4 *>(o.seg_rec + dst);
         rec[0] = make_float4(a[0], a[1], a[2], __uint_as_float(attr | (lid << 8)));
-        rec[1] = make_float4(b[0], b[1], b[2], 0.0f);
+        rec[1] = make_float4(b[0], b[1], b[2], lvx_half_len(a[0], a[1], a[2], b[0], b[1], b[2]));
     }
 }
 
@@ -535,7 +535,9 @@ seg_records_kernel(const float *__restrict__ seg_a, const float *__restrict__ se
     float4 *r = reinterpret_cast<float4 *>(rec + s);
     u32 meta = (u32)seg_attr[s] | ((u32)seg_lid[s] << 8);
     r[0] = make_float4(seg_a[3 * s], seg_a[3 * s + 1], seg_a[3 * s + 2], __uint_as_float(meta));
-    r[1] = make_float4(seg_b[3 * s], seg_b[3 * s + 1], seg_b[3 * s + 2], 0.0f);
+    r[1] = make_float4(seg_b[3 * s], seg_b[3 * s + 1], seg_b[3 * s + 2],
+                       lvx_half_len(seg_a[3 * s], seg_a[3 * s + 1], seg_a[3 * s + 2], seg_b[3 * s],
+                                    seg_b[3 * s + 1], seg_b[3 * s + 2]));
 }
 
 // Multi-GPU merge: raw records gathered from all ranks (each rank's block is grouped

@@ -164,9 +164,13 @@ def _as_ray(ray):
 
 def traverse_voxels(ray, spec, pad: int = 0):
     """Ordered (voxel, t_enter, t_exit) triples of the DDA walk (raycast.py:170-181)."""
-    torch = _lib.require_device()
     o, d = _as_ray(ray)
-    dims = tuple(int(v) for v in getattr(spec, "dims", spec))
+    return probe_dda(o, d, tuple(int(v) for v in getattr(spec, "dims", spec)), pad)
+
+
+def probe_dda(o, d, dims, pad: int = 0):
+    """dda_collect (_kernels.py:164-256) for one ray with a unit direction `d` taken as is."""
+    torch = _lib.require_device()
     cap = dims[0] + dims[1] + dims[2] + 6 * (pad + 2)
     vox = torch.empty((cap, 3), dtype=torch.int64, device="cuda")
     t = torch.empty((cap, 2), dtype=torch.float64, device="cuda")
@@ -190,7 +194,8 @@ def probe_tubes(rays: np.ndarray, a: np.ndarray, b: np.ndarray, radius: float,
     dt = np.float32 if f32_axis else np.float64
     a_d, b_d = _lib.to_device(np.asarray(a).reshape(-1, 3), dt), _lib.to_device(np.asarray(b).reshape(-1, 3), dt)
     out = torch.empty((max(n, 1), 6), dtype=torch.float64, device="cuda")
-    _lib.check(_lib.lib().lvx_probe_tube(_lib.ptr(_lib.to_device(rays)), _lib.ptr(a_d), _lib.ptr(b_d),
+    rays_d = _lib.to_device(rays)  # named: a temporary would be recycled by the caching allocator
+    _lib.check(_lib.lib().lvx_probe_tube(_lib.ptr(rays_d), _lib.ptr(a_d), _lib.ptr(b_d),
                                          C.c_double(float(radius)), C.c_int32(1 if f32_axis else 0),
                                          C.c_int64(n), _lib.ptr(out), _lib.stream_ptr()))
     return out[:n].cpu().numpy()
@@ -201,8 +206,10 @@ def probe_spheres(rays: np.ndarray, centers: np.ndarray, radius: float) -> np.nd
     rays = np.ascontiguousarray(rays, dtype=np.float64).reshape(-1, 6)
     n = rays.shape[0]
     out = torch.empty((max(n, 1), 6), dtype=torch.float64, device="cuda")
+    rays_d = _lib.to_device(rays)
+    c_d = _lib.to_device(np.asarray(centers).reshape(-1, 3), np.float64)
     _lib.check(_lib.lib().lvx_probe_sphere(
-        _lib.ptr(_lib.to_device(rays)), _lib.ptr(_lib.to_device(np.asarray(centers).reshape(-1, 3), np.float64)),
+        _lib.ptr(rays_d), _lib.ptr(c_d),
         C.c_double(float(radius)), C.c_int64(n), _lib.ptr(out), _lib.stream_ptr()))
     return out[:n].cpu().numpy()
 
@@ -340,7 +347,7 @@ class FramePlan:
         m.rx, m.ry, m.rz = model.spec.dims
         m.counts_d, m.offsets_d = counts_d.data_ptr(), offsets_d.data_ptr()
         m.seg_rec_d, m.table_d = rec_d.data_ptr(), table_d.data_ptr()
-        m.occ_d = occ_d.data_ptr() if occ_d is not None else None
+        m.nsum_d = occ_d.data_ptr() if occ_d is not None else None
         self.mdl = m
         ao_d = model.ao_device() if params.ao_mode == "precomputed" else None
         dirs_d = fibonacci_dirs_device(params.ao_rays, 1) if params.ao_mode == "density-rays" else None

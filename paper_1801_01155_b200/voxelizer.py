@@ -245,7 +245,9 @@ class VoxelModel:
 
     # -- device-side render inputs --------------------------------------------------
     def device_view(self, need_occ: bool = True):
-        """(counts_d, offsets_d, seg_rec_d, table_d, occ_d) -- the lvx_model fields."""
+        """(counts_d, offsets_d, seg_rec_d, table_d, nsum_d) -- the lvx_model fields.
+        nsum_d (27-neighbourhood segment counts over the padded grid, whose non-zero
+        pattern is the reference's dilated occupancy map) is only needed in neighbour mode."""
         torch = _lib.require_device()
         L = _lib.lib()
         st = _lib.stream_ptr()
@@ -264,11 +266,21 @@ class VoxelModel:
             d["table_src"] = self.transfer_table
         if need_occ and "occ" not in d:
             rx, ry, rz = self.spec.dims
-            occ = torch.empty((rx + 2) * (ry + 2) * (rz + 2), dtype=torch.uint8, device="cuda")
-            _lib.check(L.lvx_occupancy_dilate(_lib.ptr(self.dev("counts")), _lib.i32x3(self.spec.dims),
-                                              _lib.ptr(occ), st))
+            occ = torch.empty((rx + 2) * (ry + 2) * (rz + 2), dtype=torch.int16, device="cuda")
+            _lib.check(L.lvx_neighbor_sums(_lib.ptr(self.dev("counts")), _lib.i32x3(self.spec.dims),
+                                           _lib.ptr(occ), st))
             d["occ"] = occ
         return (self.dev("counts"), self.dev("offsets"), d["seg_rec"], d["table"], d.get("occ"))
+
+    def occupancy_dilated(self) -> np.ndarray:
+        """The reference's `_occupancy_dilated` map (raycast.py:351-366): flat u8 over the
+        grid padded by one voxel, 1 where the voxel or any 26-neighbour holds segments."""
+        torch = _lib.require_device()
+        rx, ry, rz = self.spec.dims
+        occ = torch.empty((rx + 2) * (ry + 2) * (rz + 2), dtype=torch.uint8, device="cuda")
+        _lib.check(_lib.lib().lvx_occupancy_dilate(_lib.ptr(self.dev("counts")), _lib.i32x3(self.spec.dims),
+                                                   _lib.ptr(occ), _lib.stream_ptr()))
+        return occ.cpu().numpy()
 
     def ao_device(self):
         """Flat f32[V] device tensor of the baked AO field, or None."""

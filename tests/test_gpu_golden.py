@@ -109,6 +109,7 @@ def test_tube_and_sphere_probes(lv):
 
 
 def test_dda_windows(lv):
+    from paper_1801_01155_b200 import raycast
     g = golden("prim_dda")
     dims = tuple(int(x) for x in g["dims"])
     k = pos = 0
@@ -116,12 +117,15 @@ def test_dda_windows(lv):
         for i in range(0, g["o"].shape[0]):
             n = int(g["counts"][k])
             if i % 5 == 0 or i < 25:  # one launch per ray: probe a subset
-                w = lv.traverse_voxels((g["o"][i], g["d"][i]), dims, pad)
+                w = raycast.probe_dda(g["o"][i], g["d"][i], dims, pad)  # d as stored: no re-normalisation
                 assert len(w) == n
                 assert np.array_equal(np.asarray([v for v, _, _ in w]).reshape(-1, 3), g["vox"][pos:pos + n])
                 assert np.array_equal(np.asarray([(a, b) for _, a, b in w]).reshape(-1, 2), g["t"][pos:pos + n])
             pos += n
             k += 1
+    # reference KAT, tests/test_raycast.py:52-57, through the public op
+    w = lv.traverse_voxels(((-1.0, 0.5, 0.5), (2.0, 0.0, 0.0)), lv.GridSpec((3, 3, 3)))
+    assert w == [((0, 0, 0), 1.0, 2.0), ((1, 0, 0), 2.0, 3.0), ((2, 0, 0), 3.0, 4.0)]
 
 
 def test_density_probes(lv):
