@@ -173,14 +173,16 @@ int lvx_build_octree(float *flat_d, const int32_t dims[3], void *stream);
 int lvx_occupancy_dilate(const uint8_t *counts_d, const int32_t dims[3], uint8_t *occ_d,
                          void *stream);
 
-/* nsum_d u16[(rz+2)(ry+2)(rx+2)]: per cell of the grid padded by one voxel, the sum
- * of counts over the cell's in-grid 27-neighbourhood.  nsum > 0 is the dilated
- * occupancy of _occupancy_dilated (raycast.py:351-366); the value is the number of
- * candidate segments the reference's neighbour gather visits for a window in that
- * cell (_kernels.py:811-821), i.e. what `intersection_tests` adds per window.  The
- * frame kernel reads this ONE u16 per window instead of 27 headers. */
+/* Per cell of the grid padded by one voxel, over the cell's in-grid 27-neighbourhood:
+ *   nsum_d  u16[(rz+2)(ry+2)(rx+2)]  sum of counts.  nsum > 0 is the dilated occupancy
+ *           of _occupancy_dilated (raycast.py:351-366); the value is the number of
+ *           candidate segments the reference's neighbour gather visits for a window in
+ *           that cell (_kernels.py:811-821), i.e. what `intersection_tests` adds per window;
+ *   nmask_d u32[same] (nullable)  bit (dz+1)*9+(dy+1)*3+(dx+1) set when that neighbour
+ *           holds segments; bit order == the reference's gather order.
+ * The frame kernel reads these instead of 27 voxel headers per window. */
 int lvx_neighbor_sums(const uint8_t *counts_d, const int32_t dims[3], uint16_t *nsum_d,
-                      void *stream);
+                      uint32_t *nmask_d, void *stream);
 
 /* ------------------------------------------------------------------------- */
 /* Ray-caster: render_rows + stream_hit + dda_collect + tube/sphere + sort     */
@@ -201,7 +203,8 @@ typedef struct {
     const uint32_t *offsets_d;
     const lvx_seg_record *seg_rec_d;
     const float *table_d;      /* f32[256,4] */
-    const uint16_t *nsum_d;    /* u16[(rz+2)(ry+2)(rx+2)] from lvx_neighbor_sums (neighbour mode) */
+    const uint16_t *nsum_d;    /* from lvx_neighbor_sums (both needed in neighbour mode) */
+    const uint32_t *nmask_d;
 } lvx_model;
 
 typedef struct {

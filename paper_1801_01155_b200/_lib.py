@@ -29,7 +29,7 @@ class Camera(C.Structure):
 class Model(C.Structure):
     _fields_ = [("rx", C.c_int32), ("ry", C.c_int32), ("rz", C.c_int32), ("_pad", C.c_int32),
                 ("counts_d", C.c_void_p), ("offsets_d", C.c_void_p), ("seg_rec_d", C.c_void_p),
-                ("table_d", C.c_void_p), ("nsum_d", C.c_void_p)]
+                ("table_d", C.c_void_p), ("nsum_d", C.c_void_p), ("nmask_d", C.c_void_p)]
 
 
 class Params(C.Structure):

@@ -98,23 +98,39 @@ dilate_kernel(const u8 *__restrict__ counts, int rx, int ry, int rz, u8 *__restr
     occ[c] = any;
 }
 
-// One thread per cell of the padded grid: sum of `counts` over the voxel's in-grid
-// 27-neighbourhood (max 27*255 fits u16).  nsum > 0 is exactly the dilated
-// occupancy above; the value itself is the number of candidate segments the
-// reference's neighbour gather visits for a window in this cell
-// (_kernels.py:811-821), which is what its `intersection_tests` counter adds up.
+// One thread per cell of the padded grid: over the voxel's in-grid 27-neighbourhood,
+//   nsum  = sum of `counts` (max 27*255 fits u16): nsum > 0 is exactly the dilated
+//           occupancy above, and the value is the number of candidate segments the
+//           reference's neighbour gather visits for a window in this cell
+//           (_kernels.py:811-821), i.e. what its `intersection_tests` counter adds up;
+//   nmask = bit (dz+1)*9 + (dy+1)*3 + (dx+1) set when neighbour (dx,dy,dz) holds
+//           segments: bit order == the reference's gather order (z, y, x loops).
 __global__ void __launch_bounds__(256)
-nsum_kernel(const u8 *__restrict__ counts, int rx, int ry, int rz, u16 *__restrict__ nsum) {
+nsum_kernel(const u8 *__restrict__ counts, int rx, int ry, int rz, u16 *__restrict__ nsum,
+            u32 *__restrict__ nmask) {
     const i64 sx = rx + 2, sy = ry + 2, sz = rz + 2;
     const i64 c = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= sx * sy * sz) return;
+    // padded cell p is voxel p-1; its neighbours are voxels p-2 .. p
     const int px = (int)(c % sx), py = (int)((c / sx) % sy), pz = (int)(c / (sx * sy));
-    u32 sum = 0;
-    for (int z = max(pz - 2, 0); z <= min(pz, rz - 1); ++z)
-        for (int y = max(py - 2, 0); y <= min(py, ry - 1); ++y)
-            for (int x = max(px - 2, 0); x <= min(px, rx - 1); ++x)
-                sum += counts[((i64)z * ry + y) * rx + x];
+    u32 sum = 0, mask = 0;
+    for (int dz = 0; dz < 3; ++dz) {
+        const int z = pz - 2 + dz;
+        if (z < 0 || z >= rz) continue;
+        for (int dy = 0; dy < 3; ++dy) {
+            const int y = py - 2 + dy;
+            if (y < 0 || y >= ry) continue;
+            for (int dx = 0; dx < 3; ++dx) {
+                const int x = px - 2 + dx;
+                if (x < 0 || x >= rx) continue;
+                const u32 n = counts[((i64)z * ry + y) * rx + x];
+                sum += n;
+                if (n) mask |= 1u << (dz * 9 + dy * 3 + dx);
+            }
+        }
+    }
     nsum[c] = (u16)sum;
+    if (nmask) nmask[c] = mask;
 }
 
 }  // namespace
@@ -180,12 +196,12 @@ int lvx_occupancy_dilate(const uint8_t *counts_d, const int32_t dims[3], uint8_t
 }
 
 int lvx_neighbor_sums(const uint8_t *counts_d, const int32_t dims[3], uint16_t *nsum_d,
-                      void *stream) {
+                      uint32_t *nmask_d, void *stream) {
     LVX_REQUIRE(counts_d && nsum_d && dims && dims[0] >= 1 && dims[1] >= 1 && dims[2] >= 1,
                 "bad arguments");
     const i64 cells = (i64)(dims[0] + 2) * (dims[1] + 2) * (dims[2] + 2);
     nsum_kernel<<<(unsigned)lvx_ceil_div(cells, 256), 256, 0, (cudaStream_t)stream>>>(
-        counts_d, dims[0], dims[1], dims[2], nsum_d);
+        counts_d, dims[0], dims[1], dims[2], nsum_d, nmask_d);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }

@@ -35,7 +35,9 @@
 namespace {
 
 constexpr int kHitCap = 32;       // sorted per-thread hit buffer (entries)
-constexpr int kQueue = 4;         // survivors of the float32 pre-reject awaiting the exact tests
+constexpr int kHitFlush = 10;     // a lane with this many buffered hits asks for a composite
+constexpr int kQueue = 8;         // survivors of the float32 pre-reject awaiting the exact tests
+constexpr int kSlots = 8;         // windows a lane may open between two composites (<= 16)
 constexpr int kWarpsPerBlock = 4;
 constexpr double kCullMargin = 1e-4;   // sub-box cull slack (float64 path, rounding ~1e-12)
 constexpr float kRejectMargin = 2e-3f; // bounding-sphere slack (float32 path, rounding ~1e-5)
@@ -49,6 +51,7 @@ struct RenderArgs {
     const lvx_seg_record *rec;
     const float *table;
     const u16 *nsum;
+    const u32 *nmask;
     LvxOctree oc;
     const float *ao_flat;
     const double *ao_dirs;
@@ -59,9 +62,11 @@ struct RenderArgs {
     u32 *footprint;  // instrumentation pass only: bitmap of voxels whose header the reference reads
 };
 
+// hit meta word: lid 5 bits | kind3 2 (0 tube, 1 sphere A, 2 sphere B) | gather ordinal 10 | slot 4
 __device__ __forceinline__ u32 meta_lid(u32 m) { return m & 31u; }
 __device__ __forceinline__ u32 meta_kind3(u32 m) { return (m >> 5) & 3u; }
-__device__ __forceinline__ u32 meta_ord(u32 m) { return m >> 8; }
+__device__ __forceinline__ u32 meta_ord(u32 m) { return (m >> 7) & 1023u; }
+__device__ __forceinline__ u32 meta_slot(u32 m) { return m >> 17; }
 
 // _hit_before (_kernels.py:261-270) extended by the gather ordinal, which is what a
 // stable insertion sort resolves remaining ties with.
@@ -168,9 +173,47 @@ __device__ __forceinline__ bool may_enter(float cx, float cy, float cz, float q0
     return d2 <= reach * reach && tc >= -reach && tc <= tlen + reach;
 }
 
+// Instrumentation (lvx_render_footprint): set the bits of the voxels whose headers the
+// reference's gather reads for a window at packed voxel `pv` (own voxel, or the in-grid
+// 27-neighbourhood in neighbour mode).
+__device__ void mark_footprint(const RenderArgs &A, u32 pv, bool neighbor) {
+    const int wx = (int)(pv & 1023u) - 1, wy = (int)((pv >> 10) & 1023u) - 1, wz = (int)(pv >> 20) - 1;
+    const int r = neighbor ? 1 : 0;
+    for (int nz_ = max(wz - r, 0); nz_ <= min(wz + r, A.rz - 1); ++nz_)
+        for (int ny_ = max(wy - r, 0); ny_ <= min(wy + r, A.ry - 1); ++ny_)
+            for (int nx_ = max(wx - r, 0); nx_ <= min(wx + r, A.rx - 1); ++nx_) {
+                const u32 l = (u32)(nx_ + A.rx * (ny_ + A.ry * nz_));
+                atomicOr(&A.footprint[l >> 5], 1u << (l & 31u));
+            }
+}
+
+// The 32 rays of an 8x4 tile run a three-stage software pipeline.  Every loop that
+// contains a stage runs on a warp-uniform condition (__any_sync), so lanes only idle
+// INSIDE a stage instead of serialising whole code paths:
+//
+//  stage 1  "progress": per lane, a flat loop of micro-ops -- DDA step to the next window
+//           (counters, neighbour mask, sub-box cull), pop the next occupied voxel of the
+//           sub-box, or float32 pre-reject of one candidate segment -- until the lane's
+//           survivor queue is full, its ray ends, or it has to wait for a composite.
+//           Lanes are decoupled across windows here: one may skip empty windows while
+//           another scans a crowded one.
+//  stage 2  "drain": exact float64 tests on the queued survivors (several windows' worth),
+//           ownership test against the survivor's own window, sorted insertion.
+//  stage 3  "composite": when some lane has enough hits buffered (or nobody can walk on),
+//           every lane composites the hits of its completed windows in order.
+//
+// Hits are therefore composited later than they are found, and a lane may have scanned a
+// few windows past the one in which its ray terminates.  That is invisible in the output:
+// the counters are snapshotted per window (w_tests / w_over) and the snapshot of the
+// terminating hit's window is what gets reported, exactly the reference's count.
+struct alignas(8) Ray {
+    double ox, oy, oz, dx, dy, dz;
+};
+
 template <bool FOOTPRINT>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 render_kernel(const RenderArgs A) {
+    constexpr unsigned FULL = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31;
     const i64 gw = (i64)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
     const int wpt_x = A.tl.tile_w >> 3, wpt_y = A.tl.tile_h >> 2;
@@ -186,205 +229,240 @@ render_kernel(const RenderArgs A) {
     const bool active = tile_ok && x < W && y < H;
 
     unsigned long long steps = 0, tests = 0, overflow = 0;
-    if (active) {
-        const lvx_params &p = A.p;
-        // primary ray, _kernels.py:769-776
-        const double ndc_x = (((double)x + 0.5) / (double)W * 2.0 - 1.0) * A.cam.tan_half * A.cam.aspect;
-        const double ndc_y = (1.0 - ((double)y + 0.5) / (double)H * 2.0) * A.cam.tan_half;
-        double ddx = A.cam.f[0] + ndc_x * A.cam.r[0] + ndc_y * A.cam.u[0];
-        double ddy = A.cam.f[1] + ndc_x * A.cam.r[1] + ndc_y * A.cam.u[1];
-        double ddz = A.cam.f[2] + ndc_x * A.cam.r[2] + ndc_y * A.cam.u[2];
-        const double dn = sqrt(ddx * ddx + ddy * ddy + ddz * ddz);
-        ddx = ddx / dn;
-        ddy = ddy / dn;
-        ddz = ddz / dn;
-        const double ox = A.cam.o[0], oy = A.cam.o[1], oz = A.cam.o[2];
-        const int rx = A.rx, ry = A.ry, rz = A.rz;
-        const bool neighbor = p.neighbor != 0, joints = p.joints != 0;
-        const double tube_r = p.tube_r;
-        const u32 tmul = joints ? 3u : 1u;
-        const float fdx = (float)ddx, fdy = (float)ddy, fdz = (float)ddz;
-        const float reach_pt = (float)tube_r + kRejectMargin;  // joint sphere about an endpoint
-        const double cull = tube_r + kCullMargin;
+    const lvx_params &p = A.p;
+    // primary ray, _kernels.py:769-776
+    const double ndc_x = (((double)x + 0.5) / (double)W * 2.0 - 1.0) * A.cam.tan_half * A.cam.aspect;
+    const double ndc_y = (1.0 - ((double)y + 0.5) / (double)H * 2.0) * A.cam.tan_half;
+    double ddx = A.cam.f[0] + ndc_x * A.cam.r[0] + ndc_y * A.cam.u[0];
+    double ddy = A.cam.f[1] + ndc_x * A.cam.r[1] + ndc_y * A.cam.u[1];
+    double ddz = A.cam.f[2] + ndc_x * A.cam.r[2] + ndc_y * A.cam.u[2];
+    const double dn = sqrt(ddx * ddx + ddy * ddy + ddz * ddz);
+    ddx = ddx / dn;
+    ddy = ddy / dn;
+    ddz = ddz / dn;
+    const double ox = A.cam.o[0], oy = A.cam.o[1], oz = A.cam.o[2];
+    const int rx = A.rx, ry = A.ry, rz = A.rz;
+    const bool neighbor = p.neighbor != 0, joints = p.joints != 0;
+    const double tube_r = p.tube_r;
+    const u32 tmul = joints ? 3u : 1u;
+    const float fdx = (float)ddx, fdy = (float)ddy, fdz = (float)ddz;
+    const float reach_pt = (float)tube_r + kRejectMargin;  // joint sphere about an endpoint
+    const double cull = tube_r + kCullMargin;
 
-        PixelState S;
-        S.acc[0] = S.acc[1] = S.acc[2] = S.acc[3] = 0.0;
-        S.n_seen = 0;
-        S.n_sph = 0;
-        double h_t[kHitCap];
-        u32 h_lin[kHitCap], h_seg[kHitCap], h_meta[kHitCap];
-        u32 q_seg[kQueue], q_lin[kQueue], q_mask[kQueue];
+    PixelState S;
+    S.acc[0] = S.acc[1] = S.acc[2] = S.acc[3] = 0.0;
+    S.n_seen = 0;
+    S.n_sph = 0;
+    // sorted hit buffer: the hits of the windows scanned since the last composite
+    double h_t[kHitCap];
+    u32 h_lin[kHitCap], h_seg[kHitCap], h_meta[kHitCap];  // meta: lid 5 | kind3 2 | ordinal 10 | slot 4
+    // survivors of the pre-reject awaiting the exact tests; q_mask: primitive mask 3 | slot << 3
+    u32 q_seg[kQueue], q_lin[kQueue], q_mask[kQueue];
+    // windows opened since the last composite ("slots")
+    double w_t0[kSlots], w_t1[kSlots];
+    unsigned long long w_tests[kSlots];  // intersection_tests up to and including the window
+    u32 w_over[kSlots];                  // window_overflow of the window
+    u32 w_vox[FOOTPRINT ? kSlots : 1];   // instrumentation: packed window voxel (+1 per axis)
 
-        LvxDda dda;
-        dda.init(ox, oy, oz, ddx, ddy, ddz, rx, ry, rz, neighbor ? 1 : 0);
-        bool done = false;
+    LvxDda dda;
+    dda.alive = false;
+    if (active) dda.init(ox, oy, oz, ddx, ddy, ddz, rx, ry, rz, neighbor ? 1 : 0);
+    bool alive = active && dda.alive;  // the walk has windows left
+    bool done = false;                 // early ray termination reached
+
+    // current window (valid while !win_finished)
+    int cwx = 0, cwy = 0, cwz = 0;
+    float q0x = 0.f, q0y = 0.f, q0z = 0.f, tlen = 0.f;
+    u32 cw_mask = 0, m = 0;            // sub-box occupancy bits: all / still to scan
+    u32 s = 0, cnt = 0, base = 0, lin = 0;
+    int cur_slot = 0;
+    bool win_finished = true;
+    // batch state
+    int nh = 0, nq = 0, nw = 0;
+    int d_slot = -1, win_start = 0;    // drain: slot of the last drained survivor, its first hit
+    u32 ord = 0;                       // gather ordinal of the next owned hit of d_slot
+    bool spilled = false;
+    bool have_last = false;            // continuation key of a window that overflowed the buffer
+    double last_t = 0.0;
+    u32 last_lin = 0, last_meta = 0;
+    unsigned long long over_committed = 0;
+
+    for (;;) {
+        // ================= stage 1: progress ==================================================
         for (;;) {
-            // ---- phase A: walk to the next window that has candidates ---------------------
-            int wx = 0, wy = 0, wz = 0;
-            double t0 = 0.0, t1 = 0.0;
-            bool have = false;
-            while (!have && dda.next(wx, wy, wz, t0, t1)) {
+            const bool blocked_on_hits = win_finished && (nh >= kHitFlush || nw >= kSlots || spilled);
+            const bool go = alive && !done && nq < kQueue && !blocked_on_hits;
+            if (!__any_sync(FULL, go)) break;
+            if (!go) continue;
+            if (s < cnt) {
+                // ---- candidate op: float32 pre-reject in the window-local frame --------------------
+                const u32 i = base + s;
+                s += 1;
+                const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + i));
+                const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + i) + 1);
+                const float fwx = (float)cwx, fwy = (float)cwy, fwz = (float)cwz;
+                const float ax = ra.x - fwx, ay = ra.y - fwy, az = ra.z - fwz;
+                const float bx = rb.x - fwx, by = rb.y - fwy, bz = rb.z - fwz;
+                u32 mask = 0;
+                if (may_enter(0.5f * (ax + bx), 0.5f * (ay + by), 0.5f * (az + bz), q0x, q0y, q0z, fdx, fdy,
+                              fdz, tlen, rb.w + reach_pt))
+                    mask |= 1u;
+                if (joints) {
+                    if (may_enter(ax, ay, az, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mask |= 2u;
+                    if (may_enter(bx, by, bz, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mask |= 4u;
+                }
+                if (mask) {
+                    q_seg[nq] = i;
+                    q_lin[nq] = lin;
+                    q_mask[nq] = mask | ((u32)cur_slot << 3);
+                    nq += 1;
+                }
+                if (s >= cnt && m == 0) win_finished = true;
+            } else if (m != 0) {
+                // ---- voxel op: next occupied voxel of the sub-box, scan order z,y,x ---------------------
+                const int b = __ffs((int)m) - 1;
+                m &= m - 1;
+                const int bz_ = b / 9, by_ = (b - 9 * bz_) / 3, bx_ = b - 9 * bz_ - 3 * by_;
+                lin = (u32)((cwx + bx_ - 1) + rx * ((cwy + by_ - 1) + ry * (cwz + bz_ - 1)));
+                cnt = A.counts[lin];
+                base = A.offsets[lin];
+                s = 0;
+            } else {
+                // ---- window op: DDA step ---------------------------------------------------------------
+                int wx, wy, wz;
+                double t0, t1;
+                if (!dda.next(wx, wy, wz, t0, t1)) {
+                    alive = false;
+                    continue;
+                }
                 steps += 1;  // the reference counts every window of the full walk (:785-786)
-                if (done) continue;
-                u32 n;
-                if (neighbor) n = A.nsum[((i64)(wz + 1) * (ry + 2) + (wy + 1)) * (rx + 2) + (wx + 1)];
-                else n = A.counts[wx + (i64)rx * (wy + (i64)ry * wz)];
-                if (n == 0) continue;
-                tests += (unsigned long long)n * tmul;  // _kernels.py:833,855 summed over the gather
-                have = true;
-            }
-            if (!have) break;
-
-            // ---- phase B: this window -----------------------------------------------------------
-            // neighbour voxels that can own a hit: within tube_r of the ray piece's bounding box
-            const double p0x = ox + t0 * ddx, p0y = oy + t0 * ddy, p0z = oz + t0 * ddz;
-            int x0 = wx, x1 = wx, y0 = wy, y1 = wy, z0 = wz, z1 = wz;
-            if (neighbor) {
-                const double p1x = ox + t1 * ddx, p1y = oy + t1 * ddy, p1z = oz + t1 * ddz;
-                if (fmin(p0x, p1x) - cull < (double)wx) x0 = wx - 1;
-                if (fmax(p0x, p1x) + cull > (double)(wx + 1)) x1 = wx + 1;
-                if (fmin(p0y, p1y) - cull < (double)wy) y0 = wy - 1;
-                if (fmax(p0y, p1y) + cull > (double)(wy + 1)) y1 = wy + 1;
-                if (fmin(p0z, p1z) - cull < (double)wz) z0 = wz - 1;
-                if (fmax(p0z, p1z) + cull > (double)(wz + 1)) z1 = wz + 1;
-                x0 = max(x0, 0);
-                y0 = max(y0, 0);
-                z0 = max(z0, 0);
-                x1 = min(x1, rx - 1);
-                y1 = min(y1, ry - 1);
-                z1 = min(z1, rz - 1);
-                if (FOOTPRINT) {
-                    for (int nz_ = max(wz - 1, 0); nz_ <= min(wz + 1, rz - 1); ++nz_)
-                        for (int ny_ = max(wy - 1, 0); ny_ <= min(wy + 1, ry - 1); ++ny_)
-                            for (int nx_ = max(wx - 1, 0); nx_ <= min(wx + 1, rx - 1); ++nx_) {
-                                const u32 l = (u32)(nx_ + rx * (ny_ + ry * nz_));
-                                atomicOr(&A.footprint[l >> 5], 1u << (l & 31u));
-                            }
+                have_last = false;
+                u32 nm, n;
+                if (neighbor) {
+                    const i64 pc = ((i64)(wz + 1) * (ry + 2) + (wy + 1)) * (rx + 2) + (wx + 1);
+                    nm = A.nmask[pc];
+                    n = nm ? (u32)A.nsum[pc] : 0u;
+                } else {
+                    n = A.counts[wx + (i64)rx * (wy + (i64)ry * wz)];
+                    nm = n ? (1u << 13) : 0u;
                 }
-            } else if (FOOTPRINT) {
-                const u32 l = (u32)(wx + rx * (wy + ry * wz));
-                atomicOr(&A.footprint[l >> 5], 1u << (l & 31u));
+                if (nm == 0) continue;  // the reference's cheap skip (:793-799)
+                tests += (unsigned long long)n * tmul;  // :833,855 summed over the window's gather
+                // neighbour voxels that can own a hit of this window: within tube_r of the bounding
+                // box of the ray piece inside the window's voxel
+                const double p0x = ox + t0 * ddx, p0y = oy + t0 * ddy, p0z = oz + t0 * ddz;
+                if (neighbor) {
+                    const double p1x = ox + t1 * ddx, p1y = oy + t1 * ddy, p1z = oz + t1 * ddz;
+                    u32 bx_ = 0x2492492u, by_ = 0x0E07038u, bz_ = 0x003FE00u;  // centre column/row/slab
+                    if (fmin(p0x, p1x) - cull < (double)wx) bx_ |= 0x1249249u;
+                    if (fmax(p0x, p1x) + cull > (double)(wx + 1)) bx_ |= 0x4924924u;
+                    if (fmin(p0y, p1y) - cull < (double)wy) by_ |= 0x01C0E07u;
+                    if (fmax(p0y, p1y) + cull > (double)(wy + 1)) by_ |= 0x70381C0u;
+                    if (fmin(p0z, p1z) - cull < (double)wz) bz_ |= 0x00001FFu;
+                    if (fmax(p0z, p1z) + cull > (double)(wz + 1)) bz_ |= 0x7FC0000u;
+                    nm &= bx_ & by_ & bz_;
+                }
+                if (nm == 0 && !FOOTPRINT) continue;
+                // open a slot for the window
+                cur_slot = nw++;
+                w_t0[cur_slot] = t0;
+                w_t1[cur_slot] = t1;
+                w_tests[cur_slot] = tests;
+                w_over[cur_slot] = 0;
+                cwx = wx;
+                cwy = wy;
+                cwz = wz;
+                q0x = (float)(p0x - (double)wx);  // window-local float32 frame
+                q0y = (float)(p0y - (double)wy);
+                q0z = (float)(p0z - (double)wz);
+                tlen = (float)(t1 - t0);
+                cw_mask = m = nm;
+                s = cnt = 0;
+                win_finished = nm == 0;  // (only possible in the instrumented build)
+                if (FOOTPRINT) w_vox[cur_slot] = (u32)(wx + 1) | ((u32)(wy + 1) << 10) | ((u32)(wz + 1) << 20);
             }
-            if (x0 > x1 || y0 > y1 || z0 > z1) continue;
-            // window-local float32 frame: origin at the window voxel's corner
-            const float q0x = (float)(p0x - (double)wx), q0y = (float)(p0y - (double)wy),
-                        q0z = (float)(p0z - (double)wz);
-            const float tlen = (float)(t1 - t0);
-            const float fwx = (float)wx, fwy = (float)wy, fwz = (float)wz;
+        }
 
-            // continuation key for windows that overflow the sorted buffer
-            bool have_last = false;
-            double last_t = 0.0;
-            u32 last_lin = 0, last_meta = 0;
-            for (;;) {  // gather passes (one unless the hit buffer spills)
-                int nh = 0;
-                bool spilled = false;
-                u32 ord = 0;  // gather ordinal of the next owned hit
-                int vx = x0 - 1, vy = y0, vz = z0;
-                u32 s = 0, cnt = 0, base = 0, lin = 0;
-                bool more = true;
-                while (more) {
-                    // -- scan: float32 pre-reject, queue the survivors ---------------------------
-                    int nq = 0;
-                    while (nq < kQueue) {
-                        if (s >= cnt) {
-                            do {  // next non-empty voxel of the sub-box, scan order z,y,x
-                                if (++vx > x1) {
-                                    vx = x0;
-                                    if (++vy > y1) {
-                                        vy = y0;
-                                        ++vz;
-                                    }
-                                }
-                                if (vz > z1) {
-                                    more = false;
-                                    break;
-                                }
-                                lin = (u32)(vx + rx * (vy + ry * vz));
-                                cnt = A.counts[lin];
-                            } while (cnt == 0);
-                            if (!more) break;
-                            base = A.offsets[lin];
-                            s = 0;
-                        }
-                        const u32 i = base + s;
-                        s += 1;
-                        const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + i));
-                        const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + i) + 1);
-                        const float ax = ra.x - fwx, ay = ra.y - fwy, az = ra.z - fwz;
-                        const float bx = rb.x - fwx, by = rb.y - fwy, bz = rb.z - fwz;
-                        u32 mask = 0;
-                        if (may_enter(0.5f * (ax + bx), 0.5f * (ay + by), 0.5f * (az + bz), q0x, q0y, q0z,
-                                      fdx, fdy, fdz, tlen, rb.w + reach_pt))
-                            mask |= 1u;
-                        if (joints) {
-                            if (may_enter(ax, ay, az, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mask |= 2u;
-                            if (may_enter(bx, by, bz, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mask |= 4u;
-                        }
-                        if (mask) {
-                            q_seg[nq] = i;
-                            q_lin[nq] = lin;
-                            q_mask[nq] = mask;
-                            nq += 1;
-                        }
-                    }
-                    // -- drain: exact float64 tests in candidate order --------------------------------
-                    for (int qi = 0; qi < nq; ++qi) {
-                        const u32 i = q_seg[qi], qlin = q_lin[qi], mask = q_mask[qi];
-                        const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + i));
-                        const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + i) + 1);
-                        const u32 lid = (__float_as_uint(ra.w) >> 8) & 31u;
+        // ================= stage 2: drain -- exact float64 tests, in candidate order ===================
+#pragma unroll 1
+        for (int qi = 0; qi < kQueue; ++qi) {
+            const bool on = qi < nq;
+            if (!__any_sync(FULL, on)) break;
+            if (!on) continue;
+            const u32 i = q_seg[qi], qlin = q_lin[qi], qm = q_mask[qi];
+            const int slot = (int)(qm >> 3);
+            if (slot != d_slot) {
+                d_slot = slot;
+                ord = 0;
+                win_start = nh;
+            }
+            const double t0 = w_t0[slot], t1 = w_t1[slot];
+            const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + i));
+            const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + i) + 1);
+            const u32 lid = (__float_as_uint(ra.w) >> 8) & 31u;
 #pragma unroll
-                        for (int kind3 = 0; kind3 < 3; ++kind3) {
-                            if (!(mask & (1u << kind3))) continue;
-                            LvxHit h;
-                            bool hit;
-                            if (kind3 == 0)
-                                hit = lvx_tube_f32axis(ox, oy, oz, ddx, ddy, ddz, ra.x, ra.y, ra.z, rb.x,
-                                                       rb.y, rb.z, tube_r, h);
-                            else if (kind3 == 1)
-                                hit = lvx_sphere<false>(ox, oy, oz, ddx, ddy, ddz, (double)ra.x, (double)ra.y,
-                                                        (double)ra.z, tube_r, h);
-                            else
-                                hit = lvx_sphere<false>(ox, oy, oz, ddx, ddy, ddz, (double)rb.x, (double)rb.y,
-                                                        (double)rb.z, tube_r, h);
-                            if (!(hit && t0 <= h.t_in && h.t_in < t1)) continue;  // ownership
-                            const u32 my_ord = ord++;
-                            if (my_ord >= (u32)LVX_MAX_WINDOW_HITS) {
-                                // the reference drops hits past its 1024-entry window buffer
-                                if (!have_last) overflow += 1;
-                                continue;
-                            }
-                            const u32 meta = lid | ((u32)kind3 << 5) | (my_ord << 8);
-                            if (have_last && !key_before(last_t, last_lin, last_meta, h.t_in, qlin, meta))
-                                continue;  // composited in an earlier pass
-                            int pos;
-                            if (nh < kHitCap) {
-                                pos = nh++;
-                            } else {
-                                spilled = true;
-                                if (!key_before(h.t_in, qlin, meta, h_t[kHitCap - 1], h_lin[kHitCap - 1],
-                                                h_meta[kHitCap - 1]))
-                                    continue;
-                                pos = kHitCap - 1;
-                            }
-                            while (pos > 0 && key_before(h.t_in, qlin, meta, h_t[pos - 1], h_lin[pos - 1],
-                                                         h_meta[pos - 1])) {
-                                h_t[pos] = h_t[pos - 1];
-                                h_lin[pos] = h_lin[pos - 1];
-                                h_seg[pos] = h_seg[pos - 1];
-                                h_meta[pos] = h_meta[pos - 1];
-                                --pos;
-                            }
-                            h_t[pos] = h.t_in;
-                            h_lin[pos] = qlin;
-                            h_seg[pos] = i;
-                            h_meta[pos] = meta;
-                        }
-                    }
+            for (int kind3 = 0; kind3 < 3; ++kind3) {
+                if (!(qm & (1u << kind3))) continue;
+                LvxHit h;
+                bool hit;
+                if (kind3 == 0)
+                    hit = lvx_tube_f32axis(ox, oy, oz, ddx, ddy, ddz, ra.x, ra.y, ra.z, rb.x, rb.y, rb.z,
+                                           tube_r, h);
+                else if (kind3 == 1)
+                    hit = lvx_sphere<false>(ox, oy, oz, ddx, ddy, ddz, (double)ra.x, (double)ra.y,
+                                            (double)ra.z, tube_r, h);
+                else
+                    hit = lvx_sphere<false>(ox, oy, oz, ddx, ddy, ddz, (double)rb.x, (double)rb.y,
+                                            (double)rb.z, tube_r, h);
+                if (!(hit && t0 <= h.t_in && h.t_in < t1)) continue;  // ownership
+                const u32 my_ord = ord++;
+                if (my_ord >= (u32)LVX_MAX_WINDOW_HITS) {
+                    // the reference drops hits past its 1024-entry window buffer
+                    if (!have_last) w_over[slot] += 1;
+                    continue;
                 }
-                // composite in order, _kernels.py:898-914
-                for (int q = 0; q < nh; ++q) {
+                const u32 meta = lid | ((u32)kind3 << 5) | (my_ord << 7) | ((u32)slot << 17);
+                if (have_last && !key_before(last_t, last_lin, last_meta, h.t_in, qlin, meta))
+                    continue;  // composited in an earlier pass over this window
+                int pos;
+                if (nh < kHitCap && !spilled) {
+                    pos = nh++;
+                } else {
+                    // keep the smallest keys of this window and redo the rest in another pass.  Once a
+                    // hit has been dropped nothing larger than the buffer's last key may be accepted
+                    // (even if a composite of earlier windows frees space), or pass order would break.
+                    spilled = true;
+                    if (!key_before(h.t_in, qlin, meta, h_t[nh - 1], h_lin[nh - 1], h_meta[nh - 1]))
+                        continue;
+                    pos = nh - 1;
+                }
+                while (pos > win_start && key_before(h.t_in, qlin, meta, h_t[pos - 1], h_lin[pos - 1],
+                                                     h_meta[pos - 1])) {
+                    h_t[pos] = h_t[pos - 1];
+                    h_lin[pos] = h_lin[pos - 1];
+                    h_seg[pos] = h_seg[pos - 1];
+                    h_meta[pos] = h_meta[pos - 1];
+                    --pos;
+                }
+                h_t[pos] = h.t_in;
+                h_lin[pos] = qlin;
+                h_seg[pos] = i;
+                h_meta[pos] = meta;
+            }
+        }
+        nq = 0;
+
+        // ================= stage 3: composite, _kernels.py:898-914 ======================================
+        const bool walker = alive && !done;
+        const bool blocked = walker && win_finished && (nh >= kHitFlush || nw >= kSlots || spilled);
+        const bool any_walker = __any_sync(FULL, walker);
+        if (__any_sync(FULL, blocked) || !any_walker) {
+            // hits of completed windows only: an unfinished window may still produce smaller keys
+            const int n_comp = (win_finished || d_slot != cur_slot) ? nh : win_start;
+            int q = 0;
+            bool comp = !done && n_comp > 0;
+            while (__any_sync(FULL, comp)) {
+                if (comp) {
                     const u32 i = h_seg[q], meta = h_meta[q];
                     const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + i));
                     const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + i) + 1);
@@ -392,31 +470,100 @@ render_kernel(const RenderArgs A) {
                     LvxHit h;
                     float cx = 0.0f, cy = 0.0f, cz = 0.0f;
                     if (kind3 == 0) {
-                        lvx_tube_f32axis(ox, oy, oz, ddx, ddy, ddz, ra.x, ra.y, ra.z, rb.x, rb.y, rb.z,
-                                         tube_r, h);
+                        lvx_tube_f32axis(ox, oy, oz, ddx, ddy, ddz, ra.x, ra.y, ra.z, rb.x, rb.y, rb.z, tube_r, h);
                     } else {
                         cx = kind3 == 1 ? ra.x : rb.x;
                         cy = kind3 == 1 ? ra.y : rb.y;
                         cz = kind3 == 1 ? ra.z : rb.z;
-                        lvx_sphere<true>(ox, oy, oz, ddx, ddy, ddz, (double)cx, (double)cy, (double)cz,
-                                         tube_r, h);
+                        lvx_sphere<true>(ox, oy, oz, ddx, ddy, ddz, (double)cx, (double)cy, (double)cz, tube_r, h);
                     }
                     const double a_now =
                         stream_hit(S, A, ox, oy, oz, ddx, ddy, ddz, h, h_lin[q], meta_lid(meta),
                                    __float_as_uint(ra.w) & 0xFFu, kind3 != 0, cx, cy, cz);
                     if (a_now >= p.tau) {
+                        // terminated inside window `slot`: report the counters as of that window
+                        const int slot = (int)meta_slot(meta);
                         done = true;
-                        break;
+                        comp = false;
+                        tests = w_tests[slot];
+                        overflow = over_committed;
+                        for (int j = 0; j <= slot; ++j) overflow += w_over[j];
+                        if (FOOTPRINT)
+                            for (int j = 0; j <= slot; ++j) mark_footprint(A, w_vox[j], neighbor);
+                    } else if (++q >= n_comp) {
+                        comp = false;
                     }
                 }
-                if (done || !spilled) break;
-                have_last = true;
-                last_t = h_t[kHitCap - 1];
-                last_lin = h_lin[kHitCap - 1];
-                last_meta = h_meta[kHitCap - 1];
+            }
+            if (!done) {
+                // commit the composited windows, keep the unfinished one as slot 0
+                const bool keep = !win_finished;
+                const int n_commit = keep ? cur_slot : nw;
+                for (int j = 0; j < n_commit; ++j) over_committed += w_over[j];
+                if (FOOTPRINT)
+                    for (int j = 0; j < n_commit; ++j) mark_footprint(A, w_vox[j], neighbor);
+                if (spilled && win_finished) {
+                    // the buffer held only the smallest keys of the last window: scan it
+                    // again, continuing after the last composited key
+                    have_last = true;
+                    last_t = h_t[nh - 1];
+                    last_lin = h_lin[nh - 1];
+                    last_meta = h_meta[nh - 1] & 0x1FFFFu;  // slot bits are not part of the order
+                    w_t0[0] = w_t0[cur_slot];
+                    w_t1[0] = w_t1[cur_slot];
+                    w_tests[0] = w_tests[cur_slot];
+                    w_over[0] = 0;  // its overflow was committed above; later passes do not recount
+                    if (FOOTPRINT) w_vox[0] = w_vox[cur_slot];
+                    cur_slot = 0;
+                    nw = 1;
+                    nh = 0;
+                    m = cw_mask;
+                    s = cnt = 0;
+                    win_finished = false;
+                    spilled = false;
+                    d_slot = -1;
+                } else if (keep) {
+                    const int rest = nh - n_comp;
+                    for (int j = 0; j < rest; ++j) {
+                        h_t[j] = h_t[n_comp + j];
+                        h_lin[j] = h_lin[n_comp + j];
+                        h_seg[j] = h_seg[n_comp + j];
+                        h_meta[j] = h_meta[n_comp + j] & 0x1FFFFu;  // -> slot 0
+                    }
+                    w_t0[0] = w_t0[cur_slot];
+                    w_t1[0] = w_t1[cur_slot];
+                    w_tests[0] = w_tests[cur_slot];
+                    w_over[0] = w_over[cur_slot];
+                    if (FOOTPRINT) w_vox[0] = w_vox[cur_slot];
+                    d_slot = (d_slot == cur_slot) ? 0 : -1;
+                    cur_slot = 0;
+                    nw = 1;
+                    nh = rest;
+                    win_start = 0;
+                } else {
+                    nw = 0;
+                    nh = 0;
+                    d_slot = -1;
+                }
             }
         }
+        if (!any_walker) break;
+    }
+    if (!done) overflow = over_committed;
 
+    // tail: a terminated ray still reports the window count of its full walk
+    for (;;) {
+        const bool go = alive;
+        if (!__any_sync(FULL, go)) break;
+        if (go) {
+            int wx, wy, wz;
+            double t0, t1;
+            if (dda.next(wx, wy, wz, t0, t1)) steps += 1;
+            else alive = false;
+        }
+    }
+
+    if (active) {
         // _kernels.py:916-920
         const double a = S.acc[3];
         float4 outp;
@@ -433,9 +580,9 @@ render_kernel(const RenderArgs A) {
     // per-row counters: reduce over the 8 lanes that share an image row
 #pragma unroll
     for (int o = 1; o < 8; o <<= 1) {
-        steps += __shfl_xor_sync(0xFFFFFFFFu, steps, o);
-        tests += __shfl_xor_sync(0xFFFFFFFFu, tests, o);
-        overflow += __shfl_xor_sync(0xFFFFFFFFu, overflow, o);
+        steps += __shfl_xor_sync(FULL, steps, o);
+        tests += __shfl_xor_sync(FULL, tests, o);
+        overflow += __shfl_xor_sync(FULL, overflow, o);
     }
     if ((lane & 7) == 0 && tile_ok && y < H) {
         if (steps) atomicAdd(A.row_stats + 3 * (i64)y, steps);
@@ -503,7 +650,8 @@ static int render_impl(const lvx_camera *cam, const lvx_model *model, const lvx_
                     model->offsets_d && model->table_d,
                 "bad model");
     LVX_REQUIRE((i64)model->rx * model->ry * model->rz < ((i64)1 << 31), "grid too large to render");
-    LVX_REQUIRE(!params->neighbor || model->nsum_d, "neighbour mode needs the neighbour-sum grid (lvx_neighbor_sums)");
+    LVX_REQUIRE(!params->neighbor || (model->nsum_d && model->nmask_d),
+                "neighbour mode needs the neighbour grids (lvx_neighbor_sums)");
     LVX_REQUIRE(params->opacity_mode >= 0 && params->opacity_mode <= 2, "bad opacity mode");
     LVX_REQUIRE(params->shadow_mode == LVX_SHADOW_NONE || params->shadow_mode == LVX_SHADOW_CONE,
                 "shadow_mode %d is not built in this library (none/cone only)", params->shadow_mode);
@@ -532,6 +680,7 @@ static int render_impl(const lvx_camera *cam, const lvx_model *model, const lvx_
     A.rec = model->seg_rec_d;
     A.table = model->table_d;
     A.nsum = model->nsum_d;
+    A.nmask = model->nmask_d;
     fill_octree(A.oc, lod);
     A.ao_flat = lod ? lod->ao_flat_d : nullptr;
     A.ao_dirs = lod ? lod->ao_dirs_d : nullptr;
@@ -562,6 +711,8 @@ int lvx_render_footprint(const lvx_camera *cam, const lvx_model *model, const lv
                          const lvx_lod *lod, const lvx_tiling *tiling, float *img_d,
                          int64_t *row_stats_d, uint32_t *voxel_bits_d, void *stream) {
     LVX_REQUIRE(voxel_bits_d, "null footprint bitmap");
+    LVX_REQUIRE(model && model->rx <= 1022 && model->ry <= 1022 && model->rz <= 1022,
+                "footprint instrumentation supports grids up to 1022 per axis");
     return render_impl(cam, model, params, lod, tiling, img_d, row_stats_d, voxel_bits_d, stream);
 }
 

@@ -347,7 +347,8 @@ class FramePlan:
         m.rx, m.ry, m.rz = model.spec.dims
         m.counts_d, m.offsets_d = counts_d.data_ptr(), offsets_d.data_ptr()
         m.seg_rec_d, m.table_d = rec_d.data_ptr(), table_d.data_ptr()
-        m.nsum_d = occ_d.data_ptr() if occ_d is not None else None
+        m.nsum_d = occ_d[0].data_ptr() if occ_d is not None else None
+        m.nmask_d = occ_d[1].data_ptr() if occ_d is not None else None
         self.mdl = m
         ao_d = model.ao_device() if params.ao_mode == "precomputed" else None
         dirs_d = fibonacci_dirs_device(params.ao_rays, 1) if params.ao_mode == "density-rays" else None

@@ -245,9 +245,10 @@ class VoxelModel:
 
     # -- device-side render inputs --------------------------------------------------
     def device_view(self, need_occ: bool = True):
-        """(counts_d, offsets_d, seg_rec_d, table_d, nsum_d) -- the lvx_model fields.
-        nsum_d (27-neighbourhood segment counts over the padded grid, whose non-zero
-        pattern is the reference's dilated occupancy map) is only needed in neighbour mode."""
+        """(counts_d, offsets_d, seg_rec_d, table_d, (nsum_d, nmask_d)) -- the lvx_model
+        fields.  The neighbour grids (27-neighbourhood segment counts / occupancy bits
+        over the padded grid; nsum > 0 is the reference's dilated occupancy map) are
+        only needed in neighbour mode."""
         torch = _lib.require_device()
         L = _lib.lib()
         st = _lib.stream_ptr()
@@ -266,10 +267,12 @@ class VoxelModel:
             d["table_src"] = self.transfer_table
         if need_occ and "occ" not in d:
             rx, ry, rz = self.spec.dims
-            occ = torch.empty((rx + 2) * (ry + 2) * (rz + 2), dtype=torch.int16, device="cuda")
+            cells = (rx + 2) * (ry + 2) * (rz + 2)
+            nsum = torch.empty(cells, dtype=torch.int16, device="cuda")
+            nmask = torch.empty(cells, dtype=torch.int32, device="cuda")
             _lib.check(L.lvx_neighbor_sums(_lib.ptr(self.dev("counts")), _lib.i32x3(self.spec.dims),
-                                           _lib.ptr(occ), st))
-            d["occ"] = occ
+                                           _lib.ptr(nsum), _lib.ptr(nmask), st))
+            d["occ"] = (nsum, nmask)
         return (self.dev("counts"), self.dev("offsets"), d["seg_rec"], d["table"], d.get("occ"))
 
     def occupancy_dilated(self) -> np.ndarray:
