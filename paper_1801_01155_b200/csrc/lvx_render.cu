@@ -38,6 +38,7 @@ constexpr int kHitCap = 32;       // sorted per-thread hit buffer (entries)
 constexpr int kHitFlush = 10;     // a lane with this many buffered hits asks for a composite
 constexpr int kQueue = 8;         // survivors of the float32 pre-reject awaiting the exact tests
 constexpr int kSlots = 8;         // windows a lane may open between two composites (<= 16)
+constexpr int kShadeBatch = 8;    // hits per ray and round in the pooled shading stage (<= kQueue)
 constexpr int kWarpsPerBlock = 4;
 constexpr double kCullMargin = 1e-4;   // sub-box cull slack (float64 path, rounding ~1e-12)
 constexpr float kRejectMargin = 2e-3f; // bounding-sphere slack (float32 path, rounding ~1e-5)
@@ -88,11 +89,53 @@ struct PixelState {
     float sph[LVX_MAX_SEEN][3];
 };
 
-// stream_hit, _kernels.py:650-730.  Returns the accumulated alpha.
-__device__ __noinline__ double stream_hit(PixelState &S, const RenderArgs &A, double ox, double oy,
-                                          double oz, double ddx, double ddy, double ddz,
-                                          const LvxHit &h, u32 lin, u32 lid, u32 attr,
-                                          bool is_sphere, float cx, float cy, float cz) {
+// stream_hit, _kernels.py:650-730, split in two.  Everything that does not depend on the
+// pixel's running state -- shadow term, AO term, alpha, Blinn scale (:673-718) -- is
+// `shade_hit`, which any lane of the warp can evaluate for any ray's hit; the
+// de-duplication rules and the front-to-back accumulation (:666-670, :719-730) are
+// `accumulate_hit`, run by the ray's own lane in hit order.  The arithmetic and its
+// order are the reference's, so the result is bit-identical to the fused form.
+__device__ __forceinline__ void shade_hit(const RenderArgs &A, double ox, double oy, double oz,
+                                          double ddx, double ddy, double ddz, const LvxHit &h,
+                                          u32 attr, double &scale_out, double &alpha_out) {
+    const lvx_params &p = A.p;
+    const double gx = (double)A.rx, gy = (double)A.ry, gz = (double)A.rz;
+    const double px = ox + h.t_in * ddx, py = oy + h.t_in * ddy, pz = oz + h.t_in * ddz;
+    double shadow_term = 0.0;
+    if (p.shadow_mode == LVX_SHADOW_CONE)
+        shadow_term = lvx_cone_blocking(px, py, pz, p.light[0], p.light[1], p.light[2], A.oc, gx,
+                                        gy, gz, 0.01);
+    double ao_term = 0.0;
+    if (p.ao_mode == LVX_AO_PRECOMPUTED) {
+        ao_term = lvx_trilinear(A.ao_flat, 0, A.rx, A.ry, A.rz, 1.0, px, py, pz);
+        if (ao_term > 1.0) ao_term = 1.0;
+        if (ao_term < 0.0) ao_term = 0.0;
+    } else if (p.ao_mode == LVX_AO_DENSITY) {
+        ao_term = lvx_ao_density_point(px, py, pz, h.nx, h.ny, h.nz, p.ao_n_rays, p.ao_radius, 1.0,
+                                       A.ao_dirs, A.oc.flat, A.rx, A.ry, A.rz);
+    }
+    const float table_alpha = __ldg(A.table + 4 * attr + 3);
+    alpha_out = lvx_alpha_of(p.opacity_mode, p.base_alpha, (double)table_alpha, h.t_in, h.t_out);
+    double lgx, lgy, lgz;
+    if (p.headlight != 0) {
+        lgx = -ddx;
+        lgy = -ddy;
+        lgz = -ddz;
+    } else {
+        lgx = p.light[0];
+        lgy = p.light[1];
+        lgz = p.light[2];
+    }
+    double scale = lvx_shade(h.nx, h.ny, h.nz, lgx, lgy, lgz, -ddx, -ddy, -ddz,
+                             p.ka * (1.0 - ao_term), p.kd, p.ks, p.shininess);
+    scale *= 1.0 - shadow_term;
+    scale_out = scale;
+}
+
+// Returns the accumulated alpha.
+__device__ __forceinline__ double accumulate_hit(PixelState &S, const RenderArgs &A, double scale,
+                                                 double alpha, u32 lin, u32 lid, u32 attr,
+                                                 bool is_sphere, float cx, float cy, float cz) {
     if (is_sphere) {
         for (int i = 0; i < S.n_sph; ++i)
             if (S.sph[i][0] == cx && S.sph[i][1] == cy && S.sph[i][2] == cz) return S.acc[3];
@@ -114,37 +157,7 @@ __device__ __noinline__ double stream_hit(PixelState &S, const RenderArgs &A, do
             S.n_seen += 1;
         }
     }
-    const lvx_params &p = A.p;
-    const double gx = (double)A.rx, gy = (double)A.ry, gz = (double)A.rz;
-    const double px = ox + h.t_in * ddx, py = oy + h.t_in * ddy, pz = oz + h.t_in * ddz;
-    double shadow_term = 0.0;
-    if (p.shadow_mode == LVX_SHADOW_CONE)
-        shadow_term = lvx_cone_blocking(px, py, pz, p.light[0], p.light[1], p.light[2], A.oc, gx,
-                                        gy, gz, 0.01);
-    double ao_term = 0.0;
-    if (p.ao_mode == LVX_AO_PRECOMPUTED) {
-        ao_term = lvx_trilinear(A.ao_flat, 0, A.rx, A.ry, A.rz, 1.0, px, py, pz);
-        if (ao_term > 1.0) ao_term = 1.0;
-        if (ao_term < 0.0) ao_term = 0.0;
-    } else if (p.ao_mode == LVX_AO_DENSITY) {
-        ao_term = lvx_ao_density_point(px, py, pz, h.nx, h.ny, h.nz, p.ao_n_rays, p.ao_radius, 1.0,
-                                       A.ao_dirs, A.oc.flat, A.rx, A.ry, A.rz);
-    }
     const float4 col = __ldg(reinterpret_cast<const float4 *>(A.table) + attr);
-    const double alpha = lvx_alpha_of(p.opacity_mode, p.base_alpha, (double)col.w, h.t_in, h.t_out);
-    double lgx, lgy, lgz;
-    if (p.headlight != 0) {
-        lgx = -ddx;
-        lgy = -ddy;
-        lgz = -ddz;
-    } else {
-        lgx = p.light[0];
-        lgy = p.light[1];
-        lgz = p.light[2];
-    }
-    double scale = lvx_shade(h.nx, h.ny, h.nz, lgx, lgy, lgz, -ddx, -ddy, -ddz,
-                             p.ka * (1.0 - ao_term), p.kd, p.ks, p.shininess);
-    scale *= 1.0 - shadow_term;
     const double trans = 1.0 - S.acc[3];
     const double w = trans * alpha;
     S.acc[0] += w * scale * (double)col.x;
@@ -206,8 +219,12 @@ __device__ void mark_footprint(const RenderArgs &A, u32 pv, bool neighbor) {
 // few windows past the one in which its ray terminates.  That is invisible in the output:
 // the counters are snapshotted per window (w_tests / w_over) and the snapshot of the
 // terminating hit's window is what gets reported, exactly the reference's count.
-struct alignas(8) Ray {
-    double ox, oy, oz, dx, dy, dz;
+// Per-warp work pool in shared memory (drain and shading stages).
+struct WarpPool {
+    double dir[32][3];             // ray directions of the 32 lanes (the origin is shared)
+    double res[32 * kQueue][3];    // drain: t_in of tube / sphere A / sphere B; shading: scale, alpha
+    u32 it_seg[32 * kQueue];       // segment index of the pooled item
+    u16 it_meta[32 * kQueue];      // in: primitive mask or kind | owner lane << 3; out (drain): hit mask
 };
 
 template <bool FOOTPRINT>
@@ -248,6 +265,13 @@ render_kernel(const RenderArgs A) {
     const float fdx = (float)ddx, fdy = (float)ddy, fdz = (float)ddz;
     const float reach_pt = (float)tube_r + kRejectMargin;  // joint sphere about an endpoint
     const double cull = tube_r + kCullMargin;
+
+    __shared__ WarpPool pools[kWarpsPerBlock];
+    WarpPool &P = pools[threadIdx.x >> 5];
+    P.dir[lane][0] = ddx;
+    P.dir[lane][1] = ddy;
+    P.dir[lane][2] = ddz;
+    __syncwarp(FULL);
 
     PixelState S;
     S.acc[0] = S.acc[1] = S.acc[2] = S.acc[3] = 0.0;
@@ -383,72 +407,104 @@ render_kernel(const RenderArgs A) {
             }
         }
 
-        // ================= stage 2: drain -- exact float64 tests, in candidate order ===================
-#pragma unroll 1
-        for (int qi = 0; qi < kQueue; ++qi) {
-            const bool on = qi < nq;
-            if (!__any_sync(FULL, on)) break;
-            if (!on) continue;
-            const u32 i = q_seg[qi], qlin = q_lin[qi], qm = q_mask[qi];
-            const int slot = (int)(qm >> 3);
-            if (slot != d_slot) {
-                d_slot = slot;
-                ord = 0;
-                win_start = nh;
-            }
-            const double t0 = w_t0[slot], t1 = w_t1[slot];
-            const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + i));
-            const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + i) + 1);
-            const u32 lid = (__float_as_uint(ra.w) >> 8) & 31u;
+        // ================= stage 2: drain -- exact float64 tests ====================================
+        // The survivors of all 32 rays are pooled in shared memory and dealt out evenly: a lane
+        // tests whatever (ray, segment) pair it is handed, so the few rays that pass through
+        // crowded voxels do not leave the rest of the warp idle.  Results go back to the owner,
+        // which consumes them in candidate order (ownership test, ordinals, sorted insertion).
+        {
+            int off = nq;  // inclusive scan over lanes
 #pragma unroll
-            for (int kind3 = 0; kind3 < 3; ++kind3) {
-                if (!(qm & (1u << kind3))) continue;
-                LvxHit h;
-                bool hit;
-                if (kind3 == 0)
-                    hit = lvx_tube_f32axis(ox, oy, oz, ddx, ddy, ddz, ra.x, ra.y, ra.z, rb.x, rb.y, rb.z,
-                                           tube_r, h);
-                else if (kind3 == 1)
-                    hit = lvx_sphere<false>(ox, oy, oz, ddx, ddy, ddz, (double)ra.x, (double)ra.y,
-                                            (double)ra.z, tube_r, h);
-                else
-                    hit = lvx_sphere<false>(ox, oy, oz, ddx, ddy, ddz, (double)rb.x, (double)rb.y,
-                                            (double)rb.z, tube_r, h);
-                if (!(hit && t0 <= h.t_in && h.t_in < t1)) continue;  // ownership
-                const u32 my_ord = ord++;
-                if (my_ord >= (u32)LVX_MAX_WINDOW_HITS) {
-                    // the reference drops hits past its 1024-entry window buffer
-                    if (!have_last) w_over[slot] += 1;
-                    continue;
-                }
-                const u32 meta = lid | ((u32)kind3 << 5) | (my_ord << 7) | ((u32)slot << 17);
-                if (have_last && !key_before(last_t, last_lin, last_meta, h.t_in, qlin, meta))
-                    continue;  // composited in an earlier pass over this window
-                int pos;
-                if (nh < kHitCap && !spilled) {
-                    pos = nh++;
-                } else {
-                    // keep the smallest keys of this window and redo the rest in another pass.  Once a
-                    // hit has been dropped nothing larger than the buffer's last key may be accepted
-                    // (even if a composite of earlier windows frees space), or pass order would break.
-                    spilled = true;
-                    if (!key_before(h.t_in, qlin, meta, h_t[nh - 1], h_lin[nh - 1], h_meta[nh - 1]))
-                        continue;
-                    pos = nh - 1;
-                }
-                while (pos > win_start && key_before(h.t_in, qlin, meta, h_t[pos - 1], h_lin[pos - 1],
-                                                     h_meta[pos - 1])) {
-                    h_t[pos] = h_t[pos - 1];
-                    h_lin[pos] = h_lin[pos - 1];
-                    h_seg[pos] = h_seg[pos - 1];
-                    h_meta[pos] = h_meta[pos - 1];
-                    --pos;
-                }
-                h_t[pos] = h.t_in;
-                h_lin[pos] = qlin;
-                h_seg[pos] = i;
-                h_meta[pos] = meta;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(FULL, off, o);
+                if (lane >= o) off += t;
             }
+            const int total = __shfl_sync(FULL, off, 31);
+            off -= nq;
+            for (int qi = 0; qi < nq; ++qi) {
+                P.it_seg[off + qi] = q_seg[qi];
+                P.it_meta[off + qi] = (u16)((q_mask[qi] & 7u) | ((u32)lane << 3));
+            }
+            __syncwarp(FULL);
+            for (int idx = lane; idx < total; idx += 32) {
+                const u32 i = P.it_seg[idx], im = P.it_meta[idx];
+                const int owner = (int)(im >> 3);
+                const double rdx = P.dir[owner][0], rdy = P.dir[owner][1], rdz = P.dir[owner][2];
+                const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + i));
+                const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + i) + 1);
+                u32 hits = 0;
+                LvxHit h;
+                if ((im & 1u) && lvx_tube_f32axis(ox, oy, oz, rdx, rdy, rdz, ra.x, ra.y, ra.z, rb.x, rb.y, rb.z,
+                                                  tube_r, h)) {
+                    hits |= 1u;
+                    P.res[idx][0] = h.t_in;
+                }
+                if ((im & 2u) && lvx_sphere<false>(ox, oy, oz, rdx, rdy, rdz, (double)ra.x, (double)ra.y,
+                                                   (double)ra.z, tube_r, h)) {
+                    hits |= 2u;
+                    P.res[idx][1] = h.t_in;
+                }
+                if ((im & 4u) && lvx_sphere<false>(ox, oy, oz, rdx, rdy, rdz, (double)rb.x, (double)rb.y,
+                                                   (double)rb.z, tube_r, h)) {
+                    hits |= 4u;
+                    P.res[idx][2] = h.t_in;
+                }
+                P.it_meta[idx] = (u16)hits;
+            }
+            __syncwarp(FULL);
+            for (int qi = 0; qi < nq; ++qi) {
+                const u32 hits = P.it_meta[off + qi];
+                if (hits == 0) continue;
+                const u32 i = q_seg[qi], qlin = q_lin[qi];
+                const int slot = (int)(q_mask[qi] >> 3);
+                if (slot != d_slot) {
+                    d_slot = slot;
+                    ord = 0;
+                    win_start = nh;
+                }
+                const double t0 = w_t0[slot], t1 = w_t1[slot];
+                const u32 lid = (__float_as_uint(__ldg(reinterpret_cast<const float *>(A.rec + i) + 3)) >> 8) & 31u;
+#pragma unroll 1
+                for (int kind3 = 0; kind3 < 3; ++kind3) {
+                    if (!(hits & (1u << kind3))) continue;
+                    const double t_in = P.res[off + qi][kind3];
+                    if (!(t0 <= t_in && t_in < t1)) continue;  // ownership
+                    const u32 my_ord = ord++;
+                    if (my_ord >= (u32)LVX_MAX_WINDOW_HITS) {
+                        // the reference drops hits past its 1024-entry window buffer
+                        if (!have_last) w_over[slot] += 1;
+                        continue;
+                    }
+                    const u32 meta = lid | ((u32)kind3 << 5) | (my_ord << 7) | ((u32)slot << 17);
+                    if (have_last && !key_before(last_t, last_lin, last_meta, t_in, qlin, meta))
+                        continue;  // composited in an earlier pass over this window
+                    int pos;
+                    if (nh < kHitCap && !spilled) {
+                        pos = nh++;
+                    } else {
+                        // keep the smallest keys of this window and redo the rest in another pass.
+                        // Once a hit has been dropped nothing larger than the buffer's last key may
+                        // be accepted (even if a composite of earlier windows frees space), or the
+                        // pass order would break.
+                        spilled = true;
+                        if (!key_before(t_in, qlin, meta, h_t[nh - 1], h_lin[nh - 1], h_meta[nh - 1])) continue;
+                        pos = nh - 1;
+                    }
+                    while (pos > win_start &&
+                           key_before(t_in, qlin, meta, h_t[pos - 1], h_lin[pos - 1], h_meta[pos - 1])) {
+                        h_t[pos] = h_t[pos - 1];
+                        h_lin[pos] = h_lin[pos - 1];
+                        h_seg[pos] = h_seg[pos - 1];
+                        h_meta[pos] = h_meta[pos - 1];
+                        --pos;
+                    }
+                    h_t[pos] = t_in;
+                    h_lin[pos] = qlin;
+                    h_seg[pos] = i;
+                    h_meta[pos] = meta;
+                }
+            }
+            __syncwarp(FULL);
         }
         nq = 0;
 
@@ -459,27 +515,65 @@ render_kernel(const RenderArgs A) {
         if (__any_sync(FULL, blocked) || !any_walker) {
             // hits of completed windows only: an unfinished window may still produce smaller keys
             const int n_comp = (win_finished || d_slot != cur_slot) ? nh : win_start;
+            // Shading is pooled like the exact tests: up to kShadeBatch hits per ray and round are
+            // listed in shared memory, every lane recomputes one hit (t_out, normal) and its
+            // state-free shading terms, then each ray's own lane applies them in order.
             int q = 0;
             bool comp = !done && n_comp > 0;
             while (__any_sync(FULL, comp)) {
-                if (comp) {
-                    const u32 i = h_seg[q], meta = h_meta[q];
+                const int nb = comp ? min(kShadeBatch, n_comp - q) : 0;
+                int off = nb;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(FULL, off, o);
+                    if (lane >= o) off += t;
+                }
+                const int total = __shfl_sync(FULL, off, 31);
+                off -= nb;
+                for (int j = 0; j < nb; ++j) {
+                    P.it_seg[off + j] = h_seg[q + j];
+                    P.it_meta[off + j] = (u16)(meta_kind3(h_meta[q + j]) | ((u32)lane << 3));
+                }
+                __syncwarp(FULL);
+                for (int idx = lane; idx < total; idx += 32) {
+                    const u32 i = P.it_seg[idx], im = P.it_meta[idx];
+                    const int owner = (int)(im >> 3);
+                    const u32 kind3 = im & 3u;
+                    const double rdx = P.dir[owner][0], rdy = P.dir[owner][1], rdz = P.dir[owner][2];
                     const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + i));
                     const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + i) + 1);
-                    const u32 kind3 = meta_kind3(meta);
                     LvxHit h;
-                    float cx = 0.0f, cy = 0.0f, cz = 0.0f;
                     if (kind3 == 0) {
-                        lvx_tube_f32axis(ox, oy, oz, ddx, ddy, ddz, ra.x, ra.y, ra.z, rb.x, rb.y, rb.z, tube_r, h);
+                        lvx_tube_f32axis(ox, oy, oz, rdx, rdy, rdz, ra.x, ra.y, ra.z, rb.x, rb.y, rb.z, tube_r, h);
                     } else {
-                        cx = kind3 == 1 ? ra.x : rb.x;
-                        cy = kind3 == 1 ? ra.y : rb.y;
-                        cz = kind3 == 1 ? ra.z : rb.z;
-                        lvx_sphere<true>(ox, oy, oz, ddx, ddy, ddz, (double)cx, (double)cy, (double)cz, tube_r, h);
+                        const float cx = kind3 == 1 ? ra.x : rb.x, cy = kind3 == 1 ? ra.y : rb.y,
+                                    cz = kind3 == 1 ? ra.z : rb.z;
+                        lvx_sphere<true>(ox, oy, oz, rdx, rdy, rdz, (double)cx, (double)cy, (double)cz, tube_r, h);
                     }
-                    const double a_now =
-                        stream_hit(S, A, ox, oy, oz, ddx, ddy, ddz, h, h_lin[q], meta_lid(meta),
-                                   __float_as_uint(ra.w) & 0xFFu, kind3 != 0, cx, cy, cz);
+                    double scale, alpha;
+                    shade_hit(A, ox, oy, oz, rdx, rdy, rdz, h, __float_as_uint(ra.w) & 0xFFu, scale, alpha);
+                    P.res[idx][0] = scale;
+                    P.res[idx][1] = alpha;
+                }
+                __syncwarp(FULL);
+                for (int j = 0; j < nb; ++j) {
+                    const u32 i = h_seg[q], meta = h_meta[q];
+                    const u32 kind3 = meta_kind3(meta);
+                    const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + i));
+                    float cx = 0.0f, cy = 0.0f, cz = 0.0f;
+                    if (kind3 == 1) {
+                        cx = ra.x;
+                        cy = ra.y;
+                        cz = ra.z;
+                    } else if (kind3 == 2) {
+                        const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + i) + 1);
+                        cx = rb.x;
+                        cy = rb.y;
+                        cz = rb.z;
+                    }
+                    const double a_now = accumulate_hit(S, A, P.res[off + j][0], P.res[off + j][1], h_lin[q],
+                                                        meta_lid(meta), __float_as_uint(ra.w) & 0xFFu,
+                                                        kind3 != 0, cx, cy, cz);
                     if (a_now >= p.tau) {
                         // terminated inside window `slot`: report the counters as of that window
                         const int slot = (int)meta_slot(meta);
@@ -487,13 +581,14 @@ render_kernel(const RenderArgs A) {
                         comp = false;
                         tests = w_tests[slot];
                         overflow = over_committed;
-                        for (int j = 0; j <= slot; ++j) overflow += w_over[j];
+                        for (int jj = 0; jj <= slot; ++jj) overflow += w_over[jj];
                         if (FOOTPRINT)
-                            for (int j = 0; j <= slot; ++j) mark_footprint(A, w_vox[j], neighbor);
-                    } else if (++q >= n_comp) {
-                        comp = false;
+                            for (int jj = 0; jj <= slot; ++jj) mark_footprint(A, w_vox[jj], neighbor);
+                        break;
                     }
+                    if (++q >= n_comp) comp = false;
                 }
+                __syncwarp(FULL);
             }
             if (!done) {
                 // commit the composited windows, keep the unfinished one as slot 0
