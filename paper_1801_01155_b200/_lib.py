@@ -11,7 +11,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblinevox_b200.so")
+# LVX_LIB: developer override to load an experimental build of the same ABI
+LIB_PATH = os.environ.get("LVX_LIB") or os.path.join(_HERE, "liblinevox_b200.so")
 
 MAX_LEVELS = 24
 

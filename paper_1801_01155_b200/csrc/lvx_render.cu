@@ -34,11 +34,24 @@
 
 namespace {
 
-constexpr int kHitCap = 32;       // sorted per-thread hit buffer (entries)
-constexpr int kHitFlush = 10;     // a lane with this many buffered hits asks for a composite
-constexpr int kQueue = 8;         // survivors of the float32 pre-reject awaiting the exact tests
-constexpr int kSlots = 8;         // windows a lane may open between two composites (<= 16)
-constexpr int kShadeBatch = 8;    // hits per ray and round in the pooled shading stage (<= kQueue)
+// tuning knobs (overridable with -D for experiments)
+#ifndef LVX_HIT_FLUSH
+#define LVX_HIT_FLUSH 10
+#endif
+#ifndef LVX_QUEUE
+#define LVX_QUEUE 8
+#endif
+#ifndef LVX_SLOTS
+#define LVX_SLOTS 8
+#endif
+#ifndef LVX_MIN_BLOCKS
+#define LVX_MIN_BLOCKS 3
+#endif
+constexpr int kHitCap = 32;                 // sorted per-thread hit buffer (entries)
+constexpr int kHitFlush = LVX_HIT_FLUSH;    // a lane with this many buffered hits asks for a composite
+constexpr int kQueue = LVX_QUEUE;           // survivors of the float32 pre-reject awaiting the exact tests
+constexpr int kSlots = LVX_SLOTS;           // windows a lane may open between two composites (<= 16)
+constexpr int kShadeBatch = LVX_QUEUE;      // hits per ray and round in the pooled shading stage (<= kQueue)
 constexpr int kWarpsPerBlock = 4;
 constexpr double kCullMargin = 1e-4;   // sub-box cull slack (float64 path, rounding ~1e-12)
 constexpr float kRejectMargin = 2e-3f; // bounding-sphere slack (float32 path, rounding ~1e-5)
@@ -228,7 +241,7 @@ struct WarpPool {
 };
 
 template <bool FOOTPRINT>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, LVX_MIN_BLOCKS)
 render_kernel(const RenderArgs A) {
     constexpr unsigned FULL = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31;
@@ -327,13 +340,15 @@ render_kernel(const RenderArgs A) {
                 const float fwx = (float)cwx, fwy = (float)cwy, fwz = (float)cwz;
                 const float ax = ra.x - fwx, ay = ra.y - fwy, az = ra.z - fwz;
                 const float bx = rb.x - fwx, by = rb.y - fwy, bz = rb.z - fwz;
+                // the tube AND both joint spheres lie inside the segment's bounding sphere
                 u32 mask = 0;
                 if (may_enter(0.5f * (ax + bx), 0.5f * (ay + by), 0.5f * (az + bz), q0x, q0y, q0z, fdx, fdy,
-                              fdz, tlen, rb.w + reach_pt))
-                    mask |= 1u;
-                if (joints) {
-                    if (may_enter(ax, ay, az, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mask |= 2u;
-                    if (may_enter(bx, by, bz, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mask |= 4u;
+                              fdz, tlen, rb.w + reach_pt)) {
+                    mask = 1u;
+                    if (joints) {
+                        if (may_enter(ax, ay, az, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mask |= 2u;
+                        if (may_enter(bx, by, bz, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mask |= 4u;
+                    }
                 }
                 if (mask) {
                     q_seg[nq] = i;

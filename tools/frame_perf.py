@@ -23,10 +23,13 @@ def main():
     names = sys.argv[1:] or ["c3"]
     for name in names:
         dims, m, oc = scene(name)
-        for label, kw in (("nb a.25 AO", dict(base_opacity=0.25, neighbor_mode="on", ao_mode="precomputed")),
+        cases = (("nb a.25 AO", dict(base_opacity=0.25, neighbor_mode="on", ao_mode="precomputed")),
                           ("own a.25 AO", dict(base_opacity=0.25, neighbor_mode="off", ao_mode="precomputed")),
                           ("nb a.25 AO cone", dict(base_opacity=0.25, neighbor_mode="on", ao_mode="precomputed", shadow_mode="cone", light_dir=(0.3, 0.2, 1.0))),
-                          ("nb opaque", dict(neighbor_mode="on"))):
+                          ("nb opaque", dict(neighbor_mode="on")))
+        if os.environ.get("PERF_QUICK"):
+            cases = cases[:2]
+        for label, kw in cases:
             cam = lv.default_camera(dims, 1920, 1080)
             p = lv.RenderParams(**kw)
             plan = FramePlan(cam, m, oc, p, 1 if kw["neighbor_mode"] == "on" else 0)
