@@ -38,8 +38,8 @@ namespace {
 #ifndef LVX_HIT_FLUSH
 #define LVX_HIT_FLUSH 10
 #endif
-#ifndef LVX_QUEUE
-#define LVX_QUEUE 8
+#ifndef LVX_SHADE_BATCH
+#define LVX_SHADE_BATCH 8
 #endif
 #ifndef LVX_SLOTS
 #define LVX_SLOTS 8
@@ -47,11 +47,16 @@ namespace {
 #ifndef LVX_MIN_BLOCKS
 #define LVX_MIN_BLOCKS 3
 #endif
+#ifndef LVX_WALK_STEPS
+#define LVX_WALK_STEPS 8
+#endif
 constexpr int kHitCap = 32;                 // sorted per-thread hit buffer (entries)
 constexpr int kHitFlush = LVX_HIT_FLUSH;    // a lane with this many buffered hits asks for a composite
-constexpr int kQueue = LVX_QUEUE;           // survivors of the float32 pre-reject awaiting the exact tests
 constexpr int kSlots = LVX_SLOTS;           // windows a lane may open between two composites (<= 16)
-constexpr int kShadeBatch = LVX_QUEUE;      // hits per ray and round in the pooled shading stage (<= kQueue)
+constexpr int kShadeBatch = LVX_SHADE_BATCH;  // hits per ray and round in the pooled shading stage
+constexpr int kWalkSteps = LVX_WALK_STEPS;  // DDA steps a lane may take per round looking for a window
+constexpr int kItemCap = 256;               // voxel items per round and warp (>= 27)
+constexpr int kSurvCap = 64;                // survivor ring per warp (power of two, >= 64)
 constexpr int kWarpsPerBlock = 4;
 constexpr double kCullMargin = 1e-4;   // sub-box cull slack (float64 path, rounding ~1e-12)
 constexpr float kRejectMargin = 2e-3f; // bounding-sphere slack (float32 path, rounding ~1e-5)
@@ -97,6 +102,9 @@ __device__ __forceinline__ bool key_before(double ta, u32 la, u32 ma, double tb,
 struct PixelState {
     double acc[4];
     int n_seen, n_sph;
+    // 64-bit Bloom filters over the keys of the two tables below: a clear bit proves the key
+    // was never inserted, so the linear search (the reference's, :625-647) can be skipped
+    unsigned long long seen_bloom, sph_bloom;
     u32 seen_key[LVX_MAX_SEEN];
     u32 seen_mask[LVX_MAX_SEEN];
     float sph[LVX_MAX_SEEN][3];
@@ -149,25 +157,35 @@ __device__ __forceinline__ void shade_hit(const RenderArgs &A, double ox, double
 __device__ __forceinline__ double accumulate_hit(PixelState &S, const RenderArgs &A, double scale,
                                                  double alpha, u32 lin, u32 lid, u32 attr,
                                                  bool is_sphere, float cx, float cy, float cz) {
+    unsigned long long sph_bit = 0;
     if (is_sphere) {
-        for (int i = 0; i < S.n_sph; ++i)
-            if (S.sph[i][0] == cx && S.sph[i][1] == cy && S.sph[i][2] == cz) return S.acc[3];
+        const u32 hsh = (__float_as_uint(cx) * 0x9E3779B1u) ^ (__float_as_uint(cy) * 0x85EBCA77u) ^
+                        (__float_as_uint(cz) * 0xC2B2AE3Du);
+        sph_bit = 1ull << (hsh >> 26);
+        if (S.sph_bloom & sph_bit) {
+            for (int i = S.n_sph - 1; i >= 0; --i)  // the most recent centres are the likely repeats
+                if (S.sph[i][0] == cx && S.sph[i][1] == cy && S.sph[i][2] == cz) return S.acc[3];
+        }
     }
     {
         const u32 bit = 1u << lid;
+        const unsigned long long kb = 1ull << ((lin * 0x9E3779B1u) >> 26);
         bool found = false;
-        for (int i = 0; i < S.n_seen; ++i) {
-            if (S.seen_key[i] == lin) {
-                if (S.seen_mask[i] & bit) return S.acc[3];
-                S.seen_mask[i] |= bit;
-                found = true;
-                break;
+        if (S.seen_bloom & kb) {
+            for (int i = S.n_seen - 1; i >= 0; --i) {
+                if (S.seen_key[i] == lin) {
+                    if (S.seen_mask[i] & bit) return S.acc[3];
+                    S.seen_mask[i] |= bit;
+                    found = true;
+                    break;
+                }
             }
         }
         if (!found && S.n_seen < LVX_MAX_SEEN) {
             S.seen_key[S.n_seen] = lin;
             S.seen_mask[S.n_seen] = bit;
             S.n_seen += 1;
+            S.seen_bloom |= kb;
         }
     }
     const float4 col = __ldg(reinterpret_cast<const float4 *>(A.table) + attr);
@@ -182,6 +200,7 @@ __device__ __forceinline__ double accumulate_hit(PixelState &S, const RenderArgs
         S.sph[S.n_sph][1] = cy;
         S.sph[S.n_sph][2] = cz;
         S.n_sph += 1;
+        S.sph_bloom |= sph_bit;
     }
     return S.acc[3];
 }
@@ -213,31 +232,56 @@ __device__ void mark_footprint(const RenderArgs &A, u32 pv, bool neighbor) {
             }
 }
 
-// The 32 rays of an 8x4 tile run a three-stage software pipeline.  Every loop that
-// contains a stage runs on a warp-uniform condition (__any_sync), so lanes only idle
-// INSIDE a stage instead of serialising whole code paths:
+// The 32 rays of an 8x4 tile are walked by one warp in bulk-synchronous ROUNDS.  Rays are
+// bound to lanes only where per-ray state is needed (the DDA walk, the sorted hit buffer,
+// the running colour); every gather-type stage is pooled in shared memory and dealt out
+// evenly over the 32 lanes, so the few rays that cross crowded voxels do not serialise
+// the warp:
 //
-//  stage 1  "progress": per lane, a flat loop of micro-ops -- DDA step to the next window
-//           (counters, neighbour mask, sub-box cull), pop the next occupied voxel of the
-//           sub-box, or float32 pre-reject of one candidate segment -- until the lane's
-//           survivor queue is full, its ray ends, or it has to wait for a composite.
-//           Lanes are decoupled across windows here: one may skip empty windows while
-//           another scans a crowded one.
-//  stage 2  "drain": exact float64 tests on the queued survivors (several windows' worth),
-//           ownership test against the survivor's own window, sorted insertion.
-//  stage 3  "composite": when some lane has enough hits buffered (or nobody can walk on),
-//           every lane composites the hits of its completed windows in order.
+//  W  "walk": every lane that may open a window steps its DDA (at most kWalkSteps steps)
+//     until it finds a window whose culled neighbourhood holds segments; it opens a slot
+//     and publishes the window (cell, local ray start, length) in its shared-memory row.
+//  V  "voxels": the occupied neighbour voxels of all open windows are listed (lane-major,
+//     the reference's z,y,x scan order inside a window); lanes read the voxel headers
+//     item-parallel and a running prefix sum of the counts enumerates the candidates.
+//  C  "candidates": 32 candidates at a time, one per lane whichever ray they belong to:
+//     record load + conservative float32 pre-reject against the owner's window.
+//     Survivors are appended (order-preserving) to a small ring in shared memory.
+//  E  "exact": whenever 32 survivors are queued, one exact float64 test set per lane;
+//     each owner then takes its own results in candidate order (ownership test, gather
+//     ordinals, sorted insertion into its private hit buffer).
+//  S  "composite": when some lane has enough hits buffered (or nobody can walk on), every
+//     lane composites its buffered hits in order; shading is pooled like the exact tests.
 //
-// Hits are therefore composited later than they are found, and a lane may have scanned a
-// few windows past the one in which its ray terminates.  That is invisible in the output:
-// the counters are snapshotted per window (w_tests / w_over) and the snapshot of the
-// terminating hit's window is what gets reported, exactly the reference's count.
-// Per-warp work pool in shared memory (drain and shading stages).
+// Every window opened in a round is completely scanned by the end of that round, so the
+// buffered hits always belong to complete windows.  A lane may have scanned a few windows
+// past the one in which its ray terminates; that is invisible in the output: the counters
+// are snapshotted per window (w_tests / w_over) and the snapshot of the terminating hit's
+// window is what gets reported, exactly the reference's count.
 struct WarpPool {
     double dir[32][3];             // ray directions of the 32 lanes (the origin is shared)
-    double res[32 * kQueue][3];    // drain: t_in of tube / sphere A / sphere B; shading: scale, alpha
-    u32 it_seg[32 * kQueue];       // segment index of the pooled item
-    u16 it_meta[32 * kQueue];      // in: primitive mask or kind | owner lane << 3; out (drain): hit mask
+    union {
+        struct {                       // stages V, C, E
+            double res[kSurvCap][3];   // t_in of tube / sphere A / sphere B
+            u32 it_lin[kItemCap];      // voxel items: linear index, first record, candidate prefix
+            u32 it_base[kItemCap];
+            u32 it_cstart[kItemCap + 1];
+            u16 it_key[kItemCap];      // owner lane << 5 | neighbour bit
+            u32 sv_seg[kSurvCap];      // survivor ring
+            u32 sv_lin[kSurvCap];
+            u16 sv_meta[kSurvCap];     // in: primitive mask 3 | owner << 3; out: hit mask 3 | lid << 3
+            u8 o_first[32], o_last[32];
+        } g;
+        struct {                       // stage S
+            double res[32 * kShadeBatch][2];  // scale, alpha
+            u32 seg[32 * kShadeBatch];
+            u16 meta[32 * kShadeBatch];       // kind | owner lane << 3
+        } s;
+    };
+    float fdir[32][3];             // float32 copies for the pre-reject
+    float wq0[32][3];              // open window of each lane: ray point at t0, window-local
+    float wtlen[32];
+    int wcell[32][3];
 };
 
 template <bool FOOTPRINT>
@@ -245,6 +289,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LVX_MIN_BLOCKS)
 render_kernel(const RenderArgs A) {
     constexpr unsigned FULL = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
     const i64 gw = (i64)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
     const int wpt_x = A.tl.tile_w >> 3, wpt_y = A.tl.tile_h >> 2;
     const int warps_per_tile = wpt_x * wpt_y;
@@ -275,7 +320,6 @@ render_kernel(const RenderArgs A) {
     const bool neighbor = p.neighbor != 0, joints = p.joints != 0;
     const double tube_r = p.tube_r;
     const u32 tmul = joints ? 3u : 1u;
-    const float fdx = (float)ddx, fdy = (float)ddy, fdz = (float)ddz;
     const float reach_pt = (float)tube_r + kRejectMargin;  // joint sphere about an endpoint
     const double cull = tube_r + kCullMargin;
 
@@ -284,17 +328,20 @@ render_kernel(const RenderArgs A) {
     P.dir[lane][0] = ddx;
     P.dir[lane][1] = ddy;
     P.dir[lane][2] = ddz;
+    P.fdir[lane][0] = (float)ddx;
+    P.fdir[lane][1] = (float)ddy;
+    P.fdir[lane][2] = (float)ddz;
     __syncwarp(FULL);
 
     PixelState S;
     S.acc[0] = S.acc[1] = S.acc[2] = S.acc[3] = 0.0;
     S.n_seen = 0;
     S.n_sph = 0;
+    S.seen_bloom = 0;
+    S.sph_bloom = 0;
     // sorted hit buffer: the hits of the windows scanned since the last composite
     double h_t[kHitCap];
     u32 h_lin[kHitCap], h_seg[kHitCap], h_meta[kHitCap];  // meta: lid 5 | kind3 2 | ordinal 10 | slot 4
-    // survivors of the pre-reject awaiting the exact tests; q_mask: primitive mask 3 | slot << 3
-    u32 q_seg[kQueue], q_lin[kQueue], q_mask[kQueue];
     // windows opened since the last composite ("slots")
     double w_t0[kSlots], w_t1[kSlots];
     unsigned long long w_tests[kSlots];  // intersection_tests up to and including the window
@@ -307,17 +354,12 @@ render_kernel(const RenderArgs A) {
     bool alive = active && dda.alive;  // the walk has windows left
     bool done = false;                 // early ray termination reached
 
-    // current window (valid while !win_finished)
-    int cwx = 0, cwy = 0, cwz = 0;
-    float q0x = 0.f, q0y = 0.f, q0z = 0.f, tlen = 0.f;
-    u32 cw_mask = 0, m = 0;            // sub-box occupancy bits: all / still to scan
-    u32 s = 0, cnt = 0, base = 0, lin = 0;
+    bool has_win = false;              // an open window waits to be scanned this round
+    u32 m = 0, cw_mask = 0;            // its occupied sub-box bits: still to list / all
     int cur_slot = 0;
-    bool win_finished = true;
-    // batch state
-    int nh = 0, nq = 0, nw = 0;
-    int d_slot = -1, win_start = 0;    // drain: slot of the last drained survivor, its first hit
-    u32 ord = 0;                       // gather ordinal of the next owned hit of d_slot
+    int nh = 0, nw = 0;
+    int win_start = 0;                 // first hit of the window being scanned
+    u32 ord = 0;                       // gather ordinal of its next owned hit
     bool spilled = false;
     bool have_last = false;            // continuation key of a window that overflowed the buffer
     double last_t = 0.0;
@@ -325,49 +367,14 @@ render_kernel(const RenderArgs A) {
     unsigned long long over_committed = 0;
 
     for (;;) {
-        // ================= stage 1: progress ==================================================
-        for (;;) {
-            const bool blocked_on_hits = win_finished && (nh >= kHitFlush || nw >= kSlots || spilled);
-            const bool go = alive && !done && nq < kQueue && !blocked_on_hits;
-            if (!__any_sync(FULL, go)) break;
-            if (!go) continue;
-            if (s < cnt) {
-                // ---- candidate op: float32 pre-reject in the window-local frame --------------------
-                const u32 i = base + s;
-                s += 1;
-                const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + i));
-                const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + i) + 1);
-                const float fwx = (float)cwx, fwy = (float)cwy, fwz = (float)cwz;
-                const float ax = ra.x - fwx, ay = ra.y - fwy, az = ra.z - fwz;
-                const float bx = rb.x - fwx, by = rb.y - fwy, bz = rb.z - fwz;
-                // the tube AND both joint spheres lie inside the segment's bounding sphere
-                u32 mask = 0;
-                if (may_enter(0.5f * (ax + bx), 0.5f * (ay + by), 0.5f * (az + bz), q0x, q0y, q0z, fdx, fdy,
-                              fdz, tlen, rb.w + reach_pt)) {
-                    mask = 1u;
-                    if (joints) {
-                        if (may_enter(ax, ay, az, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mask |= 2u;
-                        if (may_enter(bx, by, bz, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mask |= 4u;
-                    }
-                }
-                if (mask) {
-                    q_seg[nq] = i;
-                    q_lin[nq] = lin;
-                    q_mask[nq] = mask | ((u32)cur_slot << 3);
-                    nq += 1;
-                }
-                if (s >= cnt && m == 0) win_finished = true;
-            } else if (m != 0) {
-                // ---- voxel op: next occupied voxel of the sub-box, scan order z,y,x ---------------------
-                const int b = __ffs((int)m) - 1;
-                m &= m - 1;
-                const int bz_ = b / 9, by_ = (b - 9 * bz_) / 3, bx_ = b - 9 * bz_ - 3 * by_;
-                lin = (u32)((cwx + bx_ - 1) + rx * ((cwy + by_ - 1) + ry * (cwz + bz_ - 1)));
-                cnt = A.counts[lin];
-                base = A.offsets[lin];
-                s = 0;
-            } else {
-                // ---- window op: DDA step ---------------------------------------------------------------
+        // ================= W: walk to the next window worth scanning ================================
+        if (!__any_sync(FULL, has_win)) {
+#pragma unroll 1
+            for (int it = 0; it < kWalkSteps; ++it) {
+                const bool want = alive && !done && !has_win &&
+                                  !(nh >= kHitFlush || nw >= kSlots || spilled);
+                if (!__any_sync(FULL, want)) break;
+                if (!want) continue;
                 int wx, wy, wz;
                 double t0, t1;
                 if (!dda.next(wx, wy, wz, t0, t1)) {
@@ -379,10 +386,10 @@ render_kernel(const RenderArgs A) {
                 u32 nm, n;
                 if (neighbor) {
                     const i64 pc = ((i64)(wz + 1) * (ry + 2) + (wy + 1)) * (rx + 2) + (wx + 1);
-                    nm = A.nmask[pc];
-                    n = nm ? (u32)A.nsum[pc] : 0u;
+                    nm = __ldg(A.nmask + pc);
+                    n = nm ? (u32)__ldg(A.nsum + pc) : 0u;
                 } else {
-                    n = A.counts[wx + (i64)rx * (wy + (i64)ry * wz)];
+                    n = __ldg(A.counts + (wx + (i64)rx * (wy + (i64)ry * wz)));
                     nm = n ? (1u << 13) : 0u;
                 }
                 if (nm == 0) continue;  // the reference's cheap skip (:793-799)
@@ -408,131 +415,228 @@ render_kernel(const RenderArgs A) {
                 w_t1[cur_slot] = t1;
                 w_tests[cur_slot] = tests;
                 w_over[cur_slot] = 0;
-                cwx = wx;
-                cwy = wy;
-                cwz = wz;
-                q0x = (float)(p0x - (double)wx);  // window-local float32 frame
-                q0y = (float)(p0y - (double)wy);
-                q0z = (float)(p0z - (double)wz);
-                tlen = (float)(t1 - t0);
-                cw_mask = m = nm;
-                s = cnt = 0;
-                win_finished = nm == 0;  // (only possible in the instrumented build)
                 if (FOOTPRINT) w_vox[cur_slot] = (u32)(wx + 1) | ((u32)(wy + 1) << 10) | ((u32)(wz + 1) << 20);
+                if (nm == 0) continue;  // (only possible in the instrumented build)
+                P.wcell[lane][0] = wx;
+                P.wcell[lane][1] = wy;
+                P.wcell[lane][2] = wz;
+                P.wq0[lane][0] = (float)(p0x - (double)wx);  // window-local float32 frame
+                P.wq0[lane][1] = (float)(p0y - (double)wy);
+                P.wq0[lane][2] = (float)(p0z - (double)wz);
+                P.wtlen[lane] = (float)(t1 - t0);
+                cw_mask = m = nm;
+                has_win = true;
+                ord = 0;
+                win_start = nh;
             }
         }
 
-        // ================= stage 2: drain -- exact float64 tests ====================================
-        // The survivors of all 32 rays are pooled in shared memory and dealt out evenly: a lane
-        // tests whatever (ray, segment) pair it is handed, so the few rays that pass through
-        // crowded voxels do not leave the rest of the warp idle.  Results go back to the owner,
-        // which consumes them in candidate order (ownership test, ordinals, sorted insertion).
-        {
-            int off = nq;  // inclusive scan over lanes
+        if (__any_sync(FULL, has_win)) {
+            // ================= V: list the voxels of the open windows, read their headers ============
+            const int nv = has_win ? __popc(m) : 0;
+            int voff = nv;  // inclusive scan over lanes
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const int t = __shfl_up_sync(FULL, off, o);
-                if (lane >= o) off += t;
+                const int t = __shfl_up_sync(FULL, voff, o);
+                if (lane >= o) voff += t;
             }
-            const int total = __shfl_sync(FULL, off, 31);
-            off -= nq;
-            for (int qi = 0; qi < nq; ++qi) {
-                P.it_seg[off + qi] = q_seg[qi];
-                P.it_meta[off + qi] = (u16)((q_mask[qi] & 7u) | ((u32)lane << 3));
-            }
-            __syncwarp(FULL);
-            for (int idx = lane; idx < total; idx += 32) {
-                const u32 i = P.it_seg[idx], im = P.it_meta[idx];
-                const int owner = (int)(im >> 3);
-                const double rdx = P.dir[owner][0], rdy = P.dir[owner][1], rdz = P.dir[owner][2];
-                const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + i));
-                const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + i) + 1);
-                u32 hits = 0;
-                LvxHit h;
-                if ((im & 1u) && lvx_tube_f32axis(ox, oy, oz, rdx, rdy, rdz, ra.x, ra.y, ra.z, rb.x, rb.y, rb.z,
-                                                  tube_r, h)) {
-                    hits |= 1u;
-                    P.res[idx][0] = h.t_in;
-                }
-                if ((im & 2u) && lvx_sphere<false>(ox, oy, oz, rdx, rdy, rdz, (double)ra.x, (double)ra.y,
-                                                   (double)ra.z, tube_r, h)) {
-                    hits |= 2u;
-                    P.res[idx][1] = h.t_in;
-                }
-                if ((im & 4u) && lvx_sphere<false>(ox, oy, oz, rdx, rdy, rdz, (double)rb.x, (double)rb.y,
-                                                   (double)rb.z, tube_r, h)) {
-                    hits |= 4u;
-                    P.res[idx][2] = h.t_in;
-                }
-                P.it_meta[idx] = (u16)hits;
+            // lanes are admitted in lane order while their voxels fit (the first always does)
+            const bool admitted = has_win && voff <= kItemCap;
+            const unsigned adm = __ballot_sync(FULL, admitted);
+            const int total_v = __shfl_sync(FULL, voff, 31 - __clz((int)adm));
+            voff -= nv;
+            if (admitted) {
+                int kk = 0;
+                for (u32 mm = m; mm; mm &= mm - 1, ++kk)
+                    P.g.it_key[voff + kk] = (u16)(((u32)lane << 5) | (u32)(__ffs((int)mm) - 1));
+                has_win = false;
             }
             __syncwarp(FULL);
-            for (int qi = 0; qi < nq; ++qi) {
-                const u32 hits = P.it_meta[off + qi];
-                if (hits == 0) continue;
-                const u32 i = q_seg[qi], qlin = q_lin[qi];
-                const int slot = (int)(q_mask[qi] >> 3);
-                if (slot != d_slot) {
-                    d_slot = slot;
-                    ord = 0;
-                    win_start = nh;
+            u32 running = 0;
+            for (int i0 = 0; i0 < total_v; i0 += 32) {
+                const int i = i0 + lane;
+                u32 cnt = 0;
+                if (i < total_v) {
+                    const u32 key = P.g.it_key[i];
+                    const int owner = (int)(key >> 5), b = (int)(key & 31u);
+                    const int bz_ = b / 9, by_ = (b - 9 * bz_) / 3, bx_ = b - 9 * bz_ - 3 * by_;
+                    const u32 lin = (u32)((P.wcell[owner][0] + bx_ - 1) +
+                                          rx * ((P.wcell[owner][1] + by_ - 1) + ry * (P.wcell[owner][2] + bz_ - 1)));
+                    cnt = __ldg(A.counts + lin);
+                    P.g.it_lin[i] = lin;
+                    P.g.it_base[i] = __ldg(A.offsets + lin);
                 }
-                const double t0 = w_t0[slot], t1 = w_t1[slot];
-                const u32 lid = (__float_as_uint(__ldg(reinterpret_cast<const float *>(A.rec + i) + 3)) >> 8) & 31u;
-#pragma unroll 1
-                for (int kind3 = 0; kind3 < 3; ++kind3) {
-                    if (!(hits & (1u << kind3))) continue;
-                    const double t_in = P.res[off + qi][kind3];
-                    if (!(t0 <= t_in && t_in < t1)) continue;  // ownership
-                    const u32 my_ord = ord++;
-                    if (my_ord >= (u32)LVX_MAX_WINDOW_HITS) {
-                        // the reference drops hits past its 1024-entry window buffer
-                        if (!have_last) w_over[slot] += 1;
-                        continue;
-                    }
-                    const u32 meta = lid | ((u32)kind3 << 5) | (my_ord << 7) | ((u32)slot << 17);
-                    if (have_last && !key_before(last_t, last_lin, last_meta, t_in, qlin, meta))
-                        continue;  // composited in an earlier pass over this window
-                    int pos;
-                    if (nh < kHitCap && !spilled) {
-                        pos = nh++;
-                    } else {
-                        // keep the smallest keys of this window and redo the rest in another pass.
-                        // Once a hit has been dropped nothing larger than the buffer's last key may
-                        // be accepted (even if a composite of earlier windows frees space), or the
-                        // pass order would break.
-                        spilled = true;
-                        if (!key_before(t_in, qlin, meta, h_t[nh - 1], h_lin[nh - 1], h_meta[nh - 1])) continue;
-                        pos = nh - 1;
-                    }
-                    while (pos > win_start &&
-                           key_before(t_in, qlin, meta, h_t[pos - 1], h_lin[pos - 1], h_meta[pos - 1])) {
-                        h_t[pos] = h_t[pos - 1];
-                        h_lin[pos] = h_lin[pos - 1];
-                        h_seg[pos] = h_seg[pos - 1];
-                        h_meta[pos] = h_meta[pos - 1];
-                        --pos;
-                    }
-                    h_t[pos] = t_in;
-                    h_lin[pos] = qlin;
-                    h_seg[pos] = i;
-                    h_meta[pos] = meta;
+                u32 inc = cnt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const u32 t = __shfl_up_sync(FULL, inc, o);
+                    if (lane >= o) inc += t;
                 }
+                if (i < total_v) P.g.it_cstart[i] = running + inc - cnt;
+                running += __shfl_sync(FULL, inc, 31);
             }
+            if (lane == 0) P.g.it_cstart[total_v] = running;
+            P.g.o_first[lane] = 255;
             __syncwarp(FULL);
-        }
-        nq = 0;
+            const int total_c = (int)running;
 
-        // ================= stage 3: composite, _kernels.py:898-914 ======================================
+            // ================= C + E: pre-reject 32 candidates at a time, exact tests in batches ======
+            int sv_head = 0, nsv = 0;  // survivor ring (warp-uniform)
+            for (int g0 = 0; g0 < total_c || nsv > 0; g0 += 32) {
+                if (g0 < total_c) {
+                    const int g = g0 + lane;
+                    u32 mask = 0, seg = 0, key = 0, lin = 0;
+                    if (g < total_c) {
+                        int lo = 0, hi = total_v;  // largest item with cstart <= g
+                        while (hi - lo > 1) {
+                            const int mid = (lo + hi) >> 1;
+                            if (P.g.it_cstart[mid] <= (u32)g) lo = mid;
+                            else hi = mid;
+                        }
+                        seg = P.g.it_base[lo] + ((u32)g - P.g.it_cstart[lo]);
+                        key = P.g.it_key[lo];
+                        lin = P.g.it_lin[lo];
+                        const int owner = (int)(key >> 5);
+                        const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + seg));
+                        const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + seg) + 1);
+                        const float fwx = (float)P.wcell[owner][0], fwy = (float)P.wcell[owner][1],
+                                    fwz = (float)P.wcell[owner][2];
+                        const float q0x = P.wq0[owner][0], q0y = P.wq0[owner][1], q0z = P.wq0[owner][2];
+                        const float fdx = P.fdir[owner][0], fdy = P.fdir[owner][1], fdz = P.fdir[owner][2];
+                        const float tlen = P.wtlen[owner];
+                        const float ax = ra.x - fwx, ay = ra.y - fwy, az = ra.z - fwz;
+                        const float bx = rb.x - fwx, by = rb.y - fwy, bz = rb.z - fwz;
+                        // the tube AND both joint spheres lie inside the segment's bounding sphere
+                        if (may_enter(0.5f * (ax + bx), 0.5f * (ay + by), 0.5f * (az + bz), q0x, q0y, q0z, fdx,
+                                      fdy, fdz, tlen, rb.w + reach_pt)) {
+                            mask = 1u;
+                            if (joints) {
+                                if (may_enter(ax, ay, az, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mask |= 2u;
+                                if (may_enter(bx, by, bz, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mask |= 4u;
+                            }
+                        }
+                    }
+                    const unsigned sb = __ballot_sync(FULL, mask != 0);
+                    if (mask) {
+                        const int pos = (sv_head + nsv + __popc(sb & lt_mask)) & (kSurvCap - 1);
+                        P.g.sv_seg[pos] = seg;
+                        P.g.sv_lin[pos] = lin;
+                        P.g.sv_meta[pos] = (u16)(mask | ((key >> 5) << 3));
+                    }
+                    nsv += __popc(sb);
+                    __syncwarp(FULL);
+                }
+                if (nsv < 32 && g0 + 32 < total_c) continue;
+                if (nsv == 0) break;
+                // ---- E: exact float64 tests, one survivor per lane -------------------------------------
+                const int nb = min(nsv, 32);
+                int owner = -1;
+                if (lane < nb) {
+                    const int e = (sv_head + lane) & (kSurvCap - 1);
+                    const u32 i = P.g.sv_seg[e], im = P.g.sv_meta[e];
+                    owner = (int)(im >> 3);
+                    const double rdx = P.dir[owner][0], rdy = P.dir[owner][1], rdz = P.dir[owner][2];
+                    const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + i));
+                    const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + i) + 1);
+                    u32 hits = 0;
+                    LvxHit h;
+                    if ((im & 1u) && lvx_tube_f32axis(ox, oy, oz, rdx, rdy, rdz, ra.x, ra.y, ra.z, rb.x, rb.y, rb.z,
+                                                      tube_r, h)) {
+                        hits |= 1u;
+                        P.g.res[e][0] = h.t_in;
+                    }
+                    if ((im & 2u) && lvx_sphere<false>(ox, oy, oz, rdx, rdy, rdz, (double)ra.x, (double)ra.y,
+                                                       (double)ra.z, tube_r, h)) {
+                        hits |= 2u;
+                        P.g.res[e][1] = h.t_in;
+                    }
+                    if ((im & 4u) && lvx_sphere<false>(ox, oy, oz, rdx, rdy, rdz, (double)rb.x, (double)rb.y,
+                                                       (double)rb.z, tube_r, h)) {
+                        hits |= 4u;
+                        P.g.res[e][2] = h.t_in;
+                    }
+                    P.g.sv_meta[e] = (u16)(hits | (((__float_as_uint(ra.w) >> 8) & 31u) << 3));
+                }
+                // survivors are queued in lane-major owner order: every owner's share is contiguous
+                {
+                    const int prev = __shfl_up_sync(FULL, owner, 1), next = __shfl_down_sync(FULL, owner, 1);
+                    if (lane < nb) {
+                        if (lane == 0 || prev != owner) P.g.o_first[owner] = (u8)lane;
+                        if (lane == nb - 1 || next != owner) P.g.o_last[owner] = (u8)lane;
+                    }
+                }
+                __syncwarp(FULL);
+                // ---- each owner takes its results in candidate order ----------------------------------
+                {
+                    const int first = P.g.o_first[lane];
+                    const int last = first == 255 ? -1 : (int)P.g.o_last[lane];
+                    const double t0 = w_t0[cur_slot], t1 = w_t1[cur_slot];
+                    for (int j = first == 255 ? 0 : first; j <= last; ++j) {
+                        const int e = (sv_head + j) & (kSurvCap - 1);
+                        const u32 om = P.g.sv_meta[e];
+                        const u32 hits = om & 7u;
+                        if (hits == 0) continue;
+                        const u32 i = P.g.sv_seg[e], qlin = P.g.sv_lin[e], lid = (om >> 3) & 31u;
+#pragma unroll 1
+                        for (int kind3 = 0; kind3 < 3; ++kind3) {
+                            if (!(hits & (1u << kind3))) continue;
+                            const double t_in = P.g.res[e][kind3];
+                            if (!(t0 <= t_in && t_in < t1)) continue;  // ownership
+                            const u32 my_ord = ord++;
+                            if (my_ord >= (u32)LVX_MAX_WINDOW_HITS) {
+                                // the reference drops hits past its 1024-entry window buffer
+                                if (!have_last) w_over[cur_slot] += 1;
+                                continue;
+                            }
+                            const u32 meta = lid | ((u32)kind3 << 5) | (my_ord << 7) | ((u32)cur_slot << 17);
+                            if (have_last && !key_before(last_t, last_lin, last_meta, t_in, qlin, meta))
+                                continue;  // composited in an earlier pass over this window
+                            int pos;
+                            if (nh < kHitCap && !spilled) {
+                                pos = nh++;
+                            } else {
+                                // keep the smallest keys of this window and redo the rest in another
+                                // pass.  Once a hit has been dropped nothing larger than the buffer's
+                                // last key may be accepted, or the pass order would break.
+                                spilled = true;
+                                if (!key_before(t_in, qlin, meta, h_t[nh - 1], h_lin[nh - 1], h_meta[nh - 1]))
+                                    continue;
+                                pos = nh - 1;
+                            }
+                            while (pos > win_start &&
+                                   key_before(t_in, qlin, meta, h_t[pos - 1], h_lin[pos - 1], h_meta[pos - 1])) {
+                                h_t[pos] = h_t[pos - 1];
+                                h_lin[pos] = h_lin[pos - 1];
+                                h_seg[pos] = h_seg[pos - 1];
+                                h_meta[pos] = h_meta[pos - 1];
+                                --pos;
+                            }
+                            h_t[pos] = t_in;
+                            h_lin[pos] = qlin;
+                            h_seg[pos] = i;
+                            h_meta[pos] = meta;
+                        }
+                    }
+                }
+                __syncwarp(FULL);
+                P.g.o_first[lane] = 255;
+                sv_head = (sv_head + nb) & (kSurvCap - 1);
+                nsv -= nb;
+                __syncwarp(FULL);
+            }
+            // lanes that did not fit this round keep their window and go first in the next one
+            if (__any_sync(FULL, has_win)) continue;
+        }
+
+        // ================= S: composite, _kernels.py:898-914 ============================================
         const bool walker = alive && !done;
-        const bool blocked = walker && win_finished && (nh >= kHitFlush || nw >= kSlots || spilled);
+        const bool blocked = walker && (nh >= kHitFlush || nw >= kSlots || spilled);
         const bool any_walker = __any_sync(FULL, walker);
         if (__any_sync(FULL, blocked) || !any_walker) {
-            // hits of completed windows only: an unfinished window may still produce smaller keys
-            const int n_comp = (win_finished || d_slot != cur_slot) ? nh : win_start;
-            // Shading is pooled like the exact tests: up to kShadeBatch hits per ray and round are
-            // listed in shared memory, every lane recomputes one hit (t_out, normal) and its
-            // state-free shading terms, then each ray's own lane applies them in order.
+            const int n_comp = nh;  // every buffered hit belongs to a completely scanned window
+            // Up to kShadeBatch hits per ray and round are listed in shared memory, every lane
+            // recomputes one hit (t_out, normal) and its state-free shading terms, then each ray's
+            // own lane applies them in order.
             int q = 0;
             bool comp = !done && n_comp > 0;
             while (__any_sync(FULL, comp)) {
@@ -546,12 +650,12 @@ render_kernel(const RenderArgs A) {
                 const int total = __shfl_sync(FULL, off, 31);
                 off -= nb;
                 for (int j = 0; j < nb; ++j) {
-                    P.it_seg[off + j] = h_seg[q + j];
-                    P.it_meta[off + j] = (u16)(meta_kind3(h_meta[q + j]) | ((u32)lane << 3));
+                    P.s.seg[off + j] = h_seg[q + j];
+                    P.s.meta[off + j] = (u16)(meta_kind3(h_meta[q + j]) | ((u32)lane << 3));
                 }
                 __syncwarp(FULL);
                 for (int idx = lane; idx < total; idx += 32) {
-                    const u32 i = P.it_seg[idx], im = P.it_meta[idx];
+                    const u32 i = P.s.seg[idx], im = P.s.meta[idx];
                     const int owner = (int)(im >> 3);
                     const u32 kind3 = im & 3u;
                     const double rdx = P.dir[owner][0], rdy = P.dir[owner][1], rdz = P.dir[owner][2];
@@ -567,8 +671,8 @@ render_kernel(const RenderArgs A) {
                     }
                     double scale, alpha;
                     shade_hit(A, ox, oy, oz, rdx, rdy, rdz, h, __float_as_uint(ra.w) & 0xFFu, scale, alpha);
-                    P.res[idx][0] = scale;
-                    P.res[idx][1] = alpha;
+                    P.s.res[idx][0] = scale;
+                    P.s.res[idx][1] = alpha;
                 }
                 __syncwarp(FULL);
                 for (int j = 0; j < nb; ++j) {
@@ -586,7 +690,7 @@ render_kernel(const RenderArgs A) {
                         cy = rb.y;
                         cz = rb.z;
                     }
-                    const double a_now = accumulate_hit(S, A, P.res[off + j][0], P.res[off + j][1], h_lin[q],
+                    const double a_now = accumulate_hit(S, A, P.s.res[off + j][0], P.s.res[off + j][1], h_lin[q],
                                                         meta_lid(meta), __float_as_uint(ra.w) & 0xFFu,
                                                         kind3 != 0, cx, cy, cz);
                     if (a_now >= p.tau) {
@@ -606,15 +710,13 @@ render_kernel(const RenderArgs A) {
                 __syncwarp(FULL);
             }
             if (!done) {
-                // commit the composited windows, keep the unfinished one as slot 0
-                const bool keep = !win_finished;
-                const int n_commit = keep ? cur_slot : nw;
-                for (int j = 0; j < n_commit; ++j) over_committed += w_over[j];
+                // commit the composited windows
+                for (int j = 0; j < nw; ++j) over_committed += w_over[j];
                 if (FOOTPRINT)
-                    for (int j = 0; j < n_commit; ++j) mark_footprint(A, w_vox[j], neighbor);
-                if (spilled && win_finished) {
-                    // the buffer held only the smallest keys of the last window: scan it
-                    // again, continuing after the last composited key
+                    for (int j = 0; j < nw; ++j) mark_footprint(A, w_vox[j], neighbor);
+                if (spilled) {
+                    // the buffer held only the smallest keys of the last window: scan it again
+                    // (its row in P.w* is still in place), continuing after the last composited key
                     have_last = true;
                     last_t = h_t[nh - 1];
                     last_lin = h_lin[nh - 1];
@@ -626,38 +728,18 @@ render_kernel(const RenderArgs A) {
                     if (FOOTPRINT) w_vox[0] = w_vox[cur_slot];
                     cur_slot = 0;
                     nw = 1;
-                    nh = 0;
                     m = cw_mask;
-                    s = cnt = 0;
-                    win_finished = false;
-                    spilled = false;
-                    d_slot = -1;
-                } else if (keep) {
-                    const int rest = nh - n_comp;
-                    for (int j = 0; j < rest; ++j) {
-                        h_t[j] = h_t[n_comp + j];
-                        h_lin[j] = h_lin[n_comp + j];
-                        h_seg[j] = h_seg[n_comp + j];
-                        h_meta[j] = h_meta[n_comp + j] & 0x1FFFFu;  // -> slot 0
-                    }
-                    w_t0[0] = w_t0[cur_slot];
-                    w_t1[0] = w_t1[cur_slot];
-                    w_tests[0] = w_tests[cur_slot];
-                    w_over[0] = w_over[cur_slot];
-                    if (FOOTPRINT) w_vox[0] = w_vox[cur_slot];
-                    d_slot = (d_slot == cur_slot) ? 0 : -1;
-                    cur_slot = 0;
-                    nw = 1;
-                    nh = rest;
+                    has_win = true;
+                    ord = 0;
                     win_start = 0;
+                    spilled = false;
                 } else {
                     nw = 0;
-                    nh = 0;
-                    d_slot = -1;
                 }
+                nh = 0;
             }
         }
-        if (!any_walker) break;
+        if (!any_walker && !__any_sync(FULL, has_win)) break;
     }
     if (!done) overflow = over_committed;
 

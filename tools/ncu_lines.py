@@ -39,14 +39,17 @@ def find(pat):
     for i, l in enumerate(src):
         if pat in l: return i + 1
     return 0
-STAGES = [('stream_hit', find('__device__ __noinline__ double stream_hit'), find('// Conservative float32 test')),
+STAGES = [('accumulate_hit (dedup+blend)', find('__device__ __forceinline__ double accumulate_hit'), find('// Conservative float32 test')),
+          ('shade_hit', find('__device__ __forceinline__ void shade_hit'), find('// Returns the accumulated alpha')),
           ('may_enter', find('// Conservative float32 test'), find('// Instrumentation (lvx_render_footprint)')),
-          ('progress: candidate op', find('---- candidate op'), find('---- voxel op')),
-          ('progress: voxel op', find('---- voxel op'), find('---- window op')),
-          ('progress: window op', find('---- window op'), find('stage 2: drain')),
-          ('drain', find('stage 2: drain'), find('stage 3: composite')),
-          ('composite', find('stage 3: composite'), find('// tail: a terminated ray')),
-          ('progress loop ctl', find('stage 1: progress'), find('---- candidate op'))]
+          ('prologue (ray setup)', find('render_kernel(const RenderArgs A) {'), find('================= W:')),
+          ('W walk', find('================= W:'), find('================= V:')),
+          ('V voxel headers', find('================= V:'), find('================= C + E')),
+          ('C pre-reject', find('================= C + E'), find('---- E: exact')),
+          ('E exact-test driver', find('---- E: exact'), find('---- each owner takes')),
+          ('owner insert', find('---- each owner takes'), find('================= S:')),
+          ('S composite', find('================= S:'), find('// tail: a terminated ray')),
+          ('tail+output', find('// tail: a terminated ray'), find('__global__ void __launch_bounds__(256)'))]
 agg = collections.defaultdict(lambda: [0, 0, 0])
 for d in data:
     a = agg[stage(d)]; a[0] += d[0]; a[1] += d[1]; a[2] += d[2]
