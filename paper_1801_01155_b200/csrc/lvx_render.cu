@@ -36,7 +36,7 @@ namespace {
 
 // tuning knobs (overridable with -D for experiments)
 #ifndef LVX_HIT_FLUSH
-#define LVX_HIT_FLUSH 10
+#define LVX_HIT_FLUSH 20
 #endif
 #ifndef LVX_SHADE_BATCH
 #define LVX_SHADE_BATCH 8
@@ -282,6 +282,7 @@ struct WarpPool {
     float wq0[32][3];              // open window of each lane: ray point at t0, window-local
     float wtlen[32];
     int wcell[32][3];
+    double wt[32][2];              // its parameter range [t0, t1)
 };
 
 template <bool FOOTPRINT>
@@ -343,7 +344,6 @@ render_kernel(const RenderArgs A) {
     double h_t[kHitCap];
     u32 h_lin[kHitCap], h_seg[kHitCap], h_meta[kHitCap];  // meta: lid 5 | kind3 2 | ordinal 10 | slot 4
     // windows opened since the last composite ("slots")
-    double w_t0[kSlots], w_t1[kSlots];
     unsigned long long w_tests[kSlots];  // intersection_tests up to and including the window
     u32 w_over[kSlots];                  // window_overflow of the window
     u32 w_vox[FOOTPRINT ? kSlots : 1];   // instrumentation: packed window voxel (+1 per axis)
@@ -411,8 +411,6 @@ render_kernel(const RenderArgs A) {
                 if (nm == 0 && !FOOTPRINT) continue;
                 // open a slot for the window
                 cur_slot = nw++;
-                w_t0[cur_slot] = t0;
-                w_t1[cur_slot] = t1;
                 w_tests[cur_slot] = tests;
                 w_over[cur_slot] = 0;
                 if (FOOTPRINT) w_vox[cur_slot] = (u32)(wx + 1) | ((u32)(wy + 1) << 10) | ((u32)(wz + 1) << 20);
@@ -424,6 +422,8 @@ render_kernel(const RenderArgs A) {
                 P.wq0[lane][1] = (float)(p0y - (double)wy);
                 P.wq0[lane][2] = (float)(p0z - (double)wz);
                 P.wtlen[lane] = (float)(t1 - t0);
+                P.wt[lane][0] = t0;
+                P.wt[lane][1] = t1;
                 cw_mask = m = nm;
                 has_win = true;
                 ord = 0;
@@ -482,20 +482,27 @@ render_kernel(const RenderArgs A) {
 
             // ================= C + E: pre-reject 32 candidates at a time, exact tests in batches ======
             int sv_head = 0, nsv = 0;  // survivor ring (warp-uniform)
+            int it_next = 0;           // first item that starts at or after the current chunk
             for (int g0 = 0; g0 < total_c || nsv > 0; g0 += 32) {
                 if (g0 < total_c) {
                     const int g = g0 + lane;
                     u32 mask = 0, seg = 0, key = 0, lin = 0;
-                    if (g < total_c) {
-                        int lo = 0, hi = total_v;  // largest item with cstart <= g
-                        while (hi - lo > 1) {
-                            const int mid = (lo + hi) >> 1;
-                            if (P.g.it_cstart[mid] <= (u32)g) lo = mid;
-                            else hi = mid;
+                    // items whose first candidate falls into this chunk (at most 32: every item holds
+                    // at least one) flag that position; the item of candidate g is the last one
+                    // starting at or before g
+                    {
+                        const int ii = it_next + lane;
+                        const u32 cs = ii < total_v ? P.g.it_cstart[ii] : 0xFFFFFFFFu;
+                        const u32 starts = __reduce_or_sync(FULL, cs < (u32)(g0 + 32) ? 1u << (cs - (u32)g0) : 0u);
+                        const int item = it_next - 1 + __popc(starts & (lt_mask | (1u << lane)));
+                        it_next += __popc(starts);
+                        if (g < total_c) {
+                            seg = P.g.it_base[item] + ((u32)g - P.g.it_cstart[item]);
+                            key = P.g.it_key[item];
+                            lin = P.g.it_lin[item];
                         }
-                        seg = P.g.it_base[lo] + ((u32)g - P.g.it_cstart[lo]);
-                        key = P.g.it_key[lo];
-                        lin = P.g.it_lin[lo];
+                    }
+                    if (g < total_c) {
                         const int owner = (int)(key >> 5);
                         const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + seg));
                         const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + seg) + 1);
@@ -536,22 +543,23 @@ render_kernel(const RenderArgs A) {
                     const u32 i = P.g.sv_seg[e], im = P.g.sv_meta[e];
                     owner = (int)(im >> 3);
                     const double rdx = P.dir[owner][0], rdy = P.dir[owner][1], rdz = P.dir[owner][2];
+                    const double t0 = P.wt[owner][0], t1 = P.wt[owner][1];
                     const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + i));
                     const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + i) + 1);
-                    u32 hits = 0;
+                    u32 hits = 0;  // hits the owner's window OWNS: t0 <= t_in < t1 (:838, :858, :878)
                     LvxHit h;
                     if ((im & 1u) && lvx_tube_f32axis(ox, oy, oz, rdx, rdy, rdz, ra.x, ra.y, ra.z, rb.x, rb.y, rb.z,
-                                                      tube_r, h)) {
+                                                      tube_r, h) && t0 <= h.t_in && h.t_in < t1) {
                         hits |= 1u;
                         P.g.res[e][0] = h.t_in;
                     }
                     if ((im & 2u) && lvx_sphere<false>(ox, oy, oz, rdx, rdy, rdz, (double)ra.x, (double)ra.y,
-                                                       (double)ra.z, tube_r, h)) {
+                                                       (double)ra.z, tube_r, h) && t0 <= h.t_in && h.t_in < t1) {
                         hits |= 2u;
                         P.g.res[e][1] = h.t_in;
                     }
                     if ((im & 4u) && lvx_sphere<false>(ox, oy, oz, rdx, rdy, rdz, (double)rb.x, (double)rb.y,
-                                                       (double)rb.z, tube_r, h)) {
+                                                       (double)rb.z, tube_r, h) && t0 <= h.t_in && h.t_in < t1) {
                         hits |= 4u;
                         P.g.res[e][2] = h.t_in;
                     }
@@ -570,7 +578,6 @@ render_kernel(const RenderArgs A) {
                 {
                     const int first = P.g.o_first[lane];
                     const int last = first == 255 ? -1 : (int)P.g.o_last[lane];
-                    const double t0 = w_t0[cur_slot], t1 = w_t1[cur_slot];
                     for (int j = first == 255 ? 0 : first; j <= last; ++j) {
                         const int e = (sv_head + j) & (kSurvCap - 1);
                         const u32 om = P.g.sv_meta[e];
@@ -581,7 +588,6 @@ render_kernel(const RenderArgs A) {
                         for (int kind3 = 0; kind3 < 3; ++kind3) {
                             if (!(hits & (1u << kind3))) continue;
                             const double t_in = P.g.res[e][kind3];
-                            if (!(t0 <= t_in && t_in < t1)) continue;  // ownership
                             const u32 my_ord = ord++;
                             if (my_ord >= (u32)LVX_MAX_WINDOW_HITS) {
                                 // the reference drops hits past its 1024-entry window buffer
@@ -721,8 +727,6 @@ render_kernel(const RenderArgs A) {
                     last_t = h_t[nh - 1];
                     last_lin = h_lin[nh - 1];
                     last_meta = h_meta[nh - 1] & 0x1FFFFu;  // slot bits are not part of the order
-                    w_t0[0] = w_t0[cur_slot];
-                    w_t1[0] = w_t1[cur_slot];
                     w_tests[0] = w_tests[cur_slot];
                     w_over[0] = 0;  // its overflow was committed above; later passes do not recount
                     if (FOOTPRINT) w_vox[0] = w_vox[cur_slot];

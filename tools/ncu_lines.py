@@ -4,11 +4,16 @@ import csv, subprocess, sys
 rep = sys.argv[1]; top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass,cuda"], capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
-cur = None; data = []; hdr = None
+cur = None; data = []; hdr = None; sass = []; cur_line = None
 for r in rows:
+    if len(r) > 8 and r[0] == '' and r[2].startswith('0x'):
+        try: sass.append((cur, cur_line, int(r[7]), int(r[6])))
+        except Exception: pass
+        continue
     if len(r) == 2 and r[0] == 'File Path': cur = r[1].split('/')[-1]; continue
     if len(r) > 5 and r[0] == 'Line No': hdr = r; continue
     if hdr and len(r) >= 10 and r[0] != '':
+        cur_line = r[0]
         try: data.append((int(r[6]), int(r[7]), int(r[8]), cur, r[0], r[1]))
         except Exception: pass
 tot = sum(d[0] for d in data); toti = sum(d[1] for d in data); tott = sum(d[2] for d in data)
@@ -56,3 +61,14 @@ for d in data:
 print()
 for k, a in sorted(agg.items(), key=lambda kv: -kv[1][0]):
     print(f"{k:32s} {100*a[0]/tot:5.1f}% samples {100*a[1]/toti:5.1f}% warp-inst {100*a[2]/tott:5.1f}% thread-inst  thr/inst {a[2]/max(a[1],1):5.1f}")
+
+# static size of the code each stage actually runs (SASS instructions executed > 1e5 times)
+hot = collections.Counter(); allc = collections.Counter()
+for f, ln, ex, smp in sass:
+    k = stage((0, 0, 0, f, ln, ''))
+    allc[k] += 1
+    if ex > 1e5: hot[k] += 1
+print()
+print("hot code (executed > 1e5 times): %.1f KB of %.1f KB" % (sum(hot.values()) * 16 / 1024, sum(allc.values()) * 16 / 1024))
+for k, v in sorted(hot.items(), key=lambda kv: -kv[1]):
+    print(f"  {k:32s} {v:5d} instr {v*16/1024:5.1f} KB   (all {allc[k]})")
