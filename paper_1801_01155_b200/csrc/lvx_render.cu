@@ -516,7 +516,13 @@ render_kernel(const RenderArgs A) {
                         // the tube AND both joint spheres lie inside the segment's bounding sphere
                         if (may_enter(0.5f * (ax + bx), 0.5f * (ay + by), 0.5f * (az + bz), q0x, q0y, q0z, fdx,
                                       fdy, fdz, tlen, rb.w + reach_pt)) {
-                            mask = 1u;
+                            // the tube's entry point lies on the ray within tube_r of the segment's
+                            // axis line, so the two lines pass within tube_r of each other:
+                            // |w . (d x u)| <= reach |d x u|  (absolute slack >> float32 rounding)
+                            const float ux = bx - ax, uy = by - ay, uz = bz - az;
+                            const float nx = fdy * uz - fdz * uy, ny = fdz * ux - fdx * uz, nz = fdx * uy - fdy * ux;
+                            const float wn = (ax - q0x) * nx + (ay - q0y) * ny + (az - q0z) * nz;
+                            if (wn * wn <= reach_pt * reach_pt * (nx * nx + ny * ny + nz * nz) + 1e-6f) mask = 1u;
                             if (joints) {
                                 if (may_enter(ax, ay, az, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mask |= 2u;
                                 if (may_enter(bx, by, bz, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mask |= 4u;
@@ -574,54 +580,59 @@ render_kernel(const RenderArgs A) {
                     }
                 }
                 __syncwarp(FULL);
-                // ---- each owner takes its results in candidate order ----------------------------------
+                // ---- each owner takes its owned hits in candidate order ------------------------------
+                // (one hit per lane and iteration, so the insertions of different rays run side by side)
                 {
                     const int first = P.g.o_first[lane];
                     const int last = first == 255 ? -1 : (int)P.g.o_last[lane];
-                    for (int j = first == 255 ? 0 : first; j <= last; ++j) {
-                        const int e = (sv_head + j) & (kSurvCap - 1);
-                        const u32 om = P.g.sv_meta[e];
-                        const u32 hits = om & 7u;
-                        if (hits == 0) continue;
-                        const u32 i = P.g.sv_seg[e], qlin = P.g.sv_lin[e], lid = (om >> 3) & 31u;
-#pragma unroll 1
-                        for (int kind3 = 0; kind3 < 3; ++kind3) {
-                            if (!(hits & (1u << kind3))) continue;
-                            const double t_in = P.g.res[e][kind3];
-                            const u32 my_ord = ord++;
-                            if (my_ord >= (u32)LVX_MAX_WINDOW_HITS) {
-                                // the reference drops hits past its 1024-entry window buffer
-                                if (!have_last) w_over[cur_slot] += 1;
-                                continue;
-                            }
-                            const u32 meta = lid | ((u32)kind3 << 5) | (my_ord << 7) | ((u32)cur_slot << 17);
-                            if (have_last && !key_before(last_t, last_lin, last_meta, t_in, qlin, meta))
-                                continue;  // composited in an earlier pass over this window
-                            int pos;
-                            if (nh < kHitCap && !spilled) {
-                                pos = nh++;
-                            } else {
-                                // keep the smallest keys of this window and redo the rest in another
-                                // pass.  Once a hit has been dropped nothing larger than the buffer's
-                                // last key may be accepted, or the pass order would break.
-                                spilled = true;
-                                if (!key_before(t_in, qlin, meta, h_t[nh - 1], h_lin[nh - 1], h_meta[nh - 1]))
-                                    continue;
-                                pos = nh - 1;
-                            }
-                            while (pos > win_start &&
-                                   key_before(t_in, qlin, meta, h_t[pos - 1], h_lin[pos - 1], h_meta[pos - 1])) {
-                                h_t[pos] = h_t[pos - 1];
-                                h_lin[pos] = h_lin[pos - 1];
-                                h_seg[pos] = h_seg[pos - 1];
-                                h_meta[pos] = h_meta[pos - 1];
-                                --pos;
-                            }
-                            h_t[pos] = t_in;
-                            h_lin[pos] = qlin;
-                            h_seg[pos] = i;
-                            h_meta[pos] = meta;
+                    int j = first == 255 ? 0 : first;
+                    u32 hbits = 0, om = 0;
+                    int e = 0;
+                    for (;;) {
+                        while (hbits == 0 && j <= last) {
+                            e = (sv_head + j) & (kSurvCap - 1);
+                            om = P.g.sv_meta[e];
+                            hbits = om & 7u;
+                            ++j;
                         }
+                        if (!__any_sync(FULL, hbits != 0)) break;
+                        if (hbits == 0) continue;
+                        const u32 kind3 = (u32)(__ffs((int)hbits) - 1);
+                        hbits &= hbits - 1;
+                        const double t_in = P.g.res[e][kind3];
+                        const u32 my_ord = ord++;
+                        if (my_ord >= (u32)LVX_MAX_WINDOW_HITS) {
+                            // the reference drops hits past its 1024-entry window buffer
+                            if (!have_last) w_over[cur_slot] += 1;
+                            continue;
+                        }
+                        const u32 qlin = P.g.sv_lin[e];
+                        const u32 meta = ((om >> 3) & 31u) | (kind3 << 5) | (my_ord << 7) | ((u32)cur_slot << 17);
+                        if (have_last && !key_before(last_t, last_lin, last_meta, t_in, qlin, meta))
+                            continue;  // composited in an earlier pass over this window
+                        int pos;
+                        if (nh < kHitCap && !spilled) {
+                            pos = nh++;
+                        } else {
+                            // keep the smallest keys of this window and redo the rest in another pass.
+                            // Once a hit has been dropped nothing larger than the buffer's last key may
+                            // be accepted, or the pass order would break.
+                            spilled = true;
+                            if (!key_before(t_in, qlin, meta, h_t[nh - 1], h_lin[nh - 1], h_meta[nh - 1])) continue;
+                            pos = nh - 1;
+                        }
+                        while (pos > win_start &&
+                               key_before(t_in, qlin, meta, h_t[pos - 1], h_lin[pos - 1], h_meta[pos - 1])) {
+                            h_t[pos] = h_t[pos - 1];
+                            h_lin[pos] = h_lin[pos - 1];
+                            h_seg[pos] = h_seg[pos - 1];
+                            h_meta[pos] = h_meta[pos - 1];
+                            --pos;
+                        }
+                        h_t[pos] = t_in;
+                        h_lin[pos] = qlin;
+                        h_seg[pos] = P.g.sv_seg[e];
+                        h_meta[pos] = meta;
                     }
                 }
                 __syncwarp(FULL);
