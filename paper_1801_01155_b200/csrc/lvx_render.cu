@@ -39,7 +39,7 @@ namespace {
 #define LVX_HIT_FLUSH 20
 #endif
 #ifndef LVX_SHADE_BATCH
-#define LVX_SHADE_BATCH 8
+#define LVX_SHADE_BATCH 4
 #endif
 #ifndef LVX_SLOTS
 #define LVX_SLOTS 8
@@ -55,9 +55,12 @@ constexpr int kHitFlush = LVX_HIT_FLUSH;    // a lane with this many buffered hi
 constexpr int kSlots = LVX_SLOTS;           // windows a lane may open between two composites (<= 16)
 constexpr int kShadeBatch = LVX_SHADE_BATCH;  // hits per ray and round in the pooled shading stage
 constexpr int kWalkSteps = LVX_WALK_STEPS;  // DDA steps a lane may take per round looking for a window
-constexpr int kItemCap = 256;               // voxel items per round and warp (>= 27)
-constexpr int kSurvCap = 64;                // survivor ring per warp (power of two, >= 64)
-constexpr int kWarpsPerBlock = 4;
+constexpr int kItemCap = 1024;              // voxel items per round and block (>= 27)
+constexpr int kSurvCap = 256;               // survivor ring per block (power of two, >= 2 * threads)
+#ifndef LVX_WPB
+#define LVX_WPB 4
+#endif
+constexpr int kWarpsPerBlock = LVX_WPB;
 constexpr double kCullMargin = 1e-4;   // sub-box cull slack (float64 path, rounding ~1e-12)
 constexpr float kRejectMargin = 2e-3f; // bounding-sphere slack (float32 path, rounding ~1e-5)
 
@@ -232,66 +235,98 @@ __device__ void mark_footprint(const RenderArgs &A, u32 pv, bool neighbor) {
             }
 }
 
-// The 32 rays of an 8x4 tile are walked by one warp in bulk-synchronous ROUNDS.  Rays are
-// bound to lanes only where per-ray state is needed (the DDA walk, the sorted hit buffer,
-// the running colour); every gather-type stage is pooled in shared memory and dealt out
-// evenly over the 32 lanes, so the few rays that cross crowded voxels do not serialise
-// the warp:
+// The rays of a thread block (kWarpsPerBlock 8x4 pixel tiles, one ray per thread) are
+// processed in bulk-synchronous ROUNDS.  Rays are bound to threads only where per-ray state
+// is needed (the DDA walk, the sorted hit buffer, the running colour); every gather-type
+// stage is pooled in shared memory and dealt out evenly over all threads of the block, so
+// the few rays that cross crowded voxels do not serialise their warp, threads whose own ray
+// is finished keep working for the others, and all warps of the block run the same stage at
+// the same time (the kernel is far larger than the instruction cache):
 //
-//  W  "walk": every lane that may open a window steps its DDA (at most kWalkSteps steps)
+//  W  "walk": every thread that may open a window steps its DDA (at most kWalkSteps steps)
 //     until it finds a window whose culled neighbourhood holds segments; it opens a slot
-//     and publishes the window (cell, local ray start, length) in its shared-memory row.
-//  V  "voxels": the occupied neighbour voxels of all open windows are listed (lane-major,
-//     the reference's z,y,x scan order inside a window); lanes read the voxel headers
-//     item-parallel and a running prefix sum of the counts enumerates the candidates.
-//  C  "candidates": 32 candidates at a time, one per lane whichever ray they belong to:
-//     record load + conservative float32 pre-reject against the owner's window.
-//     Survivors are appended (order-preserving) to a small ring in shared memory.
-//  E  "exact": whenever 32 survivors are queued, one exact float64 test set per lane;
-//     each owner then takes its own results in candidate order (ownership test, gather
-//     ordinals, sorted insertion into its private hit buffer).
-//  S  "composite": when some lane has enough hits buffered (or nobody can walk on), every
-//     lane composites its buffered hits in order; shading is pooled like the exact tests.
+//     and publishes the window (cell, local ray start, length, [t0,t1)) in shared memory.
+//  V  "voxels": the occupied neighbour voxels of all open windows are listed (thread-major,
+//     the reference's z,y,x scan order inside a window); threads read the voxel headers
+//     item-parallel and a prefix sum of the counts enumerates the candidates.
+//  C  "candidates": kThreads candidates at a time, one per thread whichever ray they belong
+//     to: record load + conservative float32 pre-reject against the owner's window.
+//     Survivors are appended (order-preserving) to a ring in shared memory.
+//  E  "exact": whenever kThreads survivors are queued, one exact float64 test set per
+//     thread, including the ownership test t0 <= t_in < t1 of the owner's window; each
+//     owner then takes its owned hits in candidate order (gather ordinals, sorted insertion
+//     into its private hit buffer).
+//  S  "composite": when some thread has enough hits buffered (or nobody can walk on), every
+//     thread composites its buffered hits in order; shading is pooled like the exact tests.
 //
 // Every window opened in a round is completely scanned by the end of that round, so the
-// buffered hits always belong to complete windows.  A lane may have scanned a few windows
-// past the one in which its ray terminates; that is invisible in the output: the counters
-// are snapshotted per window (w_tests / w_over) and the snapshot of the terminating hit's
+// buffered hits always belong to complete windows.  A ray may have scanned a few windows
+// past the one in which it terminates; that is invisible in the output: the counters are
+// snapshotted per window (w_tests / w_over) and the snapshot of the terminating hit's
 // window is what gets reported, exactly the reference's count.
-struct WarpPool {
-    double dir[32][3];             // ray directions of the 32 lanes (the origin is shared)
+constexpr int kThreads = kWarpsPerBlock * 32;
+
+struct BlockPool {
+    double dir[kThreads][3];       // ray directions (the origin is shared)
+    double wt[kThreads][2];        // open window of each thread: parameter range [t0, t1)
     union {
         struct {                       // stages V, C, E
             double res[kSurvCap][3];   // t_in of tube / sphere A / sphere B
             u32 it_lin[kItemCap];      // voxel items: linear index, first record, candidate prefix
             u32 it_base[kItemCap];
             u32 it_cstart[kItemCap + 1];
-            u16 it_key[kItemCap];      // owner lane << 5 | neighbour bit
             u32 sv_seg[kSurvCap];      // survivor ring
             u32 sv_lin[kSurvCap];
-            u16 sv_meta[kSurvCap];     // in: primitive mask 3 | owner << 3; out: hit mask 3 | lid << 3
-            u8 o_first[32], o_last[32];
+            u16 it_key[kItemCap];      // owner thread << 5 | neighbour bit
+            u16 sv_meta[kSurvCap];     // in: primitive mask 3 | owner << 8; out: owned-hit mask 3 | lid << 3 | owner << 8
+            u8 o_first[kThreads], o_last[kThreads];
         } g;
         struct {                       // stage S
-            double res[32 * kShadeBatch][2];  // scale, alpha
-            u32 seg[32 * kShadeBatch];
-            u16 meta[32 * kShadeBatch];       // kind | owner lane << 3
+            double res[kThreads * kShadeBatch][2];  // scale, alpha
+            u32 seg[kThreads * kShadeBatch];
+            u16 meta[kThreads * kShadeBatch];       // kind | owner thread << 3
         } s;
     };
-    float fdir[32][3];             // float32 copies for the pre-reject
-    float wq0[32][3];              // open window of each lane: ray point at t0, window-local
-    float wtlen[32];
-    int wcell[32][3];
-    double wt[32][2];              // its parameter range [t0, t1)
+    float fdir[kThreads][3];       // float32 copies for the pre-reject
+    float wq0[kThreads][3];        // open window: ray point at t0, window-local
+    float wtlen[kThreads];
+    int wcell[kThreads][3];
+    u32 starts[2][kWarpsPerBlock];  // item-start bits of the current candidate chunk (double-buffered)
+    int wsum[2][kWarpsPerBlock];   // per-warp partial sums of the block scans (double-buffered)
+    int wcnt[2][kWarpsPerBlock];   // survivors per warp of the current chunk (double-buffered)
+    int total_v;
 };
 
+// Exclusive prefix sum over the block's threads (one barrier).  `scratch` must not be the
+// buffer used by the previous call.
+__device__ __forceinline__ int block_scan_excl(int v, int *scratch, int lane, int warp, int &total) {
+    constexpr unsigned FULL = 0xFFFFFFFFu;
+    int inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) scratch[warp] = inc;
+    __syncthreads();
+    int base = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kWarpsPerBlock; ++w) {
+        const int t = scratch[w];
+        if (w < warp) base += t;
+        tot += t;
+    }
+    total = tot;
+    return base + inc - v;
+}
+
 template <bool FOOTPRINT>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, LVX_MIN_BLOCKS)
+__global__ void __launch_bounds__(kThreads, LVX_MIN_BLOCKS)
 render_kernel(const RenderArgs A) {
     constexpr unsigned FULL = 0xFFFFFFFFu;
-    const int lane = threadIdx.x & 31;
-    const unsigned lt_mask = (1u << lane) - 1u;
-    const i64 gw = (i64)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned le_mask = 0xFFFFFFFFu >> (31 - lane), lt_mask = le_mask >> 1;
+    const i64 gw = (i64)blockIdx.x * kWarpsPerBlock + warp;
     const int wpt_x = A.tl.tile_w >> 3, wpt_y = A.tl.tile_h >> 2;
     const int warps_per_tile = wpt_x * wpt_y;
     const i64 k = gw / warps_per_tile;  // index into this rank's tile list
@@ -324,15 +359,18 @@ render_kernel(const RenderArgs A) {
     const float reach_pt = (float)tube_r + kRejectMargin;  // joint sphere about an endpoint
     const double cull = tube_r + kCullMargin;
 
-    __shared__ WarpPool pools[kWarpsPerBlock];
-    WarpPool &P = pools[threadIdx.x >> 5];
-    P.dir[lane][0] = ddx;
-    P.dir[lane][1] = ddy;
-    P.dir[lane][2] = ddz;
-    P.fdir[lane][0] = (float)ddx;
-    P.fdir[lane][1] = (float)ddy;
-    P.fdir[lane][2] = (float)ddz;
-    __syncwarp(FULL);
+    __shared__ BlockPool P;
+    P.dir[tid][0] = ddx;
+    P.dir[tid][1] = ddy;
+    P.dir[tid][2] = ddz;
+    P.fdir[tid][0] = (float)ddx;
+    P.fdir[tid][1] = (float)ddy;
+    P.fdir[tid][2] = (float)ddz;
+    P.g.o_first[tid] = 255;
+    if (tid < 2 * kWarpsPerBlock) (&P.starts[0][0])[tid] = 0;
+    if (tid == 0) P.total_v = 0;
+    int par = 0;   // which scratch buffer the next block scan uses
+    int cpar = 0;  // which starts/wcnt buffer the next candidate chunk uses (the other one is being cleared)
 
     PixelState S;
     S.acc[0] = S.acc[1] = S.acc[2] = S.acc[3] = 0.0;
@@ -366,9 +404,10 @@ render_kernel(const RenderArgs A) {
     u32 last_lin = 0, last_meta = 0;
     unsigned long long over_committed = 0;
 
+    bool pending = false;  // (block-uniform) some thread's window did not fit into the last round
     for (;;) {
         // ================= W: walk to the next window worth scanning ================================
-        if (!__any_sync(FULL, has_win)) {
+        if (!pending) {
 #pragma unroll 1
             for (int it = 0; it < kWalkSteps; ++it) {
                 const bool want = alive && !done && !has_win &&
@@ -415,15 +454,15 @@ render_kernel(const RenderArgs A) {
                 w_over[cur_slot] = 0;
                 if (FOOTPRINT) w_vox[cur_slot] = (u32)(wx + 1) | ((u32)(wy + 1) << 10) | ((u32)(wz + 1) << 20);
                 if (nm == 0) continue;  // (only possible in the instrumented build)
-                P.wcell[lane][0] = wx;
-                P.wcell[lane][1] = wy;
-                P.wcell[lane][2] = wz;
-                P.wq0[lane][0] = (float)(p0x - (double)wx);  // window-local float32 frame
-                P.wq0[lane][1] = (float)(p0y - (double)wy);
-                P.wq0[lane][2] = (float)(p0z - (double)wz);
-                P.wtlen[lane] = (float)(t1 - t0);
-                P.wt[lane][0] = t0;
-                P.wt[lane][1] = t1;
+                P.wcell[tid][0] = wx;
+                P.wcell[tid][1] = wy;
+                P.wcell[tid][2] = wz;
+                P.wq0[tid][0] = (float)(p0x - (double)wx);  // window-local float32 frame
+                P.wq0[tid][1] = (float)(p0y - (double)wy);
+                P.wq0[tid][2] = (float)(p0z - (double)wz);
+                P.wtlen[tid] = (float)(t1 - t0);
+                P.wt[tid][0] = t0;
+                P.wt[tid][1] = t1;
                 cw_mask = m = nm;
                 has_win = true;
                 ord = 0;
@@ -431,247 +470,283 @@ render_kernel(const RenderArgs A) {
             }
         }
 
-        if (__any_sync(FULL, has_win)) {
-            // ================= V: list the voxels of the open windows, read their headers ============
+        // ================= V: list the voxels of the open windows, read their headers ================
+        {
             const int nv = has_win ? __popc(m) : 0;
-            int voff = nv;  // inclusive scan over lanes
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int t = __shfl_up_sync(FULL, voff, o);
-                if (lane >= o) voff += t;
-            }
-            // lanes are admitted in lane order while their voxels fit (the first always does)
-            const bool admitted = has_win && voff <= kItemCap;
-            const unsigned adm = __ballot_sync(FULL, admitted);
-            const int total_v = __shfl_sync(FULL, voff, 31 - __clz((int)adm));
-            voff -= nv;
-            if (admitted) {
-                int kk = 0;
-                for (u32 mm = m; mm; mm &= mm - 1, ++kk)
-                    P.g.it_key[voff + kk] = (u16)(((u32)lane << 5) | (u32)(__ffs((int)mm) - 1));
-                has_win = false;
-            }
-            __syncwarp(FULL);
-            u32 running = 0;
-            for (int i0 = 0; i0 < total_v; i0 += 32) {
-                const int i = i0 + lane;
-                u32 cnt = 0;
-                if (i < total_v) {
-                    const u32 key = P.g.it_key[i];
-                    const int owner = (int)(key >> 5), b = (int)(key & 31u);
-                    const int bz_ = b / 9, by_ = (b - 9 * bz_) / 3, bx_ = b - 9 * bz_ - 3 * by_;
-                    const u32 lin = (u32)((P.wcell[owner][0] + bx_ - 1) +
-                                          rx * ((P.wcell[owner][1] + by_ - 1) + ry * (P.wcell[owner][2] + bz_ - 1)));
-                    cnt = __ldg(A.counts + lin);
-                    P.g.it_lin[i] = lin;
-                    P.g.it_base[i] = __ldg(A.offsets + lin);
+            int total_all;
+            const int voff = block_scan_excl(nv, P.wsum[par], lane, warp, total_all);
+            par ^= 1;
+            if (total_all > 0) {
+                // threads are admitted in thread order while their voxels fit (the first always does)
+                const bool admitted = has_win && voff + nv <= kItemCap;
+                if (admitted) {
+                    int kk = voff;
+                    for (u32 mm = m; mm; mm &= mm - 1, ++kk)
+                        P.g.it_key[kk] = (u16)(((u32)tid << 5) | (u32)(__ffs((int)mm) - 1));
+                    atomicMax(&P.total_v, voff + nv);
+                    has_win = false;
                 }
-                u32 inc = cnt;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const u32 t = __shfl_up_sync(FULL, inc, o);
-                    if (lane >= o) inc += t;
-                }
-                if (i < total_v) P.g.it_cstart[i] = running + inc - cnt;
-                running += __shfl_sync(FULL, inc, 31);
-            }
-            if (lane == 0) P.g.it_cstart[total_v] = running;
-            P.g.o_first[lane] = 255;
-            __syncwarp(FULL);
-            const int total_c = (int)running;
-
-            // ================= C + E: pre-reject 32 candidates at a time, exact tests in batches ======
-            int sv_head = 0, nsv = 0;  // survivor ring (warp-uniform)
-            int it_next = 0;           // first item that starts at or after the current chunk
-            for (int g0 = 0; g0 < total_c || nsv > 0; g0 += 32) {
-                if (g0 < total_c) {
-                    const int g = g0 + lane;
-                    u32 mask = 0, seg = 0, key = 0, lin = 0;
-                    // items whose first candidate falls into this chunk (at most 32: every item holds
-                    // at least one) flag that position; the item of candidate g is the last one
-                    // starting at or before g
-                    {
-                        const int ii = it_next + lane;
-                        const u32 cs = ii < total_v ? P.g.it_cstart[ii] : 0xFFFFFFFFu;
-                        const u32 starts = __reduce_or_sync(FULL, cs < (u32)(g0 + 32) ? 1u << (cs - (u32)g0) : 0u);
-                        const int item = it_next - 1 + __popc(starts & (lt_mask | (1u << lane)));
-                        it_next += __popc(starts);
-                        if (g < total_c) {
-                            seg = P.g.it_base[item] + ((u32)g - P.g.it_cstart[item]);
-                            key = P.g.it_key[item];
-                            lin = P.g.it_lin[item];
-                        }
+                pending = __syncthreads_or(has_win) != 0;
+                const int total_v = P.total_v;
+                // headers: each warp takes a contiguous slice of the items
+                const int q = (total_v + kWarpsPerBlock - 1) / kWarpsPerBlock;
+                const int s0 = warp * q, s1 = min(total_v, s0 + q);
+                u32 run = 0;
+                for (int i0 = s0; i0 < s1; i0 += 32) {
+                    const int i = i0 + lane;
+                    u32 cnt = 0;
+                    if (i < s1) {
+                        const u32 key = P.g.it_key[i];
+                        const int owner = (int)(key >> 5), b = (int)(key & 31u);
+                        const int bz_ = b / 9, by_ = (b - 9 * bz_) / 3, bx_ = b - 9 * bz_ - 3 * by_;
+                        const u32 lin = (u32)((P.wcell[owner][0] + bx_ - 1) +
+                                              rx * ((P.wcell[owner][1] + by_ - 1) + ry * (P.wcell[owner][2] + bz_ - 1)));
+                        cnt = __ldg(A.counts + lin);
+                        P.g.it_lin[i] = lin;
+                        P.g.it_base[i] = __ldg(A.offsets + lin);
                     }
-                    if (g < total_c) {
-                        const int owner = (int)(key >> 5);
-                        const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + seg));
-                        const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + seg) + 1);
-                        const float fwx = (float)P.wcell[owner][0], fwy = (float)P.wcell[owner][1],
-                                    fwz = (float)P.wcell[owner][2];
-                        const float q0x = P.wq0[owner][0], q0y = P.wq0[owner][1], q0z = P.wq0[owner][2];
-                        const float fdx = P.fdir[owner][0], fdy = P.fdir[owner][1], fdz = P.fdir[owner][2];
-                        const float tlen = P.wtlen[owner];
-                        const float ax = ra.x - fwx, ay = ra.y - fwy, az = ra.z - fwz;
-                        const float bx = rb.x - fwx, by = rb.y - fwy, bz = rb.z - fwz;
-                        // the tube AND both joint spheres lie inside the segment's bounding sphere
-                        if (may_enter(0.5f * (ax + bx), 0.5f * (ay + by), 0.5f * (az + bz), q0x, q0y, q0z, fdx,
-                                      fdy, fdz, tlen, rb.w + reach_pt)) {
-                            // the tube's entry point lies on the ray within tube_r of the segment's
-                            // axis line, so the two lines pass within tube_r of each other:
-                            // |w . (d x u)| <= reach |d x u|  (absolute slack >> float32 rounding)
-                            const float ux = bx - ax, uy = by - ay, uz = bz - az;
-                            const float nx = fdy * uz - fdz * uy, ny = fdz * ux - fdx * uz, nz = fdx * uy - fdy * ux;
-                            const float wn = (ax - q0x) * nx + (ay - q0y) * ny + (az - q0z) * nz;
-                            if (wn * wn <= reach_pt * reach_pt * (nx * nx + ny * ny + nz * nz) + 1e-6f) mask = 1u;
-                            if (joints) {
-                                if (may_enter(ax, ay, az, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mask |= 2u;
-                                if (may_enter(bx, by, bz, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mask |= 4u;
+                    u32 inc = cnt;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const u32 t = __shfl_up_sync(FULL, inc, o);
+                        if (lane >= o) inc += t;
+                    }
+                    if (i < s1) P.g.it_cstart[i] = run + inc - cnt;
+                    run += __shfl_sync(FULL, inc, 31);
+                }
+                if (lane == 0) P.wsum[par][warp] = (int)run;
+                __syncthreads();
+                int total_c = 0;
+                {
+                    u32 base = 0;
+#pragma unroll
+                    for (int w = 0; w < kWarpsPerBlock; ++w) {
+                        const int t = P.wsum[par][w];
+                        if (w < warp) base += (u32)t;
+                        total_c += t;
+                    }
+                    par ^= 1;
+                    for (int i = s0 + lane; i < s1; i += 32) P.g.it_cstart[i] += base;
+                    if (tid == 0) {
+                        P.g.it_cstart[total_v] = (u32)total_c;
+                        P.total_v = 0;  // for the next round
+                    }
+                }
+                __syncthreads();
+
+                // ============= C + E: pre-reject kThreads candidates at a time, exact tests in batches ==
+                int sv_head = 0, nsv = 0;  // survivor ring (block-uniform)
+                int it_next = 0;           // first item that starts at or after the current chunk
+                for (int g0 = 0; g0 < total_c || nsv > 0; g0 += kThreads) {
+                    if (g0 < total_c) {
+                        const int g = g0 + tid;
+                        u32 mask = 0, seg = 0, key = 0, lin = 0;
+                        // items whose first candidate falls into this chunk (at most kThreads: every
+                        // item holds at least one) flag that position; the item of candidate g is the
+                        // last one starting at or before g
+                        {
+                            const int ii = it_next + tid;
+                            const u32 cs = ii < total_v ? P.g.it_cstart[ii] : 0xFFFFFFFFu;
+                            const bool in_chunk = cs < (u32)(g0 + kThreads);
+                            const u32 pb = cs - (u32)g0;
+#pragma unroll
+                            for (int w = 0; w < kWarpsPerBlock; ++w) {
+                                const u32 r = __reduce_or_sync(FULL, (in_chunk && (pb >> 5) == (u32)w) ? 1u << (pb & 31u) : 0u);
+                                if (lane == 0 && r) atomicOr(&P.starts[cpar][w], r);
                             }
                         }
-                    }
-                    const unsigned sb = __ballot_sync(FULL, mask != 0);
-                    if (mask) {
-                        const int pos = (sv_head + nsv + __popc(sb & lt_mask)) & (kSurvCap - 1);
-                        P.g.sv_seg[pos] = seg;
-                        P.g.sv_lin[pos] = lin;
-                        P.g.sv_meta[pos] = (u16)(mask | ((key >> 5) << 3));
-                    }
-                    nsv += __popc(sb);
-                    __syncwarp(FULL);
-                }
-                if (nsv < 32 && g0 + 32 < total_c) continue;
-                if (nsv == 0) break;
-                // ---- E: exact float64 tests, one survivor per lane -------------------------------------
-                const int nb = min(nsv, 32);
-                int owner = -1;
-                if (lane < nb) {
-                    const int e = (sv_head + lane) & (kSurvCap - 1);
-                    const u32 i = P.g.sv_seg[e], im = P.g.sv_meta[e];
-                    owner = (int)(im >> 3);
-                    const double rdx = P.dir[owner][0], rdy = P.dir[owner][1], rdz = P.dir[owner][2];
-                    const double t0 = P.wt[owner][0], t1 = P.wt[owner][1];
-                    const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + i));
-                    const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + i) + 1);
-                    u32 hits = 0;  // hits the owner's window OWNS: t0 <= t_in < t1 (:838, :858, :878)
-                    LvxHit h;
-                    if ((im & 1u) && lvx_tube_f32axis(ox, oy, oz, rdx, rdy, rdz, ra.x, ra.y, ra.z, rb.x, rb.y, rb.z,
-                                                      tube_r, h) && t0 <= h.t_in && h.t_in < t1) {
-                        hits |= 1u;
-                        P.g.res[e][0] = h.t_in;
-                    }
-                    if ((im & 2u) && lvx_sphere<false>(ox, oy, oz, rdx, rdy, rdz, (double)ra.x, (double)ra.y,
-                                                       (double)ra.z, tube_r, h) && t0 <= h.t_in && h.t_in < t1) {
-                        hits |= 2u;
-                        P.g.res[e][1] = h.t_in;
-                    }
-                    if ((im & 4u) && lvx_sphere<false>(ox, oy, oz, rdx, rdy, rdz, (double)rb.x, (double)rb.y,
-                                                       (double)rb.z, tube_r, h) && t0 <= h.t_in && h.t_in < t1) {
-                        hits |= 4u;
-                        P.g.res[e][2] = h.t_in;
-                    }
-                    P.g.sv_meta[e] = (u16)(hits | (((__float_as_uint(ra.w) >> 8) & 31u) << 3));
-                }
-                // survivors are queued in lane-major owner order: every owner's share is contiguous
-                {
-                    const int prev = __shfl_up_sync(FULL, owner, 1), next = __shfl_down_sync(FULL, owner, 1);
-                    if (lane < nb) {
-                        if (lane == 0 || prev != owner) P.g.o_first[owner] = (u8)lane;
-                        if (lane == nb - 1 || next != owner) P.g.o_last[owner] = (u8)lane;
-                    }
-                }
-                __syncwarp(FULL);
-                // ---- each owner takes its owned hits in candidate order ------------------------------
-                // (one hit per lane and iteration, so the insertions of different rays run side by side)
-                {
-                    const int first = P.g.o_first[lane];
-                    const int last = first == 255 ? -1 : (int)P.g.o_last[lane];
-                    int j = first == 255 ? 0 : first;
-                    u32 hbits = 0, om = 0;
-                    int e = 0;
-                    for (;;) {
-                        while (hbits == 0 && j <= last) {
-                            e = (sv_head + j) & (kSurvCap - 1);
-                            om = P.g.sv_meta[e];
-                            hbits = om & 7u;
-                            ++j;
+                        __syncthreads();
+                        {
+                            int item = it_next - 1, adv = 0;
+#pragma unroll
+                            for (int w = 0; w < kWarpsPerBlock; ++w) {
+                                const u32 sw = P.starts[cpar][w];
+                                adv += __popc(sw);
+                                if (w < warp) item += __popc(sw);
+                                else if (w == warp) item += __popc(sw & le_mask);
+                            }
+                            it_next += adv;
+                            if (tid < kWarpsPerBlock) P.starts[cpar ^ 1][tid] = 0;  // the buffer of the next chunk
+                            if (g < total_c) {
+                                seg = P.g.it_base[item] + ((u32)g - P.g.it_cstart[item]);
+                                key = P.g.it_key[item];
+                                lin = P.g.it_lin[item];
+                            }
                         }
-                        if (!__any_sync(FULL, hbits != 0)) break;
-                        if (hbits == 0) continue;
-                        const u32 kind3 = (u32)(__ffs((int)hbits) - 1);
-                        hbits &= hbits - 1;
-                        const double t_in = P.g.res[e][kind3];
-                        const u32 my_ord = ord++;
-                        if (my_ord >= (u32)LVX_MAX_WINDOW_HITS) {
-                            // the reference drops hits past its 1024-entry window buffer
-                            if (!have_last) w_over[cur_slot] += 1;
-                            continue;
+                        if (g < total_c) {
+                            const int owner = (int)(key >> 5);
+                            const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + seg));
+                            const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + seg) + 1);
+                            const float fwx = (float)P.wcell[owner][0], fwy = (float)P.wcell[owner][1],
+                                        fwz = (float)P.wcell[owner][2];
+                            const float q0x = P.wq0[owner][0], q0y = P.wq0[owner][1], q0z = P.wq0[owner][2];
+                            const float fdx = P.fdir[owner][0], fdy = P.fdir[owner][1], fdz = P.fdir[owner][2];
+                            const float tlen = P.wtlen[owner];
+                            const float ax = ra.x - fwx, ay = ra.y - fwy, az = ra.z - fwz;
+                            const float bx = rb.x - fwx, by = rb.y - fwy, bz = rb.z - fwz;
+                            // the tube AND both joint spheres lie inside the segment's bounding sphere
+                            if (may_enter(0.5f * (ax + bx), 0.5f * (ay + by), 0.5f * (az + bz), q0x, q0y, q0z, fdx,
+                                          fdy, fdz, tlen, rb.w + reach_pt)) {
+                                // the tube's entry point lies on the ray within tube_r of the segment's
+                                // axis line, so the two lines pass within tube_r of each other:
+                                // |w . (d x u)| <= reach |d x u|  (absolute slack >> float32 rounding)
+                                const float ux = bx - ax, uy = by - ay, uz = bz - az;
+                                const float nx = fdy * uz - fdz * uy, ny = fdz * ux - fdx * uz, nz = fdx * uy - fdy * ux;
+                                const float wn = (ax - q0x) * nx + (ay - q0y) * ny + (az - q0z) * nz;
+                                if (wn * wn <= reach_pt * reach_pt * (nx * nx + ny * ny + nz * nz) + 1e-6f) mask = 1u;
+                                if (joints) {
+                                    if (may_enter(ax, ay, az, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mask |= 2u;
+                                    if (may_enter(bx, by, bz, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mask |= 4u;
+                                }
+                            }
                         }
-                        const u32 qlin = P.g.sv_lin[e];
-                        const u32 meta = ((om >> 3) & 31u) | (kind3 << 5) | (my_ord << 7) | ((u32)cur_slot << 17);
-                        if (have_last && !key_before(last_t, last_lin, last_meta, t_in, qlin, meta))
-                            continue;  // composited in an earlier pass over this window
-                        int pos;
-                        if (nh < kHitCap && !spilled) {
-                            pos = nh++;
-                        } else {
-                            // keep the smallest keys of this window and redo the rest in another pass.
-                            // Once a hit has been dropped nothing larger than the buffer's last key may
-                            // be accepted, or the pass order would break.
-                            spilled = true;
-                            if (!key_before(t_in, qlin, meta, h_t[nh - 1], h_lin[nh - 1], h_meta[nh - 1])) continue;
-                            pos = nh - 1;
+                        const unsigned sb = __ballot_sync(FULL, mask != 0);
+                        if (lane == 0) P.wcnt[cpar][warp] = __popc(sb);
+                        __syncthreads();
+                        {
+                            int base = nsv, tot = 0;
+#pragma unroll
+                            for (int w = 0; w < kWarpsPerBlock; ++w) {
+                                const int t = P.wcnt[cpar][w];
+                                if (w < warp) base += t;
+                                tot += t;
+                            }
+                            if (mask) {
+                                const int pos = (sv_head + base + __popc(sb & lt_mask)) & (kSurvCap - 1);
+                                P.g.sv_seg[pos] = seg;
+                                P.g.sv_lin[pos] = lin;
+                                P.g.sv_meta[pos] = (u16)(mask | ((key >> 5) << 8));
+                            }
+                            nsv += tot;
                         }
-                        while (pos > win_start &&
-                               key_before(t_in, qlin, meta, h_t[pos - 1], h_lin[pos - 1], h_meta[pos - 1])) {
-                            h_t[pos] = h_t[pos - 1];
-                            h_lin[pos] = h_lin[pos - 1];
-                            h_seg[pos] = h_seg[pos - 1];
-                            h_meta[pos] = h_meta[pos - 1];
-                            --pos;
-                        }
-                        h_t[pos] = t_in;
-                        h_lin[pos] = qlin;
-                        h_seg[pos] = P.g.sv_seg[e];
-                        h_meta[pos] = meta;
+                        cpar ^= 1;
                     }
+                    if (nsv < kThreads && g0 + kThreads < total_c) continue;
+                    if (nsv == 0) break;
+                    __syncthreads();
+                    // ---- E: exact float64 tests + ownership, one survivor per thread ---------------------
+                    const int nb = min(nsv, kThreads);
+                    if (tid < nb) {
+                        const int e = (sv_head + tid) & (kSurvCap - 1);
+                        const u32 i = P.g.sv_seg[e], im = P.g.sv_meta[e];
+                        const int owner = (int)(im >> 8);
+                        // survivors are queued in thread-major owner order: every owner's share is contiguous
+                        if (tid == 0 || (int)(P.g.sv_meta[(e - 1) & (kSurvCap - 1)] >> 8) != owner) P.g.o_first[owner] = (u8)tid;
+                        if (tid == nb - 1 || (int)(P.g.sv_meta[(e + 1) & (kSurvCap - 1)] >> 8) != owner) P.g.o_last[owner] = (u8)tid;
+                        const double rdx = P.dir[owner][0], rdy = P.dir[owner][1], rdz = P.dir[owner][2];
+                        const double t0 = P.wt[owner][0], t1 = P.wt[owner][1];
+                        const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + i));
+                        const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + i) + 1);
+                        u32 hits = 0;  // hits the owner's window OWNS: t0 <= t_in < t1 (:838, :858, :878)
+                        LvxHit h;
+                        if ((im & 1u) && lvx_tube_f32axis(ox, oy, oz, rdx, rdy, rdz, ra.x, ra.y, ra.z, rb.x, rb.y, rb.z,
+                                                          tube_r, h) && t0 <= h.t_in && h.t_in < t1) {
+                            hits |= 1u;
+                            P.g.res[e][0] = h.t_in;
+                        }
+                        if ((im & 2u) && lvx_sphere<false>(ox, oy, oz, rdx, rdy, rdz, (double)ra.x, (double)ra.y,
+                                                           (double)ra.z, tube_r, h) && t0 <= h.t_in && h.t_in < t1) {
+                            hits |= 2u;
+                            P.g.res[e][1] = h.t_in;
+                        }
+                        if ((im & 4u) && lvx_sphere<false>(ox, oy, oz, rdx, rdy, rdz, (double)rb.x, (double)rb.y,
+                                                           (double)rb.z, tube_r, h) && t0 <= h.t_in && h.t_in < t1) {
+                            hits |= 4u;
+                            P.g.res[e][2] = h.t_in;
+                        }
+                        // (the owner bits stay where the neighbours read them)
+                        P.g.sv_meta[e] = (u16)(hits | (((__float_as_uint(ra.w) >> 8) & 31u) << 3) | (im & 0xFF00u));
+                    }
+                    __syncthreads();
+                    // ---- each owner takes its owned hits in candidate order ------------------------------
+                    // (one hit per thread and iteration, so the insertions of different rays run side by side)
+                    {
+                        const int first = P.g.o_first[tid];
+                        const int last = first == 255 ? -1 : (int)P.g.o_last[tid];
+                        int j = first == 255 ? 0 : first;
+                        u32 hbits = 0, om = 0;
+                        int e = 0;
+                        for (;;) {
+                            while (hbits == 0 && j <= last) {
+                                e = (sv_head + j) & (kSurvCap - 1);
+                                om = P.g.sv_meta[e];
+                                hbits = om & 7u;
+                                ++j;
+                            }
+                            if (!__any_sync(FULL, hbits != 0)) break;
+                            if (hbits == 0) continue;
+                            const u32 kind3 = (u32)(__ffs((int)hbits) - 1);
+                            hbits &= hbits - 1;
+                            const double t_in = P.g.res[e][kind3];
+                            const u32 my_ord = ord++;
+                            if (my_ord >= (u32)LVX_MAX_WINDOW_HITS) {
+                                // the reference drops hits past its 1024-entry window buffer
+                                if (!have_last) w_over[cur_slot] += 1;
+                                continue;
+                            }
+                            const u32 qlin = P.g.sv_lin[e];
+                            const u32 meta = ((om >> 3) & 31u) | (kind3 << 5) | (my_ord << 7) | ((u32)cur_slot << 17);
+                            if (have_last && !key_before(last_t, last_lin, last_meta, t_in, qlin, meta))
+                                continue;  // composited in an earlier pass over this window
+                            int pos;
+                            if (nh < kHitCap && !spilled) {
+                                pos = nh++;
+                            } else {
+                                // keep the smallest keys of this window and redo the rest in another pass.
+                                // Once a hit has been dropped nothing larger than the buffer's last key may
+                                // be accepted, or the pass order would break.
+                                spilled = true;
+                                if (!key_before(t_in, qlin, meta, h_t[nh - 1], h_lin[nh - 1], h_meta[nh - 1])) continue;
+                                pos = nh - 1;
+                            }
+                            while (pos > win_start &&
+                                   key_before(t_in, qlin, meta, h_t[pos - 1], h_lin[pos - 1], h_meta[pos - 1])) {
+                                h_t[pos] = h_t[pos - 1];
+                                h_lin[pos] = h_lin[pos - 1];
+                                h_seg[pos] = h_seg[pos - 1];
+                                h_meta[pos] = h_meta[pos - 1];
+                                --pos;
+                            }
+                            h_t[pos] = t_in;
+                            h_lin[pos] = qlin;
+                            h_seg[pos] = P.g.sv_seg[e];
+                            h_meta[pos] = meta;
+                        }
+                    }
+                    P.g.o_first[tid] = 255;
+                    sv_head = (sv_head + nb) & (kSurvCap - 1);
+                    nsv -= nb;
+                    __syncthreads();
                 }
-                __syncwarp(FULL);
-                P.g.o_first[lane] = 255;
-                sv_head = (sv_head + nb) & (kSurvCap - 1);
-                nsv -= nb;
-                __syncwarp(FULL);
+                // threads that did not fit this round keep their window and go first in the next one
+                if (pending) continue;
             }
-            // lanes that did not fit this round keep their window and go first in the next one
-            if (__any_sync(FULL, has_win)) continue;
         }
 
         // ================= S: composite, _kernels.py:898-914 ============================================
         const bool walker = alive && !done;
         const bool blocked = walker && (nh >= kHitFlush || nw >= kSlots || spilled);
-        const bool any_walker = __any_sync(FULL, walker);
-        if (__any_sync(FULL, blocked) || !any_walker) {
+        const bool any_blocked = __syncthreads_or(blocked) != 0;
+        const bool any_walker = __syncthreads_or(walker) != 0;
+        if (any_blocked || !any_walker) {
             const int n_comp = nh;  // every buffered hit belongs to a completely scanned window
-            // Up to kShadeBatch hits per ray and round are listed in shared memory, every lane
+            // Up to kShadeBatch hits per ray and round are listed in shared memory, every thread
             // recomputes one hit (t_out, normal) and its state-free shading terms, then each ray's
-            // own lane applies them in order.
+            // own thread applies them in order.
             int q = 0;
             bool comp = !done && n_comp > 0;
-            while (__any_sync(FULL, comp)) {
+            for (;;) {
                 const int nb = comp ? min(kShadeBatch, n_comp - q) : 0;
-                int off = nb;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int t = __shfl_up_sync(FULL, off, o);
-                    if (lane >= o) off += t;
-                }
-                const int total = __shfl_sync(FULL, off, 31);
-                off -= nb;
+                int total;
+                const int off = block_scan_excl(nb, P.wsum[par], lane, warp, total);
+                par ^= 1;
+                if (total == 0) break;
                 for (int j = 0; j < nb; ++j) {
                     P.s.seg[off + j] = h_seg[q + j];
-                    P.s.meta[off + j] = (u16)(meta_kind3(h_meta[q + j]) | ((u32)lane << 3));
+                    P.s.meta[off + j] = (u16)(meta_kind3(h_meta[q + j]) | ((u32)tid << 3));
                 }
-                __syncwarp(FULL);
-                for (int idx = lane; idx < total; idx += 32) {
+                __syncthreads();
+                for (int idx = tid; idx < total; idx += kThreads) {
                     const u32 i = P.s.seg[idx], im = P.s.meta[idx];
                     const int owner = (int)(im >> 3);
                     const u32 kind3 = im & 3u;
@@ -691,7 +766,7 @@ render_kernel(const RenderArgs A) {
                     P.s.res[idx][0] = scale;
                     P.s.res[idx][1] = alpha;
                 }
-                __syncwarp(FULL);
+                __syncthreads();
                 for (int j = 0; j < nb; ++j) {
                     const u32 i = h_seg[q], meta = h_meta[q];
                     const u32 kind3 = meta_kind3(meta);
@@ -724,8 +799,10 @@ render_kernel(const RenderArgs A) {
                     }
                     if (++q >= n_comp) comp = false;
                 }
-                __syncwarp(FULL);
+                // (the next listing is fenced from these reads by the barrier inside block_scan_excl)
             }
+            // the pools of stages V/C/E overlay the shading pool: restore their idle state
+            P.g.o_first[tid] = 255;
             if (!done) {
                 // commit the composited windows
                 for (int j = 0; j < nw; ++j) over_committed += w_over[j];
@@ -753,8 +830,10 @@ render_kernel(const RenderArgs A) {
                 }
                 nh = 0;
             }
+            // a window re-opened after a spill is scanned before anybody walks on
+            pending = __syncthreads_or(has_win) != 0;
+            if (!any_walker && !pending) break;
         }
-        if (!any_walker && !__any_sync(FULL, has_win)) break;
     }
     if (!done) overflow = over_committed;
 

@@ -47,13 +47,13 @@ def find(pat):
 STAGES = [('accumulate_hit (dedup+blend)', find('__device__ __forceinline__ double accumulate_hit'), find('// Conservative float32 test')),
           ('shade_hit', find('__device__ __forceinline__ void shade_hit'), find('// Returns the accumulated alpha')),
           ('may_enter', find('// Conservative float32 test'), find('// Instrumentation (lvx_render_footprint)')),
-          ('prologue (ray setup)', find('render_kernel(const RenderArgs A) {'), find('================= W:')),
-          ('W walk', find('================= W:'), find('================= V:')),
-          ('V voxel headers', find('================= V:'), find('================= C + E')),
-          ('C pre-reject', find('================= C + E'), find('---- E: exact')),
+          ('prologue (ray setup)', find('render_kernel(const RenderArgs A) {'), find('= W: walk to the next')),
+          ('W walk', find('= W: walk to the next'), find('= V: list the voxels')),
+          ('V voxel headers', find('= V: list the voxels'), find('= C + E: pre-reject')),
+          ('C pre-reject', find('= C + E: pre-reject'), find('---- E: exact')),
           ('E exact-test driver', find('---- E: exact'), find('---- each owner takes')),
-          ('owner insert', find('---- each owner takes'), find('================= S:')),
-          ('S composite', find('================= S:'), find('// tail: a terminated ray')),
+          ('owner insert', find('---- each owner takes'), find('= S: composite, _kernels')),
+          ('S composite', find('= S: composite, _kernels'), find('// tail: a terminated ray')),
           ('tail+output', find('// tail: a terminated ray'), find('__global__ void __launch_bounds__(256)'))]
 agg = collections.defaultdict(lambda: [0, 0, 0])
 for d in data:
