@@ -56,11 +56,14 @@ constexpr int kSlots = LVX_SLOTS;           // windows a lane may open between t
 constexpr int kShadeBatch = LVX_SHADE_BATCH;  // hits per ray and round in the pooled shading stage
 constexpr int kWalkSteps = LVX_WALK_STEPS;  // DDA steps a lane may take per round looking for a window
 constexpr int kItemCap = 1024;              // voxel items per round and block (>= 27)
-constexpr int kSurvCap = 256;               // survivor ring per block (power of two, >= 2 * threads)
 #ifndef LVX_WPB
 #define LVX_WPB 4
 #endif
+#ifndef LVX_CAND
+#define LVX_CAND 2
+#endif
 constexpr int kWarpsPerBlock = LVX_WPB;
+constexpr int kCand = LVX_CAND;             // candidates per thread and chunk of the pre-reject stage
 constexpr double kCullMargin = 1e-4;   // sub-box cull slack (float64 path, rounding ~1e-12)
 constexpr float kRejectMargin = 2e-3f; // bounding-sphere slack (float32 path, rounding ~1e-5)
 
@@ -265,13 +268,18 @@ __device__ void mark_footprint(const RenderArgs &A, u32 pv, bool neighbor) {
 // snapshotted per window (w_tests / w_over) and the snapshot of the terminating hit's
 // window is what gets reported, exactly the reference's count.
 constexpr int kThreads = kWarpsPerBlock * 32;
+constexpr int kChunk = kThreads * kCand;    // candidates per pre-reject chunk
+constexpr int kSurvNeed = kThreads + kChunk;  // fewer than kThreads queued + one chunk of survivors
+constexpr int kSurvCap = kSurvNeed <= 256 ? 256 : (kSurvNeed <= 512 ? 512 : (kSurvNeed <= 1024 ? 1024 : 2048));
+static_assert(kThreads < 255, "owner ids travel in 8 bits and 255 is the idle mark");
+static_assert(kSurvCap >= kSurvNeed, "survivor ring too small");
 
 struct BlockPool {
     double dir[kThreads][3];       // ray directions (the origin is shared)
     double wt[kThreads][2];        // open window of each thread: parameter range [t0, t1)
     union {
         struct {                       // stages V, C, E
-            double res[kSurvCap][3];   // t_in of tube / sphere A / sphere B
+            double res[kThreads][3];   // exact batch: t_in of tube / sphere A / sphere B
             u32 it_lin[kItemCap];      // voxel items: linear index, first record, candidate prefix
             u32 it_base[kItemCap];
             u32 it_cstart[kItemCap + 1];
@@ -291,9 +299,7 @@ struct BlockPool {
     float wq0[kThreads][3];        // open window: ray point at t0, window-local
     float wtlen[kThreads];
     int wcell[kThreads][3];
-    u32 starts[2][kWarpsPerBlock];  // item-start bits of the current candidate chunk (double-buffered)
     int wsum[2][kWarpsPerBlock];   // per-warp partial sums of the block scans (double-buffered)
-    int wcnt[2][kWarpsPerBlock];   // survivors per warp of the current chunk (double-buffered)
     int total_v;
 };
 
@@ -320,12 +326,33 @@ __device__ __forceinline__ int block_scan_excl(int v, int *scratch, int lane, in
     return base + inc - v;
 }
 
+// Developer instrumentation (-DLVX_STAGE_CLOCKS): thread 0 of every block accumulates the
+// cycles between stage boundaries and a few work counters into lvx_stage_clk.
+#ifdef LVX_STAGE_CLOCKS
+__device__ unsigned long long lvx_stage_clk[32];
+#define LVX_CLK(k)                                         \
+    do {                                                   \
+        if (tid == 0) {                                    \
+            const long long now_ = clock64();              \
+            s_clk[k] += (unsigned long long)(now_ - clk_last); \
+            clk_last = now_;                               \
+        }                                                  \
+    } while (0)
+#define LVX_CNT(k, v)                                      \
+    do {                                                   \
+        if (tid == 0) s_clk[k] += (unsigned long long)(v); \
+    } while (0)
+#else
+#define LVX_CLK(k) do {} while (0)
+#define LVX_CNT(k, v) do {} while (0)
+#endif
+
 template <bool FOOTPRINT>
 __global__ void __launch_bounds__(kThreads, LVX_MIN_BLOCKS)
 render_kernel(const RenderArgs A) {
     constexpr unsigned FULL = 0xFFFFFFFFu;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const unsigned le_mask = 0xFFFFFFFFu >> (31 - lane), lt_mask = le_mask >> 1;
+
     const i64 gw = (i64)blockIdx.x * kWarpsPerBlock + warp;
     const int wpt_x = A.tl.tile_w >> 3, wpt_y = A.tl.tile_h >> 2;
     const int warps_per_tile = wpt_x * wpt_y;
@@ -367,10 +394,8 @@ render_kernel(const RenderArgs A) {
     P.fdir[tid][1] = (float)ddy;
     P.fdir[tid][2] = (float)ddz;
     P.g.o_first[tid] = 255;
-    if (tid < 2 * kWarpsPerBlock) (&P.starts[0][0])[tid] = 0;
     if (tid == 0) P.total_v = 0;
     int par = 0;   // which scratch buffer the next block scan uses
-    int cpar = 0;  // which starts/wcnt buffer the next candidate chunk uses (the other one is being cleared)
 
     PixelState S;
     S.acc[0] = S.acc[1] = S.acc[2] = S.acc[3] = 0.0;
@@ -404,8 +429,16 @@ render_kernel(const RenderArgs A) {
     u32 last_lin = 0, last_meta = 0;
     unsigned long long over_committed = 0;
 
+#ifdef LVX_STAGE_CLOCKS
+    __shared__ unsigned long long s_clk[32];
+    if (tid < 32) s_clk[tid] = 0;
+    __syncthreads();
+    long long clk_last = clock64();
+#endif
     bool pending = false;  // (block-uniform) some thread's window did not fit into the last round
     for (;;) {
+        LVX_CLK(8);
+        LVX_CNT(10, 1);
         // ================= W: walk to the next window worth scanning ================================
         if (!pending) {
 #pragma unroll 1
@@ -471,6 +504,7 @@ render_kernel(const RenderArgs A) {
         }
 
         // ================= V: list the voxels of the open windows, read their headers ================
+        LVX_CLK(0);
         {
             const int nv = has_win ? __popc(m) : 0;
             int total_all;
@@ -534,94 +568,98 @@ render_kernel(const RenderArgs A) {
                 }
                 __syncthreads();
 
-                // ============= C + E: pre-reject kThreads candidates at a time, exact tests in batches ==
+                LVX_CLK(1);
+                LVX_CNT(14, total_v);
+                LVX_CNT(15, total_c);
+                // ============= C + E: pre-reject kChunk candidates at a time, exact tests in batches ====
                 int sv_head = 0, nsv = 0;  // survivor ring (block-uniform)
-                int it_next = 0;           // first item that starts at or after the current chunk
-                for (int g0 = 0; g0 < total_c || nsv > 0; g0 += kThreads) {
-                    if (g0 < total_c) {
-                        const int g = g0 + tid;
-                        u32 mask = 0, seg = 0, key = 0, lin = 0;
-                        // items whose first candidate falls into this chunk (at most kThreads: every
-                        // item holds at least one) flag that position; the item of candidate g is the
-                        // last one starting at or before g
-                        {
-                            const int ii = it_next + tid;
-                            const u32 cs = ii < total_v ? P.g.it_cstart[ii] : 0xFFFFFFFFu;
-                            const bool in_chunk = cs < (u32)(g0 + kThreads);
-                            const u32 pb = cs - (u32)g0;
-#pragma unroll
-                            for (int w = 0; w < kWarpsPerBlock; ++w) {
-                                const u32 r = __reduce_or_sync(FULL, (in_chunk && (pb >> 5) == (u32)w) ? 1u << (pb & 31u) : 0u);
-                                if (lane == 0 && r) atomicOr(&P.starts[cpar][w], r);
+                int g0 = 0;                // first candidate of the next chunk
+                for (;;) {
+                    if (nsv < kThreads && g0 < total_c) {
+                        // ---- C: kCand consecutive candidates per thread; all record loads are issued
+                        // before the first test so their latencies overlap
+                        const int gf = g0 + tid * kCand;
+                        int item = 0;
+                        if (gf < total_c) {
+                            // the item of candidate gf: the last one starting at or before gf
+                            int lo = 0, hi = total_v;  // it_cstart[lo] <= gf < it_cstart[hi]
+                            while (hi - lo > 1) {
+                                const int mid = (lo + hi) >> 1;
+                                if (P.g.it_cstart[mid] <= (u32)gf) lo = mid;
+                                else hi = mid;
                             }
+                            item = lo;
                         }
-                        __syncthreads();
-                        {
-                            int item = it_next - 1, adv = 0;
+                        u32 mask[kCand], seg[kCand];
+                        int itm[kCand];
+                        float4 ra[kCand], rb[kCand];
 #pragma unroll
-                            for (int w = 0; w < kWarpsPerBlock; ++w) {
-                                const u32 sw = P.starts[cpar][w];
-                                adv += __popc(sw);
-                                if (w < warp) item += __popc(sw);
-                                else if (w == warp) item += __popc(sw & le_mask);
-                            }
-                            it_next += adv;
-                            if (tid < kWarpsPerBlock) P.starts[cpar ^ 1][tid] = 0;  // the buffer of the next chunk
+                        for (int j = 0; j < kCand; ++j) {
+                            const int g = gf + j;
+                            mask[j] = 0;
+                            seg[j] = 0;
+                            itm[j] = item;
                             if (g < total_c) {
-                                seg = P.g.it_base[item] + ((u32)g - P.g.it_cstart[item]);
-                                key = P.g.it_key[item];
-                                lin = P.g.it_lin[item];
+                                while ((u32)g >= P.g.it_cstart[item + 1]) ++item;
+                                itm[j] = item;
+                                seg[j] = P.g.it_base[item] + ((u32)g - P.g.it_cstart[item]);
+                                ra[j] = __ldg(reinterpret_cast<const float4 *>(A.rec + seg[j]));
+                                rb[j] = __ldg(reinterpret_cast<const float4 *>(A.rec + seg[j]) + 1);
                             }
                         }
-                        if (g < total_c) {
-                            const int owner = (int)(key >> 5);
-                            const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + seg));
-                            const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + seg) + 1);
-                            const float fwx = (float)P.wcell[owner][0], fwy = (float)P.wcell[owner][1],
-                                        fwz = (float)P.wcell[owner][2];
-                            const float q0x = P.wq0[owner][0], q0y = P.wq0[owner][1], q0z = P.wq0[owner][2];
-                            const float fdx = P.fdir[owner][0], fdy = P.fdir[owner][1], fdz = P.fdir[owner][2];
-                            const float tlen = P.wtlen[owner];
-                            const float ax = ra.x - fwx, ay = ra.y - fwy, az = ra.z - fwz;
-                            const float bx = rb.x - fwx, by = rb.y - fwy, bz = rb.z - fwz;
-                            // the tube AND both joint spheres lie inside the segment's bounding sphere
-                            if (may_enter(0.5f * (ax + bx), 0.5f * (ay + by), 0.5f * (az + bz), q0x, q0y, q0z, fdx,
-                                          fdy, fdz, tlen, rb.w + reach_pt)) {
-                                // the tube's entry point lies on the ray within tube_r of the segment's
-                                // axis line, so the two lines pass within tube_r of each other:
-                                // |w . (d x u)| <= reach |d x u|  (absolute slack >> float32 rounding)
-                                const float ux = bx - ax, uy = by - ay, uz = bz - az;
-                                const float nx = fdy * uz - fdz * uy, ny = fdz * ux - fdx * uz, nz = fdx * uy - fdy * ux;
-                                const float wn = (ax - q0x) * nx + (ay - q0y) * ny + (az - q0z) * nz;
-                                if (wn * wn <= reach_pt * reach_pt * (nx * nx + ny * ny + nz * nz) + 1e-6f) mask = 1u;
-                                if (joints) {
-                                    if (may_enter(ax, ay, az, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mask |= 2u;
-                                    if (may_enter(bx, by, bz, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mask |= 4u;
-                                }
-                            }
-                        }
-                        const unsigned sb = __ballot_sync(FULL, mask != 0);
-                        if (lane == 0) P.wcnt[cpar][warp] = __popc(sb);
-                        __syncthreads();
-                        {
-                            int base = nsv, tot = 0;
+                        int nmine = 0;
 #pragma unroll
-                            for (int w = 0; w < kWarpsPerBlock; ++w) {
-                                const int t = P.wcnt[cpar][w];
-                                if (w < warp) base += t;
-                                tot += t;
+                        for (int j = 0; j < kCand; ++j) {
+                            if (gf + j < total_c) {
+                                const int owner = (int)(P.g.it_key[itm[j]] >> 5);
+                                const float fwx = (float)P.wcell[owner][0], fwy = (float)P.wcell[owner][1],
+                                            fwz = (float)P.wcell[owner][2];
+                                const float q0x = P.wq0[owner][0], q0y = P.wq0[owner][1], q0z = P.wq0[owner][2];
+                                const float fdx = P.fdir[owner][0], fdy = P.fdir[owner][1], fdz = P.fdir[owner][2];
+                                const float tlen = P.wtlen[owner];
+                                const float ax = ra[j].x - fwx, ay = ra[j].y - fwy, az = ra[j].z - fwz;
+                                const float bx = rb[j].x - fwx, by = rb[j].y - fwy, bz = rb[j].z - fwz;
+                                u32 mk = 0;
+                                // the tube AND both joint spheres lie inside the segment's bounding sphere
+                                if (may_enter(0.5f * (ax + bx), 0.5f * (ay + by), 0.5f * (az + bz), q0x, q0y, q0z, fdx,
+                                              fdy, fdz, tlen, rb[j].w + reach_pt)) {
+                                    // the tube's entry point lies on the ray within tube_r of the segment's
+                                    // axis line, so the two lines pass within tube_r of each other:
+                                    // |w . (d x u)| <= reach |d x u|  (absolute slack >> float32 rounding)
+                                    const float ux = bx - ax, uy = by - ay, uz = bz - az;
+                                    const float nx = fdy * uz - fdz * uy, ny = fdz * ux - fdx * uz, nz = fdx * uy - fdy * ux;
+                                    const float wn = (ax - q0x) * nx + (ay - q0y) * ny + (az - q0z) * nz;
+                                    if (wn * wn <= reach_pt * reach_pt * (nx * nx + ny * ny + nz * nz) + 1e-6f) mk = 1u;
+                                    if (joints) {
+                                        if (may_enter(ax, ay, az, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mk |= 2u;
+                                        if (may_enter(bx, by, bz, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mk |= 4u;
+                                    }
+                                }
+                                mask[j] = mk;
+                                nmine += mk != 0;
                             }
-                            if (mask) {
-                                const int pos = (sv_head + base + __popc(sb & lt_mask)) & (kSurvCap - 1);
-                                P.g.sv_seg[pos] = seg;
-                                P.g.sv_lin[pos] = lin;
-                                P.g.sv_meta[pos] = (u16)(mask | ((key >> 5) << 8));
-                            }
-                            nsv += tot;
                         }
-                        cpar ^= 1;
+                        // order-preserving append: thread-major, then candidate order
+                        int tot;
+                        int pos = sv_head + nsv + block_scan_excl(nmine, P.wsum[par], lane, warp, tot);
+                        par ^= 1;
+#pragma unroll
+                        for (int j = 0; j < kCand; ++j) {
+                            if (mask[j]) {
+                                const int e = pos++ & (kSurvCap - 1);
+                                const u32 key = P.g.it_key[itm[j]];
+                                P.g.sv_seg[e] = seg[j];
+                                P.g.sv_lin[e] = P.g.it_lin[itm[j]];
+                                P.g.sv_meta[e] = (u16)(mask[j] | ((key >> 5) << 8));
+                            }
+                        }
+                        nsv += tot;
+                        g0 += kChunk;
+                        LVX_CLK(2);
+                        LVX_CNT(11, 1);
+                        LVX_CNT(16, tot);
+                        continue;
                     }
-                    if (nsv < kThreads && g0 + kThreads < total_c) continue;
                     if (nsv == 0) break;
                     __syncthreads();
                     // ---- E: exact float64 tests + ownership, one survivor per thread ---------------------
@@ -642,22 +680,24 @@ render_kernel(const RenderArgs A) {
                         if ((im & 1u) && lvx_tube_f32axis(ox, oy, oz, rdx, rdy, rdz, ra.x, ra.y, ra.z, rb.x, rb.y, rb.z,
                                                           tube_r, h) && t0 <= h.t_in && h.t_in < t1) {
                             hits |= 1u;
-                            P.g.res[e][0] = h.t_in;
+                            P.g.res[tid][0] = h.t_in;
                         }
                         if ((im & 2u) && lvx_sphere<false>(ox, oy, oz, rdx, rdy, rdz, (double)ra.x, (double)ra.y,
                                                            (double)ra.z, tube_r, h) && t0 <= h.t_in && h.t_in < t1) {
                             hits |= 2u;
-                            P.g.res[e][1] = h.t_in;
+                            P.g.res[tid][1] = h.t_in;
                         }
                         if ((im & 4u) && lvx_sphere<false>(ox, oy, oz, rdx, rdy, rdz, (double)rb.x, (double)rb.y,
                                                            (double)rb.z, tube_r, h) && t0 <= h.t_in && h.t_in < t1) {
                             hits |= 4u;
-                            P.g.res[e][2] = h.t_in;
+                            P.g.res[tid][2] = h.t_in;
                         }
                         // (the owner bits stay where the neighbours read them)
                         P.g.sv_meta[e] = (u16)(hits | (((__float_as_uint(ra.w) >> 8) & 31u) << 3) | (im & 0xFF00u));
                     }
                     __syncthreads();
+                    LVX_CLK(3);
+                    LVX_CNT(12, 1);
                     // ---- each owner takes its owned hits in candidate order ------------------------------
                     // (one hit per thread and iteration, so the insertions of different rays run side by side)
                     {
@@ -665,9 +705,10 @@ render_kernel(const RenderArgs A) {
                         const int last = first == 255 ? -1 : (int)P.g.o_last[tid];
                         int j = first == 255 ? 0 : first;
                         u32 hbits = 0, om = 0;
-                        int e = 0;
+                        int e = 0, eb = 0;  // ring slot / batch position of the survivor being taken
                         for (;;) {
                             while (hbits == 0 && j <= last) {
+                                eb = j;
                                 e = (sv_head + j) & (kSurvCap - 1);
                                 om = P.g.sv_meta[e];
                                 hbits = om & 7u;
@@ -677,7 +718,7 @@ render_kernel(const RenderArgs A) {
                             if (hbits == 0) continue;
                             const u32 kind3 = (u32)(__ffs((int)hbits) - 1);
                             hbits &= hbits - 1;
-                            const double t_in = P.g.res[e][kind3];
+                            const double t_in = P.g.res[eb][kind3];
                             const u32 my_ord = ord++;
                             if (my_ord >= (u32)LVX_MAX_WINDOW_HITS) {
                                 // the reference drops hits past its 1024-entry window buffer
@@ -717,6 +758,7 @@ render_kernel(const RenderArgs A) {
                     sv_head = (sv_head + nb) & (kSurvCap - 1);
                     nsv -= nb;
                     __syncthreads();
+                    LVX_CLK(4);
                 }
                 // threads that did not fit this round keep their window and go first in the next one
                 if (pending) continue;
@@ -728,7 +770,9 @@ render_kernel(const RenderArgs A) {
         const bool blocked = walker && (nh >= kHitFlush || nw >= kSlots || spilled);
         const bool any_blocked = __syncthreads_or(blocked) != 0;
         const bool any_walker = __syncthreads_or(walker) != 0;
+        LVX_CLK(9);
         if (any_blocked || !any_walker) {
+            LVX_CNT(17, 1);
             const int n_comp = nh;  // every buffered hit belongs to a completely scanned window
             // Up to kShadeBatch hits per ray and round are listed in shared memory, every thread
             // recomputes one hit (t_out, normal) and its state-free shading terms, then each ray's
@@ -767,6 +811,9 @@ render_kernel(const RenderArgs A) {
                     P.s.res[idx][1] = alpha;
                 }
                 __syncthreads();
+                LVX_CLK(5);
+                LVX_CNT(13, 1);
+                LVX_CNT(18, total);
                 for (int j = 0; j < nb; ++j) {
                     const u32 i = h_seg[q], meta = h_meta[q];
                     const u32 kind3 = meta_kind3(meta);
@@ -799,6 +846,7 @@ render_kernel(const RenderArgs A) {
                     }
                     if (++q >= n_comp) comp = false;
                 }
+                LVX_CLK(6);
                 // (the next listing is fenced from these reads by the barrier inside block_scan_excl)
             }
             // the pools of stages V/C/E overlay the shading pool: restore their idle state
@@ -832,10 +880,12 @@ render_kernel(const RenderArgs A) {
             }
             // a window re-opened after a spill is scanned before anybody walks on
             pending = __syncthreads_or(has_win) != 0;
+            LVX_CLK(6);
             if (!any_walker && !pending) break;
         }
     }
     if (!done) overflow = over_committed;
+    LVX_CLK(6);
 
     // tail: a terminated ray still reports the window count of its full walk
     for (;;) {
@@ -849,6 +899,14 @@ render_kernel(const RenderArgs A) {
         }
     }
 
+    LVX_CLK(7);
+#ifdef LVX_STAGE_CLOCKS
+    if (tid == 0) {
+        s_clk[19] += 1;
+        for (int q = 0; q < 32; ++q)
+            if (s_clk[q]) atomicAdd(&lvx_stage_clk[q], s_clk[q]);
+    }
+#endif
     if (active) {
         // _kernels.py:916-920
         const double a = S.acc[3];
@@ -1001,6 +1059,17 @@ int lvx_render_footprint(const lvx_camera *cam, const lvx_model *model, const lv
                 "footprint instrumentation supports grids up to 1022 per axis");
     return render_impl(cam, model, params, lod, tiling, img_d, row_stats_d, voxel_bits_d, stream);
 }
+
+#ifdef LVX_STAGE_CLOCKS
+// developer builds only: read and reset the stage counters
+int lvx_debug_stage_clocks(unsigned long long *out32) {
+    unsigned long long zero[32] = {0};
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out32, lvx_stage_clk, sizeof(zero));
+    cudaMemcpyToSymbol(lvx_stage_clk, zero, sizeof(zero));
+    return 0;
+}
+#endif
 
 int lvx_untile(const float *tiles_d, const lvx_tiling *tiling, int32_t width, int32_t height,
                float *img_d, void *stream) {

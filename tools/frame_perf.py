@@ -19,6 +19,27 @@ def scene(name):
     m.ao = lv.precompute_voxel_ao(m, oc)
     return dims, m, oc
 
+NAMES = {0: "W walk", 1: "V headers", 2: "C pre-reject", 3: "E exact", 4: "insert", 5: "S list+shade", 6: "S accumulate",
+         7: "tail", 8: "loop top", 9: "S decide", 10: "#rounds", 11: "#C chunks", 12: "#E batches", 13: "#S iters",
+         14: "sum items", 15: "sum candidates", 16: "sum survivors", 17: "#S stages", 18: "sum shaded", 19: "#blocks"}
+
+def dump_stage_clocks(quiet=False):
+    import ctypes
+    from paper_1801_01155_b200 import _lib
+    L = _lib.lib()
+    if not hasattr(L, "lvx_debug_stage_clocks"):
+        return
+    buf = (ctypes.c_uint64 * 32)()
+    L.lvx_debug_stage_clocks(buf)
+    v = list(buf)
+    if quiet:
+        return
+    tot = sum(v[:10]) or 1
+    for k in range(10):
+        print(f"   clk {NAMES[k]:14s} {v[k]/tot*100:5.1f}%  {v[k]/max(v[19],1):12.0f} cyc/block")
+    for k in range(10, 20):
+        print(f"   cnt {NAMES[k]:14s} {v[k]/5:14.0f} /frame  {v[k]/max(v[19],1):10.2f} /block")
+
 def main():
     names = sys.argv[1:] or ["c3"]
     for name in names:
@@ -38,6 +59,7 @@ def main():
             for _ in range(2):
                 plan.launch(img, st)
             torch.cuda.synchronize()
+            dump_stage_clocks(quiet=True)
             st.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -46,6 +68,7 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             h = hashlib.sha256(img.cpu().numpy().tobytes()).hexdigest()[:12]
+            dump_stage_clocks()
             print(f"[{name} {label}] S={m.segment_count} {e0.elapsed_time(e1)/5:.3f} ms  img {h} stats {(st.sum(0)//5).tolist()}", flush=True)
 
 main()
