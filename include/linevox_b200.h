@@ -248,6 +248,20 @@ int lvx_render(const lvx_camera *cam, const lvx_model *model, const lvx_params *
  * voxel and, in neighbour mode, its 26 in-grid neighbours, for every non-skipped
  * window up to early termination.  Distinct voxels / their segments give the
  * unique-bytes-touched figure of SURVEY.md 8(d). */
+/* Wavefront frame path (csrc/lvx_wavefront.cu): the same frame as lvx_render -- same image,
+ * same row_stats -- computed by streaming kernels over device queues (init / walk /
+ * candidates / exact / composite, iterated until every ray is finished) instead of one
+ * monolithic kernel.  Replaces the same reference call, _kernels.render_rows
+ * (_kernels.py:735-923, called from raycast.py:498-510).  `scratch_d` is caller-owned,
+ * 256-byte aligned, at least lvx_render_wf_scratch_bytes(cam, tiling, scale) bytes;
+ * `scale` >= 1 enlarges the queues.  Returns LVX_E_RANGE when a queue overflowed (the
+ * image is then undefined): call again with a larger scale.  Synchronises the stream. */
+size_t lvx_render_wf_scratch_bytes(const lvx_camera *cam, const lvx_tiling *tiling, double scale);
+int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_params *params,
+                  const lvx_lod *lod, const lvx_tiling *tiling, float *img_d,
+                  int64_t *row_stats_d, void *scratch_d, size_t scratch_bytes, double scale,
+                  void *stream);
+
 int lvx_render_footprint(const lvx_camera *cam, const lvx_model *model, const lvx_params *params,
                          const lvx_lod *lod, const lvx_tiling *tiling, float *img_d,
                          int64_t *row_stats_d, uint32_t *voxel_bits_d, void *stream);

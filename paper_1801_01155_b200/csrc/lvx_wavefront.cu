@@ -1,0 +1,1131 @@
+// Wavefront ray-caster for sm_100a: the frame is computed by a short sequence of
+// streaming kernels over device-resident queues instead of one monolithic kernel.
+//
+//   render_rows   _kernels.py:735-923     stream_hit   _kernels.py:650-730
+//   dda_collect   _kernels.py:164-256     _hit_before  _kernels.py:261-270
+//   _seen_check_and_mark / _sphere_seen   _kernels.py:625-647
+//
+// Why: the per-ray work of the reference is a chain of dependent, data-dependent steps
+// (walk -> gather 27 voxels -> intersect -> sort -> composite -> maybe terminate).  Bound
+// to one thread (or one block) per ray that chain is latency-bound at low occupancy: the
+// float64 tests need ~170 registers, the rays of a warp diverge, and the tile kernel
+// (lvx_render.cu) spends most of its cycles at block barriers.  Here every link of the
+// chain is its own kernel over ALL live rays, with its own register budget, full
+// occupancy and every lane busy; the links talk through queues in HBM (a few GB/s of
+// traffic per frame, three orders of magnitude below what the 7.7 TB/s can carry):
+//
+//   init       one thread per pixel: primary ray, slab clip, full-walk window count
+//              (`voxel_steps`), background for rays that miss; live rays are listed.
+//   walk       one thread per live ray: advance the DDA by a budget of non-empty windows,
+//              cull the 27-neighbourhood to the voxels that can own a hit, write one
+//              window record per window and one item (window, neighbour) per voxel.
+//   candidates one thread per item: voxel header, conservative float32 pre-reject of
+//              every segment against the window; survivors are queued.
+//   exact      one thread per survivor: exact float64 tube / joint-sphere tests, the
+//              ownership test t0 <= t_in < t1, state-free shading of the owned hits
+//              (AO / cone shadow / Blinn / alpha); hits go to a pool and are linked into
+//              their ray's list.
+//   composite  one thread per live ray: order the ray's hits by the reference's key
+//              (t_in, home voxel, lid, kind, gather order), apply the de-duplication
+//              rules, blend front to back, terminate at tau; finished rays write their
+//              pixel and counters, the others are listed for the next iteration.
+//
+// The composited sequence, the image and the three counters are the reference's:
+//  * gather order inside a window is (voxel z,y,x scan, segment, tube/A/B), which is the
+//    order of (segment index, primitive) because records are stored in voxel scan order;
+//    so the total order is a function of the hit alone and no ordinal has to be carried;
+//  * `intersection_tests` is cumulative per window (neighbour-sum grid) and a terminated
+//    ray reports the value of the window that owns its last composited hit;
+//  * the 1024-hits-per-window cap (`window_overflow`) can only bite in windows whose
+//    candidate count exceeds 1024/3; those are flagged and handled by an exact slow path.
+#include <cooperative_groups.h>
+#include <cooperative_groups/scan.h>
+#include <math_constants.h>
+
+#include "lvx_geom.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace {
+
+constexpr int kNQ = 64;            // sub-queues per queue (spreads the allocation atomics)
+constexpr int kInline = 16;        // de-duplication table entries kept inline per ray
+constexpr int kThreadsWf = 256;
+constexpr int kSortCap = 48;       // hits per ray and iteration sorted in local memory
+constexpr u32 kNil = 0xFFFFFFFFu;
+constexpr double kCullMarginWf = 1e-4;
+constexpr float kRejectMarginWf = 2e-3f;
+
+struct __align__(16) WfWindow {
+    double t0, t1;
+    unsigned long long tests;  // intersection_tests up to and including this window
+    u32 slot;                  // ray
+    u32 cxy;                   // cell (x + 1) | (y + 1) << 16
+    u32 cz;                    // cell (z + 1) | big << 31
+    float q0x, q0y, q0z, tlen;
+    u32 pad[3];
+};
+static_assert(sizeof(WfWindow) == 64, "window record is 64 bytes");
+
+struct __align__(16) WfHit {
+    double t_in, scale, alpha;
+    u32 lin, seg, meta, next;  // meta: kind3 2 | lid 5 << 2 | attr 8 << 8 | dropped << 16
+    u32 wid, pad;
+};
+static_assert(sizeof(WfHit) == 48, "hit record is 48 bytes");
+
+struct WfSurv {
+    u32 seg, wid, mb;  // mb: primitive mask 3 | neighbour bit << 3
+};
+
+// control block in device memory
+struct WfCtl {
+    u32 n_live[2];
+    u32 item_cnt[kNQ], surv_cnt[kNQ], hit_cnt[kNQ];
+    u32 pool_cnt;
+    u32 err;   // bit 0 items, 1 survivors, 2 hits, 3 table pool
+    u32 wn;    // windows per ray of the current iteration
+};
+
+struct WfArgs {
+    lvx_camera cam;
+    lvx_params p;
+    int rx, ry, rz;
+    const u8 *counts;
+    const u32 *offsets;
+    const lvx_seg_record *rec;
+    const float *table;
+    const u16 *nsum;
+    const u32 *nmask;
+    LvxOctree oc;
+    const float *ao_flat;
+    const double *ao_dirs;
+    lvx_tiling tl;
+    int tiles_x, n_my_tiles;
+    float *img;
+    unsigned long long *row_stats;
+    // scratch
+    u32 R;          // ray slots (threads of init)
+    WfCtl *ctl;
+    u32 *pix, *out_off;
+    double *dir;    // [3][R]
+    double *dda_t;  // [5][R]: t_cur, t_exit, tmax x/y/z
+    int *dda_i;     // [3][R]
+    u8 *flags;      // bit 0 walk alive, bit 1 big window seen this iteration
+    double *acc;    // [4][R]
+    unsigned long long *tests, *over, *seen_bloom, *sph_bloom;
+    u32 *n_seen, *n_sph, *ovf, *head, *nwin;
+    u32 *tab_key, *tab_mask;   // [kInline][R]
+    float *tab_sph;            // [3][kInline][R]
+    u32 *pool_key, *pool_mask; // [pool_cap][LVX_MAX_SEEN - kInline]
+    float *pool_sph;           // [pool_cap][LVX_MAX_SEEN - kInline][3]
+    u32 pool_cap;
+    u32 *live[2];
+    WfWindow *win;
+    u32 cap_win;
+    u32 *item_wid;
+    u8 *item_b;
+    u32 capq_item;
+    WfSurv *surv;
+    u32 capq_surv;
+    WfHit *hit;
+    u32 capq_hit;
+    u32 *win_over;  // [cap_win] overflow of a window (slow path only)
+    int wn_sched, cand_budget;
+};
+
+__device__ __forceinline__ int warp_queue() {
+    return (int)(((blockIdx.x * (blockDim.x >> 5)) + (threadIdx.x >> 5)) & (kNQ - 1));
+}
+
+// Allocate `n` consecutive entries of sub-queue q for this thread (aggregated over the
+// currently converged lanes).  Returns the global index or kNil when the queue is full.
+__device__ __forceinline__ u32 queue_alloc(u32 *cnt, int q, u32 capq, u32 n, u32 *err, u32 err_bit) {
+    cg::coalesced_group g = cg::coalesced_threads();
+    const u32 pre = cg::exclusive_scan(g, n);
+    u32 base = 0;
+    if (g.thread_rank() == g.size() - 1) base = atomicAdd(&cnt[q], pre + n);
+    base = g.shfl(base, g.size() - 1);
+    if (base + pre + n > capq) {
+        atomicOr(err, err_bit);
+        return kNil;
+    }
+    return (u32)q * capq + base + pre;
+}
+
+// Flat index over the filled parts of the kNQ sub-queues -> global entry index.
+struct QueueView {
+    u32 pre[kNQ + 1];
+};
+__device__ __forceinline__ void queue_view_load(QueueView &v, const u32 *cnt, u32 capq) {
+    // (called by all threads of the block; v lives in shared memory)
+    if (threadIdx.x == 0) {
+        u32 run = 0;
+        for (int q = 0; q < kNQ; ++q) {
+            v.pre[q] = run;
+            const u32 c = cnt[q];
+            run += c < capq ? c : capq;
+        }
+        v.pre[kNQ] = run;
+    }
+    __syncthreads();
+}
+__device__ __forceinline__ u32 queue_view_index(const QueueView &v, u32 f, u32 capq) {
+    int lo = 0, hi = kNQ;  // pre[lo] <= f < pre[hi]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (v.pre[mid] <= f) lo = mid;
+        else hi = mid;
+    }
+    return (u32)lo * capq + (f - v.pre[lo]);
+}
+
+__device__ __forceinline__ void ray_dir(const lvx_camera &cam, int x, int y, double &ddx, double &ddy,
+                                        double &ddz) {
+    // primary ray, _kernels.py:769-776
+    const int W = cam.width, H = cam.height;
+    const double ndc_x = (((double)x + 0.5) / (double)W * 2.0 - 1.0) * cam.tan_half * cam.aspect;
+    const double ndc_y = (1.0 - ((double)y + 0.5) / (double)H * 2.0) * cam.tan_half;
+    ddx = cam.f[0] + ndc_x * cam.r[0] + ndc_y * cam.u[0];
+    ddy = cam.f[1] + ndc_x * cam.r[1] + ndc_y * cam.u[1];
+    ddz = cam.f[2] + ndc_x * cam.r[2] + ndc_y * cam.u[2];
+    const double dn = sqrt(ddx * ddx + ddy * ddy + ddz * ddz);
+    ddx = ddx / dn;
+    ddy = ddy / dn;
+    ddz = ddz / dn;
+}
+
+__device__ __forceinline__ void write_pixel(const WfArgs &A, u32 o, double a0, double a1, double a2,
+                                            double a) {
+    // _kernels.py:916-920
+    const lvx_params &p = A.p;
+    float4 outp;
+    outp.x = (float)(a0 + (1.0 - a) * p.bg[3] * p.bg[0]);
+    outp.y = (float)(a1 + (1.0 - a) * p.bg[3] * p.bg[1]);
+    outp.z = (float)(a2 + (1.0 - a) * p.bg[3] * p.bg[2]);
+    outp.w = (float)(a + (1.0 - a) * p.bg[3]);
+    reinterpret_cast<float4 *>(A.img)[o] = outp;
+}
+
+__device__ __forceinline__ void dda_store(const WfArgs &A, u32 s, const LvxDda &d) {
+    const size_t R = A.R;
+    A.dda_t[s] = d.t_cur;
+    A.dda_t[R + s] = d.t_exit;
+    A.dda_t[2 * R + s] = d.tmax_x;
+    A.dda_t[3 * R + s] = d.tmax_y;
+    A.dda_t[4 * R + s] = d.tmax_z;
+    A.dda_i[s] = d.ix;
+    A.dda_i[R + s] = d.iy;
+    A.dda_i[2 * R + s] = d.iz;
+}
+
+// Rebuild the walker from its stored progress (the constants are functions of the ray).
+__device__ __forceinline__ void dda_load(const WfArgs &A, u32 s, double dx, double dy, double dz,
+                                         int pad, LvxDda &d) {
+    const size_t R = A.R;
+    d.t_cur = A.dda_t[s];
+    d.t_exit = A.dda_t[R + s];
+    d.tmax_x = A.dda_t[2 * R + s];
+    d.tmax_y = A.dda_t[3 * R + s];
+    d.tmax_z = A.dda_t[4 * R + s];
+    d.ix = A.dda_i[s];
+    d.iy = A.dda_i[R + s];
+    d.iz = A.dda_i[2 * R + s];
+    d.step_x = dx > 0.0 ? 1 : (dx < 0.0 ? -1 : 0);
+    d.step_y = dy > 0.0 ? 1 : (dy < 0.0 ? -1 : 0);
+    d.step_z = dz > 0.0 ? 1 : (dz < 0.0 ? -1 : 0);
+    const double big = CUDART_INF;
+    d.tdel_x = d.step_x != 0 ? fabs(1.0 / dx) : big;
+    d.tdel_y = d.step_y != 0 ? fabs(1.0 / dy) : big;
+    d.tdel_z = d.step_z != 0 ? fabs(1.0 / dz) : big;
+    d.ilo = -pad;
+    d.ihx = A.rx + pad - 1;
+    d.ihy = A.ry + pad - 1;
+    d.ihz = A.rz + pad - 1;
+    d.alive = true;
+}
+
+// ---------------------------------------------------------------------------------------
+// init: one thread per pixel (8x4 tiles per warp, the tile kernel's mapping)
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreadsWf) wf_init_kernel(const WfArgs A) {
+    constexpr unsigned FULL = 0xFFFFFFFFu;
+    const int lane = threadIdx.x & 31;
+    const i64 gw = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int wpt_x = A.tl.tile_w >> 3, wpt_y = A.tl.tile_h >> 2;
+    const int warps_per_tile = wpt_x * wpt_y;
+    const i64 k = gw / warps_per_tile;
+    const int wi = (int)(gw % warps_per_tile);
+    const bool tile_ok = k < A.n_my_tiles;
+    const i64 tile = (i64)A.tl.tile_first + k * A.tl.tile_step;
+    const int tx = (int)(tile % A.tiles_x), ty = (int)(tile / A.tiles_x);
+    const int lx = (wi % wpt_x) * 8 + (lane & 7), ly = (wi / wpt_x) * 4 + (lane >> 3);
+    const int x = tx * A.tl.tile_w + lx, y = ty * A.tl.tile_h + ly;
+    const int W = A.cam.width, H = A.cam.height;
+    const bool active = tile_ok && x < W && y < H;
+    const u32 slot = (u32)(gw * 32 + lane);
+
+    unsigned long long steps = 0;
+    bool live = false;
+    if (active) {
+        double ddx, ddy, ddz;
+        ray_dir(A.cam, x, y, ddx, ddy, ddz);
+        const int pad = A.p.neighbor != 0 ? 1 : 0;
+        LvxDda dda;
+        dda.init(A.cam.o[0], A.cam.o[1], A.cam.o[2], ddx, ddy, ddz, A.rx, A.ry, A.rz, pad);
+        i64 o;
+        if (A.tl.compact) o = ((k * A.tl.tile_h + ly) * (i64)A.tl.tile_w + lx);
+        else o = (i64)y * W + x;
+        if (dda.alive) {
+            // the reference collects the whole walk up front (:785-786): voxel_steps does not
+            // depend on where compositing stops
+            LvxDda full = dda;
+            int wx, wy, wz;
+            double t0, t1;
+            while (full.next(wx, wy, wz, t0, t1)) steps += 1;
+            const size_t R = A.R;
+            A.pix[slot] = (u32)x | ((u32)y << 16);
+            A.out_off[slot] = (u32)o;
+            A.dir[slot] = ddx;
+            A.dir[R + slot] = ddy;
+            A.dir[2 * R + slot] = ddz;
+            dda_store(A, slot, dda);
+            A.flags[slot] = 1;
+            A.acc[slot] = 0.0;
+            A.acc[R + slot] = 0.0;
+            A.acc[2 * R + slot] = 0.0;
+            A.acc[3 * R + slot] = 0.0;
+            A.tests[slot] = 0;
+            A.over[slot] = 0;
+            A.seen_bloom[slot] = 0;
+            A.sph_bloom[slot] = 0;
+            A.n_seen[slot] = 0;
+            A.n_sph[slot] = 0;
+            A.ovf[slot] = kNil;
+            A.head[slot] = kNil;
+            A.nwin[slot] = 0;
+            live = true;
+        } else {
+            write_pixel(A, (u32)o, 0.0, 0.0, 0.0, 0.0);
+        }
+    }
+    // list the live rays (warp order keeps neighbouring pixels together)
+    const unsigned lb = __ballot_sync(FULL, live);
+    if (lb) {
+        u32 base = 0;
+        if (lane == 0) base = atomicAdd(&A.ctl->n_live[0], (u32)__popc(lb));
+        base = __shfl_sync(FULL, base, 0);
+        if (live) A.live[0][base + __popc(lb & ((1u << lane) - 1u))] = slot;
+    }
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) steps += __shfl_xor_sync(FULL, steps, o);
+    if ((lane & 7) == 0 && tile_ok && y < H && steps) atomicAdd(A.row_stats + 3 * (i64)y, steps);
+}
+
+// ---------------------------------------------------------------------------------------
+// walk: one thread per live ray
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreadsWf) wf_walk_kernel(const WfArgs A, int par) {
+    const u32 n_live = A.ctl->n_live[par];
+    const u32 wn = A.ctl->wn;
+    const lvx_params &p = A.p;
+    const bool neighbor = p.neighbor != 0;
+    const int rx = A.rx, ry = A.ry;
+    const u32 tmul = p.joints != 0 ? 3u : 1u;
+    const double cull = p.tube_r + kCullMarginWf;
+    const double ox = A.cam.o[0], oy = A.cam.o[1], oz = A.cam.o[2];
+    const int q = warp_queue();
+    const size_t R = A.R;
+    for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n_live; i += gridDim.x * blockDim.x) {
+        const u32 slot = A.live[par][i];
+        const double ddx = A.dir[slot], ddy = A.dir[R + slot], ddz = A.dir[2 * R + slot];
+        LvxDda dda;
+        dda_load(A, slot, ddx, ddy, ddz, neighbor ? 1 : 0, dda);
+        unsigned long long tests = A.tests[slot];
+        u32 kw = 0, csum = 0;
+        bool big_any = false;
+        while (kw < wn && csum < (u32)A.cand_budget) {
+            int wx, wy, wz;
+            double t0, t1;
+            if (!dda.next(wx, wy, wz, t0, t1)) break;
+            u32 nm, n;
+            if (neighbor) {
+                const i64 pc = ((i64)(wz + 1) * (ry + 2) + (wy + 1)) * (rx + 2) + (wx + 1);
+                nm = __ldg(A.nmask + pc);
+                n = nm ? (u32)__ldg(A.nsum + pc) : 0u;
+            } else {
+                n = __ldg(A.counts + (wx + (i64)rx * (wy + (i64)ry * wz)));
+                nm = n ? (1u << 13) : 0u;
+            }
+            if (nm == 0) continue;  // the reference's cheap skip (:793-799)
+            tests += (unsigned long long)n * tmul;  // :833,855 summed over the window's gather
+            const double p0x = ox + t0 * ddx, p0y = oy + t0 * ddy, p0z = oz + t0 * ddz;
+            if (neighbor) {
+                // neighbour voxels that can own a hit of this window: within tube_r of the
+                // bounding box of the ray piece inside the window's voxel
+                const double p1x = ox + t1 * ddx, p1y = oy + t1 * ddy, p1z = oz + t1 * ddz;
+                u32 bx_ = 0x2492492u, by_ = 0x0E07038u, bz_ = 0x003FE00u;
+                if (fmin(p0x, p1x) - cull < (double)wx) bx_ |= 0x1249249u;
+                if (fmax(p0x, p1x) + cull > (double)(wx + 1)) bx_ |= 0x4924924u;
+                if (fmin(p0y, p1y) - cull < (double)wy) by_ |= 0x01C0E07u;
+                if (fmax(p0y, p1y) + cull > (double)(wy + 1)) by_ |= 0x70381C0u;
+                if (fmin(p0z, p1z) - cull < (double)wz) bz_ |= 0x00001FFu;
+                if (fmax(p0z, p1z) + cull > (double)(wz + 1)) bz_ |= 0x7FC0000u;
+                nm &= bx_ & by_ & bz_;
+            }
+            csum += n;
+            if (nm == 0) continue;
+            const bool big = n * tmul > (u32)LVX_MAX_WINDOW_HITS;
+            big_any |= big;
+            const u32 wid = i * wn + kw;
+            const u32 ni = (u32)__popc(nm);
+            const u32 ib = queue_alloc(A.ctl->item_cnt, q, A.capq_item, ni, &A.ctl->err, 1u);
+            WfWindow w;
+            w.t0 = t0;
+            w.t1 = t1;
+            w.tests = tests;
+            w.slot = slot;
+            w.cxy = (u32)(wx + 1) | ((u32)(wy + 1) << 16);  // padded-grid coordinates (the walk starts at -1)
+            w.cz = (u32)(wz + 1) | (big ? 0x80000000u : 0u);
+            w.q0x = (float)(p0x - (double)wx);  // window-local float32 frame
+            w.q0y = (float)(p0y - (double)wy);
+            w.q0z = (float)(p0z - (double)wz);
+            w.tlen = (float)(t1 - t0);
+            w.pad[0] = w.pad[1] = w.pad[2] = 0;
+            A.win[wid] = w;
+            if (big) A.win_over[wid] = 0;
+            if (ib != kNil) {
+                u32 j = ib;
+                for (u32 mm = nm; mm; mm &= mm - 1, ++j) {
+                    A.item_wid[j] = wid;
+                    A.item_b[j] = (u8)(__ffs((int)mm) - 1);
+                }
+            }
+            kw += 1;
+        }
+        dda_store(A, slot, dda);
+        A.tests[slot] = tests;
+        A.nwin[slot] = kw;
+        A.flags[slot] = (u8)((dda.alive ? 1 : 0) | (big_any ? 2 : 0));
+    }
+}
+
+// Conservative float32 test in window-local coordinates (see lvx_render.cu).
+__device__ __forceinline__ bool wf_may_enter(float cx, float cy, float cz, float q0x, float q0y,
+                                             float q0z, float dx, float dy, float dz, float tlen,
+                                             float reach) {
+    const float wx = cx - q0x, wy = cy - q0y, wz = cz - q0z;
+    const float tc = wx * dx + wy * dy + wz * dz;
+    const float d2 = (wx * wx + wy * wy + wz * wz) - tc * tc;
+    return d2 <= reach * reach && tc >= -reach && tc <= tlen + reach;
+}
+
+// ---------------------------------------------------------------------------------------
+// candidates: one thread per (window, neighbour voxel) item
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreadsWf) wf_cand_kernel(const WfArgs A) {
+    __shared__ QueueView V;
+    queue_view_load(V, A.ctl->item_cnt, A.capq_item);
+    const u32 total = V.pre[kNQ];
+    const bool joints = A.p.joints != 0;
+    const float reach_pt = (float)A.p.tube_r + kRejectMarginWf;
+    const int q = warp_queue();
+    const size_t R = A.R;
+    for (u32 f = blockIdx.x * blockDim.x + threadIdx.x; f < total; f += gridDim.x * blockDim.x) {
+        const u32 it = queue_view_index(V, f, A.capq_item);
+        const u32 wid = A.item_wid[it];
+        const int b = (int)A.item_b[it];
+        const WfWindow *wp = A.win + wid;
+        const uint4 w1 = __ldg(reinterpret_cast<const uint4 *>(wp) + 1);  // tests(2) slot cxy
+        const uint4 w2 = __ldg(reinterpret_cast<const uint4 *>(wp) + 2);  // cz q0x q0y q0z
+        const float tlen = __ldg(&wp->tlen);
+        const u32 slot = w1.z;
+        const int cx = (int)(w1.w & 0xFFFFu) - 1, cy = (int)(w1.w >> 16) - 1, cz = (int)(w2.x & 0x7FFFFFFFu) - 1;
+        const float q0x = __uint_as_float(w2.y), q0y = __uint_as_float(w2.z), q0z = __uint_as_float(w2.w);
+        const float fdx = (float)A.dir[slot], fdy = (float)A.dir[R + slot], fdz = (float)A.dir[2 * R + slot];
+        const int bz_ = b / 9, by_ = (b - 9 * bz_) / 3, bx_ = b - 9 * bz_ - 3 * by_;
+        const u32 lin = (u32)((cx + bx_ - 1) + A.rx * ((cy + by_ - 1) + A.ry * (cz + bz_ - 1)));
+        const u32 cnt = __ldg(A.counts + lin);
+        const u32 base = __ldg(A.offsets + lin);
+        const float fwx = (float)cx, fwy = (float)cy, fwz = (float)cz;
+        for (u32 s = 0; s < cnt; ++s) {
+            const u32 seg = base + s;
+            const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + seg));
+            const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + seg) + 1);
+            const float ax = ra.x - fwx, ay = ra.y - fwy, az = ra.z - fwz;
+            const float bx = rb.x - fwx, by = rb.y - fwy, bz = rb.z - fwz;
+            u32 mk = 0;
+            // the tube AND both joint spheres lie inside the segment's bounding sphere
+            if (wf_may_enter(0.5f * (ax + bx), 0.5f * (ay + by), 0.5f * (az + bz), q0x, q0y, q0z, fdx, fdy,
+                             fdz, tlen, rb.w + reach_pt)) {
+                // the tube's entry point lies on the ray within tube_r of the segment's axis line:
+                // |w . (d x u)| <= reach |d x u|  (absolute slack >> float32 rounding)
+                const float ux = bx - ax, uy = by - ay, uz = bz - az;
+                const float nx = fdy * uz - fdz * uy, ny = fdz * ux - fdx * uz, nz = fdx * uy - fdy * ux;
+                const float wn = (ax - q0x) * nx + (ay - q0y) * ny + (az - q0z) * nz;
+                if (wn * wn <= reach_pt * reach_pt * (nx * nx + ny * ny + nz * nz) + 1e-6f) mk = 1u;
+                if (joints) {
+                    if (wf_may_enter(ax, ay, az, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mk |= 2u;
+                    if (wf_may_enter(bx, by, bz, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mk |= 4u;
+                }
+            }
+            if (mk) {
+                const u32 e = queue_alloc(A.ctl->surv_cnt, q, A.capq_surv, 1u, &A.ctl->err, 2u);
+                if (e != kNil) {
+                    WfSurv sv;
+                    sv.seg = seg;
+                    sv.wid = wid;
+                    sv.mb = mk | ((u32)b << 3);
+                    A.surv[e] = sv;
+                }
+            }
+        }
+    }
+}
+
+// state-free half of stream_hit (_kernels.py:673-718): shadow term, AO term, alpha, Blinn scale
+__device__ __forceinline__ void wf_shade(const WfArgs &A, double ox, double oy, double oz, double ddx,
+                                         double ddy, double ddz, const LvxHit &h, u32 attr,
+                                         double &scale_out, double &alpha_out) {
+    const lvx_params &p = A.p;
+    const double gx = (double)A.rx, gy = (double)A.ry, gz = (double)A.rz;
+    const double px = ox + h.t_in * ddx, py = oy + h.t_in * ddy, pz = oz + h.t_in * ddz;
+    double shadow_term = 0.0;
+    if (p.shadow_mode == LVX_SHADOW_CONE)
+        shadow_term = lvx_cone_blocking(px, py, pz, p.light[0], p.light[1], p.light[2], A.oc, gx, gy, gz, 0.01);
+    double ao_term = 0.0;
+    if (p.ao_mode == LVX_AO_PRECOMPUTED) {
+        ao_term = lvx_trilinear(A.ao_flat, 0, A.rx, A.ry, A.rz, 1.0, px, py, pz);
+        if (ao_term > 1.0) ao_term = 1.0;
+        if (ao_term < 0.0) ao_term = 0.0;
+    } else if (p.ao_mode == LVX_AO_DENSITY) {
+        ao_term = lvx_ao_density_point(px, py, pz, h.nx, h.ny, h.nz, p.ao_n_rays, p.ao_radius, 1.0,
+                                       A.ao_dirs, A.oc.flat, A.rx, A.ry, A.rz);
+    }
+    const float table_alpha = __ldg(A.table + 4 * attr + 3);
+    alpha_out = lvx_alpha_of(p.opacity_mode, p.base_alpha, (double)table_alpha, h.t_in, h.t_out);
+    double lgx, lgy, lgz;
+    if (p.headlight != 0) {
+        lgx = -ddx;
+        lgy = -ddy;
+        lgz = -ddz;
+    } else {
+        lgx = p.light[0];
+        lgy = p.light[1];
+        lgz = p.light[2];
+    }
+    double scale = lvx_shade(h.nx, h.ny, h.nz, lgx, lgy, lgz, -ddx, -ddy, -ddz, p.ka * (1.0 - ao_term),
+                             p.kd, p.ks, p.shininess);
+    scale *= 1.0 - shadow_term;
+    scale_out = scale;
+}
+
+// ---------------------------------------------------------------------------------------
+// exact: one thread per survivor
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreadsWf) wf_exact_kernel(const WfArgs A) {
+    __shared__ QueueView V;
+    queue_view_load(V, A.ctl->surv_cnt, A.capq_surv);
+    const u32 total = V.pre[kNQ];
+    const double ox = A.cam.o[0], oy = A.cam.o[1], oz = A.cam.o[2];
+    const double tube_r = A.p.tube_r;
+    const int q = warp_queue();
+    const size_t R = A.R;
+    for (u32 f = blockIdx.x * blockDim.x + threadIdx.x; f < total; f += gridDim.x * blockDim.x) {
+        const WfSurv sv = A.surv[queue_view_index(V, f, A.capq_surv)];
+        const WfWindow *wp = A.win + sv.wid;
+        const double t0 = __ldg(&wp->t0), t1 = __ldg(&wp->t1);
+        const u32 slot = __ldg(&wp->slot);
+        const u32 cxy = __ldg(&wp->cxy), czb = __ldg(&wp->cz);
+        const double rdx = A.dir[slot], rdy = A.dir[R + slot], rdz = A.dir[2 * R + slot];
+        const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + sv.seg));
+        const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + sv.seg) + 1);
+        const int b = (int)(sv.mb >> 3);
+        const int bz_ = b / 9, by_ = (b - 9 * bz_) / 3, bx_ = b - 9 * bz_ - 3 * by_;
+        const u32 lin = (u32)(((int)(cxy & 0xFFFFu) + bx_ - 2) +
+                              A.rx * (((int)(cxy >> 16) + by_ - 2) + A.ry * ((int)(czb & 0x7FFFFFFFu) + bz_ - 2)));
+        const u32 rmeta = __float_as_uint(ra.w);
+        const u32 attr = rmeta & 0xFFu, lid = (rmeta >> 8) & 31u;
+#pragma unroll 1
+        for (u32 kind3 = 0; kind3 < 3; ++kind3) {
+            if (!(sv.mb & (1u << kind3))) continue;
+            LvxHit h;
+            bool hit;
+            if (kind3 == 0) {
+                hit = lvx_tube_f32axis(ox, oy, oz, rdx, rdy, rdz, ra.x, ra.y, ra.z, rb.x, rb.y, rb.z, tube_r, h);
+            } else {
+                const float cx = kind3 == 1 ? ra.x : rb.x, cy = kind3 == 1 ? ra.y : rb.y,
+                            cz = kind3 == 1 ? ra.z : rb.z;
+                hit = lvx_sphere<true>(ox, oy, oz, rdx, rdy, rdz, (double)cx, (double)cy, (double)cz, tube_r, h);
+            }
+            // ownership: the window whose range holds the entry parameter (:838, :858, :878)
+            if (!(hit && t0 <= h.t_in && h.t_in < t1)) continue;
+            double scale, alpha;
+            wf_shade(A, ox, oy, oz, rdx, rdy, rdz, h, attr, scale, alpha);
+            const u32 e = queue_alloc(A.ctl->hit_cnt, q, A.capq_hit, 1u, &A.ctl->err, 4u);
+            if (e == kNil) continue;
+            WfHit rec;
+            rec.t_in = h.t_in;
+            rec.scale = scale;
+            rec.alpha = alpha;
+            rec.lin = lin;
+            rec.seg = sv.seg;
+            rec.meta = kind3 | (lid << 2) | (attr << 8);
+            rec.wid = sv.wid;
+            rec.pad = 0;
+            rec.next = atomicExch(&A.head[slot], e);
+            A.hit[e] = rec;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// composite: one thread per live ray
+// ---------------------------------------------------------------------------------------
+
+// total order of the reference: _hit_before (_kernels.py:261-270) = (t_in, home voxel, lid,
+// kind), remaining ties in gather order = (segment, primitive)
+__device__ __forceinline__ bool wf_key_before(double ta, u32 la, u32 sa, u32 ma, double tb, u32 lb,
+                                              u32 sb, u32 mb) {
+    if (ta != tb) return ta < tb;
+    if (la != lb) return la < lb;
+    const u32 lida = (ma >> 2) & 31u, lidb = (mb >> 2) & 31u;
+    if (lida != lidb) return lida < lidb;
+    const u32 ka = (ma & 3u) ? 1u : 0u, kb = (mb & 3u) ? 1u : 0u;
+    if (ka != kb) return ka < kb;
+    if (sa != sb) return sa < sb;
+    return (ma & 3u) < (mb & 3u);
+}
+
+struct WfTables {
+    const WfArgs &A;
+    u32 slot;
+    u32 ovf;
+    __device__ __forceinline__ u32 *key(u32 i) const {
+        return i < (u32)kInline ? A.tab_key + (size_t)i * A.R + slot
+                                : A.pool_key + (size_t)ovf * (LVX_MAX_SEEN - kInline) + (i - kInline);
+    }
+    __device__ __forceinline__ u32 *mask(u32 i) const {
+        return i < (u32)kInline ? A.tab_mask + (size_t)i * A.R + slot
+                                : A.pool_mask + (size_t)ovf * (LVX_MAX_SEEN - kInline) + (i - kInline);
+    }
+    __device__ __forceinline__ float *sph(u32 i, int c) const {
+        return i < (u32)kInline ? A.tab_sph + ((size_t)c * kInline + i) * A.R + slot
+                                : A.pool_sph + ((size_t)ovf * (LVX_MAX_SEEN - kInline) + (i - kInline)) * 3 + c;
+    }
+};
+
+struct WfPixel {
+    double acc[4];
+    u32 n_seen, n_sph;
+    unsigned long long seen_bloom, sph_bloom;
+};
+
+// de-duplication + front-to-back accumulation of stream_hit (_kernels.py:666-670, 719-730).
+// Returns false when the pool of overflow tables is exhausted (reported through ctl->err).
+__device__ __forceinline__ void wf_accumulate(const WfArgs &A, WfTables &T, WfPixel &S, double scale,
+                                              double alpha, u32 lin, u32 lid, u32 attr, bool is_sphere,
+                                              float cx, float cy, float cz) {
+    unsigned long long sph_bit = 0;
+    if (is_sphere) {
+        const u32 hsh = (__float_as_uint(cx) * 0x9E3779B1u) ^ (__float_as_uint(cy) * 0x85EBCA77u) ^
+                        (__float_as_uint(cz) * 0xC2B2AE3Du);
+        sph_bit = 1ull << (hsh >> 26);
+        if (S.sph_bloom & sph_bit) {
+            for (int i = (int)S.n_sph - 1; i >= 0; --i)
+                if (*T.sph(i, 0) == cx && *T.sph(i, 1) == cy && *T.sph(i, 2) == cz) return;
+        }
+    }
+    const bool need_pool = (S.n_seen == (u32)kInline || (is_sphere && S.n_sph == (u32)kInline)) && T.ovf == kNil;
+    if (need_pool) {
+        const u32 blk = atomicAdd(&A.ctl->pool_cnt, 1u);
+        if (blk >= A.pool_cap) {
+            atomicOr(&A.ctl->err, 8u);
+            return;
+        }
+        T.ovf = blk;
+    }
+    {
+        const u32 bit = 1u << lid;
+        const unsigned long long kb = 1ull << ((lin * 0x9E3779B1u) >> 26);
+        bool found = false;
+        if (S.seen_bloom & kb) {
+            for (int i = (int)S.n_seen - 1; i >= 0; --i) {
+                if (*T.key(i) == lin) {
+                    u32 *mp = T.mask(i);
+                    const u32 mv = *mp;
+                    if (mv & bit) return;
+                    *mp = mv | bit;
+                    found = true;
+                    break;
+                }
+            }
+        }
+        if (!found && S.n_seen < (u32)LVX_MAX_SEEN) {
+            *T.key(S.n_seen) = lin;
+            *T.mask(S.n_seen) = bit;
+            S.n_seen += 1;
+            S.seen_bloom |= kb;
+        }
+    }
+    const float4 col = __ldg(reinterpret_cast<const float4 *>(A.table) + attr);
+    const double trans = 1.0 - S.acc[3];
+    const double w = trans * alpha;
+    S.acc[0] += w * scale * (double)col.x;
+    S.acc[1] += w * scale * (double)col.y;
+    S.acc[2] += w * scale * (double)col.z;
+    S.acc[3] += w;
+    if (is_sphere && S.n_sph < (u32)LVX_MAX_SEEN) {
+        *T.sph(S.n_sph, 0) = cx;
+        *T.sph(S.n_sph, 1) = cy;
+        *T.sph(S.n_sph, 2) = cz;
+        S.n_sph += 1;
+        S.sph_bloom |= sph_bit;
+    }
+}
+
+// Slow path for rays that crossed a window with more than 1024/3 candidates: the reference
+// keeps the first 1024 owned hits of a window in gather order and counts the rest in
+// window_overflow (_kernels.py:852-853).  Gather order is (segment, primitive).
+__device__ void wf_apply_window_cap(const WfArgs &A, u32 head) {
+    for (u32 a = head; a != kNil; a = A.hit[a].next) {
+        const u32 wid = A.hit[a].wid;
+        if (!(A.win[wid].cz & 0x80000000u)) continue;
+        const u32 sa = A.hit[a].seg, ka = A.hit[a].meta & 3u;
+        u32 rank = 0;
+        for (u32 b = head; b != kNil; b = A.hit[b].next) {
+            if (A.hit[b].wid != wid) continue;
+            const u32 sb = A.hit[b].seg, kb = A.hit[b].meta & 3u;
+            if (sb < sa || (sb == sa && kb < ka)) rank += 1;
+        }
+        if (rank >= (u32)LVX_MAX_WINDOW_HITS) {
+            A.hit[a].meta |= 1u << 16;
+            A.win_over[wid] += 1;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A, int par) {
+    const u32 n_live = A.ctl->n_live[par];
+    const u32 wn = A.ctl->wn;
+    const size_t R = A.R;
+    const double tau = A.p.tau;
+    for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n_live; i += gridDim.x * blockDim.x) {
+        const u32 slot = A.live[par][i];
+        const u32 head = A.head[slot];
+        const u8 fl = A.flags[slot];
+        bool finished = !(fl & 1);  // the walk is over: this was the last batch
+        bool terminated = false;
+        unsigned long long tests = 0, over = 0;
+        if (head != kNil) {
+            A.head[slot] = kNil;
+            const bool big = (fl & 2) != 0;
+            if (big) wf_apply_window_cap(A, head);
+            WfPixel S;
+            S.acc[0] = A.acc[slot];
+            S.acc[1] = A.acc[R + slot];
+            S.acc[2] = A.acc[2 * R + slot];
+            S.acc[3] = A.acc[3 * R + slot];
+            S.n_seen = A.n_seen[slot];
+            S.n_sph = A.n_sph[slot];
+            S.seen_bloom = A.seen_bloom[slot];
+            S.sph_bloom = A.sph_bloom[slot];
+            WfTables T = {A, slot, A.ovf[slot]};
+            // gather + order
+            double s_t[kSortCap];
+            u32 s_idx[kSortCap];
+            int n = 0;
+            bool fits = true;
+            for (u32 e = head; e != kNil; e = A.hit[e].next) {
+                if (A.hit[e].meta & (1u << 16)) continue;  // dropped by the window cap
+                if (n == kSortCap) {
+                    fits = false;
+                    break;
+                }
+                const double t = A.hit[e].t_in;
+                int pos = n++;
+                while (pos > 0) {
+                    const u32 o = s_idx[pos - 1];
+                    bool before;
+                    if (t != s_t[pos - 1]) before = t < s_t[pos - 1];
+                    else before = wf_key_before(t, A.hit[e].lin, A.hit[e].seg, A.hit[e].meta, s_t[pos - 1],
+                                                A.hit[o].lin, A.hit[o].seg, A.hit[o].meta);
+                    if (!before) break;
+                    s_t[pos] = s_t[pos - 1];
+                    s_idx[pos] = o;
+                    --pos;
+                }
+                s_t[pos] = t;
+                s_idx[pos] = e;
+            }
+            u32 term_wid = 0;
+            if (fits) {
+                for (int j = 0; j < n; ++j) {
+                    const WfHit h = A.hit[s_idx[j]];
+                    const u32 kind3 = h.meta & 3u;
+                    float cx = 0.0f, cy = 0.0f, cz = 0.0f;
+                    if (kind3) {
+                        const float4 c = __ldg(reinterpret_cast<const float4 *>(A.rec + h.seg) + (kind3 - 1));
+                        cx = c.x;
+                        cy = c.y;
+                        cz = c.z;
+                    }
+                    wf_accumulate(A, T, S, h.scale, h.alpha, h.lin, (h.meta >> 2) & 31u, (h.meta >> 8) & 0xFFu,
+                                  kind3 != 0, cx, cy, cz);
+                    if (S.acc[3] >= tau) {
+                        terminated = true;
+                        term_wid = h.wid;
+                        break;
+                    }
+                }
+            } else {
+                // more hits than the local buffer holds: selection instead of sorting --
+                // repeatedly take the smallest key after the last composited one
+                bool have_last = false;
+                double lt = 0.0;
+                u32 ll = 0, ls = 0, lm = 0;
+                for (;;) {
+                    u32 best = kNil;
+                    double bt = 0.0;
+                    u32 bl = 0, bs = 0, bm = 0;
+                    for (u32 e = head; e != kNil; e = A.hit[e].next) {
+                        const u32 m = A.hit[e].meta;
+                        if (m & (1u << 16)) continue;
+                        const double t = A.hit[e].t_in;
+                        const u32 l = A.hit[e].lin, sg = A.hit[e].seg;
+                        if (have_last && !wf_key_before(lt, ll, ls, lm, t, l, sg, m)) continue;
+                        if (best == kNil || wf_key_before(t, l, sg, m, bt, bl, bs, bm)) {
+                            best = e;
+                            bt = t;
+                            bl = l;
+                            bs = sg;
+                            bm = m;
+                        }
+                    }
+                    if (best == kNil) break;
+                    const WfHit h = A.hit[best];
+                    const u32 kind3 = h.meta & 3u;
+                    float cx = 0.0f, cy = 0.0f, cz = 0.0f;
+                    if (kind3) {
+                        const float4 c = __ldg(reinterpret_cast<const float4 *>(A.rec + h.seg) + (kind3 - 1));
+                        cx = c.x;
+                        cy = c.y;
+                        cz = c.z;
+                    }
+                    wf_accumulate(A, T, S, h.scale, h.alpha, h.lin, (h.meta >> 2) & 31u, (h.meta >> 8) & 0xFFu,
+                                  kind3 != 0, cx, cy, cz);
+                    if (S.acc[3] >= tau) {
+                        terminated = true;
+                        term_wid = h.wid;
+                        break;
+                    }
+                    have_last = true;
+                    lt = bt;
+                    ll = bl;
+                    ls = bs;
+                    lm = bm;
+                }
+            }
+            A.acc[slot] = S.acc[0];
+            A.acc[R + slot] = S.acc[1];
+            A.acc[2 * R + slot] = S.acc[2];
+            A.acc[3 * R + slot] = S.acc[3];
+            A.n_seen[slot] = S.n_seen;
+            A.n_sph[slot] = S.n_sph;
+            A.seen_bloom[slot] = S.seen_bloom;
+            A.sph_bloom[slot] = S.sph_bloom;
+            A.ovf[slot] = T.ovf;
+            if (big) {
+                // window_overflow of the windows gathered up to (and including) the last one used
+                const u32 w0 = i * wn, nw = A.nwin[slot];
+                unsigned long long ov = 0;
+                for (u32 k = 0; k < nw; ++k) {
+                    const u32 wid = w0 + k;
+                    if (A.win[wid].cz & 0x80000000u) ov += A.win_over[wid];
+                    if (terminated && wid == term_wid) break;
+                }
+                A.over[slot] += ov;
+            }
+            if (terminated) {
+                tests = A.win[term_wid].tests;
+                finished = true;
+            }
+        }
+        if (finished) {
+            if (!terminated) tests = A.tests[slot];
+            over = A.over[slot];
+            write_pixel(A, A.out_off[slot], A.acc[slot], A.acc[R + slot], A.acc[2 * R + slot], A.acc[3 * R + slot]);
+            const u32 y = A.pix[slot] >> 16;
+            if (tests) atomicAdd(A.row_stats + 3 * (i64)y + 1, tests);
+            if (over) atomicAdd(A.row_stats + 3 * (i64)y + 2, over);
+        } else {
+            cg::coalesced_group g = cg::coalesced_threads();
+            u32 base = 0;
+            if (g.thread_rank() == 0) base = atomicAdd(&A.ctl->n_live[par ^ 1], g.size());
+            base = g.shfl(base, 0);
+            A.live[par ^ 1][base + g.thread_rank()] = slot;
+        }
+    }
+}
+
+// between iterations: clear the queues, retire the consumed live list, set the next budget
+__global__ void wf_next_kernel(const WfArgs A, int par, int it_next) {
+    const int t = threadIdx.x;
+    if (t < kNQ) {
+        A.ctl->item_cnt[t] = 0;
+        A.ctl->surv_cnt[t] = 0;
+        A.ctl->hit_cnt[t] = 0;
+    }
+    if (t == 0) {
+        A.ctl->n_live[par] = 0;
+        const u32 live = A.ctl->n_live[par ^ 1];
+        u32 wn = (u32)A.wn_sched << (it_next < 4 ? it_next : 4);
+        const u32 fit = live ? A.cap_win / live : A.cap_win;
+        if (wn > fit) wn = fit;
+        if (wn < 1) wn = 1;
+        A.ctl->wn = wn;
+    }
+}
+
+__global__ void wf_begin_kernel(const WfArgs A) {
+    const int t = threadIdx.x;
+    if (t < kNQ) {
+        A.ctl->item_cnt[t] = 0;
+        A.ctl->surv_cnt[t] = 0;
+        A.ctl->hit_cnt[t] = 0;
+    }
+    if (t == 0) {
+        A.ctl->n_live[0] = 0;
+        A.ctl->n_live[1] = 0;
+        A.ctl->pool_cnt = 0;
+        A.ctl->err = 0;
+        A.ctl->wn = (u32)A.wn_sched;
+    }
+}
+
+// scratch layout ------------------------------------------------------------------------
+struct WfLayout {
+    size_t total;
+    size_t ctl, pix, out_off, dir, dda_t, dda_i, flags, acc, tests, over, seen_bloom, sph_bloom, n_seen,
+        n_sph, ovf, head, nwin, tab_key, tab_mask, tab_sph, pool_key, pool_mask, pool_sph, live0, live1, win,
+        win_over, item_wid, item_b, surv, hit;
+    u32 R, pool_cap, cap_win, capq_item, capq_surv, capq_hit;
+};
+
+size_t take(size_t &cur, size_t bytes) {
+    const size_t at = (cur + 255) & ~(size_t)255;
+    cur = at + bytes;
+    return at;
+}
+
+WfLayout wf_layout(i64 R, double scale) {
+    WfLayout L;
+    memset(&L, 0, sizeof(L));
+    L.R = (u32)R;
+    const double f = scale < 1.0 ? 1.0 : scale;
+    L.pool_cap = (u32)(R / 16 * f) + 1024;
+    L.cap_win = (u32)fmin(4.0e9, (double)R * 8.0);
+    L.capq_item = (u32)fmin(4.0e9 / kNQ, ((double)R * 40.0 * f + 65536.0) / kNQ);
+    L.capq_surv = (u32)fmin(4.0e9 / kNQ, ((double)R * 12.0 * f + 65536.0) / kNQ);
+    L.capq_hit = (u32)fmin(4.0e9 / kNQ, ((double)R * 8.0 * f + 65536.0) / kNQ);
+    size_t c = 0;
+    const size_t r = (size_t)R, po = (size_t)L.pool_cap * (LVX_MAX_SEEN - kInline);
+    L.ctl = take(c, sizeof(WfCtl));
+    L.pix = take(c, r * 4);
+    L.out_off = take(c, r * 4);
+    L.dir = take(c, r * 24);
+    L.dda_t = take(c, r * 40);
+    L.dda_i = take(c, r * 12);
+    L.flags = take(c, r);
+    L.acc = take(c, r * 32);
+    L.tests = take(c, r * 8);
+    L.over = take(c, r * 8);
+    L.seen_bloom = take(c, r * 8);
+    L.sph_bloom = take(c, r * 8);
+    L.n_seen = take(c, r * 4);
+    L.n_sph = take(c, r * 4);
+    L.ovf = take(c, r * 4);
+    L.head = take(c, r * 4);
+    L.nwin = take(c, r * 4);
+    L.tab_key = take(c, r * 4 * kInline);
+    L.tab_mask = take(c, r * 4 * kInline);
+    L.tab_sph = take(c, r * 12 * kInline);
+    L.pool_key = take(c, po * 4);
+    L.pool_mask = take(c, po * 4);
+    L.pool_sph = take(c, po * 12);
+    L.live0 = take(c, r * 4);
+    L.live1 = take(c, r * 4);
+    L.win = take(c, (size_t)L.cap_win * sizeof(WfWindow));
+    L.win_over = take(c, (size_t)L.cap_win * 4);
+    L.item_wid = take(c, (size_t)L.capq_item * kNQ * 4);
+    L.item_b = take(c, (size_t)L.capq_item * kNQ);
+    L.surv = take(c, (size_t)L.capq_surv * kNQ * sizeof(WfSurv));
+    L.hit = take(c, (size_t)L.capq_hit * kNQ * sizeof(WfHit));
+    L.total = take(c, 0);
+    return L;
+}
+
+i64 wf_ray_slots(const lvx_camera *cam, const lvx_tiling *t) {
+    const i64 tiles_x = lvx_ceil_div(cam->width, t->tile_w), tiles_y = lvx_ceil_div(cam->height, t->tile_h);
+    const i64 total = tiles_x * tiles_y;
+    i64 mine = 0;
+    if (t->tile_first < total) mine = (total - t->tile_first + t->tile_step - 1) / t->tile_step;
+    return mine * t->tile_w * t->tile_h;
+}
+
+int wf_check_tiling(const lvx_tiling *t) {
+    LVX_REQUIRE(t && t->tile_w >= 8 && t->tile_h >= 4 && (t->tile_w % 8) == 0 && (t->tile_h % 4) == 0 &&
+                    t->tile_step >= 1 && t->tile_first >= 0 && t->tile_first < t->tile_step,
+                "tiling: tile_w %% 8 == 0, tile_h %% 4 == 0, 0 <= tile_first < tile_step required");
+    return LVX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t lvx_render_wf_scratch_bytes(const lvx_camera *cam, const lvx_tiling *tiling, double scale) {
+    if (!cam || !tiling || tiling->tile_w < 8 || tiling->tile_h < 4 || tiling->tile_step < 1) return 0;
+    const i64 R = wf_ray_slots(cam, tiling);
+    return wf_layout(R > 0 ? R : 32, scale).total;
+}
+
+int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_params *params,
+                  const lvx_lod *lod, const lvx_tiling *tiling, float *img_d, int64_t *row_stats_d,
+                  void *scratch_d, size_t scratch_bytes, double scale, void *stream) {
+    LVX_REQUIRE(cam && model && params && img_d && row_stats_d && scratch_d, "null argument");
+    LVX_REQUIRE(cam->width >= 1 && cam->height >= 1 && cam->width < 65536 && cam->height < 65536,
+                "image dims must be in [1, 65535]");
+    if (int rc = wf_check_tiling(tiling)) return rc;
+    LVX_REQUIRE(model->rx >= 1 && model->ry >= 1 && model->rz >= 1 && model->counts_d && model->offsets_d &&
+                    model->table_d,
+                "bad model");
+    LVX_REQUIRE(model->rx < 65535 && model->ry < 65535 && (i64)model->rx * model->ry * model->rz < ((i64)1 << 31),
+                "grid too large to render");
+    LVX_REQUIRE(!params->neighbor || (model->nsum_d && model->nmask_d),
+                "neighbour mode needs the neighbour grids (lvx_neighbor_sums)");
+    LVX_REQUIRE(params->opacity_mode >= 0 && params->opacity_mode <= 2, "bad opacity mode");
+    LVX_REQUIRE(params->shadow_mode == LVX_SHADOW_NONE || params->shadow_mode == LVX_SHADOW_CONE,
+                "shadow_mode %d is not built in this library (none/cone only)", params->shadow_mode);
+    LVX_REQUIRE(params->ao_mode == LVX_AO_NONE || params->ao_mode == LVX_AO_DENSITY ||
+                    params->ao_mode == LVX_AO_PRECOMPUTED,
+                "ao_mode %d is not built in this library (none/density-rays/precomputed only)", params->ao_mode);
+    const bool need_oct = params->shadow_mode == LVX_SHADOW_CONE || params->ao_mode == LVX_AO_DENSITY;
+    LVX_REQUIRE(!need_oct || (lod && lod->oct_flat_d && lod->n_levels >= 1 && lod->n_levels <= LVX_MAX_LEVELS),
+                "cone shadows / density-rays AO need a density octree");
+    LVX_REQUIRE(params->ao_mode != LVX_AO_PRECOMPUTED || (lod && lod->ao_flat_d),
+                "precomputed AO requested but no AO field given");
+    LVX_REQUIRE(params->ao_mode != LVX_AO_DENSITY || (lod->ao_dirs_d && params->ao_n_rays >= 1),
+                "density-rays AO needs the direction lattice");
+
+    const i64 R = wf_ray_slots(cam, tiling);
+    if (R == 0) return LVX_OK;
+    LVX_REQUIRE(R < ((i64)1 << 31), "too many rays for one launch");
+    const WfLayout L = wf_layout(R, scale);
+    LVX_REQUIRE(scratch_bytes >= L.total, "scratch too small: %zu < %zu bytes", scratch_bytes, L.total);
+    LVX_REQUIRE(((uintptr_t)scratch_d & 255) == 0, "scratch must be 256-byte aligned");
+
+    WfArgs A;
+    memset(&A, 0, sizeof(A));
+    A.cam = *cam;
+    A.p = *params;
+    A.rx = model->rx;
+    A.ry = model->ry;
+    A.rz = model->rz;
+    A.counts = model->counts_d;
+    A.offsets = model->offsets_d;
+    A.rec = model->seg_rec_d;
+    A.table = model->table_d;
+    A.nsum = model->nsum_d;
+    A.nmask = model->nmask_d;
+    if (lod) {
+        A.oc.flat = lod->oct_flat_d;
+        A.oc.n_levels = lod->n_levels;
+        for (int l = 0; l <= lod->n_levels && l <= LVX_MAX_LEVELS; ++l) A.oc.off[l] = lod->oct_off[l];
+        for (int l = 0; l < lod->n_levels * 3 && l < LVX_MAX_LEVELS * 3; ++l) A.oc.dims[l] = (int)lod->oct_dims[l];
+        A.ao_flat = lod->ao_flat_d;
+        A.ao_dirs = lod->ao_dirs_d;
+    }
+    A.tl = *tiling;
+    {
+        const i64 tiles_x = lvx_ceil_div(cam->width, tiling->tile_w);
+        A.tiles_x = (int)tiles_x;
+        A.n_my_tiles = (int)(R / ((i64)tiling->tile_w * tiling->tile_h));
+    }
+    A.img = img_d;
+    A.row_stats = reinterpret_cast<unsigned long long *>(row_stats_d);
+    char *base = (char *)scratch_d;
+    A.R = L.R;
+    A.ctl = (WfCtl *)(base + L.ctl);
+    A.pix = (u32 *)(base + L.pix);
+    A.out_off = (u32 *)(base + L.out_off);
+    A.dir = (double *)(base + L.dir);
+    A.dda_t = (double *)(base + L.dda_t);
+    A.dda_i = (int *)(base + L.dda_i);
+    A.flags = (u8 *)(base + L.flags);
+    A.acc = (double *)(base + L.acc);
+    A.tests = (unsigned long long *)(base + L.tests);
+    A.over = (unsigned long long *)(base + L.over);
+    A.seen_bloom = (unsigned long long *)(base + L.seen_bloom);
+    A.sph_bloom = (unsigned long long *)(base + L.sph_bloom);
+    A.n_seen = (u32 *)(base + L.n_seen);
+    A.n_sph = (u32 *)(base + L.n_sph);
+    A.ovf = (u32 *)(base + L.ovf);
+    A.head = (u32 *)(base + L.head);
+    A.nwin = (u32 *)(base + L.nwin);
+    A.tab_key = (u32 *)(base + L.tab_key);
+    A.tab_mask = (u32 *)(base + L.tab_mask);
+    A.tab_sph = (float *)(base + L.tab_sph);
+    A.pool_key = (u32 *)(base + L.pool_key);
+    A.pool_mask = (u32 *)(base + L.pool_mask);
+    A.pool_sph = (float *)(base + L.pool_sph);
+    A.pool_cap = L.pool_cap;
+    A.live[0] = (u32 *)(base + L.live0);
+    A.live[1] = (u32 *)(base + L.live1);
+    A.win = (WfWindow *)(base + L.win);
+    A.cap_win = L.cap_win;
+    A.win_over = (u32 *)(base + L.win_over);
+    A.item_wid = (u32 *)(base + L.item_wid);
+    A.item_b = (u8 *)(base + L.item_b);
+    A.capq_item = L.capq_item;
+    A.surv = (WfSurv *)(base + L.surv);
+    A.capq_surv = L.capq_surv;
+    A.hit = (WfHit *)(base + L.hit);
+    A.capq_hit = L.capq_hit;
+    A.wn_sched = 8;
+    A.cand_budget = 192;
+
+    cudaStream_t st = (cudaStream_t)stream;
+    const int sms = lvx_sm_count();
+    const unsigned grid_rays = (unsigned)(sms * 8), grid_q = (unsigned)(sms * 8);
+    wf_begin_kernel<<<1, 64, 0, st>>>(A);
+    wf_init_kernel<<<(unsigned)lvx_ceil_div(R, kThreadsWf), kThreadsWf, 0, st>>>(A);
+    LVX_LAUNCH_CHECK();
+    u32 host[4] = {0, 0, 0, 0};
+    int it = 0;
+    for (;;) {
+        const int burst = it == 0 ? 6 : 3;
+        for (int b = 0; b < burst; ++b, ++it) {
+            const int par = it & 1;
+            wf_walk_kernel<<<grid_rays, kThreadsWf, 0, st>>>(A, par);
+            wf_cand_kernel<<<grid_q, kThreadsWf, 0, st>>>(A);
+            wf_exact_kernel<<<grid_q, kThreadsWf, 0, st>>>(A);
+            wf_composite_kernel<<<grid_rays, kThreadsWf, 0, st>>>(A, par);
+            wf_next_kernel<<<1, 64, 0, st>>>(A, par, it + 1);
+        }
+        LVX_LAUNCH_CHECK();
+        // rays left?  (n_live of the list the next iteration reads, and the error bits)
+        LVX_CUDA_CHECK(cudaMemcpyAsync(&host[0], &A.ctl->n_live[it & 1], 4, cudaMemcpyDeviceToHost, st));
+        LVX_CUDA_CHECK(cudaMemcpyAsync(&host[1], &A.ctl->err, 4, cudaMemcpyDeviceToHost, st));
+        LVX_CUDA_CHECK(cudaStreamSynchronize(st));
+        if (host[1]) {
+            lvx_set_error("wavefront queues overflowed (bits %u): retry with a larger scratch scale", host[1]);
+            return LVX_E_RANGE;
+        }
+        if (host[0] == 0) break;
+        LVX_REQUIRE(it < 100000, "wavefront did not converge");
+    }
+    return LVX_OK;
+}
+
+}  // extern "C"

@@ -331,15 +331,44 @@ def check_modes(params: RenderParams, model: VoxelModel, octree):
         raise ValueError("precomputed AO requested but the model carries none")
 
 
+def default_engine() -> str:
+    """Frame engine used when none is named: LVX_ENGINE=tile|wavefront (developer switch)."""
+    import os
+    return os.environ.get("LVX_ENGINE", "wavefront")
+
+
+_WF_SCRATCH = {}
+
+
+def _wf_scratch(cam, til, scale: float):
+    """Scratch buffer of the wavefront engine, cached per device and grown on demand."""
+    torch = _lib.require_device()
+    need = int(_lib.lib().lvx_render_wf_scratch_bytes(C.byref(cam), C.byref(til), C.c_double(scale)))
+    dev = torch.cuda.current_device()
+    buf = _WF_SCRATCH.get(dev)
+    if buf is None or buf.numel() < need:
+        _WF_SCRATCH.pop(dev, None)
+        buf = None
+        torch.cuda.empty_cache()
+        buf = torch.empty(need, dtype=torch.uint8, device="cuda")
+        _WF_SCRATCH[dev] = buf
+    return buf
+
+
 class FramePlan:
     """Everything `lvx_render` needs for one (camera, model, params) triple, resolved
     once: C structs plus the device tensors they point into (kept alive here)."""
 
     def __init__(self, camera: Camera, model: VoxelModel, octree: Optional[DensityOctree],
                  params: RenderParams, neighbor: int, tile_first: int = 0, tile_step: int = 1,
-                 compact: bool = False, tile_w: int = TILE_W, tile_h: int = TILE_H):
+                 compact: bool = False, tile_w: int = TILE_W, tile_h: int = TILE_H,
+                 engine: Optional[str] = None):
         from .illumination import fibonacci_dirs_device
         check_modes(params, model, octree)
+        self.engine = engine or default_engine()
+        if self.engine not in ("wavefront", "tile"):
+            raise ValueError(f"unknown frame engine {self.engine!r}")
+        self._scale = 1.0
         self.cam = camera_struct(camera)
         self.par = params_struct(params, neighbor)
         counts_d, offsets_d, rec_d, table_d, occ_d = model.device_view(need_occ=bool(neighbor))
@@ -374,10 +403,30 @@ class FramePlan:
         return (total - self.til.tile_first + self.til.tile_step - 1) // self.til.tile_step
 
     def launch(self, img_d, row_stats_d):
-        """Enqueue the frame kernel on the current stream (row_stats_d must be zeroed)."""
-        _lib.check(_lib.lib().lvx_render(C.byref(self.cam), C.byref(self.mdl), C.byref(self.par),
-                                         C.byref(self.lod), C.byref(self.til), _lib.ptr(img_d),
-                                         _lib.ptr(row_stats_d), None, _lib.stream_ptr()))
+        """Render the frame on the current stream (row_stats_d must be zeroed).
+
+        engine "tile": one monolithic kernel (lvx_render), asynchronous.
+        engine "wavefront": streaming kernels over device queues (lvx_render_wf); the call
+        returns when the frame is complete.  A queue overflow (LVX_E_RANGE) is retried with
+        a larger scratch buffer."""
+        L = _lib.lib()
+        if self.engine == "tile":
+            _lib.check(L.lvx_render(C.byref(self.cam), C.byref(self.mdl), C.byref(self.par),
+                                    C.byref(self.lod), C.byref(self.til), _lib.ptr(img_d),
+                                    _lib.ptr(row_stats_d), None, _lib.stream_ptr()))
+            return
+        while True:
+            scratch = _wf_scratch(self.cam, self.til, self._scale)
+            rc = L.lvx_render_wf(C.byref(self.cam), C.byref(self.mdl), C.byref(self.par),
+                                 C.byref(self.lod), C.byref(self.til), _lib.ptr(img_d),
+                                 _lib.ptr(row_stats_d), _lib.ptr(scratch), C.c_size_t(scratch.numel()),
+                                 C.c_double(self._scale), _lib.stream_ptr())
+            if rc == 4 and self._scale < 64.0:  # LVX_E_RANGE: queues too small for this scene
+                self._scale *= 2.0
+                row_stats_d.zero_()
+                continue
+            _lib.check(rc)
+            return
 
 
     def launch_footprint(self, img_d, row_stats_d, voxel_bits_d):
