@@ -41,6 +41,7 @@
 #include <cooperative_groups.h>
 #include <cooperative_groups/scan.h>
 #include <math_constants.h>
+#include <stdlib.h>
 
 #include "lvx_geom.cuh"
 
@@ -63,7 +64,7 @@ struct __align__(16) WfWindow {
     u32 cxy;                   // cell (x + 1) | (y + 1) << 16
     u32 cz;                    // cell (z + 1) | big << 31
     float q0x, q0y, q0z, tlen;
-    u32 pad[3];
+    float fdx, fdy, fdz;       // float32 ray direction for the pre-reject
 };
 static_assert(sizeof(WfWindow) == 64, "window record is 64 bytes");
 
@@ -74,17 +75,23 @@ struct __align__(16) WfHit {
 };
 static_assert(sizeof(WfHit) == 48, "hit record is 48 bytes");
 
-struct WfSurv {
-    u32 seg, wid, mb;  // mb: primitive mask 3 | neighbour bit << 3
+constexpr int kWidBits = 27;       // window ids; the neighbour bit (0..26) rides above them
+constexpr u32 kWidMask = (1u << kWidBits) - 1u;
+constexpr int kHitSlots = 12;      // hits per ray and iteration stored ray-parallel (the rest is listed)
+
+struct WfEntry {
+    u32 seg;  // segment (| sphere B << 31 in the sphere queue)
+    u32 wb;   // window id | neighbour bit << 27
 };
 
 // control block in device memory
 struct WfCtl {
     u32 n_live[2];
-    u32 item_cnt[kNQ], surv_cnt[kNQ], hit_cnt[kNQ];
+    u32 item_cnt[kNQ], cand_cnt[kNQ], tube_cnt[kNQ], sph_cnt[kNQ], hit_cnt[kNQ];
     u32 pool_cnt;
-    u32 err;   // bit 0 items, 1 survivors, 2 hits, 3 table pool
+    u32 err;   // bit 0 items / candidates, 1 survivors, 2 listed hits, 3 table pool
     u32 wn;    // windows per ray of the current iteration
+    u32 budget;  // candidate budget per ray of the current iteration (neighbour-sum units)
 };
 
 struct WfArgs {
@@ -126,12 +133,14 @@ struct WfArgs {
     u32 *item_wid;
     u8 *item_b;
     u32 capq_item;
-    WfSurv *surv;
-    u32 capq_surv;
-    WfHit *hit;
+    WfEntry *cand, *tube, *sph;
+    u32 capq_cand, capq_surv;
+    WfHit *hit;       // overflow pool (linked lists)
     u32 capq_hit;
+    WfHit *hit_slot;  // [kHitSlots][R], indexed by the ray's position in the live list
+    u32 *hcnt;        // hits of the ray this iteration
     u32 *win_over;  // [cap_win] overflow of a window (slow path only)
-    int wn_sched, cand_budget;
+    int wn_sched, cand_budget, grow_from;
 };
 
 __device__ __forceinline__ int warp_queue() {
@@ -303,6 +312,7 @@ __global__ void __launch_bounds__(kThreadsWf) wf_init_kernel(const WfArgs A) {
             A.n_sph[slot] = 0;
             A.ovf[slot] = kNil;
             A.head[slot] = kNil;
+            A.hcnt[slot] = 0;
             A.nwin[slot] = 0;
             live = true;
         } else {
@@ -328,6 +338,7 @@ __global__ void __launch_bounds__(kThreadsWf) wf_init_kernel(const WfArgs A) {
 __global__ void __launch_bounds__(kThreadsWf) wf_walk_kernel(const WfArgs A, int par) {
     const u32 n_live = A.ctl->n_live[par];
     const u32 wn = A.ctl->wn;
+    const u32 budget = A.ctl->budget;
     const lvx_params &p = A.p;
     const bool neighbor = p.neighbor != 0;
     const int rx = A.rx, ry = A.ry;
@@ -344,7 +355,7 @@ __global__ void __launch_bounds__(kThreadsWf) wf_walk_kernel(const WfArgs A, int
         unsigned long long tests = A.tests[slot];
         u32 kw = 0, csum = 0;
         bool big_any = false;
-        while (kw < wn && csum < (u32)A.cand_budget) {
+        while (kw < wn && csum < budget) {
             int wx, wy, wz;
             double t0, t1;
             if (!dda.next(wx, wy, wz, t0, t1)) break;
@@ -391,7 +402,9 @@ __global__ void __launch_bounds__(kThreadsWf) wf_walk_kernel(const WfArgs A, int
             w.q0y = (float)(p0y - (double)wy);
             w.q0z = (float)(p0z - (double)wz);
             w.tlen = (float)(t1 - t0);
-            w.pad[0] = w.pad[1] = w.pad[2] = 0;
+            w.fdx = (float)ddx;
+            w.fdy = (float)ddy;
+            w.fdz = (float)ddz;
             A.win[wid] = w;
             if (big) A.win_over[wid] = 0;
             if (ib != kNil) {
@@ -421,62 +434,89 @@ __device__ __forceinline__ bool wf_may_enter(float cx, float cy, float cz, float
 }
 
 // ---------------------------------------------------------------------------------------
-// candidates: one thread per (window, neighbour voxel) item
+// expand: one thread per (window, neighbour voxel) item -> one queue entry per segment
 // ---------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreadsWf) wf_cand_kernel(const WfArgs A) {
+__global__ void __launch_bounds__(kThreadsWf) wf_expand_kernel(const WfArgs A) {
     __shared__ QueueView V;
     queue_view_load(V, A.ctl->item_cnt, A.capq_item);
     const u32 total = V.pre[kNQ];
-    const bool joints = A.p.joints != 0;
-    const float reach_pt = (float)A.p.tube_r + kRejectMarginWf;
     const int q = warp_queue();
-    const size_t R = A.R;
     for (u32 f = blockIdx.x * blockDim.x + threadIdx.x; f < total; f += gridDim.x * blockDim.x) {
         const u32 it = queue_view_index(V, f, A.capq_item);
         const u32 wid = A.item_wid[it];
         const int b = (int)A.item_b[it];
         const WfWindow *wp = A.win + wid;
-        const uint4 w1 = __ldg(reinterpret_cast<const uint4 *>(wp) + 1);  // tests(2) slot cxy
-        const uint4 w2 = __ldg(reinterpret_cast<const uint4 *>(wp) + 2);  // cz q0x q0y q0z
-        const float tlen = __ldg(&wp->tlen);
-        const u32 slot = w1.z;
-        const int cx = (int)(w1.w & 0xFFFFu) - 1, cy = (int)(w1.w >> 16) - 1, cz = (int)(w2.x & 0x7FFFFFFFu) - 1;
-        const float q0x = __uint_as_float(w2.y), q0y = __uint_as_float(w2.z), q0z = __uint_as_float(w2.w);
-        const float fdx = (float)A.dir[slot], fdy = (float)A.dir[R + slot], fdz = (float)A.dir[2 * R + slot];
+        const u32 cxy = __ldg(&wp->cxy), czb = __ldg(&wp->cz);
         const int bz_ = b / 9, by_ = (b - 9 * bz_) / 3, bx_ = b - 9 * bz_ - 3 * by_;
-        const u32 lin = (u32)((cx + bx_ - 1) + A.rx * ((cy + by_ - 1) + A.ry * (cz + bz_ - 1)));
+        const u32 lin = (u32)(((int)(cxy & 0xFFFFu) + bx_ - 2) +
+                              A.rx * (((int)(cxy >> 16) + by_ - 2) + A.ry * ((int)(czb & 0x7FFFFFFFu) + bz_ - 2)));
         const u32 cnt = __ldg(A.counts + lin);
         const u32 base = __ldg(A.offsets + lin);
-        const float fwx = (float)cx, fwy = (float)cy, fwz = (float)cz;
-        for (u32 s = 0; s < cnt; ++s) {
-            const u32 seg = base + s;
-            const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + seg));
-            const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + seg) + 1);
-            const float ax = ra.x - fwx, ay = ra.y - fwy, az = ra.z - fwz;
-            const float bx = rb.x - fwx, by = rb.y - fwy, bz = rb.z - fwz;
-            u32 mk = 0;
-            // the tube AND both joint spheres lie inside the segment's bounding sphere
-            if (wf_may_enter(0.5f * (ax + bx), 0.5f * (ay + by), 0.5f * (az + bz), q0x, q0y, q0z, fdx, fdy,
-                             fdz, tlen, rb.w + reach_pt)) {
-                // the tube's entry point lies on the ray within tube_r of the segment's axis line:
-                // |w . (d x u)| <= reach |d x u|  (absolute slack >> float32 rounding)
-                const float ux = bx - ax, uy = by - ay, uz = bz - az;
-                const float nx = fdy * uz - fdz * uy, ny = fdz * ux - fdx * uz, nz = fdx * uy - fdy * ux;
-                const float wn = (ax - q0x) * nx + (ay - q0y) * ny + (az - q0z) * nz;
-                if (wn * wn <= reach_pt * reach_pt * (nx * nx + ny * ny + nz * nz) + 1e-6f) mk = 1u;
-                if (joints) {
-                    if (wf_may_enter(ax, ay, az, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mk |= 2u;
-                    if (wf_may_enter(bx, by, bz, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mk |= 4u;
-                }
+        const u32 e = queue_alloc(A.ctl->cand_cnt, q, A.capq_cand, cnt, &A.ctl->err, 1u);
+        if (e == kNil) continue;
+        const u32 wb = wid | ((u32)b << kWidBits);
+        for (u32 sg = 0; sg < cnt; ++sg) {
+            WfEntry c;
+            c.seg = base + sg;
+            c.wb = wb;
+            A.cand[e + sg] = c;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// candidates: one thread per (window, segment) pair: conservative float32 pre-reject
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreadsWf) wf_cand_kernel(const WfArgs A) {
+    __shared__ QueueView V;
+    queue_view_load(V, A.ctl->cand_cnt, A.capq_cand);
+    const u32 total = V.pre[kNQ];
+    const bool joints = A.p.joints != 0;
+    const float reach_pt = (float)A.p.tube_r + kRejectMarginWf;
+    const int q = warp_queue();
+    for (u32 f = blockIdx.x * blockDim.x + threadIdx.x; f < total; f += gridDim.x * blockDim.x) {
+        const WfEntry c = A.cand[queue_view_index(V, f, A.capq_cand)];
+        const WfWindow *wp = A.win + (c.wb & kWidMask);
+        const uint4 w1 = __ldg(reinterpret_cast<const uint4 *>(wp) + 1);  // tests(2) slot cxy
+        const uint4 w2 = __ldg(reinterpret_cast<const uint4 *>(wp) + 2);  // cz q0x q0y q0z
+        const uint4 w3 = __ldg(reinterpret_cast<const uint4 *>(wp) + 3);  // tlen fdx fdy fdz
+        const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + c.seg));
+        const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + c.seg) + 1);
+        const float fwx = (float)((int)(w1.w & 0xFFFFu) - 1), fwy = (float)((int)(w1.w >> 16) - 1),
+                    fwz = (float)((int)(w2.x & 0x7FFFFFFFu) - 1);
+        const float q0x = __uint_as_float(w2.y), q0y = __uint_as_float(w2.z), q0z = __uint_as_float(w2.w);
+        const float tlen = __uint_as_float(w3.x);
+        const float fdx = __uint_as_float(w3.y), fdy = __uint_as_float(w3.z), fdz = __uint_as_float(w3.w);
+        const float ax = ra.x - fwx, ay = ra.y - fwy, az = ra.z - fwz;
+        const float bx = rb.x - fwx, by = rb.y - fwy, bz = rb.z - fwz;
+        u32 mk = 0;
+        // the tube AND both joint spheres lie inside the segment's bounding sphere
+        if (wf_may_enter(0.5f * (ax + bx), 0.5f * (ay + by), 0.5f * (az + bz), q0x, q0y, q0z, fdx, fdy, fdz,
+                         tlen, rb.w + reach_pt)) {
+            // the tube's entry point lies on the ray within tube_r of the segment's axis line:
+            // |w . (d x u)| <= reach |d x u|  (absolute slack >> float32 rounding)
+            const float ux = bx - ax, uy = by - ay, uz = bz - az;
+            const float nx = fdy * uz - fdz * uy, ny = fdz * ux - fdx * uz, nz = fdx * uy - fdy * ux;
+            const float wn = (ax - q0x) * nx + (ay - q0y) * ny + (az - q0z) * nz;
+            if (wn * wn <= reach_pt * reach_pt * (nx * nx + ny * ny + nz * nz) + 1e-6f) mk = 1u;
+            if (joints) {
+                if (wf_may_enter(ax, ay, az, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mk |= 2u;
+                if (wf_may_enter(bx, by, bz, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mk |= 4u;
             }
-            if (mk) {
-                const u32 e = queue_alloc(A.ctl->surv_cnt, q, A.capq_surv, 1u, &A.ctl->err, 2u);
-                if (e != kNil) {
-                    WfSurv sv;
-                    sv.seg = seg;
-                    sv.wid = wid;
-                    sv.mb = mk | ((u32)b << 3);
-                    A.surv[e] = sv;
+        }
+        if (mk & 1u) {
+            const u32 e = queue_alloc(A.ctl->tube_cnt, q, A.capq_surv, 1u, &A.ctl->err, 2u);
+            if (e != kNil) A.tube[e] = c;
+        }
+        if (mk & 6u) {
+            const u32 ns = (mk & 2u ? 1u : 0u) + (mk & 4u ? 1u : 0u);
+            u32 e = queue_alloc(A.ctl->sph_cnt, q, A.capq_surv, ns, &A.ctl->err, 2u);
+            if (e != kNil) {
+                WfEntry sa = c;
+                if (mk & 2u) A.sph[e++] = sa;
+                if (mk & 4u) {
+                    sa.seg |= 0x80000000u;
+                    A.sph[e] = sa;
                 }
             }
         }
@@ -521,58 +561,69 @@ __device__ __forceinline__ void wf_shade(const WfArgs &A, double ox, double oy, 
 }
 
 // ---------------------------------------------------------------------------------------
-// exact: one thread per survivor
+// exact: one thread per surviving primitive (KIND 0: tubes, 1: joint spheres)
 // ---------------------------------------------------------------------------------------
+template <int KIND>
 __global__ void __launch_bounds__(kThreadsWf) wf_exact_kernel(const WfArgs A) {
     __shared__ QueueView V;
-    queue_view_load(V, A.ctl->surv_cnt, A.capq_surv);
+    queue_view_load(V, KIND == 0 ? A.ctl->tube_cnt : A.ctl->sph_cnt, A.capq_surv);
     const u32 total = V.pre[kNQ];
     const double ox = A.cam.o[0], oy = A.cam.o[1], oz = A.cam.o[2];
     const double tube_r = A.p.tube_r;
     const int q = warp_queue();
     const size_t R = A.R;
+    const u32 wn = A.ctl->wn;
+    const WfEntry *queue = KIND == 0 ? A.tube : A.sph;
     for (u32 f = blockIdx.x * blockDim.x + threadIdx.x; f < total; f += gridDim.x * blockDim.x) {
-        const WfSurv sv = A.surv[queue_view_index(V, f, A.capq_surv)];
-        const WfWindow *wp = A.win + sv.wid;
+        const WfEntry c = queue[queue_view_index(V, f, A.capq_surv)];
+        const u32 wid = c.wb & kWidMask, seg = c.seg & 0x7FFFFFFFu;
+        const WfWindow *wp = A.win + wid;
         const double t0 = __ldg(&wp->t0), t1 = __ldg(&wp->t1);
         const u32 slot = __ldg(&wp->slot);
-        const u32 cxy = __ldg(&wp->cxy), czb = __ldg(&wp->cz);
         const double rdx = A.dir[slot], rdy = A.dir[R + slot], rdz = A.dir[2 * R + slot];
-        const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + sv.seg));
-        const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + sv.seg) + 1);
-        const int b = (int)(sv.mb >> 3);
-        const int bz_ = b / 9, by_ = (b - 9 * bz_) / 3, bx_ = b - 9 * bz_ - 3 * by_;
-        const u32 lin = (u32)(((int)(cxy & 0xFFFFu) + bx_ - 2) +
-                              A.rx * (((int)(cxy >> 16) + by_ - 2) + A.ry * ((int)(czb & 0x7FFFFFFFu) + bz_ - 2)));
+        const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + seg));
+        LvxHit h;
+        bool hit;
+        u32 kind3;
+        if (KIND == 0) {
+            const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + seg) + 1);
+            hit = lvx_tube_f32axis(ox, oy, oz, rdx, rdy, rdz, ra.x, ra.y, ra.z, rb.x, rb.y, rb.z, tube_r, h);
+            kind3 = 0;
+        } else {
+            float4 cc = ra;
+            kind3 = 1;
+            if (c.seg & 0x80000000u) {
+                cc = __ldg(reinterpret_cast<const float4 *>(A.rec + seg) + 1);
+                kind3 = 2;
+            }
+            hit = lvx_sphere<true>(ox, oy, oz, rdx, rdy, rdz, (double)cc.x, (double)cc.y, (double)cc.z, tube_r, h);
+        }
+        // ownership: the window whose range holds the entry parameter (:838, :858, :878)
+        if (!(hit && t0 <= h.t_in && h.t_in < t1)) continue;
         const u32 rmeta = __float_as_uint(ra.w);
         const u32 attr = rmeta & 0xFFu, lid = (rmeta >> 8) & 31u;
-#pragma unroll 1
-        for (u32 kind3 = 0; kind3 < 3; ++kind3) {
-            if (!(sv.mb & (1u << kind3))) continue;
-            LvxHit h;
-            bool hit;
-            if (kind3 == 0) {
-                hit = lvx_tube_f32axis(ox, oy, oz, rdx, rdy, rdz, ra.x, ra.y, ra.z, rb.x, rb.y, rb.z, tube_r, h);
-            } else {
-                const float cx = kind3 == 1 ? ra.x : rb.x, cy = kind3 == 1 ? ra.y : rb.y,
-                            cz = kind3 == 1 ? ra.z : rb.z;
-                hit = lvx_sphere<true>(ox, oy, oz, rdx, rdy, rdz, (double)cx, (double)cy, (double)cz, tube_r, h);
-            }
-            // ownership: the window whose range holds the entry parameter (:838, :858, :878)
-            if (!(hit && t0 <= h.t_in && h.t_in < t1)) continue;
-            double scale, alpha;
-            wf_shade(A, ox, oy, oz, rdx, rdy, rdz, h, attr, scale, alpha);
+        double scale, alpha;
+        wf_shade(A, ox, oy, oz, rdx, rdy, rdz, h, attr, scale, alpha);
+        const u32 cxy = __ldg(&wp->cxy), czb = __ldg(&wp->cz);
+        const int b = (int)(c.wb >> kWidBits);
+        const int bz_ = b / 9, by_ = (b - 9 * bz_) / 3, bx_ = b - 9 * bz_ - 3 * by_;
+        WfHit rec;
+        rec.t_in = h.t_in;
+        rec.scale = scale;
+        rec.alpha = alpha;
+        rec.lin = (u32)(((int)(cxy & 0xFFFFu) + bx_ - 2) +
+                        A.rx * (((int)(cxy >> 16) + by_ - 2) + A.ry * ((int)(czb & 0x7FFFFFFFu) + bz_ - 2)));
+        rec.seg = seg;
+        rec.meta = kind3 | (lid << 2) | (attr << 8);
+        rec.wid = wid;
+        rec.pad = 0;
+        rec.next = kNil;
+        const u32 j = atomicAdd(&A.hcnt[slot], 1u);
+        if (j < (u32)kHitSlots) {
+            A.hit_slot[(size_t)j * R + wid / wn] = rec;  // wid / wn: the ray's place in the live list
+        } else {
             const u32 e = queue_alloc(A.ctl->hit_cnt, q, A.capq_hit, 1u, &A.ctl->err, 4u);
             if (e == kNil) continue;
-            WfHit rec;
-            rec.t_in = h.t_in;
-            rec.scale = scale;
-            rec.alpha = alpha;
-            rec.lin = lin;
-            rec.seg = sv.seg;
-            rec.meta = kind3 | (lid << 2) | (attr << 8);
-            rec.wid = sv.wid;
-            rec.pad = 0;
             rec.next = atomicExch(&A.head[slot], e);
             A.hit[e] = rec;
         }
@@ -684,25 +735,66 @@ __device__ __forceinline__ void wf_accumulate(const WfArgs &A, WfTables &T, WfPi
     }
 }
 
+// The hits of one ray and iteration: the first kHitSlots sit ray-parallel in hit_slot
+// ([j][place in the live list]: neighbouring threads read neighbouring records), the
+// rest hangs in a linked list.  A reference is j for the former, kHitSlots + pool index
+// for the latter.
+struct WfRayHits {
+    const WfArgs &A;
+    u32 place, nslot, head;
+    __device__ __forceinline__ WfHit *at(u32 ref) const {
+        return ref < (u32)kHitSlots ? A.hit_slot + (size_t)ref * A.R + place : A.hit + (ref - kHitSlots);
+    }
+    // iteration: ref = first(); while (ref != kNil) { ...; ref = next(ref); }
+    __device__ __forceinline__ u32 first() const {
+        return nslot ? 0u : (head == kNil ? kNil : head + kHitSlots);
+    }
+    __device__ __forceinline__ u32 next(u32 ref) const {
+        if (ref < (u32)kHitSlots) {
+            if (ref + 1 < nslot) return ref + 1;
+            return head == kNil ? kNil : head + kHitSlots;
+        }
+        const u32 e = A.hit[ref - kHitSlots].next;
+        return e == kNil ? kNil : e + kHitSlots;
+    }
+};
+
 // Slow path for rays that crossed a window with more than 1024/3 candidates: the reference
 // keeps the first 1024 owned hits of a window in gather order and counts the rest in
 // window_overflow (_kernels.py:852-853).  Gather order is (segment, primitive).
-__device__ void wf_apply_window_cap(const WfArgs &A, u32 head) {
-    for (u32 a = head; a != kNil; a = A.hit[a].next) {
-        const u32 wid = A.hit[a].wid;
+__device__ void wf_apply_window_cap(const WfArgs &A, const WfRayHits &H) {
+    for (u32 a = H.first(); a != kNil; a = H.next(a)) {
+        WfHit *ha = H.at(a);
+        const u32 wid = ha->wid;
         if (!(A.win[wid].cz & 0x80000000u)) continue;
-        const u32 sa = A.hit[a].seg, ka = A.hit[a].meta & 3u;
+        const u32 sa = ha->seg, ka = ha->meta & 3u;
         u32 rank = 0;
-        for (u32 b = head; b != kNil; b = A.hit[b].next) {
-            if (A.hit[b].wid != wid) continue;
-            const u32 sb = A.hit[b].seg, kb = A.hit[b].meta & 3u;
+        for (u32 b = H.first(); b != kNil; b = H.next(b)) {
+            const WfHit *hb = H.at(b);
+            if (hb->wid != wid) continue;
+            const u32 sb = hb->seg, kb = hb->meta & 3u;
             if (sb < sa || (sb == sa && kb < ka)) rank += 1;
         }
         if (rank >= (u32)LVX_MAX_WINDOW_HITS) {
-            A.hit[a].meta |= 1u << 16;
+            ha->meta |= 1u << 16;
             A.win_over[wid] += 1;
         }
     }
+}
+
+__device__ __forceinline__ bool wf_composite_one(const WfArgs &A, WfTables &T, WfPixel &S, const WfHit &h,
+                                                 double tau) {
+    const u32 kind3 = h.meta & 3u;
+    float cx = 0.0f, cy = 0.0f, cz = 0.0f;
+    if (kind3) {
+        const float4 c = __ldg(reinterpret_cast<const float4 *>(A.rec + h.seg) + (kind3 - 1));
+        cx = c.x;
+        cy = c.y;
+        cz = c.z;
+    }
+    wf_accumulate(A, T, S, h.scale, h.alpha, h.lin, (h.meta >> 2) & 31u, (h.meta >> 8) & 0xFFu, kind3 != 0, cx,
+                  cy, cz);
+    return S.acc[3] >= tau;
 }
 
 __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A, int par) {
@@ -712,15 +804,20 @@ __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A
     const double tau = A.p.tau;
     for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n_live; i += gridDim.x * blockDim.x) {
         const u32 slot = A.live[par][i];
-        const u32 head = A.head[slot];
+        const u32 nhit = A.hcnt[slot];
         const u8 fl = A.flags[slot];
         bool finished = !(fl & 1);  // the walk is over: this was the last batch
         bool terminated = false;
         unsigned long long tests = 0, over = 0;
-        if (head != kNil) {
-            A.head[slot] = kNil;
+        if (nhit) {
+            A.hcnt[slot] = 0;
+            WfRayHits H = {A, i, nhit < (u32)kHitSlots ? nhit : (u32)kHitSlots, kNil};
+            if (nhit > (u32)kHitSlots) {
+                H.head = A.head[slot];
+                A.head[slot] = kNil;
+            }
             const bool big = (fl & 2) != 0;
-            if (big) wf_apply_window_cap(A, head);
+            if (big) wf_apply_window_cap(A, H);
             WfPixel S;
             S.acc[0] = A.acc[slot];
             S.acc[1] = A.acc[R + slot];
@@ -731,48 +828,37 @@ __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A
             S.seen_bloom = A.seen_bloom[slot];
             S.sph_bloom = A.sph_bloom[slot];
             WfTables T = {A, slot, A.ovf[slot]};
-            // gather + order
-            double s_t[kSortCap];
-            u32 s_idx[kSortCap];
-            int n = 0;
-            bool fits = true;
-            for (u32 e = head; e != kNil; e = A.hit[e].next) {
-                if (A.hit[e].meta & (1u << 16)) continue;  // dropped by the window cap
-                if (n == kSortCap) {
-                    fits = false;
-                    break;
-                }
-                const double t = A.hit[e].t_in;
-                int pos = n++;
-                while (pos > 0) {
-                    const u32 o = s_idx[pos - 1];
-                    bool before;
-                    if (t != s_t[pos - 1]) before = t < s_t[pos - 1];
-                    else before = wf_key_before(t, A.hit[e].lin, A.hit[e].seg, A.hit[e].meta, s_t[pos - 1],
-                                                A.hit[o].lin, A.hit[o].seg, A.hit[o].meta);
-                    if (!before) break;
-                    s_t[pos] = s_t[pos - 1];
-                    s_idx[pos] = o;
-                    --pos;
-                }
-                s_t[pos] = t;
-                s_idx[pos] = e;
-            }
             u32 term_wid = 0;
-            if (fits) {
-                for (int j = 0; j < n; ++j) {
-                    const WfHit h = A.hit[s_idx[j]];
-                    const u32 kind3 = h.meta & 3u;
-                    float cx = 0.0f, cy = 0.0f, cz = 0.0f;
-                    if (kind3) {
-                        const float4 c = __ldg(reinterpret_cast<const float4 *>(A.rec + h.seg) + (kind3 - 1));
-                        cx = c.x;
-                        cy = c.y;
-                        cz = c.z;
+            if (nhit <= (u32)kSortCap) {
+                // gather + order (insertion sort on t_in; full key only on ties)
+                double s_t[kSortCap];
+                u32 s_ref[kSortCap];
+                int n = 0;
+                for (u32 ref = H.first(); ref != kNil; ref = H.next(ref)) {
+                    const WfHit *hp = H.at(ref);
+                    if (hp->meta & (1u << 16)) continue;  // dropped by the window cap
+                    const double t = hp->t_in;
+                    int pos = n++;
+                    while (pos > 0) {
+                        bool before;
+                        if (t != s_t[pos - 1]) {
+                            before = t < s_t[pos - 1];
+                        } else {
+                            const WfHit *ho = H.at(s_ref[pos - 1]);
+                            before = wf_key_before(t, hp->lin, hp->seg, hp->meta, s_t[pos - 1], ho->lin, ho->seg,
+                                                   ho->meta);
+                        }
+                        if (!before) break;
+                        s_t[pos] = s_t[pos - 1];
+                        s_ref[pos] = s_ref[pos - 1];
+                        --pos;
                     }
-                    wf_accumulate(A, T, S, h.scale, h.alpha, h.lin, (h.meta >> 2) & 31u, (h.meta >> 8) & 0xFFu,
-                                  kind3 != 0, cx, cy, cz);
-                    if (S.acc[3] >= tau) {
+                    s_t[pos] = t;
+                    s_ref[pos] = ref;
+                }
+                for (int j = 0; j < n; ++j) {
+                    const WfHit h = *H.at(s_ref[j]);
+                    if (wf_composite_one(A, T, S, h, tau)) {
                         terminated = true;
                         term_wid = h.wid;
                         break;
@@ -788,14 +874,15 @@ __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A
                     u32 best = kNil;
                     double bt = 0.0;
                     u32 bl = 0, bs = 0, bm = 0;
-                    for (u32 e = head; e != kNil; e = A.hit[e].next) {
-                        const u32 m = A.hit[e].meta;
+                    for (u32 ref = H.first(); ref != kNil; ref = H.next(ref)) {
+                        const WfHit *hp = H.at(ref);
+                        const u32 m = hp->meta;
                         if (m & (1u << 16)) continue;
-                        const double t = A.hit[e].t_in;
-                        const u32 l = A.hit[e].lin, sg = A.hit[e].seg;
+                        const double t = hp->t_in;
+                        const u32 l = hp->lin, sg = hp->seg;
                         if (have_last && !wf_key_before(lt, ll, ls, lm, t, l, sg, m)) continue;
                         if (best == kNil || wf_key_before(t, l, sg, m, bt, bl, bs, bm)) {
-                            best = e;
+                            best = ref;
                             bt = t;
                             bl = l;
                             bs = sg;
@@ -803,18 +890,8 @@ __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A
                         }
                     }
                     if (best == kNil) break;
-                    const WfHit h = A.hit[best];
-                    const u32 kind3 = h.meta & 3u;
-                    float cx = 0.0f, cy = 0.0f, cz = 0.0f;
-                    if (kind3) {
-                        const float4 c = __ldg(reinterpret_cast<const float4 *>(A.rec + h.seg) + (kind3 - 1));
-                        cx = c.x;
-                        cy = c.y;
-                        cz = c.z;
-                    }
-                    wf_accumulate(A, T, S, h.scale, h.alpha, h.lin, (h.meta >> 2) & 31u, (h.meta >> 8) & 0xFFu,
-                                  kind3 != 0, cx, cy, cz);
-                    if (S.acc[3] >= tau) {
+                    const WfHit h = *H.at(best);
+                    if (wf_composite_one(A, T, S, h, tau)) {
                         terminated = true;
                         term_wid = h.wid;
                         break;
@@ -873,7 +950,9 @@ __global__ void wf_next_kernel(const WfArgs A, int par, int it_next) {
     const int t = threadIdx.x;
     if (t < kNQ) {
         A.ctl->item_cnt[t] = 0;
-        A.ctl->surv_cnt[t] = 0;
+        A.ctl->cand_cnt[t] = 0;
+        A.ctl->tube_cnt[t] = 0;
+        A.ctl->sph_cnt[t] = 0;
         A.ctl->hit_cnt[t] = 0;
     }
     if (t == 0) {
@@ -884,6 +963,11 @@ __global__ void wf_next_kernel(const WfArgs A, int par, int it_next) {
         if (wn > fit) wn = fit;
         if (wn < 1) wn = 1;
         A.ctl->wn = wn;
+        // later iterations hold few rays, all with low hit rates: let them run further
+        {
+            const int g = it_next - A.grow_from;
+            A.ctl->budget = (u32)A.cand_budget << (g < 0 ? 0 : (g < 8 ? g : 8));
+        }
     }
 }
 
@@ -891,7 +975,9 @@ __global__ void wf_begin_kernel(const WfArgs A) {
     const int t = threadIdx.x;
     if (t < kNQ) {
         A.ctl->item_cnt[t] = 0;
-        A.ctl->surv_cnt[t] = 0;
+        A.ctl->cand_cnt[t] = 0;
+        A.ctl->tube_cnt[t] = 0;
+        A.ctl->sph_cnt[t] = 0;
         A.ctl->hit_cnt[t] = 0;
     }
     if (t == 0) {
@@ -900,6 +986,7 @@ __global__ void wf_begin_kernel(const WfArgs A) {
         A.ctl->pool_cnt = 0;
         A.ctl->err = 0;
         A.ctl->wn = (u32)A.wn_sched;
+        A.ctl->budget = (u32)A.cand_budget;
     }
 }
 
@@ -908,8 +995,8 @@ struct WfLayout {
     size_t total;
     size_t ctl, pix, out_off, dir, dda_t, dda_i, flags, acc, tests, over, seen_bloom, sph_bloom, n_seen,
         n_sph, ovf, head, nwin, tab_key, tab_mask, tab_sph, pool_key, pool_mask, pool_sph, live0, live1, win,
-        win_over, item_wid, item_b, surv, hit;
-    u32 R, pool_cap, cap_win, capq_item, capq_surv, capq_hit;
+        win_over, item_wid, item_b, cand, tube, sph, hit, hit_slot, hcnt;
+    u32 R, pool_cap, cap_win, capq_item, capq_cand, capq_surv, capq_hit;
 };
 
 size_t take(size_t &cur, size_t bytes) {
@@ -924,10 +1011,11 @@ WfLayout wf_layout(i64 R, double scale) {
     L.R = (u32)R;
     const double f = scale < 1.0 ? 1.0 : scale;
     L.pool_cap = (u32)(R / 16 * f) + 1024;
-    L.cap_win = (u32)fmin(4.0e9, (double)R * 8.0);
+    L.cap_win = (u32)fmin((double)kWidMask, (double)R * 8.0);
     L.capq_item = (u32)fmin(4.0e9 / kNQ, ((double)R * 40.0 * f + 65536.0) / kNQ);
-    L.capq_surv = (u32)fmin(4.0e9 / kNQ, ((double)R * 12.0 * f + 65536.0) / kNQ);
-    L.capq_hit = (u32)fmin(4.0e9 / kNQ, ((double)R * 8.0 * f + 65536.0) / kNQ);
+    L.capq_cand = (u32)fmin(4.0e9 / kNQ, ((double)R * 56.0 * f + 65536.0) / kNQ);
+    L.capq_surv = (u32)fmin(4.0e9 / kNQ, ((double)R * 10.0 * f + 65536.0) / kNQ);
+    L.capq_hit = (u32)fmin(4.0e9 / kNQ, ((double)R * 2.0 * f + 65536.0) / kNQ);
     size_t c = 0;
     const size_t r = (size_t)R, po = (size_t)L.pool_cap * (LVX_MAX_SEEN - kInline);
     L.ctl = take(c, sizeof(WfCtl));
@@ -959,8 +1047,12 @@ WfLayout wf_layout(i64 R, double scale) {
     L.win_over = take(c, (size_t)L.cap_win * 4);
     L.item_wid = take(c, (size_t)L.capq_item * kNQ * 4);
     L.item_b = take(c, (size_t)L.capq_item * kNQ);
-    L.surv = take(c, (size_t)L.capq_surv * kNQ * sizeof(WfSurv));
+    L.cand = take(c, (size_t)L.capq_cand * kNQ * sizeof(WfEntry));
+    L.tube = take(c, (size_t)L.capq_surv * kNQ * sizeof(WfEntry));
+    L.sph = take(c, (size_t)L.capq_surv * kNQ * sizeof(WfEntry));
     L.hit = take(c, (size_t)L.capq_hit * kNQ * sizeof(WfHit));
+    L.hit_slot = take(c, r * kHitSlots * sizeof(WfHit));
+    L.hcnt = take(c, r * 4);
     L.total = take(c, 0);
     return L;
 }
@@ -1088,13 +1180,23 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     A.item_wid = (u32 *)(base + L.item_wid);
     A.item_b = (u8 *)(base + L.item_b);
     A.capq_item = L.capq_item;
-    A.surv = (WfSurv *)(base + L.surv);
+    A.cand = (WfEntry *)(base + L.cand);
+    A.tube = (WfEntry *)(base + L.tube);
+    A.sph = (WfEntry *)(base + L.sph);
+    A.capq_cand = L.capq_cand;
     A.capq_surv = L.capq_surv;
     A.hit = (WfHit *)(base + L.hit);
     A.capq_hit = L.capq_hit;
+    A.hit_slot = (WfHit *)(base + L.hit_slot);
+    A.hcnt = (u32 *)(base + L.hcnt);
     A.wn_sched = 8;
     A.cand_budget = 192;
+    A.grow_from = 2;
+    if (const char *e = getenv("LVX_WF_BUDGET")) A.cand_budget = atoi(e) > 0 ? atoi(e) : A.cand_budget;
+    if (const char *e = getenv("LVX_WF_GROW")) A.grow_from = atoi(e);
+    if (const char *e = getenv("LVX_WF_WN")) A.wn_sched = atoi(e) > 0 ? atoi(e) : A.wn_sched;
 
+    const bool debug = getenv("LVX_WF_DEBUG") != nullptr;
     cudaStream_t st = (cudaStream_t)stream;
     const int sms = lvx_sm_count();
     const unsigned grid_rays = (unsigned)(sms * 8), grid_q = (unsigned)(sms * 8);
@@ -1108,9 +1210,27 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
         for (int b = 0; b < burst; ++b, ++it) {
             const int par = it & 1;
             wf_walk_kernel<<<grid_rays, kThreadsWf, 0, st>>>(A, par);
+            wf_expand_kernel<<<grid_q, kThreadsWf, 0, st>>>(A);
             wf_cand_kernel<<<grid_q, kThreadsWf, 0, st>>>(A);
-            wf_exact_kernel<<<grid_q, kThreadsWf, 0, st>>>(A);
+            wf_exact_kernel<0><<<grid_q, kThreadsWf, 0, st>>>(A);
+            if (params->joints) wf_exact_kernel<1><<<grid_q, kThreadsWf, 0, st>>>(A);
             wf_composite_kernel<<<grid_rays, kThreadsWf, 0, st>>>(A, par);
+            if (debug) {
+                WfCtl c;
+                cudaMemcpyAsync(&c, A.ctl, sizeof(c), cudaMemcpyDeviceToHost, st);
+                cudaStreamSynchronize(st);
+                unsigned long long ni = 0, nc = 0, nt = 0, ns = 0, nh = 0;
+                for (int q = 0; q < kNQ; ++q) {
+                    ni += c.item_cnt[q];
+                    nc += c.cand_cnt[q];
+                    nt += c.tube_cnt[q];
+                    ns += c.sph_cnt[q];
+                    nh += c.hit_cnt[q];
+                }
+                fprintf(stderr, "wf it %2d: live %8u -> %8u  wn %4u budget %6u  items %10llu  candidates %10llu  tubes %9llu  "
+                        "spheres %9llu  listed hits %8llu\n",
+                        it, c.n_live[par], c.n_live[par ^ 1], c.wn, c.budget, ni, nc, nt, ns, nh);
+            }
             wf_next_kernel<<<1, 64, 0, st>>>(A, par, it + 1);
         }
         LVX_LAUNCH_CHECK();
