@@ -57,37 +57,32 @@ constexpr u32 kNil = 0xFFFFFFFFu;
 constexpr double kCullMarginWf = 1e-4;
 constexpr float kRejectMarginWf = 2e-3f;
 
+// one record per window that can own hits (per-ray stride layout: ray place * wn + k)
 struct __align__(16) WfWindow {
-    double t0, t1;
-    unsigned long long tests;  // intersection_tests up to and including this window
-    u32 slot;                  // ray
-    u32 cxy;                   // cell (x + 1) | (y + 1) << 16
-    u32 cz;                    // cell (z + 1) | big << 31
-    float q0x, q0y, q0z, tlen;
-    float fdx, fdy, fdz;       // float32 ray direction for the pre-reject
+    double t1;                 // end of the window's parameter range
+    unsigned long long tests;  // intersection_tests up to and including this window | big << 63
 };
-static_assert(sizeof(WfWindow) == 64, "window record is 64 bytes");
+static_assert(sizeof(WfWindow) == 16, "window record is 16 bytes");
+constexpr unsigned long long kBigBit = 1ull << 63;
 
 struct __align__(16) WfHit {
     double t_in, scale, alpha;
     u32 lin, seg, meta, next;  // meta: kind3 2 | lid 5 << 2 | attr 8 << 8 | dropped << 16
-    u32 wid, pad;
+    u32 pad[2];
 };
 static_assert(sizeof(WfHit) == 48, "hit record is 48 bytes");
 
-constexpr int kWidBits = 27;       // window ids; the neighbour bit (0..26) rides above them
-constexpr u32 kWidMask = (1u << kWidBits) - 1u;
 constexpr int kHitSlots = 12;      // hits per ray and iteration stored ray-parallel (the rest is listed)
 
 struct WfEntry {
-    u32 seg;  // segment (| sphere B << 31 in the sphere queue)
-    u32 wb;   // window id | neighbour bit << 27
+    u32 seg;   // segment (| sphere B << 31 in the sphere queue)
+    u32 item;  // the (ray, voxel) item it came from
 };
 
 // control block in device memory
 struct WfCtl {
     u32 n_live[2];
-    u32 item_cnt[kNQ], cand_cnt[kNQ], tube_cnt[kNQ], sph_cnt[kNQ], hit_cnt[kNQ];
+    u32 item_cnt[kNQ], tube_cnt[kNQ], sph_cnt[kNQ], hit_cnt[kNQ];
     u32 pool_cnt;
     u32 err;   // bit 0 items / candidates, 1 survivors, 2 listed hits, 3 table pool
     u32 wn;    // windows per ray of the current iteration
@@ -130,11 +125,14 @@ struct WfArgs {
     u32 *live[2];
     WfWindow *win;
     u32 cap_win;
-    u32 *item_wid;
-    u8 *item_b;
+    u32 *item_place, *item_lin;  // (ray place in the live list, home voxel)
+    float4 *item_q;              // ray point near the voxel, relative to the voxel's corner (float32)
+    double2 *item_t;             // own-voxel mode: parameter range of the item's window
     u32 capq_item;
-    WfEntry *cand, *tube, *sph;
-    u32 capq_cand, capq_surv;
+    float *fdir;                 // [3][R] float32 ray direction by place
+    double *span;                // [2][R] parameter range walked this iteration, by place
+    WfEntry *tube, *sph;
+    u32 capq_surv;
     WfHit *hit;       // overflow pool (linked lists)
     u32 capq_hit;
     WfHit *hit_slot;  // [kHitSlots][R], indexed by the ray's position in the live list
@@ -335,6 +333,20 @@ __global__ void __launch_bounds__(kThreadsWf) wf_init_kernel(const WfArgs A) {
 // ---------------------------------------------------------------------------------------
 // walk: one thread per live ray
 // ---------------------------------------------------------------------------------------
+
+// The 27-neighbourhood mask `e` of the cell the walk just left, re-expressed around the
+// cell it moved to (step d per axis, each in {-1, 0, 1}); voxels that leave the 3x3x3
+// frame drop out.
+__device__ __forceinline__ u32 shift_mask(u32 e, int dx, int dy, int dz) {
+    if (dx > 0) e = (e & 0x6DB6DB6u) >> 1;
+    else if (dx < 0) e = (e & 0x36DB6DBu) << 1;
+    if (dy > 0) e = (e & 0x7E3F1F8u) >> 3;
+    else if (dy < 0) e = (e & 0x0FC7E3Fu) << 3;
+    if (dz > 0) e = (e & 0x7FFFE00u) >> 9;
+    else if (dz < 0) e = (e & 0x003FFFFu) << 9;
+    return e;
+}
+
 __global__ void __launch_bounds__(kThreadsWf) wf_walk_kernel(const WfArgs A, int par) {
     const u32 n_live = A.ctl->n_live[par];
     const u32 wn = A.ctl->wn;
@@ -355,10 +367,23 @@ __global__ void __launch_bounds__(kThreadsWf) wf_walk_kernel(const WfArgs A, int
         unsigned long long tests = A.tests[slot];
         u32 kw = 0, csum = 0;
         bool big_any = false;
+        const double span0 = dda.t_cur;
+        // voxels already listed in this iteration, as a 27-neighbourhood mask around the
+        // previous cell: a voxel is tested once per iteration however many windows see it
+        u32 listed = 0;
+        int px = 0, py = 0, pz = 0;
         while (kw < wn && csum < budget) {
             int wx, wy, wz;
             double t0, t1;
             if (!dda.next(wx, wy, wz, t0, t1)) break;
+            if (listed) {
+                const int dx = wx - px, dy = wy - py, dz = wz - pz;
+                listed = (dx < -1 || dx > 1 || dy < -1 || dy > 1 || dz < -1 || dz > 1) ? 0u
+                                                                                     : shift_mask(listed, dx, dy, dz);
+            }
+            px = wx;
+            py = wy;
+            pz = wz;
             u32 nm, n;
             if (neighbor) {
                 const i64 pc = ((i64)(wz + 1) * (ry + 2) + (wy + 1)) * (rx + 2) + (wx + 1);
@@ -388,135 +413,116 @@ __global__ void __launch_bounds__(kThreadsWf) wf_walk_kernel(const WfArgs A, int
             if (nm == 0) continue;
             const bool big = n * tmul > (u32)LVX_MAX_WINDOW_HITS;
             big_any |= big;
-            const u32 wid = i * wn + kw;
-            const u32 ni = (u32)__popc(nm);
-            const u32 ib = queue_alloc(A.ctl->item_cnt, q, A.capq_item, ni, &A.ctl->err, 1u);
             WfWindow w;
-            w.t0 = t0;
             w.t1 = t1;
-            w.tests = tests;
-            w.slot = slot;
-            w.cxy = (u32)(wx + 1) | ((u32)(wy + 1) << 16);  // padded-grid coordinates (the walk starts at -1)
-            w.cz = (u32)(wz + 1) | (big ? 0x80000000u : 0u);
-            w.q0x = (float)(p0x - (double)wx);  // window-local float32 frame
-            w.q0y = (float)(p0y - (double)wy);
-            w.q0z = (float)(p0z - (double)wz);
-            w.tlen = (float)(t1 - t0);
-            w.fdx = (float)ddx;
-            w.fdy = (float)ddy;
-            w.fdz = (float)ddz;
-            A.win[wid] = w;
-            if (big) A.win_over[wid] = 0;
+            w.tests = tests | (big ? kBigBit : 0ull);
+            A.win[i * wn + kw] = w;
+            if (big) A.win_over[i * wn + kw] = 0;
+            kw += 1;
+            const u32 fresh = nm & ~listed;
+            listed |= nm;
+            if (fresh == 0) continue;
+            const u32 ni = (u32)__popc(fresh);
+            const u32 ib = queue_alloc(A.ctl->item_cnt, q, A.capq_item, ni, &A.ctl->err, 1u);
             if (ib != kNil) {
                 u32 j = ib;
-                for (u32 mm = nm; mm; mm &= mm - 1, ++j) {
-                    A.item_wid[j] = wid;
-                    A.item_b[j] = (u8)(__ffs((int)mm) - 1);
+                for (u32 mm = fresh; mm; mm &= mm - 1, ++j) {
+                    const int b = __ffs((int)mm) - 1;
+                    const int bz_ = b / 9, by_ = (b - 9 * bz_) / 3, bx_ = b - 9 * bz_ - 3 * by_;
+                    const int hx = wx + bx_ - 1, hy = wy + by_ - 1, hz = wz + bz_ - 1;
+                    A.item_place[j] = i;
+                    A.item_lin[j] = (u32)(hx + rx * (hy + ry * hz));
+                    // voxel-local float32 frame for the pre-reject
+                    A.item_q[j] = make_float4((float)(p0x - (double)hx), (float)(p0y - (double)hy),
+                                              (float)(p0z - (double)hz), 0.0f);
+                    // own-voxel mode: only the window of the voxel itself gathers it (:797-799)
+                    if (!neighbor) A.item_t[j] = make_double2(t0, t1);
                 }
             }
-            kw += 1;
         }
         dda_store(A, slot, dda);
         A.tests[slot] = tests;
         A.nwin[slot] = kw;
         A.flags[slot] = (u8)((dda.alive ? 1 : 0) | (big_any ? 2 : 0));
+        A.fdir[i] = (float)ddx;
+        A.fdir[R + i] = (float)ddy;
+        A.fdir[2 * R + i] = (float)ddz;
+        A.span[i] = span0;
+        A.span[R + i] = dda.t_cur;
     }
 }
 
-// Conservative float32 test in window-local coordinates (see lvx_render.cu).
-__device__ __forceinline__ bool wf_may_enter(float cx, float cy, float cz, float q0x, float q0y,
-                                             float q0z, float dx, float dy, float dz, float tlen,
-                                             float reach) {
+// Conservative float32 test: can a primitive whose points all lie within `reach` of
+// centre c be touched by the ray (q0, unit d)?  (distance of c to the ray's line)
+__device__ __forceinline__ bool wf_near_line(float cx, float cy, float cz, float q0x, float q0y, float q0z,
+                                             float dx, float dy, float dz, float reach) {
     const float wx = cx - q0x, wy = cy - q0y, wz = cz - q0z;
     const float tc = wx * dx + wy * dy + wz * dz;
     const float d2 = (wx * wx + wy * wy + wz * wz) - tc * tc;
-    return d2 <= reach * reach && tc >= -reach && tc <= tlen + reach;
+    return d2 <= reach * reach;
 }
 
 // ---------------------------------------------------------------------------------------
-// expand: one thread per (window, neighbour voxel) item -> one queue entry per segment
-// ---------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreadsWf) wf_expand_kernel(const WfArgs A) {
-    __shared__ QueueView V;
-    queue_view_load(V, A.ctl->item_cnt, A.capq_item);
-    const u32 total = V.pre[kNQ];
-    const int q = warp_queue();
-    for (u32 f = blockIdx.x * blockDim.x + threadIdx.x; f < total; f += gridDim.x * blockDim.x) {
-        const u32 it = queue_view_index(V, f, A.capq_item);
-        const u32 wid = A.item_wid[it];
-        const int b = (int)A.item_b[it];
-        const WfWindow *wp = A.win + wid;
-        const u32 cxy = __ldg(&wp->cxy), czb = __ldg(&wp->cz);
-        const int bz_ = b / 9, by_ = (b - 9 * bz_) / 3, bx_ = b - 9 * bz_ - 3 * by_;
-        const u32 lin = (u32)(((int)(cxy & 0xFFFFu) + bx_ - 2) +
-                              A.rx * (((int)(cxy >> 16) + by_ - 2) + A.ry * ((int)(czb & 0x7FFFFFFFu) + bz_ - 2)));
-        const u32 cnt = __ldg(A.counts + lin);
-        const u32 base = __ldg(A.offsets + lin);
-        const u32 e = queue_alloc(A.ctl->cand_cnt, q, A.capq_cand, cnt, &A.ctl->err, 1u);
-        if (e == kNil) continue;
-        const u32 wb = wid | ((u32)b << kWidBits);
-        for (u32 sg = 0; sg < cnt; ++sg) {
-            WfEntry c;
-            c.seg = base + sg;
-            c.wb = wb;
-            A.cand[e + sg] = c;
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------------------
-// candidates: one thread per (window, segment) pair: conservative float32 pre-reject
+// candidates: one thread per (ray, voxel) item: conservative float32 pre-reject of the
+// voxel's segments against the ray
 // ---------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreadsWf) wf_cand_kernel(const WfArgs A) {
     __shared__ QueueView V;
-    queue_view_load(V, A.ctl->cand_cnt, A.capq_cand);
+    queue_view_load(V, A.ctl->item_cnt, A.capq_item);
     const u32 total = V.pre[kNQ];
     const bool joints = A.p.joints != 0;
     const float reach_pt = (float)A.p.tube_r + kRejectMarginWf;
     const int q = warp_queue();
+    const size_t R = A.R;
     for (u32 f = blockIdx.x * blockDim.x + threadIdx.x; f < total; f += gridDim.x * blockDim.x) {
-        const WfEntry c = A.cand[queue_view_index(V, f, A.capq_cand)];
-        const WfWindow *wp = A.win + (c.wb & kWidMask);
-        const uint4 w1 = __ldg(reinterpret_cast<const uint4 *>(wp) + 1);  // tests(2) slot cxy
-        const uint4 w2 = __ldg(reinterpret_cast<const uint4 *>(wp) + 2);  // cz q0x q0y q0z
-        const uint4 w3 = __ldg(reinterpret_cast<const uint4 *>(wp) + 3);  // tlen fdx fdy fdz
-        const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + c.seg));
-        const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + c.seg) + 1);
-        const float fwx = (float)((int)(w1.w & 0xFFFFu) - 1), fwy = (float)((int)(w1.w >> 16) - 1),
-                    fwz = (float)((int)(w2.x & 0x7FFFFFFFu) - 1);
-        const float q0x = __uint_as_float(w2.y), q0y = __uint_as_float(w2.z), q0z = __uint_as_float(w2.w);
-        const float tlen = __uint_as_float(w3.x);
-        const float fdx = __uint_as_float(w3.y), fdy = __uint_as_float(w3.z), fdz = __uint_as_float(w3.w);
-        const float ax = ra.x - fwx, ay = ra.y - fwy, az = ra.z - fwz;
-        const float bx = rb.x - fwx, by = rb.y - fwy, bz = rb.z - fwz;
-        u32 mk = 0;
-        // the tube AND both joint spheres lie inside the segment's bounding sphere
-        if (wf_may_enter(0.5f * (ax + bx), 0.5f * (ay + by), 0.5f * (az + bz), q0x, q0y, q0z, fdx, fdy, fdz,
-                         tlen, rb.w + reach_pt)) {
-            // the tube's entry point lies on the ray within tube_r of the segment's axis line:
-            // |w . (d x u)| <= reach |d x u|  (absolute slack >> float32 rounding)
-            const float ux = bx - ax, uy = by - ay, uz = bz - az;
-            const float nx = fdy * uz - fdz * uy, ny = fdz * ux - fdx * uz, nz = fdx * uy - fdy * ux;
-            const float wn = (ax - q0x) * nx + (ay - q0y) * ny + (az - q0z) * nz;
-            if (wn * wn <= reach_pt * reach_pt * (nx * nx + ny * ny + nz * nz) + 1e-6f) mk = 1u;
-            if (joints) {
-                if (wf_may_enter(ax, ay, az, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mk |= 2u;
-                if (wf_may_enter(bx, by, bz, q0x, q0y, q0z, fdx, fdy, fdz, tlen, reach_pt)) mk |= 4u;
+        const u32 it = queue_view_index(V, f, A.capq_item);
+        const u32 place = A.item_place[it], lin = A.item_lin[it];
+        const float4 q0 = A.item_q[it];
+        const float fdx = A.fdir[place], fdy = A.fdir[R + place], fdz = A.fdir[2 * R + place];
+        const u32 cnt = __ldg(A.counts + lin);
+        const u32 base = __ldg(A.offsets + lin);
+        const int hz = (int)(lin / (u32)(A.rx * A.ry));
+        const int hy = (int)((lin - (u32)hz * (u32)(A.rx * A.ry)) / (u32)A.rx);
+        const int hx = (int)(lin - (u32)hz * (u32)(A.rx * A.ry) - (u32)hy * (u32)A.rx);
+        const float fhx = (float)hx, fhy = (float)hy, fhz = (float)hz;
+        for (u32 sg = 0; sg < cnt; ++sg) {
+            const u32 seg = base + sg;
+            const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + seg));
+            const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + seg) + 1);
+            const float ax = ra.x - fhx, ay = ra.y - fhy, az = ra.z - fhz;
+            const float bx = rb.x - fhx, by = rb.y - fhy, bz = rb.z - fhz;
+            u32 mk = 0;
+            // the tube AND both joint spheres lie inside the segment's bounding sphere
+            if (wf_near_line(0.5f * (ax + bx), 0.5f * (ay + by), 0.5f * (az + bz), q0.x, q0.y, q0.z, fdx, fdy,
+                             fdz, rb.w + reach_pt)) {
+                // the tube's entry point lies on the ray within tube_r of the segment's axis line:
+                // |w . (d x u)| <= reach |d x u|  (absolute slack >> float32 rounding)
+                const float ux = bx - ax, uy = by - ay, uz = bz - az;
+                const float nx = fdy * uz - fdz * uy, ny = fdz * ux - fdx * uz, nz = fdx * uy - fdy * ux;
+                const float wn = (ax - q0.x) * nx + (ay - q0.y) * ny + (az - q0.z) * nz;
+                if (wn * wn <= reach_pt * reach_pt * (nx * nx + ny * ny + nz * nz) + 1e-6f) mk = 1u;
+                if (joints) {
+                    if (wf_near_line(ax, ay, az, q0.x, q0.y, q0.z, fdx, fdy, fdz, reach_pt)) mk |= 2u;
+                    if (wf_near_line(bx, by, bz, q0.x, q0.y, q0.z, fdx, fdy, fdz, reach_pt)) mk |= 4u;
+                }
             }
-        }
-        if (mk & 1u) {
-            const u32 e = queue_alloc(A.ctl->tube_cnt, q, A.capq_surv, 1u, &A.ctl->err, 2u);
-            if (e != kNil) A.tube[e] = c;
-        }
-        if (mk & 6u) {
-            const u32 ns = (mk & 2u ? 1u : 0u) + (mk & 4u ? 1u : 0u);
-            u32 e = queue_alloc(A.ctl->sph_cnt, q, A.capq_surv, ns, &A.ctl->err, 2u);
-            if (e != kNil) {
-                WfEntry sa = c;
-                if (mk & 2u) A.sph[e++] = sa;
-                if (mk & 4u) {
-                    sa.seg |= 0x80000000u;
-                    A.sph[e] = sa;
+            if (mk & 1u) {
+                const u32 e = queue_alloc(A.ctl->tube_cnt, q, A.capq_surv, 1u, &A.ctl->err, 2u);
+                if (e != kNil) {
+                    WfEntry c = {seg, it};
+                    A.tube[e] = c;
+                }
+            }
+            if (mk & 6u) {
+                const u32 ns = (mk & 2u ? 1u : 0u) + (mk & 4u ? 1u : 0u);
+                u32 e = queue_alloc(A.ctl->sph_cnt, q, A.capq_surv, ns, &A.ctl->err, 2u);
+                if (e != kNil) {
+                    WfEntry c = {seg, it};
+                    if (mk & 2u) A.sph[e++] = c;
+                    if (mk & 4u) {
+                        c.seg |= 0x80000000u;
+                        A.sph[e] = c;
+                    }
                 }
             }
         }
@@ -564,7 +570,7 @@ __device__ __forceinline__ void wf_shade(const WfArgs &A, double ox, double oy, 
 // exact: one thread per surviving primitive (KIND 0: tubes, 1: joint spheres)
 // ---------------------------------------------------------------------------------------
 template <int KIND>
-__global__ void __launch_bounds__(kThreadsWf) wf_exact_kernel(const WfArgs A) {
+__global__ void __launch_bounds__(kThreadsWf) wf_exact_kernel(const WfArgs A, int par) {
     __shared__ QueueView V;
     queue_view_load(V, KIND == 0 ? A.ctl->tube_cnt : A.ctl->sph_cnt, A.capq_surv);
     const u32 total = V.pre[kNQ];
@@ -572,14 +578,13 @@ __global__ void __launch_bounds__(kThreadsWf) wf_exact_kernel(const WfArgs A) {
     const double tube_r = A.p.tube_r;
     const int q = warp_queue();
     const size_t R = A.R;
-    const u32 wn = A.ctl->wn;
     const WfEntry *queue = KIND == 0 ? A.tube : A.sph;
+    const bool neighbor = A.p.neighbor != 0;
     for (u32 f = blockIdx.x * blockDim.x + threadIdx.x; f < total; f += gridDim.x * blockDim.x) {
         const WfEntry c = queue[queue_view_index(V, f, A.capq_surv)];
-        const u32 wid = c.wb & kWidMask, seg = c.seg & 0x7FFFFFFFu;
-        const WfWindow *wp = A.win + wid;
-        const double t0 = __ldg(&wp->t0), t1 = __ldg(&wp->t1);
-        const u32 slot = __ldg(&wp->slot);
+        const u32 seg = c.seg & 0x7FFFFFFFu;
+        const u32 place = A.item_place[c.item];
+        const u32 slot = A.live[par][place];
         const double rdx = A.dir[slot], rdy = A.dir[R + slot], rdz = A.dir[2 * R + slot];
         const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + seg));
         LvxHit h;
@@ -598,29 +603,32 @@ __global__ void __launch_bounds__(kThreadsWf) wf_exact_kernel(const WfArgs A) {
             }
             hit = lvx_sphere<true>(ox, oy, oz, rdx, rdy, rdz, (double)cc.x, (double)cc.y, (double)cc.z, tube_r, h);
         }
-        // ownership: the window whose range holds the entry parameter (:838, :858, :878)
-        if (!(hit && t0 <= h.t_in && h.t_in < t1)) continue;
+        // ownership (:838, :858, :878): a hit belongs to the window whose range holds its entry
+        // parameter; the windows tile the walked range, so every hit entered inside the range
+        // walked this iteration is owned by exactly one of this iteration's windows
+        if (!hit) continue;
+        if (neighbor) {
+            if (!(A.span[place] <= h.t_in && h.t_in < A.span[R + place])) continue;
+        } else {
+            const double2 tr = A.item_t[c.item];
+            if (!(tr.x <= h.t_in && h.t_in < tr.y)) continue;
+        }
         const u32 rmeta = __float_as_uint(ra.w);
         const u32 attr = rmeta & 0xFFu, lid = (rmeta >> 8) & 31u;
         double scale, alpha;
         wf_shade(A, ox, oy, oz, rdx, rdy, rdz, h, attr, scale, alpha);
-        const u32 cxy = __ldg(&wp->cxy), czb = __ldg(&wp->cz);
-        const int b = (int)(c.wb >> kWidBits);
-        const int bz_ = b / 9, by_ = (b - 9 * bz_) / 3, bx_ = b - 9 * bz_ - 3 * by_;
         WfHit rec;
         rec.t_in = h.t_in;
         rec.scale = scale;
         rec.alpha = alpha;
-        rec.lin = (u32)(((int)(cxy & 0xFFFFu) + bx_ - 2) +
-                        A.rx * (((int)(cxy >> 16) + by_ - 2) + A.ry * ((int)(czb & 0x7FFFFFFFu) + bz_ - 2)));
+        rec.lin = A.item_lin[c.item];
         rec.seg = seg;
         rec.meta = kind3 | (lid << 2) | (attr << 8);
-        rec.wid = wid;
-        rec.pad = 0;
+        rec.pad[0] = rec.pad[1] = 0;
         rec.next = kNil;
         const u32 j = atomicAdd(&A.hcnt[slot], 1u);
         if (j < (u32)kHitSlots) {
-            A.hit_slot[(size_t)j * R + wid / wn] = rec;  // wid / wn: the ray's place in the live list
+            A.hit_slot[(size_t)j * R + place] = rec;
         } else {
             const u32 e = queue_alloc(A.ctl->hit_cnt, q, A.capq_hit, 1u, &A.ctl->err, 4u);
             if (e == kNil) continue;
@@ -759,25 +767,41 @@ struct WfRayHits {
     }
 };
 
+// Index (within the ray's windows of this iteration) of the window that owns parameter t:
+// the first one whose range ends after t.
+__device__ __forceinline__ u32 wf_find_window(const WfWindow *w, u32 nw, double t) {
+    u32 lo = 0, hi = nw;  // answer in [lo, hi)
+    while (hi - lo > 1) {
+        const u32 mid = (lo + hi) >> 1;
+        if (w[mid - 1].t1 > t) hi = mid;
+        else lo = mid;
+    }
+    return lo;
+}
+
 // Slow path for rays that crossed a window with more than 1024/3 candidates: the reference
 // keeps the first 1024 owned hits of a window in gather order and counts the rest in
 // window_overflow (_kernels.py:852-853).  Gather order is (segment, primitive).
-__device__ void wf_apply_window_cap(const WfArgs &A, const WfRayHits &H) {
+__device__ void wf_apply_window_cap(const WfArgs &A, const WfRayHits &H, const WfWindow *w, u32 nw, u32 w0) {
     for (u32 a = H.first(); a != kNil; a = H.next(a)) {
         WfHit *ha = H.at(a);
-        const u32 wid = ha->wid;
-        if (!(A.win[wid].cz & 0x80000000u)) continue;
+        ha->pad[0] = wf_find_window(w, nw, ha->t_in);
+    }
+    for (u32 a = H.first(); a != kNil; a = H.next(a)) {
+        WfHit *ha = H.at(a);
+        const u32 k = ha->pad[0];
+        if (!(w[k].tests & kBigBit)) continue;
         const u32 sa = ha->seg, ka = ha->meta & 3u;
         u32 rank = 0;
         for (u32 b = H.first(); b != kNil; b = H.next(b)) {
             const WfHit *hb = H.at(b);
-            if (hb->wid != wid) continue;
+            if (hb->pad[0] != k) continue;
             const u32 sb = hb->seg, kb = hb->meta & 3u;
             if (sb < sa || (sb == sa && kb < ka)) rank += 1;
         }
         if (rank >= (u32)LVX_MAX_WINDOW_HITS) {
             ha->meta |= 1u << 16;
-            A.win_over[wid] += 1;
+            A.win_over[w0 + k] += 1;
         }
     }
 }
@@ -817,7 +841,9 @@ __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A
                 A.head[slot] = kNil;
             }
             const bool big = (fl & 2) != 0;
-            if (big) wf_apply_window_cap(A, H);
+            const u32 w0 = i * wn, nw = A.nwin[slot];
+            const WfWindow *wins = A.win + w0;
+            if (big) wf_apply_window_cap(A, H, wins, nw, w0);
             WfPixel S;
             S.acc[0] = A.acc[slot];
             S.acc[1] = A.acc[R + slot];
@@ -828,7 +854,7 @@ __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A
             S.seen_bloom = A.seen_bloom[slot];
             S.sph_bloom = A.sph_bloom[slot];
             WfTables T = {A, slot, A.ovf[slot]};
-            u32 term_wid = 0;
+            double term_t = 0.0;
             if (nhit <= (u32)kSortCap) {
                 // gather + order (insertion sort on t_in; full key only on ties)
                 double s_t[kSortCap];
@@ -860,7 +886,7 @@ __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A
                     const WfHit h = *H.at(s_ref[j]);
                     if (wf_composite_one(A, T, S, h, tau)) {
                         terminated = true;
-                        term_wid = h.wid;
+                        term_t = h.t_in;
                         break;
                     }
                 }
@@ -893,7 +919,7 @@ __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A
                     const WfHit h = *H.at(best);
                     if (wf_composite_one(A, T, S, h, tau)) {
                         terminated = true;
-                        term_wid = h.wid;
+                        term_t = h.t_in;
                         break;
                     }
                     have_last = true;
@@ -912,19 +938,18 @@ __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A
             A.seen_bloom[slot] = S.seen_bloom;
             A.sph_bloom[slot] = S.sph_bloom;
             A.ovf[slot] = T.ovf;
+            const u32 term_k = terminated ? wf_find_window(wins, nw, term_t) : 0u;
             if (big) {
                 // window_overflow of the windows gathered up to (and including) the last one used
-                const u32 w0 = i * wn, nw = A.nwin[slot];
                 unsigned long long ov = 0;
                 for (u32 k = 0; k < nw; ++k) {
-                    const u32 wid = w0 + k;
-                    if (A.win[wid].cz & 0x80000000u) ov += A.win_over[wid];
-                    if (terminated && wid == term_wid) break;
+                    if (wins[k].tests & kBigBit) ov += A.win_over[w0 + k];
+                    if (terminated && k == term_k) break;
                 }
                 A.over[slot] += ov;
             }
             if (terminated) {
-                tests = A.win[term_wid].tests;
+                tests = wins[term_k].tests & ~kBigBit;
                 finished = true;
             }
         }
@@ -950,7 +975,6 @@ __global__ void wf_next_kernel(const WfArgs A, int par, int it_next) {
     const int t = threadIdx.x;
     if (t < kNQ) {
         A.ctl->item_cnt[t] = 0;
-        A.ctl->cand_cnt[t] = 0;
         A.ctl->tube_cnt[t] = 0;
         A.ctl->sph_cnt[t] = 0;
         A.ctl->hit_cnt[t] = 0;
@@ -975,7 +999,6 @@ __global__ void wf_begin_kernel(const WfArgs A) {
     const int t = threadIdx.x;
     if (t < kNQ) {
         A.ctl->item_cnt[t] = 0;
-        A.ctl->cand_cnt[t] = 0;
         A.ctl->tube_cnt[t] = 0;
         A.ctl->sph_cnt[t] = 0;
         A.ctl->hit_cnt[t] = 0;
@@ -995,8 +1018,8 @@ struct WfLayout {
     size_t total;
     size_t ctl, pix, out_off, dir, dda_t, dda_i, flags, acc, tests, over, seen_bloom, sph_bloom, n_seen,
         n_sph, ovf, head, nwin, tab_key, tab_mask, tab_sph, pool_key, pool_mask, pool_sph, live0, live1, win,
-        win_over, item_wid, item_b, cand, tube, sph, hit, hit_slot, hcnt;
-    u32 R, pool_cap, cap_win, capq_item, capq_cand, capq_surv, capq_hit;
+        win_over, item_place, item_lin, item_q, item_t, fdir, span, tube, sph, hit, hit_slot, hcnt;
+    u32 R, pool_cap, cap_win, capq_item, capq_surv, capq_hit;
 };
 
 size_t take(size_t &cur, size_t bytes) {
@@ -1011,9 +1034,8 @@ WfLayout wf_layout(i64 R, double scale) {
     L.R = (u32)R;
     const double f = scale < 1.0 ? 1.0 : scale;
     L.pool_cap = (u32)(R / 16 * f) + 1024;
-    L.cap_win = (u32)fmin((double)kWidMask, (double)R * 8.0);
-    L.capq_item = (u32)fmin(4.0e9 / kNQ, ((double)R * 40.0 * f + 65536.0) / kNQ);
-    L.capq_cand = (u32)fmin(4.0e9 / kNQ, ((double)R * 56.0 * f + 65536.0) / kNQ);
+    L.cap_win = (u32)fmin(4.0e9, (double)R * 8.0);
+    L.capq_item = (u32)fmin(4.0e9 / kNQ, ((double)R * 24.0 * f + 65536.0) / kNQ);
     L.capq_surv = (u32)fmin(4.0e9 / kNQ, ((double)R * 10.0 * f + 65536.0) / kNQ);
     L.capq_hit = (u32)fmin(4.0e9 / kNQ, ((double)R * 2.0 * f + 65536.0) / kNQ);
     size_t c = 0;
@@ -1045,9 +1067,12 @@ WfLayout wf_layout(i64 R, double scale) {
     L.live1 = take(c, r * 4);
     L.win = take(c, (size_t)L.cap_win * sizeof(WfWindow));
     L.win_over = take(c, (size_t)L.cap_win * 4);
-    L.item_wid = take(c, (size_t)L.capq_item * kNQ * 4);
-    L.item_b = take(c, (size_t)L.capq_item * kNQ);
-    L.cand = take(c, (size_t)L.capq_cand * kNQ * sizeof(WfEntry));
+    L.item_place = take(c, (size_t)L.capq_item * kNQ * 4);
+    L.item_lin = take(c, (size_t)L.capq_item * kNQ * 4);
+    L.item_q = take(c, (size_t)L.capq_item * kNQ * 16);
+    L.item_t = take(c, (size_t)L.capq_item * kNQ * 16);
+    L.fdir = take(c, r * 12);
+    L.span = take(c, r * 16);
     L.tube = take(c, (size_t)L.capq_surv * kNQ * sizeof(WfEntry));
     L.sph = take(c, (size_t)L.capq_surv * kNQ * sizeof(WfEntry));
     L.hit = take(c, (size_t)L.capq_hit * kNQ * sizeof(WfHit));
@@ -1177,13 +1202,15 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     A.win = (WfWindow *)(base + L.win);
     A.cap_win = L.cap_win;
     A.win_over = (u32 *)(base + L.win_over);
-    A.item_wid = (u32 *)(base + L.item_wid);
-    A.item_b = (u8 *)(base + L.item_b);
+    A.item_place = (u32 *)(base + L.item_place);
+    A.item_lin = (u32 *)(base + L.item_lin);
+    A.item_q = (float4 *)(base + L.item_q);
+    A.item_t = (double2 *)(base + L.item_t);
+    A.fdir = (float *)(base + L.fdir);
+    A.span = (double *)(base + L.span);
     A.capq_item = L.capq_item;
-    A.cand = (WfEntry *)(base + L.cand);
     A.tube = (WfEntry *)(base + L.tube);
     A.sph = (WfEntry *)(base + L.sph);
-    A.capq_cand = L.capq_cand;
     A.capq_surv = L.capq_surv;
     A.hit = (WfHit *)(base + L.hit);
     A.capq_hit = L.capq_hit;
@@ -1191,7 +1218,7 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     A.hcnt = (u32 *)(base + L.hcnt);
     A.wn_sched = 8;
     A.cand_budget = 192;
-    A.grow_from = 2;
+    A.grow_from = 4;
     if (const char *e = getenv("LVX_WF_BUDGET")) A.cand_budget = atoi(e) > 0 ? atoi(e) : A.cand_budget;
     if (const char *e = getenv("LVX_WF_GROW")) A.grow_from = atoi(e);
     if (const char *e = getenv("LVX_WF_WN")) A.wn_sched = atoi(e) > 0 ? atoi(e) : A.wn_sched;
@@ -1210,10 +1237,9 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
         for (int b = 0; b < burst; ++b, ++it) {
             const int par = it & 1;
             wf_walk_kernel<<<grid_rays, kThreadsWf, 0, st>>>(A, par);
-            wf_expand_kernel<<<grid_q, kThreadsWf, 0, st>>>(A);
             wf_cand_kernel<<<grid_q, kThreadsWf, 0, st>>>(A);
-            wf_exact_kernel<0><<<grid_q, kThreadsWf, 0, st>>>(A);
-            if (params->joints) wf_exact_kernel<1><<<grid_q, kThreadsWf, 0, st>>>(A);
+            wf_exact_kernel<0><<<grid_q, kThreadsWf, 0, st>>>(A, par);
+            if (params->joints) wf_exact_kernel<1><<<grid_q, kThreadsWf, 0, st>>>(A, par);
             wf_composite_kernel<<<grid_rays, kThreadsWf, 0, st>>>(A, par);
             if (debug) {
                 WfCtl c;
@@ -1222,7 +1248,6 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
                 unsigned long long ni = 0, nc = 0, nt = 0, ns = 0, nh = 0;
                 for (int q = 0; q < kNQ; ++q) {
                     ni += c.item_cnt[q];
-                    nc += c.cand_cnt[q];
                     nt += c.tube_cnt[q];
                     ns += c.sph_cnt[q];
                     nh += c.hit_cnt[q];
