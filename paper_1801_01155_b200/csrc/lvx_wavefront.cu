@@ -66,11 +66,25 @@ static_assert(sizeof(WfWindow) == 16, "window record is 16 bytes");
 constexpr unsigned long long kBigBit = 1ull << 63;
 
 struct __align__(16) WfHit {
-    double t_in, scale, alpha;
-    u32 lin, seg, meta, next;  // meta: kind3 2 | lid 5 << 2 | attr 8 << 8 | dropped << 16
-    u32 pad[2];
+    double t_in;
+    // the rest of the reference's order (home voxel, lid, kind, then gather order) and the
+    // hit's small fields as one integer:
+    //   lin << 24 | lid << 19 | (kind != tube) << 18 | index in voxel << 10 | kind3 << 8 | attr
+    unsigned long long key2;
+    double scale, alpha;
+    float cx, cy, cz;  // sphere centre (joint hits)
+    u32 next;          // overflow list link; bit 31: dropped by the window cap
 };
 static_assert(sizeof(WfHit) == 48, "hit record is 48 bytes");
+constexpr u32 kDropped = 0x80000000u;
+__device__ __forceinline__ u32 hit_lin(unsigned long long k) { return (u32)(k >> 24); }
+__device__ __forceinline__ u32 hit_lid(unsigned long long k) { return (u32)(k >> 19) & 31u; }
+__device__ __forceinline__ u32 hit_kind3(unsigned long long k) { return (u32)(k >> 8) & 3u; }
+__device__ __forceinline__ u32 hit_attr(unsigned long long k) { return (u32)k & 0xFFu; }
+// gather order inside a window: (voxel scan order, index in voxel, primitive)
+__device__ __forceinline__ unsigned long long hit_gather(unsigned long long k) {
+    return ((k >> 24) << 10) | (((k >> 10) & 255ull) << 2) | ((k >> 8) & 3ull);
+}
 
 constexpr int kHitSlots = 12;      // hits per ray and iteration stored ray-parallel (the rest is listed)
 
@@ -78,6 +92,26 @@ struct WfEntry {
     u32 seg;   // segment (| sphere B << 31 in the sphere queue)
     u32 item;  // the (ray, voxel) item it came from
 };
+
+// per-ray state, one record per pixel slot (read and written with 16-byte accesses)
+struct __align__(16) WfRayWalk {   // owned by the walk
+    double dir[3];
+    double t_cur, t_exit, tmax_x, tmax_y, tmax_z;
+    int ix, iy, iz;
+    u32 flags;                     // bit 0 walk alive, bit 1 big window seen this iteration
+    unsigned long long tests;      // intersection_tests of the windows walked so far
+    u32 nwin, pad;                 // windows recorded this iteration
+};
+static_assert(sizeof(WfRayWalk) == 96, "walk state is 96 bytes");
+
+struct __align__(16) WfRayPix {    // owned by the compositor
+    double acc[4];
+    unsigned long long seen_bloom, sph_bloom;
+    unsigned long long over;
+    u32 n_seen, n_sph;
+    u32 ovf, pix, out_off, pad;
+};
+static_assert(sizeof(WfRayPix) == 80, "pixel state is 80 bytes");
 
 // control block in device memory
 struct WfCtl {
@@ -109,14 +143,9 @@ struct WfArgs {
     // scratch
     u32 R;          // ray slots (threads of init)
     WfCtl *ctl;
-    u32 *pix, *out_off;
-    double *dir;    // [3][R]
-    double *dda_t;  // [5][R]: t_cur, t_exit, tmax x/y/z
-    int *dda_i;     // [3][R]
-    u8 *flags;      // bit 0 walk alive, bit 1 big window seen this iteration
-    double *acc;    // [4][R]
-    unsigned long long *tests, *over, *seen_bloom, *sph_bloom;
-    u32 *n_seen, *n_sph, *ovf, *head, *nwin;
+    WfRayWalk *rw;  // [R]
+    WfRayPix *rp;   // [R]
+    u32 *head;      // [R] overflow hit list
     u32 *tab_key, *tab_mask;   // [kInline][R]
     float *tab_sph;            // [3][kInline][R]
     u32 *pool_key, *pool_mask; // [pool_cap][LVX_MAX_SEEN - kInline]
@@ -214,30 +243,28 @@ __device__ __forceinline__ void write_pixel(const WfArgs &A, u32 o, double a0, d
     reinterpret_cast<float4 *>(A.img)[o] = outp;
 }
 
-__device__ __forceinline__ void dda_store(const WfArgs &A, u32 s, const LvxDda &d) {
-    const size_t R = A.R;
-    A.dda_t[s] = d.t_cur;
-    A.dda_t[R + s] = d.t_exit;
-    A.dda_t[2 * R + s] = d.tmax_x;
-    A.dda_t[3 * R + s] = d.tmax_y;
-    A.dda_t[4 * R + s] = d.tmax_z;
-    A.dda_i[s] = d.ix;
-    A.dda_i[R + s] = d.iy;
-    A.dda_i[2 * R + s] = d.iz;
+__device__ __forceinline__ void dda_store(WfRayWalk &r, const LvxDda &d) {
+    r.t_cur = d.t_cur;
+    r.t_exit = d.t_exit;
+    r.tmax_x = d.tmax_x;
+    r.tmax_y = d.tmax_y;
+    r.tmax_z = d.tmax_z;
+    r.ix = d.ix;
+    r.iy = d.iy;
+    r.iz = d.iz;
 }
 
 // Rebuild the walker from its stored progress (the constants are functions of the ray).
-__device__ __forceinline__ void dda_load(const WfArgs &A, u32 s, double dx, double dy, double dz,
-                                         int pad, LvxDda &d) {
-    const size_t R = A.R;
-    d.t_cur = A.dda_t[s];
-    d.t_exit = A.dda_t[R + s];
-    d.tmax_x = A.dda_t[2 * R + s];
-    d.tmax_y = A.dda_t[3 * R + s];
-    d.tmax_z = A.dda_t[4 * R + s];
-    d.ix = A.dda_i[s];
-    d.iy = A.dda_i[R + s];
-    d.iz = A.dda_i[2 * R + s];
+__device__ __forceinline__ void dda_load(const WfArgs &A, const WfRayWalk &r, int pad, LvxDda &d) {
+    const double dx = r.dir[0], dy = r.dir[1], dz = r.dir[2];
+    d.t_cur = r.t_cur;
+    d.t_exit = r.t_exit;
+    d.tmax_x = r.tmax_x;
+    d.tmax_y = r.tmax_y;
+    d.tmax_z = r.tmax_z;
+    d.ix = r.ix;
+    d.iy = r.iy;
+    d.iz = r.iz;
     d.step_x = dx > 0.0 ? 1 : (dx < 0.0 ? -1 : 0);
     d.step_y = dy > 0.0 ? 1 : (dy < 0.0 ? -1 : 0);
     d.step_z = dz > 0.0 ? 1 : (dz < 0.0 ? -1 : 0);
@@ -290,28 +317,28 @@ __global__ void __launch_bounds__(kThreadsWf) wf_init_kernel(const WfArgs A) {
             int wx, wy, wz;
             double t0, t1;
             while (full.next(wx, wy, wz, t0, t1)) steps += 1;
-            const size_t R = A.R;
-            A.pix[slot] = (u32)x | ((u32)y << 16);
-            A.out_off[slot] = (u32)o;
-            A.dir[slot] = ddx;
-            A.dir[R + slot] = ddy;
-            A.dir[2 * R + slot] = ddz;
-            dda_store(A, slot, dda);
-            A.flags[slot] = 1;
-            A.acc[slot] = 0.0;
-            A.acc[R + slot] = 0.0;
-            A.acc[2 * R + slot] = 0.0;
-            A.acc[3 * R + slot] = 0.0;
-            A.tests[slot] = 0;
-            A.over[slot] = 0;
-            A.seen_bloom[slot] = 0;
-            A.sph_bloom[slot] = 0;
-            A.n_seen[slot] = 0;
-            A.n_sph[slot] = 0;
-            A.ovf[slot] = kNil;
+            WfRayWalk rw;
+            rw.dir[0] = ddx;
+            rw.dir[1] = ddy;
+            rw.dir[2] = ddz;
+            dda_store(rw, dda);
+            rw.flags = 1;
+            rw.tests = 0;
+            rw.nwin = 0;
+            rw.pad = 0;
+            A.rw[slot] = rw;
+            WfRayPix rp;
+            rp.acc[0] = rp.acc[1] = rp.acc[2] = rp.acc[3] = 0.0;
+            rp.seen_bloom = rp.sph_bloom = 0;
+            rp.over = 0;
+            rp.n_seen = rp.n_sph = 0;
+            rp.ovf = kNil;
+            rp.pix = (u32)x | ((u32)y << 16);
+            rp.out_off = (u32)o;
+            rp.pad = 0;
+            A.rp[slot] = rp;
             A.head[slot] = kNil;
             A.hcnt[slot] = 0;
-            A.nwin[slot] = 0;
             live = true;
         } else {
             write_pixel(A, (u32)o, 0.0, 0.0, 0.0, 0.0);
@@ -347,7 +374,10 @@ __device__ __forceinline__ u32 shift_mask(u32 e, int dx, int dy, int dz) {
     return e;
 }
 
-__global__ void __launch_bounds__(kThreadsWf) wf_walk_kernel(const WfArgs A, int par) {
+#ifndef LVX_WF_WALK_MINB
+#define LVX_WF_WALK_MINB 4
+#endif
+__global__ void __launch_bounds__(kThreadsWf, LVX_WF_WALK_MINB) wf_walk_kernel(const WfArgs A, int par) {
     const u32 n_live = A.ctl->n_live[par];
     const u32 wn = A.ctl->wn;
     const u32 budget = A.ctl->budget;
@@ -361,10 +391,11 @@ __global__ void __launch_bounds__(kThreadsWf) wf_walk_kernel(const WfArgs A, int
     const size_t R = A.R;
     for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n_live; i += gridDim.x * blockDim.x) {
         const u32 slot = A.live[par][i];
-        const double ddx = A.dir[slot], ddy = A.dir[R + slot], ddz = A.dir[2 * R + slot];
+        WfRayWalk rw = A.rw[slot];
+        const double ddx = rw.dir[0], ddy = rw.dir[1], ddz = rw.dir[2];
         LvxDda dda;
-        dda_load(A, slot, ddx, ddy, ddz, neighbor ? 1 : 0, dda);
-        unsigned long long tests = A.tests[slot];
+        dda_load(A, rw, neighbor ? 1 : 0, dda);
+        unsigned long long tests = rw.tests;
         u32 kw = 0, csum = 0;
         bool big_any = false;
         const double span0 = dda.t_cur;
@@ -440,10 +471,11 @@ __global__ void __launch_bounds__(kThreadsWf) wf_walk_kernel(const WfArgs A, int
                 }
             }
         }
-        dda_store(A, slot, dda);
-        A.tests[slot] = tests;
-        A.nwin[slot] = kw;
-        A.flags[slot] = (u8)((dda.alive ? 1 : 0) | (big_any ? 2 : 0));
+        dda_store(rw, dda);
+        rw.tests = tests;
+        rw.nwin = kw;
+        rw.flags = (dda.alive ? 1u : 0u) | (big_any ? 2u : 0u);
+        A.rw[slot] = rw;
         A.fdir[i] = (float)ddx;
         A.fdir[R + i] = (float)ddy;
         A.fdir[2 * R + i] = (float)ddz;
@@ -569,8 +601,11 @@ __device__ __forceinline__ void wf_shade(const WfArgs &A, double ox, double oy, 
 // ---------------------------------------------------------------------------------------
 // exact: one thread per surviving primitive (KIND 0: tubes, 1: joint spheres)
 // ---------------------------------------------------------------------------------------
+#ifndef LVX_WF_EXACT_MINB
+#define LVX_WF_EXACT_MINB 4
+#endif
 template <int KIND>
-__global__ void __launch_bounds__(kThreadsWf) wf_exact_kernel(const WfArgs A, int par) {
+__global__ void __launch_bounds__(kThreadsWf, LVX_WF_EXACT_MINB) wf_exact_kernel(const WfArgs A, int par) {
     __shared__ QueueView V;
     queue_view_load(V, KIND == 0 ? A.ctl->tube_cnt : A.ctl->sph_cnt, A.capq_surv);
     const u32 total = V.pre[kNQ];
@@ -585,11 +620,12 @@ __global__ void __launch_bounds__(kThreadsWf) wf_exact_kernel(const WfArgs A, in
         const u32 seg = c.seg & 0x7FFFFFFFu;
         const u32 place = A.item_place[c.item];
         const u32 slot = A.live[par][place];
-        const double rdx = A.dir[slot], rdy = A.dir[R + slot], rdz = A.dir[2 * R + slot];
+        const double rdx = A.rw[slot].dir[0], rdy = A.rw[slot].dir[1], rdz = A.rw[slot].dir[2];
         const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + seg));
         LvxHit h;
         bool hit;
         u32 kind3;
+        float ccx = 0.0f, ccy = 0.0f, ccz = 0.0f;
         if (KIND == 0) {
             const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + seg) + 1);
             hit = lvx_tube_f32axis(ox, oy, oz, rdx, rdy, rdz, ra.x, ra.y, ra.z, rb.x, rb.y, rb.z, tube_r, h);
@@ -602,6 +638,9 @@ __global__ void __launch_bounds__(kThreadsWf) wf_exact_kernel(const WfArgs A, in
                 kind3 = 2;
             }
             hit = lvx_sphere<true>(ox, oy, oz, rdx, rdy, rdz, (double)cc.x, (double)cc.y, (double)cc.z, tube_r, h);
+            ccx = cc.x;
+            ccy = cc.y;
+            ccz = cc.z;
         }
         // ownership (:838, :858, :878): a hit belongs to the window whose range holds its entry
         // parameter; the windows tile the walked range, so every hit entered inside the range
@@ -617,22 +656,25 @@ __global__ void __launch_bounds__(kThreadsWf) wf_exact_kernel(const WfArgs A, in
         const u32 attr = rmeta & 0xFFu, lid = (rmeta >> 8) & 31u;
         double scale, alpha;
         wf_shade(A, ox, oy, oz, rdx, rdy, rdz, h, attr, scale, alpha);
+        const u32 lin = A.item_lin[c.item];
+        const u32 rank = seg - __ldg(A.offsets + lin);  // index in the voxel's list
         WfHit rec;
         rec.t_in = h.t_in;
+        rec.key2 = ((unsigned long long)lin << 24) | ((unsigned long long)lid << 19) | (kind3 ? 1ull << 18 : 0ull) |
+                   ((unsigned long long)(rank & 255u) << 10) | ((unsigned long long)kind3 << 8) | attr;
         rec.scale = scale;
         rec.alpha = alpha;
-        rec.lin = A.item_lin[c.item];
-        rec.seg = seg;
-        rec.meta = kind3 | (lid << 2) | (attr << 8);
-        rec.pad[0] = rec.pad[1] = 0;
-        rec.next = kNil;
+        rec.cx = ccx;
+        rec.cy = ccy;
+        rec.cz = ccz;
+        rec.next = kNil & ~kDropped;
         const u32 j = atomicAdd(&A.hcnt[slot], 1u);
         if (j < (u32)kHitSlots) {
             A.hit_slot[(size_t)j * R + place] = rec;
         } else {
             const u32 e = queue_alloc(A.ctl->hit_cnt, q, A.capq_hit, 1u, &A.ctl->err, 4u);
             if (e == kNil) continue;
-            rec.next = atomicExch(&A.head[slot], e);
+            rec.next = atomicExch(&A.head[slot], e) & ~kDropped;
             A.hit[e] = rec;
         }
     }
@@ -643,17 +685,9 @@ __global__ void __launch_bounds__(kThreadsWf) wf_exact_kernel(const WfArgs A, in
 // ---------------------------------------------------------------------------------------
 
 // total order of the reference: _hit_before (_kernels.py:261-270) = (t_in, home voxel, lid,
-// kind), remaining ties in gather order = (segment, primitive)
-__device__ __forceinline__ bool wf_key_before(double ta, u32 la, u32 sa, u32 ma, double tb, u32 lb,
-                                              u32 sb, u32 mb) {
-    if (ta != tb) return ta < tb;
-    if (la != lb) return la < lb;
-    const u32 lida = (ma >> 2) & 31u, lidb = (mb >> 2) & 31u;
-    if (lida != lidb) return lida < lidb;
-    const u32 ka = (ma & 3u) ? 1u : 0u, kb = (mb & 3u) ? 1u : 0u;
-    if (ka != kb) return ka < kb;
-    if (sa != sb) return sa < sb;
-    return (ma & 3u) < (mb & 3u);
+// kind), remaining ties in gather order = (index in voxel, primitive): (t_in, key2)
+__device__ __forceinline__ bool wf_before(double ta, unsigned long long ka, double tb, unsigned long long kb) {
+    return ta < tb || (ta == tb && (ka >> 8) < (kb >> 8));
 }
 
 struct WfTables {
@@ -762,8 +796,8 @@ struct WfRayHits {
             if (ref + 1 < nslot) return ref + 1;
             return head == kNil ? kNil : head + kHitSlots;
         }
-        const u32 e = A.hit[ref - kHitSlots].next;
-        return e == kNil ? kNil : e + kHitSlots;
+        const u32 e = A.hit[ref - kHitSlots].next & ~kDropped;
+        return e == (kNil & ~kDropped) ? kNil : e + kHitSlots;
     }
 };
 
@@ -785,22 +819,17 @@ __device__ __forceinline__ u32 wf_find_window(const WfWindow *w, u32 nw, double 
 __device__ void wf_apply_window_cap(const WfArgs &A, const WfRayHits &H, const WfWindow *w, u32 nw, u32 w0) {
     for (u32 a = H.first(); a != kNil; a = H.next(a)) {
         WfHit *ha = H.at(a);
-        ha->pad[0] = wf_find_window(w, nw, ha->t_in);
-    }
-    for (u32 a = H.first(); a != kNil; a = H.next(a)) {
-        WfHit *ha = H.at(a);
-        const u32 k = ha->pad[0];
+        const u32 k = wf_find_window(w, nw, ha->t_in);
         if (!(w[k].tests & kBigBit)) continue;
-        const u32 sa = ha->seg, ka = ha->meta & 3u;
+        const unsigned long long ga = hit_gather(ha->key2);
         u32 rank = 0;
         for (u32 b = H.first(); b != kNil; b = H.next(b)) {
             const WfHit *hb = H.at(b);
-            if (hb->pad[0] != k) continue;
-            const u32 sb = hb->seg, kb = hb->meta & 3u;
-            if (sb < sa || (sb == sa && kb < ka)) rank += 1;
+            if (wf_find_window(w, nw, hb->t_in) != k) continue;
+            if (hit_gather(hb->key2) < ga) rank += 1;
         }
         if (rank >= (u32)LVX_MAX_WINDOW_HITS) {
-            ha->meta |= 1u << 16;
+            ha->next |= kDropped;
             A.win_over[w0 + k] += 1;
         }
     }
@@ -808,16 +837,8 @@ __device__ void wf_apply_window_cap(const WfArgs &A, const WfRayHits &H, const W
 
 __device__ __forceinline__ bool wf_composite_one(const WfArgs &A, WfTables &T, WfPixel &S, const WfHit &h,
                                                  double tau) {
-    const u32 kind3 = h.meta & 3u;
-    float cx = 0.0f, cy = 0.0f, cz = 0.0f;
-    if (kind3) {
-        const float4 c = __ldg(reinterpret_cast<const float4 *>(A.rec + h.seg) + (kind3 - 1));
-        cx = c.x;
-        cy = c.y;
-        cz = c.z;
-    }
-    wf_accumulate(A, T, S, h.scale, h.alpha, h.lin, (h.meta >> 2) & 31u, (h.meta >> 8) & 0xFFu, kind3 != 0, cx,
-                  cy, cz);
+    wf_accumulate(A, T, S, h.scale, h.alpha, hit_lin(h.key2), hit_lid(h.key2), hit_attr(h.key2),
+                  hit_kind3(h.key2) != 0, h.cx, h.cy, h.cz);
     return S.acc[3] >= tau;
 }
 
@@ -829,10 +850,11 @@ __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A
     for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n_live; i += gridDim.x * blockDim.x) {
         const u32 slot = A.live[par][i];
         const u32 nhit = A.hcnt[slot];
-        const u8 fl = A.flags[slot];
+        const u32 fl = A.rw[slot].flags;
         bool finished = !(fl & 1);  // the walk is over: this was the last batch
         bool terminated = false;
         unsigned long long tests = 0, over = 0;
+        WfRayPix rp;
         if (nhit) {
             A.hcnt[slot] = 0;
             WfRayHits H = {A, i, nhit < (u32)kHitSlots ? nhit : (u32)kHitSlots, kNil};
@@ -841,45 +863,42 @@ __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A
                 A.head[slot] = kNil;
             }
             const bool big = (fl & 2) != 0;
-            const u32 w0 = i * wn, nw = A.nwin[slot];
+            const u32 w0 = i * wn, nw = A.rw[slot].nwin;
             const WfWindow *wins = A.win + w0;
             if (big) wf_apply_window_cap(A, H, wins, nw, w0);
             WfPixel S;
-            S.acc[0] = A.acc[slot];
-            S.acc[1] = A.acc[R + slot];
-            S.acc[2] = A.acc[2 * R + slot];
-            S.acc[3] = A.acc[3 * R + slot];
-            S.n_seen = A.n_seen[slot];
-            S.n_sph = A.n_sph[slot];
-            S.seen_bloom = A.seen_bloom[slot];
-            S.sph_bloom = A.sph_bloom[slot];
-            WfTables T = {A, slot, A.ovf[slot]};
+            rp = A.rp[slot];
+            S.acc[0] = rp.acc[0];
+            S.acc[1] = rp.acc[1];
+            S.acc[2] = rp.acc[2];
+            S.acc[3] = rp.acc[3];
+            S.n_seen = rp.n_seen;
+            S.n_sph = rp.n_sph;
+            S.seen_bloom = rp.seen_bloom;
+            S.sph_bloom = rp.sph_bloom;
+            WfTables T = {A, slot, rp.ovf};
             double term_t = 0.0;
             if (nhit <= (u32)kSortCap) {
-                // gather + order (insertion sort on t_in; full key only on ties)
+                // gather the keys, order them locally (insertion sort on (t_in, key2))
                 double s_t[kSortCap];
+                unsigned long long s_k[kSortCap];
                 u32 s_ref[kSortCap];
                 int n = 0;
                 for (u32 ref = H.first(); ref != kNil; ref = H.next(ref)) {
                     const WfHit *hp = H.at(ref);
-                    if (hp->meta & (1u << 16)) continue;  // dropped by the window cap
-                    const double t = hp->t_in;
+                    if (big && (hp->next & kDropped)) continue;  // dropped by the window cap
+                    const double2 v = *reinterpret_cast<const double2 *>(hp);
+                    const double t = v.x;
+                    const unsigned long long k2 = (unsigned long long)__double_as_longlong(v.y);
                     int pos = n++;
-                    while (pos > 0) {
-                        bool before;
-                        if (t != s_t[pos - 1]) {
-                            before = t < s_t[pos - 1];
-                        } else {
-                            const WfHit *ho = H.at(s_ref[pos - 1]);
-                            before = wf_key_before(t, hp->lin, hp->seg, hp->meta, s_t[pos - 1], ho->lin, ho->seg,
-                                                   ho->meta);
-                        }
-                        if (!before) break;
+                    while (pos > 0 && wf_before(t, k2, s_t[pos - 1], s_k[pos - 1])) {
                         s_t[pos] = s_t[pos - 1];
+                        s_k[pos] = s_k[pos - 1];
                         s_ref[pos] = s_ref[pos - 1];
                         --pos;
                     }
                     s_t[pos] = t;
+                    s_k[pos] = k2;
                     s_ref[pos] = ref;
                 }
                 for (int j = 0; j < n; ++j) {
@@ -895,24 +914,21 @@ __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A
                 // repeatedly take the smallest key after the last composited one
                 bool have_last = false;
                 double lt = 0.0;
-                u32 ll = 0, ls = 0, lm = 0;
+                unsigned long long lk = 0;
                 for (;;) {
                     u32 best = kNil;
                     double bt = 0.0;
-                    u32 bl = 0, bs = 0, bm = 0;
+                    unsigned long long bk = 0;
                     for (u32 ref = H.first(); ref != kNil; ref = H.next(ref)) {
                         const WfHit *hp = H.at(ref);
-                        const u32 m = hp->meta;
-                        if (m & (1u << 16)) continue;
+                        if (hp->next & kDropped) continue;
                         const double t = hp->t_in;
-                        const u32 l = hp->lin, sg = hp->seg;
-                        if (have_last && !wf_key_before(lt, ll, ls, lm, t, l, sg, m)) continue;
-                        if (best == kNil || wf_key_before(t, l, sg, m, bt, bl, bs, bm)) {
+                        const unsigned long long k2 = hp->key2;
+                        if (have_last && !wf_before(lt, lk, t, k2)) continue;
+                        if (best == kNil || wf_before(t, k2, bt, bk)) {
                             best = ref;
                             bt = t;
-                            bl = l;
-                            bs = sg;
-                            bm = m;
+                            bk = k2;
                         }
                     }
                     if (best == kNil) break;
@@ -924,20 +940,18 @@ __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A
                     }
                     have_last = true;
                     lt = bt;
-                    ll = bl;
-                    ls = bs;
-                    lm = bm;
+                    lk = bk;
                 }
             }
-            A.acc[slot] = S.acc[0];
-            A.acc[R + slot] = S.acc[1];
-            A.acc[2 * R + slot] = S.acc[2];
-            A.acc[3 * R + slot] = S.acc[3];
-            A.n_seen[slot] = S.n_seen;
-            A.n_sph[slot] = S.n_sph;
-            A.seen_bloom[slot] = S.seen_bloom;
-            A.sph_bloom[slot] = S.sph_bloom;
-            A.ovf[slot] = T.ovf;
+            rp.acc[0] = S.acc[0];
+            rp.acc[1] = S.acc[1];
+            rp.acc[2] = S.acc[2];
+            rp.acc[3] = S.acc[3];
+            rp.n_seen = S.n_seen;
+            rp.n_sph = S.n_sph;
+            rp.seen_bloom = S.seen_bloom;
+            rp.sph_bloom = S.sph_bloom;
+            rp.ovf = T.ovf;
             const u32 term_k = terminated ? wf_find_window(wins, nw, term_t) : 0u;
             if (big) {
                 // window_overflow of the windows gathered up to (and including) the last one used
@@ -946,18 +960,21 @@ __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A
                     if (wins[k].tests & kBigBit) ov += A.win_over[w0 + k];
                     if (terminated && k == term_k) break;
                 }
-                A.over[slot] += ov;
+                rp.over += ov;
             }
             if (terminated) {
                 tests = wins[term_k].tests & ~kBigBit;
                 finished = true;
             }
+            if (!finished) A.rp[slot] = rp;
+        } else if (finished) {
+            rp = A.rp[slot];
         }
         if (finished) {
-            if (!terminated) tests = A.tests[slot];
-            over = A.over[slot];
-            write_pixel(A, A.out_off[slot], A.acc[slot], A.acc[R + slot], A.acc[2 * R + slot], A.acc[3 * R + slot]);
-            const u32 y = A.pix[slot] >> 16;
+            if (!terminated) tests = A.rw[slot].tests;
+            over = rp.over;
+            write_pixel(A, rp.out_off, rp.acc[0], rp.acc[1], rp.acc[2], rp.acc[3]);
+            const u32 y = rp.pix >> 16;
             if (tests) atomicAdd(A.row_stats + 3 * (i64)y + 1, tests);
             if (over) atomicAdd(A.row_stats + 3 * (i64)y + 2, over);
         } else {
@@ -1016,8 +1033,7 @@ __global__ void wf_begin_kernel(const WfArgs A) {
 // scratch layout ------------------------------------------------------------------------
 struct WfLayout {
     size_t total;
-    size_t ctl, pix, out_off, dir, dda_t, dda_i, flags, acc, tests, over, seen_bloom, sph_bloom, n_seen,
-        n_sph, ovf, head, nwin, tab_key, tab_mask, tab_sph, pool_key, pool_mask, pool_sph, live0, live1, win,
+    size_t ctl, rw, rp, head, tab_key, tab_mask, tab_sph, pool_key, pool_mask, pool_sph, live0, live1, win,
         win_over, item_place, item_lin, item_q, item_t, fdir, span, tube, sph, hit, hit_slot, hcnt;
     u32 R, pool_cap, cap_win, capq_item, capq_surv, capq_hit;
 };
@@ -1041,22 +1057,9 @@ WfLayout wf_layout(i64 R, double scale) {
     size_t c = 0;
     const size_t r = (size_t)R, po = (size_t)L.pool_cap * (LVX_MAX_SEEN - kInline);
     L.ctl = take(c, sizeof(WfCtl));
-    L.pix = take(c, r * 4);
-    L.out_off = take(c, r * 4);
-    L.dir = take(c, r * 24);
-    L.dda_t = take(c, r * 40);
-    L.dda_i = take(c, r * 12);
-    L.flags = take(c, r);
-    L.acc = take(c, r * 32);
-    L.tests = take(c, r * 8);
-    L.over = take(c, r * 8);
-    L.seen_bloom = take(c, r * 8);
-    L.sph_bloom = take(c, r * 8);
-    L.n_seen = take(c, r * 4);
-    L.n_sph = take(c, r * 4);
-    L.ovf = take(c, r * 4);
+    L.rw = take(c, r * sizeof(WfRayWalk));
+    L.rp = take(c, r * sizeof(WfRayPix));
     L.head = take(c, r * 4);
-    L.nwin = take(c, r * 4);
     L.tab_key = take(c, r * 4 * kInline);
     L.tab_mask = take(c, r * 4 * kInline);
     L.tab_sph = take(c, r * 12 * kInline);
@@ -1174,22 +1177,9 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     char *base = (char *)scratch_d;
     A.R = L.R;
     A.ctl = (WfCtl *)(base + L.ctl);
-    A.pix = (u32 *)(base + L.pix);
-    A.out_off = (u32 *)(base + L.out_off);
-    A.dir = (double *)(base + L.dir);
-    A.dda_t = (double *)(base + L.dda_t);
-    A.dda_i = (int *)(base + L.dda_i);
-    A.flags = (u8 *)(base + L.flags);
-    A.acc = (double *)(base + L.acc);
-    A.tests = (unsigned long long *)(base + L.tests);
-    A.over = (unsigned long long *)(base + L.over);
-    A.seen_bloom = (unsigned long long *)(base + L.seen_bloom);
-    A.sph_bloom = (unsigned long long *)(base + L.sph_bloom);
-    A.n_seen = (u32 *)(base + L.n_seen);
-    A.n_sph = (u32 *)(base + L.n_sph);
-    A.ovf = (u32 *)(base + L.ovf);
+    A.rw = (WfRayWalk *)(base + L.rw);
+    A.rp = (WfRayPix *)(base + L.rp);
     A.head = (u32 *)(base + L.head);
-    A.nwin = (u32 *)(base + L.nwin);
     A.tab_key = (u32 *)(base + L.tab_key);
     A.tab_mask = (u32 *)(base + L.tab_mask);
     A.tab_sph = (float *)(base + L.tab_sph);
