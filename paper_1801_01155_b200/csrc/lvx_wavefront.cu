@@ -170,9 +170,8 @@ struct WfArgs {
     int wn_sched, cand_budget, grow_from;
 };
 
-__device__ __forceinline__ int warp_queue() {
-    return (int)(((blockIdx.x * (blockDim.x >> 5)) + (threadIdx.x >> 5)) & (kNQ - 1));
-}
+// sub-queue of the warp that works on flat index f (warp-uniform: f is lane + a multiple of 32)
+__device__ __forceinline__ int warp_queue(u32 f) { return (int)((f >> 5) & (kNQ - 1)); }
 
 // Allocate `n` consecutive entries of sub-queue q for this thread (aggregated over the
 // currently converged lanes).  Returns the global index or kNil when the queue is full.
@@ -193,7 +192,7 @@ __device__ __forceinline__ u32 queue_alloc(u32 *cnt, int q, u32 capq, u32 n, u32
 struct QueueView {
     u32 pre[kNQ + 1];
 };
-__device__ __forceinline__ void queue_view_load(QueueView &v, const u32 *cnt, u32 capq) {
+__device__ __forceinline__ void queue_view_load(QueueView &v, const u32 *cnt, u32 capq, u32 err) {
     // (called by all threads of the block; v lives in shared memory)
     if (threadIdx.x == 0) {
         u32 run = 0;
@@ -202,7 +201,9 @@ __device__ __forceinline__ void queue_view_load(QueueView &v, const u32 *cnt, u3
             const u32 c = cnt[q];
             run += c < capq ? c : capq;
         }
-        v.pre[kNQ] = run;
+        // an overflowed queue holds unwritten entries: the frame is void (the host retries
+        // with larger queues), nothing downstream may touch it
+        v.pre[kNQ] = err ? 0u : run;
     }
     __syncthreads();
 }
@@ -378,7 +379,7 @@ __device__ __forceinline__ u32 shift_mask(u32 e, int dx, int dy, int dz) {
 #define LVX_WF_WALK_MINB 4
 #endif
 __global__ void __launch_bounds__(kThreadsWf, LVX_WF_WALK_MINB) wf_walk_kernel(const WfArgs A, int par) {
-    const u32 n_live = A.ctl->n_live[par];
+    const u32 n_live = A.ctl->err ? 0u : A.ctl->n_live[par];
     const u32 wn = A.ctl->wn;
     const u32 budget = A.ctl->budget;
     const lvx_params &p = A.p;
@@ -387,9 +388,9 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_WALK_MINB) wf_walk_kernel(c
     const u32 tmul = p.joints != 0 ? 3u : 1u;
     const double cull = p.tube_r + kCullMarginWf;
     const double ox = A.cam.o[0], oy = A.cam.o[1], oz = A.cam.o[2];
-    const int q = warp_queue();
     const size_t R = A.R;
     for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n_live; i += gridDim.x * blockDim.x) {
+        const int q = warp_queue(i);
         const u32 slot = A.live[par][i];
         WfRayWalk rw = A.rw[slot];
         const double ddx = rw.dir[0], ddy = rw.dir[1], ddz = rw.dir[2];
@@ -500,13 +501,13 @@ __device__ __forceinline__ bool wf_near_line(float cx, float cy, float cz, float
 // ---------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreadsWf) wf_cand_kernel(const WfArgs A) {
     __shared__ QueueView V;
-    queue_view_load(V, A.ctl->item_cnt, A.capq_item);
+    queue_view_load(V, A.ctl->item_cnt, A.capq_item, A.ctl->err);
     const u32 total = V.pre[kNQ];
     const bool joints = A.p.joints != 0;
     const float reach_pt = (float)A.p.tube_r + kRejectMarginWf;
-    const int q = warp_queue();
     const size_t R = A.R;
     for (u32 f = blockIdx.x * blockDim.x + threadIdx.x; f < total; f += gridDim.x * blockDim.x) {
+        const int q = warp_queue(f);
         const u32 it = queue_view_index(V, f, A.capq_item);
         const u32 place = A.item_place[it], lin = A.item_lin[it];
         const float4 q0 = A.item_q[it];
@@ -607,15 +608,15 @@ __device__ __forceinline__ void wf_shade(const WfArgs &A, double ox, double oy, 
 template <int KIND>
 __global__ void __launch_bounds__(kThreadsWf, LVX_WF_EXACT_MINB) wf_exact_kernel(const WfArgs A, int par) {
     __shared__ QueueView V;
-    queue_view_load(V, KIND == 0 ? A.ctl->tube_cnt : A.ctl->sph_cnt, A.capq_surv);
+    queue_view_load(V, KIND == 0 ? A.ctl->tube_cnt : A.ctl->sph_cnt, A.capq_surv, A.ctl->err);
     const u32 total = V.pre[kNQ];
     const double ox = A.cam.o[0], oy = A.cam.o[1], oz = A.cam.o[2];
     const double tube_r = A.p.tube_r;
-    const int q = warp_queue();
     const size_t R = A.R;
     const WfEntry *queue = KIND == 0 ? A.tube : A.sph;
     const bool neighbor = A.p.neighbor != 0;
     for (u32 f = blockIdx.x * blockDim.x + threadIdx.x; f < total; f += gridDim.x * blockDim.x) {
+        const int q = warp_queue(f);
         const WfEntry c = queue[queue_view_index(V, f, A.capq_surv)];
         const u32 seg = c.seg & 0x7FFFFFFFu;
         const u32 place = A.item_place[c.item];
@@ -843,7 +844,7 @@ __device__ __forceinline__ bool wf_composite_one(const WfArgs &A, WfTables &T, W
 }
 
 __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A, int par) {
-    const u32 n_live = A.ctl->n_live[par];
+    const u32 n_live = A.ctl->err ? 0u : A.ctl->n_live[par];
     const u32 wn = A.ctl->wn;
     const size_t R = A.R;
     const double tau = A.p.tau;
@@ -1048,7 +1049,7 @@ WfLayout wf_layout(i64 R, double scale) {
     WfLayout L;
     memset(&L, 0, sizeof(L));
     L.R = (u32)R;
-    const double f = scale < 1.0 ? 1.0 : scale;
+    const double f = scale < 1.0 / 64.0 ? 1.0 / 64.0 : scale;  // (< 1 only to exercise the overflow path)
     L.pool_cap = (u32)(R / 16 * f) + 1024;
     L.cap_win = (u32)fmin(4.0e9, (double)R * 8.0);
     L.capq_item = (u32)fmin(4.0e9 / kNQ, ((double)R * 24.0 * f + 65536.0) / kNQ);
@@ -1226,11 +1227,24 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
         const int burst = it == 0 ? 6 : 3;
         for (int b = 0; b < burst; ++b, ++it) {
             const int par = it & 1;
+#define WF_DEBUG_SYNC(name)                                                                   \
+    if (debug) {                                                                              \
+        cudaError_t e_ = cudaStreamSynchronize(st);                                           \
+        if (e_ != cudaSuccess) {                                                              \
+            lvx_set_error("wavefront iteration %d: %s failed: %s", it, name, cudaGetErrorString(e_)); \
+            return LVX_E_CUDA;                                                                \
+        }                                                                                     \
+    }
             wf_walk_kernel<<<grid_rays, kThreadsWf, 0, st>>>(A, par);
+            WF_DEBUG_SYNC("walk");
             wf_cand_kernel<<<grid_q, kThreadsWf, 0, st>>>(A);
+            WF_DEBUG_SYNC("candidates");
             wf_exact_kernel<0><<<grid_q, kThreadsWf, 0, st>>>(A, par);
+            WF_DEBUG_SYNC("exact<tube>");
             if (params->joints) wf_exact_kernel<1><<<grid_q, kThreadsWf, 0, st>>>(A, par);
+            WF_DEBUG_SYNC("exact<sphere>");
             wf_composite_kernel<<<grid_rays, kThreadsWf, 0, st>>>(A, par);
+            WF_DEBUG_SYNC("composite");
             if (debug) {
                 WfCtl c;
                 cudaMemcpyAsync(&c, A.ctl, sizeof(c), cudaMemcpyDeviceToHost, st);

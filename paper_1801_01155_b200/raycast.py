@@ -332,9 +332,14 @@ def check_modes(params: RenderParams, model: VoxelModel, octree):
 
 
 def default_engine() -> str:
-    """Frame engine used when none is named: LVX_ENGINE=tile|wavefront (developer switch)."""
+    """Frame engine used when none is named: LVX_ENGINE=auto|tile|wavefront.
+
+    Both engines produce the same bytes.  "auto" picks the faster one for the mode: the
+    wavefront engine (streaming kernels over device queues) in neighbour mode, the tile
+    engine (one monolithic kernel) in own-voxel mode, where there is too little work per
+    window for the queues to pay off."""
     import os
-    return os.environ.get("LVX_ENGINE", "wavefront")
+    return os.environ.get("LVX_ENGINE", "auto")
 
 
 _WF_SCRATCH = {}
@@ -366,6 +371,8 @@ class FramePlan:
         from .illumination import fibonacci_dirs_device
         check_modes(params, model, octree)
         self.engine = engine or default_engine()
+        if self.engine == "auto":
+            self.engine = "wavefront" if neighbor else "tile"
         if self.engine not in ("wavefront", "tile"):
             raise ValueError(f"unknown frame engine {self.engine!r}")
         self._scale = 1.0

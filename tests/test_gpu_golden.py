@@ -81,8 +81,11 @@ def gpu_render(lv, name, **extra):
     return g, fr
 
 
+@pytest.mark.parametrize("engine", ["tile", "wavefront"])
 @pytest.mark.parametrize("name", RENDER_CASES)
-def test_render_matches_reference(lv, name):
+def test_render_matches_reference(lv, name, engine, monkeypatch):
+    # both frame engines (csrc/lvx_render.cu, csrc/lvx_wavefront.cu) against every fixture
+    monkeypatch.setenv("LVX_ENGINE", engine)
     g, fr = gpu_render(lv, name)
     assert fr.image.shape == g["image"].shape and fr.image.dtype == np.float32
     err = np.abs(fr.image.astype(np.float64) - g["image"].astype(np.float64))

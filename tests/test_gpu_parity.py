@@ -78,7 +78,9 @@ def test_c1_lod_and_ao(lv, oracle, c1):
     dict(neighbor_mode="off", base_opacity=0.25, ao_mode="density-rays"),
     dict(neighbor_mode="on", base_opacity=0.05, tau=1.0),
 ], ids=lambda kw: "-".join(f"{k}={v}" for k, v in kw.items() if k != "light_dir"))
-def test_c1_frames(lv, oracle, c1, kw):
+@pytest.mark.parametrize("engine", ["tile", "wavefront"])
+def test_c1_frames(lv, oracle, c1, kw, engine, monkeypatch):
+    monkeypatch.setenv("LVX_ENGINE", engine)
     dims, m, ref = c1
     oc = lv.build_lod(m)
     levels = oracle.build_octree(oracle.compute_density_level0(ref))
@@ -211,6 +213,34 @@ def test_model_from_host_arrays_renders_identically(lv, synth):
     host.seg_attr = np.zeros_like(host.seg_attr)
     c = lv.render_frame(cam, host, None, None, p)
     assert not np.array_equal(c.image, b.image)
+
+
+def test_frame_engines_agree_and_queue_overflow_is_retried(lv, synth):
+    """The tile kernel and the wavefront engine produce the same bytes; a wavefront run whose
+    queues are too small reports it (LVX_E_RANGE) and is repeated with larger ones."""
+    import torch
+    from paper_1801_01155_b200.raycast import FramePlan
+    dims = (24, 24, 24)
+    m = lv.build_voxel_model(lv.CurveSet.from_flat(*synth.turbulence(1500, 50, dims)), lv.GridSpec(dims))
+    oc = lv.build_lod(m)
+    cam = lv.default_camera(dims, 200, 120)
+    for kw in (dict(base_opacity=0.2, neighbor_mode="on"), dict(base_opacity=0.2, neighbor_mode="off"),
+               dict(base_opacity=0.03, tau=1.0, neighbor_mode="on", shadow_mode="cone", light_dir=(0.1, 0.5, 1.0))):
+        p = lv.RenderParams(**kw)
+        nb = 1 if kw["neighbor_mode"] == "on" else 0
+        out = {}
+        for engine, scale in (("tile", 1.0), ("wavefront", 1.0), ("wavefront-small", 1.0 / 64.0)):
+            plan = FramePlan(cam, m, oc, p, nb, engine=engine.split("-")[0])
+            plan._scale = scale
+            img = torch.empty((120, 200, 4), dtype=torch.float32, device="cuda")
+            st = torch.zeros((120, 3), dtype=torch.int64, device="cuda")
+            plan.launch(img, st)
+            torch.cuda.synchronize()
+            out[engine] = (img.cpu().numpy(), st.cpu().numpy(), plan._scale)
+        for engine in ("wavefront", "wavefront-small"):
+            assert np.array_equal(out["tile"][0], out[engine][0]), (kw, engine)
+            assert np.array_equal(out["tile"][1], out[engine][1]), (kw, engine)
+    assert out["wavefront-small"][2] > 1.0 / 64.0  # the low-opacity frame does not fit the tiny queues
 
 
 # --- error behaviour (SURVEY.md 8b) ------------------------------------------------------
