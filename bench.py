@@ -270,9 +270,15 @@ def run_ours(args, wl):
         full_d = torch.empty((H, W, 4), dtype=torch.float32, device="cuda") if rank == 0 else None
     stats_d = torch.zeros((H, 3), dtype=torch.int64, device="cuda")
 
+    L = _lib.lib()
+
+    def frame_launches():
+        """kernels of this repo launched by the last plan.launch()"""
+        return int(L.lvx_render_wf_last_launches(None)) if plan.engine == "wavefront" else 1
+
     def step():
         plan.launch(img_d, stats_d)
-        launches["n"] += 1
+        launches["n"] += frame_launches()
         if world > 1:
             parts = parallel.gather_tiles(img_d[:plan.n_my_tiles()], 0)
             if rank == 0:
@@ -294,7 +300,7 @@ def run_ours(args, wl):
             kern_ev[i][0].record()
             plan.launch(img_d, stats_d)
             kern_ev[i][1].record()
-            launches["n"] += 1
+            launches["n"] += frame_launches()
             if world > 1:
                 parts = parallel.gather_tiles(img_d[:plan.n_my_tiles()], 0)
                 if rank == 0:
@@ -351,17 +357,21 @@ def run_ours(args, wl):
     tot1 = st1.sum(0).tolist()
     requested = tot1[0] + 32 * (tot1[1] // (3 if params.joint_spheres else 1)) + 16 * W * H
     k1 = kern_ms if world == 1 else min(ev_ms(lambda: plan1.launch(img1, st1)) for _ in range(2))
-    roofline = {"bound": "hbm", "kernel": "render_kernel", "achieved": alg_bytes / k1 / 1e6, "peak": peak,
+    kname = "render_kernel" if plan.engine == "tile" else \
+        "wavefront frame: wf_init + N x (wf_walk, wf_cand, wf_exact<tube>, wf_exact<sphere>, wf_composite)"
+    roofline = {"bound": "hbm", "kernel": kname, "engine": plan.engine, "achieved": alg_bytes / k1 / 1e6, "peak": peak,
                 "unit": "GB/s", "frac": alg_bytes / k1 / 1e6 / peak, "traffic": None,
                 "peak_source": peak_src, "alg_bytes_per_launch": alg_bytes, "voxels_touched": n_vox,
                 "segments_touched": n_seg, "kernel_ms": k1, "requested_bytes": requested,
                 "requested_gbs": requested / k1 / 1e6,
                 "note": "unique bytes the reference's algorithm touches per frame (6 B/voxel header+occupancy, "
-                        "32 B/segment, 16 B/pixel out); the kernel is FP64-issue/latency bound, not HBM bound"}
+                        "32 B/segment, 16 B/pixel out); the frame is latency / L2-transaction bound, not HBM bound "
+                        "(see profiles/); kernel_ms is the CUDA-event time of the whole frame"}
     prof = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof):
         try:
-            roofline["traffic"] = json.load(open(prof)).get(args.workload, {}).get("render_kernel")
+            roofline["traffic"] = json.load(open(prof)).get(args.workload, {}).get(
+                "render_kernel" if plan.engine == "tile" else "wavefront_frame")
         except Exception:
             pass
 
@@ -386,7 +396,7 @@ def run_ours(args, wl):
                    "parallelism": "1 GPU" if world == 1 else f"{world} GPUs, interleaved {parallel.MG_TILE_W}x"
                                   f"{parallel.MG_TILE_H} screen tiles, NCCL gather to rank 0"},
         "frame_stats": {"voxel_steps": tot[0], "intersection_tests": tot[1], "window_overflow": tot[2]},
-        "kernel_ms": kern_ms,
+        "kernel_ms": kern_ms, "engine": plan.engine,
         "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "render_frame" if world == 1 else "render_frame_tiled"},
         "gpu_launches": gpu_launches,

@@ -262,6 +262,9 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
                   int64_t *row_stats_d, void *scratch_d, size_t scratch_bytes, double scale,
                   void *stream);
 
+/* Kernel launches (and walk/composite iterations) of this thread's last lvx_render_wf call. */
+int lvx_render_wf_last_launches(int *iterations);
+
 int lvx_render_footprint(const lvx_camera *cam, const lvx_model *model, const lvx_params *params,
                          const lvx_lod *lod, const lvx_tiling *tiling, float *img_d,
                          int64_t *row_stats_d, uint32_t *voxel_bits_d, void *stream);

@@ -59,7 +59,7 @@ SYMBOLS = [
     "lvx_mark_curve_starts", "lvx_voxelize_count", "lvx_scan_scratch_bytes", "lvx_voxel_scan",
     "lvx_voxelize_emit", "lvx_voxelize_compact", "lvx_raw_regroup", "lvx_scan_u16", "lvx_provenance",
     "lvx_build_seg_records", "lvx_density_l0", "lvx_octree_layout", "lvx_build_octree",
-    "lvx_occupancy_dilate", "lvx_neighbor_sums", "lvx_render_scratch_bytes", "lvx_render", "lvx_render_wf_scratch_bytes", "lvx_render_wf",
+    "lvx_occupancy_dilate", "lvx_neighbor_sums", "lvx_render_scratch_bytes", "lvx_render", "lvx_render_wf_scratch_bytes", "lvx_render_wf", "lvx_render_wf_last_launches",
     "lvx_render_footprint", "lvx_untile",
     "lvx_fibonacci_dirs", "lvx_ao_bake", "lvx_probe_dda", "lvx_probe_tube", "lvx_probe_sphere",
     "lvx_probe_trilinear", "lvx_probe_cone", "lvx_probe_ao_density",

@@ -1103,7 +1103,14 @@ int wf_check_tiling(const lvx_tiling *t) {
 
 }  // namespace
 
+static thread_local int g_last_launches = 0, g_last_iterations = 0;
+
 extern "C" {
+
+int lvx_render_wf_last_launches(int *iterations) {
+    if (iterations) *iterations = g_last_iterations;
+    return g_last_launches;
+}
 
 size_t lvx_render_wf_scratch_bytes(const lvx_camera *cam, const lvx_tiling *tiling, double scale) {
     if (!cam || !tiling || tiling->tile_w < 8 || tiling->tile_h < 4 || tiling->tile_step < 1) return 0;
@@ -1223,6 +1230,7 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     LVX_LAUNCH_CHECK();
     u32 host[4] = {0, 0, 0, 0};
     int it = 0;
+    g_last_launches = 2;
     for (;;) {
         const int burst = it == 0 ? 6 : 3;
         for (int b = 0; b < burst; ++b, ++it) {
@@ -1271,6 +1279,8 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
             lvx_set_error("wavefront queues overflowed (bits %u): retry with a larger scratch scale", host[1]);
             return LVX_E_RANGE;
         }
+        g_last_iterations = it;
+        g_last_launches = 2 + it * (params->joints ? 6 : 5);
         if (host[0] == 0) break;
         LVX_REQUIRE(it < 100000, "wavefront did not converge");
     }
