@@ -39,11 +39,11 @@ extern "C" {
 #define LVX_OPACITY_TRANSFER 1
 #define LVX_OPACITY_DISTANCE 2
 #define LVX_SHADOW_NONE 0
-#define LVX_SHADOW_HARD 1     /* not built (SURVEY 8f "next") -> LVX_E_INVALID */
+#define LVX_SHADOW_HARD 1     /* geometry shadow rays (needs the neighbour grids) */
 #define LVX_SHADOW_REPLINES 2 /* not built (SURVEY 8f "next") -> LVX_E_INVALID */
 #define LVX_SHADOW_CONE 3
 #define LVX_AO_NONE 0
-#define LVX_AO_HEMISPHERE 1 /* not built (SURVEY 8f "next") -> LVX_E_INVALID */
+#define LVX_AO_HEMISPHERE 1 /* geometry hemisphere rays (needs the neighbour grids + lattice) */
 #define LVX_AO_DENSITY 2
 #define LVX_AO_PRECOMPUTED 3
 
@@ -307,6 +307,20 @@ int lvx_probe_cone(const lvx_lod *lod, const double *pts_d, const double light[3
 int lvx_probe_ao_density(const lvx_lod *lod, const double *pts_d, const double *normals_d,
                          int32_t n_rays, double radius, double step, const double *dirs_d,
                          int64_t n, double *out_d, void *stream);
+
+/* Geometry secondary rays as point probes.
+ * lvx_probe_blocked: _kernels.geometry_ray_blocked (_kernels.py:450-495), the kernel behind
+ * illumination.hard_shadow (illumination.py:96-112): rays f64[n,6] = origin + unit direction,
+ * out[i] = 1 if a tube (or joint sphere) is entered at 1e-9 < t_in < max_t[i].
+ * lvx_probe_ao_hemisphere: _kernels.ao_hemisphere_point (_kernels.py:572-589), behind
+ * illumination.ao_hemisphere_geometry (illumination.py:158-173), jitter 0; dirs_d is the
+ * hemisphere lattice of lvx_fibonacci_dirs(n_rays, 1, 0).  The model needs counts, offsets,
+ * seg_rec and nmask. */
+int lvx_probe_blocked(const lvx_model *model, const double *rays_d, const double *max_t_d,
+                      double radius, int32_t joints, int64_t n, int32_t *out_d, void *stream);
+int lvx_probe_ao_hemisphere(const lvx_model *model, const double *pts_d, const double *normals_d,
+                            int32_t n_rays, double radius, const double *dirs_d, double tube_r,
+                            int64_t n, double *out_d, void *stream);
 
 #ifdef __cplusplus
 }

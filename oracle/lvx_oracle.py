@@ -311,6 +311,43 @@ def default_camera(dims, width=640, height=360):
                 width=width, height=height)
 
 
+def hard_shadow(point, light, model, radius=0.3, normal=None, joint_spheres=True) -> int:
+    """illumination.hard_shadow (illumination.py:96-112): 1 if the point sees the light position."""
+    o = _f64(point)
+    if normal is not None:
+        nn = _f64(normal)
+        o = o + 1e-3 * (nn / np.linalg.norm(nn))
+    to_light = _f64(light) - o
+    max_t = float(np.linalg.norm(to_light))
+    if max_t == 0.0:
+        return 1
+    d = to_light / max_t
+    rx, ry, rz = model.dims
+    seg_a = np.ascontiguousarray(model.seg_a, dtype=np.float32)
+    seg_b = np.ascontiguousarray(model.seg_b, dtype=np.float32)
+    fn = lib().lvo_geometry_blocked
+    fn.restype = C.c_int
+    blocked = fn(_p(o), _p(d), C.c_double(max_t), C.c_int64(rx), C.c_int64(ry), C.c_int64(rz),
+                 _p(model.counts), _p(model.offsets), _p(seg_a), _p(seg_b), C.c_double(float(radius)),
+                 C.c_int(1 if joint_spheres else 0))
+    return 0 if blocked else 1
+
+
+def ao_hemisphere_geometry(point, normal, model, n_rays=100, radius=15.0, tube_radius=0.3, jitter=0.0) -> float:
+    """illumination.ao_hemisphere_geometry (illumination.py:158-173)."""
+    p = _f64(point)
+    nn = _f64(normal)
+    nn = nn / np.linalg.norm(nn)
+    rx, ry, rz = model.dims
+    seg_a = np.ascontiguousarray(model.seg_a, dtype=np.float32)
+    seg_b = np.ascontiguousarray(model.seg_b, dtype=np.float32)
+    fn = lib().lvo_ao_hemisphere_point
+    fn.restype = C.c_double
+    return float(fn(_p(p), _p(nn), C.c_int64(int(n_rays)), C.c_double(float(radius)), C.c_double(float(jitter)),
+                    C.c_int64(rx), C.c_int64(ry), C.c_int64(rz), _p(model.counts), _p(model.offsets),
+                    _p(seg_a), _p(seg_b), C.c_double(float(tube_radius))))
+
+
 def render(camera: dict, model, levels=None, *, tube_radius=0.3, opacity_mode="constant",
            base_opacity=1.0, tau=0.95, neighbor=True, joint_spheres=True, shadow_mode="none",
            ao_mode="none", background=(0.0, 0.0, 0.0, 1.0), light_dir=None, ambient=0.2,

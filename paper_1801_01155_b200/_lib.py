@@ -62,7 +62,8 @@ SYMBOLS = [
     "lvx_occupancy_dilate", "lvx_neighbor_sums", "lvx_render_scratch_bytes", "lvx_render", "lvx_render_wf_scratch_bytes", "lvx_render_wf", "lvx_render_wf_last_launches",
     "lvx_render_footprint", "lvx_untile",
     "lvx_fibonacci_dirs", "lvx_ao_bake", "lvx_probe_dda", "lvx_probe_tube", "lvx_probe_sphere",
-    "lvx_probe_trilinear", "lvx_probe_cone", "lvx_probe_ao_density",
+    "lvx_probe_trilinear", "lvx_probe_cone", "lvx_probe_ao_density", "lvx_probe_blocked",
+    "lvx_probe_ao_hemisphere",
 ]
 
 _lib = None

@@ -133,6 +133,42 @@ int fill_octree(LvxOctree &oc, const lvx_lod *lod) {
 
 }  // namespace
 
+namespace {
+
+__global__ void __launch_bounds__(64)
+probe_blocked_kernel(LvxGeomModel M, const double *__restrict__ rays, const double *__restrict__ max_t,
+                     double radius, int joints, i64 n, int32_t *__restrict__ out) {
+    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double *r = rays + 6 * i;
+    out[i] = lvx_geometry_blocked(r[0], r[1], r[2], r[3], r[4], r[5], max_t[i], M, radius, joints != 0) ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(64)
+probe_ao_hemi_kernel(LvxGeomModel M, const double *__restrict__ pts, const double *__restrict__ nrm, int n_rays,
+                     double radius, const double *__restrict__ dirs, double tube_r, i64 n,
+                     double *__restrict__ out) {
+    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    out[i] = lvx_ao_hemisphere_point(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], nrm[3 * i], nrm[3 * i + 1],
+                                     nrm[3 * i + 2], n_rays, radius, dirs, M, tube_r);
+}
+
+int geom_model(LvxGeomModel &G, const lvx_model *m) {
+    LVX_REQUIRE(m && m->rx >= 1 && m->ry >= 1 && m->rz >= 1 && m->counts_d && m->offsets_d && m->nmask_d,
+                "geometry rays need counts, offsets and the neighbour grids (lvx_neighbor_sums)");
+    G.rx = m->rx;
+    G.ry = m->ry;
+    G.rz = m->rz;
+    G.counts = m->counts_d;
+    G.offsets = m->offsets_d;
+    G.rec = m->seg_rec_d;
+    G.nmask = m->nmask_d;
+    return LVX_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 int lvx_ao_bake(const uint8_t *counts_d, const int32_t dims[3], int32_t n_rays, double radius,
@@ -221,6 +257,33 @@ int lvx_probe_ao_density(const lvx_lod *lod, const double *pts_d, const double *
     LVX_REQUIRE(pts_d && normals_d && dirs_d && out_d, "null argument");
     probe_ao_kernel<<<(unsigned)lvx_ceil_div(n, 64), 64, 0, (cudaStream_t)stream>>>(
         oc, pts_d, normals_d, n_rays, radius, step, dirs_d, n, out_d);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_probe_blocked(const lvx_model *model, const double *rays_d, const double *max_t_d, double radius,
+                      int32_t joints, int64_t n, int32_t *out_d, void *stream) {
+    LvxGeomModel G;
+    if (int rc = geom_model(G, model)) return rc;
+    LVX_REQUIRE(n >= 0 && radius > 0.0, "bad arguments");
+    if (n == 0) return LVX_OK;
+    LVX_REQUIRE(rays_d && max_t_d && out_d, "null argument");
+    probe_blocked_kernel<<<(unsigned)lvx_ceil_div(n, 64), 64, 0, (cudaStream_t)stream>>>(G, rays_d, max_t_d, radius,
+                                                                                       joints, n, out_d);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_probe_ao_hemisphere(const lvx_model *model, const double *pts_d, const double *normals_d, int32_t n_rays,
+                            double radius, const double *dirs_d, double tube_r, int64_t n, double *out_d,
+                            void *stream) {
+    LvxGeomModel G;
+    if (int rc = geom_model(G, model)) return rc;
+    LVX_REQUIRE(n >= 0 && n_rays >= 1 && tube_r > 0.0, "bad arguments");
+    if (n == 0) return LVX_OK;
+    LVX_REQUIRE(pts_d && normals_d && dirs_d && out_d, "null argument");
+    probe_ao_hemi_kernel<<<(unsigned)lvx_ceil_div(n, 64), 64, 0, (cudaStream_t)stream>>>(
+        G, pts_d, normals_d, n_rays, radius, dirs_d, tube_r, n, out_d);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }

@@ -420,6 +420,135 @@ __device__ __forceinline__ double lvx_ao_density_point(double px, double py, dou
     return total / (double)n_rays;
 }
 
+// ---------------------------------------------------------------------------
+// Geometry secondary rays: geometry_ray_blocked / ao_hemisphere_point,
+// _kernels.py:450-495, 572-589.
+// ---------------------------------------------------------------------------
+
+// What the secondary rays read of the voxel model.
+struct LvxGeomModel {
+    int rx, ry, rz;
+    const u8 *counts;
+    const u32 *offsets;
+    const lvx_seg_record *rec;
+    const u32 *nmask;  // occupancy bits of the 27-neighbourhood over the padded grid (lvx_neighbor_sums)
+};
+
+// 27-neighbourhood mask `e` of the cell a walk just left, re-expressed around the cell it
+// moved to (step per axis in {-1, 0, 1}); voxels leaving the 3x3x3 frame drop out.
+__device__ __forceinline__ u32 lvx_shift_mask27(u32 e, int dx, int dy, int dz) {
+    if (dx > 0) e = (e & 0x6DB6DB6u) >> 1;
+    else if (dx < 0) e = (e & 0x36DB6DBu) << 1;
+    if (dy > 0) e = (e & 0x7E3F1F8u) >> 3;
+    else if (dy < 0) e = (e & 0x0FC7E3Fu) << 3;
+    if (dz > 0) e = (e & 0x7FFFE00u) >> 9;
+    else if (dz < 0) e = (e & 0x003FFFFu) << 9;
+    return e;
+}
+
+// geometry_ray_blocked, _kernels.py:450-495: true if any tube (or joint sphere) is entered
+// by the ray at 1e-9 < t_in < max_t.  The reference walks the padded grid and tests the 27
+// neighbours of every window that starts before max_t; the answer is a disjunction over
+// (ray, segment) pairs, so each voxel is tested once (the first time a window sees it), only
+// voxels within tube radius of the ray piece are listed (a hit's entry point lies in some
+// window and within the radius of its segment), and a conservative float32 distance test
+// runs ahead of the exact float64 ones.  Same set of hits, same boolean.
+__device__ inline bool lvx_geometry_blocked(double ox, double oy, double oz, double dx, double dy,
+                                            double dz, double max_t, const LvxGeomModel &M, double radius,
+                                            bool joints) {
+    LvxDda dda;
+    dda.init(ox, oy, oz, dx, dy, dz, M.rx, M.ry, M.rz, 1);
+    if (!dda.alive) return false;
+    const double cull = radius + 1e-4;
+    const float reach_pt = (float)radius + 2e-3f;
+    const float fdx = (float)dx, fdy = (float)dy, fdz = (float)dz;
+    u32 listed = 0;
+    int px = 0, py = 0, pz = 0;
+    int wx, wy, wz;
+    double t0, t1;
+    while (dda.next(wx, wy, wz, t0, t1)) {
+        if (t0 >= max_t) break;
+        if (listed) {
+            const int sx = wx - px, sy = wy - py, sz = wz - pz;
+            listed = (sx < -1 || sx > 1 || sy < -1 || sy > 1 || sz < -1 || sz > 1) ? 0u
+                                                                                 : lvx_shift_mask27(listed, sx, sy, sz);
+        }
+        px = wx;
+        py = wy;
+        pz = wz;
+        u32 nm = __ldg(M.nmask + (((i64)(wz + 1) * (M.ry + 2) + (wy + 1)) * (M.rx + 2) + (wx + 1)));
+        if (nm == 0) continue;
+        const double p0x = ox + t0 * dx, p0y = oy + t0 * dy, p0z = oz + t0 * dz;
+        const double p1x = ox + t1 * dx, p1y = oy + t1 * dy, p1z = oz + t1 * dz;
+        u32 bx_ = 0x2492492u, by_ = 0x0E07038u, bz_ = 0x003FE00u;
+        if (fmin(p0x, p1x) - cull < (double)wx) bx_ |= 0x1249249u;
+        if (fmax(p0x, p1x) + cull > (double)(wx + 1)) bx_ |= 0x4924924u;
+        if (fmin(p0y, p1y) - cull < (double)wy) by_ |= 0x01C0E07u;
+        if (fmax(p0y, p1y) + cull > (double)(wy + 1)) by_ |= 0x70381C0u;
+        if (fmin(p0z, p1z) - cull < (double)wz) bz_ |= 0x00001FFu;
+        if (fmax(p0z, p1z) + cull > (double)(wz + 1)) bz_ |= 0x7FC0000u;
+        nm &= bx_ & by_ & bz_;
+        const u32 fresh = nm & ~listed;
+        listed |= nm;
+        for (u32 mm = fresh; mm; mm &= mm - 1) {
+            const int b = __ffs((int)mm) - 1;
+            const int bz = b / 9, by = (b - 9 * bz) / 3, bx = b - 9 * bz - 3 * by;
+            const int hx = wx + bx - 1, hy = wy + by - 1, hz = wz + bz - 1;
+            const u32 lin = (u32)(hx + M.rx * (hy + M.ry * hz));
+            const u32 cnt = __ldg(M.counts + lin), base = __ldg(M.offsets + lin);
+            // voxel-local float32 frame
+            const float q0x = (float)(p0x - (double)hx), q0y = (float)(p0y - (double)hy),
+                        q0z = (float)(p0z - (double)hz);
+            const float fhx = (float)hx, fhy = (float)hy, fhz = (float)hz;
+            for (u32 s = 0; s < cnt; ++s) {
+                const float4 ra = __ldg(reinterpret_cast<const float4 *>(M.rec + base + s));
+                const float4 rb = __ldg(reinterpret_cast<const float4 *>(M.rec + base + s) + 1);
+                {
+                    // bounding sphere of the segment (tube and both joints) against the ray's line
+                    const float cx = 0.5f * ((ra.x - fhx) + (rb.x - fhx)) - q0x, cy = 0.5f * ((ra.y - fhy) + (rb.y - fhy)) - q0y,
+                                cz = 0.5f * ((ra.z - fhz) + (rb.z - fhz)) - q0z;
+                    const float tc = cx * fdx + cy * fdy + cz * fdz;
+                    const float reach = rb.w + reach_pt;
+                    if ((cx * cx + cy * cy + cz * cz) - tc * tc > reach * reach) continue;
+                }
+                LvxHit h;
+                if (lvx_tube_f32axis(ox, oy, oz, dx, dy, dz, ra.x, ra.y, ra.z, rb.x, rb.y, rb.z, radius, h) &&
+                    1e-9 < h.t_in && h.t_in < max_t)
+                    return true;
+                if (joints) {
+                    if (lvx_sphere<false>(ox, oy, oz, dx, dy, dz, (double)ra.x, (double)ra.y, (double)ra.z, radius, h) &&
+                        1e-9 < h.t_in && h.t_in < max_t)
+                        return true;
+                    if (lvx_sphere<false>(ox, oy, oz, dx, dy, dz, (double)rb.x, (double)rb.y, (double)rb.z, radius, h) &&
+                        1e-9 < h.t_in && h.t_in < max_t)
+                        return true;
+                }
+            }
+        }
+    }
+    return false;
+}
+
+// ao_hemisphere_point, _kernels.py:572-589 (jitter 0: `dirs` is the host-built hemisphere
+// lattice, see lvx_ao_density_point)
+__device__ inline double lvx_ao_hemisphere_point(double px, double py, double pz, double nx, double ny,
+                                                 double nz, int n_rays, double radius,
+                                                 const double *__restrict__ dirs, const LvxGeomModel &M,
+                                                 double tube_r) {
+    int blocked = 0;
+    double t[3], b[3];
+    lvx_orient_frame(nx, ny, nz, t, b);
+    const double ox = px + 1e-3 * nx, oy = py + 1e-3 * ny, oz = pz + 1e-3 * nz;
+    for (int i = 0; i < n_rays; ++i) {
+        const double lx = dirs[3 * i], ly = dirs[3 * i + 1], lz = dirs[3 * i + 2];
+        const double dx = lx * t[0] + ly * b[0] + lz * nx;
+        const double dy = lx * t[1] + ly * b[1] + lz * ny;
+        const double dz = lx * t[2] + ly * b[2] + lz * nz;
+        if (lvx_geometry_blocked(ox, oy, oz, dx, dy, dz, radius, M, tube_r, true)) blocked += 1;
+    }
+    return (double)blocked / (double)n_rays;
+}
+
 // shade_scalar, _kernels.py:316-329
 __device__ __forceinline__ double lvx_shade(double nx, double ny, double nz, double lx, double ly,
                                             double lz, double vx, double vy, double vz, double ka,

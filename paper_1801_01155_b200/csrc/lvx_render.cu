@@ -129,9 +129,15 @@ __device__ __forceinline__ void shade_hit(const RenderArgs &A, double ox, double
     const double gx = (double)A.rx, gy = (double)A.ry, gz = (double)A.rz;
     const double px = ox + h.t_in * ddx, py = oy + h.t_in * ddy, pz = oz + h.t_in * ddz;
     double shadow_term = 0.0;
-    if (p.shadow_mode == LVX_SHADOW_CONE)
+    if (p.shadow_mode == LVX_SHADOW_CONE) {
         shadow_term = lvx_cone_blocking(px, py, pz, p.light[0], p.light[1], p.light[2], A.oc, gx,
                                         gy, gz, 0.01);
+    } else if (p.shadow_mode == LVX_SHADOW_HARD) {
+        const LvxGeomModel G = {A.rx, A.ry, A.rz, A.counts, A.offsets, A.rec, A.nmask};
+        if (lvx_geometry_blocked(px + 1e-3 * h.nx, py + 1e-3 * h.ny, pz + 1e-3 * h.nz, p.light[0], p.light[1],
+                                 p.light[2], 1e30, G, p.tube_r, p.joints != 0))
+            shadow_term = 1.0;
+    }
     double ao_term = 0.0;
     if (p.ao_mode == LVX_AO_PRECOMPUTED) {
         ao_term = lvx_trilinear(A.ao_flat, 0, A.rx, A.ry, A.rz, 1.0, px, py, pz);
@@ -140,6 +146,10 @@ __device__ __forceinline__ void shade_hit(const RenderArgs &A, double ox, double
     } else if (p.ao_mode == LVX_AO_DENSITY) {
         ao_term = lvx_ao_density_point(px, py, pz, h.nx, h.ny, h.nz, p.ao_n_rays, p.ao_radius, 1.0,
                                        A.ao_dirs, A.oc.flat, A.rx, A.ry, A.rz);
+    } else if (p.ao_mode == LVX_AO_HEMISPHERE) {
+        const LvxGeomModel G = {A.rx, A.ry, A.rz, A.counts, A.offsets, A.rec, A.nmask};
+        ao_term = lvx_ao_hemisphere_point(px, py, pz, h.nx, h.ny, h.nz, p.ao_n_rays, p.ao_radius, A.ao_dirs, G,
+                                          p.tube_r);
     }
     const float table_alpha = __ldg(A.table + 4 * attr + 3);
     alpha_out = lvx_alpha_of(p.opacity_mode, p.base_alpha, (double)table_alpha, h.t_in, h.t_out);
@@ -997,20 +1007,22 @@ static int render_impl(const lvx_camera *cam, const lvx_model *model, const lvx_
     LVX_REQUIRE(!params->neighbor || (model->nsum_d && model->nmask_d),
                 "neighbour mode needs the neighbour grids (lvx_neighbor_sums)");
     LVX_REQUIRE(params->opacity_mode >= 0 && params->opacity_mode <= 2, "bad opacity mode");
-    LVX_REQUIRE(params->shadow_mode == LVX_SHADOW_NONE || params->shadow_mode == LVX_SHADOW_CONE,
-                "shadow_mode %d is not built in this library (none/cone only)", params->shadow_mode);
-    LVX_REQUIRE(params->ao_mode == LVX_AO_NONE || params->ao_mode == LVX_AO_DENSITY ||
-                    params->ao_mode == LVX_AO_PRECOMPUTED,
-                "ao_mode %d is not built in this library (none/density-rays/precomputed only)",
+    LVX_REQUIRE(params->shadow_mode == LVX_SHADOW_NONE || params->shadow_mode == LVX_SHADOW_CONE ||
+                    params->shadow_mode == LVX_SHADOW_HARD,
+                "shadow_mode %d is not built in this library (none/hard/cone only)", params->shadow_mode);
+    LVX_REQUIRE(params->ao_mode >= LVX_AO_NONE && params->ao_mode <= LVX_AO_PRECOMPUTED, "bad ao_mode %d",
                 params->ao_mode);
+    LVX_REQUIRE((params->shadow_mode != LVX_SHADOW_HARD && params->ao_mode != LVX_AO_HEMISPHERE) || model->nmask_d,
+                "geometry secondary rays (hard shadows, hemisphere AO) need the neighbour grids (lvx_neighbor_sums)");
     const bool need_oct = params->shadow_mode == LVX_SHADOW_CONE || params->ao_mode == LVX_AO_DENSITY;
     LVX_REQUIRE(!need_oct || (lod && lod->oct_flat_d && lod->n_levels >= 1 &&
                               lod->n_levels <= LVX_MAX_LEVELS),
                 "cone shadows / density-rays AO need a density octree");
     LVX_REQUIRE(params->ao_mode != LVX_AO_PRECOMPUTED || (lod && lod->ao_flat_d),
                 "precomputed AO requested but no AO field given");
-    LVX_REQUIRE(params->ao_mode != LVX_AO_DENSITY || (lod->ao_dirs_d && params->ao_n_rays >= 1),
-                "density-rays AO needs the direction lattice");
+    LVX_REQUIRE((params->ao_mode != LVX_AO_DENSITY && params->ao_mode != LVX_AO_HEMISPHERE) ||
+                    (lod && lod->ao_dirs_d && params->ao_n_rays >= 1),
+                "density-rays / hemisphere AO need the direction lattice");
 
     RenderArgs A;
     memset(&A, 0, sizeof(A));

@@ -7,9 +7,11 @@ _kernels.py:346-445, 541-620 of the reference), evaluated on the GPU.
     lvx_probe_ao_density  <- ao_density_rays
     lvx_probe_trilinear   <- sample_ao / DensityOctree.sample
 
-The geometry-based secondary rays of the reference (`hard_shadow`,
-`replines_shadow`, `ao_hemisphere_geometry`) are outside the accelerated path
- and raise NotImplementedError here.
+    lvx_probe_blocked        <- hard_shadow / geometry_ray_blocked
+    lvx_probe_ao_hemisphere  <- ao_hemisphere_geometry / ao_hemisphere_point
+
+`replines_shadow` (representative lines) is outside the
+accelerated path and raises NotImplementedError here.
 """
 from __future__ import annotations
 
@@ -213,6 +215,74 @@ def _not_built(name):
     return fn
 
 
-hard_shadow = _not_built("hard_shadow")
 replines_shadow = _not_built("replines_shadow")
-ao_hemisphere_geometry = _not_built("ao_hemisphere_geometry")
+
+
+def _model_struct(model: VoxelModel) -> "_lib.Model":
+    counts_d, offsets_d, rec_d, table_d, occ_d = model.device_view(need_occ=True)
+    m = _lib.Model()
+    m.rx, m.ry, m.rz = model.spec.dims
+    m.counts_d, m.offsets_d = counts_d.data_ptr(), offsets_d.data_ptr()
+    m.seg_rec_d, m.table_d = rec_d.data_ptr(), table_d.data_ptr()
+    m.nsum_d, m.nmask_d = occ_d[0].data_ptr(), occ_d[1].data_ptr()
+    m._keep = (counts_d, offsets_d, rec_d, table_d, occ_d)
+    return m
+
+
+def _shadow_origin(point, normal) -> np.ndarray:
+    p = np.asarray(point, dtype=np.float64)
+    if normal is None:
+        return p
+    return p + 1e-3 * _unit(normal, "normal")
+
+
+def hard_shadow(point, light, model: VoxelModel, radius: float = 0.3, normal=None,
+                joint_spheres: bool = True) -> int:
+    """1 if the point sees the light position, 0 if any tube or joint sphere lies
+    strictly between (illumination.py:96-112 -> geometry_ray_blocked,
+    _kernels.py:450-495).  Passing the surface normal offsets the ray origin by 1e-3
+    along it."""
+    torch = _lib.require_device()
+    o = _shadow_origin(point, normal)
+    to_light = np.asarray(light, dtype=np.float64) - o
+    max_t = float(np.linalg.norm(to_light))
+    if max_t == 0.0:
+        return 1
+    d = to_light / max_t
+    m = _model_struct(model)
+    rays = _lib.to_device(np.concatenate([o, d])[None])
+    mt = _lib.to_device(np.asarray([max_t], dtype=np.float64))
+    out = torch.empty(1, dtype=torch.int32, device="cuda")
+    _lib.check(_lib.lib().lvx_probe_blocked(C.byref(m), _lib.ptr(rays), _lib.ptr(mt), C.c_double(float(radius)),
+                                            C.c_int32(1 if joint_spheres else 0), C.c_int64(1), _lib.ptr(out),
+                                            _lib.stream_ptr()))
+    return 0 if int(out.item()) else 1
+
+
+def ao_hemisphere_geometry(point, normal, model: VoxelModel, params: Optional[AOParams] = None,
+                           tube_radius: float = 0.3, jitter: float = 0.0):
+    """Fraction of deterministic hemisphere rays around the normal that hit a tube within
+    the radius of influence (illumination.py:158-173 -> ao_hemisphere_point,
+    _kernels.py:572-589).  `point` may be one point or an (n,3) array."""
+    if params is None:
+        params = AOParams()
+    torch = _lib.require_device()
+    pts = np.asarray(point, dtype=np.float64)
+    single = pts.ndim == 1
+    pts = np.ascontiguousarray(pts.reshape(-1, 3))
+    nrm = np.asarray(normal, dtype=np.float64).reshape(-1, 3)
+    nrm = np.stack([_unit(v, "normal") for v in nrm])
+    if nrm.shape[0] == 1 and pts.shape[0] > 1:
+        nrm = np.repeat(nrm, pts.shape[0], axis=0)
+    n = pts.shape[0]
+    m = _model_struct(model)
+    dirs = _lib.to_device(_lib.fibonacci_dirs(params.n_rays, 1, float(jitter))) if jitter else \
+        fibonacci_dirs_device(params.n_rays, 1)
+    out = torch.empty(max(n, 1), dtype=torch.float64, device="cuda")
+    pts_d, nrm_d = _lib.to_device(pts), _lib.to_device(np.ascontiguousarray(nrm))
+    _lib.check(_lib.lib().lvx_probe_ao_hemisphere(
+        C.byref(m), _lib.ptr(pts_d), _lib.ptr(nrm_d), C.c_int32(int(params.n_rays)),
+        C.c_double(float(params.radius)), _lib.ptr(dirs), C.c_double(float(tube_radius)), C.c_int64(n),
+        _lib.ptr(out), _lib.stream_ptr()))
+    v = out[:n].cpu().numpy()
+    return float(v[0]) if single else v

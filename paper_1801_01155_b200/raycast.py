@@ -317,12 +317,9 @@ def params_struct(params: RenderParams, neighbor: int) -> "_lib.Params":
 def check_modes(params: RenderParams, model: VoxelModel, octree):
     """The error behaviour of _illum_args (raycast.py:414-421), plus the modes this
     build does not accelerate."""
-    if params.shadow_mode in ("hard", "replines"):
-        raise NotImplementedError(f"shadow_mode={params.shadow_mode!r} traces geometry secondary "
-                                  "rays and is outside the accelerated path (none/cone only)")
-    if params.ao_mode == "hemisphere-geometry":
-        raise NotImplementedError("ao_mode='hemisphere-geometry' is outside the accelerated path "
-                                  "(none/density-rays/precomputed only)")
+    if params.shadow_mode == "replines":
+        raise NotImplementedError("shadow_mode='replines' (representative lines) is outside the "
+                                  "accelerated path (none/hard/cone only)")
     if params.shadow_mode == "cone" and octree is None:
         raise ValueError("cone shadows need a density octree")
     if params.ao_mode == "density-rays" and octree is None:
@@ -378,7 +375,8 @@ class FramePlan:
         self._scale = 1.0
         self.cam = camera_struct(camera)
         self.par = params_struct(params, neighbor)
-        counts_d, offsets_d, rec_d, table_d, occ_d = model.device_view(need_occ=bool(neighbor))
+        geometry_rays = params.shadow_mode == "hard" or params.ao_mode == "hemisphere-geometry"
+        counts_d, offsets_d, rec_d, table_d, occ_d = model.device_view(need_occ=bool(neighbor) or geometry_rays)
         m = _lib.Model()
         m.rx, m.ry, m.rz = model.spec.dims
         m.counts_d, m.offsets_d = counts_d.data_ptr(), offsets_d.data_ptr()
@@ -387,13 +385,15 @@ class FramePlan:
         m.nmask_d = occ_d[1].data_ptr() if occ_d is not None else None
         self.mdl = m
         ao_d = model.ao_device() if params.ao_mode == "precomputed" else None
-        dirs_d = fibonacci_dirs_device(params.ao_rays, 1) if params.ao_mode == "density-rays" else None
+        dirs_d = fibonacci_dirs_device(params.ao_rays, 1) \
+            if params.ao_mode in ("density-rays", "hemisphere-geometry") else None
         if octree is not None:
             self.lod = octree.lod_struct(ao_d, dirs_d)
         else:
             self.lod = _lib.Lod()
             self.lod.n_levels = 0
             self.lod.ao_flat_d = ao_d.data_ptr() if ao_d is not None else None
+            self.lod.ao_dirs_d = dirs_d.data_ptr() if dirs_d is not None else None
         t = _lib.Tiling()
         t.tile_w, t.tile_h = tile_w, tile_h
         t.tile_first, t.tile_step, t.compact = int(tile_first), int(tile_step), 1 if compact else 0

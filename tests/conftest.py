@@ -26,7 +26,9 @@ VOX_CASES = ["helices", "turbulence", "wiggles", "lattice", "cap255", "bins4", "
 
 RENDER_CASES = ["opaque_nb", "opaque_own", "alpha25_nb", "alpha25_own_nojoints", "alpha25_nb_ao_cone",
                 "alpha25_own_densao", "alpha05_tau1_nb", "distance_scaled", "transfer_light",
-                "cap255_overflow"]
+                "cap255_overflow",
+                # geometry secondary rays: hard shadows, hemisphere-geometry AO
+                "geom_hard_nb", "geom_hard_own_nojoints", "geom_hemi_nb", "geom_hard_hemi"]
 
 
 def render_kwargs(g):

@@ -46,7 +46,12 @@ def ref_model(pts, attrs, off, dims, n_bins):
     return RV.build_voxel_model(curveset(pts, attrs, off), GridSpec(dims, n_bins))
 
 
+ONLY = None  # `--only <prefix>`: write just the fixtures whose name starts with the prefix
+
+
 def save(name, **arrays):
+    if ONLY is not None and not name.startswith(ONLY):
+        return
     path = os.path.join(HERE, name + ".npz")
     np.savez_compressed(path, **arrays)
     print(f"{name}.npz  {os.path.getsize(path) / 1024:.1f} KiB")
@@ -128,11 +133,24 @@ RENDER_CASES = [
     ("transfer_light", "wiggles", (48, 36), dict(neighbor_mode="on", opacity_mode="transfer",
                                                   light_dir=(1.0, -0.5, 0.25), shininess=7.5)),
     ("cap255_overflow", "cap255", (40, 30), dict(neighbor_mode="on", base_opacity=0.02, tau=1.0)),
+    # geometry secondary rays: hard shadows, hemisphere-geometry AO
+    ("geom_hard_nb", "helices", (48, 36), dict(neighbor_mode="on", base_opacity=0.4, shadow_mode="hard",
+                                                light_dir=(0.3, 0.2, 1.0))),
+    ("geom_hard_own_nojoints", "turbulence", (40, 30), dict(neighbor_mode="off", base_opacity=0.5,
+                                                             shadow_mode="hard", light_dir=(-0.4, 0.7, 0.5),
+                                                             joint_spheres=False)),
+    ("geom_hemi_nb", "wiggles", (40, 30), dict(neighbor_mode="on", base_opacity=0.5,
+                                                ao_mode="hemisphere-geometry", ao_rays=7, ao_radius=3.0)),
+    ("geom_hard_hemi", "turbulence", (32, 24), dict(neighbor_mode="on", base_opacity=0.6, shadow_mode="hard",
+                                                     light_dir=(0.2, -0.3, 1.0), ao_mode="hemisphere-geometry",
+                                                     ao_rays=5, ao_radius=4.0)),
 ]
 
 
 def make_render(models, octrees, ao_fields):
     for name, mname, (W, H), kw in RENDER_CASES:
+        if ONLY is not None and not ("render_" + name).startswith(ONLY):
+            continue
         m, dims = models[mname]
         m.ao = ao_fields[mname].values if mname in ao_fields else None
         if kw.get("opacity_mode") == "transfer":
@@ -239,12 +257,45 @@ def make_primitives(models, octrees, ao_fields):
     save("prim_shade", n=nn_, l=ll, v=vv, shade=sh)
 
 
+def make_geometry_probes(models):
+    """Point probes of the geometry secondary rays: hard_shadow / ao_hemisphere_geometry."""
+    from linevox.illumination import ao_hemisphere_geometry, hard_shadow
+    rng = np.random.default_rng(123)
+    for mname in ("helices", "turbulence"):
+        m, dims = models[mname]
+        d = np.asarray(dims, dtype=np.float64)
+        n = 160
+        P = rng.uniform(0.5, 1.0, (n, 3)) * 0 + rng.uniform(0.2, 0.8, (n, 3)) * d
+        # half of the points sit on a segment's surface (the interesting case)
+        seg = rng.integers(0, m.seg_a.shape[0], n // 2)
+        mid = 0.5 * (m.seg_a[seg].astype(np.float64) + m.seg_b[seg].astype(np.float64))
+        off = rng.normal(size=(n // 2, 3))
+        off /= np.linalg.norm(off, axis=1, keepdims=True)
+        P[: n // 2] = mid + 0.3 * off
+        N = rng.normal(size=(n, 3))
+        N[: n // 2] = off
+        N /= np.linalg.norm(N, axis=1, keepdims=True)
+        L = rng.uniform(-0.5, 1.5, (n, 3)) * d
+        L[::7] = P[::7] + 0.05 * N[::7]  # a few very close lights
+        hs = np.array([hard_shadow(P[i], L[i], m, 0.3, N[i] if i % 2 == 0 else None, bool(i % 3))
+                       for i in range(n)], dtype=np.int64)
+        ao = np.array([ao_hemisphere_geometry(P[i], N[i], m, AOParams(n_rays=9, radius=3.5), 0.3)
+                       for i in range(n)])
+        aoj = np.array([ao_hemisphere_geometry(P[i], N[i], m, AOParams(n_rays=6, radius=2.5), 0.25, jitter=0.37)
+                        for i in range(0, n, 4)])
+        save("geom_probe_" + mname, P=P, N=N, L=L, hard=hs, ao=ao, ao_jitter=aoj)
+
+
 def main():
+    global ONLY
+    if "--only" in sys.argv:
+        ONLY = sys.argv[sys.argv.index("--only") + 1]
     models = make_voxelize()
     octrees = make_lod(models)
     ao_fields = make_ao(models, octrees)
     make_render(models, octrees, ao_fields)
     make_primitives(models, octrees, ao_fields)
+    make_geometry_probes(models)
 
 
 if __name__ == "__main__":

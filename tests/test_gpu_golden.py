@@ -98,6 +98,23 @@ def test_render_matches_reference(lv, name, engine, monkeypatch):
     assert (err > 1e-6).mean() < 1e-3
 
 
+@pytest.mark.parametrize("mname", ["helices", "turbulence"])
+def test_geometry_secondary_ray_probes(lv, mname):
+    """hard_shadow / ao_hemisphere_geometry (geometry_ray_blocked, ao_hemisphere_point) against
+    the reference's values: booleans and blocked-ray fractions, bit-exact."""
+    g = golden("geom_probe_" + mname)
+    m = gpu_model(lv, golden("vox_" + mname))
+    P, N, L = g["P"], g["N"], g["L"]
+    hs = [lv.hard_shadow(P[i], L[i], m, 0.3, N[i] if i % 2 == 0 else None, bool(i % 3)) for i in range(len(P))]
+    assert hs == list(g["hard"])
+    ao = lv.ao_hemisphere_geometry(P, N, m, lv.AOParams(n_rays=9, radius=3.5), 0.3)
+    assert np.array_equal(ao, g["ao"])
+    assert lv.ao_hemisphere_geometry(P[3], N[3], m, lv.AOParams(n_rays=9, radius=3.5), 0.3) == g["ao"][3]
+    aoj = np.array([lv.ao_hemisphere_geometry(P[i], N[i], m, lv.AOParams(n_rays=6, radius=2.5), 0.25, jitter=0.37)
+                    for i in range(0, len(P), 4)])
+    assert np.array_equal(aoj, g["ao_jitter"])
+
+
 def test_tube_and_sphere_probes(lv):
     from paper_1801_01155_b200 import raycast
     g = golden("prim_tube_sphere")

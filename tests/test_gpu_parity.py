@@ -260,8 +260,8 @@ def test_error_conventions(lv, synth):
         lv.render_frame(cam, m, None, None, lv.RenderParams(ao_mode="density-rays"))
     with pytest.raises(ValueError, match="precomputed AO"):
         lv.render_frame(cam, m, None, None, lv.RenderParams(ao_mode="precomputed"))
-    with pytest.raises(NotImplementedError):
-        lv.render_frame(cam, m, None, None, lv.RenderParams(shadow_mode="hard", light_dir=(0, 0, 1)))
+    with pytest.raises(NotImplementedError):  # representative lines: SURVEY 8f row 3, not built
+        lv.render_frame(cam, m, None, None, lv.RenderParams(shadow_mode="replines", light_dir=(0, 0, 1)))
     with pytest.raises(ValueError):
         lv.build_octree(np.zeros((0, 2, 2), np.float32))
 

@@ -80,6 +80,23 @@ def test_render_matches_reference(oracle, name):
     assert [st["voxel_steps"], st["intersection_tests"], st["window_overflow"]] == list(g["stats"])
 
 
+@pytest.mark.parametrize("mname", ["helices", "turbulence"])
+def test_geometry_secondary_ray_probes(oracle, mname):
+    """hard_shadow / ao_hemisphere_geometry (illumination.py:96-112, 158-173) as point probes."""
+    g = golden("geom_probe_" + mname)
+    m = oracle_model(oracle, golden("vox_" + mname))
+    P, N, L = g["P"], g["N"], g["L"]
+    hs = [oracle.hard_shadow(P[i], L[i], m, 0.3, N[i] if i % 2 == 0 else None, bool(i % 3)) for i in range(len(P))]
+    assert hs == list(g["hard"])
+    assert 0 < sum(hs) < len(hs)  # the fixture holds lit and shadowed points
+    ao = np.array([oracle.ao_hemisphere_geometry(P[i], N[i], m, 9, 3.5, 0.3) for i in range(len(P))])
+    assert np.array_equal(ao, g["ao"])
+    aoj = np.array([oracle.ao_hemisphere_geometry(P[i], N[i], m, 6, 2.5, 0.25, jitter=0.37)
+                    for i in range(0, len(P), 4)])
+    assert np.array_equal(aoj, g["ao_jitter"])
+    assert ao.max() > 0.0
+
+
 def test_tube_and_sphere_primitives(oracle):
     g = golden("prim_tube_sphere")
     r = float(g["r"])
