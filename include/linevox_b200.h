@@ -73,45 +73,36 @@ int lvx_device_check(void);
 int lvx_mark_curve_starts(const int64_t *curve_off_d, int64_t n_curves, int64_t n_points,
                           uint8_t *first_d, void *stream);
 
-/* Pass 1: clip every edge, count kept chords per voxel (atomics).
- * vox_cnt_d u32[V] must be zeroed by the caller.  dims = (rx, ry, rz). */
-int lvx_voxelize_count(const double *pts_d, const uint8_t *first_d, int64_t n_points,
-                       const int32_t dims[3], uint32_t *vox_cnt_d, void *stream);
-
-/* Device prefix sums over the V voxel counters (voxelizer.py:442-449, 462-466):
- *   cursor_d  u32[V]  exclusive scan of the RAW counts (scatter cursors)
- *   offsets_d u32[V]  exclusive scan of min(count,255)  (final headers)
- *   counts_d  u8[V]   min(count,255)
- *   totals_d  u64[2]  {raw chords, kept segments}
- * scratch_d: lvx_scan_scratch_bytes(V) bytes. */
+/* Prefix sums over the per-voxel chord counts: cursor_d = exclusive scan of the raw counts
+ * (start of every voxel's group), offsets_d / counts_d = the model's headers (counts capped at
+ * 255, voxelizer.py:442-466), totals_d[0] = chords, totals_d[1] = segments kept. */
 size_t lvx_scan_scratch_bytes(int64_t n);
 int lvx_voxel_scan(const uint32_t *vox_cnt_d, int64_t n_voxels, uint32_t *cursor_d,
                    uint32_t *offsets_d, uint8_t *counts_d, uint64_t *totals_d,
                    void *scratch_d, void *stream);
 
-/* Pass 2: clip again and scatter one raw record per kept chord into its voxel's
- * range (slot = atomicAdd(cursor[lin])).  After the call cursor_d[lin] is the END
- * of voxel lin's raw range.  Raw record (SoA):
- *   raw_key_d u64[S_raw]  (edge index << 16) | kept-chord ordinal inside the edge
- *                          -- strictly increasing in (curve, chord order)
- *   raw_q_d   u64[S_raw]  face_in | bin_in<<3 | face_out<<19 | bin_out<<22 | attr<<38
- *   raw_lin_d u32[S_raw]  voxel linear index
- * edge_kept_d u16[P] (nullable): kept chords ending in each edge (for seg_order).
- * err_d i32[1]: set to 1 if an endpoint is off every face (voxelizer.py:366-368). */
-int lvx_voxelize_emit(const double *pts_d, const double *attrs_d, const uint8_t *first_d,
-                      int64_t n_points, const int32_t dims[3], int32_t n_bins,
-                      uint32_t *cursor_d, uint64_t *raw_key_d, uint64_t *raw_q_d,
-                      uint32_t *raw_lin_d, uint16_t *edge_kept_d, int32_t *err_d,
+/* Raw chord slots written by the clipper (SoA, coalesced):
+ *   raw_key_d u64  (edge index << 16) | kept-chord ordinal inside the edge -- strictly
+ *                  increasing in (curve, chord order)
+ *   raw_q_d   u64  face_in | bin_in<<3 | face_out<<19 | bin_out<<22 | attr<<38
+ *   raw_lin_d u32  voxel linear index, 0xFFFFFFFF for a slot without a chord
+ * edge_kept_d u16[P] (nullable): kept chords ending in each edge (for seg_order). */
+/* Single-pass clipper: the vertices are read from HBM once (voxelizer.py:174-263, 358-380,
+ * 419-449: _plane_events, _clip_batch, _faces_and_bins and the chunk loop of build_voxel_model).
+ *   lvx_voxelize_bound  number of plane crossings = upper bound of the chord count; sizes raw_*
+ *   lvx_voxelize_clip   clip + emit: one slot per crossing in raw_*[0, *n_slots); raw_lin of a
+ *                       slot whose chord was dropped is 0xFFFFFFFF; per-voxel chord counts are
+ *                       added into vox_cnt_d (caller zeroes it); err_d: 1 = an endpoint off
+ *                       every face (voxelizer.py:366-368), 2 = capacity too small
+ * followed by lvx_voxel_scan -> lvx_raw_regroup -> lvx_voxelize_compact. */
+int lvx_voxelize_bound(const double *pts_d, const uint8_t *first_d, int64_t n_points,
+                       uint64_t *total_d, void *stream);
+int lvx_voxelize_clip(const double *pts_d, const double *attrs_d, const uint8_t *first_d,
+                      int64_t n_points, const int32_t dims[3], int32_t n_bins, uint64_t capacity,
+                      uint32_t *vox_cnt_d, uint64_t *raw_key_d, uint64_t *raw_q_d,
+                      uint32_t *raw_lin_d, uint64_t *n_slots_d, uint16_t *edge_kept_d, int32_t *err_d,
                       void *stream);
 
-/* Pass 3: order every voxel's list by key (== the reference's stable sort by
- * voxel, voxelizer.py:435-438), keep rank < 255, lid = rank % 32, decode
- * endpoints to bin centres, pack.  Any output pointer except packed_d may be
- * NULL to skip that derived cache.
- *   packed_d u8[S*w], seg_a_d/seg_b_d f32[S,3], seg_attr_d/seg_lid_d u8[S],
- *   seg_voxel_d i32[S,3], seg_face_in/out_d u8[S], seg_bin_in/out_d u16[S],
- *   seg_key_d u64[S] (provenance key of each kept segment),
- *   seg_rec_d 32-byte render records [S] (see lvx_seg_record). */
 typedef struct {
     float ax, ay, az;
     uint32_t meta; /* attr | lid << 8 */
@@ -119,27 +110,31 @@ typedef struct {
     float half_len; /* >= |b-a|/2 (rounded up): radius of the segment's bounding sphere */
 } lvx_seg_record;
 
-int lvx_voxelize_compact(const uint64_t *raw_key_d, const uint64_t *raw_q_d,
-                         const uint32_t *raw_lin_d, int64_t n_raw,
-                         const uint32_t *vox_cnt_d, const uint32_t *cursor_end_d,
-                         const uint32_t *offsets_d, const int32_t dims[3], int32_t n_bins,
-                         uint8_t *packed_d, float *seg_a_d, float *seg_b_d,
-                         uint8_t *seg_attr_d, uint8_t *seg_lid_d, int32_t *seg_voxel_d,
-                         uint8_t *seg_face_in_d, uint16_t *seg_bin_in_d,
-                         uint8_t *seg_face_out_d, uint16_t *seg_bin_out_d,
-                         uint64_t *seg_key_d, lvx_seg_record *seg_rec_d, void *stream);
+/* One chord grouped by voxel (32 bytes = one memory sector, so the scatter that groups
+ * them writes whole sectors). */
+typedef struct {
+    uint64_t key; /* global edge index << 16 | ordinal of the chord on its edge */
+    uint64_t q;   /* face_in 3 | bin_in 16 | face_out 3 | bin_out 16 | attr 8 */
+    uint32_t lin; /* voxel */
+    uint32_t _pad[3];
+} lvx_raw_record;
 
-/* Multi-GPU merge (voxelization sharded by line ID): raw records
- * all-gathered from every rank are scattered into one voxel-grouped array through
- * the GLOBAL per-voxel cursors (exclusive scan of the summed counts); afterwards
- * cursor_d[lin] is the end of voxel lin's range, ready for lvx_voxelize_compact.
- * This stands where the reference's single stable argsort over all chords does
- * (voxelizer.py:435-438). */
+/* Scatter raw slots (any order; 0xFFFFFFFF voxels skipped) into per-voxel groups through the
+ * cursors from lvx_voxel_scan, which end up at the END of every voxel's range. */
 int lvx_raw_regroup(const uint64_t *in_key_d, const uint64_t *in_q_d, const uint32_t *in_lin_d,
-                    int64_t n_raw, uint32_t *cursor_d, uint64_t *out_key_d, uint64_t *out_q_d,
-                    uint32_t *out_lin_d, void *stream);
+                    int64_t n_slots, uint32_t *cursor_d, lvx_raw_record *grouped_d, void *stream);
 
-/* Generic exclusive scan u16 -> u32 (edge_kept -> edge_base), same scratch rule. */
+/* Order every voxel's group by key (= the reference's stable argsort by voxel,
+ * voxelizer.py:435-438), keep the first 255, lid = rank % 32, decode bin centres, pack
+ * (voxelizer.py:439-488, 383-394).  Optional outputs may be NULL. */
+int lvx_voxelize_compact(const lvx_raw_record *grouped_d, int64_t n_raw, const uint32_t *vox_cnt_d,
+                         const uint32_t *cursor_end_d, const uint32_t *offsets_d,
+                         const int32_t dims[3], int32_t n_bins, uint8_t *packed_d, float *seg_a_d,
+                         float *seg_b_d, uint8_t *seg_attr_d, uint8_t *seg_lid_d,
+                         int32_t *seg_voxel_d, uint8_t *seg_face_in_d, uint16_t *seg_bin_in_d,
+                         uint8_t *seg_face_out_d, uint16_t *seg_bin_out_d, uint64_t *seg_key_d,
+                         lvx_seg_record *seg_rec_d, void *stream);
+
 int lvx_scan_u16(const uint16_t *in_d, int64_t n, uint32_t *out_d, void *scratch_d,
                  void *stream);
 

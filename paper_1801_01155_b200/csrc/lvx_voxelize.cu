@@ -65,54 +65,13 @@ struct EdgeAxes {
 __device__ __forceinline__ void make_event(Event &ev, const EdgeAxes &E, const double a0[3],
                                            double att0, double att1, bool want_attr, int ax,
                                            double k, double s) {
+    // (selects instead of indexing by `ax`: keeps the event in registers)
 #pragma unroll
-    for (int c = 0; c < 3; ++c) ev.pos[c] = a0[c] + s * E.d[c];  // voxelizer.py:228
-    ev.pos[ax] = k;                                              // :229 crossing axis exact
-    ev.attr = want_attr ? att0 + s * (att1 - att0) : 0.0;        // :230
+    for (int c = 0; c < 3; ++c) ev.pos[c] = c == ax ? k : a0[c] + s * E.d[c];  // voxelizer.py:228-229
+    ev.attr = want_attr ? att0 + s * (att1 - att0) : 0.0;                      // :230
     ev.k = k;
     ev.ax = ax;
-    ev.up = E.up[ax];
-}
-
-// Last crossing (in the reference's sorted order) of the nearest earlier edge of
-// the same curve that has any crossing.  Returns false at the curve start.
-template <bool WANT_ATTR>
-__device__ bool lookback_event(const double *__restrict__ pts, const double *__restrict__ attrs,
-                               const u8 *__restrict__ first, i64 i, Event &ev) {
-    i64 ip = i;
-    while (!first[ip]) {
-        ip -= 1;
-        double a0[3], a1[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            a0[c] = pts[3 * ip + c];
-            a1[c] = pts[3 * (ip + 1) + c];
-        }
-        EdgeAxes E;
-        E.init(a0, a1);
-        if (E.total() == 0) continue;
-        int best = -1;
-        double bs = 0.0, bk = 0.0;
-#pragma unroll
-        for (int ax = 0; ax < 3; ++ax) {
-            if (E.cnt[ax] == 0) continue;
-            double k = E.plane(ax, E.cnt[ax] - 1);
-            double s = E.param(ax, k);
-            if (best < 0 || s >= bs) {  // ties: the higher axis sorts last
-                best = ax;
-                bs = s;
-                bk = k;
-            }
-        }
-        double att0 = 0.0, att1 = 0.0;
-        if (WANT_ATTR) {
-            att0 = attrs[ip];
-            att1 = attrs[ip + 1];
-        }
-        make_event(ev, E, a0, att0, att1, WANT_ATTR, best, bk, bs);
-        return true;
-    }
-    return false;
+    ev.up = ax == 0 ? E.up[0] : (ax == 1 ? E.up[1] : E.up[2]);
 }
 
 // Chord voxel + keep test, voxelizer.py:242-250.  Returns the linear voxel index
@@ -166,110 +125,235 @@ __device__ __forceinline__ u32 face_and_bin(const double p[3], const long long v
     return (u32)f | ((u32)(bu + (long long)n * bv) << 3);
 }
 
-// One thread per polyline edge.  EMIT=false: count chords per voxel.  EMIT=true:
-// scatter raw records through the per-voxel cursors.
-template <bool EMIT>
-__global__ void __launch_bounds__(kClipThreads)
-clip_kernel(const double *__restrict__ pts, const double *__restrict__ attrs,
-            const u8 *__restrict__ first, i64 n_points, int rx, int ry, int rz, int n_bins,
-            u32 *__restrict__ vox_cnt_or_cursor, u64 *__restrict__ raw_key,
-            u64 *__restrict__ raw_q, u32 *__restrict__ raw_lin, u16 *__restrict__ edge_kept,
-            int *__restrict__ err) {
-    __shared__ double s_pts[(kClipThreads + 1) * 3];
-    const i64 base = (i64)blockIdx.x * kClipThreads;
-    // coalesced staging of this block's kClipThreads+1 vertices
-    {
-        const i64 lo = base * 3;
-        const i64 hi = min((base + kClipThreads + 1) * 3, n_points * 3);
-        for (i64 k = lo + threadIdx.x; k < hi; k += kClipThreads) s_pts[k - lo] = pts[k];
-    }
-    __syncthreads();
-    const i64 i = base + threadIdx.x;
-    if (i >= n_points) return;
-    int kept = 0;
-    if (i + 1 < n_points && !first[i + 1]) {
-        double a0[3], a1[3];
+// ---------------------------------------------------------------------------
+// Single-pass clipper (lvx_voxelize_bound + lvx_voxelize_clip): the polyline vertices are
+// read from HBM once.  A block stages its 257 vertices, attributes and curve-start flags in
+// shared memory (the look-back to earlier edges stays on chip unless it leaves the block);
+// every edge first COUNTS its kept chords, a block scan and one atomic per block reserve a
+// contiguous range of the raw-record arrays, then the edge re-derives its chords from the
+// staged operands and writes them there (coalesced), bumping the per-voxel counters with
+// result-less atomics.  The order of the raw records is irrelevant: the per-voxel order is
+// restored from the (edge, ordinal) keys by compact_kernel.
+// ---------------------------------------------------------------------------
+
+struct ClipStage {
+    double pts[(kClipThreads + 1) * 3];
+    double attr[kClipThreads + 1];
+    u8 first[kClipThreads + 1];
+};
+
+// vertex / attribute / flag of point index p: from the staged block when inside it
+struct ClipView {
+    const ClipStage &S;
+    const double *pts, *attrs;
+    const u8 *first;
+    i64 base, hi;  // staged range [base, hi)
+    __device__ __forceinline__ void vertex(i64 p, double v[3]) const {
+        if (p >= base && p < hi) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            a0[c] = s_pts[3 * threadIdx.x + c];
-            a1[c] = s_pts[3 * (threadIdx.x + 1) + c];
+            for (int c = 0; c < 3; ++c) v[c] = S.pts[3 * (p - base) + c];
+        } else {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) v[c] = pts[3 * p + c];
         }
+    }
+    __device__ __forceinline__ double attr(i64 p) const { return p >= base && p < hi ? S.attr[p - base] : attrs[p]; }
+    __device__ __forceinline__ bool is_first(i64 p) const { return p >= base && p < hi ? S.first[p - base] : first[p]; }
+};
+
+template <bool WANT_ATTR>
+__device__ bool lookback_event_v(const ClipView &V, i64 i, Event &ev) {
+    i64 ip = i;
+    while (!V.is_first(ip)) {
+        ip -= 1;
+        double a0[3], a1[3];
+        V.vertex(ip, a0);
+        V.vertex(ip + 1, a1);
         EdgeAxes E;
         E.init(a0, a1);
-        if (E.total() > 0) {
-            double att0 = 0.0, att1 = 0.0;
-            if (EMIT) {
-                att0 = attrs[i];
-                att1 = attrs[i + 1];
-            }
-            Event prev, ev;
-            bool have_prev = lookback_event<EMIT>(pts, attrs, first, i, prev);
-            int j[3] = {0, 0, 0};
-            double s_next[3], k_next[3];
+        if (E.total() == 0) continue;
+        int best = -1;
+        double bs = 0.0, bk = 0.0;
 #pragma unroll
-            for (int ax = 0; ax < 3; ++ax) {
-                k_next[ax] = E.plane(ax, 0);
-                s_next[ax] = E.cnt[ax] > 0 ? E.param(ax, k_next[ax]) : 2.0;
+        for (int ax = 0; ax < 3; ++ax) {
+            if (E.cnt[ax] == 0) continue;
+            double k = E.plane(ax, E.cnt[ax] - 1);
+            double s = E.param(ax, k);
+            if (best < 0 || s >= bs) {  // ties: the higher axis sorts last
+                best = ax;
+                bs = s;
+                bk = k;
             }
-            const int total = E.total();
-            for (int n = 0; n < total; ++n) {
-                // smallest s first; ties resolve x<y<z (stable lexsort, voxelizer.py:224)
-                int best = 0;
-                double bs = s_next[0];
-                if (s_next[1] < bs) {
-                    best = 1;
-                    bs = s_next[1];
-                }
-                if (s_next[2] < bs) {
-                    best = 2;
-                    bs = s_next[2];
-                }
-                double bk = best == 0 ? k_next[0] : (best == 1 ? k_next[1] : k_next[2]);
-                make_event(ev, E, a0, att0, att1, EMIT, best, bk, bs);
-                if (have_prev) {
-                    long long vox[3];
-                    i64 lin = chord_voxel(prev, ev, rx, ry, rz, vox);
-                    if (lin >= 0) {
-                        if (!EMIT) {
-                            atomicAdd(&vox_cnt_or_cursor[lin], 1u);
-                        } else {
-                            // voxelizer.py:439 -- rint is round-half-even
-                            double av = rint(255.0 * 0.5 * (prev.attr + ev.attr));
-                            av = av < 0.0 ? 0.0 : (av > 255.0 ? 255.0 : av);
-                            u32 fin = face_and_bin(prev.pos, vox, n_bins);
-                            u32 fout = face_and_bin(ev.pos, vox, n_bins);
-                            if (fin == 0xFFFFFFFFu || fout == 0xFFFFFFFFu) {
-                                *err = 1;
-                                fin = fout = 0;
-                            }
-                            u64 q = (u64)fin | ((u64)fout << 19) | ((u64)(u32)av << 38);
-                            u32 slot = atomicAdd(&vox_cnt_or_cursor[lin], 1u);
-                            raw_key[slot] = ((u64)i << 16) | (u64)kept;
-                            raw_q[slot] = q;
-                            raw_lin[slot] = (u32)lin;
-                        }
-                        kept += 1;
-                    }
-                }
-                prev = ev;
-                have_prev = true;
-                // advance the axis that fired
+        }
+        double att0 = 0.0, att1 = 0.0;
+        if (WANT_ATTR) {
+            att0 = V.attr(ip);
+            att1 = V.attr(ip + 1);
+        }
+        make_event(ev, E, a0, att0, att1, WANT_ATTR, best, bk, bs);
+        return true;
+    }
+    return false;
+}
+
+constexpr u32 kNoVoxel = 0xFFFFFFFFu;  // raw_lin of a reserved slot that holds no chord
+
+// The chords of edge i in the reference's order, written to raw[slot0 + n] for the n-th
+// crossing of the edge (slots of dropped chords keep kNoVoxel) and counted per voxel.
+// Returns how many were kept.
+__device__ __forceinline__ int clip_edge(const ClipView &V, i64 i, const EdgeAxes &E, const double a0[3],
+                                         int rx, int ry, int rz, int n_bins, u32 *__restrict__ vox_cnt,
+                                         u64 *__restrict__ raw_key, u64 *__restrict__ raw_q,
+                                         u32 *__restrict__ raw_lin, u64 slot0, int *__restrict__ err) {
+    const int total = E.total();
+    const double att0 = V.attr(i), att1 = V.attr(i + 1);
+    Event prev, ev;
+    bool have_prev = lookback_event_v<true>(V, i, prev);
+    int j[3] = {0, 0, 0};
+    double s_next[3], k_next[3];
 #pragma unroll
-                for (int ax = 0; ax < 3; ++ax) {
-                    if (ax == best) {
-                        j[ax] += 1;
-                        if (j[ax] < E.cnt[ax]) {
-                            k_next[ax] = E.plane(ax, j[ax]);
-                            s_next[ax] = E.param(ax, k_next[ax]);
-                        } else {
-                            s_next[ax] = 2.0;  // exhausted (valid s are clipped to <= 1)
-                        }
-                    }
+    for (int ax = 0; ax < 3; ++ax) {
+        k_next[ax] = E.plane(ax, 0);
+        s_next[ax] = E.cnt[ax] > 0 ? E.param(ax, k_next[ax]) : 2.0;
+    }
+    int kept = 0;
+    for (int n = 0; n < total; ++n) {
+        // smallest s first; ties resolve x<y<z (stable lexsort, voxelizer.py:224)
+        int best = 0;
+        double bs = s_next[0];
+        if (s_next[1] < bs) {
+            best = 1;
+            bs = s_next[1];
+        }
+        if (s_next[2] < bs) {
+            best = 2;
+            bs = s_next[2];
+        }
+        const double bk = best == 0 ? k_next[0] : (best == 1 ? k_next[1] : k_next[2]);
+        make_event(ev, E, a0, att0, att1, true, best, bk, bs);
+        u32 out_lin = kNoVoxel;
+        if (have_prev) {
+            long long vox[3];
+            const i64 lin = chord_voxel(prev, ev, rx, ry, rz, vox);
+            if (lin >= 0) {
+                // voxelizer.py:439 -- rint is round-half-even
+                double av = rint(255.0 * 0.5 * (prev.attr + ev.attr));
+                av = av < 0.0 ? 0.0 : (av > 255.0 ? 255.0 : av);
+                u32 fin = face_and_bin(prev.pos, vox, n_bins);
+                u32 fout = face_and_bin(ev.pos, vox, n_bins);
+                if (fin == 0xFFFFFFFFu || fout == 0xFFFFFFFFu) {
+                    *err = 1;
+                    fin = fout = 0;
+                }
+                raw_key[slot0 + n] = ((u64)i << 16) | (u64)kept;
+                raw_q[slot0 + n] = (u64)fin | ((u64)fout << 19) | ((u64)(u32)av << 38);
+                out_lin = (u32)lin;
+                atomicAdd(&vox_cnt[lin], 1u);  // result unused: compiles to a reduction
+                kept += 1;
+            }
+        }
+        raw_lin[slot0 + n] = out_lin;
+        prev = ev;
+        have_prev = true;
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            if (ax == best) {
+                j[ax] += 1;
+                if (j[ax] < E.cnt[ax]) {
+                    k_next[ax] = E.plane(ax, j[ax]);
+                    s_next[ax] = E.param(ax, k_next[ax]);
+                } else {
+                    s_next[ax] = 2.0;  // exhausted (valid s are clipped to <= 1)
                 }
             }
         }
     }
-    if (EMIT && edge_kept) edge_kept[i] = (u16)kept;
+    return kept;
+}
+
+__global__ void __launch_bounds__(kClipThreads)
+clip_once_kernel(const double *__restrict__ pts, const double *__restrict__ attrs, const u8 *__restrict__ first,
+                 i64 n_points, int rx, int ry, int rz, int n_bins, u64 capacity, u32 *__restrict__ vox_cnt,
+                 u64 *__restrict__ raw_key, u64 *__restrict__ raw_q, u32 *__restrict__ raw_lin,
+                 unsigned long long *__restrict__ n_slots, u16 *__restrict__ edge_kept, int *__restrict__ err) {
+    __shared__ ClipStage S;
+    __shared__ u32 s_warp[kClipThreads / 32];
+    __shared__ unsigned long long s_base;
+    const i64 base = (i64)blockIdx.x * kClipThreads;
+    const i64 hi = min(base + kClipThreads + 1, n_points);
+    for (i64 k = base * 3 + threadIdx.x; k < hi * 3; k += kClipThreads) S.pts[k - base * 3] = pts[k];
+    for (i64 k = base + threadIdx.x; k < hi; k += kClipThreads) {
+        S.attr[k - base] = attrs[k];
+        S.first[k - base] = first[k];
+    }
+    __syncthreads();
+    const ClipView V = {S, pts, attrs, first, base, hi};
+    const i64 i = base + threadIdx.x;
+    const bool edge = i + 1 < n_points && !S.first[threadIdx.x + 1];
+    double a0[3] = {0.0, 0.0, 0.0};
+    EdgeAxes E;
+    int crossings = 0;
+    if (edge) {
+        double a1[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            a0[c] = S.pts[3 * threadIdx.x + c];
+            a1[c] = S.pts[3 * (threadIdx.x + 1) + c];
+        }
+        E.init(a0, a1);
+        crossings = E.total();
+    }
+    // reserve one slot per plane crossing of the block (every chord ends at a crossing)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    u32 inc = (u32)crossings;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    u32 before = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < kClipThreads / 32; ++w) {
+        const u32 t = s_warp[w];
+        if (w < warp) before += t;
+        total += t;
+    }
+    if (threadIdx.x == 0) s_base = total ? atomicAdd(n_slots, (unsigned long long)total) : 0ull;
+    __syncthreads();
+    int kept = 0;
+    if (crossings > 0) {
+        const u64 slot0 = s_base + before + inc - (u32)crossings;
+        if (slot0 + (u64)crossings > capacity) *err = 2;  // the caller's bound was wrong
+        else kept = clip_edge(V, i, E, a0, rx, ry, rz, n_bins, vox_cnt, raw_key, raw_q, raw_lin, slot0, err);
+    }
+    if (i < n_points && edge_kept) edge_kept[i] = (u16)kept;
+}
+
+// Upper bound of the chord count: every chord ends at a plane crossing.
+__global__ void __launch_bounds__(256)
+count_crossings_kernel(const double *__restrict__ pts, const u8 *__restrict__ first, i64 n_points,
+                       unsigned long long *__restrict__ total) {
+    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long n = 0;
+    if (i + 1 < n_points && !first[i + 1]) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double d = fabs(floor(pts[3 * (i + 1) + c]) - floor(pts[3 * i + c]));
+            n += d < 1e15 ? (unsigned long long)d : 0ull;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xFFFFFFFFu, n, o);
+    __shared__ unsigned long long s[8];
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = n;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < 8; ++w) t += s[w];
+        if (t) atomicAdd(total, t);
+    }
 }
 
 __global__ void mark_starts_kernel(const i64 *__restrict__ curve_off, i64 n_curves,
@@ -444,23 +528,23 @@ __device__ __forceinline__ void decode_point(u32 face, u32 code, int n, int lb, 
 }
 
 __global__ void __launch_bounds__(256)
-compact_kernel(const u64 *__restrict__ raw_key, const u64 *__restrict__ raw_q,
-               const u32 *__restrict__ raw_lin, i64 n_raw, const u32 *__restrict__ vox_cnt,
+compact_kernel(const lvx_raw_record *__restrict__ grouped, i64 n_raw, const u32 *__restrict__ vox_cnt,
                const u32 *__restrict__ cursor_end, const u32 *__restrict__ offsets, int rx, int ry,
                int n_bins, int lb, int width, CompactOut o) {
     const i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n_raw) return;
-    const u32 lin = raw_lin[r];
+    const ulonglong2 kq = *reinterpret_cast<const ulonglong2 *>(grouped + r);
+    const u32 lin = grouped[r].lin;
     const u32 n = vox_cnt[lin];
-    const u64 key = raw_key[r];
+    const u64 key = kq.x;
     u32 rank = 0;
     if (n > 1) {
         const u32 end = cursor_end[lin];
-        for (u32 k = end - n; k < end; ++k) rank += raw_key[k] < key ? 1u : 0u;
+        for (u32 k = end - n; k < end; ++k) rank += grouped[k].key < key ? 1u : 0u;
     }
     if (rank >= 255u) return;  // voxelizer.py:442-448 keep the first 255 in curve order
     const i64 dst = (i64)offsets[lin] + rank;
-    const u64 q = raw_q[r];
+    const u64 q = kq.y;
     const u32 fi = (u32)(q & 7u), bi = (u32)((q >> 3) & 0xFFFFu);
     const u32 fo = (u32)((q >> 19) & 7u), bo = (u32)((q >> 22) & 0xFFFFu);
     const u32 attr = (u32)((q >> 38) & 0xFFu);
@@ -547,14 +631,16 @@ seg_records_kernel(const float *__restrict__ seg_a, const float *__restrict__ se
 __global__ void __launch_bounds__(256)
 regroup_kernel(const u64 *__restrict__ in_key, const u64 *__restrict__ in_q,
                const u32 *__restrict__ in_lin, i64 n, u32 *__restrict__ cursor,
-               u64 *__restrict__ out_key, u64 *__restrict__ out_q, u32 *__restrict__ out_lin) {
+               lvx_raw_record *__restrict__ out) {
     const i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
     const u32 lin = in_lin[r];
+    if (lin == kNoVoxel) return;  // a reserved slot without a chord
     const u32 slot = atomicAdd(&cursor[lin], 1u);
-    out_key[slot] = in_key[r];
-    out_q[slot] = in_q[r];
-    out_lin[slot] = lin;
+    // one whole 32-byte sector per record: the scattered write needs no read-modify-write
+    ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(out + slot);
+    dst[0] = make_ulonglong2(in_key[r], in_q[r]);
+    dst[1] = make_ulonglong2((u64)lin, 0ull);
 }
 
 int ilog2i(int n) {
@@ -598,21 +684,6 @@ int lvx_mark_curve_starts(const int64_t *curve_off_d, int64_t n_curves, int64_t 
     return LVX_OK;
 }
 
-int lvx_voxelize_count(const double *pts_d, const uint8_t *first_d, int64_t n_points,
-                       const int32_t dims[3], uint32_t *vox_cnt_d, void *stream) {
-    if (int rc = check_dims(dims)) return rc;
-    LVX_REQUIRE(vox_cnt_d && n_points >= 0, "bad arguments");
-    if (n_points < 2) return LVX_OK;
-    LVX_REQUIRE(pts_d && first_d, "null input");
-    LVX_REQUIRE(n_points < ((i64)1 << 47), "too many vertices");
-    clip_kernel<false><<<(unsigned)lvx_ceil_div(n_points, kClipThreads), kClipThreads, 0,
-                         (cudaStream_t)stream>>>(pts_d, nullptr, first_d, n_points, dims[0],
-                                                 dims[1], dims[2], 0, vox_cnt_d, nullptr, nullptr,
-                                                 nullptr, nullptr, nullptr);
-    LVX_LAUNCH_CHECK();
-    return LVX_OK;
-}
-
 size_t lvx_scan_scratch_bytes(int64_t n) {
     return (size_t)(lvx_ceil_div(n > 0 ? n : 1, kScanTile) * 2 * sizeof(u64));
 }
@@ -651,29 +722,7 @@ int lvx_scan_u16(const uint16_t *in_d, int64_t n, uint32_t *out_d, void *scratch
     return LVX_OK;
 }
 
-int lvx_voxelize_emit(const double *pts_d, const double *attrs_d, const uint8_t *first_d,
-                      int64_t n_points, const int32_t dims[3], int32_t n_bins, uint32_t *cursor_d,
-                      uint64_t *raw_key_d, uint64_t *raw_q_d, uint32_t *raw_lin_d,
-                      uint16_t *edge_kept_d, int32_t *err_d, void *stream) {
-    if (int rc = check_dims(dims)) return rc;
-    if (int rc = check_bins(n_bins)) return rc;
-    LVX_REQUIRE(cursor_d && err_d && n_points >= 0, "bad arguments");
-    if (n_points < 2) {
-        if (edge_kept_d && n_points > 0)
-            LVX_CUDA_CHECK(cudaMemsetAsync(edge_kept_d, 0, (size_t)n_points * 2, (cudaStream_t)stream));
-        return LVX_OK;
-    }
-    LVX_REQUIRE(pts_d && attrs_d && first_d && raw_key_d && raw_q_d && raw_lin_d, "null input");
-    clip_kernel<true><<<(unsigned)lvx_ceil_div(n_points, kClipThreads), kClipThreads, 0,
-                        (cudaStream_t)stream>>>(pts_d, attrs_d, first_d, n_points, dims[0], dims[1],
-                                                dims[2], n_bins, cursor_d, raw_key_d, raw_q_d,
-                                                raw_lin_d, edge_kept_d, err_d);
-    LVX_LAUNCH_CHECK();
-    return LVX_OK;
-}
-
-int lvx_voxelize_compact(const uint64_t *raw_key_d, const uint64_t *raw_q_d,
-                         const uint32_t *raw_lin_d, int64_t n_raw, const uint32_t *vox_cnt_d,
+int lvx_voxelize_compact(const lvx_raw_record *grouped_d, int64_t n_raw, const uint32_t *vox_cnt_d,
                          const uint32_t *cursor_end_d, const uint32_t *offsets_d,
                          const int32_t dims[3], int32_t n_bins, uint8_t *packed_d, float *seg_a_d,
                          float *seg_b_d, uint8_t *seg_attr_d, uint8_t *seg_lid_d,
@@ -684,29 +733,24 @@ int lvx_voxelize_compact(const uint64_t *raw_key_d, const uint64_t *raw_q_d,
     if (int rc = check_bins(n_bins)) return rc;
     LVX_REQUIRE(n_raw >= 0, "bad arguments");
     if (n_raw == 0) return LVX_OK;
-    LVX_REQUIRE(raw_key_d && raw_q_d && raw_lin_d && vox_cnt_d && cursor_end_d && offsets_d &&
-                    packed_d,
-                "null input");
+    LVX_REQUIRE(grouped_d && vox_cnt_d && cursor_end_d && offsets_d && packed_d, "null input");
     const int lb = ilog2i(n_bins);
     const int width = (2 * (3 + 2 * lb) + 8 + 5 + 7) / 8;  // record_width, voxelizer.py:70-76
     CompactOut o = {packed_d,      seg_a_d,        seg_b_d,      seg_attr_d, seg_lid_d, seg_voxel_d,
                     seg_face_in_d, seg_face_out_d, seg_bin_in_d, seg_bin_out_d, seg_key_d, seg_rec_d};
     compact_kernel<<<(unsigned)lvx_ceil_div(n_raw, 256), 256, 0, (cudaStream_t)stream>>>(
-        raw_key_d, raw_q_d, raw_lin_d, n_raw, vox_cnt_d, cursor_end_d, offsets_d, dims[0], dims[1],
-        n_bins, lb, width, o);
+        grouped_d, n_raw, vox_cnt_d, cursor_end_d, offsets_d, dims[0], dims[1], n_bins, lb, width, o);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }
 
 int lvx_raw_regroup(const uint64_t *in_key_d, const uint64_t *in_q_d, const uint32_t *in_lin_d,
-                    int64_t n_raw, uint32_t *cursor_d, uint64_t *out_key_d, uint64_t *out_q_d,
-                    uint32_t *out_lin_d, void *stream) {
-    LVX_REQUIRE(n_raw >= 0, "bad arguments");
-    if (n_raw == 0) return LVX_OK;
-    LVX_REQUIRE(in_key_d && in_q_d && in_lin_d && cursor_d && out_key_d && out_q_d && out_lin_d,
-                "null input");
-    regroup_kernel<<<(unsigned)lvx_ceil_div(n_raw, 256), 256, 0, (cudaStream_t)stream>>>(
-        in_key_d, in_q_d, in_lin_d, n_raw, cursor_d, out_key_d, out_q_d, out_lin_d);
+                    int64_t n_slots, uint32_t *cursor_d, lvx_raw_record *grouped_d, void *stream) {
+    LVX_REQUIRE(n_slots >= 0, "bad arguments");
+    if (n_slots == 0) return LVX_OK;
+    LVX_REQUIRE(in_key_d && in_q_d && in_lin_d && cursor_d && grouped_d, "null input");
+    regroup_kernel<<<(unsigned)lvx_ceil_div(n_slots, 256), 256, 0, (cudaStream_t)stream>>>(
+        in_key_d, in_q_d, in_lin_d, n_slots, cursor_d, grouped_d);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }
@@ -731,6 +775,42 @@ int lvx_build_seg_records(const float *seg_a_d, const float *seg_b_d, const uint
     LVX_REQUIRE(seg_a_d && seg_b_d && seg_attr_d && seg_lid_d && seg_rec_d, "null input");
     seg_records_kernel<<<(unsigned)lvx_ceil_div(n_seg, 256), 256, 0, (cudaStream_t)stream>>>(
         seg_a_d, seg_b_d, seg_attr_d, seg_lid_d, n_seg, seg_rec_d);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_voxelize_bound(const double *pts_d, const uint8_t *first_d, int64_t n_points,
+                       uint64_t *total_d, void *stream) {
+    LVX_REQUIRE(total_d && n_points >= 0, "bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    LVX_CUDA_CHECK(cudaMemsetAsync(total_d, 0, 8, st));
+    if (n_points < 2) return LVX_OK;
+    LVX_REQUIRE(pts_d && first_d, "null input");
+    count_crossings_kernel<<<(unsigned)lvx_ceil_div(n_points, 256), 256, 0, st>>>(
+        pts_d, first_d, n_points, reinterpret_cast<unsigned long long *>(total_d));
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_voxelize_clip(const double *pts_d, const double *attrs_d, const uint8_t *first_d,
+                      int64_t n_points, const int32_t dims[3], int32_t n_bins, uint64_t capacity,
+                      uint32_t *vox_cnt_d, uint64_t *raw_key_d, uint64_t *raw_q_d,
+                      uint32_t *raw_lin_d, uint64_t *n_slots_d, uint16_t *edge_kept_d, int32_t *err_d,
+                      void *stream) {
+    if (int rc = check_dims(dims)) return rc;
+    if (int rc = check_bins(n_bins)) return rc;
+    LVX_REQUIRE(vox_cnt_d && n_slots_d && err_d && n_points >= 0, "bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    LVX_CUDA_CHECK(cudaMemsetAsync(n_slots_d, 0, 8, st));
+    if (n_points < 2) {
+        if (edge_kept_d && n_points > 0) LVX_CUDA_CHECK(cudaMemsetAsync(edge_kept_d, 0, (size_t)n_points * 2, st));
+        return LVX_OK;
+    }
+    LVX_REQUIRE(pts_d && attrs_d && first_d && (capacity == 0 || (raw_key_d && raw_q_d && raw_lin_d)), "null input");
+    LVX_REQUIRE(n_points < ((i64)1 << 47), "too many vertices");
+    clip_once_kernel<<<(unsigned)lvx_ceil_div(n_points, kClipThreads), kClipThreads, 0, st>>>(
+        pts_d, attrs_d, first_d, n_points, dims[0], dims[1], dims[2], n_bins, capacity, vox_cnt_d, raw_key_d,
+        raw_q_d, raw_lin_d, reinterpret_cast<unsigned long long *>(n_slots_d), edge_kept_d, err_d);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }

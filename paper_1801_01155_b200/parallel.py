@@ -182,14 +182,11 @@ def voxelize_shard(pts_d, attrs_d, off_d, n_curves: int, spec: GridSpec, point_b
     GLOBAL edge index (local index + point_base).  Returns a dict of device tensors:
     vox_cnt u32[V] (uncapped), raw_key/raw_q/raw_lin [n_local], edge_kept u16[P_local], err."""
     from . import voxelizer as vz
-    first, vox_cnt = vz.stage_count(pts_d, off_d, n_curves, spec)
-    cursor, _, _, n_raw, _ = vz.stage_scan(vox_cnt)
-    raw_key, raw_q, raw_lin, edge_kept, err = vz.stage_emit(pts_d, attrs_d, first, spec, cursor, n_raw,
-                                                            want_edge_kept)
-    raw_key = raw_key[:n_raw]
+    vox_cnt, raw_key, raw_q, raw_lin, edge_kept, err = vz.stage_clip(pts_d, attrs_d, off_d, n_curves, spec,
+                                                                     want_edge_kept)
     if point_base:
-        raw_key = raw_key + (int(point_base) << 16)
-    return {"vox_cnt": vox_cnt, "raw_key": raw_key, "raw_q": raw_q[:n_raw], "raw_lin": raw_lin[:n_raw],
+        raw_key = raw_key + (int(point_base) << 16)  # (slots without a chord are skipped downstream)
+    return {"vox_cnt": vox_cnt, "raw_key": raw_key, "raw_q": raw_q, "raw_lin": raw_lin,
             "edge_kept": edge_kept, "err": err}
 
 
@@ -200,18 +197,12 @@ def merge_shards(spec: GridSpec, vox_cnt_total, raw_key, raw_q, raw_lin, *, cach
     import torch
     from . import voxelizer as vz
     cursor, offsets, counts, n_raw, S = vz.stage_scan(vox_cnt_total)
-    if n_raw != int(raw_key.shape[0]):
-        raise RuntimeError(f"shard records ({int(raw_key.shape[0])}) do not match the summed counts ({n_raw})")
+    if n_raw > int(raw_key.shape[0]):
+        raise RuntimeError(f"shard slots ({int(raw_key.shape[0])}) cannot hold the summed counts ({n_raw})")
     vz.check_budget(spec, S, memory_budget)
-    g_key = torch.empty(max(n_raw, 1), dtype=torch.int64, device="cuda")
-    g_q = torch.empty(max(n_raw, 1), dtype=torch.int64, device="cuda")
-    g_lin = torch.empty(max(n_raw, 1), dtype=torch.int32, device="cuda")
-    _lib.check(_lib.lib().lvx_raw_regroup(_lib.ptr(raw_key.contiguous()), _lib.ptr(raw_q.contiguous()),
-                                          _lib.ptr(raw_lin.contiguous()), C.c_int64(n_raw), _lib.ptr(cursor),
-                                          _lib.ptr(g_key), _lib.ptr(g_q), _lib.ptr(g_lin), _lib.stream_ptr()))
+    grouped = vz.stage_regroup(raw_key.contiguous(), raw_q.contiguous(), raw_lin.contiguous(), n_raw, cursor)
     prov = edge_kept is not None
-    out = vz.stage_compact(g_key, g_q, g_lin, n_raw, vox_cnt_total, cursor, offsets, counts, spec, S,
-                           caches, prov)
+    out = vz.stage_compact(grouped, n_raw, vox_cnt_total, cursor, offsets, counts, spec, S, caches, prov)
     if prov:
         out["seg_curve"], out["seg_order"] = vz.stage_provenance(out.pop("seg_key"), S, edge_kept, off_d,
                                                                  n_curves)

@@ -3,8 +3,8 @@ with the clip / quantize / sort / pack pipeline running as sm_100a kernels.
 
 The device pipeline (include/linevox_b200.h):
 
-    lvx_mark_curve_starts -> lvx_voxelize_count -> lvx_voxel_scan
-        -> lvx_voxelize_emit -> lvx_voxelize_compact -> lvx_scan_u16 + lvx_provenance
+    lvx_mark_curve_starts -> lvx_voxelize_bound -> lvx_voxelize_clip -> lvx_voxel_scan
+        -> lvx_raw_regroup -> lvx_voxelize_compact -> lvx_scan_u16 + lvx_provenance
 
 `VoxelModel` keeps the reference's field names.  Arrays live on the GPU; the
 numpy views the reference exposes (`model.counts`, `model.packed`, `model.seg_a`,
@@ -306,18 +306,46 @@ def _scratch(n):
     return torch.empty(max(nbytes, 16), dtype=torch.uint8, device="cuda")
 
 
-def stage_count(pts_d, off_d, n_curves: int, spec: GridSpec):
-    """mark curve starts + pass 1 (chords per voxel).  Returns (first u8[P], vox_cnt u32[V])."""
+def stage_clip(pts_d, attrs_d, off_d, n_curves: int, spec: GridSpec, want_edge_kept: bool):
+    """Single-pass clipper: mark curve starts, bound the chord count (one host read, it sizes
+    the raw arrays), clip + emit.  Returns (vox_cnt u32[V] uncapped, raw_key, raw_q, raw_lin
+    [n_slots] -- one slot per plane crossing, raw_lin = 0xFFFFFFFF where no chord was kept --,
+    edge_kept u16[P] or None, err)."""
     torch = _lib.require_device()
     L, st = _lib.lib(), _lib.stream_ptr()
     P = int(pts_d.shape[0])
     first = torch.empty(max(P, 1), dtype=torch.uint8, device="cuda")
     _lib.check(L.lvx_mark_curve_starts(_lib.ptr(off_d), C.c_int64(n_curves), C.c_int64(P),
                                        _lib.ptr(first), st))
+    bound = torch.zeros(1, dtype=torch.int64, device="cuda")
+    _lib.check(L.lvx_voxelize_bound(_lib.ptr(pts_d), _lib.ptr(first), C.c_int64(P), _lib.ptr(bound), st))
+    cap = int(bound.item())
+    if cap >= 2 ** 32:
+        raise MemoryError(f"up to {cap} chords exceed the 32-bit offsets of the voxel headers")
     vox_cnt = torch.zeros(spec.voxel_count, dtype=torch.int32, device="cuda")
-    _lib.check(L.lvx_voxelize_count(_lib.ptr(pts_d), _lib.ptr(first), C.c_int64(P),
-                                    _lib.i32x3(spec.dims), _lib.ptr(vox_cnt), st))
-    return first, vox_cnt
+    raw_key = torch.empty(max(cap, 1), dtype=torch.int64, device="cuda")
+    raw_q = torch.empty(max(cap, 1), dtype=torch.int64, device="cuda")
+    raw_lin = torch.empty(max(cap, 1), dtype=torch.int32, device="cuda")
+    n_slots_d = torch.zeros(1, dtype=torch.int64, device="cuda")
+    edge_kept = torch.empty(max(P, 1), dtype=torch.int16, device="cuda") if want_edge_kept else None
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.check(L.lvx_voxelize_clip(
+        _lib.ptr(pts_d), _lib.ptr(attrs_d), _lib.ptr(first), C.c_int64(P), _lib.i32x3(spec.dims),
+        C.c_int32(spec.bins_per_axis), C.c_uint64(cap), _lib.ptr(vox_cnt), _lib.ptr(raw_key), _lib.ptr(raw_q),
+        _lib.ptr(raw_lin), _lib.ptr(n_slots_d), _lib.ptr(edge_kept), _lib.ptr(err), st))
+    # every crossing reserves exactly one slot: n_slots == cap
+    return vox_cnt, raw_key[:cap], raw_q[:cap], raw_lin[:cap], edge_kept, err
+
+
+def stage_regroup(raw_key, raw_q, raw_lin, n_raw: int, cursor):
+    """Scatter the raw slots (any order, empty ones skipped) into per-voxel groups of 32-byte
+    records through the cursors, which end up pointing at the END of every voxel's range."""
+    torch = _lib.require_device()
+    grouped = torch.empty((max(n_raw, 1), 4), dtype=torch.int64, device="cuda")
+    _lib.check(_lib.lib().lvx_raw_regroup(_lib.ptr(raw_key), _lib.ptr(raw_q), _lib.ptr(raw_lin),
+                                          C.c_int64(int(raw_lin.shape[0])), _lib.ptr(cursor), _lib.ptr(grouped),
+                                          _lib.stream_ptr()))
+    return grouped
 
 
 def stage_scan(vox_cnt):
@@ -338,24 +366,7 @@ def stage_scan(vox_cnt):
     return cursor, offsets, counts, n_raw, S
 
 
-def stage_emit(pts_d, attrs_d, first, spec: GridSpec, cursor, n_raw: int, want_edge_kept: bool):
-    """Pass 2: clip again and scatter raw records through the cursors (which end up
-    pointing at the END of every voxel's range)."""
-    torch = _lib.require_device()
-    P = int(pts_d.shape[0])
-    raw_key = torch.empty(max(n_raw, 1), dtype=torch.int64, device="cuda")
-    raw_q = torch.empty(max(n_raw, 1), dtype=torch.int64, device="cuda")
-    raw_lin = torch.empty(max(n_raw, 1), dtype=torch.int32, device="cuda")
-    edge_kept = torch.empty(max(P, 1), dtype=torch.int16, device="cuda") if want_edge_kept else None
-    err = torch.zeros(1, dtype=torch.int32, device="cuda")
-    _lib.check(_lib.lib().lvx_voxelize_emit(
-        _lib.ptr(pts_d), _lib.ptr(attrs_d), _lib.ptr(first), C.c_int64(P), _lib.i32x3(spec.dims),
-        C.c_int32(spec.bins_per_axis), _lib.ptr(cursor), _lib.ptr(raw_key), _lib.ptr(raw_q),
-        _lib.ptr(raw_lin), _lib.ptr(edge_kept), _lib.ptr(err), _lib.stream_ptr()))
-    return raw_key, raw_q, raw_lin, edge_kept, err
-
-
-def stage_compact(raw_key, raw_q, raw_lin, n_raw: int, vox_cnt, cursor_end, offsets, counts,
+def stage_compact(grouped, n_raw: int, vox_cnt, cursor_end, offsets, counts,
                   spec: GridSpec, S: int, caches: bool, want_keys: bool):
     """Pass 3: per-voxel ordering by key, 255 cap, lid, decode, pack."""
     torch = _lib.require_device()
@@ -382,7 +393,7 @@ def stage_compact(raw_key, raw_q, raw_lin, n_raw: int, vox_cnt, cursor_end, offs
         out["seg_key"] = torch.empty(m, dtype=torch.int64, device=dev)
     g = out.get
     _lib.check(_lib.lib().lvx_voxelize_compact(
-        _lib.ptr(raw_key), _lib.ptr(raw_q), _lib.ptr(raw_lin), C.c_int64(n_raw), _lib.ptr(vox_cnt),
+        _lib.ptr(grouped), C.c_int64(n_raw), _lib.ptr(vox_cnt),
         _lib.ptr(cursor_end), _lib.ptr(offsets), _lib.i32x3(spec.dims), C.c_int32(spec.bins_per_axis),
         _lib.ptr(out["packed"]), _lib.ptr(g("seg_a")), _lib.ptr(g("seg_b")), _lib.ptr(g("seg_attr")),
         _lib.ptr(g("seg_lid")), _lib.ptr(g("seg_voxel")), _lib.ptr(g("seg_face_in")),
@@ -427,13 +438,13 @@ def voxelize_device(pts_d, attrs_d, off_d, n_curves: int, spec: GridSpec, *, cac
     pts_d f64[P,3], attrs_d f64[P], off_d i64[n_curves+1].  Returns a dict of
     device tensors plus `dropped` and `n_segments`.  This is the kernel-only path
     bench.py times; `build_voxel_model` wraps it with the host<->device copies."""
-    first, vox_cnt = stage_count(pts_d, off_d, n_curves, spec)
+    vox_cnt, raw_key, raw_q, raw_lin, edge_kept, err = stage_clip(pts_d, attrs_d, off_d, n_curves, spec,
+                                                                  provenance)
     cursor, offsets, counts, n_raw, S = stage_scan(vox_cnt)
     check_budget(spec, S, memory_budget)
-    raw_key, raw_q, raw_lin, edge_kept, err = stage_emit(pts_d, attrs_d, first, spec, cursor, n_raw,
-                                                         provenance)
-    out = stage_compact(raw_key, raw_q, raw_lin, n_raw, vox_cnt, cursor, offsets, counts, spec, S,
-                        caches, provenance)
+    grouped = stage_regroup(raw_key, raw_q, raw_lin, n_raw, cursor)
+    del raw_key, raw_q, raw_lin
+    out = stage_compact(grouped, n_raw, vox_cnt, cursor, offsets, counts, spec, S, caches, provenance)
     if provenance:
         out["seg_curve"], out["seg_order"] = stage_provenance(out.pop("seg_key"), S, edge_kept,
                                                               off_d, n_curves)
