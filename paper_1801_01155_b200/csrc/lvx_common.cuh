@@ -53,3 +53,14 @@ __host__ __device__ __forceinline__ float lvx_half_len(float ax, float ay, float
     const float ux = bx - ax, uy = by - ay, uz = bz - az;
     return 0.5f * sqrtf(ux * ux + uy * uy + uz * uz) * 1.0001f + 1e-6f;
 }
+
+#ifdef __CUDACC__
+// 32-byte (one sector) global accesses: sm_100 has 256-bit vector loads/stores
+// (LDG/STG.E.ENL2.256).  `p` must be 32-byte aligned.
+__device__ __forceinline__ void lvx_st256(void *p, u64 a, u64 b, u64 c, u64 d) {
+    asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+}
+__device__ __forceinline__ void lvx_ld256(const void *p, u64 &a, u64 &b, u64 &c, u64 &d) {
+    asm volatile("ld.global.v4.b64 {%0, %1, %2, %3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+}
+#endif

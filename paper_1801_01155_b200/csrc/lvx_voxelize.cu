@@ -17,7 +17,10 @@ namespace {
 
 constexpr double kMinChord = 1e-9;  // voxelizer.py:37
 constexpr double kFaceEps = 1e-9;   // voxelizer.py:361
-constexpr int kClipThreads = 256;
+#ifndef LVX_CLIP_THREADS
+#define LVX_CLIP_THREADS 128
+#endif
+constexpr int kClipThreads = LVX_CLIP_THREADS;
 
 struct Event {
     double pos[3];
@@ -271,7 +274,10 @@ __device__ __forceinline__ int clip_edge(const ClipView &V, i64 i, const EdgeAxe
     return kept;
 }
 
-__global__ void __launch_bounds__(kClipThreads)
+#ifndef LVX_CLIP_MINB
+#define LVX_CLIP_MINB 8
+#endif
+__global__ void __launch_bounds__(kClipThreads, LVX_CLIP_MINB)
 clip_once_kernel(const double *__restrict__ pts, const double *__restrict__ attrs, const u8 *__restrict__ first,
                  i64 n_points, int rx, int ry, int rz, int n_bins, u64 capacity, u32 *__restrict__ vox_cnt,
                  u64 *__restrict__ raw_key, u64 *__restrict__ raw_q, u32 *__restrict__ raw_lin,
@@ -405,6 +411,32 @@ __device__ __forceinline__ u32 load_count(const T *in, i64 idx, i64 n) {
     return idx < n ? (u32)in[idx] : 0u;
 }
 
+// the kScanItems counters of one thread (one 32-byte access when they are u32 and in range)
+template <typename T>
+__device__ __forceinline__ void load_counts(const T *in, i64 t0, i64 n, u32 v[kScanItems]) {
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) v[k] = load_count(in, t0 + k, n);
+}
+template <>
+__device__ __forceinline__ void load_counts<u32>(const u32 *in, i64 t0, i64 n, u32 v[kScanItems]) {
+    static_assert(kScanItems == 8, "one 32-byte vector per thread");
+    if (t0 + kScanItems <= n && (reinterpret_cast<uintptr_t>(in) & 31) == 0) {
+        u64 a, b, c, d;
+        lvx_ld256(in + t0, a, b, c, d);
+        v[0] = (u32)a;
+        v[1] = (u32)(a >> 32);
+        v[2] = (u32)b;
+        v[3] = (u32)(b >> 32);
+        v[4] = (u32)c;
+        v[5] = (u32)(c >> 32);
+        v[6] = (u32)d;
+        v[7] = (u32)(d >> 32);
+    } else {
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) v[k] = load_count(in, t0 + k, n);
+    }
+}
+
 // phase 1: per-tile sums of raw and capped counts
 template <typename T, bool CAP>
 __global__ void __launch_bounds__(kScanThreads)
@@ -412,9 +444,11 @@ scan_tile_sums(const T *__restrict__ in, i64 n, u64 *__restrict__ partial) {
     __shared__ u32 s_warp[kScanThreads / 32 + 1];
     const i64 t0 = (i64)blockIdx.x * kScanTile + (i64)threadIdx.x * kScanItems;
     u32 raw = 0, cap = 0;
+    u32 vv[kScanItems];
+    load_counts(in, t0, n, vv);
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
-        u32 v = load_count(in, t0 + k, n);
+        const u32 v = vv[k];
         raw += v;
         cap += CAP ? (v > 255u ? 255u : v) : 0u;
     }
@@ -470,9 +504,9 @@ scan_write(const T *__restrict__ in, i64 n, const u64 *__restrict__ partial,
     const i64 t0 = (i64)blockIdx.x * kScanTile + (i64)threadIdx.x * kScanItems;
     u32 v[kScanItems];
     u32 raw = 0, cap = 0;
+    load_counts(in, t0, n, v);
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
-        v[k] = load_count(in, t0 + k, n);
         raw += v[k];
         cap += CAP ? (v[k] > 255u ? 255u : v[k]) : 0u;
     }
@@ -480,6 +514,31 @@ scan_write(const T *__restrict__ in, i64 n, const u64 *__restrict__ partial,
     u32 pr = block_exclusive_scan(raw, s_warp, &total) + (u32)partial[2 * (i64)blockIdx.x];
     u32 pc = 0;
     if (CAP) pc = block_exclusive_scan(cap, s_warp, &total) + (u32)partial[2 * (i64)blockIdx.x + 1];
+    const bool full = t0 + kScanItems <= n && (reinterpret_cast<uintptr_t>(out_raw) & 31) == 0 &&
+                      (!CAP || ((reinterpret_cast<uintptr_t>(out_cap) & 31) == 0 &&
+                                (reinterpret_cast<uintptr_t>(out_counts) & 7) == 0));
+    if (full) {
+        // one 32-byte store per output array and thread
+        u32 r[kScanItems], c[kScanItems];
+        u64 cnt8 = 0;
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) {
+            r[k] = pr;
+            pr += v[k];
+            const u32 cc = v[k] > 255u ? 255u : v[k];
+            c[k] = pc;
+            pc += cc;
+            cnt8 |= (u64)cc << (8 * k);
+        }
+        lvx_st256(out_raw + t0, r[0] | ((u64)r[1] << 32), r[2] | ((u64)r[3] << 32), r[4] | ((u64)r[5] << 32),
+                  r[6] | ((u64)r[7] << 32));
+        if (CAP) {
+            lvx_st256(out_cap + t0, c[0] | ((u64)c[1] << 32), c[2] | ((u64)c[3] << 32), c[4] | ((u64)c[5] << 32),
+                      c[6] | ((u64)c[7] << 32));
+            *reinterpret_cast<u64 *>(out_counts + t0) = cnt8;
+        }
+        return;
+    }
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         i64 idx = t0 + k;
@@ -533,10 +592,10 @@ compact_kernel(const lvx_raw_record *__restrict__ grouped, i64 n_raw, const u32 
                int n_bins, int lb, int width, CompactOut o) {
     const i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n_raw) return;
-    const ulonglong2 kq = *reinterpret_cast<const ulonglong2 *>(grouped + r);
-    const u32 lin = grouped[r].lin;
+    u64 key, q, lin64, unused;
+    lvx_ld256(grouped + r, key, q, lin64, unused);
+    const u32 lin = (u32)lin64;
     const u32 n = vox_cnt[lin];
-    const u64 key = kq.x;
     u32 rank = 0;
     if (n > 1) {
         const u32 end = cursor_end[lin];
@@ -544,7 +603,6 @@ compact_kernel(const lvx_raw_record *__restrict__ grouped, i64 n_raw, const u32 
     }
     if (rank >= 255u) return;  // voxelizer.py:442-448 keep the first 255 in curve order
     const i64 dst = (i64)offsets[lin] + rank;
-    const u64 q = kq.y;
     const u32 fi = (u32)(q & 7u), bi = (u32)((q >> 3) & 0xFFFFu);
     const u32 fo = (u32)((q >> 19) & 7u), bo = (u32)((q >> 22) & 0xFFFFu);
     const u32 attr = (u32)((q >> 38) & 0xFFu);
@@ -583,9 +641,11 @@ compact_kernel(const lvx_raw_record *__restrict__ grouped, i64 n_raw, const u32 
     if (o.bin_out) o.bin_out[dst] = (u16)bo;
     if (o.seg_key) o.seg_key[dst] = key;
     if (o.seg_rec) {
-        float4 *rec = reinterpret_cast<float4 *>(o.seg_rec + dst);
-        rec[0] = make_float4(a[0], a[1], a[2], __uint_as_float(attr | (lid << 8)));
-        rec[1] = make_float4(b[0], b[1], b[2], lvx_half_len(a[0], a[1], a[2], b[0], b[1], b[2]));
+        const float hl = lvx_half_len(a[0], a[1], a[2], b[0], b[1], b[2]);
+        lvx_st256(o.seg_rec + dst, (u64)__float_as_uint(a[0]) | ((u64)__float_as_uint(a[1]) << 32),
+                  (u64)__float_as_uint(a[2]) | ((u64)(attr | (lid << 8)) << 32),
+                  (u64)__float_as_uint(b[0]) | ((u64)__float_as_uint(b[1]) << 32),
+                  (u64)__float_as_uint(b[2]) | ((u64)__float_as_uint(hl) << 32));
     }
 }
 
@@ -638,9 +698,7 @@ regroup_kernel(const u64 *__restrict__ in_key, const u64 *__restrict__ in_q,
     if (lin == kNoVoxel) return;  // a reserved slot without a chord
     const u32 slot = atomicAdd(&cursor[lin], 1u);
     // one whole 32-byte sector per record: the scattered write needs no read-modify-write
-    ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(out + slot);
-    dst[0] = make_ulonglong2(in_key[r], in_q[r]);
-    dst[1] = make_ulonglong2((u64)lin, 0ull);
+    lvx_st256(out + slot, in_key[r], in_q[r], (u64)lin, 0ull);
 }
 
 int ilog2i(int n) {
