@@ -135,6 +135,16 @@ int lvx_voxelize_compact(const lvx_raw_record *grouped_d, int64_t n_raw, const u
                          uint8_t *seg_face_out_d, uint16_t *seg_bin_out_d, uint64_t *seg_key_d,
                          lvx_seg_record *seg_rec_d, void *stream);
 
+/* Device-side decode of the packed records (model_io.py:151-179
+ * _decode_records + _bin_centers, the expansion load_vxl does on the host): render records
+ * and, optionally, the reference's per-segment caches straight from (counts, offsets, packed).
+ * err_d = 1 when a record carries a face id > 5 (model_io.py:277-278).  Outputs may be NULL. */
+int lvx_decode_packed(const uint8_t *packed_d, const uint8_t *counts_d, const uint32_t *offsets_d,
+                      const int32_t dims[3], int32_t n_bins, float *seg_a_d, float *seg_b_d,
+                      uint8_t *seg_attr_d, uint8_t *seg_lid_d, int32_t *seg_voxel_d,
+                      uint8_t *seg_face_in_d, uint16_t *seg_bin_in_d, uint8_t *seg_face_out_d,
+                      uint16_t *seg_bin_out_d, lvx_seg_record *seg_rec_d, int32_t *err_d, void *stream);
+
 int lvx_scan_u16(const uint16_t *in_d, int64_t n, uint32_t *out_d, void *scratch_d,
                  void *stream);
 

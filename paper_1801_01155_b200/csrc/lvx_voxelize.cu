@@ -649,6 +649,69 @@ compact_kernel(const lvx_raw_record *__restrict__ grouped, i64 n_raw, const u32 
     }
 }
 
+// Inverse of the packer: one thread per voxel walks its records (model_io.py:151-179,
+// _decode_records + _bin_centers).  A model that arrives as (counts, offsets, packed) --
+// e.g. read from a .vxl file -- gets its render records and, if wanted, the reference's
+// per-segment caches without a host-side expansion.
+__global__ void __launch_bounds__(128)
+decode_packed_kernel(const u8 *__restrict__ packed, const u8 *__restrict__ counts,
+                     const u32 *__restrict__ offsets, i64 n_voxels, int rx, int ry, int n_bins, int lb,
+                     int width, CompactOut o, int *__restrict__ err) {
+    const i64 lin = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (lin >= n_voxels) return;
+    const u32 cnt = counts[lin];
+    if (cnt == 0) return;
+    const i64 base = offsets[lin];
+    const int vx = (int)(lin % rx), vy = (int)((lin / rx) % ry), vz = (int)(lin / ((i64)rx * ry));
+    const int bb = 2 * lb;
+    const u64 bmask = ((u64)1 << bb) - 1;
+    for (u32 sgi = 0; sgi < cnt; ++sgi) {
+        const i64 dst = base + sgi;
+        const u8 *pk = packed + dst * width;
+        u64 value = 0;
+        for (int k = 0; k < width; ++k) value |= (u64)pk[k] << (8 * k);
+        // _field_layout, voxelizer.py:79-89 (LSB first)
+        const u32 fi = (u32)(value & 7u), bi = (u32)((value >> 3) & bmask);
+        const u32 fo = (u32)((value >> (3 + bb)) & 7u), bo = (u32)((value >> (6 + bb)) & bmask);
+        const u32 attr = (u32)((value >> (6 + 2 * bb)) & 0xFFu), lid = (u32)((value >> (14 + 2 * bb)) & 31u);
+        if (fi > 5u || fo > 5u) {
+            *err = 1;  // model_io.py:277-278: segment record with face ID > 5
+            continue;
+        }
+        float a[3], b[3];
+        decode_point(fi, bi, n_bins, lb, vx, vy, vz, a);
+        decode_point(fo, bo, n_bins, lb, vx, vy, vz, b);
+        if (o.seg_a) {
+            o.seg_a[3 * dst] = a[0];
+            o.seg_a[3 * dst + 1] = a[1];
+            o.seg_a[3 * dst + 2] = a[2];
+        }
+        if (o.seg_b) {
+            o.seg_b[3 * dst] = b[0];
+            o.seg_b[3 * dst + 1] = b[1];
+            o.seg_b[3 * dst + 2] = b[2];
+        }
+        if (o.seg_attr) o.seg_attr[dst] = (u8)attr;
+        if (o.seg_lid) o.seg_lid[dst] = (u8)lid;
+        if (o.seg_voxel) {
+            o.seg_voxel[3 * dst] = vx;
+            o.seg_voxel[3 * dst + 1] = vy;
+            o.seg_voxel[3 * dst + 2] = vz;
+        }
+        if (o.face_in) o.face_in[dst] = (u8)fi;
+        if (o.face_out) o.face_out[dst] = (u8)fo;
+        if (o.bin_in) o.bin_in[dst] = (u16)bi;
+        if (o.bin_out) o.bin_out[dst] = (u16)bo;
+        if (o.seg_rec) {
+            const float hl = lvx_half_len(a[0], a[1], a[2], b[0], b[1], b[2]);
+            lvx_st256(o.seg_rec + dst, (u64)__float_as_uint(a[0]) | ((u64)__float_as_uint(a[1]) << 32),
+                      (u64)__float_as_uint(a[2]) | ((u64)(attr | (lid << 8)) << 32),
+                      (u64)__float_as_uint(b[0]) | ((u64)__float_as_uint(b[1]) << 32),
+                      (u64)__float_as_uint(b[2]) | ((u64)__float_as_uint(hl) << 32));
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256)
 provenance_kernel(const u64 *__restrict__ seg_key, i64 n_seg, const u32 *__restrict__ edge_base,
                   const i64 *__restrict__ curve_off, i64 n_curves, int32_t *__restrict__ seg_curve,
@@ -869,6 +932,25 @@ int lvx_voxelize_clip(const double *pts_d, const double *attrs_d, const uint8_t 
     clip_once_kernel<<<(unsigned)lvx_ceil_div(n_points, kClipThreads), kClipThreads, 0, st>>>(
         pts_d, attrs_d, first_d, n_points, dims[0], dims[1], dims[2], n_bins, capacity, vox_cnt_d, raw_key_d,
         raw_q_d, raw_lin_d, reinterpret_cast<unsigned long long *>(n_slots_d), edge_kept_d, err_d);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_decode_packed(const uint8_t *packed_d, const uint8_t *counts_d, const uint32_t *offsets_d,
+                      const int32_t dims[3], int32_t n_bins, float *seg_a_d, float *seg_b_d,
+                      uint8_t *seg_attr_d, uint8_t *seg_lid_d, int32_t *seg_voxel_d,
+                      uint8_t *seg_face_in_d, uint16_t *seg_bin_in_d, uint8_t *seg_face_out_d,
+                      uint16_t *seg_bin_out_d, lvx_seg_record *seg_rec_d, int32_t *err_d, void *stream) {
+    if (int rc = check_dims(dims)) return rc;
+    if (int rc = check_bins(n_bins)) return rc;
+    LVX_REQUIRE(packed_d && counts_d && offsets_d && err_d, "null input");
+    const i64 V = (i64)dims[0] * dims[1] * dims[2];
+    const int lb = ilog2i(n_bins);
+    const int width = (2 * (3 + 2 * lb) + 8 + 5 + 7) / 8;  // record_width, voxelizer.py:70-76
+    CompactOut o = {nullptr,       seg_a_d,        seg_b_d,      seg_attr_d,    seg_lid_d, seg_voxel_d,
+                    seg_face_in_d, seg_face_out_d, seg_bin_in_d, seg_bin_out_d, nullptr,   seg_rec_d};
+    decode_packed_kernel<<<(unsigned)lvx_ceil_div(V, 128), 128, 0, (cudaStream_t)stream>>>(
+        packed_d, counts_d, offsets_d, V, dims[0], dims[1], n_bins, lb, width, o, err_d);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }

@@ -92,6 +92,10 @@ def default_transfer_table() -> np.ndarray:
     return table
 
 
+_DECODED_FIELDS = ("seg_a", "seg_b", "seg_attr", "seg_lid", "seg_voxel", "seg_face_in", "seg_bin_in",
+                   "seg_face_out", "seg_bin_out")
+
+
 def _array_property(name):
     def get(self):
         return self._get_array(name)
@@ -157,13 +161,55 @@ class VoxelModel:
             if d is None:
                 if name in ("seg_curve", "seg_order"):
                     return None  # optional in the reference too
-                raise AttributeError(f"model carries no {name}")
+                if name in _DECODED_FIELDS and self._has("packed"):
+                    self._decode_packed(caches=True)
+                    d = self._dev[name]
+                else:
+                    raise AttributeError(f"model carries no {name}")
             h = d.cpu().numpy()
             dt = np.dtype(_ARRAY_FIELDS[name][0])
             if h.dtype != dt:  # u16/u32 travel as same-width signed torch tensors
                 h = h.view(dt)
             self._host[name] = h
         return h
+
+    def _has(self, name) -> bool:
+        return name in self._host or name in self._dev
+
+    def _decode_packed(self, caches: bool):
+        """Expand (counts, offsets, packed) on the device (lvx_decode_packed; the reference
+        does this on the host when it loads a .vxl file, model_io.py:151-179, 268-297):
+        always the render records, with `caches` also the per-segment cache arrays."""
+        torch = _lib.require_device()
+        S = self.segment_count
+        m = max(S, 1)
+        rec = torch.empty((m, 8), dtype=torch.float32, device="cuda")
+        out = {}
+        if caches:
+            out = dict(seg_a=torch.empty((m, 3), dtype=torch.float32, device="cuda"),
+                       seg_b=torch.empty((m, 3), dtype=torch.float32, device="cuda"),
+                       seg_attr=torch.empty(m, dtype=torch.uint8, device="cuda"),
+                       seg_lid=torch.empty(m, dtype=torch.uint8, device="cuda"),
+                       seg_voxel=torch.empty((m, 3), dtype=torch.int32, device="cuda"),
+                       seg_face_in=torch.empty(m, dtype=torch.uint8, device="cuda"),
+                       seg_bin_in=torch.empty(m, dtype=torch.int16, device="cuda"),
+                       seg_face_out=torch.empty(m, dtype=torch.uint8, device="cuda"),
+                       seg_bin_out=torch.empty(m, dtype=torch.int16, device="cuda"))
+        err = torch.zeros(1, dtype=torch.int32, device="cuda")
+        g = out.get
+        if S:
+            _lib.check(_lib.lib().lvx_decode_packed(
+                _lib.ptr(self.dev("packed")), _lib.ptr(self.dev("counts")), _lib.ptr(self.dev("offsets")),
+                _lib.i32x3(self.spec.dims), C.c_int32(self.spec.bins_per_axis), _lib.ptr(g("seg_a")),
+                _lib.ptr(g("seg_b")), _lib.ptr(g("seg_attr")), _lib.ptr(g("seg_lid")), _lib.ptr(g("seg_voxel")),
+                _lib.ptr(g("seg_face_in")), _lib.ptr(g("seg_bin_in")), _lib.ptr(g("seg_face_out")),
+                _lib.ptr(g("seg_bin_out")), _lib.ptr(rec), _lib.ptr(err), _lib.stream_ptr()))
+            if int(err.item()) != 0:
+                raise ValueError("segment record with face ID > 5")  # model_io.py:277-278
+        for k, v in out.items():
+            if not self._has(k):
+                self._dev[k] = v[:S]
+        return rec
 
     counts = _array_property("counts")
     offsets = _array_property("offsets")
@@ -254,6 +300,9 @@ class VoxelModel:
         st = _lib.stream_ptr()
         d = self._derived
         S = self.segment_count
+        if "seg_rec" not in d and not all(self._has(k) for k in ("seg_a", "seg_b", "seg_attr", "seg_lid")):
+            # only the encoded arrays are there (e.g. a .vxl file): render straight from them
+            d["seg_rec"] = self._decode_packed(caches=False)
         if "seg_rec" not in d:
             rec = torch.empty((max(S, 1), 8), dtype=torch.float32, device="cuda")
             if S:

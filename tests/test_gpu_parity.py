@@ -243,6 +243,31 @@ def test_frame_engines_agree_and_queue_overflow_is_retried(lv, synth):
     assert out["wavefront-small"][2] > 1.0 / 64.0  # the low-opacity frame does not fit the tiny queues
 
 
+def test_model_from_encoded_arrays_only(lv, synth):
+    """a model that arrives as (counts, offsets, packed) only -- what a .vxl
+    file holds -- is decoded on the device (lvx_decode_packed, model_io.py:151-179): caches
+    equal the builder's bit for bit and the frame is byte-identical (tests/test_model_io.py:105-116)."""
+    for dims, n_bins, lines in (((16, 16, 16), 32, synth.helices(50, 40, (16, 16, 16))),
+                                ((10, 12, 9), 128, synth.turbulence(80, 40, (10, 12, 9))),
+                                ((8, 8, 8), 4, synth.wiggles(40, 20, (8, 8, 8)))):
+        m = lv.build_voxel_model(lv.CurveSet.from_flat(*lines), lv.GridSpec(dims, n_bins))
+        enc = lv.VoxelModel(spec=m.spec, counts=m.counts.copy(), offsets=m.offsets.copy(), packed=m.packed.copy(),
+                            transfer_table=m.transfer_table)
+        cam = lv.default_camera(dims, 72, 54)
+        p = lv.RenderParams(base_opacity=0.35, neighbor_mode="on")
+        a, b = lv.render_frame(cam, m, None, None, p), lv.render_frame(cam, enc, None, None, p)  # records only
+        assert np.array_equal(a.image, b.image) and a.stats["intersection_tests"] == b.stats["intersection_tests"]
+        for f in ("seg_a", "seg_b", "seg_attr", "seg_lid", "seg_voxel", "seg_face_in", "seg_bin_in",
+                  "seg_face_out", "seg_bin_out"):
+            assert np.array_equal(getattr(enc, f), getattr(m, f)), f
+        assert np.array_equal(lv.compute_density_level0(enc), lv.compute_density_level0(m))
+    bad = m.packed.copy()
+    bad[0] |= 7  # face_in = 7
+    with pytest.raises(ValueError, match="face ID"):
+        lv.VoxelModel(spec=m.spec, counts=m.counts, offsets=m.offsets, packed=bad,
+                      transfer_table=m.transfer_table).seg_a
+
+
 # --- error behaviour (SURVEY.md 8b) ------------------------------------------------------
 
 def test_error_conventions(lv, synth):
