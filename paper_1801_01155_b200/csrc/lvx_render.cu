@@ -122,6 +122,7 @@ struct PixelState {
 // de-duplication rules and the front-to-back accumulation (:666-670, :719-730) are
 // `accumulate_hit`, run by the ray's own lane in hit order.  The arithmetic and its
 // order are the reference's, so the result is bit-identical to the fused form.
+template <bool GEOM>
 __device__ __forceinline__ void shade_hit(const RenderArgs &A, double ox, double oy, double oz,
                                           double ddx, double ddy, double ddz, const LvxHit &h,
                                           u32 attr, double &scale_out, double &alpha_out) {
@@ -132,7 +133,7 @@ __device__ __forceinline__ void shade_hit(const RenderArgs &A, double ox, double
     if (p.shadow_mode == LVX_SHADOW_CONE) {
         shadow_term = lvx_cone_blocking(px, py, pz, p.light[0], p.light[1], p.light[2], A.oc, gx,
                                         gy, gz, 0.01);
-    } else if (p.shadow_mode == LVX_SHADOW_HARD) {
+    } else if (GEOM && p.shadow_mode == LVX_SHADOW_HARD) {
         const LvxGeomModel G = {A.rx, A.ry, A.rz, A.counts, A.offsets, A.rec, A.nmask};
         if (lvx_geometry_blocked(px + 1e-3 * h.nx, py + 1e-3 * h.ny, pz + 1e-3 * h.nz, p.light[0], p.light[1],
                                  p.light[2], 1e30, G, p.tube_r, p.joints != 0))
@@ -146,7 +147,7 @@ __device__ __forceinline__ void shade_hit(const RenderArgs &A, double ox, double
     } else if (p.ao_mode == LVX_AO_DENSITY) {
         ao_term = lvx_ao_density_point(px, py, pz, h.nx, h.ny, h.nz, p.ao_n_rays, p.ao_radius, 1.0,
                                        A.ao_dirs, A.oc.flat, A.rx, A.ry, A.rz);
-    } else if (p.ao_mode == LVX_AO_HEMISPHERE) {
+    } else if (GEOM && p.ao_mode == LVX_AO_HEMISPHERE) {
         const LvxGeomModel G = {A.rx, A.ry, A.rz, A.counts, A.offsets, A.rec, A.nmask};
         ao_term = lvx_ao_hemisphere_point(px, py, pz, h.nx, h.ny, h.nz, p.ao_n_rays, p.ao_radius, A.ao_dirs, G,
                                           p.tube_r);
@@ -357,7 +358,9 @@ __device__ unsigned long long lvx_stage_clk[32];
 #define LVX_CNT(k, v) do {} while (0)
 #endif
 
-template <bool FOOTPRINT>
+// GEOM: the frame uses geometry secondary rays (hard shadows / hemisphere AO); kept out of
+// the common instantiation, whose register budget is tight
+template <bool FOOTPRINT, bool GEOM>
 __global__ void __launch_bounds__(kThreads, LVX_MIN_BLOCKS)
 render_kernel(const RenderArgs A) {
     constexpr unsigned FULL = 0xFFFFFFFFu;
@@ -816,7 +819,7 @@ render_kernel(const RenderArgs A) {
                         lvx_sphere<true>(ox, oy, oz, rdx, rdy, rdz, (double)cx, (double)cy, (double)cz, tube_r, h);
                     }
                     double scale, alpha;
-                    shade_hit(A, ox, oy, oz, rdx, rdy, rdz, h, __float_as_uint(ra.w) & 0xFFu, scale, alpha);
+                    shade_hit<GEOM>(A, ox, oy, oz, rdx, rdy, rdz, h, __float_as_uint(ra.w) & 0xFFu, scale, alpha);
                     P.s.res[idx][0] = scale;
                     P.s.res[idx][1] = alpha;
                 }
@@ -1048,10 +1051,15 @@ static int render_impl(const lvx_camera *cam, const lvx_model *model, const lvx_
     const i64 warps = (i64)A.n_my_tiles * (tiling->tile_w / 8) * (tiling->tile_h / 4);
     const i64 blocks = lvx_ceil_div(warps, kWarpsPerBlock);
     A.footprint = footprint_d;
-    if (footprint_d)
-        render_kernel<true><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, (cudaStream_t)stream>>>(A);
+    const bool geom = params->shadow_mode == LVX_SHADOW_HARD || params->ao_mode == LVX_AO_HEMISPHERE;
+    if (footprint_d && geom)
+        render_kernel<true, true><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, (cudaStream_t)stream>>>(A);
+    else if (footprint_d)
+        render_kernel<true, false><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, (cudaStream_t)stream>>>(A);
+    else if (geom)
+        render_kernel<false, true><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, (cudaStream_t)stream>>>(A);
     else
-        render_kernel<false><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, (cudaStream_t)stream>>>(A);
+        render_kernel<false, false><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, (cudaStream_t)stream>>>(A);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }

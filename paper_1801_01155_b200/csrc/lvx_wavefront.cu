@@ -39,7 +39,6 @@
 //  * the 1024-hits-per-window cap (`window_overflow`) can only bite in windows whose
 //    candidate count exceeds 1024/3; those are flagged and handled by an exact slow path.
 #include <cooperative_groups.h>
-#include <cooperative_groups/scan.h>
 #include <math_constants.h>
 #include <stdlib.h>
 
@@ -173,14 +172,53 @@ struct WfArgs {
 // sub-queue of the warp that works on flat index f (warp-uniform: f is lane + a multiple of 32)
 __device__ __forceinline__ int warp_queue(u32 f) { return (int)((f >> 5) & (kNQ - 1)); }
 
-// Allocate `n` consecutive entries of sub-queue q for this thread (aggregated over the
-// currently converged lanes).  Returns the global index or kNil when the queue is full.
+// Allocate `n` consecutive entries of sub-queue q for this thread alone.  Returns the global
+// index or kNil when the queue is full.
 __device__ __forceinline__ u32 queue_alloc(u32 *cnt, int q, u32 capq, u32 n, u32 *err, u32 err_bit) {
-    cg::coalesced_group g = cg::coalesced_threads();
-    const u32 pre = cg::exclusive_scan(g, n);
+    const u32 base = atomicAdd(&cnt[q], n);
+    if (base + n > capq) {
+        atomicOr(err, err_bit);
+        return kNil;
+    }
+    return (u32)q * capq + base;
+}
+
+// Allocate `n` consecutive entries for every lane that is converged here (any subset of the
+// warp): the lanes of the subset pass their counts round in lane order, one atomic per
+// subset.  `q` must be uniform over the subset.
+__device__ __forceinline__ u32 queue_alloc_n(u32 *cnt, int q, u32 capq, u32 n, u32 *err, u32 err_bit) {
+    const unsigned mask = __activemask();
+    const int lane = (int)(threadIdx.x & 31);
+    u32 pre = 0, total = 0;
+    for (unsigned m = mask; m; m &= m - 1) {
+        const int src = __ffs((int)m) - 1;
+        const u32 v = __shfl_sync(mask, n, src);
+        if (src < lane) pre += v;
+        total += v;
+    }
+    const int leader = __ffs((int)mask) - 1;
     u32 base = 0;
-    if (g.thread_rank() == g.size() - 1) base = atomicAdd(&cnt[q], pre + n);
-    base = g.shfl(base, g.size() - 1);
+    if (lane == leader) base = atomicAdd(&cnt[q], total);
+    base = __shfl_sync(mask, base, leader);
+    if (base + pre + n > capq) {
+        atomicOr(err, err_bit);
+        return kNil;
+    }
+    return (u32)q * capq + base + pre;
+}
+
+// Allocate a + b entries (a, b in {0, 1}) for every lane that is converged here; one atomic
+// per warp.  `q` must be warp-uniform.  Returns the index of the lane's first entry or kNil.
+__device__ __forceinline__ u32 queue_alloc_bits(u32 *cnt, int q, u32 capq, bool a, bool b, u32 *err, u32 err_bit) {
+    const unsigned mask = __activemask();
+    const unsigned ba = __ballot_sync(mask, a), bb = __ballot_sync(mask, b);
+    const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
+    const u32 total = (u32)(__popc(ba) + __popc(bb)), pre = (u32)(__popc(ba & lt) + __popc(bb & lt));
+    const int leader = __ffs((int)mask) - 1;
+    u32 base = 0;
+    if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(&cnt[q], total);
+    base = __shfl_sync(mask, base, leader);
+    const u32 n = (a ? 1u : 0u) + (b ? 1u : 0u);
     if (base + pre + n > capq) {
         atomicOr(err, err_bit);
         return kNil;
@@ -442,7 +480,7 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_WALK_MINB) wf_walk_kernel(c
             listed |= nm;
             if (fresh == 0) continue;
             const u32 ni = (u32)__popc(fresh);
-            const u32 ib = queue_alloc(A.ctl->item_cnt, q, A.capq_item, ni, &A.ctl->err, 1u);
+            const u32 ib = queue_alloc_n(A.ctl->item_cnt, q, A.capq_item, ni, &A.ctl->err, 1u);
             if (ib != kNil) {
                 u32 j = ib;
                 for (u32 mm = fresh; mm; mm &= mm - 1, ++j) {
@@ -527,15 +565,14 @@ __global__ void __launch_bounds__(kThreadsWf) wf_cand_kernel(const WfArgs A) {
                 }
             }
             if (mk & 1u) {
-                const u32 e = queue_alloc(A.ctl->tube_cnt, q, A.capq_surv, 1u, &A.ctl->err, 2u);
+                const u32 e = queue_alloc_bits(A.ctl->tube_cnt, q, A.capq_surv, true, false, &A.ctl->err, 2u);
                 if (e != kNil) {
                     WfEntry c = {seg, it};
                     A.tube[e] = c;
                 }
             }
             if (mk & 6u) {
-                const u32 ns = (mk & 2u ? 1u : 0u) + (mk & 4u ? 1u : 0u);
-                u32 e = queue_alloc(A.ctl->sph_cnt, q, A.capq_surv, ns, &A.ctl->err, 2u);
+                u32 e = queue_alloc_bits(A.ctl->sph_cnt, q, A.capq_surv, (mk & 2u) != 0, (mk & 4u) != 0, &A.ctl->err, 2u);
                 if (e != kNil) {
                     WfEntry c = {seg, it};
                     if (mk & 2u) A.sph[e++] = c;
@@ -550,6 +587,7 @@ __global__ void __launch_bounds__(kThreadsWf) wf_cand_kernel(const WfArgs A) {
 }
 
 // state-free half of stream_hit (_kernels.py:673-718): shadow term, AO term, alpha, Blinn scale
+template <bool GEOM>
 __device__ __forceinline__ void wf_shade(const WfArgs &A, double ox, double oy, double oz, double ddx,
                                          double ddy, double ddz, const LvxHit &h, u32 attr,
                                          double &scale_out, double &alpha_out) {
@@ -559,7 +597,7 @@ __device__ __forceinline__ void wf_shade(const WfArgs &A, double ox, double oy, 
     double shadow_term = 0.0;
     if (p.shadow_mode == LVX_SHADOW_CONE) {
         shadow_term = lvx_cone_blocking(px, py, pz, p.light[0], p.light[1], p.light[2], A.oc, gx, gy, gz, 0.01);
-    } else if (p.shadow_mode == LVX_SHADOW_HARD) {
+    } else if (GEOM && p.shadow_mode == LVX_SHADOW_HARD) {
         const LvxGeomModel G = {A.rx, A.ry, A.rz, A.counts, A.offsets, A.rec, A.nmask};
         if (lvx_geometry_blocked(px + 1e-3 * h.nx, py + 1e-3 * h.ny, pz + 1e-3 * h.nz, p.light[0], p.light[1],
                                  p.light[2], 1e30, G, p.tube_r, p.joints != 0))
@@ -573,7 +611,7 @@ __device__ __forceinline__ void wf_shade(const WfArgs &A, double ox, double oy, 
     } else if (p.ao_mode == LVX_AO_DENSITY) {
         ao_term = lvx_ao_density_point(px, py, pz, h.nx, h.ny, h.nz, p.ao_n_rays, p.ao_radius, 1.0,
                                        A.ao_dirs, A.oc.flat, A.rx, A.ry, A.rz);
-    } else if (p.ao_mode == LVX_AO_HEMISPHERE) {
+    } else if (GEOM && p.ao_mode == LVX_AO_HEMISPHERE) {
         const LvxGeomModel G = {A.rx, A.ry, A.rz, A.counts, A.offsets, A.rec, A.nmask};
         ao_term = lvx_ao_hemisphere_point(px, py, pz, h.nx, h.ny, h.nz, p.ao_n_rays, p.ao_radius, A.ao_dirs, G,
                                           p.tube_r);
@@ -602,7 +640,7 @@ __device__ __forceinline__ void wf_shade(const WfArgs &A, double ox, double oy, 
 #ifndef LVX_WF_EXACT_MINB
 #define LVX_WF_EXACT_MINB 4
 #endif
-template <int KIND>
+template <int KIND, bool GEOM>
 __global__ void __launch_bounds__(kThreadsWf, LVX_WF_EXACT_MINB) wf_exact_kernel(const WfArgs A, int par) {
     __shared__ QueueView V;
     queue_view_load(V, KIND == 0 ? A.ctl->tube_cnt : A.ctl->sph_cnt, A.capq_surv, A.ctl->err);
@@ -653,7 +691,7 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_EXACT_MINB) wf_exact_kernel
         const u32 rmeta = __float_as_uint(ra.w);
         const u32 attr = rmeta & 0xFFu, lid = (rmeta >> 8) & 31u;
         double scale, alpha;
-        wf_shade(A, ox, oy, oz, rdx, rdy, rdz, h, attr, scale, alpha);
+        wf_shade<GEOM>(A, ox, oy, oz, rdx, rdy, rdz, h, attr, scale, alpha);
         const u32 lin = A.item_lin[c.item];
         const u32 rank = seg - __ldg(A.offsets + lin);  // index in the voxel's list
         WfHit rec;
@@ -670,7 +708,7 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_EXACT_MINB) wf_exact_kernel
         if (j < (u32)kHitSlots) {
             A.hit_slot[(size_t)j * R + place] = rec;
         } else {
-            const u32 e = queue_alloc(A.ctl->hit_cnt, q, A.capq_hit, 1u, &A.ctl->err, 4u);
+            const u32 e = queue_alloc_bits(A.ctl->hit_cnt, q, A.capq_hit, true, false, &A.ctl->err, 4u);
             if (e == kNil) continue;
             rec.next = atomicExch(&A.head[slot], e) & ~kDropped;
             A.hit[e] = rec;
@@ -976,11 +1014,12 @@ __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A
             if (tests) atomicAdd(A.row_stats + 3 * (i64)y + 1, tests);
             if (over) atomicAdd(A.row_stats + 3 * (i64)y + 2, over);
         } else {
-            cg::coalesced_group g = cg::coalesced_threads();
+            const unsigned mask = __activemask();
+            const int leader = __ffs((int)mask) - 1;
             u32 base = 0;
-            if (g.thread_rank() == 0) base = atomicAdd(&A.ctl->n_live[par ^ 1], g.size());
-            base = g.shfl(base, 0);
-            A.live[par ^ 1][base + g.thread_rank()] = slot;
+            if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(&A.ctl->n_live[par ^ 1], (u32)__popc(mask));
+            base = __shfl_sync(mask, base, leader);
+            A.live[par ^ 1][base + __popc(mask & ((1u << (threadIdx.x & 31)) - 1u))] = slot;
         }
     }
 }
@@ -1222,6 +1261,7 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     if (const char *e = getenv("LVX_WF_WN")) A.wn_sched = atoi(e) > 0 ? atoi(e) : A.wn_sched;
 
     const bool debug = getenv("LVX_WF_DEBUG") != nullptr;
+    const bool geom = params->shadow_mode == LVX_SHADOW_HARD || params->ao_mode == LVX_AO_HEMISPHERE;
     cudaStream_t st = (cudaStream_t)stream;
     const int sms = lvx_sm_count();
     const unsigned grid_rays = (unsigned)(sms * 8), grid_q = (unsigned)(sms * 8);
@@ -1247,9 +1287,11 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
             WF_DEBUG_SYNC("walk");
             wf_cand_kernel<<<grid_q, kThreadsWf, 0, st>>>(A);
             WF_DEBUG_SYNC("candidates");
-            wf_exact_kernel<0><<<grid_q, kThreadsWf, 0, st>>>(A, par);
+            if (geom) wf_exact_kernel<0, true><<<grid_q, kThreadsWf, 0, st>>>(A, par);
+            else wf_exact_kernel<0, false><<<grid_q, kThreadsWf, 0, st>>>(A, par);
             WF_DEBUG_SYNC("exact<tube>");
-            if (params->joints) wf_exact_kernel<1><<<grid_q, kThreadsWf, 0, st>>>(A, par);
+            if (params->joints && geom) wf_exact_kernel<1, true><<<grid_q, kThreadsWf, 0, st>>>(A, par);
+            else if (params->joints) wf_exact_kernel<1, false><<<grid_q, kThreadsWf, 0, st>>>(A, par);
             WF_DEBUG_SYNC("exact<sphere>");
             wf_composite_kernel<<<grid_rays, kThreadsWf, 0, st>>>(A, par);
             WF_DEBUG_SYNC("composite");
