@@ -35,6 +35,115 @@ ao_bake_kernel(const u8 *__restrict__ counts, int rx, int ry, int rz, int n_rays
     out[lin] = res;
 }
 
+// Brick version of the bake (used when the halo fits in shared memory).  One block per 8x8x8
+// voxel brick: the level-0 density of the brick plus a halo of ceil(radius)+1 voxels is staged
+// in shared memory (indices clamped to the grid exactly like sample_field_trilinear does), so
+// the 8 loads of every trilinear sample stay on chip.  Occupied voxels are listed; each warp
+// takes one voxel at a time and spreads its rays over the lanes (all lanes busy whatever the
+// occupancy pattern).  The per-ray results are then summed by one lane in lattice order --
+// the reference's float64 summation order (_kernels.py:592-605) -- so the result is
+// bit-identical to the one-thread-per-voxel kernel above.
+constexpr int kBrick = 8;
+constexpr int kBakeWarps = 8;
+
+__device__ __forceinline__ double bake_trilinear(const float *__restrict__ s, int E, int lox, int loy, int loz,
+                                                 int ldx, int ldy, int ldz, double x, double y, double z) {
+    // sample_field_trilinear (_kernels.py:346-383) at scale 1: x / 1.0 - 0.5 == x - 0.5
+    const double qx = x / 1.0 - 0.5, qy = y / 1.0 - 0.5, qz = z / 1.0 - 0.5;
+    const double flx = floor(qx), fly = floor(qy), flz = floor(qz);
+    const double fx = qx - flx, fy = qy - fly, fz = qz - flz;
+    const double hx = (double)(ldx - 1), hy = (double)(ldy - 1), hz = (double)(ldz - 1);
+    const int x0 = (int)fmin(fmax(flx, 0.0), hx) - lox, x1 = (int)fmin(fmax(flx + 1.0, 0.0), hx) - lox;
+    const int y0 = (int)fmin(fmax(fly, 0.0), hy) - loy, y1 = (int)fmin(fmax(fly + 1.0, 0.0), hy) - loy;
+    const int z0 = (int)fmin(fmax(flz, 0.0), hz) - loz, z1 = (int)fmin(fmax(flz + 1.0, 0.0), hz) - loz;
+    const int sy = E, sz = E * E;
+    const double v000 = (double)s[z0 * sz + y0 * sy + x0], v001 = (double)s[z0 * sz + y0 * sy + x1];
+    const double v010 = (double)s[z0 * sz + y1 * sy + x0], v011 = (double)s[z0 * sz + y1 * sy + x1];
+    const double v100 = (double)s[z1 * sz + y0 * sy + x0], v101 = (double)s[z1 * sz + y0 * sy + x1];
+    const double v110 = (double)s[z1 * sz + y1 * sy + x0], v111 = (double)s[z1 * sz + y1 * sy + x1];
+    const double c00 = v000 * (1.0 - fx) + v001 * fx;
+    const double c01 = v010 * (1.0 - fx) + v011 * fx;
+    const double c10 = v100 * (1.0 - fx) + v101 * fx;
+    const double c11 = v110 * (1.0 - fx) + v111 * fx;
+    const double c0 = c00 * (1.0 - fy) + c01 * fy;
+    const double c1 = c10 * (1.0 - fy) + c11 * fy;
+    return c0 * (1.0 - fz) + c1 * fz;
+}
+
+__global__ void __launch_bounds__(kBakeWarps * 32)
+ao_bake_brick_kernel(const u8 *__restrict__ counts, int rx, int ry, int rz, int n_rays, double radius,
+                     double step, const double *__restrict__ dirs, const float *__restrict__ l0, int H,
+                     float *__restrict__ out) {
+    extern __shared__ double s_mem[];
+    const int E = kBrick + 2 * H;
+    double *s_dirs = s_mem;                            // [3 * n_rays]
+    double *s_ray = s_dirs + 3 * n_rays;               // [kBakeWarps][n_rays]
+    float *s_l0 = reinterpret_cast<float *>(s_ray + kBakeWarps * n_rays);  // [E^3]
+    __shared__ unsigned short s_list[kBrick * kBrick * kBrick];
+    __shared__ int s_n;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int bx = blockIdx.x * kBrick, by = blockIdx.y * kBrick, bz = blockIdx.z * kBrick;
+    const int lox = bx - H, loy = by - H, loz = bz - H;
+    if (tid == 0) s_n = 0;
+    for (int k = tid; k < 3 * n_rays; k += blockDim.x) s_dirs[k] = dirs[k];
+    for (int k = tid; k < E * E * E; k += blockDim.x) {
+        const int ix = k % E, iy = (k / E) % E, iz = k / (E * E);
+        const int gx_ = min(max(lox + ix, 0), rx - 1), gy_ = min(max(loy + iy, 0), ry - 1),
+                  gz_ = min(max(loz + iz, 0), rz - 1);
+        s_l0[k] = __ldg(l0 + ((i64)gz_ * ry + gy_) * rx + gx_);
+    }
+    __syncthreads();
+    // list the occupied voxels of the brick; empty ones are written now
+    for (int k = tid; k < kBrick * kBrick * kBrick; k += blockDim.x) {
+        const int x = bx + (k & 7), y = by + ((k >> 3) & 7), z = bz + (k >> 6);
+        if (x >= rx || y >= ry || z >= rz) continue;
+        const i64 lin = x + (i64)rx * (y + (i64)ry * z);
+        if (counts[lin] != 0) s_list[atomicAdd(&s_n, 1)] = (unsigned short)k;
+        else out[lin] = 0.0f;
+    }
+    __syncthreads();
+    const int n_occ = s_n;
+    const double gx = (double)rx, gy = (double)ry, gz = (double)rz;
+    double *my_ray = s_ray + warp * n_rays;
+    for (int e = warp; e < n_occ; e += kBakeWarps) {
+        const int k = s_list[e];
+        const int x = bx + (k & 7), y = by + ((k >> 3) & 7), z = bz + (k >> 6);
+        const double px = (double)x + 0.5, py = (double)y + 0.5, pz = (double)z + 0.5;
+        // orient_frame for the normal (0,0,1) (_kernels.py:555-569): t = (1,0,0), b = (0,1,0)
+        double tf[3], bf[3];
+        lvx_orient_frame(0.0, 0.0, 1.0, tf, bf);
+        for (int r = lane; r < n_rays; r += 32) {
+            const double lx = s_dirs[3 * r], ly = s_dirs[3 * r + 1], lz = s_dirs[3 * r + 2];
+            const double dx = lx * tf[0] + ly * bf[0] + lz * 0.0;
+            const double dy = lx * tf[1] + ly * bf[1] + lz * 0.0;
+            const double dz = lx * tf[2] + ly * bf[2] + lz * 1.0;
+            // density_ray_blocking, _kernels.py:425-445
+            double acc = 0.0, t_cur = step;
+            bool sat = false;
+            while (t_cur <= radius) {
+                const double sx = px + t_cur * dx, sy_ = py + t_cur * dy, sz_ = pz + t_cur * dz;
+                if (sx < 0.0 || sy_ < 0.0 || sz_ < 0.0 || sx > gx || sy_ > gy || sz_ > gz) break;
+                acc += bake_trilinear(s_l0, E, lox, loy, loz, rx, ry, rz, sx, sy_, sz_) * step;
+                if (acc >= 1.0) {
+                    sat = true;
+                    break;
+                }
+                t_cur += step;
+            }
+            my_ray[r] = sat ? 1.0 : (acc < 1.0 ? acc : 1.0);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            double total = 0.0;
+            for (int r = 0; r < n_rays; ++r) total += my_ray[r];
+            double v = total / (double)n_rays;
+            v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+            out[x + (i64)rx * (y + (i64)ry * z)] = (float)v;
+        }
+        __syncwarp();
+    }
+}
+
 __global__ void probe_dda_kernel(double ox, double oy, double oz, double dx, double dy, double dz,
                                  int rx, int ry, int rz, int pad, i64 cap, i64 *out_vox,
                                  double *out_t, i64 *n_out) {
@@ -178,6 +287,23 @@ int lvx_ao_bake(const uint8_t *counts_d, const int32_t dims[3], int32_t n_rays, 
     LVX_REQUIRE(dims[0] >= 1 && dims[1] >= 1 && dims[2] >= 1, "grid dims must be >= 1");
     LVX_REQUIRE(n_rays >= 1 && n_rays <= 8192, "n_rays must be in [1, 8192], got %d", n_rays);
     LVX_REQUIRE(radius > 0.0 && step > 0.0, "radius and step must be positive");
+    {
+        // brick kernel when the halo of the radius of influence fits in shared memory
+        const int H = (int)ceil(radius) + 1;
+        const size_t E = (size_t)kBrick + 2 * (size_t)H;
+        const size_t need = ((size_t)n_rays * 3 + (size_t)kBakeWarps * n_rays) * sizeof(double) + E * E * E * sizeof(float);
+        if (radius < 64.0 && need <= 160 * 1024) {
+            dim3 bgrid((unsigned)lvx_ceil_div(dims[0], kBrick), (unsigned)lvx_ceil_div(dims[1], kBrick),
+                       (unsigned)lvx_ceil_div(dims[2], kBrick));
+            if (need > 48 * 1024)
+                LVX_CUDA_CHECK(cudaFuncSetAttribute(ao_bake_brick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    (int)need));
+            ao_bake_brick_kernel<<<bgrid, kBakeWarps * 32, need, (cudaStream_t)stream>>>(
+                counts_d, dims[0], dims[1], dims[2], n_rays, radius, step, dirs_d, level0_d, H, ao_d);
+            LVX_LAUNCH_CHECK();
+            return LVX_OK;
+        }
+    }
     dim3 grid((unsigned)lvx_ceil_div(dims[0], 4), (unsigned)lvx_ceil_div(dims[1], 4),
               (unsigned)lvx_ceil_div(dims[2], 8));
     const size_t smem = (size_t)n_rays * 3 * sizeof(double);
