@@ -1,4 +1,4 @@
-tag=r1c; out=gpurun_out; mkdir -p $out
+tag=${1:-r1e}; out=gpurun_out; mkdir -p $out
 timeout 600 python bench.py > $out/bench_$tag.json 2> $out/bench_$tag.err; echo "bench rc=$?"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 900 --csv --log-file $out/launches_$tag.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu > $out/ncu_launch_$tag.log 2>&1; echo "ncu launches rc=$?"
