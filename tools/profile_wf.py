@@ -34,7 +34,7 @@ for r in rows[2:]:
         continue  # exactly one frame: from the first wf_begin to the next
     name = d["Kernel Name"].split("(")[0].split("::")[-1]
     if "wf_exact_kernel" in d["Kernel Name"]:
-        name = "wf_exact<%s>" % ("tube" if "<0>" in d["Kernel Name"] or "Li0" in d["Kernel Name"] else "sphere")
+        name = "wf_exact<%s>" % ("tube" if "<0" in d["Kernel Name"].split("wf_exact_kernel")[1][:4] else "sphere")
     e = agg.setdefault(name, collections.defaultdict(float))
     e["n"] += 1
     t = float(d[M["ms"]]) * unit_scale(M["ms"])
