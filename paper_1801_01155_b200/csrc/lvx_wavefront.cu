@@ -166,7 +166,7 @@ struct WfArgs {
     WfHit *hit_slot;  // [kHitSlots][R], indexed by the ray's position in the live list
     u32 *hcnt;        // hits of the ray this iteration
     u32 *win_over;  // [cap_win] overflow of a window (slow path only)
-    int wn_sched, cand_budget, grow_from;
+    int wn_sched, cand_budget, grow_from, grow_bits, wn_shift_max;
 };
 
 // sub-queue of the warp that works on flat index f (warp-uniform: f is lane + a multiple of 32)
@@ -524,66 +524,193 @@ __device__ __forceinline__ bool wf_near_line(float cx, float cy, float cz, float
 // candidates: one thread per (ray, voxel) item: conservative float32 pre-reject of the
 // voxel's segments against the ray
 // ---------------------------------------------------------------------------------------
+// what the pre-reject needs of one item
+struct CandItem {
+    u32 it, cnt, base;
+    float q0x, q0y, q0z, fdx, fdy, fdz, fhx, fhy, fhz;
+};
+
+// Survivors are staged per warp in shared memory (positions from ballots and one shared-
+// memory atomic per converged subset) and flushed to the global queues at warp-converged
+// points with one global atomic and coalesced stores: the round trip of a global atomic is
+// off the inner loop.  Entries that do not fit the stage go to the global queue directly.
+constexpr int kStageTube = 128, kStageSph = 256;
+struct CandStage {
+    WfEntry tube[kThreadsWf / 32][kStageTube];
+    WfEntry sph[kThreadsWf / 32][kStageSph];
+    u32 n_tube[kThreadsWf / 32], n_sph[kThreadsWf / 32];
+};
+
+// all 32 lanes of the warp
+__device__ __forceinline__ void cand_flush(const WfArgs &A, CandStage &S, int warp, int lane, int q) {
+    __syncwarp();
+    const u32 nt = min(S.n_tube[warp], (u32)kStageTube), ns = min(S.n_sph[warp], (u32)kStageSph);
+    if (nt) {
+        u32 base = 0;
+        if (lane == 0) base = atomicAdd(&A.ctl->tube_cnt[q], nt);
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        if (base + nt > A.capq_surv) {
+            if (lane == 0) atomicOr(&A.ctl->err, 2u);
+        } else {
+            for (u32 k = lane; k < nt; k += 32) A.tube[(u32)q * A.capq_surv + base + k] = S.tube[warp][k];
+        }
+    }
+    if (ns) {
+        u32 base = 0;
+        if (lane == 0) base = atomicAdd(&A.ctl->sph_cnt[q], ns);
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        if (base + ns > A.capq_surv) {
+            if (lane == 0) atomicOr(&A.ctl->err, 2u);
+        } else {
+            for (u32 k = lane; k < ns; k += 32) A.sph[(u32)q * A.capq_surv + base + k] = S.sph[warp][k];
+        }
+    }
+    __syncwarp();
+    if (lane == 0) {
+        S.n_tube[warp] = 0;
+        S.n_sph[warp] = 0;
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void cand_segment(const WfArgs &A, CandStage &S, int warp, const CandItem &I, u32 seg,
+                                             const float4 ra, const float4 rb, bool joints, float reach_pt, int q) {
+    const float ax = ra.x - I.fhx, ay = ra.y - I.fhy, az = ra.z - I.fhz;
+    const float bx = rb.x - I.fhx, by = rb.y - I.fhy, bz = rb.z - I.fhz;
+    u32 mk = 0;
+    // the tube AND both joint spheres lie inside the segment's bounding sphere
+    if (wf_near_line(0.5f * (ax + bx), 0.5f * (ay + by), 0.5f * (az + bz), I.q0x, I.q0y, I.q0z, I.fdx, I.fdy, I.fdz,
+                     rb.w + reach_pt)) {
+        // the tube's entry point lies on the ray within tube_r of the segment's axis line:
+        // |w . (d x u)| <= reach |d x u|  (absolute slack >> float32 rounding)
+        const float ux = bx - ax, uy = by - ay, uz = bz - az;
+        const float nx = I.fdy * uz - I.fdz * uy, ny = I.fdz * ux - I.fdx * uz, nz = I.fdx * uy - I.fdy * ux;
+        const float wn = (ax - I.q0x) * nx + (ay - I.q0y) * ny + (az - I.q0z) * nz;
+        if (wn * wn <= reach_pt * reach_pt * (nx * nx + ny * ny + nz * nz) + 1e-6f) mk = 1u;
+        if (joints) {
+            if (wf_near_line(ax, ay, az, I.q0x, I.q0y, I.q0z, I.fdx, I.fdy, I.fdz, reach_pt)) mk |= 2u;
+            if (wf_near_line(bx, by, bz, I.q0x, I.q0y, I.q0z, I.fdx, I.fdy, I.fdz, reach_pt)) mk |= 4u;
+        }
+    }
+    const unsigned act = __activemask();
+    const unsigned bt = __ballot_sync(act, (mk & 1u) != 0);
+    const unsigned ba = __ballot_sync(act, (mk & 2u) != 0), bb = __ballot_sync(act, (mk & 4u) != 0);
+    if ((bt | ba | bb) == 0) return;
+    const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
+    const int leader = __ffs((int)act) - 1;
+    u32 t0 = 0, s0 = 0;
+    if ((int)(threadIdx.x & 31) == leader) {
+        if (bt) t0 = atomicAdd(&S.n_tube[warp], (u32)__popc(bt));
+        if (ba | bb) s0 = atomicAdd(&S.n_sph[warp], (u32)(__popc(ba) + __popc(bb)));
+    }
+    t0 = __shfl_sync(act, t0, leader);
+    s0 = __shfl_sync(act, s0, leader);
+    if (mk & 1u) {
+        const u32 pos = t0 + (u32)__popc(bt & lt);
+        const WfEntry c = {seg, I.it};
+        if (pos < (u32)kStageTube) {
+            S.tube[warp][pos] = c;
+        } else {
+            const u32 e = queue_alloc(A.ctl->tube_cnt, q, A.capq_surv, 1u, &A.ctl->err, 2u);
+            if (e != kNil) A.tube[e] = c;
+        }
+    }
+    if (mk & 6u) {
+        u32 pos = s0 + (u32)(__popc(ba & lt) + __popc(bb & lt));
+        WfEntry c = {seg, I.it};
+        if (mk & 2u) {
+            if (pos < (u32)kStageSph) {
+                S.sph[warp][pos] = c;
+            } else {
+                const u32 e = queue_alloc(A.ctl->sph_cnt, q, A.capq_surv, 1u, &A.ctl->err, 2u);
+                if (e != kNil) A.sph[e] = c;
+            }
+            ++pos;
+        }
+        if (mk & 4u) {
+            c.seg |= 0x80000000u;
+            if (pos < (u32)kStageSph) {
+                S.sph[warp][pos] = c;
+            } else {
+                const u32 e = queue_alloc(A.ctl->sph_cnt, q, A.capq_surv, 1u, &A.ctl->err, 2u);
+                if (e != kNil) A.sph[e] = c;
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kThreadsWf) wf_cand_kernel(const WfArgs A) {
     __shared__ QueueView V;
+    __shared__ CandStage S;
     queue_view_load(V, A.ctl->item_cnt, A.capq_item, A.ctl->err);
     const u32 total = V.pre[kNQ];
     const bool joints = A.p.joints != 0;
     const float reach_pt = (float)A.p.tube_r + kRejectMarginWf;
     const size_t R = A.R;
-    for (u32 f = blockIdx.x * blockDim.x + threadIdx.x; f < total; f += gridDim.x * blockDim.x) {
-        const int q = warp_queue(f);
-        const u32 it = queue_view_index(V, f, A.capq_item);
-        const u32 place = A.item_place[it], lin = A.item_lin[it];
-        const float4 q0 = A.item_q[it];
-        const float fdx = A.fdir[place], fdy = A.fdir[R + place], fdz = A.fdir[2 * R + place];
-        const u32 cnt = __ldg(A.counts + lin);
-        const u32 base = __ldg(A.offsets + lin);
-        const int hz = (int)(lin / (u32)(A.rx * A.ry));
-        const int hy = (int)((lin - (u32)hz * (u32)(A.rx * A.ry)) / (u32)A.rx);
-        const int hx = (int)(lin - (u32)hz * (u32)(A.rx * A.ry) - (u32)hy * (u32)A.rx);
-        const float fhx = (float)hx, fhy = (float)hy, fhz = (float)hz;
-        for (u32 sg = 0; sg < cnt; ++sg) {
-            const u32 seg = base + sg;
-            const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + seg));
-            const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + seg) + 1);
-            const float ax = ra.x - fhx, ay = ra.y - fhy, az = ra.z - fhz;
-            const float bx = rb.x - fhx, by = rb.y - fhy, bz = rb.z - fhz;
-            u32 mk = 0;
-            // the tube AND both joint spheres lie inside the segment's bounding sphere
-            if (wf_near_line(0.5f * (ax + bx), 0.5f * (ay + by), 0.5f * (az + bz), q0.x, q0.y, q0.z, fdx, fdy,
-                             fdz, rb.w + reach_pt)) {
-                // the tube's entry point lies on the ray within tube_r of the segment's axis line:
-                // |w . (d x u)| <= reach |d x u|  (absolute slack >> float32 rounding)
-                const float ux = bx - ax, uy = by - ay, uz = bz - az;
-                const float nx = fdy * uz - fdz * uy, ny = fdz * ux - fdx * uz, nz = fdx * uy - fdy * ux;
-                const float wn = (ax - q0.x) * nx + (ay - q0.y) * ny + (az - q0.z) * nz;
-                if (wn * wn <= reach_pt * reach_pt * (nx * nx + ny * ny + nz * nz) + 1e-6f) mk = 1u;
-                if (joints) {
-                    if (wf_near_line(ax, ay, az, q0.x, q0.y, q0.z, fdx, fdy, fdz, reach_pt)) mk |= 2u;
-                    if (wf_near_line(bx, by, bz, q0.x, q0.y, q0.z, fdx, fdy, fdz, reach_pt)) mk |= 4u;
-                }
-            }
-            if (mk & 1u) {
-                const u32 e = queue_alloc_bits(A.ctl->tube_cnt, q, A.capq_surv, true, false, &A.ctl->err, 2u);
-                if (e != kNil) {
-                    WfEntry c = {seg, it};
-                    A.tube[e] = c;
-                }
-            }
-            if (mk & 6u) {
-                u32 e = queue_alloc_bits(A.ctl->sph_cnt, q, A.capq_surv, (mk & 2u) != 0, (mk & 4u) != 0, &A.ctl->err, 2u);
-                if (e != kNil) {
-                    WfEntry c = {seg, it};
-                    if (mk & 2u) A.sph[e++] = c;
-                    if (mk & 4u) {
-                        c.seg |= 0x80000000u;
-                        A.sph[e] = c;
-                    }
-                }
+    const u32 stride = gridDim.x * blockDim.x;
+    const u32 plane = (u32)A.rx * (u32)A.ry;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        S.n_tube[warp] = 0;
+        S.n_sph[warp] = 0;
+    }
+    __syncwarp();
+    int q = 0;
+    // two items per thread and round (the loop bound is warp-uniform: the stage is flushed
+    // by the whole warp)
+    for (u32 f0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); f0 < total; f0 += 2 * stride) {
+        q = warp_queue(f0);
+        if (S.n_tube[warp] > (u32)kStageTube / 2 || S.n_sph[warp] > (u32)kStageSph / 2) cand_flush(A, S, warp, lane, q);
+        const u32 f = f0 + (u32)lane;
+        CandItem I[2];
+        u32 lin[2], place[2];
+        float4 q0[2];
+        bool have[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const u32 fk = f + (u32)k * stride;
+            have[k] = fk < total;
+            I[k].it = queue_view_index(V, have[k] ? fk : 0u, A.capq_item);
+            place[k] = A.item_place[I[k].it];
+            lin[k] = A.item_lin[I[k].it];
+            q0[k] = A.item_q[I[k].it];
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            I[k].fdx = A.fdir[place[k]];
+            I[k].fdy = A.fdir[R + place[k]];
+            I[k].fdz = A.fdir[2 * R + place[k]];
+            I[k].cnt = have[k] ? __ldg(A.counts + lin[k]) : 0u;
+            I[k].base = __ldg(A.offsets + lin[k]);
+        }
+        float4 ra[2], rb[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            // (a listed voxel holds at least one record)
+            ra[k] = __ldg(reinterpret_cast<const float4 *>(A.rec + I[k].base));
+            rb[k] = __ldg(reinterpret_cast<const float4 *>(A.rec + I[k].base) + 1);
+            const u32 hz = lin[k] / plane, hy = (lin[k] - hz * plane) / (u32)A.rx, hx = lin[k] - hz * plane - hy * (u32)A.rx;
+            I[k].fhx = (float)hx;
+            I[k].fhy = (float)hy;
+            I[k].fhz = (float)hz;
+            I[k].q0x = q0[k].x;
+            I[k].q0y = q0[k].y;
+            I[k].q0z = q0[k].z;
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            if (I[k].cnt == 0) continue;
+            cand_segment(A, S, warp, I[k], I[k].base, ra[k], rb[k], joints, reach_pt, q);
+            for (u32 sg = 1; sg < I[k].cnt; ++sg) {
+                const u32 seg = I[k].base + sg;
+                const float4 a4 = __ldg(reinterpret_cast<const float4 *>(A.rec + seg));
+                const float4 b4 = __ldg(reinterpret_cast<const float4 *>(A.rec + seg) + 1);
+                cand_segment(A, S, warp, I[k], seg, a4, b4, joints, reach_pt, q);
             }
         }
+        __syncwarp();
     }
+    cand_flush(A, S, warp, lane, q);
 }
 
 // state-free half of stream_hit (_kernels.py:673-718): shadow term, AO term, alpha, Blinn scale
@@ -1036,7 +1163,7 @@ __global__ void wf_next_kernel(const WfArgs A, int par, int it_next) {
     if (t == 0) {
         A.ctl->n_live[par] = 0;
         const u32 live = A.ctl->n_live[par ^ 1];
-        u32 wn = (u32)A.wn_sched << (it_next < 4 ? it_next : 4);
+        u32 wn = (u32)A.wn_sched << (it_next < A.wn_shift_max ? it_next : A.wn_shift_max);
         const u32 fit = live ? A.cap_win / live : A.cap_win;
         if (wn > fit) wn = fit;
         if (wn < 1) wn = 1;
@@ -1044,7 +1171,8 @@ __global__ void wf_next_kernel(const WfArgs A, int par, int it_next) {
         // later iterations hold few rays, all with low hit rates: let them run further
         {
             const int g = it_next - A.grow_from;
-            A.ctl->budget = (u32)A.cand_budget << (g < 0 ? 0 : (g < 8 ? g : 8));
+            const int sh = g < 0 ? 0 : g * A.grow_bits;
+            A.ctl->budget = (u32)A.cand_budget << (sh < 12 ? sh : 12);
         }
     }
 }
@@ -1256,6 +1384,10 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     A.wn_sched = 8;
     A.cand_budget = 192;
     A.grow_from = 4;
+    A.grow_bits = 1;
+    A.wn_shift_max = 4;
+    if (const char *e = getenv("LVX_WF_GROW_BITS")) A.grow_bits = atoi(e);
+    if (const char *e = getenv("LVX_WF_WN_SHIFT")) A.wn_shift_max = atoi(e);
     if (const char *e = getenv("LVX_WF_BUDGET")) A.cand_budget = atoi(e) > 0 ? atoi(e) : A.cand_budget;
     if (const char *e = getenv("LVX_WF_GROW")) A.grow_from = atoi(e);
     if (const char *e = getenv("LVX_WF_WN")) A.wn_sched = atoi(e) > 0 ? atoi(e) : A.wn_sched;
