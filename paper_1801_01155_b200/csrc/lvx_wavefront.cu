@@ -400,6 +400,62 @@ __global__ void __launch_bounds__(kThreadsWf) wf_init_kernel(const WfArgs A) {
 // walk: one thread per live ray
 // ---------------------------------------------------------------------------------------
 
+// The windows that bring fresh voxels are staged per warp in shared memory and expanded to
+// items when the warp is converged again (end of the rays' batches): one global atomic and
+// one scan per warp instead of an allocation round trip inside the walk (neighbour mode).
+constexpr int kWalkStage = 176;
+struct __align__(16) WalkRec {
+    u32 place, fresh;
+    unsigned long long cell;  // (x + 1) | (y + 1) << 20 | (z + 1) << 40
+    float qx, qy, qz, pad;    // ray point at the window start, window-local
+};
+static_assert(sizeof(WalkRec) == 32, "staged window record is 32 bytes");
+struct WalkStage {
+    WalkRec rec[kThreadsWf / 32][kWalkStage];
+    u32 n[kThreadsWf / 32];
+};
+
+// all 32 lanes of the warp
+__device__ __forceinline__ void walk_flush(const WfArgs &A, WalkStage &S, int warp, int lane, int q) {
+    __syncwarp();
+    const u32 n = min(S.n[warp], (u32)kWalkStage);
+    if (n) {
+        u32 mine = 0;
+        for (u32 r = lane; r < n; r += 32) mine += (u32)__popc(S.rec[warp][r].fresh);
+        u32 inc = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        const u32 total = __shfl_sync(0xFFFFFFFFu, inc, 31);
+        u32 base = 0;
+        if (lane == 31) base = atomicAdd(&A.ctl->item_cnt[q], total);
+        base = __shfl_sync(0xFFFFFFFFu, base, 31);
+        if (base + total > A.capq_item) {
+            if (lane == 31) atomicOr(&A.ctl->err, 1u);
+        } else {
+            u32 j = (u32)q * A.capq_item + base + inc - mine;
+            for (u32 r = lane; r < n; r += 32) {
+                const WalkRec w = S.rec[warp][r];
+                const int wx = (int)(w.cell & 0xFFFFFu) - 1, wy = (int)((w.cell >> 20) & 0xFFFFFu) - 1,
+                          wz = (int)(w.cell >> 40) - 1;
+                for (u32 mm = w.fresh; mm; mm &= mm - 1, ++j) {
+                    const int b = __ffs((int)mm) - 1;
+                    const int bz_ = b / 9, by_ = (b - 9 * bz_) / 3, bx_ = b - 9 * bz_ - 3 * by_;
+                    A.item_place[j] = w.place;
+                    A.item_lin[j] = (u32)((wx + bx_ - 1) + A.rx * ((wy + by_ - 1) + A.ry * (wz + bz_ - 1)));
+                    // voxel-local float32 frame for the (conservative) pre-reject
+                    A.item_q[j] = make_float4(w.qx - (float)(bx_ - 1), w.qy - (float)(by_ - 1), w.qz - (float)(bz_ - 1), 0.0f);
+                }
+            }
+        }
+    }
+    __syncwarp();
+    if (lane == 0) S.n[warp] = 0;
+    __syncwarp();
+}
+
 #ifndef LVX_WF_WALK_MINB
 #define LVX_WF_WALK_MINB 4
 #endif
@@ -414,8 +470,15 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_WALK_MINB) wf_walk_kernel(c
     const double cull = p.tube_r + kCullMarginWf;
     const double ox = A.cam.o[0], oy = A.cam.o[1], oz = A.cam.o[2];
     const size_t R = A.R;
-    for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n_live; i += gridDim.x * blockDim.x) {
-        const int q = warp_queue(i);
+    __shared__ WalkStage S;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) S.n[warp] = 0;
+    __syncwarp();
+    // (the loop bound is warp-uniform: the stage is flushed by the whole warp)
+    for (u32 i0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); i0 < n_live; i0 += gridDim.x * blockDim.x) {
+        const u32 i = i0 + (u32)lane;
+        const int q = warp_queue(i0);
+        if (i < n_live) {
         const u32 slot = A.live[par][i];
         WfRayWalk rw = A.rw[slot];
         const double ddx = rw.dir[0], ddy = rw.dir[1], ddz = rw.dir[2];
@@ -479,6 +542,23 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_WALK_MINB) wf_walk_kernel(c
             const u32 fresh = nm & ~listed;
             listed |= nm;
             if (fresh == 0) continue;
+            if (neighbor) {
+                const u32 pos = atomicAdd(&S.n[warp], 1u);
+                if (pos < (u32)kWalkStage) {
+                    WalkRec wr;
+                    wr.place = i;
+                    wr.fresh = fresh;
+                    wr.cell = (unsigned long long)(u32)(wx + 1) | ((unsigned long long)(u32)(wy + 1) << 20) |
+                              ((unsigned long long)(u32)(wz + 1) << 40);
+                    wr.qx = (float)(p0x - (double)wx);
+                    wr.qy = (float)(p0y - (double)wy);
+                    wr.qz = (float)(p0z - (double)wz);
+                    wr.pad = 0.0f;
+                    S.rec[warp][pos] = wr;
+                    continue;
+                }
+            }
+            // (own-voxel mode, or the stage is full: reserve in the global queue directly)
             const u32 ni = (u32)__popc(fresh);
             const u32 ib = queue_alloc_n(A.ctl->item_cnt, q, A.capq_item, ni, &A.ctl->err, 1u);
             if (ib != kNil) {
@@ -507,6 +587,8 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_WALK_MINB) wf_walk_kernel(c
         A.fdir[2 * R + i] = (float)ddz;
         A.span[i] = span0;
         A.span[R + i] = dda.t_cur;
+        }
+        walk_flush(A, S, warp, lane, q);
     }
 }
 
