@@ -1087,30 +1087,117 @@ __device__ __forceinline__ bool wf_composite_one(const WfArgs &A, WfTables &T, W
     return S.acc[3] >= tau;
 }
 
+constexpr int kLight = 12;  // up to this many hits a ray orders by itself; more are ranked by its warp
+
+struct SortStage {
+    double t[kThreadsWf / 32][kSortCap];
+    unsigned long long k[kThreadsWf / 32][kSortCap];
+    u32 ref[kThreadsWf / 32][kSortCap], out[kThreadsWf / 32][kSortCap];
+    u32 n[kThreadsWf / 32];
+};
+
 __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A, int par) {
+    constexpr unsigned FULL = 0xFFFFFFFFu;
+    __shared__ SortStage Q;
     const u32 n_live = A.ctl->err ? 0u : A.ctl->n_live[par];
     const u32 wn = A.ctl->wn;
     const size_t R = A.R;
     const double tau = A.p.tau;
-    for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n_live; i += gridDim.x * blockDim.x) {
-        const u32 slot = A.live[par][i];
-        const u32 nhit = A.hcnt[slot];
-        const u32 fl = A.rw[slot].flags;
-        bool finished = !(fl & 1);  // the walk is over: this was the last batch
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // (the loop bound is warp-uniform: rays with many hits are ordered by the whole warp)
+    for (u32 i0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); i0 < n_live; i0 += gridDim.x * blockDim.x) {
+        const u32 i = i0 + (u32)lane;
+        const bool valid = i < n_live;
+        u32 slot = 0, nhit = 0, fl = 1;
+        if (valid) {
+            slot = A.live[par][i];
+            nhit = A.hcnt[slot];
+            fl = A.rw[slot].flags;
+        }
+        bool finished = valid && !(fl & 1);  // the walk is over: this was the last batch
         bool terminated = false;
         unsigned long long tests = 0, over = 0;
-        WfRayPix rp;
+        const bool big = (fl & 2) != 0;
+        const u32 w0 = i * wn;
+        u32 nw = 0;
+        const WfWindow *wins = A.win + w0;
+        WfRayHits H = {A, i, nhit < (u32)kHitSlots ? nhit : (u32)kHitSlots, kNil};
         if (nhit) {
             A.hcnt[slot] = 0;
-            WfRayHits H = {A, i, nhit < (u32)kHitSlots ? nhit : (u32)kHitSlots, kNil};
             if (nhit > (u32)kHitSlots) {
                 H.head = A.head[slot];
                 A.head[slot] = kNil;
             }
-            const bool big = (fl & 2) != 0;
-            const u32 w0 = i * wn, nw = A.rw[slot].nwin;
-            const WfWindow *wins = A.win + w0;
+            nw = A.rw[slot].nwin;
             if (big) wf_apply_window_cap(A, H, wins, nw, w0);
+        }
+        // ---- order the hits: (t_in, key2) ---------------------------------------------------
+        u32 order[kSortCap];
+        int n = 0;
+        if (nhit && nhit <= (u32)kLight) {
+            // few hits: insertion sort by the ray's own thread
+            double s_t[kLight];
+            unsigned long long s_k[kLight];
+            for (u32 ref = H.first(); ref != kNil; ref = H.next(ref)) {
+                const WfHit *hp = H.at(ref);
+                if (big && (hp->next & kDropped)) continue;  // dropped by the window cap
+                const double2 v = *reinterpret_cast<const double2 *>(hp);
+                const double t = v.x;
+                const unsigned long long k2 = (unsigned long long)__double_as_longlong(v.y);
+                int pos = n++;
+                while (pos > 0 && wf_before(t, k2, s_t[pos - 1], s_k[pos - 1])) {
+                    s_t[pos] = s_t[pos - 1];
+                    s_k[pos] = s_k[pos - 1];
+                    order[pos] = order[pos - 1];
+                    --pos;
+                }
+                s_t[pos] = t;
+                s_k[pos] = k2;
+                order[pos] = ref;
+            }
+        }
+        __syncwarp();
+        // many hits: the warp ranks them together, one such ray at a time
+        unsigned hm = __ballot_sync(FULL, nhit > (u32)kLight && nhit <= (u32)kSortCap);
+        while (hm) {
+            const int L = __ffs((int)hm) - 1;
+            hm &= hm - 1;
+            if (lane == L) {
+                u32 m = 0;
+                for (u32 ref = H.first(); ref != kNil; ref = H.next(ref)) {
+                    if (big && (H.at(ref)->next & kDropped)) continue;
+                    Q.ref[warp][m++] = ref;
+                }
+                Q.n[warp] = m;
+            }
+            __syncwarp();
+            const u32 m = Q.n[warp];
+            const u32 placeL = __shfl_sync(FULL, i, L);
+            for (u32 j = lane; j < m; j += 32) {
+                const u32 ref = Q.ref[warp][j];
+                const WfHit *hp = ref < (u32)kHitSlots ? A.hit_slot + (size_t)ref * R + placeL : A.hit + (ref - kHitSlots);
+                const double2 v = *reinterpret_cast<const double2 *>(hp);
+                Q.t[warp][j] = v.x;
+                Q.k[warp][j] = (unsigned long long)__double_as_longlong(v.y);
+            }
+            __syncwarp();
+            for (u32 j = lane; j < m; j += 32) {
+                const double t = Q.t[warp][j];
+                const unsigned long long k2 = Q.k[warp][j];
+                u32 rank = 0;
+                for (u32 q = 0; q < m; ++q) rank += wf_before(Q.t[warp][q], Q.k[warp][q], t, k2) ? 1u : 0u;
+                Q.out[warp][rank] = Q.ref[warp][j];  // (keys are unique: a permutation)
+            }
+            __syncwarp();
+            if (lane == L) {
+                for (u32 j = 0; j < m; ++j) order[j] = Q.out[warp][j];
+                n = (int)m;
+            }
+            __syncwarp();
+        }
+        // ---- composite ----------------------------------------------------------------------
+        WfRayPix rp;
+        if (nhit) {
             WfPixel S;
             rp = A.rp[slot];
             S.acc[0] = rp.acc[0];
@@ -1124,30 +1211,8 @@ __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A
             WfTables T = {A, slot, rp.ovf};
             double term_t = 0.0;
             if (nhit <= (u32)kSortCap) {
-                // gather the keys, order them locally (insertion sort on (t_in, key2))
-                double s_t[kSortCap];
-                unsigned long long s_k[kSortCap];
-                u32 s_ref[kSortCap];
-                int n = 0;
-                for (u32 ref = H.first(); ref != kNil; ref = H.next(ref)) {
-                    const WfHit *hp = H.at(ref);
-                    if (big && (hp->next & kDropped)) continue;  // dropped by the window cap
-                    const double2 v = *reinterpret_cast<const double2 *>(hp);
-                    const double t = v.x;
-                    const unsigned long long k2 = (unsigned long long)__double_as_longlong(v.y);
-                    int pos = n++;
-                    while (pos > 0 && wf_before(t, k2, s_t[pos - 1], s_k[pos - 1])) {
-                        s_t[pos] = s_t[pos - 1];
-                        s_k[pos] = s_k[pos - 1];
-                        s_ref[pos] = s_ref[pos - 1];
-                        --pos;
-                    }
-                    s_t[pos] = t;
-                    s_k[pos] = k2;
-                    s_ref[pos] = ref;
-                }
                 for (int j = 0; j < n; ++j) {
-                    const WfHit h = *H.at(s_ref[j]);
+                    const WfHit h = *H.at(order[j]);
                     if (wf_composite_one(A, T, S, h, tau)) {
                         terminated = true;
                         term_t = h.t_in;
@@ -1155,7 +1220,7 @@ __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A
                     }
                 }
             } else {
-                // more hits than the local buffer holds: selection instead of sorting --
+                // more hits than the buffers hold: selection instead of sorting --
                 // repeatedly take the smallest key after the last composited one
                 bool have_last = false;
                 double lt = 0.0;
@@ -1222,14 +1287,15 @@ __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A
             const u32 y = rp.pix >> 16;
             if (tests) atomicAdd(A.row_stats + 3 * (i64)y + 1, tests);
             if (over) atomicAdd(A.row_stats + 3 * (i64)y + 2, over);
-        } else {
+        } else if (valid) {
             const unsigned mask = __activemask();
             const int leader = __ffs((int)mask) - 1;
             u32 base = 0;
-            if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(&A.ctl->n_live[par ^ 1], (u32)__popc(mask));
+            if (lane == leader) base = atomicAdd(&A.ctl->n_live[par ^ 1], (u32)__popc(mask));
             base = __shfl_sync(mask, base, leader);
-            A.live[par ^ 1][base + __popc(mask & ((1u << (threadIdx.x & 31)) - 1u))] = slot;
+            A.live[par ^ 1][base + __popc(mask & ((1u << lane) - 1u))] = slot;
         }
+        __syncwarp();
     }
 }
 

@@ -2,7 +2,8 @@
 usage: python tools/ncu_src.py report.ncu-rep kernel-regex [top_n]"""
 import csv, subprocess, sys
 rep, kre = sys.argv[1], sys.argv[2]; top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
-out = subprocess.run(["ncu", "-i", rep, "-k", "regex:" + kre, "--page", "source", "--csv", "--print-source", "sass,cuda"],
+skip = sys.argv[4] if len(sys.argv) > 4 else "0"
+out = subprocess.run(["ncu", "-i", rep, "-k", "regex:" + kre, "-s", skip, "-c", "1", "--page", "source", "--csv", "--print-source", "sass,cuda"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 cur = None; data = []; hdr = None
