@@ -1087,7 +1087,10 @@ __device__ __forceinline__ bool wf_composite_one(const WfArgs &A, WfTables &T, W
     return S.acc[3] >= tau;
 }
 
-constexpr int kLight = 12;  // up to this many hits a ray orders by itself; more are ranked by its warp
+#ifndef LVX_WF_LIGHT
+#define LVX_WF_LIGHT 12
+#endif
+constexpr int kLight = LVX_WF_LIGHT;  // up to this many hits a ray orders by itself; more are ranked by its warp
 
 struct SortStage {
     double t[kThreadsWf / 32][kSortCap];
@@ -1531,7 +1534,7 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     A.hcnt = (u32 *)(base + L.hcnt);
     A.wn_sched = 8;
     A.cand_budget = 192;
-    A.grow_from = 4;
+    A.grow_from = 24;  // (growing earlier does not pay: the late iterations are cheap, over-scanning is not)
     A.grow_bits = 1;
     A.wn_shift_max = 4;
     if (const char *e = getenv("LVX_WF_GROW_BITS")) A.grow_bits = atoi(e);
