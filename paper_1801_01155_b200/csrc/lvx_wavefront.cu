@@ -166,7 +166,7 @@ struct WfArgs {
     WfHit *hit_slot;  // [kHitSlots][R], indexed by the ray's position in the live list
     u32 *hcnt;        // hits of the ray this iteration
     u32 *win_over;  // [cap_win] overflow of a window (slow path only)
-    int wn_sched, cand_budget, grow_from, grow_bits, wn_shift_max;
+    int wn_sched, cand_budget, grow_from, grow_bits, wn_shift_max, tail_rays, tail_bits;
 };
 
 // sub-queue of the warp that works on flat index f (warp-uniform: f is lane + a multiple of 32)
@@ -1322,7 +1322,9 @@ __global__ void wf_next_kernel(const WfArgs A, int par, int it_next) {
         // later iterations hold few rays, all with low hit rates: let them run further
         {
             const int g = it_next - A.grow_from;
-            const int sh = g < 0 ? 0 : g * A.grow_bits;
+            int sh = g < 0 ? 0 : g * A.grow_bits;
+            // the last few thousand rays: finish them in few iterations (their over-scan is noise)
+            if (live < (u32)A.tail_rays) sh += A.tail_bits;
             A.ctl->budget = (u32)A.cand_budget << (sh < 12 ? sh : 12);
         }
     }
@@ -1536,6 +1538,10 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     A.cand_budget = 192;
     A.grow_from = 24;  // (growing earlier does not pay: the late iterations are cheap, over-scanning is not)
     A.grow_bits = 1;
+    A.tail_rays = 0;
+    A.tail_bits = 4;
+    if (const char *e = getenv("LVX_WF_TAIL_RAYS")) A.tail_rays = atoi(e);
+    if (const char *e = getenv("LVX_WF_TAIL_BITS")) A.tail_bits = atoi(e);
     A.wn_shift_max = 4;
     if (const char *e = getenv("LVX_WF_GROW_BITS")) A.grow_bits = atoi(e);
     if (const char *e = getenv("LVX_WF_WN_SHIFT")) A.wn_shift_max = atoi(e);
