@@ -1126,6 +1126,12 @@ __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A
         const WfWindow *wins = A.win + w0;
         WfRayHits H = {A, i, nhit < (u32)kHitSlots ? nhit : (u32)kHitSlots, kNil};
         if (nhit) {
+            // the hit records sit in kHitSlots different planes: fetch them all at once, the
+            // ordering loop below then reads them from cache one after the other
+#pragma unroll
+            for (int j = 0; j < kHitSlots; ++j)
+                if ((u32)j < nhit) asm volatile("prefetch.global.L1 [%0];" ::"l"(A.hit_slot + (size_t)j * R + i));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(A.rp + slot));
             A.hcnt[slot] = 0;
             if (nhit > (u32)kHitSlots) {
                 H.head = A.head[slot];
