@@ -297,7 +297,8 @@ struct BlockPool {
             u32 sv_seg[kSurvCap];      // survivor ring
             u32 sv_lin[kSurvCap];
             u16 it_key[kItemCap];      // owner thread << 5 | neighbour bit
-            u16 sv_meta[kSurvCap];     // in: primitive mask 3 | owner << 8; out: owned-hit mask 3 | lid << 3 | owner << 8
+            u16 sv_meta[kSurvCap];     // primitive mask 3 | owner << 8
+            u16 sv_hit[kSurvCap];      // exact stage's result: owned-hit mask 3 | lid << 3 | owner << 8
             u8 o_first[kThreads], o_last[kThreads];
         } g;
         struct {                       // stage S
@@ -705,8 +706,8 @@ render_kernel(const RenderArgs A) {
                             hits |= 4u;
                             P.g.res[tid][2] = h.t_in;
                         }
-                        // (the owner bits stay where the neighbours read them)
-                        P.g.sv_meta[e] = (u16)(hits | (((__float_as_uint(ra.w) >> 8) & 31u) << 3) | (im & 0xFF00u));
+                        // (a separate array: the neighbours read sv_meta's owner bits at the same time)
+                        P.g.sv_hit[e] = (u16)(hits | (((__float_as_uint(ra.w) >> 8) & 31u) << 3) | (im & 0xFF00u));
                     }
                     __syncthreads();
                     LVX_CLK(3);
@@ -723,7 +724,7 @@ render_kernel(const RenderArgs A) {
                             while (hbits == 0 && j <= last) {
                                 eb = j;
                                 e = (sv_head + j) & (kSurvCap - 1);
-                                om = P.g.sv_meta[e];
+                                om = P.g.sv_hit[e];
                                 hbits = om & 7u;
                                 ++j;
                             }
