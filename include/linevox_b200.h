@@ -40,7 +40,7 @@ extern "C" {
 #define LVX_OPACITY_DISTANCE 2
 #define LVX_SHADOW_NONE 0
 #define LVX_SHADOW_HARD 1     /* geometry shadow rays (needs the neighbour grids) */
-#define LVX_SHADOW_REPLINES 2 /* not built (SURVEY 8f "next") -> LVX_E_INVALID */
+#define LVX_SHADOW_REPLINES 2 /* representative-line shadow rays (needs lvx_lod.rep) */
 #define LVX_SHADOW_CONE 3
 #define LVX_AO_NONE 0
 #define LVX_AO_HEMISPHERE 1 /* geometry hemisphere rays (needs the neighbour grids + lattice) */
@@ -222,6 +222,18 @@ typedef struct {
     double ao_radius;
 } lvx_params;
 
+/* One level of the representative-line field (lod.py:61-79 RepLevel + _rep_args,
+ * raycast.py:391-402): one optional line per voxel of the grid coarsened `level` times. */
+typedef struct {
+    const uint8_t *valid_d; /* u8[V_level] */
+    const float *a_d;       /* f32[V_level,3] grid units */
+    const float *b_d;
+    const float *w_d;       /* f32[V_level] summed member length */
+    int32_t dims[3];        /* ceil(grid / 2^level) */
+    int32_t _pad;
+    double size;            /* 2^level */
+} lvx_replines;
+
 typedef struct {
     const float *oct_flat_d;           /* flat octree (nullable when unused) */
     int64_t oct_off[LVX_MAX_LEVELS + 1];
@@ -229,6 +241,7 @@ typedef struct {
     int32_t n_levels, _pad;
     const float *ao_flat_d;            /* baked AO field f32[V] (nullable) */
     const double *ao_dirs_d;           /* f64[ao_n_rays,3] hemisphere lattice (nullable) */
+    lvx_replines rep;                  /* level used by shadow_mode = LVX_SHADOW_REPLINES (valid_d nullable) */
 } lvx_lod;
 
 /* Screen partition for multi-GPU: the image is cut into tile_w x tile_h pixel
@@ -312,6 +325,23 @@ int lvx_probe_cone(const lvx_lod *lod, const double *pts_d, const double light[3
 int lvx_probe_ao_density(const lvx_lod *lod, const double *pts_d, const double *normals_d,
                          int32_t n_rays, double radius, double step, const double *dirs_d,
                          int64_t n, double *out_d, void *stream);
+
+/* Representative lines.
+ * lvx_rep_level: one level of build_rep_lines (lod.py:224-284): every parent voxel averages
+ * its members -- level 1: the segments of its 2x2x2 child voxels (counts/offsets/seg_rec of
+ * the model, c_valid/c_a/c_b/c_w NULL); level >= 2: the representatives of the level below
+ * (seg_rec NULL) -- with the flip rule and face-bin snap of representative_line (:141-169)
+ * and, if `adjacency`, the three passes of _adjacency_snap (:176-221).  child_dims is the
+ * grid of the level below; outputs cover ceil(child_dims / 2).
+ * lvx_probe_replines: _kernels.replines_ray_blocked (_kernels.py:498-538), the kernel behind
+ * illumination.replines_shadow (illumination.py:115-139); out[i] = 1 when blocked. */
+int lvx_rep_level(const int32_t child_dims[3], const uint8_t *c_counts_d, const uint32_t *c_offsets_d,
+                  const lvx_seg_record *seg_rec_d, const uint8_t *c_valid_d, const float *c_a_d,
+                  const float *c_b_d, const float *c_w_d, int32_t level, int32_t n_bins,
+                  int32_t adjacency, uint8_t *valid_d, float *rep_a_d, float *rep_b_d, float *rep_w_d,
+                  void *stream);
+int lvx_probe_replines(const lvx_replines *rep, const double *rays_d, const double *max_t_d,
+                       double radius_base, int64_t n, int32_t *out_d, void *stream);
 
 /* Geometry secondary rays as point probes.
  * lvx_probe_blocked: _kernels.geometry_ray_blocked (_kernels.py:450-495), the kernel behind

@@ -311,6 +311,82 @@ def default_camera(dims, width=640, height=360):
                 width=width, height=height)
 
 
+class RepLevel:
+    def __init__(self, valid, a, b, weight):
+        self.valid, self.a, self.b, self.weight = valid, a, b, weight
+
+
+def build_rep_lines(model, n_levels: int, adjacency: bool = True):
+    """build_rep_lines (lod.py:224-284): list indexed by level, entry 0 is None."""
+    n_bins = int(model.n_bins)
+    levels = [None]
+    cur_a = np.asarray(model.seg_a, dtype=np.float64)
+    cur_b = np.asarray(model.seg_b, dtype=np.float64)
+    cur_vox = np.asarray(model.seg_voxel, dtype=np.int64)
+    d = cur_b - cur_a
+    cur_w = np.sqrt((d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2])
+    cur_dims = tuple(int(x) for x in model.dims)
+    L = lib()
+    for level in range(1, int(n_levels)):
+        pd = tuple((x + 1) // 2 for x in cur_dims)
+        size = float(1 << level)
+        pvox = cur_vox // 2
+        plin = pvox[:, 0] + pd[0] * (pvox[:, 1] + pd[1] * pvox[:, 2])
+        order = np.argsort(plin, kind="stable")
+        n_parent = pd[0] * pd[1] * pd[2]
+        valid = np.zeros(n_parent, dtype=np.uint8)
+        rep_a = np.zeros((n_parent, 3), dtype=np.float32)
+        rep_b = np.zeros((n_parent, 3), dtype=np.float32)
+        rep_w = np.zeros(n_parent, dtype=np.float32)
+        a_s = np.ascontiguousarray(cur_a[order])
+        b_s = np.ascontiguousarray(cur_b[order])
+        w_s = np.ascontiguousarray(cur_w[order])
+        p_s = np.ascontiguousarray(plin[order])
+        pdv = np.asarray(pd, dtype=np.int64)
+        L.lvo_rep_level(C.c_int64(a_s.shape[0]), _p(a_s), _p(b_s), _p(w_s), _p(p_s), _p(pdv), C.c_double(size),
+                        C.c_int64(n_bins), _p(valid), _p(rep_a), _p(rep_b), _p(rep_w))
+        if adjacency:
+            L.lvo_rep_adjacency(_p(pdv), C.c_double(size), C.c_int64(n_bins), _p(valid), _p(rep_a), _p(rep_b))
+        levels.append(RepLevel(valid.astype(bool), rep_a, rep_b, rep_w))
+        keep = np.nonzero(valid)[0]
+        cur_a = rep_a[keep].astype(np.float64)
+        cur_b = rep_b[keep].astype(np.float64)
+        cur_w = rep_w[keep].astype(np.float64)
+        cur_vox = np.stack([keep % pd[0], (keep // pd[0]) % pd[1], keep // (pd[0] * pd[1])], axis=1)
+        cur_dims = pd
+    return levels
+
+
+def _rep_level_args(levels, dims, level):
+    level = max(1, min(int(level), len(levels) - 1))
+    lvl = levels[level]
+    ld = np.asarray([-(-int(g) // (1 << level)) for g in dims], dtype=np.int64)
+    return (np.ascontiguousarray(lvl.valid, dtype=np.uint8), np.ascontiguousarray(lvl.a, dtype=np.float32),
+            np.ascontiguousarray(lvl.b, dtype=np.float32), np.ascontiguousarray(lvl.weight, dtype=np.float32), ld,
+            float(1 << level))
+
+
+def replines_shadow(point, light, levels, grid_dims, level=1, tube_radius=0.3, normal=None) -> int:
+    """illumination.replines_shadow (illumination.py:115-139): 1 if the point sees the light."""
+    if not 1 <= level < len(levels):
+        raise ValueError(f"level must be in [1, {len(levels) - 1}], got {level}")
+    o = _f64(point)
+    if normal is not None:
+        nn = _f64(normal)
+        o = o + 1e-3 * (nn / np.linalg.norm(nn))
+    to_light = _f64(light) - o
+    max_t = float(np.linalg.norm(to_light))
+    if max_t == 0.0:
+        return 1
+    d = to_light / max_t
+    valid, a, b, w, ld, size = _rep_level_args(levels, grid_dims, level)
+    fn = lib().lvo_replines_blocked
+    fn.restype = C.c_int
+    blocked = fn(_p(o), _p(d), C.c_double(max_t), _p(valid), _p(a), _p(b), _p(w), _p(ld), C.c_double(size),
+                 C.c_double(float(tube_radius) * size))
+    return 0 if blocked else 1
+
+
 def hard_shadow(point, light, model, radius=0.3, normal=None, joint_spheres=True) -> int:
     """illumination.hard_shadow (illumination.py:96-112): 1 if the point sees the light position."""
     o = _f64(point)
@@ -352,7 +428,7 @@ def render(camera: dict, model, levels=None, *, tube_radius=0.3, opacity_mode="c
            base_opacity=1.0, tau=0.95, neighbor=True, joint_spheres=True, shadow_mode="none",
            ao_mode="none", background=(0.0, 0.0, 0.0, 1.0), light_dir=None, ambient=0.2,
            diffuse=0.7, specular=0.3, shininess=32.0, ao_rays=25, ao_radius=15.0, threads=0,
-           rows=None):
+           rows=None, replines=None, shadow_rep_level=2):
     """render_frame (raycast.py:468-521): returns (image (H,W,4) f32, stats dict).
 
     `rows=(y0, y1[, step])` renders only rows y0, y0+step, ... < y1 (bounded CPU timing)."""
@@ -383,6 +459,13 @@ def render(camera: dict, model, levels=None, *, tube_radius=0.3, opacity_mode="c
     table = np.ascontiguousarray(model.transfer_table, dtype=np.float32)
     seg_a = np.ascontiguousarray(model.seg_a, dtype=np.float32)
     seg_b = np.ascontiguousarray(model.seg_b, dtype=np.float32)
+    rep_keep = None
+    if SHADOW_MODES[shadow_mode] == 2:
+        if replines is None:
+            raise ValueError("replines shadows need a representative-line field")
+        rep_keep = _rep_level_args(replines, model.dims, shadow_rep_level)
+        lib().lvo_set_replines(_p(rep_keep[0]), _p(rep_keep[1]), _p(rep_keep[2]), _p(rep_keep[3]), _p(rep_keep[4]),
+                               C.c_double(rep_keep[5]))
     rc = lib().lvo_render_rows(
         _p(cam[0]), _p(cam[1]), _p(cam[2]), _p(cam[3]), C.c_double(cam[4]), C.c_double(cam[5]),
         C.c_int64(W), C.c_int64(H), C.c_int64(y0), C.c_int64(y1), C.c_int64(max(1, ystep)), C.c_int64(rx), C.c_int64(ry),

@@ -42,10 +42,16 @@ class Params(C.Structure):
                 ("ao_n_rays", C.c_int32), ("_pad", C.c_int32), ("ao_radius", C.c_double)]
 
 
+class RepLines(C.Structure):
+    _fields_ = [("valid_d", C.c_void_p), ("a_d", C.c_void_p), ("b_d", C.c_void_p), ("w_d", C.c_void_p),
+                ("dims", C.c_int32 * 3), ("_pad", C.c_int32), ("size", C.c_double)]
+
+
 class Lod(C.Structure):
     _fields_ = [("oct_flat_d", C.c_void_p), ("oct_off", C.c_int64 * (MAX_LEVELS + 1)),
                 ("oct_dims", C.c_int64 * (MAX_LEVELS * 3)), ("n_levels", C.c_int32),
-                ("_pad", C.c_int32), ("ao_flat_d", C.c_void_p), ("ao_dirs_d", C.c_void_p)]
+                ("_pad", C.c_int32), ("ao_flat_d", C.c_void_p), ("ao_dirs_d", C.c_void_p),
+                ("rep", RepLines)]
 
 
 class Tiling(C.Structure):
@@ -63,7 +69,7 @@ SYMBOLS = [
     "lvx_render_footprint", "lvx_untile",
     "lvx_fibonacci_dirs", "lvx_ao_bake", "lvx_probe_dda", "lvx_probe_tube", "lvx_probe_sphere",
     "lvx_probe_trilinear", "lvx_probe_cone", "lvx_probe_ao_density", "lvx_probe_blocked",
-    "lvx_probe_ao_hemisphere",
+    "lvx_probe_ao_hemisphere", "lvx_rep_level", "lvx_probe_replines",
 ]
 
 _lib = None

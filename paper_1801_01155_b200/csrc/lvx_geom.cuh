@@ -549,6 +549,58 @@ __device__ inline double lvx_ao_hemisphere_point(double px, double py, double pz
     return (double)blocked / (double)n_rays;
 }
 
+// One level of the representative-line field (lvx_rep.cu).
+struct LvxRepLevel {
+    const u8 *valid;
+    const float *a, *b, *w;
+    int dx, dy, dz;
+    double size;  // 2^level grid units
+};
+
+// replines_ray_blocked, _kernels.py:498-538: shadow test against one representative line
+// per coarse voxel; the radius grows with the aggregated weight (clamped to [1, 4]).  The
+// reference walks the coarse grid and tests the 27 neighbours of every window that starts
+// before max_t; the answer is a disjunction, so each coarse voxel is tested once.
+__device__ inline bool lvx_replines_blocked(double ox, double oy, double oz, double dx, double dy, double dz,
+                                            double max_t, const LvxRepLevel &R, double radius_base) {
+    LvxDda dda;
+    dda.init(ox / R.size, oy / R.size, oz / R.size, dx, dy, dz, R.dx, R.dy, R.dz, 1);
+    if (!dda.alive) return false;
+    u32 listed = 0;
+    int px = 0, py = 0, pz = 0;
+    int wx, wy, wz;
+    double t0, t1;
+    while (dda.next(wx, wy, wz, t0, t1)) {
+        if (t0 * R.size >= max_t) break;
+        if (listed) {
+            const int sx = wx - px, sy = wy - py, sz = wz - pz;
+            listed = (sx < -1 || sx > 1 || sy < -1 || sy > 1 || sz < -1 || sz > 1) ? 0u
+                                                                                 : lvx_shift_mask27(listed, sx, sy, sz);
+        }
+        px = wx;
+        py = wy;
+        pz = wz;
+        const u32 fresh = 0x7FFFFFFu & ~listed;
+        listed = 0x7FFFFFFu;
+        for (u32 mm = fresh; mm; mm &= mm - 1) {
+            const int b = __ffs((int)mm) - 1;
+            const int bz = b / 9, by = (b - 9 * bz) / 3, bx = b - 9 * bz - 3 * by;
+            const int hx = wx + bx - 1, hy = wy + by - 1, hz = wz + bz - 1;
+            if (hx < 0 || hy < 0 || hz < 0 || hx >= R.dx || hy >= R.dy || hz >= R.dz) continue;
+            const i64 lin = hx + (i64)R.dx * (hy + (i64)R.dy * hz);
+            if (!R.valid[lin]) continue;
+            double wgt = (double)R.w[lin];
+            wgt = wgt < 1.0 ? 1.0 : (wgt > 4.0 ? 4.0 : wgt);
+            LvxHit h;
+            if (lvx_tube_f32axis(ox, oy, oz, dx, dy, dz, R.a[3 * lin], R.a[3 * lin + 1], R.a[3 * lin + 2], R.b[3 * lin],
+                                 R.b[3 * lin + 1], R.b[3 * lin + 2], radius_base * wgt, h) &&
+                1e-9 < h.t_in && h.t_in < max_t)
+                return true;
+        }
+    }
+    return false;
+}
+
 // shade_scalar, _kernels.py:316-329
 __device__ __forceinline__ double lvx_shade(double nx, double ny, double nz, double lx, double ly,
                                             double lz, double vx, double vy, double vz, double ka,

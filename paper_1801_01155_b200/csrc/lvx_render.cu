@@ -80,6 +80,8 @@ struct RenderArgs {
     LvxOctree oc;
     const float *ao_flat;
     const double *ao_dirs;
+    LvxRepLevel rep;          // representative-line level of shadow_mode = replines
+    double rep_radius_base;   // tube_radius * 2^level (raycast.py:425)
     lvx_tiling tl;
     int tiles_x, n_my_tiles;
     float *img;
@@ -137,6 +139,10 @@ __device__ __forceinline__ void shade_hit(const RenderArgs &A, double ox, double
         const LvxGeomModel G = {A.rx, A.ry, A.rz, A.counts, A.offsets, A.rec, A.nmask};
         if (lvx_geometry_blocked(px + 1e-3 * h.nx, py + 1e-3 * h.ny, pz + 1e-3 * h.nz, p.light[0], p.light[1],
                                  p.light[2], 1e30, G, p.tube_r, p.joints != 0))
+            shadow_term = 1.0;
+    } else if (GEOM && p.shadow_mode == LVX_SHADOW_REPLINES) {
+        if (lvx_replines_blocked(px + 1e-3 * h.nx, py + 1e-3 * h.ny, pz + 1e-3 * h.nz, p.light[0], p.light[1],
+                                 p.light[2], 1e30, A.rep, A.rep_radius_base))
             shadow_term = 1.0;
     }
     double ao_term = 0.0;
@@ -1011,9 +1017,11 @@ static int render_impl(const lvx_camera *cam, const lvx_model *model, const lvx_
     LVX_REQUIRE(!params->neighbor || (model->nsum_d && model->nmask_d),
                 "neighbour mode needs the neighbour grids (lvx_neighbor_sums)");
     LVX_REQUIRE(params->opacity_mode >= 0 && params->opacity_mode <= 2, "bad opacity mode");
-    LVX_REQUIRE(params->shadow_mode == LVX_SHADOW_NONE || params->shadow_mode == LVX_SHADOW_CONE ||
-                    params->shadow_mode == LVX_SHADOW_HARD,
-                "shadow_mode %d is not built in this library (none/hard/cone only)", params->shadow_mode);
+    LVX_REQUIRE(params->shadow_mode >= LVX_SHADOW_NONE && params->shadow_mode <= LVX_SHADOW_CONE, "bad shadow_mode %d",
+                params->shadow_mode);
+    LVX_REQUIRE(params->shadow_mode != LVX_SHADOW_REPLINES ||
+                    (lod && lod->rep.valid_d && lod->rep.a_d && lod->rep.b_d && lod->rep.w_d && lod->rep.size >= 2.0),
+                "replines shadows need a representative-line level (lvx_lod.rep)");
     LVX_REQUIRE(params->ao_mode >= LVX_AO_NONE && params->ao_mode <= LVX_AO_PRECOMPUTED, "bad ao_mode %d",
                 params->ao_mode);
     LVX_REQUIRE((params->shadow_mode != LVX_SHADOW_HARD && params->ao_mode != LVX_AO_HEMISPHERE) || model->nmask_d,
@@ -1044,6 +1052,11 @@ static int render_impl(const lvx_camera *cam, const lvx_model *model, const lvx_
     fill_octree(A.oc, lod);
     A.ao_flat = lod ? lod->ao_flat_d : nullptr;
     A.ao_dirs = lod ? lod->ao_dirs_d : nullptr;
+    if (lod && lod->rep.valid_d) {
+        A.rep = LvxRepLevel{lod->rep.valid_d, lod->rep.a_d, lod->rep.b_d, lod->rep.w_d, lod->rep.dims[0], lod->rep.dims[1],
+                            lod->rep.dims[2], lod->rep.size};
+        A.rep_radius_base = params->tube_r * lod->rep.size;
+    }
     A.tl = *tiling;
     A.n_my_tiles = (int)my_tile_count(tiling, cam->width, cam->height, &A.tiles_x);
     A.img = img_d;
@@ -1052,7 +1065,8 @@ static int render_impl(const lvx_camera *cam, const lvx_model *model, const lvx_
     const i64 warps = (i64)A.n_my_tiles * (tiling->tile_w / 8) * (tiling->tile_h / 4);
     const i64 blocks = lvx_ceil_div(warps, kWarpsPerBlock);
     A.footprint = footprint_d;
-    const bool geom = params->shadow_mode == LVX_SHADOW_HARD || params->ao_mode == LVX_AO_HEMISPHERE;
+    const bool geom = params->shadow_mode == LVX_SHADOW_HARD || params->shadow_mode == LVX_SHADOW_REPLINES ||
+                      params->ao_mode == LVX_AO_HEMISPHERE;
     if (footprint_d && geom)
         render_kernel<true, true><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, (cudaStream_t)stream>>>(A);
     else if (footprint_d)

@@ -135,6 +135,8 @@ struct WfArgs {
     LvxOctree oc;
     const float *ao_flat;
     const double *ao_dirs;
+    LvxRepLevel rep;          // representative-line level of shadow_mode = replines
+    double rep_radius_base;   // tube_radius * 2^level (raycast.py:425)
     lvx_tiling tl;
     int tiles_x, n_my_tiles;
     float *img;
@@ -811,6 +813,10 @@ __device__ __forceinline__ void wf_shade(const WfArgs &A, double ox, double oy, 
         if (lvx_geometry_blocked(px + 1e-3 * h.nx, py + 1e-3 * h.ny, pz + 1e-3 * h.nz, p.light[0], p.light[1],
                                  p.light[2], 1e30, G, p.tube_r, p.joints != 0))
             shadow_term = 1.0;
+    } else if (GEOM && p.shadow_mode == LVX_SHADOW_REPLINES) {
+        if (lvx_replines_blocked(px + 1e-3 * h.nx, py + 1e-3 * h.ny, pz + 1e-3 * h.nz, p.light[0], p.light[1],
+                                 p.light[2], 1e30, A.rep, A.rep_radius_base))
+            shadow_term = 1.0;
     }
     double ao_term = 0.0;
     if (p.ao_mode == LVX_AO_PRECOMPUTED) {
@@ -1456,9 +1462,11 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     LVX_REQUIRE(!params->neighbor || (model->nsum_d && model->nmask_d),
                 "neighbour mode needs the neighbour grids (lvx_neighbor_sums)");
     LVX_REQUIRE(params->opacity_mode >= 0 && params->opacity_mode <= 2, "bad opacity mode");
-    LVX_REQUIRE(params->shadow_mode == LVX_SHADOW_NONE || params->shadow_mode == LVX_SHADOW_CONE ||
-                    params->shadow_mode == LVX_SHADOW_HARD,
-                "shadow_mode %d is not built in this library (none/hard/cone only)", params->shadow_mode);
+    LVX_REQUIRE(params->shadow_mode >= LVX_SHADOW_NONE && params->shadow_mode <= LVX_SHADOW_CONE, "bad shadow_mode %d",
+                params->shadow_mode);
+    LVX_REQUIRE(params->shadow_mode != LVX_SHADOW_REPLINES ||
+                    (lod && lod->rep.valid_d && lod->rep.a_d && lod->rep.b_d && lod->rep.w_d && lod->rep.size >= 2.0),
+                "replines shadows need a representative-line level (lvx_lod.rep)");
     LVX_REQUIRE(params->ao_mode >= LVX_AO_NONE && params->ao_mode <= LVX_AO_PRECOMPUTED, "bad ao_mode %d",
                 params->ao_mode);
     LVX_REQUIRE((params->shadow_mode != LVX_SHADOW_HARD && params->ao_mode != LVX_AO_HEMISPHERE) || model->nmask_d,
@@ -1499,6 +1507,11 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
         for (int l = 0; l < lod->n_levels * 3 && l < LVX_MAX_LEVELS * 3; ++l) A.oc.dims[l] = (int)lod->oct_dims[l];
         A.ao_flat = lod->ao_flat_d;
         A.ao_dirs = lod->ao_dirs_d;
+        if (lod->rep.valid_d) {
+            A.rep = LvxRepLevel{lod->rep.valid_d, lod->rep.a_d, lod->rep.b_d, lod->rep.w_d, lod->rep.dims[0],
+                                lod->rep.dims[1], lod->rep.dims[2], lod->rep.size};
+            A.rep_radius_base = params->tube_r * lod->rep.size;
+        }
     }
     A.tl = *tiling;
     {
@@ -1556,7 +1569,8 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     if (const char *e = getenv("LVX_WF_WN")) A.wn_sched = atoi(e) > 0 ? atoi(e) : A.wn_sched;
 
     const bool debug = getenv("LVX_WF_DEBUG") != nullptr;
-    const bool geom = params->shadow_mode == LVX_SHADOW_HARD || params->ao_mode == LVX_AO_HEMISPHERE;
+    const bool geom = params->shadow_mode == LVX_SHADOW_HARD || params->shadow_mode == LVX_SHADOW_REPLINES ||
+                      params->ao_mode == LVX_AO_HEMISPHERE;
     cudaStream_t st = (cudaStream_t)stream;
     const int sms = lvx_sm_count();
     const unsigned grid_rays = (unsigned)(sms * 8), grid_q = (unsigned)(sms * 8);

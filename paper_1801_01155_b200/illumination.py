@@ -10,8 +10,7 @@ _kernels.py:346-445, 541-620 of the reference), evaluated on the GPU.
     lvx_probe_blocked        <- hard_shadow / geometry_ray_blocked
     lvx_probe_ao_hemisphere  <- ao_hemisphere_geometry / ao_hemisphere_point
 
-`replines_shadow` (representative lines) is outside the
-accelerated path and raises NotImplementedError here.
+    lvx_probe_replines       <- replines_shadow / replines_ray_blocked
 """
 from __future__ import annotations
 
@@ -205,17 +204,29 @@ def sample_ao(field: AOField, point, normal=None):
     return float(v[0]) if single else v
 
 
-def _not_built(name):
-    def fn(*args, **kwargs):
-        raise NotImplementedError(
-            f"{name} traces secondary rays against the segment geometry; only the "
-            "density-grid secondary rays (cone_soft_shadow, ao_density_rays, "
-            "precompute_voxel_ao) are part of the accelerated path")
-    fn.__name__ = name
-    return fn
-
-
-replines_shadow = _not_built("replines_shadow")
+def replines_shadow(point, light, replines, grid_dims, level: int = 1, tube_radius: float = 0.3,
+                    normal=None) -> int:
+    """Like hard_shadow but tested against at most one representative line per coarse voxel
+    at the given level; the line's radius is the tube radius scaled to the level and
+    thickened by its aggregated weight, clamped to [1,4] (illumination.py:115-139 ->
+    replines_ray_blocked, _kernels.py:498-538)."""
+    if not 1 <= level < len(replines.levels):
+        raise ValueError(f"level must be in [1, {len(replines.levels) - 1}], got {level}")
+    torch = _lib.require_device()
+    o = _shadow_origin(point, normal)
+    to_light = np.asarray(light, dtype=np.float64) - o
+    max_t = float(np.linalg.norm(to_light))
+    if max_t == 0.0:
+        return 1
+    d = to_light / max_t
+    rep = replines.level_struct(level, grid_dims)
+    rays = _lib.to_device(np.concatenate([o, d])[None])
+    mt = _lib.to_device(np.asarray([max_t], dtype=np.float64))
+    out = torch.empty(1, dtype=torch.int32, device="cuda")
+    _lib.check(_lib.lib().lvx_probe_replines(C.byref(rep), _lib.ptr(rays), _lib.ptr(mt),
+                                             C.c_double(float(tube_radius) * float(1 << level)), C.c_int64(1),
+                                             _lib.ptr(out), _lib.stream_ptr()))
+    return 0 if int(out.item()) else 1
 
 
 def _model_struct(model: VoxelModel) -> "_lib.Model":

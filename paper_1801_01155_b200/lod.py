@@ -138,3 +138,101 @@ def build_octree(level0: np.ndarray) -> DensityOctree:
 def build_lod(model: VoxelModel) -> DensityOctree:
     """compute_density_level0 + build_octree without leaving the GPU."""
     return _octree_from_level0_device(density_level0_device(model), model.spec.dims)
+
+
+# --- representative lines (lod.py:61-79, 122-284) ---------------------------------------------
+
+class RepLevel:
+    """One representative line per voxel of a coarsened grid (lod.py:61-65): `valid` (V,) bool,
+    `a`, `b` (V,3) float32 grid units, `weight` (V,) float32 summed member length.  Built on
+    the device; the numpy views are downloaded on first access."""
+
+    def __init__(self, valid_d, a_d, b_d, w_d, dims):
+        self._d = (valid_d, a_d, b_d, w_d)
+        self.dims = tuple(int(x) for x in dims)
+        self._h = {}
+
+    def _host(self, k, i, conv=None):
+        if k not in self._h:
+            v = self._d[i].cpu().numpy()
+            self._h[k] = conv(v) if conv else v
+        return self._h[k]
+
+    @property
+    def valid(self):
+        return self._host("valid", 0, lambda v: v.astype(bool))
+
+    @property
+    def a(self):
+        return self._host("a", 1)
+
+    @property
+    def b(self):
+        return self._host("b", 2)
+
+    @property
+    def weight(self):
+        return self._host("weight", 3)
+
+    def device(self):
+        return self._d
+
+
+class RepLineField:
+    """One optional representative line per voxel at every level >= 1 (lod.py:68-79);
+    index 0 is None (the fine level keeps its real segments)."""
+
+    def __init__(self, levels):
+        self.levels = levels
+
+    def level_dims(self, level: int, octree_dims) -> tuple:
+        d = tuple(octree_dims)
+        for _ in range(level):
+            d = tuple((x + 1) // 2 for x in d)
+        return d
+
+    def level_struct(self, level: int, grid_dims) -> "_lib.RepLines":
+        """_rep_args (raycast.py:391-402) as the C struct; the level is clamped like there."""
+        level = max(1, min(int(level), len(self.levels) - 1))
+        lvl = self.levels[level]
+        r = _lib.RepLines()
+        v, a, b, w = lvl.device()
+        r.valid_d, r.a_d, r.b_d, r.w_d = v.data_ptr(), a.data_ptr(), b.data_ptr(), w.data_ptr()
+        for i in range(3):
+            r.dims[i] = -(-int(grid_dims[i]) // (1 << level))
+        r.size = float(1 << level)
+        r._keep = (v, a, b, w)
+        return r
+
+
+def build_rep_lines(model: VoxelModel, octree: DensityOctree, adjacency: bool = True) -> RepLineField:
+    """Representative lines for every level >= 1 (lod.py:224-284): level 1 averages the model's
+    segments grouped into 2x2x2 voxel blocks, each further level the representatives of the
+    level below; the weight is the summed member length.  One kernel per level
+    (lvx_rep_level), one thread per parent voxel, same member order as the reference."""
+    torch = _lib.require_device()
+    L, st = _lib.lib(), _lib.stream_ptr()
+    counts_d, offsets_d, rec_d, _, _ = model.device_view(need_occ=False)
+    n_bins = int(model.spec.bins_per_axis)
+    levels = [None]
+    child_dims = tuple(int(x) for x in model.spec.dims)
+    prev = None
+    for level in range(1, octree.n_levels):
+        pd = tuple((x + 1) // 2 for x in child_dims)
+        V = pd[0] * pd[1] * pd[2]
+        valid = torch.empty(V, dtype=torch.uint8, device="cuda")
+        a = torch.empty((V, 3), dtype=torch.float32, device="cuda")
+        b = torch.empty((V, 3), dtype=torch.float32, device="cuda")
+        w = torch.empty(V, dtype=torch.float32, device="cuda")
+        if prev is None:
+            args = (_lib.ptr(counts_d), _lib.ptr(offsets_d), _lib.ptr(rec_d), None, None, None, None)
+        else:
+            pv, pa, pb, pw = prev
+            args = (None, None, None, _lib.ptr(pv), _lib.ptr(pa), _lib.ptr(pb), _lib.ptr(pw))
+        _lib.check(L.lvx_rep_level(_lib.i32x3(child_dims), *args, C.c_int32(level), C.c_int32(n_bins),
+                                   C.c_int32(1 if adjacency else 0), _lib.ptr(valid), _lib.ptr(a), _lib.ptr(b),
+                                   _lib.ptr(w), st))
+        levels.append(RepLevel(valid, a, b, w, pd))
+        prev = (valid, a, b, w)
+        child_dims = pd
+    return RepLineField(levels)

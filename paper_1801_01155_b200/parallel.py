@@ -115,12 +115,13 @@ def gather_tiles(tiles, dst: int = 0, group=None):
 # --- rendering ---------------------------------------------------------------------------
 
 def render_my_tiles(camera: Camera, model, octree, params: RenderParams, rank: int, world: int,
-                    moving: bool = False, tile_w: int = MG_TILE_W, tile_h: int = MG_TILE_H):
+                    moving: bool = False, tile_w: int = MG_TILE_W, tile_h: int = MG_TILE_H, replines=None):
     """Render rank's interleaved tiles into a compact buffer.
     Returns (tiles f32[n_tiles, tile_h, tile_w, 4], row_stats i64[H,3]) on the device."""
     torch = _lib.require_device()
     plan = FramePlan(camera, model, octree, params, resolve_neighbor(params, moving),
-                     tile_first=rank, tile_step=world, compact=True, tile_w=tile_w, tile_h=tile_h)
+                     tile_first=rank, tile_step=world, compact=True, tile_w=tile_w, tile_h=tile_h,
+                     replines=replines)
     n = plan.n_my_tiles()
     tiles = torch.zeros((max(n, 1), tile_h, tile_w, 4), dtype=torch.float32, device="cuda")
     stats = torch.zeros((camera.height, 3), dtype=torch.int64, device="cuda")
@@ -152,7 +153,7 @@ def render_frame_tiled(camera: Camera, model, octree=None, replines=None,
     rank = dist.get_rank(group)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    tiles, stats = render_my_tiles(camera, model, octree, params, rank, world, moving)
+    tiles, stats = render_my_tiles(camera, model, octree, params, rank, world, moving, replines=replines)
     e1.record()
     tot = stats.sum(dim=0)
     dist.reduce(tot, dst=0, group=group)

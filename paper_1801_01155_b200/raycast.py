@@ -253,11 +253,13 @@ def default_camera(dims, width: int = 640, height: int = 360) -> Camera:
 
 def ensure_lod(model: VoxelModel, octree: Optional[DensityOctree], replines, params: RenderParams):
     """Build the octree the requested shadow/AO modes need (raycast.py:451-465)."""
-    if params.shadow_mode == "replines":
-        raise NotImplementedError("shadow_mode='replines' is outside the accelerated path")
-    need_octree = params.shadow_mode == "cone" or params.ao_mode == "density-rays"
+    need_octree = (params.shadow_mode == "cone" or params.ao_mode == "density-rays"
+                   or (params.shadow_mode == "replines" and replines is None))
     if need_octree and octree is None:
         octree = build_lod(model)
+    if params.shadow_mode == "replines" and replines is None:
+        from .lod import build_rep_lines
+        replines = build_rep_lines(model, octree)
     if params.ao_mode == "precomputed" and model.ao is None:
         raise ValueError("the model carries no baked AO field; run `linevox precompute-ao` first")
     return octree, replines
@@ -314,12 +316,11 @@ def params_struct(params: RenderParams, neighbor: int) -> "_lib.Params":
     return p
 
 
-def check_modes(params: RenderParams, model: VoxelModel, octree):
+def check_modes(params: RenderParams, model: VoxelModel, octree, replines=None):
     """The error behaviour of _illum_args (raycast.py:414-421), plus the modes this
     build does not accelerate."""
-    if params.shadow_mode == "replines":
-        raise NotImplementedError("shadow_mode='replines' (representative lines) is outside the "
-                                  "accelerated path (none/hard/cone only)")
+    if params.shadow_mode == "replines" and replines is None:
+        raise ValueError("replines shadows need a representative-line field")  # raycast.py:416-417
     if params.shadow_mode == "cone" and octree is None:
         raise ValueError("cone shadows need a density octree")
     if params.ao_mode == "density-rays" and octree is None:
@@ -364,9 +365,9 @@ class FramePlan:
     def __init__(self, camera: Camera, model: VoxelModel, octree: Optional[DensityOctree],
                  params: RenderParams, neighbor: int, tile_first: int = 0, tile_step: int = 1,
                  compact: bool = False, tile_w: int = TILE_W, tile_h: int = TILE_H,
-                 engine: Optional[str] = None):
+                 engine: Optional[str] = None, replines=None):
         from .illumination import fibonacci_dirs_device
-        check_modes(params, model, octree)
+        check_modes(params, model, octree, replines)
         self.engine = engine or default_engine()
         if self.engine == "auto":
             self.engine = "wavefront" if neighbor else "tile"
@@ -376,6 +377,7 @@ class FramePlan:
         self.cam = camera_struct(camera)
         self.par = params_struct(params, neighbor)
         geometry_rays = params.shadow_mode == "hard" or params.ao_mode == "hemisphere-geometry"
+        self._rep = None
         counts_d, offsets_d, rec_d, table_d, occ_d = model.device_view(need_occ=bool(neighbor) or geometry_rays)
         m = _lib.Model()
         m.rx, m.ry, m.rz = model.spec.dims
@@ -394,6 +396,10 @@ class FramePlan:
             self.lod.n_levels = 0
             self.lod.ao_flat_d = ao_d.data_ptr() if ao_d is not None else None
             self.lod.ao_dirs_d = dirs_d.data_ptr() if dirs_d is not None else None
+        if params.shadow_mode == "replines":
+            # the level is clamped like _rep_args does (raycast.py:391-402)
+            self._rep = replines.level_struct(params.shadow_rep_level, model.spec.dims)
+            self.lod.rep = self._rep
         t = _lib.Tiling()
         t.tile_w, t.tile_h = tile_w, tile_h
         t.tile_first, t.tile_step, t.compact = int(tile_first), int(tile_step), 1 if compact else 0
@@ -454,7 +460,7 @@ def render_frame(camera: Camera, model: VoxelModel, octree: Optional[DensityOctr
         params = RenderParams()
     torch = _lib.require_device()
     neighbor = resolve_neighbor(params, moving)
-    plan = FramePlan(camera, model, octree, params, neighbor)
+    plan = FramePlan(camera, model, octree, params, neighbor, replines=replines)
     H, W = camera.height, camera.width
     img_d = torch.empty((H, W, 4), dtype=torch.float32, device="cuda")
     stats_d = torch.zeros((H, 3), dtype=torch.int64, device="cuda")

@@ -30,6 +30,9 @@ RENDER_CASES = ["opaque_nb", "opaque_own", "alpha25_nb", "alpha25_own_nojoints",
                 # geometry secondary rays: hard shadows, hemisphere-geometry AO
                 "geom_hard_nb", "geom_hard_own_nojoints", "geom_hemi_nb", "geom_hard_hemi"]
 
+# frames with shadow_mode="replines" (they also need the representative-line field)
+REP_RENDER_CASES = ["rep_frame_helices", "rep_frame_turbulence"]
+
 
 def render_kwargs(g):
     """The RenderParams kwargs a render fixture was made with."""

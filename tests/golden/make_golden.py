@@ -286,6 +286,54 @@ def make_geometry_probes(models):
         save("geom_probe_" + mname, P=P, N=N, L=L, hard=hs, ao=ao, ao_jitter=aoj)
 
 
+def make_replines(models, octrees):
+    """Representative lines (lod.py:224-284), their shadow probes (illumination.py:115-139)
+    and frames with shadow_mode="replines"."""
+    from linevox.illumination import replines_shadow
+    from linevox.lod import build_rep_lines
+    rng = np.random.default_rng(321)
+    fields = {}
+    for mname in ("helices", "turbulence", "wiggles"):
+        m, dims = models[mname]
+        oc = octrees[mname]
+        rl = build_rep_lines(m, oc)
+        loose = build_rep_lines(m, oc, adjacency=False)
+        fields[mname] = rl
+        out = {"n_levels": np.int64(len(rl.levels))}
+        for l in range(1, len(rl.levels)):
+            for tag, f in (("", rl), ("loose_", loose)):
+                lv_ = f.levels[l]
+                out[f"{tag}valid{l}"] = lv_.valid
+                out[f"{tag}a{l}"] = lv_.a
+                out[f"{tag}b{l}"] = lv_.b
+                out[f"{tag}w{l}"] = lv_.weight
+        d = np.asarray(dims, dtype=np.float64)
+        n = 120
+        P = rng.uniform(0.1, 0.9, (n, 3)) * d
+        N = rng.normal(size=(n, 3))
+        N /= np.linalg.norm(N, axis=1, keepdims=True)
+        Lp = rng.uniform(-0.5, 1.5, (n, 3)) * d
+        lev = np.array([1 + (i % (len(rl.levels) - 1)) for i in range(n)], dtype=np.int64)
+        sh = np.array([replines_shadow(P[i], Lp[i], rl, dims, level=int(lev[i]), tube_radius=0.3,
+                                       normal=N[i] if i % 2 else None) for i in range(n)], dtype=np.int64)
+        save("rep_" + mname, P=P, N=N, L=Lp, level=lev, shadow=sh, **out)
+    cases = [("rep_frame_helices", "helices", (48, 36), dict(neighbor_mode="on", base_opacity=0.4, shadow_mode="replines",
+                                                             light_dir=(0.3, 0.2, 1.0), shadow_rep_level=1)),
+             ("rep_frame_turbulence", "turbulence", (40, 30), dict(neighbor_mode="off", base_opacity=0.5,
+                                                                   shadow_mode="replines", light_dir=(-0.4, 0.7, 0.5)))]
+    for name, mname, (W, H), kw in cases:
+        if ONLY is not None and not ("render_" + name).startswith(ONLY):
+            continue
+        m, dims = models[mname]
+        m.ao = None
+        fr = RR.render_frame(RR.default_camera(dims, W, H), m, octrees.get(mname), fields[mname], RR.RenderParams(**kw),
+                             workers=4)
+        st = fr.stats
+        save("render_" + name, image=fr.image, model=np.array(mname),
+             stats=np.asarray([st["voxel_steps"], st["intersection_tests"], st["window_overflow"]], np.int64),
+             transfer_table=np.asarray(m.transfer_table, np.float32), size=np.asarray([W, H]), params=np.array(repr(kw)))
+
+
 def main():
     global ONLY
     if "--only" in sys.argv:
@@ -296,6 +344,7 @@ def main():
     make_render(models, octrees, ao_fields)
     make_primitives(models, octrees, ao_fields)
     make_geometry_probes(models)
+    make_replines(models, octrees)
 
 
 if __name__ == "__main__":

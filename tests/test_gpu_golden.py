@@ -5,7 +5,7 @@ counters; point probes bit-exact except where CUDA libm differs (pow)."""
 import numpy as np
 import pytest
 
-from conftest import RENDER_CASES, VOX_CASES, assert_model_equal, golden, render_kwargs
+from conftest import RENDER_CASES, REP_RENDER_CASES, VOX_CASES, assert_model_equal, golden, render_kwargs
 
 pytestmark = pytest.mark.gpu
 
@@ -77,12 +77,14 @@ def gpu_render(lv, name, **extra):
         m.ao = golden("ao_" + mname)["values"]
     W, H = (int(x) for x in g["size"])
     cam = lv.default_camera(m.spec.dims, W, H)
-    fr = lv.render_frame(cam, m, oc, None, lv.RenderParams(**render_kwargs(g)), **extra)
+    params = lv.RenderParams(**render_kwargs(g))
+    rl = lv.build_rep_lines(m, oc) if params.shadow_mode == "replines" else None
+    fr = lv.render_frame(cam, m, oc, rl, params, **extra)
     return g, fr
 
 
 @pytest.mark.parametrize("engine", ["tile", "wavefront"])
-@pytest.mark.parametrize("name", RENDER_CASES)
+@pytest.mark.parametrize("name", RENDER_CASES + REP_RENDER_CASES)
 def test_render_matches_reference(lv, name, engine, monkeypatch):
     # both frame engines (csrc/lvx_render.cu, csrc/lvx_wavefront.cu) against every fixture
     monkeypatch.setenv("LVX_ENGINE", engine)
@@ -113,6 +115,35 @@ def test_geometry_secondary_ray_probes(lv, mname):
     aoj = np.array([lv.ao_hemisphere_geometry(P[i], N[i], m, lv.AOParams(n_rays=6, radius=2.5), 0.25, jitter=0.37)
                     for i in range(0, len(P), 4)])
     assert np.array_equal(aoj, g["ao_jitter"])
+
+
+@pytest.mark.parametrize("mname", ["helices", "turbulence", "wiggles"])
+def test_representative_lines(lv, mname):
+    """build_rep_lines (every level, with and without the adjacency pass) and replines_shadow
+    against the reference's values, bit-exact (lod.py:224-284, illumination.py:115-139)."""
+    g = golden("rep_" + mname)
+    m = gpu_model(lv, golden("vox_" + mname))
+    oc = lv.build_lod(m)
+    n_levels = int(g["n_levels"])
+    assert oc.n_levels == n_levels
+    for adjacency, tag in ((True, ""), (False, "loose_")):
+        rl = lv.build_rep_lines(m, oc, adjacency=adjacency)
+        assert len(rl.levels) == n_levels and rl.levels[0] is None
+        for l in range(1, n_levels):
+            lvl = rl.levels[l]
+            assert np.array_equal(lvl.valid, g[f"{tag}valid{l}"]), (tag, l)
+            assert np.array_equal(lvl.a, g[f"{tag}a{l}"]), (tag, l)
+            assert np.array_equal(lvl.b, g[f"{tag}b{l}"]), (tag, l)
+            assert np.array_equal(lvl.weight, g[f"{tag}w{l}"]), (tag, l)
+    rl = lv.build_rep_lines(m, oc)
+    P, N, L, lev = g["P"], g["N"], g["L"], g["level"]
+    sh = [lv.replines_shadow(P[i], L[i], rl, m.spec.dims, level=int(lev[i]), tube_radius=0.3,
+                             normal=N[i] if i % 2 else None) for i in range(len(P))]
+    assert sh == list(g["shadow"])
+    with pytest.raises(ValueError):
+        lv.replines_shadow(P[0], L[0], rl, m.spec.dims, level=0)
+    with pytest.raises(ValueError):
+        lv.replines_shadow(P[0], L[0], rl, m.spec.dims, level=99)
 
 
 def test_tube_and_sphere_probes(lv):

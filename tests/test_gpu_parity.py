@@ -285,8 +285,11 @@ def test_error_conventions(lv, synth):
         lv.render_frame(cam, m, None, None, lv.RenderParams(ao_mode="density-rays"))
     with pytest.raises(ValueError, match="precomputed AO"):
         lv.render_frame(cam, m, None, None, lv.RenderParams(ao_mode="precomputed"))
-    with pytest.raises(NotImplementedError):  # representative lines: SURVEY 8f row 3, not built
-        lv.render_frame(cam, m, None, None, lv.RenderParams(shadow_mode="replines", light_dir=(0, 0, 1)))
+    # replines without a field: render_frame builds what is missing (raycast.py:451-465 ensure_lod is the
+    # CLI's job there; the kernel call itself raises, raycast.py:416-417)
+    from paper_1801_01155_b200.raycast import FramePlan
+    with pytest.raises(ValueError, match="representative-line"):
+        FramePlan(cam, m, None, lv.RenderParams(shadow_mode="replines", light_dir=(0, 0, 1)), 1)
     with pytest.raises(ValueError):
         lv.build_octree(np.zeros((0, 2, 2), np.float32))
 

@@ -97,6 +97,44 @@ def test_geometry_secondary_ray_probes(oracle, mname):
     assert ao.max() > 0.0
 
 
+@pytest.mark.parametrize("mname", ["helices", "turbulence", "wiggles"])
+def test_representative_lines(oracle, mname):
+    """build_rep_lines (lod.py:224-284) with and without the adjacency pass, and
+    replines_shadow (illumination.py:115-139) as point probes."""
+    g = golden("rep_" + mname)
+    m = oracle_model(oracle, golden("vox_" + mname))
+    n_levels = int(g["n_levels"])
+    for adjacency, tag in ((True, ""), (False, "loose_")):
+        rl = oracle.build_rep_lines(m, n_levels, adjacency=adjacency)
+        assert len(rl) == n_levels and rl[0] is None
+        for l in range(1, n_levels):
+            assert np.array_equal(rl[l].valid, g[f"{tag}valid{l}"]), (tag, l)
+            assert np.array_equal(rl[l].a, g[f"{tag}a{l}"]), (tag, l)
+            assert np.array_equal(rl[l].b, g[f"{tag}b{l}"]), (tag, l)
+            assert np.array_equal(rl[l].weight, g[f"{tag}w{l}"]), (tag, l)
+    rl = oracle.build_rep_lines(m, n_levels)
+    P, N, L, lev = g["P"], g["N"], g["L"], g["level"]
+    sh = [oracle.replines_shadow(P[i], L[i], rl, m.dims, level=int(lev[i]), tube_radius=0.3,
+                                 normal=N[i] if i % 2 else None) for i in range(len(P))]
+    assert sh == list(g["shadow"])
+    assert 0 < sum(sh) < len(sh)
+
+
+@pytest.mark.parametrize("name", ["rep_frame_helices", "rep_frame_turbulence"])
+def test_render_with_replines_shadows(oracle, name):
+    g = golden("render_" + name)
+    mname = str(g["model"])
+    m = oracle_model(oracle, golden("vox_" + mname), g["transfer_table"])
+    levels = oracle.build_octree(oracle.compute_density_level0(oracle_model(oracle, golden("vox_" + mname))))
+    rl = oracle.build_rep_lines(m, len(levels))
+    W, H = (int(x) for x in g["size"])
+    kw = dict(render_kwargs(g))
+    nb = kw.pop("neighbor_mode") == "on"
+    img, st = oracle.render(oracle.default_camera(m.dims, W, H), m, levels, neighbor=nb, replines=rl, **kw)
+    assert np.array_equal(img, g["image"]), f"max diff {np.abs(img - g['image']).max()}"
+    assert [st["voxel_steps"], st["intersection_tests"], st["window_overflow"]] == list(g["stats"])
+
+
 def test_tube_and_sphere_primitives(oracle):
     g = golden("prim_tube_sphere")
     r = float(g["r"])
