@@ -343,6 +343,21 @@ int lvx_rep_level(const int32_t child_dims[3], const uint8_t *c_counts_d, const 
 int lvx_probe_replines(const lvx_replines *rep, const double *rays_d, const double *max_t_d,
                        double radius_base, int64_t n, int32_t *out_d, void *stream);
 
+/* Brute-force reference renderer: _kernels.oracle_rows (_kernels.py:926-1082)
+ * behind metrics.brute_force_render (metrics.py:58-107) -- every primitive against every pixel,
+ * hits ordered globally, the shared compositing rules; no DDA, windows or ownership.
+ *   lvx_brute_count   hit_count_d[y*W+x] = hits of the pixel (uncapped)
+ *   lvx_brute_render  hit_off_d = exclusive scan of min(hit_count, 8192) (caller); the hit buffers
+ *                     hold sum(min(hit_count, 8192)) entries; seg_lin_d[i] = home voxel of segment
+ *                     i; row_stats as lvx_render with voxel_steps 0 and the definitional test count */
+int lvx_brute_count(const lvx_camera *cam, const lvx_model *model, const lvx_params *params,
+                    int64_t n_seg, uint32_t *hit_count_d, void *stream);
+int lvx_brute_render(const lvx_camera *cam, const lvx_model *model, const lvx_params *params,
+                     const lvx_lod *lod, int64_t n_seg, const uint32_t *seg_lin_d,
+                     uint32_t *hit_count_d, const int64_t *hit_off_d, double *hit_t_d,
+                     uint64_t *hit_key_d, double *hit_scale_d, double *hit_alpha_d, float *hit_c_d,
+                     float *img_d, int64_t *row_stats_d, void *stream);
+
 /* Geometry secondary rays as point probes.
  * lvx_probe_blocked: _kernels.geometry_ray_blocked (_kernels.py:450-495), the kernel behind
  * illumination.hard_shadow (illumination.py:96-112): rays f64[n,6] = origin + unit direction,

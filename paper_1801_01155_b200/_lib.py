@@ -69,7 +69,7 @@ SYMBOLS = [
     "lvx_render_footprint", "lvx_untile",
     "lvx_fibonacci_dirs", "lvx_ao_bake", "lvx_probe_dda", "lvx_probe_tube", "lvx_probe_sphere",
     "lvx_probe_trilinear", "lvx_probe_cone", "lvx_probe_ao_density", "lvx_probe_blocked",
-    "lvx_probe_ao_hemisphere", "lvx_rep_level", "lvx_probe_replines",
+    "lvx_probe_ao_hemisphere", "lvx_rep_level", "lvx_probe_replines", "lvx_brute_count", "lvx_brute_render",
 ]
 
 _lib = None

@@ -33,6 +33,9 @@ RENDER_CASES = ["opaque_nb", "opaque_own", "alpha25_nb", "alpha25_own_nojoints",
 # frames with shadow_mode="replines" (they also need the representative-line field)
 REP_RENDER_CASES = ["rep_frame_helices", "rep_frame_turbulence"]
 
+# frames of the reference's brute-force renderer (metrics.brute_force_render)
+BRUTE_RENDER_CASES = ["brute_opaque", "brute_alpha_cone_ao", "brute_alpha_nojoints", "brute_hard"]
+
 
 def render_kwargs(g):
     """The RenderParams kwargs a render fixture was made with."""

@@ -334,6 +334,25 @@ def make_replines(models, octrees):
              transfer_table=np.asarray(m.transfer_table, np.float32), size=np.asarray([W, H]), params=np.array(repr(kw)))
 
 
+def make_brute(models, octrees, ao_fields):
+    """The reference's brute-force renderer (metrics.brute_force_render) on small scenes."""
+    from linevox.metrics import brute_force_render
+    cases = [("brute_opaque", "helices", (40, 30), dict(neighbor_mode="on")),
+             ("brute_alpha_cone_ao", "helices", (40, 30), dict(base_opacity=0.3, ao_mode="precomputed", shadow_mode="cone",
+                                                               light_dir=(0.3, 0.2, 1.0))),
+             ("brute_alpha_nojoints", "turbulence", (36, 28), dict(base_opacity=0.2, joint_spheres=False, tau=1.0)),
+             ("brute_hard", "wiggles", (32, 24), dict(base_opacity=0.5, shadow_mode="hard", light_dir=(0.2, -0.3, 1.0)))]
+    for name, mname, (W, H), kw in cases:
+        m, dims = models[mname]
+        m.ao = ao_fields[mname].values if mname in ao_fields else None
+        m.transfer_table = RV.default_transfer_table()
+        fr = brute_force_render(RR.default_camera(dims, W, H), m, octrees.get(mname), None, RR.RenderParams(**kw), workers=4)
+        st = fr.stats
+        save("render_" + name, image=fr.image, model=np.array(mname),
+             stats=np.asarray([st["voxel_steps"], st["intersection_tests"], st["window_overflow"]], np.int64),
+             transfer_table=np.asarray(m.transfer_table, np.float32), size=np.asarray([W, H]), params=np.array(repr(kw)))
+
+
 def main():
     global ONLY
     if "--only" in sys.argv:
@@ -345,6 +364,7 @@ def main():
     make_primitives(models, octrees, ao_fields)
     make_geometry_probes(models)
     make_replines(models, octrees)
+    make_brute(models, octrees, ao_fields)
 
 
 if __name__ == "__main__":

@@ -5,7 +5,8 @@ counters; point probes bit-exact except where CUDA libm differs (pow)."""
 import numpy as np
 import pytest
 
-from conftest import RENDER_CASES, REP_RENDER_CASES, VOX_CASES, assert_model_equal, golden, render_kwargs
+from conftest import (BRUTE_RENDER_CASES, RENDER_CASES, REP_RENDER_CASES, VOX_CASES, assert_model_equal, golden,
+                      render_kwargs)
 
 pytestmark = pytest.mark.gpu
 
@@ -144,6 +145,44 @@ def test_representative_lines(lv, mname):
         lv.replines_shadow(P[0], L[0], rl, m.spec.dims, level=0)
     with pytest.raises(ValueError):
         lv.replines_shadow(P[0], L[0], rl, m.spec.dims, level=99)
+
+
+@pytest.mark.parametrize("name", BRUTE_RENDER_CASES)
+def test_brute_force_render(lv, name):
+    """The GPU brute-force renderer (every primitive at every pixel, no DDA) against the
+    reference's brute_force_render, and against both accelerated engines on the same scene:
+    the reference's own cross-check (tests/test_metrics.py:117-125, test_illumination.py:363-387)."""
+    g = golden("render_" + name)
+    mname = str(g["model"])
+    vg = golden("vox_" + mname)
+    m = gpu_model(lv, vg, g["transfer_table"])
+    oc = lv.build_lod(gpu_model(lv, vg))
+    if mname in ("helices", "turbulence"):
+        m.ao = golden("ao_" + mname)["values"]
+    W, H = (int(x) for x in g["size"])
+    cam = lv.default_camera(m.spec.dims, W, H)
+    params = lv.RenderParams(**render_kwargs(g))
+    fr = lv.brute_force_render(cam, m, oc, None, params)
+    err = np.abs(fr.image.astype(np.float64) - g["image"].astype(np.float64))
+    assert err.max() <= MAX_ERR and err.mean() < MEAN_ERR
+    assert (err > 1e-6).mean() < 1e-3
+    st = fr.stats
+    assert [st["voxel_steps"], st["intersection_tests"], st["window_overflow"]] == list(g["stats"])
+    n_prim = (3 if params.joint_spheres else 1) * m.segment_count
+    assert st["intersection_tests"] == W * H * n_prim  # tests/test_metrics.py:128-134
+    # the accelerated engines agree with it to the bit (neighbour mode: the brute force has no
+    # notion of own-voxel gathering)
+    import os
+    for engine in ("tile", "wavefront"):
+        os.environ["LVX_ENGINE"] = engine
+        try:
+            acc = lv.render_frame(cam, m, oc, None, lv.RenderParams(**{**render_kwargs(g), "neighbor_mode": "on"}))
+        finally:
+            os.environ.pop("LVX_ENGINE", None)
+        assert np.array_equal(acc.image, fr.image), engine
+    cmp_ = lv.image_compare(fr, g["image"])
+    assert cmp_["fraction_close"] == 1.0
+    assert lv.memory_report(m)["total"] == 5 * m.voxel_count + m.record_width * m.segment_count
 
 
 def test_tube_and_sphere_probes(lv):

@@ -8,7 +8,7 @@ S=paper_1801_01155_b200/csrc
 while [ $# -gt 1 ]; do
   name=$1; flags=$2; shift 2
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -fmad=false -prec-div=true -prec-sqrt=true -ftz=false \
-    -Xcompiler -fPIC -shared $flags $S/lvx_api.cu $S/lvx_voxelize.cu $S/lvx_lod.cu $S/lvx_render.cu $S/lvx_wavefront.cu $S/lvx_ao.cu $S/lvx_rep.cu -o build/variants/$name.so &
+    -Xcompiler -fPIC -shared $flags $S/lvx_api.cu $S/lvx_voxelize.cu $S/lvx_lod.cu $S/lvx_render.cu $S/lvx_wavefront.cu $S/lvx_ao.cu $S/lvx_rep.cu $S/lvx_brute.cu -o build/variants/$name.so &
 done
 wait
 ls -la build/variants
