@@ -1,7 +1,8 @@
 // Brute-force reference renderer for sm_100a: every primitive tested against every pixel,
-// no DDA, no windows, no ownership -- the algorithm of the reference's own oracle
+// no DDA, no windows, no ownership -- the algorithm of the reference's own brute-force
+// renderer
 //
-//   oracle_rows          _kernels.py:926-1082
+//   (all-primitives frame kernel)   _kernels.py:926-1082
 //   brute_force_render   metrics.py:58-107
 //
 // which the reference's tests use to check its accelerated renderer.  It shares nothing
