@@ -172,6 +172,19 @@ struct WfArgs {
     int wn_sched, cand_budget, grow_from, grow_bits, wn_shift_max, tail_rays, tail_bits;
 };
 
+// Rays per warp in the ray-parallel kernels (walk, composite).  Lanes of a warp run their rays
+// in lock step, so a warp is as slow as the union of its rays' paths; once the live list is
+// shorter than the launch, the rays are spread over more warps: ray i is worked on by thread
+// i << spread (the other lanes only take part in the warp-cooperative steps).
+#ifndef LVX_WF_SPREAD_MAX
+#define LVX_WF_SPREAD_MAX 5
+#endif
+__device__ __forceinline__ u32 wf_spread(u32 n_live, u32 threads) {
+    u32 ls = 0;
+    while (ls < (u32)LVX_WF_SPREAD_MAX && ((unsigned long long)n_live << (ls + 1)) <= threads) ++ls;
+    return ls;
+}
+
 // sub-queue of the warp that works on flat index f (warp-uniform: f is lane + a multiple of 32)
 __device__ __forceinline__ int warp_queue(u32 f) { return (int)((f >> 5) & (kNQ - 1)); }
 
@@ -478,10 +491,11 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_WALK_MINB) wf_walk_kernel(c
     if (lane == 0) S.n[warp] = 0;
     __syncwarp();
     // (the loop bound is warp-uniform: the stage is flushed by the whole warp)
-    for (u32 i0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); i0 < n_live; i0 += gridDim.x * blockDim.x) {
-        const u32 i = i0 + (u32)lane;
-        const int q = warp_queue(i0);
-        if (i < n_live) {
+    const u32 spread = wf_spread(n_live, gridDim.x * blockDim.x);
+    for (u32 g0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); (g0 >> spread) < n_live; g0 += gridDim.x * blockDim.x) {
+        const u32 i = (g0 + (u32)lane) >> spread;
+        const int q = warp_queue(g0);
+        if ((((u32)lane) & ((1u << spread) - 1u)) == 0 && i < n_live) {
         const u32 slot = A.live[par][i];
         WfRayWalk rw = A.rw[slot];
         const double ddx = rw.dir[0], ddy = rw.dir[1], ddz = rw.dir[2];
@@ -1063,9 +1077,10 @@ __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A
     const double tau = A.p.tau;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // (the loop bound is warp-uniform: rays with many hits are ordered by the whole warp)
-    for (u32 i0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); i0 < n_live; i0 += gridDim.x * blockDim.x) {
-        const u32 i = i0 + (u32)lane;
-        const bool valid = i < n_live;
+    const u32 spread = wf_spread(n_live, gridDim.x * blockDim.x);
+    for (u32 g0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); (g0 >> spread) < n_live; g0 += gridDim.x * blockDim.x) {
+        const u32 i = (g0 + (u32)lane) >> spread;
+        const bool valid = (((u32)lane) & ((1u << spread) - 1u)) == 0 && i < n_live;
         u32 slot = 0, nhit = 0, fl = 1;
         if (valid) {
             slot = A.live[par][i];
@@ -1522,7 +1537,9 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
                       params->ao_mode == LVX_AO_HEMISPHERE;
     cudaStream_t st = (cudaStream_t)stream;
     const int sms = lvx_sm_count();
-    const unsigned grid_rays = (unsigned)(sms * 8), grid_q = (unsigned)(sms * 8);
+    int rays_mult = 8;
+    if (const char *e = getenv("LVX_WF_GRID_RAYS")) rays_mult = atoi(e) > 0 ? atoi(e) : rays_mult;
+    const unsigned grid_rays = (unsigned)(sms * rays_mult), grid_q = (unsigned)(sms * 8);
     wf_begin_kernel<<<1, 64, 0, st>>>(A);
     wf_init_kernel<<<(unsigned)lvx_ceil_div(R, kThreadsWf), kThreadsWf, 0, st>>>(A);
     LVX_LAUNCH_CHECK();
