@@ -88,6 +88,12 @@ __device__ __forceinline__ unsigned long long hit_gather(unsigned long long k) {
 
 constexpr int kHitSlots = 12;      // hits per ray and iteration stored ray-parallel (the rest is listed)
 
+// what an exact test needs of its ray, by place: one 32-byte sector, two hops from the queue
+// entry (entry -> item_place -> here) instead of three (-> live -> the ray's state record)
+struct __align__(32) WfRayDir {
+    double dx, dy, dz, t_lo;
+};
+
 struct WfEntry {
     u32 seg;   // segment (| sphere B << 31 in the sphere queue)
     u32 item;  // the (ray, voxel) item it came from
@@ -162,6 +168,7 @@ struct WfArgs {
     u32 capq_item;
     float *fdir;                 // [3][R] float32 ray direction by place
     double *span;                // [2][R] parameter range walked this iteration, by place
+    WfRayDir *rdir;              // [R] float64 direction + start of the walked range, by place (exact kernels)
     WfEntry *tube, *sph;
     u32 capq_surv;
     WfHit *hit;       // overflow pool (linked lists)
@@ -604,6 +611,12 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_WALK_MINB) wf_walk_kernel(c
         A.fdir[2 * R + i] = (float)ddz;
         A.span[i] = span0;
         A.span[R + i] = dda.t_cur;
+        WfRayDir rd;
+        rd.dx = ddx;
+        rd.dy = ddy;
+        rd.dz = ddz;
+        rd.t_lo = span0;
+        A.rdir[i] = rd;
         }
         walk_flush(A, S, warp, lane, q);
     }
@@ -833,8 +846,9 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_EXACT_MINB) wf_exact_kernel
         const WfEntry c = queue[queue_view_index(V, f, A.capq_surv)];
         const u32 seg = c.seg & 0x7FFFFFFFu;
         const u32 place = A.item_place[c.item];
-        const u32 slot = A.live[par][place];
-        const double rdx = A.rw[slot].dir[0], rdy = A.rw[slot].dir[1], rdz = A.rw[slot].dir[2];
+        const u32 slot = A.live[par][place];  // (only needed once there is a hit)
+        const WfRayDir rd = A.rdir[place];
+        const double rdx = rd.dx, rdy = rd.dy, rdz = rd.dz;
         const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + seg));
         LvxHit h;
         bool hit;
@@ -861,7 +875,7 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_EXACT_MINB) wf_exact_kernel
         // walked this iteration is owned by exactly one of this iteration's windows
         if (!hit) continue;
         if (neighbor) {
-            if (!(A.span[place] <= h.t_in && h.t_in < A.span[R + place])) continue;
+            if (!(rd.t_lo <= h.t_in && h.t_in < A.span[R + place])) continue;
         } else {
             const double2 tr = A.item_t[c.item];
             if (!(tr.x <= h.t_in && h.t_in < tr.y)) continue;
@@ -1328,7 +1342,7 @@ __global__ void wf_begin_kernel(const WfArgs A) {
 struct WfLayout {
     size_t total;
     size_t ctl, rw, rp, head, tab_key, tab_mask, tab_sph, pool_key, pool_mask, pool_sph, live0, live1, win,
-        win_over, item_place, item_lin, item_q, item_t, fdir, span, tube, sph, hit, hit_slot, hcnt;
+        win_over, item_place, item_lin, item_q, item_t, fdir, span, rdir, tube, sph, hit, hit_slot, hcnt;
     u32 R, pool_cap, cap_win, capq_item, capq_surv, capq_hit;
 };
 
@@ -1370,6 +1384,7 @@ WfLayout wf_layout(i64 R, double scale) {
     L.item_t = take(c, (size_t)L.capq_item * kNQ * 16);
     L.fdir = take(c, r * 12);
     L.span = take(c, r * 16);
+    L.rdir = take(c, r * sizeof(WfRayDir));
     L.tube = take(c, (size_t)L.capq_surv * kNQ * sizeof(WfEntry));
     L.sph = take(c, (size_t)L.capq_surv * kNQ * sizeof(WfEntry));
     L.hit = take(c, (size_t)L.capq_hit * kNQ * sizeof(WfHit));
@@ -1509,6 +1524,7 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     A.item_t = (double2 *)(base + L.item_t);
     A.fdir = (float *)(base + L.fdir);
     A.span = (double *)(base + L.span);
+    A.rdir = (WfRayDir *)(base + L.rdir);
     A.capq_item = L.capq_item;
     A.tube = (WfEntry *)(base + L.tube);
     A.sph = (WfEntry *)(base + L.sph);
