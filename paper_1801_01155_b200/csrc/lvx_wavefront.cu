@@ -95,8 +95,9 @@ struct __align__(32) WfRayDir {
 };
 
 struct WfEntry {
-    u32 seg;   // segment (| sphere B << 31 in the sphere queue)
-    u32 item;  // the (ray, voxel) item it came from
+    u32 seg;    // segment (| sphere B << 31 in the sphere queue)
+    u32 item;   // the (ray, voxel) item it came from
+    u32 place;  // the ray's position in the live list (saves the exact kernels a dependent load)
 };
 
 // per-ray state, one record per pixel slot (read and written with 16-byte accesses)
@@ -638,7 +639,7 @@ __device__ __forceinline__ bool wf_near_line(float cx, float cy, float cz, float
 // ---------------------------------------------------------------------------------------
 // what the pre-reject needs of one item
 struct CandItem {
-    u32 it, cnt, base;
+    u32 it, cnt, base, place;
     float q0x, q0y, q0z, fdx, fdy, fdz, fhx, fhy, fhz;
 };
 
@@ -719,7 +720,7 @@ __device__ __forceinline__ void cand_segment(const WfArgs &A, CandStage &S, int 
     s0 = __shfl_sync(act, s0, leader);
     if (mk & 1u) {
         const u32 pos = t0 + (u32)__popc(bt & lt);
-        const WfEntry c = {seg, I.it};
+        const WfEntry c = {seg, I.it, I.place};
         if (pos < (u32)kStageTube) {
             S.tube[warp][pos] = c;
         } else {
@@ -729,7 +730,7 @@ __device__ __forceinline__ void cand_segment(const WfArgs &A, CandStage &S, int 
     }
     if (mk & 6u) {
         u32 pos = s0 + (u32)(__popc(ba & lt) + __popc(bb & lt));
-        WfEntry c = {seg, I.it};
+        WfEntry c = {seg, I.it, I.place};
         if (mk & 2u) {
             if (pos < (u32)kStageSph) {
                 S.sph[warp][pos] = c;
@@ -784,6 +785,7 @@ __global__ void __launch_bounds__(kThreadsWf) wf_cand_kernel(const WfArgs A) {
             have[k] = fk < total;
             I[k].it = queue_view_index(V, have[k] ? fk : 0u, A.capq_item);
             place[k] = A.item_place[I[k].it];
+            I[k].place = place[k];
             lin[k] = A.item_lin[I[k].it];
             q0[k] = A.item_q[I[k].it];
         }
@@ -845,7 +847,7 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_EXACT_MINB) wf_exact_kernel
         const int q = warp_queue(f);
         const WfEntry c = queue[queue_view_index(V, f, A.capq_surv)];
         const u32 seg = c.seg & 0x7FFFFFFFu;
-        const u32 place = A.item_place[c.item];
+        const u32 place = c.place;
         const u32 slot = A.live[par][place];  // (only needed once there is a hit)
         const WfRayDir rd = A.rdir[place];
         const double rdx = rd.dx, rdy = rd.dy, rdz = rd.dz;
