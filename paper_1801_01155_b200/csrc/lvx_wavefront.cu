@@ -175,7 +175,7 @@ struct WfArgs {
     WfHit *hit;       // overflow pool (linked lists)
     u32 capq_hit;
     WfHit *hit_slot;  // [kHitSlots][R], indexed by the ray's position in the live list
-    u32 *hcnt;        // hits of the ray this iteration
+    u32 *hcnt;        // hits of the ray this iteration, by place
     u32 *win_over;  // [cap_win] overflow of a window (slow path only)
     int wn_sched, cand_budget, grow_from, grow_bits, wn_shift_max, tail_rays, tail_bits;
 };
@@ -364,6 +364,12 @@ __global__ void __launch_bounds__(kThreadsWf) wf_init_kernel(const WfArgs A) {
 
     unsigned long long steps = 0;
     bool live = false;
+    // hit counters and overflow-list heads are indexed by PLACE (position in the live list of
+    // the iteration): every possible place starts empty, composite re-empties what it reads
+    if (tile_ok) {
+        A.head[slot] = kNil;
+        A.hcnt[slot] = 0;
+    }
     if (active) {
         double ddx, ddy, ddz;
         ray_dir(A.cam, x, y, ddx, ddy, ddz);
@@ -400,8 +406,6 @@ __global__ void __launch_bounds__(kThreadsWf) wf_init_kernel(const WfArgs A) {
             rp.out_off = (u32)o;
             rp.pad = 0;
             A.rp[slot] = rp;
-            A.head[slot] = kNil;
-            A.hcnt[slot] = 0;
             live = true;
         } else {
             write_pixel(A, (u32)o, 0.0, 0.0, 0.0, 0.0);
@@ -848,7 +852,6 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_EXACT_MINB) wf_exact_kernel
         const WfEntry c = queue[queue_view_index(V, f, A.capq_surv)];
         const u32 seg = c.seg & 0x7FFFFFFFu;
         const u32 place = c.place;
-        const u32 slot = A.live[par][place];  // (only needed once there is a hit)
         const WfRayDir rd = A.rdir[place];
         const double rdx = rd.dx, rdy = rd.dy, rdz = rd.dz;
         const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + seg));
@@ -898,13 +901,13 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_EXACT_MINB) wf_exact_kernel
         rec.cy = ccy;
         rec.cz = ccz;
         rec.next = kNil & ~kDropped;
-        const u32 j = atomicAdd(&A.hcnt[slot], 1u);
+        const u32 j = atomicAdd(&A.hcnt[place], 1u);
         if (j < (u32)kHitSlots) {
             A.hit_slot[(size_t)j * R + place] = rec;
         } else {
             const u32 e = queue_alloc_bits(A.ctl->hit_cnt, q, A.capq_hit, true, false, &A.ctl->err, 4u);
             if (e == kNil) continue;
-            rec.next = atomicExch(&A.head[slot], e) & ~kDropped;
+            rec.next = atomicExch(&A.head[place], e) & ~kDropped;
             A.hit[e] = rec;
         }
     }
@@ -1100,7 +1103,7 @@ __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A
         u32 slot = 0, nhit = 0, fl = 1;
         if (valid) {
             slot = A.live[par][i];
-            nhit = A.hcnt[slot];
+            nhit = A.hcnt[i];
             fl = A.rw[slot].flags;
         }
         bool finished = valid && !(fl & 1);  // the walk is over: this was the last batch
@@ -1118,10 +1121,10 @@ __global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A
             for (int j = 0; j < kHitSlots; ++j)
                 if ((u32)j < nhit) asm volatile("prefetch.global.L1 [%0];" ::"l"(A.hit_slot + (size_t)j * R + i));
             asm volatile("prefetch.global.L1 [%0];" ::"l"(A.rp + slot));
-            A.hcnt[slot] = 0;
+            A.hcnt[i] = 0;
             if (nhit > (u32)kHitSlots) {
-                H.head = A.head[slot];
-                A.head[slot] = kNil;
+                H.head = A.head[i];
+                A.head[i] = kNil;
             }
             nw = A.rw[slot].nwin;
             if (big) wf_apply_window_cap(A, H, wins, nw, w0);
