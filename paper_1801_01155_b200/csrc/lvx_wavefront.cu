@@ -177,7 +177,8 @@ struct WfArgs {
     WfHit *hit_slot;  // [kHitSlots][R], indexed by the ray's position in the live list
     u32 *hcnt;        // hits of the ray this iteration, by place
     u32 *win_over;  // [cap_win] overflow of a window (slow path only)
-    int wn_sched, cand_budget, grow_from, grow_bits, wn_shift_max, tail_rays, tail_bits;
+    int wn_sched, cand_budget, grow_from, grow_bits, wn_shift_max, tail_rays, tail_bits, tail_mode;
+    u32 ray_threads;  // threads of a walk / composite launch
 };
 
 // Rays per warp in the ray-parallel kernels (walk, composite).  Lanes of a warp run their rays
@@ -1320,6 +1321,13 @@ __global__ void wf_next_kernel(const WfArgs A, int par, int it_next) {
             int sh = g < 0 ? 0 : g * A.grow_bits;
             // the last few thousand rays: finish them in few iterations (their over-scan is noise)
             if (live < (u32)A.tail_rays) sh += A.tail_bits;
+            // once the rays are spread over the warps (wf_spread) a ray no longer waits for
+            // the others of its warp: a larger budget then only saves iterations
+            const u32 ls = wf_spread(live, A.ray_threads);
+            if (A.tail_mode == 1) sh += (ls >= 3 ? 1 : 0) + (ls >= 5 ? 1 : 0);
+            else if (A.tail_mode == 2) sh += (ls >= 2 ? 1 : 0) + (ls >= 4 ? 1 : 0);
+            else if (A.tail_mode == 3) sh += (ls >= 3 ? 1 : 0) + (ls >= 5 ? 2 : 0);
+            else if (A.tail_mode == 4) sh += (ls >= 1 ? 1 : 0) + (ls >= 5 ? 1 : 0);
             A.ctl->budget = (u32)A.cand_budget << (sh < 12 ? sh : 12);
         }
     }
@@ -1544,6 +1552,8 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     A.grow_bits = 1;
     A.tail_rays = 0;
     A.tail_bits = 4;
+    A.tail_mode = 1;
+    if (const char *e = getenv("LVX_WF_TAIL_MODE")) A.tail_mode = atoi(e);
     if (const char *e = getenv("LVX_WF_TAIL_RAYS")) A.tail_rays = atoi(e);
     if (const char *e = getenv("LVX_WF_TAIL_BITS")) A.tail_bits = atoi(e);
     A.wn_shift_max = 4;
@@ -1561,6 +1571,7 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     int rays_mult = 8;
     if (const char *e = getenv("LVX_WF_GRID_RAYS")) rays_mult = atoi(e) > 0 ? atoi(e) : rays_mult;
     const unsigned grid_rays = (unsigned)(sms * rays_mult), grid_q = (unsigned)(sms * 8);
+    A.ray_threads = grid_rays * (unsigned)kThreadsWf;
     wf_begin_kernel<<<1, 64, 0, st>>>(A);
     wf_init_kernel<<<(unsigned)lvx_ceil_div(R, kThreadsWf), kThreadsWf, 0, st>>>(A);
     LVX_LAUNCH_CHECK();

@@ -243,6 +243,23 @@ def test_frame_engines_agree_and_queue_overflow_is_retried(lv, synth):
     assert out["wavefront-small"][2] > 1.0 / 64.0  # the low-opacity frame does not fit the tiny queues
 
 
+def test_frame_written_to_pinned_host_memory_equals_device_frame(lv, synth, monkeypatch):
+    """render_frame lets the kernels write the image straight into pinned host memory (the
+    default) or into HBM followed by a copy: same bytes, same counters, both engines."""
+    dims = (24, 24, 24)
+    m = lv.build_voxel_model(lv.CurveSet.from_flat(*synth.turbulence(1500, 50, dims)), lv.GridSpec(dims))
+    oc = lv.build_lod(m)
+    cam = lv.default_camera(dims, 203, 117)
+    for kw in (dict(base_opacity=0.2, neighbor_mode="on"), dict(base_opacity=0.2, neighbor_mode="off")):
+        out = {}
+        for where in ("host", "device"):
+            monkeypatch.setenv("LVX_FRAME_OUT", where)
+            fr = lv.render_frame(cam, m, oc, None, lv.RenderParams(**kw))
+            out[where] = (fr.image.copy(), {k: v for k, v in fr.stats.items() if k != "ms"})
+        assert np.array_equal(out["host"][0], out["device"][0]), kw
+        assert out["host"][1] == out["device"][1], kw
+
+
 def test_model_from_encoded_arrays_only(lv, synth):
     """a model that arrives as (counts, offsets, packed) only -- what a .vxl
     file holds -- is decoded on the device (lvx_decode_packed, model_io.py:151-179): caches
