@@ -757,7 +757,10 @@ __device__ __forceinline__ void cand_segment(const WfArgs &A, CandStage &S, int 
     }
 }
 
-__global__ void __launch_bounds__(kThreadsWf) wf_cand_kernel(const WfArgs A) {
+#ifndef LVX_WF_CAND_MINB
+#define LVX_WF_CAND_MINB 4
+#endif
+__global__ void __launch_bounds__(kThreadsWf, LVX_WF_CAND_MINB) wf_cand_kernel(const WfArgs A) {
     __shared__ QueueView V;
     __shared__ CandStage S;
     queue_view_load(V, A.ctl->item_cnt, A.capq_item, A.ctl->err);
@@ -1088,7 +1091,10 @@ struct SortStage {
     u32 n[kThreadsWf / 32];
 };
 
-__global__ void __launch_bounds__(kThreadsWf) wf_composite_kernel(const WfArgs A, int par) {
+#ifndef LVX_WF_COMP_MINB
+#define LVX_WF_COMP_MINB 4
+#endif
+__global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_kernel(const WfArgs A, int par) {
     constexpr unsigned FULL = 0xFFFFFFFFu;
     __shared__ SortStage Q;
     const u32 n_live = A.ctl->err ? 0u : A.ctl->n_live[par];
