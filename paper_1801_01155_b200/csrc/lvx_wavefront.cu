@@ -1040,14 +1040,23 @@ struct WfRayHits {
 
 // Index (within the ray's windows of this iteration) of the window that owns parameter t:
 // the first one whose range ends after t.
+// (8-way search: the seven probes of a round are independent loads, so 128 windows take three
+// memory round trips instead of seven)
 __device__ __forceinline__ u32 wf_find_window(const WfWindow *w, u32 nw, double t) {
-    u32 lo = 0, hi = nw;  // answer in [lo, hi)
-    while (hi - lo > 1) {
-        const u32 mid = (lo + hi) >> 1;
-        if (w[mid - 1].t1 > t) hi = mid;
-        else lo = mid;
+    u32 lo = 0, hi = nw;  // answer in [lo, hi); "answer >= p" <=> w[p - 1].t1 <= t (ends are monotonic)
+    while (hi - lo > 8) {
+        const u32 step = (hi - lo) >> 3;
+        u32 c = 0;
+#pragma unroll
+        for (u32 j = 1; j < 8; ++j) c += w[lo + j * step - 1].t1 <= t ? 1u : 0u;
+        if (c < 7) hi = lo + (c + 1) * step;
+        lo += c * step;
     }
-    return lo;
+    u32 c = 0;
+#pragma unroll
+    for (u32 j = 1; j < 8; ++j)
+        if (lo + j < hi) c += w[lo + j - 1].t1 <= t ? 1u : 0u;
+    return lo + c;
 }
 
 // Slow path for rays that crossed a window with more than 1024/3 candidates: the reference
