@@ -254,7 +254,10 @@ typedef struct {
 } lvx_tiling;
 
 /* img_d f32, row_stats_d i64[H,3] (steps, tests, overflow; caller zeroes it),
- * hitbuf_d: per-thread hit scratch, lvx_render_scratch_bytes() bytes. */
+ * hitbuf_d: per-thread hit scratch, lvx_render_scratch_bytes() bytes.
+ * Every pixel of the image is written exactly once and never read, so img_d may also be
+ * pinned host memory mapped into the device's address space (cudaHostAlloc under unified
+ * addressing): the image then reaches the host while the frame is still being computed. */
 size_t lvx_render_scratch_bytes(const lvx_camera *cam, const lvx_tiling *tiling);
 int lvx_render(const lvx_camera *cam, const lvx_model *model, const lvx_params *params,
                const lvx_lod *lod, const lvx_tiling *tiling, float *img_d,
