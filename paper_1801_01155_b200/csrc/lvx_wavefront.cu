@@ -128,6 +128,7 @@ struct WfCtl {
     u32 err;   // bit 0 items / candidates, 1 survivors, 2 listed hits, 3 table pool
     u32 wn;    // windows per ray of the current iteration
     u32 budget;  // candidate budget per ray of the current iteration (neighbour-sum units)
+    u32 live0;   // rays alive after the first iteration (what "few rays left" is measured against)
 };
 
 struct WfArgs {
@@ -177,7 +178,7 @@ struct WfArgs {
     WfHit *hit_slot;  // [kHitSlots][R], indexed by the ray's position in the live list
     u32 *hcnt;        // hits of the ray this iteration, by place
     u32 *win_over;  // [cap_win] overflow of a window (slow path only)
-    int wn_sched, cand_budget, grow_from, grow_bits, wn_shift_max, tail_rays, tail_bits, tail_mode;
+    int wn_sched, cand_budget, grow_from, grow_bits, wn_shift_max, tail_rays, tail_bits, tail_mode, tail_from;
     u32 ray_threads;  // threads of a walk / composite launch
 };
 
@@ -1338,7 +1339,14 @@ __global__ void wf_next_kernel(const WfArgs A, int par, int it_next) {
             if (live < (u32)A.tail_rays) sh += A.tail_bits;
             // once the rays are spread over the warps (wf_spread) a ray no longer waits for
             // the others of its warp: a larger budget then only saves iterations
-            const u32 ls = wf_spread(live, A.ray_threads);
+            // (only the tail of a frame: rays that have survived tail_from iterations, once
+            // fewer than 1/16 of the frame's rays are left -- those rarely terminate and collect
+            // few hits, so walking further ahead of the compositing is not wasted; in a small or
+            // very transparent frame every ray is spread and long-lived, and a larger budget
+            // only pushes rays onto the many-hits paths of the composite kernel)
+            if (it_next == 1) A.ctl->live0 = live;
+            const bool tail = it_next >= A.tail_from && (unsigned long long)live * 16u <= A.ctl->live0;
+            const u32 ls = tail ? wf_spread(live, A.ray_threads) : 0u;
             if (A.tail_mode == 1) sh += (ls >= 3 ? 1 : 0) + (ls >= 5 ? 1 : 0);
             else if (A.tail_mode == 2) sh += (ls >= 2 ? 1 : 0) + (ls >= 4 ? 1 : 0);
             else if (A.tail_mode == 3) sh += (ls >= 3 ? 1 : 0) + (ls >= 5 ? 2 : 0);
@@ -1569,6 +1577,8 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     A.tail_bits = 4;
     A.tail_mode = 1;
     if (const char *e = getenv("LVX_WF_TAIL_MODE")) A.tail_mode = atoi(e);
+    A.tail_from = 6;
+    if (const char *e = getenv("LVX_WF_TAIL_FROM")) A.tail_from = atoi(e);
     if (const char *e = getenv("LVX_WF_TAIL_RAYS")) A.tail_rays = atoi(e);
     if (const char *e = getenv("LVX_WF_TAIL_BITS")) A.tail_bits = atoi(e);
     A.wn_shift_max = 4;

@@ -345,6 +345,9 @@ def default_engine() -> str:
 _WF_SCRATCH = {}
 
 
+_WF_SCALE = {}  # frame shape -> queue scale that shape needed so far
+
+
 def _wf_scratch(cam, til, scale: float):
     """Scratch buffer of the wavefront engine, cached per device and grown on demand."""
     torch = _lib.require_device()
@@ -375,7 +378,11 @@ class FramePlan:
             self.engine = "wavefront" if neighbor else "tile"
         if self.engine not in ("wavefront", "tile"):
             raise ValueError(f"unknown frame engine {self.engine!r}")
-        self._scale = 1.0
+        # queue scale that this frame shape last needed (a frame whose queues overflow is
+        # repeated with doubled queues: remember it, render_frame builds a plan per call)
+        self._shape = (int(camera.width), int(camera.height), int(tile_first), int(tile_step), bool(compact),
+                       int(tile_w), int(tile_h))
+        self._scale = _WF_SCALE.get(self._shape, 1.0)
         self.cam = camera_struct(camera)
         self.par = params_struct(params, neighbor)
         geometry_rays = params.shadow_mode == "hard" or params.ao_mode == "hemisphere-geometry"
@@ -438,6 +445,8 @@ class FramePlan:
                                  C.c_double(self._scale), _lib.stream_ptr())
             if rc == 4 and self._scale < 64.0:  # LVX_E_RANGE: queues too small for this scene
                 self._scale *= 2.0
+                if self._scale > _WF_SCALE.get(self._shape, 1.0):
+                    _WF_SCALE[self._shape] = self._scale
                 row_stats_d.zero_()
                 continue
             _lib.check(rc)
