@@ -398,7 +398,10 @@ def run_ours(args, wl):
         "frame_stats": {"voxel_steps": tot[0], "intersection_tests": tot[1], "window_overflow": tot[2]},
         "kernel_ms": kern_ms, "engine": plan.engine,
         "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "api": "render_frame" if world == 1 else "render_frame_tiled"},
+                "api": "render_frame" if world == 1 else "render_frame_tiled",
+                "image_path": ("kernels write each finished pixel into the pinned host image through its device "
+                               "mapping (counted in d2h_bytes_per_step); counters copied after the frame")
+                if world == 1 else "tiles gathered to rank 0 over NCCL, then one copy to pinned host memory"},
         "gpu_launches": gpu_launches,
         "clocks": clocks.summary(),
         "roofline": roofline,
