@@ -1090,7 +1090,7 @@ __device__ __forceinline__ bool wf_composite_one(const WfArgs &A, WfTables &T, W
 }
 
 #ifndef LVX_WF_LIGHT
-#define LVX_WF_LIGHT 12
+#define LVX_WF_LIGHT 8
 #endif
 constexpr int kLight = LVX_WF_LIGHT;  // up to this many hits a ray orders by itself; more are ranked by its warp
 
