@@ -121,6 +121,11 @@ struct __align__(16) WfRayPix {    // owned by the compositor
 static_assert(sizeof(WfRayPix) == 80, "pixel state is 80 bytes");
 
 // control block in device memory
+// windows a ray may record in the first iteration (doubling per iteration after that); also
+// what the window arrays are sized for.  Swept with the spread / tail rules in place: 8 -> 12 is
+// worth 0.05-0.15 ms on C2, C3 and the 1M-line scene.
+constexpr int kWinFirst = 12;
+
 struct WfCtl {
     u32 n_live[2];
     u32 item_cnt[kNQ], tube_cnt[kNQ], sph_cnt[kNQ], hit_cnt[kNQ];
@@ -1369,7 +1374,9 @@ __global__ void wf_begin_kernel(const WfArgs A) {
         A.ctl->n_live[1] = 0;
         A.ctl->pool_cnt = 0;
         A.ctl->err = 0;
-        A.ctl->wn = (u32)A.wn_sched;
+        // (the window records of iteration 0 must fit whatever LVX_WF_WN asks for)
+        const u32 fit = A.R ? (u32)(A.cap_win / A.R) : A.cap_win;
+        A.ctl->wn = (u32)A.wn_sched < fit ? (u32)A.wn_sched : (fit ? fit : 1u);
         A.ctl->budget = (u32)A.cand_budget;
     }
 }
@@ -1394,7 +1401,7 @@ WfLayout wf_layout(i64 R, double scale) {
     L.R = (u32)R;
     const double f = scale < 1.0 / 64.0 ? 1.0 / 64.0 : scale;  // (< 1 only to exercise the overflow path)
     L.pool_cap = (u32)(R / 16 * f) + 1024;
-    L.cap_win = (u32)fmin(4.0e9, (double)R * 8.0);
+    L.cap_win = (u32)fmin(4.0e9, (double)R * (double)kWinFirst);  // every ray may record kWinFirst windows in iteration 0
     L.capq_item = (u32)fmin(4.0e9 / kNQ, ((double)R * 24.0 * f + 65536.0) / kNQ);
     L.capq_surv = (u32)fmin(4.0e9 / kNQ, ((double)R * 10.0 * f + 65536.0) / kNQ);
     L.capq_hit = (u32)fmin(4.0e9 / kNQ, ((double)R * 2.0 * f + 65536.0) / kNQ);
@@ -1569,7 +1576,7 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     A.capq_hit = L.capq_hit;
     A.hit_slot = (WfHit *)(base + L.hit_slot);
     A.hcnt = (u32 *)(base + L.hcnt);
-    A.wn_sched = 8;
+    A.wn_sched = kWinFirst;
     A.cand_budget = 192;
     A.grow_from = 24;  // (growing earlier does not pay: the late iterations are cheap, over-scanning is not)
     A.grow_bits = 1;
