@@ -294,6 +294,14 @@ int lvx_render_footprint(const lvx_camera *cam, const lvx_model *model, const lv
 int lvx_untile(const float *tiles_d, const lvx_tiling *tiling, int32_t width, int32_t height,
                float *img_d, void *stream);
 
+/* Multi-GPU frame assembly on the gathering rank (no reference counterpart: the reference is
+ * single-process, raycast.py:468-521 writes rows in place): the compact tile buffers of all
+ * `world` ranks, rank r's at recv_d + r * rank_stride_floats (tile k of the frame is tile
+ * k / world of rank k % world, tiles of tile_w x tile_h RGBA float32 pixels), are scattered
+ * into the (height, width, 4) image with ONE launch.  Pointers 16-byte aligned. */
+int lvx_untile_all(const float *recv_d, int64_t rank_stride_floats, int32_t world, int32_t tile_w,
+                   int32_t tile_h, int32_t width, int32_t height, float *img_d, void *stream);
+
 /* ------------------------------------------------------------------------- */
 /* AO bake: precompute_ao_kernel (_kernels.py:608-620) + the clip/cast of      */
 /* precompute_voxel_ao (illumination.py:193-214).                              */

@@ -66,7 +66,7 @@ SYMBOLS = [
     "lvx_voxelize_bound", "lvx_voxelize_clip", "lvx_voxelize_compact", "lvx_raw_regroup", "lvx_scan_u16", "lvx_provenance",
     "lvx_build_seg_records", "lvx_decode_packed", "lvx_density_l0", "lvx_octree_layout", "lvx_build_octree",
     "lvx_occupancy_dilate", "lvx_neighbor_sums", "lvx_render_scratch_bytes", "lvx_render", "lvx_render_wf_scratch_bytes", "lvx_render_wf", "lvx_render_wf_last_launches",
-    "lvx_render_footprint", "lvx_untile",
+    "lvx_render_footprint", "lvx_untile", "lvx_untile_all",
     "lvx_fibonacci_dirs", "lvx_ao_bake", "lvx_probe_dda", "lvx_probe_tube", "lvx_probe_sphere",
     "lvx_probe_trilinear", "lvx_probe_cone", "lvx_probe_ao_density", "lvx_probe_blocked",
     "lvx_probe_ao_hemisphere", "lvx_rep_level", "lvx_probe_replines", "lvx_brute_count", "lvx_brute_render",

@@ -917,6 +917,22 @@ untile_kernel(const float4 *__restrict__ tiles, lvx_tiling tl, int tiles_x, i64 
     if (x < W && y < H) img[(i64)y * W + x] = tiles[idx];
 }
 
+// All ranks' compact tile buffers (rank r's tiles start at recv + r * rank_stride float4s;
+// tile k of the frame is tile k / world of rank k % world) -> the full image, one thread per
+// output pixel: coalesced stores, one launch whatever the number of ranks.
+__global__ void __launch_bounds__(256)
+untile_all_kernel(const float4 *__restrict__ recv, i64 rank_stride, int world, int tile_w, int tile_h,
+                  int tiles_x, int W, int H, float4 *__restrict__ img) {
+    const i64 idx = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (i64)W * H) return;
+    const int x = (int)(idx % W), y = (int)(idx / W);
+    const i64 tile = (i64)(y / tile_h) * tiles_x + x / tile_w;
+    const i64 k = tile / world;
+    const int r = (int)(tile % world);
+    const i64 src = (k * tile_h + (y % tile_h)) * tile_w + (x % tile_w);
+    img[idx] = recv[(i64)r * rank_stride + src];
+}
+
 int check_tiling(const lvx_tiling *t) {
     LVX_REQUIRE(t && t->tile_w >= 8 && t->tile_h >= 4 && (t->tile_w % 8) == 0 &&
                     (t->tile_h % 4) == 0 && t->tile_step >= 1 && t->tile_first >= 0 &&
@@ -1066,6 +1082,26 @@ int lvx_untile(const float *tiles_d, const lvx_tiling *tiling, int32_t width, in
     untile_kernel<<<(unsigned)lvx_ceil_div(px, 256), 256, 0, (cudaStream_t)stream>>>(
         reinterpret_cast<const float4 *>(tiles_d), *tiling, tiles_x, n, width, height,
         reinterpret_cast<float4 *>(img_d));
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_untile_all(const float *recv_d, int64_t rank_stride_floats, int32_t world, int32_t tile_w,
+                   int32_t tile_h, int32_t width, int32_t height, float *img_d, void *stream) {
+    LVX_REQUIRE(recv_d && img_d && width >= 1 && height >= 1 && world >= 1, "bad arguments");
+    LVX_REQUIRE(tile_w >= 8 && tile_h >= 4 && (tile_w % 8) == 0 && (tile_h % 4) == 0,
+                "tiling: tile_w %% 8 == 0, tile_h %% 4 == 0 required");
+    LVX_REQUIRE(rank_stride_floats >= 0 && (rank_stride_floats % 4) == 0 && ((uintptr_t)recv_d & 15) == 0 &&
+                    ((uintptr_t)img_d & 15) == 0,
+                "tile buffers must be 16-byte aligned and a whole number of pixels apart");
+    const i64 tiles_x = lvx_ceil_div(width, tile_w), tiles_y = lvx_ceil_div(height, tile_h);
+    const i64 per_rank = lvx_ceil_div(tiles_x * tiles_y, world) * tile_w * tile_h;
+    LVX_REQUIRE(world == 1 || rank_stride_floats / 4 >= per_rank, "rank stride %lld floats is smaller than a rank's tiles",
+                (long long)rank_stride_floats);
+    const i64 px = (i64)width * height;
+    untile_all_kernel<<<(unsigned)lvx_ceil_div(px, 256), 256, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<const float4 *>(recv_d), rank_stride_floats / 4, world, tile_w, tile_h, (int)tiles_x, width,
+        height, reinterpret_cast<float4 *>(img_d));
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }

@@ -69,64 +69,139 @@ def tile_pixel_indices(rank: int, world: int, width: int, height: int, tile_w: i
     return (ys * width + xs).astype(np.int64), mask
 
 
-def allgather_varlen(t, group=None):
-    """all_gather of 1-D/2-D tensors whose first dimension differs per rank.
-    Returns the list of per-rank tensors (rank order)."""
+# dtypes every backend (NCCL included) can move; anything else travels as its bytes
+_WIRE_DTYPES = ("torch.uint8", "torch.int8", "torch.int32", "torch.int64", "torch.float16", "torch.bfloat16",
+                "torch.float32", "torch.float64")
+
+
+def _as_wire(t):
+    """ProcessGroupNCCL has no mapping for int16 / uint16 / uint32 / uint64 / bool: ship the bytes."""
+    import torch
+    if str(t.dtype) in _WIRE_DTYPES:
+        return t, None
+    # (rows stay rows: [n, ...] -> [n, bytes per row], so the first dimension keeps its meaning)
+    return t.contiguous().reshape(t.shape[0], -1).view(torch.uint8), (t.dtype, tuple(t.shape[1:]))
+
+
+def allgather_varlen_multi(tensors, group=None):
+    """all_gather of several 1-D/2-D tensors whose first dimension differs per rank, with ONE
+    size exchange (and one host read) for all of them and one `all_gather_into_tensor` per
+    tensor.  Returns, per input tensor, the list of per-rank tensors in rank order."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
-    n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
-    sizes = [torch.zeros_like(n) for _ in range(world)]
-    dist.all_gather(sizes, n, group=group)
-    sizes = [int(s.item()) for s in sizes]
-    m = max(max(sizes), 1)
-    pad = torch.zeros((m,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-    pad[:t.shape[0]] = t
-    out = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(out, pad, group=group)
-    return [o[:s] for o, s in zip(out, sizes)]
+    dev = tensors[0].device
+    mine = torch.tensor([int(t.shape[0]) for t in tensors], dtype=torch.int64, device=dev)
+    sizes = torch.empty(world * len(tensors), dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(sizes, mine, group=group)  # (flat output: what gloo and NCCL both accept)
+    sizes = sizes.view(world, len(tensors)).cpu().tolist()  # the one synchronisation: it sizes the receive buffers
+    out = []
+    for k, t in enumerate(tensors):
+        wire, orig = _as_wire(t)
+        m = max(max(sizes[r][k] for r in range(world)), 1)
+        if wire.shape[0] == m:
+            send = wire.contiguous()
+        else:
+            send = torch.zeros((m,) + tuple(wire.shape[1:]), dtype=wire.dtype, device=dev)
+            send[:wire.shape[0]] = wire
+        recv = torch.empty(world * send.numel(), dtype=send.dtype, device=dev)
+        dist.all_gather_into_tensor(recv, send.reshape(-1), group=group)
+        recv = recv.view((world,) + tuple(send.shape))
+        parts = [recv[r, :sizes[r][k]] for r in range(world)]
+        if orig is not None:
+            parts = [p.contiguous().view(orig[0]).reshape((p.shape[0],) + orig[1]) for p in parts]
+        out.append(parts)
+    return out
 
 
-def gather_tiles(tiles, dst: int = 0, group=None):
-    """Gather every rank's compact tile buffer on `dst` (list in rank order there,
-    None elsewhere).  Buffers differ by at most one tile, so they are padded to
-    the largest and sent with ONE collective."""
+def allgather_varlen(t, group=None):
+    """all_gather of one 1-D/2-D tensor whose first dimension differs per rank.
+    Returns the list of per-rank tensors (rank order)."""
+    return allgather_varlen_multi([t], group)[0]
+
+
+# --- frame exchange: ONE collective per frame, no host synchronisation ------------------------
+#
+# Every rank's send buffer is a flat float32 tensor of the same length on all ranks,
+#   [ m * tile_h * tile_w * 4 floats of tiles | 8 floats of tail ]
+# with m = the largest tile count of any rank (a pure function of W, H, world: rank 0's) and
+# the tail holding the rank's three frame counters (voxel_steps, intersection_tests,
+# window_overflow) as int64 bit patterns.  The kernels render straight into the front part.
+
+TAIL_FLOATS = 8  # 3 int64 counters + one spare, keeps the buffer a multiple of 16 bytes
+
+
+def tile_counts(world: int, width: int, height: int, tile_w: int = MG_TILE_W, tile_h: int = MG_TILE_H):
+    """Tiles per rank of the interleaved partition (rank order): no communication needed."""
+    tx, ty = tile_grid(width, height, tile_w, tile_h)
+    total = tx * ty
+    return [max(0, (total - r + world - 1) // world) for r in range(world)]
+
+
+def send_layout(world: int, width: int, height: int, tile_w: int = MG_TILE_W, tile_h: int = MG_TILE_H):
+    """(m, tile floats per rank, send-buffer length in floats)."""
+    m = max(tile_counts(world, width, height, tile_w, tile_h)[0], 1)
+    body = m * tile_h * tile_w * 4
+    return m, body, body + TAIL_FLOATS
+
+
+def new_send_buffer(world: int, width: int, height: int, device, tile_w: int = MG_TILE_W, tile_h: int = MG_TILE_H):
+    import torch
+    return torch.zeros(send_layout(world, width, height, tile_w, tile_h)[2], dtype=torch.float32, device=device)
+
+
+def send_tiles_view(send, n_tiles: int, tile_w: int = MG_TILE_W, tile_h: int = MG_TILE_H):
+    """The first n_tiles tiles of a send buffer as [n, tile_h, tile_w, 4]."""
+    return send[:n_tiles * tile_h * tile_w * 4].view(n_tiles, tile_h, tile_w, 4)
+
+
+def pack_counters(send, totals):
+    """Write the rank's int64[3] counters into the tail of its send buffer (device-side copy)."""
+    import torch
+    send[-TAIL_FLOATS:].view(torch.int64)[:3].copy_(totals.to(torch.int64))
+
+
+def unpack_counters(recv):
+    """Sum of the ranks' counters: int64[3] tensor (recv is [world, L])."""
+    import torch
+    return recv[:, -TAIL_FLOATS:].contiguous().view(torch.int64)[:, :3].sum(dim=0)
+
+
+def gather_tiles(send, dst: int = 0, group=None, recv=None):
+    """Gather every rank's send buffer (same length everywhere, see above) on `dst` with ONE
+    collective and no size exchange or host read.  Returns the [world, L] receive tensor on
+    `dst` (pass `recv` to reuse a preallocated one) and None elsewhere."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    n = torch.tensor([tiles.shape[0]], dtype=torch.int64, device=tiles.device)
-    sizes = [torch.zeros_like(n) for _ in range(world)]
-    dist.all_gather(sizes, n, group=group)
-    sizes = [int(s.item()) for s in sizes]
-    m = max(max(sizes), 1)
-    if tiles.shape[0] == m:
-        send = tiles.contiguous()
-    else:
-        send = torch.zeros((m,) + tuple(tiles.shape[1:]), dtype=tiles.dtype, device=tiles.device)
-        send[:tiles.shape[0]] = tiles
-    recv = [torch.empty_like(send) for _ in range(world)] if rank == dst else None
-    dist.gather(send, recv, dst=dst, group=group)
     if rank != dst:
+        dist.gather(send, None, dst=dst, group=group)
         return None
-    return [r[:s] for r, s in zip(recv, sizes)]
+    if recv is None:
+        recv = torch.empty((world, send.numel()), dtype=send.dtype, device=send.device)
+    dist.gather(send, list(recv.unbind(0)), dst=dst, group=group)
+    return recv
 
 
 # --- rendering ---------------------------------------------------------------------------
 
 def render_my_tiles(camera: Camera, model, octree, params: RenderParams, rank: int, world: int,
-                    moving: bool = False, tile_w: int = MG_TILE_W, tile_h: int = MG_TILE_H, replines=None):
-    """Render rank's interleaved tiles into a compact buffer.
-    Returns (tiles f32[n_tiles, tile_h, tile_w, 4], row_stats i64[H,3]) on the device."""
+                    moving: bool = False, tile_w: int = MG_TILE_W, tile_h: int = MG_TILE_H, replines=None,
+                    send=None):
+    """Render rank's interleaved tiles straight into (the front of) its send buffer.
+    Returns (tiles f32[n_tiles, tile_h, tile_w, 4] -- a view of `send` --, row_stats i64[H,3], send)."""
     torch = _lib.require_device()
     plan = FramePlan(camera, model, octree, params, resolve_neighbor(params, moving),
                      tile_first=rank, tile_step=world, compact=True, tile_w=tile_w, tile_h=tile_h,
                      replines=replines)
     n = plan.n_my_tiles()
-    tiles = torch.zeros((max(n, 1), tile_h, tile_w, 4), dtype=torch.float32, device="cuda")
+    if send is None:
+        send = new_send_buffer(world, camera.width, camera.height, "cuda", tile_w, tile_h)
+    tiles = send_tiles_view(send, max(n, 1), tile_w, tile_h)
     stats = torch.zeros((camera.height, 3), dtype=torch.int64, device="cuda")
     plan.launch(tiles, stats)
-    return tiles[:n], stats
+    return tiles[:n], stats, send
 
 
 def untile_into(tiles, rank: int, world: int, width: int, height: int, img_d,
@@ -140,11 +215,23 @@ def untile_into(tiles, rank: int, world: int, width: int, height: int, img_d,
                                      _lib.ptr(img_d), _lib.stream_ptr()))
 
 
+def untile_all(recv, world: int, width: int, height: int, img_d, tile_w: int = MG_TILE_W,
+               tile_h: int = MG_TILE_H):
+    """Scatter the gathered buffers of ALL ranks ([world, L]) into the image with one launch."""
+    _lib.check(_lib.lib().lvx_untile_all(_lib.ptr(recv), C.c_int64(int(recv.stride(0))), C.c_int32(world),
+                                         C.c_int32(tile_w), C.c_int32(tile_h), C.c_int32(width),
+                                         C.c_int32(height), _lib.ptr(img_d), _lib.stream_ptr()))
+
+
 def render_frame_tiled(camera: Camera, model, octree=None, replines=None,
                        params: Optional[RenderParams] = None, moving: bool = False, group=None,
                        to_host: bool = True):
     """`render_frame` over all ranks of `group` (default: the world).  Every rank
-    must hold the same model.  Returns a Frame on rank 0 and None elsewhere."""
+    must hold the same model.  Returns a Frame on rank 0 and None elsewhere.
+
+    Per frame: render into the send buffer, append the three counters, ONE gather, one
+    untile launch on rank 0.  No size exchange, no separate reduce, no host read before the
+    final copy."""
     import torch
     import torch.distributed as dist
     if params is None:
@@ -153,21 +240,19 @@ def render_frame_tiled(camera: Camera, model, octree=None, replines=None,
     rank = dist.get_rank(group)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    tiles, stats = render_my_tiles(camera, model, octree, params, rank, world, moving, replines=replines)
+    tiles, stats, send = render_my_tiles(camera, model, octree, params, rank, world, moving, replines=replines)
     e1.record()
-    tot = stats.sum(dim=0)
-    dist.reduce(tot, dst=0, group=group)
-    parts = gather_tiles(tiles, 0, group)
+    pack_counters(send, stats.sum(dim=0))
+    recv = gather_tiles(send, 0, group)
     if rank != 0:
         return None
     H, W = camera.height, camera.width
     img_d = torch.empty((H, W, 4), dtype=torch.float32, device="cuda")
-    for r, part in enumerate(parts):
-        untile_into(part, r, world, W, H, img_d)
+    untile_all(recv, world, W, H, img_d)
     if to_host:
         host = torch.empty((H, W, 4), dtype=torch.float32, pin_memory=True)
         host.copy_(img_d, non_blocking=True)
-    tot = tot.cpu()
+    tot = unpack_counters(recv).cpu()
     torch.cuda.current_stream().synchronize()
     stats = {"rays": W * H, "voxel_steps": int(tot[0]), "intersection_tests": int(tot[1]),
              "ms": float(e0.elapsed_time(e1)), "workers": world, "window_overflow": int(tot[2]),
@@ -215,7 +300,10 @@ def merge_shards(spec: GridSpec, vox_cnt_total, raw_key, raw_q, raw_lin, *, cach
 def build_voxel_model_sharded(curves: CurveSet, spec: GridSpec, transfer_table=None,
                               memory_budget: Optional[int] = None, group=None):
     """`build_voxel_model` with the clipping sharded by line ID over the ranks of
-    `group`; every rank passes the same `curves` and receives the same full model."""
+    `group`; every rank passes the same `curves` and receives the same full model.
+
+    A failure on one rank (MemoryError of its crossing bound, a CUDA error) is agreed on by
+    all ranks BEFORE the data collectives, so nobody is left waiting in NCCL."""
     import torch
     import torch.distributed as dist
     from . import voxelizer as vz
@@ -227,17 +315,28 @@ def build_voxel_model_sharded(curves: CurveSet, spec: GridSpec, transfer_table=N
     c0, c1 = shard_range(n_curves, rank, world)
     p0, p1 = int(off[c0]), int(off[c1])
     local_off = _lib.to_device(off[c0:c1 + 1] - p0, np.int64)
-    sh = voxelize_shard(_lib.to_device(pts[p0:p1], np.float64), _lib.to_device(attrs[p0:p1], np.float64),
-                        local_off, c1 - c0, spec, p0)
+    sh, failure = None, None
+    try:
+        sh = voxelize_shard(_lib.to_device(pts[p0:p1], np.float64), _lib.to_device(attrs[p0:p1], np.float64),
+                            local_off, c1 - c0, spec, p0)
+    except Exception as e:  # agreed on below; re-raised on every rank
+        failure = e
+    flag = torch.tensor([0 if failure is None else (2 if isinstance(failure, MemoryError) else 1)],
+                        dtype=torch.int32, device=local_off.device)
+    dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+    if int(flag.item()) != 0:
+        if failure is not None:
+            raise failure
+        kind = MemoryError if int(flag.item()) == 2 else RuntimeError
+        raise kind("sharded voxelization failed on another rank")
     total = sh["vox_cnt"].clone()
     dist.all_reduce(total, group=group)  # int32 bit patterns of u32 counts add correctly
     err = sh["err"].clone()
     dist.all_reduce(err, op=dist.ReduceOp.MAX, group=group)
-    keys = torch.cat(allgather_varlen(sh["raw_key"], group))
-    qs = torch.cat(allgather_varlen(sh["raw_q"], group))
-    lins = torch.cat(allgather_varlen(sh["raw_lin"], group))
-    edge_kept = torch.cat(allgather_varlen(sh["edge_kept"][:p1 - p0], group))
-    out = merge_shards(spec, total, keys, qs, lins, edge_kept=edge_kept,
+    # (edge_kept is u16 in an int16 tensor: it travels as bytes, NCCL has no 16-bit integer type)
+    keys, qs, lins, kept = allgather_varlen_multi(
+        [sh["raw_key"], sh["raw_q"], sh["raw_lin"], sh["edge_kept"][:p1 - p0]], group)
+    out = merge_shards(spec, total, torch.cat(keys), torch.cat(qs), torch.cat(lins), edge_kept=torch.cat(kept),
                        off_d=_lib.to_device(off, np.int64), n_curves=n_curves, memory_budget=memory_budget)
     out["err"] = err
     return vz.model_from_device(out, spec, transfer_table)

@@ -33,8 +33,9 @@ _ARRAY_FIELDS = {
     "seg_face_out": (np.uint8, ()), "seg_bin_out": (np.uint16, ()),
     "seg_curve": (np.int32, ()), "seg_order": (np.int32, ()),
 }
-# device mirrors that feed the render kernels
-_RENDER_INPUTS = ("counts", "offsets", "seg_a", "seg_b", "seg_attr", "seg_lid")
+# arrays the render inputs are derived from: the per-segment caches, or -- for a model that
+# carries only the encoded arrays (a .vxl file) -- the packed records they are decoded from
+_RENDER_INPUTS = ("counts", "offsets", "packed", "seg_a", "seg_b", "seg_attr", "seg_lid")
 
 
 def _check_bins(n_bins: int) -> int:
@@ -124,6 +125,7 @@ class VoxelModel:
         self._host = {}
         self._dev = {}
         self._derived = {}  # seg_rec, occ, table: device-only render inputs
+        self._decoded = set()  # per-segment fields produced by _decode_packed (not user-supplied)
         self._ao = None
         for name, value in (("counts", counts), ("offsets", offsets), ("packed", packed),
                             ("seg_voxel", seg_voxel), ("seg_a", seg_a), ("seg_b", seg_b),
@@ -150,9 +152,16 @@ class VoxelModel:
         else:
             self._dev[name] = value
             self._host.pop(name, None)
+        self._decoded.discard(name)  # now user-supplied
         if name in _RENDER_INPUTS:
             self._derived.clear()
             self.__dict__.pop("_occ_dilated", None)
+        if name in ("counts", "offsets", "packed"):
+            # caches decoded from the old encoded arrays are stale (host mirrors included)
+            for k in list(self._decoded):
+                self._dev.pop(k, None)
+                self._host.pop(k, None)
+            self._decoded.clear()
 
     def _get_array(self, name):
         h = self._host.get(name)
@@ -209,6 +218,7 @@ class VoxelModel:
         for k, v in out.items():
             if not self._has(k):
                 self._dev[k] = v[:S]
+                self._decoded.add(k)
         return rec
 
     counts = _array_property("counts")

@@ -397,12 +397,25 @@ def test_untile_round_trip(lv, synth):
         img = torch.zeros((70, 150, 4), dtype=torch.float32, device="cuda")
         stats = torch.zeros((70, 3), dtype=torch.int64, device="cuda")
         for rank in range(world):
-            tiles, st = parallel.render_my_tiles(cam, m, None, p, rank, world)
+            tiles, st, _ = parallel.render_my_tiles(cam, m, None, p, rank, world)
             parallel.untile_into(tiles, rank, world, cam.width, cam.height, img)
             stats += st
         assert np.array_equal(img.cpu().numpy(), full.image), world
         tot = stats.sum(0).tolist()
         assert tot[0] == full.stats["voxel_steps"] and tot[1] == full.stats["intersection_tests"]
+        # the multi-GPU frame exchange as rank 0 sees it after the gather: every rank's send buffer
+        # (tiles in front, counters in the tail) side by side, scattered with ONE launch
+        recv = torch.empty((world, parallel.send_layout(world, cam.width, cam.height)[2]), dtype=torch.float32,
+                           device="cuda")
+        for rank in range(world):
+            _, st, send = parallel.render_my_tiles(cam, m, None, p, rank, world)
+            parallel.pack_counters(send, st.sum(dim=0))
+            recv[rank].copy_(send)
+        img2 = torch.full((70, 150, 4), -1.0, dtype=torch.float32, device="cuda")
+        parallel.untile_all(recv, world, cam.width, cam.height, img2)
+        assert np.array_equal(img2.cpu().numpy(), full.image), world
+        tot2 = parallel.unpack_counters(recv).tolist()
+        assert tot2 == [full.stats["voxel_steps"], full.stats["intersection_tests"], full.stats["window_overflow"]]
 
 
 def test_sharded_voxelization_merges_to_single_gpu_result(lv, synth):

@@ -42,24 +42,44 @@ def _worker_tiles(rank, world, W, H):
     import torch
     from paper_1801_01155_b200 import parallel
     idx, mask = parallel.tile_pixel_indices(rank, world, W, H)
-    # stand-in for the render kernel: pixel value = f(pixel index), zeros outside the image
+    # sizes are a pure function of (W, H, world): nobody exchanges them
+    counts = parallel.tile_counts(world, W, H)
+    assert counts[rank] == idx.shape[0] and counts[0] == max(counts)
+    m, body, L = parallel.send_layout(world, W, H)
+    send = parallel.new_send_buffer(world, W, H, "cpu")
+    assert send.numel() == L and m == counts[0]
+    # stand-in for the render kernel: pixel value = f(pixel index), zeros outside the image,
+    # written straight into the front of the send buffer
     tiles = np.where(mask, idx, 0).astype(np.float32)[..., None] * np.array([1, 2, 3, 4], np.float32)
-    parts = parallel.gather_tiles(torch.from_numpy(tiles), 0)
+    parallel.send_tiles_view(send, idx.shape[0]).copy_(torch.from_numpy(tiles))
+    # the rank's three counters ride in the tail of the same buffer (values beyond 2^53: bit patterns)
+    mine = torch.tensor([10 + rank, (1 << 60) + 7 * rank, rank], dtype=torch.int64)
+    parallel.pack_counters(send, mine)
+    recv = parallel.gather_tiles(send, 0)
+    again = parallel.gather_tiles(send, 0, recv=recv)  # a preallocated receive buffer is filled in place
     if rank != 0:
-        assert parts is None
+        assert recv is None and again is None
         return
+    assert again is recv
+    assert tuple(recv.shape) == (world, L)
     img = np.full((H * W, 4), -1.0, np.float32)
-    for r, part in enumerate(parts):
-        i, m = parallel.tile_pixel_indices(r, world, W, H)
-        assert part.shape[0] == i.shape[0]
-        img[i[m]] = part.numpy()[m]
+    for r in range(world):
+        i, msk = parallel.tile_pixel_indices(r, world, W, H)
+        part = parallel.send_tiles_view(recv[r], i.shape[0]).numpy()
+        img[i[msk]] = part[msk]
     want = np.arange(H * W, dtype=np.float32)[:, None] * np.array([1, 2, 3, 4], np.float32)
     assert np.array_equal(img, want)  # every pixel written exactly once, by the right tile
+    tot = parallel.unpack_counters(recv).tolist()
+    assert tot == [sum(10 + r for r in range(world)), world * (1 << 60) + 7 * sum(range(world)), sum(range(world))]
 
 
 @pytest.mark.parametrize("size", [(150, 70), (64, 32), (33, 17)])
 def test_tile_gather_reassembles_the_frame(size):
     _run(_worker_tiles, 2, *size)
+
+
+def test_tile_gather_three_ranks_uneven():
+    _run(_worker_tiles, 3, 150, 70)  # 5 x 5 tiles over 3 ranks: 9 / 8 / 8
 
 
 def _worker_voxelize(rank, world):
@@ -100,6 +120,99 @@ def _worker_voxelize(rank, world):
 
 def test_line_id_sharding_and_varlen_allgather():
     _run(_worker_voxelize, 2)
+
+
+def _worker_sharded_build(rank, world, fail_rank):
+    """`build_voxel_model_sharded` itself, end to end over gloo, with the two GPU stages stood
+    in for: the clip of a shard by the CPU oracle (records in the device pipeline's raw format,
+    edge_kept as int16 like the kernel's), the merge by a check against the single-process
+    result.  Exercises the shard ranges, the failure agreement, the count all-reduce and the
+    single-size-exchange all-gather with a 16-bit tensor that must travel as bytes."""
+    import torch
+    from oracle import lvx_oracle as orc
+    from paper_1801_01155_b200 import _lib, parallel, synth, voxelizer as vz
+    import paper_1801_01155_b200 as lv
+    dims = (6, 5, 4)
+    pts, attrs, off = synth.lattice_adversarial(301, 9, dims, seed=5)
+    V = dims[0] * dims[1] * dims[2]
+
+    def raw_of(p, a, o, point_base):
+        vox, p_in, p_out, a_in, a_out, curve, within = orc.clip_batch(p, a, o, dims)
+        lin = (vox[:, 0] + dims[0] * (vox[:, 1] + dims[1] * vox[:, 2])).astype(np.int64)
+        # stand-in key: (global first point of the curve, chord order) -- increasing in curve order
+        key = ((o[curve] + point_base) << 16) | within
+        q = (p_in * 1e3).astype(np.int64).sum(1) * 7 + (p_out * 1e3).astype(np.int64).sum(1)
+        kept = np.zeros(p.shape[0], np.int16)
+        np.add.at(kept, o[curve], 1)
+        return dict(vox_cnt=torch.from_numpy(np.bincount(lin, minlength=V).astype(np.int32)),
+                    raw_key=torch.from_numpy(key.astype(np.int64)), raw_q=torch.from_numpy(q),
+                    raw_lin=torch.from_numpy(lin.astype(np.int32)), edge_kept=torch.from_numpy(kept),
+                    err=torch.zeros(1, dtype=torch.int32))
+
+    def fake_shard(pts_d, attrs_d, off_d, n_curves, spec, point_base, want_edge_kept=True):
+        if rank == fail_rank:
+            raise MemoryError("this rank's crossing bound exceeds 2^32")
+        return raw_of(pts_d.numpy(), attrs_d.numpy(), off_d.numpy(), point_base)
+
+    seen = {}
+
+    def fake_merge(spec, total, keys, qs, lins, *, caches=True, edge_kept=None, off_d=None, n_curves=0,
+                   memory_budget=None):
+        want = raw_of(pts, attrs, off, 0)
+        assert torch.equal(total, want["vox_cnt"])
+        assert torch.equal(keys, want["raw_key"]) and torch.equal(qs, want["raw_q"]) and torch.equal(lins, want["raw_lin"])
+        assert edge_kept.dtype == torch.int16 and torch.equal(edge_kept, want["edge_kept"])
+        assert n_curves == off.size - 1 and torch.equal(off_d, torch.from_numpy(off))
+        seen["merged"] = True
+        return {"n_segments": int(keys.shape[0]), "dropped": 0}
+
+    def to_cpu(a, dtype=None):
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=dtype))
+
+    orig = (parallel.voxelize_shard, parallel.merge_shards, _lib.to_device, _lib.require_device, vz.model_from_device)
+    parallel.voxelize_shard, parallel.merge_shards = fake_shard, fake_merge
+    _lib.to_device, _lib.require_device = to_cpu, (lambda: torch)
+    vz.model_from_device = lambda out, spec, table: out
+    try:
+        cs = lv.CurveSet.from_flat(pts, attrs, off)
+        if fail_rank is None:
+            out = parallel.build_voxel_model_sharded(cs, lv.GridSpec(dims))
+            assert seen.get("merged") and int(out["err"].item()) == 0
+        else:
+            # the failing rank's exception surfaces on EVERY rank, before any data collective
+            with pytest.raises(MemoryError):
+                parallel.build_voxel_model_sharded(cs, lv.GridSpec(dims))
+            assert not seen
+    finally:
+        (parallel.voxelize_shard, parallel.merge_shards, _lib.to_device, _lib.require_device,
+         vz.model_from_device) = orig
+
+
+def test_sharded_build_end_to_end_over_gloo():
+    _run(_worker_sharded_build, 2, None)
+
+
+def test_sharded_build_failure_is_raised_on_every_rank():
+    _run(_worker_sharded_build, 2, 1)
+
+
+def test_allgather_varlen_multi_mixed_dtypes():
+    _run(_worker_varlen_multi, 2)
+
+
+def _worker_varlen_multi(rank, world):
+    import torch
+    from paper_1801_01155_b200 import parallel
+    n = 3 + 2 * rank
+    a = torch.arange(n, dtype=torch.int64) + 100 * rank
+    b = (torch.arange(n * 2, dtype=torch.int16) - 5 + rank).reshape(n, 2)   # 16-bit: travels as bytes
+    c = torch.zeros(0, dtype=torch.int32) if rank == 0 else torch.ones(4, dtype=torch.int32)  # empty on one rank
+    pa, pb, pc = parallel.allgather_varlen_multi([a, b, c])
+    for r in range(world):
+        m = 3 + 2 * r
+        assert torch.equal(pa[r], torch.arange(m, dtype=torch.int64) + 100 * r)
+        assert pb[r].dtype == torch.int16 and torch.equal(pb[r], (torch.arange(m * 2, dtype=torch.int16) - 5 + r).reshape(m, 2))
+    assert pc[0].numel() == 0 and torch.equal(pc[1], torch.ones(4, dtype=torch.int32))
 
 
 def test_shard_ranges_partition():
