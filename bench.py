@@ -429,7 +429,7 @@ def run_ours(args, wl):
     import paper_1801_01155_b200 as lv
     from paper_1801_01155_b200 import _lib, parallel
     from paper_1801_01155_b200.illumination import ao_bake_device
-    from paper_1801_01155_b200.lod import density_level0_device, _octree_from_level0_device
+    from paper_1801_01155_b200.lod import density_level0_device, mips_inplace, octree_buffer
     from paper_1801_01155_b200.raycast import FramePlan, resolve_neighbor
 
     D = Dist(args)
@@ -452,9 +452,11 @@ def run_ours(args, wl):
 
     def lod_and_ao(model, ao):
         st = {}
-        l0 = density_level0_device(model)
-        t_l0 = min(ev_ms(lambda: density_level0_device(model)) for _ in range(3))
-        t_mip = min(ev_ms(lambda: _octree_from_level0_device(l0, dims)) for _ in range(3))
+        flat, v0 = octree_buffer(dims)
+        density_level0_device(model, out=flat[:v0])
+        t_l0 = min(ev_ms(lambda: density_level0_device(model, out=flat[:v0])) for _ in range(3))
+        t_mip = min(ev_ms(lambda: mips_inplace(flat, dims)) for _ in range(3))
+        del flat
         Sm = model.segment_count
         b_lod = 25 * Sm + 4 * V + 4 * V * (8 / 7 + 1 / 7)
         st["lod"] = {"ms": t_l0 + t_mip, "density_ms": t_l0, "mip_ms": t_mip, "alg_bytes": int(b_lod),

@@ -8,61 +8,97 @@
 
 namespace {
 
-// One thread per voxel; its segments are summed in stored order in float64
-// (np.bincount with weights is a sequential f64 accumulation), one cast to f32.
-__global__ void __launch_bounds__(256)
+// Level-0 density.  np.bincount with weights is a sequential float64 accumulation of the
+// per-segment products length * sigma in stored order, one cast to float32 (lod.py:87-94).
+//
+// A warp owns 32 consecutive voxels.  Their records are one contiguous span of the record array
+// (headers are exclusive prefix sums in voxel scan order), so the lanes load the span together --
+// one 32-byte record per lane and round, every sector used once, all loads independent -- and
+// leave the float64 products in shared memory; each lane then adds up the products of ITS voxel in
+// stored order.  The span is worked through in chunks of kDlChunk records, so the accumulation
+// order per voxel is the stored order whatever the group sizes.  A model whose offsets are not
+// prefix sums (nothing in the reference produces one) takes the per-thread loop.
+constexpr int kDlThreads = 256;
+constexpr int kDlChunk = 256;  // records per warp and round
+
+__device__ __forceinline__ double density_weight(const float4 a, const float4 b, const float *s_sigma) {
+    // endpoints are widened BEFORE the subtraction (lod.py:87-89)
+    const double ex = (double)b.x - (double)a.x;
+    const double ey = (double)b.y - (double)a.y;
+    const double ez = (double)b.z - (double)a.z;
+    const double len = sqrt(ex * ex + ey * ey + ez * ez);
+    return len * (double)s_sigma[__float_as_uint(a.w) & 0xFFu];
+}
+
+__global__ void __launch_bounds__(kDlThreads)
 density_l0_kernel(const u8 *__restrict__ counts, const u32 *__restrict__ offsets,
                   const lvx_seg_record *__restrict__ rec, const float *__restrict__ table,
                   i64 n_voxels, float *__restrict__ out) {
+    constexpr unsigned FULL = 0xFFFFFFFFu;
     __shared__ float s_sigma[256];
+    __shared__ double s_w[kDlThreads / 32][kDlChunk];
     s_sigma[threadIdx.x] = table[4 * threadIdx.x + 3];
     __syncthreads();
-    const i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n_voxels) return;
-    const u32 n = counts[v];
-    double acc = 0.0;
-    if (n) {
-        const float4 *r = reinterpret_cast<const float4 *>(rec + offsets[v]);
-        for (u32 k = 0; k < n; ++k) {
-            const float4 a = __ldg(r + 2 * k), b = __ldg(r + 2 * k + 1);
-            // endpoints are widened BEFORE the subtraction (lod.py:87-89)
-            const double ex = (double)b.x - (double)a.x;
-            const double ey = (double)b.y - (double)a.y;
-            const double ez = (double)b.z - (double)a.z;
-            const double len = sqrt(ex * ex + ey * ey + ez * ez);
-            const double sigma = (double)s_sigma[__float_as_uint(a.w) & 0xFFu];
-            acc += len * sigma;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const i64 n_warps = ((i64)gridDim.x * blockDim.x) >> 5;
+    for (i64 w = (((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5); w * 32 < n_voxels; w += n_warps) {
+        const i64 v = w * 32 + lane;
+        const u32 n = v < n_voxels ? counts[v] : 0u;
+        const unsigned occ = __ballot_sync(FULL, n != 0);
+        if (occ == 0) {
+            if (v < n_voxels) out[v] = 0.0f;
+            continue;
         }
+        const u32 off = n ? offsets[v] : 0u;
+        u32 inc = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 t = __shfl_up_sync(FULL, inc, o);
+            if (lane >= o) inc += t;
+        }
+        const u32 total = __shfl_sync(FULL, inc, 31);
+        const u32 first = inc - n;  // my records are [first, first + n) of the span
+        const u32 base = __shfl_sync(FULL, off, __ffs((int)occ) - 1);
+        const bool contiguous = __all_sync(FULL, n == 0 || off == base + first);
+        double acc = 0.0;
+        if (contiguous) {
+            const float4 *r = reinterpret_cast<const float4 *>(rec + base);
+            for (u32 j0 = 0; j0 < total; j0 += kDlChunk) {
+                const u32 m = min((u32)kDlChunk, total - j0);
+                for (u32 j = lane; j < m; j += 32) {
+                    const float4 a = __ldg(r + 2 * (size_t)(j0 + j)), b = __ldg(r + 2 * (size_t)(j0 + j) + 1);
+                    s_w[warp][j] = density_weight(a, b, s_sigma);
+                }
+                __syncwarp();
+                const u32 lo = max(first, j0), hi = min(first + n, j0 + m);
+                for (u32 k = lo; k < hi; ++k) acc += s_w[warp][k - j0];
+                __syncwarp();
+            }
+        } else if (n) {
+            const float4 *r = reinterpret_cast<const float4 *>(rec + off);
+            for (u32 k = 0; k < n; ++k) acc += density_weight(__ldg(r + 2 * k), __ldg(r + 2 * k + 1), s_sigma);
+        }
+        if (v < n_voxels) out[v] = (float)acc;
     }
-    out[v] = (float)acc;
 }
 
-// Shared-memory staged 2x2x2 reduction.  A block owns an 8x8x8 parent brick; it
-// stages the 16x16x16 child brick with coalesced row loads, then every thread
-// sums its (up to) eight children in the fixed (oz, oy, ox) order in float32 and
-// divides by the float32 child count (lod.py:97-110).
-constexpr int kMipP = 8;             // parent brick edge
+// Mip chain (lod.py:97-110): a parent is the float32 sum of its (up to) eight existing children in
+// the fixed (oz, oy, ox) order divided by the float32 child count.
+//
+// mip3_kernel: a block owns an 8x8x8 brick of level l+1; it stages the 16x16x16 child brick of level
+// l with coalesced row loads and reduces it three times in shared memory, writing its 8^3 / 4^3 /
+// 2^3 share of levels l+1, l+2, l+3 (as many of them as exist).  One pass over level l, no re-read of
+// the levels in between.
+constexpr int kMipP = 8;             // brick edge at the first output level
 constexpr int kMipC = 2 * kMipP;     // child brick edge
-constexpr int kMipPitch = kMipC + 1; // +1: conflict-free strided reads
 
-__global__ void __launch_bounds__(kMipP *kMipP *kMipP)
-mip_kernel(const float *__restrict__ src, int sx, int sy, int sz, float *__restrict__ dst, int px,
-           int py, int pz) {
-    __shared__ float s[kMipC][kMipC][kMipPitch];
-    const int bx = blockIdx.x * kMipP, by = blockIdx.y * kMipP, bz = blockIdx.z * kMipP;
-    const int cx0 = 2 * bx, cy0 = 2 * by, cz0 = 2 * bz;
-    for (int idx = threadIdx.x; idx < kMipC * kMipC * kMipC; idx += blockDim.x) {
-        const int lx = idx % kMipC, ly = (idx / kMipC) % kMipC, lz = idx / (kMipC * kMipC);
-        const int gx = cx0 + lx, gy = cy0 + ly, gz = cz0 + lz;
-        float v = 0.0f;
-        if (gx < sx && gy < sy && gz < sz) v = src[((i64)gz * sy + gy) * sx + gx];
-        s[lz][ly][lx] = v;
-    }
-    __syncthreads();
-    const int tx = threadIdx.x % kMipP, ty = (threadIdx.x / kMipP) % kMipP,
-              tz = threadIdx.x / (kMipP * kMipP);
-    const int x = bx + tx, y = by + ty, z = bz + tz;
-    if (x >= px || y >= py || z >= pz) return;
+struct MipDims {
+    int x, y, z;
+};
+
+__device__ __forceinline__ float mip_reduce(const float *s, int pitch_y, int pitch_z, int tx, int ty, int tz, int gx,
+                                            int gy, int gz, MipDims child) {
+    // children (2g + o) that exist at the child level, (oz, oy, ox) order, float32
     float acc = 0.0f, cnt = 0.0f;
 #pragma unroll
     for (int oz = 0; oz < 2; ++oz)
@@ -70,12 +106,94 @@ mip_kernel(const float *__restrict__ src, int sx, int sy, int sz, float *__restr
         for (int oy = 0; oy < 2; ++oy)
 #pragma unroll
             for (int ox = 0; ox < 2; ++ox) {
-                if (2 * z + oz < sz && 2 * y + oy < sy && 2 * x + ox < sx) {
-                    acc = acc + s[2 * tz + oz][2 * ty + oy][2 * tx + ox];
+                if (2 * gz + oz < child.z && 2 * gy + oy < child.y && 2 * gx + ox < child.x) {
+                    acc = acc + s[(2 * tz + oz) * pitch_z + (2 * ty + oy) * pitch_y + (2 * tx + ox)];
                     cnt = cnt + 1.0f;
                 }
             }
-    dst[((i64)z * py + y) * px + x] = acc / cnt;
+    return acc / cnt;
+}
+
+__global__ void __launch_bounds__(kMipP *kMipP *kMipP)
+mip3_kernel(const float *__restrict__ src, MipDims d0, float *__restrict__ dst1, MipDims d1,
+            float *__restrict__ dst2, MipDims d2, float *__restrict__ dst3, MipDims d3, int n_out) {
+    __shared__ float s0[kMipC * kMipC * (kMipC + 1)];
+    __shared__ float s1[kMipP * kMipP * (kMipP + 1)];
+    __shared__ float s2[4 * 4 * 5];
+    const int bx = blockIdx.x * kMipP, by = blockIdx.y * kMipP, bz = blockIdx.z * kMipP;
+    for (int idx = threadIdx.x; idx < kMipC * kMipC * kMipC; idx += blockDim.x) {
+        const int lx = idx % kMipC, ly = (idx / kMipC) % kMipC, lz = idx / (kMipC * kMipC);
+        const int gx = 2 * bx + lx, gy = 2 * by + ly, gz = 2 * bz + lz;
+        float v = 0.0f;
+        if (gx < d0.x && gy < d0.y && gz < d0.z) v = src[((i64)gz * d0.y + gy) * d0.x + gx];
+        s0[(lz * kMipC + ly) * (kMipC + 1) + lx] = v;
+    }
+    __syncthreads();
+    {
+        const int tx = threadIdx.x % kMipP, ty = (threadIdx.x / kMipP) % kMipP, tz = threadIdx.x / (kMipP * kMipP);
+        const int x = bx + tx, y = by + ty, z = bz + tz;
+        float v = 0.0f;
+        if (x < d1.x && y < d1.y && z < d1.z) {
+            v = mip_reduce(s0, kMipC + 1, kMipC * (kMipC + 1), tx, ty, tz, x, y, z, d0);
+            dst1[((i64)z * d1.y + y) * d1.x + x] = v;
+        }
+        s1[(tz * kMipP + ty) * (kMipP + 1) + tx] = v;
+    }
+    if (n_out < 2) return;
+    __syncthreads();
+    if (threadIdx.x < 64) {
+        const int tx = threadIdx.x % 4, ty = (threadIdx.x / 4) % 4, tz = threadIdx.x / 16;
+        const int x = bx / 2 + tx, y = by / 2 + ty, z = bz / 2 + tz;
+        float v = 0.0f;
+        if (x < d2.x && y < d2.y && z < d2.z) {
+            v = mip_reduce(s1, kMipP + 1, kMipP * (kMipP + 1), tx, ty, tz, x, y, z, d1);
+            dst2[((i64)z * d2.y + y) * d2.x + x] = v;
+        }
+        s2[(tz * 4 + ty) * 5 + tx] = v;
+    }
+    if (n_out < 3) return;
+    __syncthreads();
+    if (threadIdx.x < 8) {
+        const int tx = threadIdx.x % 2, ty = (threadIdx.x / 2) % 2, tz = threadIdx.x / 4;
+        const int x = bx / 4 + tx, y = by / 4 + ty, z = bz / 4 + tz;
+        if (x < d3.x && y < d3.y && z < d3.z)
+            dst3[((i64)z * d3.y + y) * d3.x + x] = mip_reduce(s2, 5, 20, tx, ty, tz, x, y, z, d2);
+    }
+}
+
+// The small top of the pyramid (from a level of at most 64^3 cells down to 1x1x1) in ONE block:
+// level after level through global memory (L2), a block barrier between levels.
+struct MipTail {
+    i64 off[LVX_MAX_LEVELS + 1];
+    int dims[LVX_MAX_LEVELS * 3];
+    int first, n_levels;  // levels first+1 .. n_levels-1 are computed from level `first`
+};
+
+__global__ void __launch_bounds__(1024) mip_tail_kernel(float *__restrict__ flat, const MipTail T) {
+    for (int l = T.first + 1; l < T.n_levels; ++l) {
+        const float *src = flat + T.off[l - 1];
+        float *dst = flat + T.off[l];
+        const int sx = T.dims[3 * (l - 1)], sy = T.dims[3 * (l - 1) + 1], sz = T.dims[3 * (l - 1) + 2];
+        const int px = T.dims[3 * l], py = T.dims[3 * l + 1], pz = T.dims[3 * l + 2];
+        const i64 n = (i64)px * py * pz;
+        for (i64 i = threadIdx.x; i < n; i += blockDim.x) {
+            const int x = (int)(i % px), y = (int)((i / px) % py), z = (int)(i / ((i64)px * py));
+            float acc = 0.0f, cnt = 0.0f;
+#pragma unroll
+            for (int oz = 0; oz < 2; ++oz)
+#pragma unroll
+                for (int oy = 0; oy < 2; ++oy)
+#pragma unroll
+                    for (int ox = 0; ox < 2; ++ox) {
+                        if (2 * z + oz < sz && 2 * y + oy < sy && 2 * x + ox < sx) {
+                            acc = acc + src[((i64)(2 * z + oz) * sy + (2 * y + oy)) * sx + (2 * x + ox)];
+                            cnt = cnt + 1.0f;
+                        }
+                    }
+            dst[i] = acc / cnt;
+        }
+        __syncthreads();  // (block-scope visibility of the level just written)
+    }
 }
 
 // One thread per cell of the grid padded by one voxel: 1 if the voxel or any of
@@ -141,7 +259,12 @@ int lvx_density_l0(const uint8_t *counts_d, const uint32_t *offsets_d,
                    const lvx_seg_record *seg_rec_d, const float *table_d, int64_t n_voxels,
                    float *level0_d, void *stream) {
     LVX_REQUIRE(counts_d && offsets_d && table_d && level0_d && n_voxels > 0, "bad arguments");
-    density_l0_kernel<<<(unsigned)lvx_ceil_div(n_voxels, 256), 256, 0, (cudaStream_t)stream>>>(
+    LVX_REQUIRE(((uintptr_t)seg_rec_d & 15) == 0, "seg_rec_d must be 16-byte aligned");
+    // a few warps' worth of voxels per warp keeps the grid at some waves of the 148 SMs
+    const i64 warps = lvx_ceil_div(n_voxels, 32);
+    const i64 blocks = lvx_ceil_div(warps, kDlThreads / 32);
+    const i64 cap = (i64)lvx_sm_count() * 64;
+    density_l0_kernel<<<(unsigned)(blocks < cap ? blocks : cap), kDlThreads, 0, (cudaStream_t)stream>>>(
         counts_d, offsets_d, seg_rec_d, table_d, n_voxels, level0_d);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
@@ -172,13 +295,33 @@ int lvx_build_octree(float *flat_d, const int32_t dims[3], void *stream) {
     i64 off[LVX_MAX_LEVELS + 1], ld[LVX_MAX_LEVELS * 3];
     int32_t L = 0;
     if (int rc = lvx_octree_layout(dims, off, ld, &L)) return rc;
-    for (int l = 1; l < L; ++l) {
-        const int sx = (int)ld[3 * (l - 1)], sy = (int)ld[3 * (l - 1) + 1], sz = (int)ld[3 * (l - 1) + 2];
-        const int px = (int)ld[3 * l], py = (int)ld[3 * l + 1], pz = (int)ld[3 * l + 2];
-        dim3 grid((unsigned)lvx_ceil_div(px, kMipP), (unsigned)lvx_ceil_div(py, kMipP),
-                  (unsigned)lvx_ceil_div(pz, kMipP));
-        mip_kernel<<<grid, kMipP * kMipP * kMipP, 0, (cudaStream_t)stream>>>(
-            flat_d + off[l - 1], sx, sy, sz, flat_d + off[l], px, py, pz);
+    auto dims_of = [&](int l) {
+        MipDims d = {1, 1, 1};
+        if (l < L) d = MipDims{(int)ld[3 * l], (int)ld[3 * l + 1], (int)ld[3 * l + 2]};
+        return d;
+    };
+    int l = 0;
+    // three levels per pass while the level is large ...
+    while (l + 1 < L && ld[3 * l] * ld[3 * l + 1] * ld[3 * l + 2] > 64 * 64 * 64) {
+        const int n_out = (L - 1 - l) < 3 ? (L - 1 - l) : 3;
+        const MipDims d0 = dims_of(l), d1 = dims_of(l + 1), d2 = dims_of(l + 2), d3 = dims_of(l + 3);
+        dim3 grid((unsigned)lvx_ceil_div(d1.x, kMipP), (unsigned)lvx_ceil_div(d1.y, kMipP),
+                  (unsigned)lvx_ceil_div(d1.z, kMipP));
+        mip3_kernel<<<grid, kMipP * kMipP * kMipP, 0, (cudaStream_t)stream>>>(
+            flat_d + off[l], d0, flat_d + off[l + 1], d1, n_out >= 2 ? flat_d + off[l + 2] : nullptr, d2,
+            n_out >= 3 ? flat_d + off[l + 3] : nullptr, d3, n_out);
+        LVX_LAUNCH_CHECK();
+        l += n_out;
+    }
+    // ... and the rest of the pyramid in one block
+    if (l + 1 < L) {
+        MipTail T;
+        memset(&T, 0, sizeof(T));
+        for (int k = 0; k <= L; ++k) T.off[k] = off[k];
+        for (int k = 0; k < 3 * L; ++k) T.dims[k] = (int)ld[k];
+        T.first = l;
+        T.n_levels = L;
+        mip_tail_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(flat_d, T);
         LVX_LAUNCH_CHECK();
     }
     return LVX_OK;

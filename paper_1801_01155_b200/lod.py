@@ -94,12 +94,14 @@ class DensityOctree:
                                       float(1 << level), np.asarray(point, dtype=np.float64)[None])[0])
 
 
-def density_level0_device(model: VoxelModel):
-    """Level-0 density as a device tensor f32[V] (no host copy)."""
+def density_level0_device(model: VoxelModel, out=None):
+    """Level-0 density as a device tensor f32[V] (no host copy); `out` may be the front of an
+    octree buffer, so the mip chain reads it in place."""
     torch = _lib.require_device()
     counts_d, offsets_d, rec_d, table_d, _ = model.device_view(need_occ=False)
     V = model.voxel_count
-    out = torch.empty(V, dtype=torch.float32, device="cuda")
+    if out is None:
+        out = torch.empty(V, dtype=torch.float32, device="cuda")
     _lib.check(_lib.lib().lvx_density_l0(_lib.ptr(counts_d), _lib.ptr(offsets_d), _lib.ptr(rec_d),
                                          _lib.ptr(table_d), C.c_int64(V), _lib.ptr(out),
                                          _lib.stream_ptr()))
@@ -135,9 +137,26 @@ def build_octree(level0: np.ndarray) -> DensityOctree:
     return _octree_from_level0_device(l0, (dx, dy, dz))
 
 
+def octree_buffer(dims):
+    """Uninitialised flat device buffer of all levels (level 0 first)."""
+    torch = _lib.require_device()
+    off, _, _ = octree_layout(dims)
+    return torch.empty(int(off[-1]), dtype=torch.float32, device="cuda"), int(off[1])
+
+
+def mips_inplace(flat, dims):
+    """Levels 1.. of the pyramid from level 0 at the front of `flat` (lvx_build_octree)."""
+    _lib.check(_lib.lib().lvx_build_octree(_lib.ptr(flat), _lib.i32x3(dims), _lib.stream_ptr()))
+
+
 def build_lod(model: VoxelModel) -> DensityOctree:
-    """compute_density_level0 + build_octree without leaving the GPU."""
-    return _octree_from_level0_device(density_level0_device(model), model.spec.dims)
+    """compute_density_level0 + build_octree without leaving the GPU: the density kernel writes
+    level 0 straight into the octree buffer, the mip kernels fill the rest."""
+    dims = model.spec.dims
+    flat, v0 = octree_buffer(dims)
+    density_level0_device(model, out=flat[:v0])
+    mips_inplace(flat, dims)
+    return DensityOctree(_flat_dev=flat, _dims=dims)
 
 
 # --- representative lines (lod.py:61-79, 122-284) ---------------------------------------------

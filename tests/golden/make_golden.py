@@ -353,6 +353,92 @@ def make_brute(models, octrees, ao_fields):
              transfer_table=np.asarray(m.transfer_table, np.float32), size=np.asarray([W, H]), params=np.array(repr(kw)))
 
 
+def make_occupancy(models):
+    """_occupancy_dilated (raycast.py:351-366): u8 map over the grid padded by one voxel."""
+    for name in ("helices", "turbulence", "lattice", "cap255", "wiggles"):
+        m, dims = models[name]
+        m.__dict__.pop("_occ_dilated", None)
+        save("occ_" + name, occ=np.ascontiguousarray(RR._occupancy_dilated(m)), dims=np.asarray(dims))
+
+
+def _sha(a):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+ROW_STEP = 16  # big frames: every 16th row of the reference's image is stored (plus the hash of all of it)
+
+
+def _save_big_frame(name, fr, m, kw, W, H, extra=None):
+    st = fr.stats
+    save(name, rows=np.ascontiguousarray(fr.image[::ROW_STEP]), row_step=np.int64(ROW_STEP),
+         image_sha256=np.array(_sha(fr.image)), size=np.asarray([W, H]), params=np.array(repr(kw)),
+         stats=np.asarray([st["voxel_steps"], st["intersection_tests"], st["window_overflow"]], np.int64),
+         packed_sha256=np.array(_sha(m.packed)), counts_sha256=np.array(_sha(m.counts)),
+         segments=np.int64(m.segment_count), **(extra or {}))
+
+
+def make_big():
+    """The frames bench.py times, rendered by the unmodified reference at full size:
+    BASELINE configs[1] (C2) and configs[2] (C3) at 1920x1080 (SURVEY.md 8d generators)."""
+    import time
+    if ONLY is None or "big_c2_1080p".startswith(ONLY):
+        dims = (128, 128, 128)
+        t0 = time.time()
+        m = ref_model(*synth.helices(10000, 100, dims), dims, 32)
+        kw = dict(base_opacity=0.25, tau=0.95, neighbor_mode="on")
+        fr = RR.render_frame(RR.default_camera(dims, 1920, 1080), m, None, None, RR.RenderParams(**kw), workers=8)
+        print(f"C2: {time.time() - t0:.0f} s, stats {fr.stats}")
+        _save_big_frame("big_c2_1080p", fr, m, kw, 1920, 1080)
+        # own-voxel mode of the same frame
+        kw2 = dict(kw, neighbor_mode="off")
+        fr = RR.render_frame(RR.default_camera(dims, 1920, 1080), m, None, None, RR.RenderParams(**kw2), workers=8)
+        _save_big_frame("big_c2_1080p_own", fr, m, kw2, 1920, 1080)
+    if ONLY is None or "big_c3_1080p".startswith(ONLY):
+        dims = (256, 256, 256)
+        t0 = time.time()
+        m = ref_model(*synth.turbulence(100000, 100, dims), dims, 32)
+        print(f"C3 voxelized: {time.time() - t0:.0f} s")
+        l0 = compute_density_level0(m)
+        oc = build_octree(l0)
+        ao = precompute_voxel_ao(m, oc, AOParams(n_rays=100, radius=5.0, step=1.0), workers=8)
+        m.ao = ao.values
+        print(f"C3 LoD + AO: {time.time() - t0:.0f} s")
+        kw = dict(base_opacity=0.25, tau=0.95, neighbor_mode="on", ao_mode="precomputed")
+        fr = RR.render_frame(RR.default_camera(dims, 1920, 1080), m, oc, None, RR.RenderParams(**kw), workers=8)
+        print(f"C3: {time.time() - t0:.0f} s, stats {fr.stats}")
+        _save_big_frame("big_c3_1080p", fr, m, kw, 1920, 1080,
+                        extra=dict(level0_sha256=np.array(_sha(l0)), ao_sha256=np.array(_sha(ao.values)),
+                                   levels_sha256=np.array([_sha(l) for l in oc.levels])))
+
+
+def make_acceptance():
+    """The reference's own acceptance scene (tests/test_acceptance.py:144-169): tornado(1000, 250, 42)
+    normalised into a 256^3 grid, N = 32, 640x360, opaque and alpha = 0.25, neighbour mode on."""
+    if ONLY is not None and not "accept_tornado256".startswith(ONLY):
+        return
+    from linevox.scene_io import generate_tornado, normalize_to_grid
+    spec = GridSpec((256, 256, 256), 32)
+    cs = normalize_to_grid(generate_tornado(1000, 250, 42), spec)
+    m = RV.build_voxel_model(cs, spec)
+    pts = np.concatenate([c.points for c in cs.curves])
+    attrs = np.concatenate([c.attrs for c in cs.curves])
+    off = np.zeros(len(cs.curves) + 1, np.int64)
+    np.cumsum([len(c.points) for c in cs.curves], out=off[1:])
+    cam = RR.default_camera(spec.dims, 640, 360)
+    out = {}
+    for tag, kw in (("opaque", dict(neighbor_mode="on")), ("alpha25", dict(neighbor_mode="on", base_opacity=0.25))):
+        fr = RR.render_frame(cam, m, None, None, RR.RenderParams(**kw), workers=8)
+        st = fr.stats
+        out["rows_" + tag] = np.ascontiguousarray(fr.image[::4])
+        out["sha_" + tag] = np.array(_sha(fr.image))
+        out["stats_" + tag] = np.asarray([st["voxel_steps"], st["intersection_tests"], st["window_overflow"]], np.int64)
+        out["params_" + tag] = np.array(repr(kw))
+    save("accept_tornado256", pts=pts, attrs=attrs, off=off, dims=np.asarray(spec.dims), row_step=np.int64(4),
+         packed_sha256=np.array(_sha(m.packed)), counts_sha256=np.array(_sha(m.counts)),
+         segments=np.int64(m.segment_count), dropped=np.int64(m.dropped_overflow), **out)
+
+
 def main():
     global ONLY
     if "--only" in sys.argv:
@@ -365,6 +451,9 @@ def main():
     make_geometry_probes(models)
     make_replines(models, octrees)
     make_brute(models, octrees, ao_fields)
+    make_occupancy(models)
+    make_acceptance()
+    make_big()
 
 
 if __name__ == "__main__":

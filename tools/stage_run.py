@@ -7,7 +7,7 @@ import torch
 import paper_1801_01155_b200 as lv
 from paper_1801_01155_b200 import synth, _lib
 from paper_1801_01155_b200.illumination import ao_bake_device
-from paper_1801_01155_b200.lod import density_level0_device, _octree_from_level0_device
+from paper_1801_01155_b200.lod import density_level0_device, mips_inplace, octree_buffer
 
 dims = (256,) * 3
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 100000
@@ -20,8 +20,9 @@ torch.cuda.synchronize()
 print("== passes start", flush=True)
 for rep in range(2):
     lv.voxelize_device(pts_d, attrs_d, off_d, n, spec, caches=False, provenance=False)
-    l0 = density_level0_device(model)
-    _octree_from_level0_device(l0, dims)
+    flat, v0 = octree_buffer(dims)
+    density_level0_device(model, out=flat[:v0])
+    mips_inplace(flat, dims)
     ao_bake_device(model, octree, lv.AOParams(n_rays=100, radius=5.0, step=1.0))
     torch.cuda.synchronize()
 print("done")
