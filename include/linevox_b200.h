@@ -32,7 +32,7 @@ extern "C" {
 #define LVX_E_NO_DEVICE 3 /* no sm_100-class device visible */
 #define LVX_E_RANGE 4     /* size exceeds a documented limit */
 
-#define LVX_ABI_VERSION 1
+#define LVX_ABI_VERSION 2
 
 /* mode codes: _kernels.py:43-55 */
 #define LVX_OPACITY_CONSTANT 0
@@ -184,10 +184,12 @@ int lvx_occupancy_dilate(const uint8_t *counts_d, const int32_t dims[3], uint8_t
  *           candidate segments the reference's neighbour gather visits for a window in
  *           that cell (_kernels.py:811-821), i.e. what `intersection_tests` adds per window;
  *   nmask_d u32[same] (nullable)  bit (dz+1)*9+(dy+1)*3+(dx+1) set when that neighbour
- *           holds segments; bit order == the reference's gather order.
+ *           holds segments; bit order == the reference's gather order;
+ *   ncell_d u64[same] (nullable)  nmask | (u64)nsum << 32: both in ONE 8-byte load per DDA window
+ *           (the wavefront engine's walk reads these).
  * The frame kernel reads these instead of 27 voxel headers per window. */
 int lvx_neighbor_sums(const uint8_t *counts_d, const int32_t dims[3], uint16_t *nsum_d,
-                      uint32_t *nmask_d, void *stream);
+                      uint32_t *nmask_d, uint64_t *ncell_d, void *stream);
 
 /* ------------------------------------------------------------------------- */
 /* Ray-caster: render_rows + stream_hit + dda_collect + tube/sphere + sort     */
@@ -203,13 +205,16 @@ typedef struct {
 
 typedef struct {
     int32_t rx, ry, rz;
-    int32_t _pad;
+    int32_t n_bins;            /* bin resolution of packed_d (only read when the frame renders from packed_d) */
     const uint8_t *counts_d;
     const uint32_t *offsets_d;
     const lvx_seg_record *seg_rec_d;
     const float *table_d;      /* f32[256,4] */
-    const uint16_t *nsum_d;    /* from lvx_neighbor_sums (both needed in neighbour mode) */
+    const uint16_t *nsum_d;    /* from lvx_neighbor_sums (all three needed in neighbour mode) */
     const uint32_t *nmask_d;
+    const uint64_t *ncell_d;
+    const uint8_t *packed_d;   /* the encoded records (voxelizer.py:79-89); NULL unless the frame is to be
+                                * rendered straight from them (lvx_render_wf) */
 } lvx_model;
 
 typedef struct {
@@ -382,6 +387,31 @@ int lvx_probe_blocked(const lvx_model *model, const double *rays_d, const double
 int lvx_probe_ao_hemisphere(const lvx_model *model, const double *pts_d, const double *normals_d,
                             int32_t n_rays, double radius, const double *dirs_d, double tube_r,
                             int64_t n, double *out_d, void *stream);
+
+/* ------------------------------------------------------------------------- */
+/* Probes behind the remaining Python-level reference ops (tests re-pointed at   */
+/* this package call them through the same names as the reference's).            */
+/* ------------------------------------------------------------------------- */
+
+/* _clip_batch (voxelizer.py:213-263) with its float64 outputs, as used by the reference op
+ * clip_curve_to_voxels (voxelizer.py:273-287): every kept chord's voxel (i64[.,3]), entry and
+ * exit point (f64[.,3]), entry / exit attribute (f64[.,2]) and its key (edge index << 16 |
+ * ordinal on the edge).  Chords are appended in arbitrary order; sorting by key gives the
+ * reference's order.  *n_d = number of chords found (may exceed `capacity`: call again). */
+int lvx_probe_clip(const double *pts_d, const double *attrs_d, const uint8_t *first_d, int64_t n_points,
+                   const int32_t dims[3], uint64_t capacity, int64_t *vox_d, double *p_in_d, double *p_out_d,
+                   double *attr_d, uint64_t *key_d, uint64_t *n_d, void *stream);
+
+/* shade_scalar (_kernels.py:316-329) for n rows of (normal, light, view) = f64[n,9]; the op behind
+ * shade_local (raycast.py:286-294). */
+int lvx_probe_shade(const double *nlv_d, double ka, double kd, double ks, double shininess, int64_t n,
+                    double *out_d, void *stream);
+
+/* representative_line (lod.py:141-169) for one explicit member list: starts/ends f64[m,3] in the
+ * given order, voxel cube (origin, size), bin resolution.  out_d f64[7] = a, b, weight;
+ * scratch_d f64[m]. */
+int lvx_probe_rep_line(const double *starts_d, const double *ends_d, int64_t m, const double origin[3],
+                       double size, int32_t n_bins, double *scratch_d, double *out_d, void *stream);
 
 #ifdef __cplusplus
 }

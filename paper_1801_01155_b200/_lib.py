@@ -28,9 +28,10 @@ class Camera(C.Structure):
 
 
 class Model(C.Structure):
-    _fields_ = [("rx", C.c_int32), ("ry", C.c_int32), ("rz", C.c_int32), ("_pad", C.c_int32),
+    _fields_ = [("rx", C.c_int32), ("ry", C.c_int32), ("rz", C.c_int32), ("n_bins", C.c_int32),
                 ("counts_d", C.c_void_p), ("offsets_d", C.c_void_p), ("seg_rec_d", C.c_void_p),
-                ("table_d", C.c_void_p), ("nsum_d", C.c_void_p), ("nmask_d", C.c_void_p)]
+                ("table_d", C.c_void_p), ("nsum_d", C.c_void_p), ("nmask_d", C.c_void_p),
+                ("ncell_d", C.c_void_p), ("packed_d", C.c_void_p)]
 
 
 class Params(C.Structure):
@@ -70,6 +71,7 @@ SYMBOLS = [
     "lvx_fibonacci_dirs", "lvx_ao_bake", "lvx_probe_dda", "lvx_probe_tube", "lvx_probe_sphere",
     "lvx_probe_trilinear", "lvx_probe_cone", "lvx_probe_ao_density", "lvx_probe_blocked",
     "lvx_probe_ao_hemisphere", "lvx_rep_level", "lvx_probe_replines", "lvx_brute_count", "lvx_brute_render",
+    "lvx_probe_clip", "lvx_probe_shade", "lvx_probe_rep_line",
 ]
 
 _lib = None

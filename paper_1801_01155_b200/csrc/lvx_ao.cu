@@ -229,6 +229,14 @@ __global__ void probe_ao_kernel(const LvxOctree oc, const double *__restrict__ p
                                   oc.flat, oc.dims[0], oc.dims[1], oc.dims[2]);
 }
 
+__global__ void probe_shade_kernel(const double *__restrict__ nlv, double ka, double kd, double ks, double shininess,
+                                   i64 n, double *__restrict__ out) {
+    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double *q = nlv + 9 * i;
+    out[i] = lvx_shade(q[0], q[1], q[2], q[3], q[4], q[5], q[6], q[7], q[8], ka, kd, ks, shininess);
+}
+
 int fill_octree(LvxOctree &oc, const lvx_lod *lod) {
     LVX_REQUIRE(lod && lod->oct_flat_d && lod->n_levels >= 1 && lod->n_levels <= LVX_MAX_LEVELS,
                 "a density octree is required");
@@ -345,6 +353,17 @@ int lvx_probe_sphere(const double *rays_d, const double *c_d, double radius, int
     LVX_REQUIRE(rays_d && c_d && out_d, "null argument");
     probe_sphere_kernel<<<(unsigned)lvx_ceil_div(n, 128), 128, 0, (cudaStream_t)stream>>>(
         rays_d, c_d, radius, n, out_d);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_probe_shade(const double *nlv_d, double ka, double kd, double ks, double shininess, int64_t n,
+                    double *out_d, void *stream) {
+    LVX_REQUIRE(n >= 0, "bad arguments");
+    if (n == 0) return LVX_OK;
+    LVX_REQUIRE(nlv_d && out_d, "null argument");
+    probe_shade_kernel<<<(unsigned)lvx_ceil_div(n, 128), 128, 0, (cudaStream_t)stream>>>(nlv_d, ka, kd, ks, shininess, n,
+                                                                                        out_d);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }

@@ -225,7 +225,7 @@ dilate_kernel(const u8 *__restrict__ counts, int rx, int ry, int rz, u8 *__restr
 //           segments: bit order == the reference's gather order (z, y, x loops).
 __global__ void __launch_bounds__(256)
 nsum_kernel(const u8 *__restrict__ counts, int rx, int ry, int rz, u16 *__restrict__ nsum,
-            u32 *__restrict__ nmask) {
+            u32 *__restrict__ nmask, u64 *__restrict__ ncell) {
     const i64 sx = rx + 2, sy = ry + 2, sz = rz + 2;
     const i64 c = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= sx * sy * sz) return;
@@ -249,6 +249,7 @@ nsum_kernel(const u8 *__restrict__ counts, int rx, int ry, int rz, u16 *__restri
     }
     nsum[c] = (u16)sum;
     if (nmask) nmask[c] = mask;
+    if (ncell) ncell[c] = (u64)mask | ((u64)sum << 32);
 }
 
 }  // namespace
@@ -339,12 +340,12 @@ int lvx_occupancy_dilate(const uint8_t *counts_d, const int32_t dims[3], uint8_t
 }
 
 int lvx_neighbor_sums(const uint8_t *counts_d, const int32_t dims[3], uint16_t *nsum_d,
-                      uint32_t *nmask_d, void *stream) {
+                      uint32_t *nmask_d, uint64_t *ncell_d, void *stream) {
     LVX_REQUIRE(counts_d && nsum_d && dims && dims[0] >= 1 && dims[1] >= 1 && dims[2] >= 1,
                 "bad arguments");
     const i64 cells = (i64)(dims[0] + 2) * (dims[1] + 2) * (dims[2] + 2);
     nsum_kernel<<<(unsigned)lvx_ceil_div(cells, 256), 256, 0, (cudaStream_t)stream>>>(
-        counts_d, dims[0], dims[1], dims[2], nsum_d, nmask_d);
+        counts_d, dims[0], dims[1], dims[2], nsum_d, nmask_d, ncell_d);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }

@@ -277,9 +277,84 @@ probe_replines_kernel(LvxRepLevel rep, const double *__restrict__ rays, const do
     out[i] = lvx_replines_blocked(r[0], r[1], r[2], r[3], r[4], r[5], max_t[i], rep, radius_base) ? 1 : 0;
 }
 
+// numpy's pairwise float64 sum over a plain vector (np.sum of the member lengths, lod.py:168)
+__device__ double pairwise_sum_vec(const double *w, int n) {
+    if (n < 8) {
+        double res = 0.0;
+        for (int i = 0; i < n; ++i) res += w[i];
+        return res;
+    }
+    if (n <= 128) {
+        double r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = w[j];
+        int i;
+        for (i = 8; i < n - (n % 8); i += 8) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] += w[i + j];
+        }
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; ++i) res += w[i];
+        return res;
+    }
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    return pairwise_sum_vec(w, n2) + pairwise_sum_vec(w + n2, n - n2);
+}
+
+// representative_line (lod.py:141-169) for one explicit member list: the same flip rule, sums
+// and face-bin snap the level kernel applies per parent voxel.  One thread; `len_d` is scratch.
+__global__ void probe_rep_line_kernel(const double *__restrict__ starts, const double *__restrict__ ends, int m,
+                                      double ox, double oy, double oz, double size, int n_bins,
+                                      double *__restrict__ len_d, double *__restrict__ out) {
+    double sa[3] = {0.0, 0.0, 0.0}, sb[3] = {0.0, 0.0, 0.0};
+    for (int i = 0; i < m; ++i) {
+        const double *a = starts + 3 * i, *b = ends + 3 * i;
+        bool flip = false;
+        if (i > 0) {
+            const double d0 = b[0] - a[0], d1 = b[1] - a[1], d2 = b[2] - a[2];
+            const double e0 = sb[0] - sa[0], e1 = sb[1] - sa[1], e2 = sb[2] - sa[2];
+            flip = d0 * e0 + d1 * e1 + d2 * e2 < 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            sa[q] += flip ? b[q] : a[q];
+            sb[q] += flip ? a[q] : b[q];
+        }
+        const double d0 = b[0] - a[0], d1 = b[1] - a[1], d2 = b[2] - a[2];
+        len_d[i] = sqrt((d0 * d0 + d1 * d1) + d2 * d2);
+    }
+    const double origin[3] = {ox, oy, oz};
+    double la[3], lb[3], qa[3], qb[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        la[q] = (sa[q] / (double)m - origin[q]) / size;
+        lb[q] = (sb[q] / (double)m - origin[q]) / size;
+    }
+    snap_to_face_bin(la, n_bins, qa);
+    snap_to_face_bin(lb, n_bins, qb);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        out[q] = qa[q] * size + origin[q];
+        out[3 + q] = qb[q] * size + origin[q];
+    }
+    out[6] = pairwise_sum_vec(len_d, m);
+}
+
 }  // namespace
 
 extern "C" {
+
+int lvx_probe_rep_line(const double *starts_d, const double *ends_d, int64_t m, const double origin[3],
+                       double size, int32_t n_bins, double *scratch_d, double *out_d, void *stream) {
+    LVX_REQUIRE(starts_d && ends_d && origin && scratch_d && out_d && m >= 1 && m < ((int64_t)1 << 30), "bad arguments");
+    LVX_REQUIRE(size > 0.0, "size must be positive");
+    LVX_REQUIRE(n_bins >= 2 && n_bins <= 256 && (n_bins & (n_bins - 1)) == 0, "bad bin resolution %d", n_bins);
+    probe_rep_line_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(starts_d, ends_d, (int)m, origin[0], origin[1], origin[2],
+                                                            size, n_bins, scratch_d, out_d);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
 
 int lvx_rep_level(const int32_t child_dims[3], const uint8_t *c_counts_d, const uint32_t *c_offsets_d,
                   const lvx_seg_record *seg_rec_d, const uint8_t *c_valid_d, const float *c_a_d,

@@ -337,6 +337,69 @@ clip_once_kernel(const double *__restrict__ pts, const double *__restrict__ attr
     if (i < n_points && edge_kept) edge_kept[i] = (u16)kept;
 }
 
+// _clip_batch (voxelizer.py:213-263) with its float64 outputs, for the reference op
+// clip_curve_to_voxels and the parity tests: one thread per edge, the kept chords are appended
+// in any order with their (edge, ordinal) key; the host sorts by key.
+__global__ void __launch_bounds__(128)
+probe_clip_kernel(const double *__restrict__ pts, const double *__restrict__ attrs, const u8 *__restrict__ first,
+                  i64 n_points, int rx, int ry, int rz, u64 capacity, i64 *__restrict__ out_vox,
+                  double *__restrict__ out_pin, double *__restrict__ out_pout, double *__restrict__ out_attr,
+                  u64 *__restrict__ out_key, unsigned long long *__restrict__ n_out) {
+    __shared__ ClipStage S;  // (unused: everything is read from global memory)
+    const ClipView V = {S, pts, attrs, first, 0, 0};
+    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i + 1 >= n_points || first[i + 1]) return;
+    double a0[3], a1[3];
+    V.vertex(i, a0);
+    V.vertex(i + 1, a1);
+    EdgeAxes E;
+    E.init(a0, a1);
+    const int total = E.total();
+    if (total == 0) return;
+    const double att0 = attrs[i], att1 = attrs[i + 1];
+    Event prev, ev;
+    bool have_prev = lookback_event_v<true>(V, i, prev);
+    int j[3] = {0, 0, 0};
+    u32 kept = 0;
+    for (int n = 0; n < total; ++n) {
+        int best = -1;
+        double bs = 0.0, bk = 0.0;
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            if (j[ax] >= E.cnt[ax]) continue;
+            const double k = E.plane(ax, j[ax]);
+            const double sv = E.param(ax, k);
+            if (best < 0 || sv < bs) {  // ties resolve x<y<z (stable lexsort, voxelizer.py:224)
+                best = ax;
+                bs = sv;
+                bk = k;
+            }
+        }
+        j[best] += 1;
+        make_event(ev, E, a0, att0, att1, true, best, bk, bs);
+        if (have_prev) {
+            long long vox[3];
+            if (chord_voxel(prev, ev, rx, ry, rz, vox) >= 0) {
+                const unsigned long long slot = atomicAdd(n_out, 1ull);
+                if (slot < capacity) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        out_vox[3 * slot + c] = vox[c];
+                        out_pin[3 * slot + c] = prev.pos[c];
+                        out_pout[3 * slot + c] = ev.pos[c];
+                    }
+                    out_attr[2 * slot] = prev.attr;
+                    out_attr[2 * slot + 1] = ev.attr;
+                    out_key[slot] = ((u64)i << 16) | (u64)kept;
+                }
+                kept += 1;
+            }
+        }
+        prev = ev;
+        have_prev = true;
+    }
+}
+
 // Upper bound of the chord count: every chord ends at a plane crossing.
 __global__ void __launch_bounds__(256)
 count_crossings_kernel(const double *__restrict__ pts, const u8 *__restrict__ first, i64 n_points,
@@ -932,6 +995,23 @@ int lvx_voxelize_clip(const double *pts_d, const double *attrs_d, const uint8_t 
     clip_once_kernel<<<(unsigned)lvx_ceil_div(n_points, kClipThreads), kClipThreads, 0, st>>>(
         pts_d, attrs_d, first_d, n_points, dims[0], dims[1], dims[2], n_bins, capacity, vox_cnt_d, raw_key_d,
         raw_q_d, raw_lin_d, reinterpret_cast<unsigned long long *>(n_slots_d), edge_kept_d, err_d);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_probe_clip(const double *pts_d, const double *attrs_d, const uint8_t *first_d, int64_t n_points,
+                   const int32_t dims[3], uint64_t capacity, int64_t *vox_d, double *p_in_d, double *p_out_d,
+                   double *attr_d, uint64_t *key_d, uint64_t *n_d, void *stream) {
+    if (int rc = check_dims(dims)) return rc;
+    LVX_REQUIRE(n_d && n_points >= 0, "bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    LVX_CUDA_CHECK(cudaMemsetAsync(n_d, 0, 8, st));
+    if (n_points < 2) return LVX_OK;
+    LVX_REQUIRE(pts_d && attrs_d && first_d && (capacity == 0 || (vox_d && p_in_d && p_out_d && attr_d && key_d)),
+                "null input");
+    probe_clip_kernel<<<(unsigned)lvx_ceil_div(n_points, 128), 128, 0, st>>>(
+        pts_d, attrs_d, first_d, n_points, dims[0], dims[1], dims[2], capacity, vox_d, p_in_d, p_out_d, attr_d, key_d,
+        reinterpret_cast<unsigned long long *>(n_d));
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }

@@ -11,8 +11,10 @@
 // float64 tests need ~170 registers, the rays of a warp diverge, and the tile kernel
 // (lvx_render.cu) spends most of its cycles at block barriers.  Here every link of the
 // chain is its own kernel over ALL live rays, with its own register budget, full
-// occupancy and every lane busy; the links talk through queues in HBM (a few GB/s of
-// traffic per frame, three orders of magnitude below what the 7.7 TB/s can carry):
+// occupancy; the links talk through queues in device memory.  That decoupling is not free: the
+// queues and the per-ray state move ~13 GB per C3 frame through L2/HBM (ncu, profiles/) against
+// 0.16 GB of model bytes the algorithm touches -- ~1.5 TB/s, a fifth of the HBM peak -- and the
+// frame is bound by load latency and lane divergence of the ray-parallel links, not by bandwidth:
 //
 //   init       one thread per pixel: primary ray, slab clip, full-walk window count
 //              (`voxel_steps`), background for rays that miss; live rays are listed.
@@ -94,11 +96,13 @@ struct __align__(32) WfRayDir {
     double dx, dy, dz, t_lo;
 };
 
-struct WfEntry {
+struct __align__(16) WfEntry {
     u32 seg;    // segment (| sphere B << 31 in the sphere queue)
-    u32 item;   // the (ray, voxel) item it came from
     u32 place;  // the ray's position in the live list (saves the exact kernels a dependent load)
+    u32 lin;    // home voxel of the segment
+    u32 aux;    // neighbour mode: index of the segment in its voxel; own-voxel mode: the item (its window range)
 };
+static_assert(sizeof(WfEntry) == 16, "survivor entry is one 16-byte access");
 
 // per-ray state, one record per pixel slot (read and written with 16-byte accesses)
 struct __align__(16) WfRayWalk {   // owned by the walk
@@ -134,7 +138,15 @@ struct WfCtl {
     u32 wn;    // windows per ray of the current iteration
     u32 budget;  // candidate budget per ray of the current iteration (neighbour-sum units)
     u32 live0;   // rays alive after the first iteration (what "few rays left" is measured against)
+#ifdef LVX_WF_STATS
+    unsigned long long dbg[8];  // developer counters: owned hits, composited, suppressed, rays with hits, terminated
+#endif
 };
+#ifdef LVX_WF_STATS
+#define WF_STAT(k, v) atomicAdd(&A.ctl->dbg[k], (unsigned long long)(v))
+#else
+#define WF_STAT(k, v)
+#endif
 
 struct WfArgs {
     lvx_camera cam;
@@ -146,6 +158,7 @@ struct WfArgs {
     const float *table;
     const u16 *nsum;
     const u32 *nmask;
+    const unsigned long long *ncell;  // nmask | nsum << 32 per padded cell (one load per window)
     LvxOctree oc;
     const float *ao_flat;
     const double *ao_dirs;
@@ -173,7 +186,7 @@ struct WfArgs {
     float4 *item_q;              // ray point near the voxel, relative to the voxel's corner (float32)
     double2 *item_t;             // own-voxel mode: parameter range of the item's window
     u32 capq_item;
-    float *fdir;                 // [3][R] float32 ray direction by place
+    float4 *fdir;                // [R] float32 ray direction by place (one sector per item in the pre-reject)
     double *span;                // [2][R] parameter range walked this iteration, by place
     WfRayDir *rdir;              // [R] float64 direction + start of the walked range, by place (exact kernels)
     WfEntry *tube, *sph;
@@ -447,42 +460,58 @@ struct __align__(16) WalkRec {
 static_assert(sizeof(WalkRec) == 32, "staged window record is 32 bytes");
 struct WalkStage {
     WalkRec rec[kThreadsWf / 32][kWalkStage];
+    u16 pre[kThreadsWf / 32][kWalkStage];  // items before record r (exclusive prefix of popc(fresh))
     u32 n[kThreadsWf / 32];
 };
 
-// all 32 lanes of the warp
+// all 32 lanes of the warp.  The staged windows are expanded to items so that CONSECUTIVE LANES
+// WRITE CONSECUTIVE ITEMS: every store instruction fills whole sectors (a lane that wrote the
+// items of "its" window one after the other touched a different sector per lane and store).
 __device__ __forceinline__ void walk_flush(const WfArgs &A, WalkStage &S, int warp, int lane, int q) {
+    constexpr unsigned FULL = 0xFFFFFFFFu;
     __syncwarp();
     const u32 n = min(S.n[warp], (u32)kWalkStage);
     if (n) {
-        u32 mine = 0;
-        for (u32 r = lane; r < n; r += 32) mine += (u32)__popc(S.rec[warp][r].fresh);
-        u32 inc = mine;
+        u32 total = 0;
+        for (u32 r0 = 0; r0 < n; r0 += 32) {
+            const u32 r = r0 + (u32)lane;
+            const u32 v = r < n ? (u32)__popc(S.rec[warp][r].fresh) : 0u;
+            u32 inc = v;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const u32 t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
-            if (lane >= o) inc += t;
+            for (int o = 1; o < 32; o <<= 1) {
+                const u32 t = __shfl_up_sync(FULL, inc, o);
+                if (lane >= o) inc += t;
+            }
+            if (r < n) S.pre[warp][r] = (u16)(total + inc - v);
+            total += __shfl_sync(FULL, inc, 31);
         }
-        const u32 total = __shfl_sync(0xFFFFFFFFu, inc, 31);
         u32 base = 0;
-        if (lane == 31) base = atomicAdd(&A.ctl->item_cnt[q], total);
-        base = __shfl_sync(0xFFFFFFFFu, base, 31);
+        if (lane == 0) base = atomicAdd(&A.ctl->item_cnt[q], total);
+        base = __shfl_sync(FULL, base, 0);
+        __syncwarp();
         if (base + total > A.capq_item) {
-            if (lane == 31) atomicOr(&A.ctl->err, 1u);
+            if (lane == 0) atomicOr(&A.ctl->err, 1u);
         } else {
-            u32 j = (u32)q * A.capq_item + base + inc - mine;
-            for (u32 r = lane; r < n; r += 32) {
-                const WalkRec w = S.rec[warp][r];
+            const u32 out0 = (u32)q * A.capq_item + base;
+            for (u32 j = (u32)lane; j < total; j += 32) {
+                // the record that holds item j: the last r with pre[r] <= j
+                u32 lo = 0, hi = n;
+                while (hi - lo > 1) {
+                    const u32 mid = (lo + hi) >> 1;
+                    if ((u32)S.pre[warp][mid] <= j) lo = mid;
+                    else hi = mid;
+                }
+                const WalkRec w = S.rec[warp][lo];
+                u32 mm = w.fresh;
+                for (u32 k = j - (u32)S.pre[warp][lo]; k; --k) mm &= mm - 1;  // its k-th fresh voxel
+                const int b = __ffs((int)mm) - 1;
                 const int wx = (int)(w.cell & 0xFFFFFu) - 1, wy = (int)((w.cell >> 20) & 0xFFFFFu) - 1,
                           wz = (int)(w.cell >> 40) - 1;
-                for (u32 mm = w.fresh; mm; mm &= mm - 1, ++j) {
-                    const int b = __ffs((int)mm) - 1;
-                    const int bz_ = b / 9, by_ = (b - 9 * bz_) / 3, bx_ = b - 9 * bz_ - 3 * by_;
-                    A.item_place[j] = w.place;
-                    A.item_lin[j] = (u32)((wx + bx_ - 1) + A.rx * ((wy + by_ - 1) + A.ry * (wz + bz_ - 1)));
-                    // voxel-local float32 frame for the (conservative) pre-reject
-                    A.item_q[j] = make_float4(w.qx - (float)(bx_ - 1), w.qy - (float)(by_ - 1), w.qz - (float)(bz_ - 1), 0.0f);
-                }
+                const int bz_ = b / 9, by_ = (b - 9 * bz_) / 3, bx_ = b - 9 * bz_ - 3 * by_;
+                A.item_place[out0 + j] = w.place;
+                A.item_lin[out0 + j] = (u32)((wx + bx_ - 1) + A.rx * ((wy + by_ - 1) + A.ry * (wz + bz_ - 1)));
+                // voxel-local float32 frame for the (conservative) pre-reject
+                A.item_q[out0 + j] = make_float4(w.qx - (float)(bx_ - 1), w.qy - (float)(by_ - 1), w.qz - (float)(bz_ - 1), 0.0f);
             }
         }
     }
@@ -491,10 +520,12 @@ __device__ __forceinline__ void walk_flush(const WfArgs &A, WalkStage &S, int wa
     __syncwarp();
 }
 
+// (3 blocks/SM: with 4 the lock-step walk spills its DDA state; same-box A/B 9.34 -> 8.94 ms)
 #ifndef LVX_WF_WALK_MINB
-#define LVX_WF_WALK_MINB 4
+#define LVX_WF_WALK_MINB 3
 #endif
 __global__ void __launch_bounds__(kThreadsWf, LVX_WF_WALK_MINB) wf_walk_kernel(const WfArgs A, int par) {
+    constexpr unsigned FULL = 0xFFFFFFFFu;
     const u32 n_live = A.ctl->err ? 0u : A.ctl->n_live[par];
     const u32 wn = A.ctl->wn;
     const u32 budget = A.ctl->budget;
@@ -514,121 +545,138 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_WALK_MINB) wf_walk_kernel(c
     for (u32 g0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); (g0 >> spread) < n_live; g0 += gridDim.x * blockDim.x) {
         const u32 i = (g0 + (u32)lane) >> spread;
         const int q = warp_queue(g0);
-        if ((((u32)lane) & ((1u << spread) - 1u)) == 0 && i < n_live) {
-        const u32 slot = A.live[par][i];
-        WfRayWalk rw = A.rw[slot];
-        const double ddx = rw.dir[0], ddy = rw.dir[1], ddz = rw.dir[2];
+        const bool mine = (((u32)lane) & ((1u << spread) - 1u)) == 0 && i < n_live;
+        u32 slot = 0;
+        WfRayWalk rw;
         LvxDda dda;
-        dda_load(A, rw, neighbor ? 1 : 0, dda);
-        unsigned long long tests = rw.tests;
+        double ddx = 0.0, ddy = 0.0, ddz = 0.0, span0 = 0.0;
+        unsigned long long tests = 0;
+        if (mine) {
+            slot = A.live[par][i];
+            rw = A.rw[slot];
+            ddx = rw.dir[0];
+            ddy = rw.dir[1];
+            ddz = rw.dir[2];
+            dda_load(A, rw, neighbor ? 1 : 0, dda);
+            tests = rw.tests;
+            span0 = dda.t_cur;
+        }
         u32 kw = 0, csum = 0;
         bool big_any = false;
-        const double span0 = dda.t_cur;
         // voxels already listed in this iteration, as a 27-neighbourhood mask around the
         // previous cell: a voxel is tested once per iteration however many windows see it
         u32 listed = 0;
         int px = 0, py = 0, pz = 0;
-        while (kw < wn && csum < budget) {
-            int wx, wy, wz;
-            double t0, t1;
-            if (!dda.next(wx, wy, wz, t0, t1)) break;
-            if (listed) {
-                const int dx = wx - px, dy = wy - py, dz = wz - pz;
-                listed = (dx < -1 || dx > 1 || dy < -1 || dy > 1 || dz < -1 || dz > 1) ? 0u
-                                                                                     : lvx_shift_mask27(listed, dx, dy, dz);
-            }
-            px = wx;
-            py = wy;
-            pz = wz;
-            u32 nm, n;
-            if (neighbor) {
-                const i64 pc = ((i64)(wz + 1) * (ry + 2) + (wy + 1)) * (rx + 2) + (wx + 1);
-                nm = __ldg(A.nmask + pc);
-                n = nm ? (u32)__ldg(A.nsum + pc) : 0u;
-            } else {
-                n = __ldg(A.counts + (wx + (i64)rx * (wy + (i64)ry * wz)));
-                nm = n ? (1u << 13) : 0u;
-            }
-            if (nm == 0) continue;  // the reference's cheap skip (:793-799)
-            tests += (unsigned long long)n * tmul;  // :833,855 summed over the window's gather
-            const double p0x = ox + t0 * ddx, p0y = oy + t0 * ddy, p0z = oz + t0 * ddz;
-            if (neighbor) {
-                // neighbour voxels that can own a hit of this window: within tube_r of the
-                // bounding box of the ray piece inside the window's voxel
-                const double p1x = ox + t1 * ddx, p1y = oy + t1 * ddy, p1z = oz + t1 * ddz;
-                u32 bx_ = 0x2492492u, by_ = 0x0E07038u, bz_ = 0x003FE00u;
-                if (fmin(p0x, p1x) - cull < (double)wx) bx_ |= 0x1249249u;
-                if (fmax(p0x, p1x) + cull > (double)(wx + 1)) bx_ |= 0x4924924u;
-                if (fmin(p0y, p1y) - cull < (double)wy) by_ |= 0x01C0E07u;
-                if (fmax(p0y, p1y) + cull > (double)(wy + 1)) by_ |= 0x70381C0u;
-                if (fmin(p0z, p1z) - cull < (double)wz) bz_ |= 0x00001FFu;
-                if (fmax(p0z, p1z) + cull > (double)(wz + 1)) bz_ |= 0x7FC0000u;
-                nm &= bx_ & by_ & bz_;
-            }
-            csum += n;
-            if (nm == 0) continue;
-            const bool big = n * tmul > (u32)LVX_MAX_WINDOW_HITS;
-            big_any |= big;
-            WfWindow w;
-            w.t1 = t1;
-            w.tests = tests | (big ? kBigBit : 0ull);
-            A.win[i * wn + kw] = w;
-            if (big) A.win_over[i * wn + kw] = 0;
-            kw += 1;
-            const u32 fresh = nm & ~listed;
-            listed |= nm;
-            if (fresh == 0) continue;
-            if (neighbor) {
-                const u32 pos = atomicAdd(&S.n[warp], 1u);
-                if (pos < (u32)kWalkStage) {
-                    WalkRec wr;
-                    wr.place = i;
-                    wr.fresh = fresh;
-                    wr.cell = (unsigned long long)(u32)(wx + 1) | ((unsigned long long)(u32)(wy + 1) << 20) |
-                              ((unsigned long long)(u32)(wz + 1) << 40);
-                    wr.qx = (float)(p0x - (double)wx);
-                    wr.qy = (float)(p0y - (double)wy);
-                    wr.qz = (float)(p0z - (double)wz);
-                    wr.pad = 0.0f;
-                    S.rec[warp][pos] = wr;
-                    continue;
+        // The rays of the warp advance in lock step, one DDA window per round: the loads of a
+        // round are issued together, and between rounds the warp is converged, so the stage of
+        // fresh windows is flushed (one global atomic, coalesced stores) BEFORE it can overflow
+        // -- no allocation round trip ever sits inside a ray's walk.
+        bool go = mine;
+        for (;;) {
+            go = go && kw < wn && csum < budget;
+            if (!__any_sync(FULL, go)) break;
+            if (go) {
+                int wx, wy, wz;
+                double t0, t1;
+                if (!dda.next(wx, wy, wz, t0, t1)) {
+                    go = false;
+                } else {
+                    if (listed) {
+                        const int dx = wx - px, dy = wy - py, dz = wz - pz;
+                        listed = (dx < -1 || dx > 1 || dy < -1 || dy > 1 || dz < -1 || dz > 1)
+                                     ? 0u
+                                     : lvx_shift_mask27(listed, dx, dy, dz);
+                    }
+                    px = wx;
+                    py = wy;
+                    pz = wz;
+                    u32 nm, n;
+                    if (neighbor) {
+                        // one 8-byte cell: occupancy bits of the 27-neighbourhood | its segment count << 32
+                        const i64 pc = ((i64)(wz + 1) * (ry + 2) + (wy + 1)) * (rx + 2) + (wx + 1);
+                        const unsigned long long cell = __ldg(A.ncell + pc);
+                        nm = (u32)cell;
+                        n = (u32)(cell >> 32);
+                    } else {
+                        n = __ldg(A.counts + (wx + (i64)rx * (wy + (i64)ry * wz)));
+                        nm = n ? (1u << 13) : 0u;
+                    }
+                    if (nm != 0) {  // (else: the reference's cheap skip, :793-799)
+                        tests += (unsigned long long)n * tmul;  // :833,855 summed over the window's gather
+                        const double p0x = ox + t0 * ddx, p0y = oy + t0 * ddy, p0z = oz + t0 * ddz;
+                        if (neighbor) {
+                            // neighbour voxels that can own a hit of this window: within tube_r of the
+                            // bounding box of the ray piece inside the window's voxel
+                            const double p1x = ox + t1 * ddx, p1y = oy + t1 * ddy, p1z = oz + t1 * ddz;
+                            u32 bx_ = 0x2492492u, by_ = 0x0E07038u, bz_ = 0x003FE00u;
+                            if (fmin(p0x, p1x) - cull < (double)wx) bx_ |= 0x1249249u;
+                            if (fmax(p0x, p1x) + cull > (double)(wx + 1)) bx_ |= 0x4924924u;
+                            if (fmin(p0y, p1y) - cull < (double)wy) by_ |= 0x01C0E07u;
+                            if (fmax(p0y, p1y) + cull > (double)(wy + 1)) by_ |= 0x70381C0u;
+                            if (fmin(p0z, p1z) - cull < (double)wz) bz_ |= 0x00001FFu;
+                            if (fmax(p0z, p1z) + cull > (double)(wz + 1)) bz_ |= 0x7FC0000u;
+                            nm &= bx_ & by_ & bz_;
+                        }
+                        csum += n;
+                        if (nm != 0) {
+                            const bool big = n * tmul > (u32)LVX_MAX_WINDOW_HITS;
+                            big_any |= big;
+                            WfWindow w;
+                            w.t1 = t1;
+                            w.tests = tests | (big ? kBigBit : 0ull);
+                            A.win[i * wn + kw] = w;
+                            if (big) A.win_over[i * wn + kw] = 0;
+                            kw += 1;
+                            const u32 fresh = nm & ~listed;
+                            listed |= nm;
+                            if (fresh != 0 && neighbor) {
+                                const u32 pos = atomicAdd(&S.n[warp], 1u);  // (< kWalkStage: flushed below)
+                                WalkRec wr;
+                                wr.place = i;
+                                wr.fresh = fresh;
+                                wr.cell = (unsigned long long)(u32)(wx + 1) | ((unsigned long long)(u32)(wy + 1) << 20) |
+                                          ((unsigned long long)(u32)(wz + 1) << 40);
+                                wr.qx = (float)(p0x - (double)wx);
+                                wr.qy = (float)(p0y - (double)wy);
+                                wr.qz = (float)(p0z - (double)wz);
+                                wr.pad = 0.0f;
+                                S.rec[warp][pos] = wr;
+                            } else if (fresh != 0) {
+                                // own-voxel mode: one item, reserved in the global queue directly
+                                const u32 ib = queue_alloc_n(A.ctl->item_cnt, q, A.capq_item, 1u, &A.ctl->err, 1u);
+                                if (ib != kNil) {
+                                    A.item_place[ib] = i;
+                                    A.item_lin[ib] = (u32)(wx + rx * (wy + ry * wz));
+                                    // voxel-local float32 frame for the pre-reject
+                                    A.item_q[ib] = make_float4((float)(p0x - (double)wx), (float)(p0y - (double)wy),
+                                                               (float)(p0z - (double)wz), 0.0f);
+                                    // only the window of the voxel itself gathers it (:797-799)
+                                    A.item_t[ib] = make_double2(t0, t1);
+                                }
+                            }
+                        }
+                    }
                 }
             }
-            // (own-voxel mode, or the stage is full: reserve in the global queue directly)
-            const u32 ni = (u32)__popc(fresh);
-            const u32 ib = queue_alloc_n(A.ctl->item_cnt, q, A.capq_item, ni, &A.ctl->err, 1u);
-            if (ib != kNil) {
-                u32 j = ib;
-                for (u32 mm = fresh; mm; mm &= mm - 1, ++j) {
-                    const int b = __ffs((int)mm) - 1;
-                    const int bz_ = b / 9, by_ = (b - 9 * bz_) / 3, bx_ = b - 9 * bz_ - 3 * by_;
-                    const int hx = wx + bx_ - 1, hy = wy + by_ - 1, hz = wz + bz_ - 1;
-                    A.item_place[j] = i;
-                    A.item_lin[j] = (u32)(hx + rx * (hy + ry * hz));
-                    // voxel-local float32 frame for the pre-reject
-                    A.item_q[j] = make_float4((float)(p0x - (double)hx), (float)(p0y - (double)hy),
-                                              (float)(p0z - (double)hz), 0.0f);
-                    // own-voxel mode: only the window of the voxel itself gathers it (:797-799)
-                    if (!neighbor) A.item_t[j] = make_double2(t0, t1);
-                }
-            }
+            __syncwarp();
+            // every round adds at most one record per lane
+            if (S.n[warp] + 32u > (u32)kWalkStage) walk_flush(A, S, warp, lane, q);
         }
-        dda_store(rw, dda);
-        rw.tests = tests;
-        rw.nwin = kw;
-        rw.flags = (dda.alive ? 1u : 0u) | (big_any ? 2u : 0u);
-        A.rw[slot] = rw;
-        A.fdir[i] = (float)ddx;
-        A.fdir[R + i] = (float)ddy;
-        A.fdir[2 * R + i] = (float)ddz;
-        A.span[i] = span0;
-        A.span[R + i] = dda.t_cur;
-        WfRayDir rd;
-        rd.dx = ddx;
-        rd.dy = ddy;
-        rd.dz = ddz;
-        rd.t_lo = span0;
-        A.rdir[i] = rd;
+        if (mine) {
+            dda_store(rw, dda);
+            rw.tests = tests;
+            rw.nwin = kw;
+            rw.flags = (dda.alive ? 1u : 0u) | (big_any ? 2u : 0u);
+            A.rw[slot] = rw;
+            A.fdir[i] = make_float4((float)ddx, (float)ddy, (float)ddz, 0.0f);
+            A.span[i] = span0;
+            A.span[R + i] = dda.t_cur;
+            WfRayDir rd;
+            rd.dx = ddx;
+            rd.dy = ddy;
+            rd.dz = ddz;
+            rd.t_lo = span0;
+            A.rdir[i] = rd;
         }
         walk_flush(A, S, warp, lane, q);
     }
@@ -650,7 +698,8 @@ __device__ __forceinline__ bool wf_near_line(float cx, float cy, float cz, float
 // ---------------------------------------------------------------------------------------
 // what the pre-reject needs of one item
 struct CandItem {
-    u32 it, cnt, base, place;
+    u32 it, cnt, base, place, lin;
+    u32 aux0, aux_step;  // WfEntry::aux of segment seg = aux0 + (seg - base) * aux_step
     float q0x, q0y, q0z, fdx, fdy, fdz, fhx, fhy, fhz;
 };
 
@@ -658,7 +707,7 @@ struct CandItem {
 // memory atomic per converged subset) and flushed to the global queues at warp-converged
 // points with one global atomic and coalesced stores: the round trip of a global atomic is
 // off the inner loop.  Entries that do not fit the stage go to the global queue directly.
-constexpr int kStageTube = 128, kStageSph = 256;
+constexpr int kStageTube = 96, kStageSph = 192;
 struct CandStage {
     WfEntry tube[kThreadsWf / 32][kStageTube];
     WfEntry sph[kThreadsWf / 32][kStageSph];
@@ -731,7 +780,7 @@ __device__ __forceinline__ void cand_segment(const WfArgs &A, CandStage &S, int 
     s0 = __shfl_sync(act, s0, leader);
     if (mk & 1u) {
         const u32 pos = t0 + (u32)__popc(bt & lt);
-        const WfEntry c = {seg, I.it, I.place};
+        const WfEntry c = {seg, I.place, I.lin, I.aux0 + (seg - I.base) * I.aux_step};
         if (pos < (u32)kStageTube) {
             S.tube[warp][pos] = c;
         } else {
@@ -741,7 +790,7 @@ __device__ __forceinline__ void cand_segment(const WfArgs &A, CandStage &S, int 
     }
     if (mk & 6u) {
         u32 pos = s0 + (u32)(__popc(ba & lt) + __popc(bb & lt));
-        WfEntry c = {seg, I.it, I.place};
+        WfEntry c = {seg, I.place, I.lin, I.aux0 + (seg - I.base) * I.aux_step};
         if (mk & 2u) {
             if (pos < (u32)kStageSph) {
                 S.sph[warp][pos] = c;
@@ -772,8 +821,8 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_CAND_MINB) wf_cand_kernel(c
     queue_view_load(V, A.ctl->item_cnt, A.capq_item, A.ctl->err);
     const u32 total = V.pre[kNQ];
     const bool joints = A.p.joints != 0;
+    const bool nbr = A.p.neighbor != 0;
     const float reach_pt = (float)A.p.tube_r + kRejectMarginWf;
-    const size_t R = A.R;
     const u32 stride = gridDim.x * blockDim.x;
     const u32 plane = (u32)A.rx * (u32)A.ry;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -805,11 +854,16 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_CAND_MINB) wf_cand_kernel(c
         }
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-            I[k].fdx = A.fdir[place[k]];
-            I[k].fdy = A.fdir[R + place[k]];
-            I[k].fdz = A.fdir[2 * R + place[k]];
+            const float4 fd = A.fdir[place[k]];
+            I[k].fdx = fd.x;
+            I[k].fdy = fd.y;
+            I[k].fdz = fd.z;
             I[k].cnt = have[k] ? __ldg(A.counts + lin[k]) : 0u;
             I[k].base = __ldg(A.offsets + lin[k]);
+            I[k].lin = lin[k];
+            // neighbour mode: the segment's index in its voxel; own-voxel mode: the item
+            I[k].aux0 = nbr ? 0u : I[k].it;
+            I[k].aux_step = nbr ? 1u : 0u;
         }
         float4 ra[2], rb[2];
 #pragma unroll
@@ -892,15 +946,15 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_EXACT_MINB) wf_exact_kernel
         if (neighbor) {
             if (!(rd.t_lo <= h.t_in && h.t_in < A.span[R + place])) continue;
         } else {
-            const double2 tr = A.item_t[c.item];
+            const double2 tr = A.item_t[c.aux];
             if (!(tr.x <= h.t_in && h.t_in < tr.y)) continue;
         }
         const u32 rmeta = __float_as_uint(ra.w);
         const u32 attr = rmeta & 0xFFu, lid = (rmeta >> 8) & 31u;
         double scale, alpha;
         lvx_shade_hit<GEOM>(A, ox, oy, oz, rdx, rdy, rdz, h, attr, scale, alpha);
-        const u32 lin = A.item_lin[c.item];
-        const u32 rank = seg - __ldg(A.offsets + lin);  // index in the voxel's list
+        const u32 lin = c.lin;
+        const u32 rank = neighbor ? c.aux : seg - __ldg(A.offsets + lin);  // index in the voxel's list
         WfHit rec;
         rec.t_in = h.t_in;
         rec.key2 = ((unsigned long long)lin << 24) | ((unsigned long long)lid << 19) | (kind3 ? 1ull << 18 : 0ull) |
@@ -1089,6 +1143,7 @@ __device__ void wf_apply_window_cap(const WfArgs &A, const WfRayHits &H, const W
 
 __device__ __forceinline__ bool wf_composite_one(const WfArgs &A, WfTables &T, WfPixel &S, const WfHit &h,
                                                  double tau) {
+    WF_STAT(1, 1);
     wf_accumulate(A, T, S, h.scale, h.alpha, hit_lin(h.key2), hit_lid(h.key2), hit_attr(h.key2),
                   hit_kind3(h.key2) != 0, h.cx, h.cy, h.cz);
     return S.acc[3] >= tau;
@@ -1137,6 +1192,8 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_ker
         const WfWindow *wins = A.win + w0;
         WfRayHits H = {A, i, nhit < (u32)kHitSlots ? nhit : (u32)kHitSlots, kNil};
         if (nhit) {
+            WF_STAT(0, nhit);
+            WF_STAT(3, 1);
             // the hit records sit in kHitSlots different planes: fetch them all at once, the
             // ordering loop below then reads them from cache one after the other
 #pragma unroll
@@ -1295,6 +1352,9 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_ker
             if (terminated) {
                 tests = wins[term_k].tests & ~kBigBit;
                 finished = true;
+                WF_STAT(4, 1);
+                WF_STAT(5, S.n_seen);
+                WF_STAT(6, S.n_sph);
             }
             if (!finished) A.rp[slot] = rp;
         } else if (finished) {
@@ -1374,6 +1434,9 @@ __global__ void wf_begin_kernel(const WfArgs A) {
         A.ctl->n_live[1] = 0;
         A.ctl->pool_cnt = 0;
         A.ctl->err = 0;
+#ifdef LVX_WF_STATS
+        for (int k = 0; k < 8; ++k) A.ctl->dbg[k] = 0;
+#endif
         // (the window records of iteration 0 must fit whatever LVX_WF_WN asks for)
         const u32 fit = A.R ? (u32)(A.cap_win / A.R) : A.cap_win;
         A.ctl->wn = (u32)A.wn_sched < fit ? (u32)A.wn_sched : (fit ? fit : 1u);
@@ -1425,7 +1488,7 @@ WfLayout wf_layout(i64 R, double scale) {
     L.item_lin = take(c, (size_t)L.capq_item * kNQ * 4);
     L.item_q = take(c, (size_t)L.capq_item * kNQ * 16);
     L.item_t = take(c, (size_t)L.capq_item * kNQ * 16);
-    L.fdir = take(c, r * 12);
+    L.fdir = take(c, r * 16);
     L.span = take(c, r * 16);
     L.rdir = take(c, r * sizeof(WfRayDir));
     L.tube = take(c, (size_t)L.capq_surv * kNQ * sizeof(WfEntry));
@@ -1450,6 +1513,45 @@ int wf_check_tiling(const lvx_tiling *t) {
                     t->tile_step >= 1 && t->tile_first >= 0 && t->tile_first < t->tile_step,
                 "tiling: tile_w %% 8 == 0, tile_h %% 4 == 0, 0 <= tile_first < tile_step required");
     return LVX_OK;
+}
+
+// Schedule constants of the engine.  The environment is consulted once per process (developer
+// sweeps), never per frame.
+struct WfTuning {
+    int wn_sched = kWinFirst;
+    int cand_budget = 192;
+    int grow_from = 24;  // (growing earlier does not pay: the late iterations are cheap, over-scanning is not)
+    int grow_bits = 1;
+    int tail_rays = 0, tail_bits = 4, tail_mode = 1, tail_from = 6;
+    int wn_shift_max = 4;
+    int rays_mult = 8;
+    bool debug = false;
+};
+
+int env_int(const char *name, int dflt, bool positive_only = false) {
+    const char *e = getenv(name);
+    if (!e) return dflt;
+    const int v = atoi(e);
+    return positive_only && v <= 0 ? dflt : v;
+}
+
+const WfTuning &wf_tuning() {
+    static const WfTuning T = [] {
+        WfTuning t;
+        t.tail_mode = env_int("LVX_WF_TAIL_MODE", t.tail_mode);
+        t.tail_from = env_int("LVX_WF_TAIL_FROM", t.tail_from);
+        t.tail_rays = env_int("LVX_WF_TAIL_RAYS", t.tail_rays);
+        t.tail_bits = env_int("LVX_WF_TAIL_BITS", t.tail_bits);
+        t.grow_bits = env_int("LVX_WF_GROW_BITS", t.grow_bits);
+        t.wn_shift_max = env_int("LVX_WF_WN_SHIFT", t.wn_shift_max);
+        t.cand_budget = env_int("LVX_WF_BUDGET", t.cand_budget, true);
+        t.grow_from = env_int("LVX_WF_GROW", t.grow_from);
+        t.wn_sched = env_int("LVX_WF_WN", t.wn_sched, true);
+        t.rays_mult = env_int("LVX_WF_GRID_RAYS", t.rays_mult, true);
+        t.debug = getenv("LVX_WF_DEBUG") != nullptr;
+        return t;
+    }();
+    return T;
 }
 
 }  // namespace
@@ -1481,8 +1583,8 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
                 "bad model");
     LVX_REQUIRE(model->rx < 65535 && model->ry < 65535 && (i64)model->rx * model->ry * model->rz < ((i64)1 << 31),
                 "grid too large to render");
-    LVX_REQUIRE(!params->neighbor || (model->nsum_d && model->nmask_d),
-                "neighbour mode needs the neighbour grids (lvx_neighbor_sums)");
+    LVX_REQUIRE(!params->neighbor || (model->nsum_d && model->nmask_d && model->ncell_d),
+                "neighbour mode needs the neighbour grids (lvx_neighbor_sums, with the merged cells)");
     LVX_REQUIRE(params->opacity_mode >= 0 && params->opacity_mode <= 2, "bad opacity mode");
     LVX_REQUIRE(params->shadow_mode >= LVX_SHADOW_NONE && params->shadow_mode <= LVX_SHADOW_CONE, "bad shadow_mode %d",
                 params->shadow_mode);
@@ -1522,6 +1624,7 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     A.table = model->table_d;
     A.nsum = model->nsum_d;
     A.nmask = model->nmask_d;
+    A.ncell = reinterpret_cast<const unsigned long long *>(model->ncell_d);
     if (lod) {
         A.oc.flat = lod->oct_flat_d;
         A.oc.n_levels = lod->n_levels;
@@ -1565,7 +1668,7 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     A.item_lin = (u32 *)(base + L.item_lin);
     A.item_q = (float4 *)(base + L.item_q);
     A.item_t = (double2 *)(base + L.item_t);
-    A.fdir = (float *)(base + L.fdir);
+    A.fdir = (float4 *)(base + L.fdir);
     A.span = (double *)(base + L.span);
     A.rdir = (WfRayDir *)(base + L.rdir);
     A.capq_item = L.capq_item;
@@ -1576,32 +1679,24 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     A.capq_hit = L.capq_hit;
     A.hit_slot = (WfHit *)(base + L.hit_slot);
     A.hcnt = (u32 *)(base + L.hcnt);
-    A.wn_sched = kWinFirst;
-    A.cand_budget = 192;
-    A.grow_from = 24;  // (growing earlier does not pay: the late iterations are cheap, over-scanning is not)
-    A.grow_bits = 1;
-    A.tail_rays = 0;
-    A.tail_bits = 4;
-    A.tail_mode = 1;
-    if (const char *e = getenv("LVX_WF_TAIL_MODE")) A.tail_mode = atoi(e);
-    A.tail_from = 6;
-    if (const char *e = getenv("LVX_WF_TAIL_FROM")) A.tail_from = atoi(e);
-    if (const char *e = getenv("LVX_WF_TAIL_RAYS")) A.tail_rays = atoi(e);
-    if (const char *e = getenv("LVX_WF_TAIL_BITS")) A.tail_bits = atoi(e);
-    A.wn_shift_max = 4;
-    if (const char *e = getenv("LVX_WF_GROW_BITS")) A.grow_bits = atoi(e);
-    if (const char *e = getenv("LVX_WF_WN_SHIFT")) A.wn_shift_max = atoi(e);
-    if (const char *e = getenv("LVX_WF_BUDGET")) A.cand_budget = atoi(e) > 0 ? atoi(e) : A.cand_budget;
-    if (const char *e = getenv("LVX_WF_GROW")) A.grow_from = atoi(e);
-    if (const char *e = getenv("LVX_WF_WN")) A.wn_sched = atoi(e) > 0 ? atoi(e) : A.wn_sched;
+    // schedule constants; the LVX_WF_* developer overrides are read ONCE per process
+    const WfTuning &tune = wf_tuning();
+    A.wn_sched = tune.wn_sched;
+    A.cand_budget = tune.cand_budget;
+    A.grow_from = tune.grow_from;
+    A.grow_bits = tune.grow_bits;
+    A.tail_rays = tune.tail_rays;
+    A.tail_bits = tune.tail_bits;
+    A.tail_mode = tune.tail_mode;
+    A.tail_from = tune.tail_from;
+    A.wn_shift_max = tune.wn_shift_max;
 
-    const bool debug = getenv("LVX_WF_DEBUG") != nullptr;
+    const bool debug = tune.debug;
     const bool geom = params->shadow_mode == LVX_SHADOW_HARD || params->shadow_mode == LVX_SHADOW_REPLINES ||
                       params->ao_mode == LVX_AO_HEMISPHERE;
     cudaStream_t st = (cudaStream_t)stream;
     const int sms = lvx_sm_count();
-    int rays_mult = 8;
-    if (const char *e = getenv("LVX_WF_GRID_RAYS")) rays_mult = atoi(e) > 0 ? atoi(e) : rays_mult;
+    const int rays_mult = tune.rays_mult;
     const unsigned grid_rays = (unsigned)(sms * rays_mult), grid_q = (unsigned)(sms * 8);
     A.ray_threads = grid_rays * (unsigned)kThreadsWf;
     wf_begin_kernel<<<1, 64, 0, st>>>(A);
@@ -1648,6 +1743,10 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
                 fprintf(stderr, "wf it %2d: live %8u -> %8u  wn %4u budget %6u  items %10llu  candidates %10llu  tubes %9llu  "
                         "spheres %9llu  listed hits %8llu\n",
                         it, c.n_live[par], c.n_live[par ^ 1], c.wn, c.budget, ni, nc, nt, ns, nh);
+#ifdef LVX_WF_STATS
+                fprintf(stderr, "      cumulative: owned hits %llu  composited %llu  rays-with-hits %llu  terminated %llu  "
+                        "sum n_seen %llu  sum n_sph %llu\n", c.dbg[0], c.dbg[1], c.dbg[3], c.dbg[4], c.dbg[5], c.dbg[6]);
+#endif
             }
             wf_next_kernel<<<1, 64, 0, st>>>(A, par, it + 1);
         }

@@ -235,7 +235,7 @@ def _model_struct(model: VoxelModel) -> "_lib.Model":
     m.rx, m.ry, m.rz = model.spec.dims
     m.counts_d, m.offsets_d = counts_d.data_ptr(), offsets_d.data_ptr()
     m.seg_rec_d, m.table_d = rec_d.data_ptr(), table_d.data_ptr()
-    m.nsum_d, m.nmask_d = occ_d[0].data_ptr(), occ_d[1].data_ptr()
+    m.nsum_d, m.nmask_d, m.ncell_d = occ_d[0].data_ptr(), occ_d[1].data_ptr(), occ_d[2].data_ptr()
     m._keep = (counts_d, offsets_d, rec_d, table_d, occ_d)
     return m
 

@@ -161,6 +161,28 @@ def build_lod(model: VoxelModel) -> DensityOctree:
 
 # --- representative lines (lod.py:61-79, 122-284) ---------------------------------------------
 
+def representative_line(starts, ends, origin, size: float, n_bins: int):
+    """Average the member segments of one (coarse) voxel into a single line (lod.py:141-169):
+    members in the given order, the flip rule, the face-bin snap and the summed length, computed
+    by the same device code the level kernel runs per parent voxel.  Returns (a, b, weight) in
+    grid units, or None without segments."""
+    starts = np.asarray(starts, dtype=np.float64).reshape(-1, 3)
+    ends = np.asarray(ends, dtype=np.float64).reshape(-1, 3)
+    m = starts.shape[0]
+    if m == 0:
+        return None
+    torch = _lib.require_device()
+    s_d, e_d = _lib.to_device(starts), _lib.to_device(ends)
+    scratch = torch.empty(m, dtype=torch.float64, device="cuda")
+    out = torch.empty(7, dtype=torch.float64, device="cuda")
+    _lib.check(_lib.lib().lvx_probe_rep_line(_lib.ptr(s_d), _lib.ptr(e_d), C.c_int64(m),
+                                             _lib.f64x3(np.asarray(origin, dtype=np.float64)), C.c_double(float(size)),
+                                             C.c_int32(int(n_bins)), _lib.ptr(scratch), _lib.ptr(out),
+                                             _lib.stream_ptr()))
+    o = out.cpu().numpy()
+    return o[0:3].copy(), o[3:6].copy(), float(o[6])
+
+
 class RepLevel:
     """One representative line per voxel of a coarsened grid (lod.py:61-65): `valid` (V,) bool,
     `a`, `b` (V,3) float32 grid units, `weight` (V,) float32 summed member length.  Built on

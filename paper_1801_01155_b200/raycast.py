@@ -242,6 +242,129 @@ def intersect_ray_tube(ray, a, b, radius: float) -> Optional[HitRecord]:
     return HitRecord(t_in=float(r[1]), t_out=float(r[2]), normal=r[3:6].copy(), kind="tube")
 
 
+def probe_shade(nlv: np.ndarray, ambient, diffuse, specular, shininess) -> np.ndarray:
+    """shade_scalar (_kernels.py:316-329) for rows of (normal, light, view) on the device."""
+    torch = _lib.require_device()
+    nlv = np.ascontiguousarray(nlv, dtype=np.float64).reshape(-1, 9)
+    n = nlv.shape[0]
+    out = torch.empty(max(n, 1), dtype=torch.float64, device="cuda")
+    nlv_d = _lib.to_device(nlv)
+    _lib.check(_lib.lib().lvx_probe_shade(_lib.ptr(nlv_d), C.c_double(float(ambient)), C.c_double(float(diffuse)),
+                                          C.c_double(float(specular)), C.c_double(float(shininess)),
+                                          C.c_int64(n), _lib.ptr(out), _lib.stream_ptr()))
+    return out[:n].cpu().numpy()
+
+
+def _hit_sort_key(model_dims, hit: HitRecord):
+    rx, ry, _ = model_dims
+    vx, vy, vz = hit.voxel
+    return (hit.t_in, vx + rx * (vy + ry * vz), hit.local_line_id, 0 if hit.kind == "tube" else 1)
+
+
+def gather_voxel_hits(ray, voxel, model: VoxelModel, params: RenderParams, seen: Optional[dict] = None,
+                      t_window=None):
+    """Hits owned by `voxel`, in compositing order (raycast.py:224-283): the voxel's own segments
+    -- in neighbour mode those of its 26 neighbours too -- are tested (all-float64 tube / sphere
+    tests, batched through the device probes) and a hit is kept when its entry parameter lies
+    in the voxel's traversal window.  `seen` maps voxel linear index -> bitmask of line ids that
+    are already composited; those segments are skipped."""
+    o, d = _as_ray(ray)
+    voxel = tuple(int(v) for v in voxel)
+    dims = model.spec.dims
+    if t_window is None:
+        pad = 1 if params.neighbor_mode != "off" else 0
+        for vox, t0, t1 in traverse_voxels((o, d), model.spec, pad=pad):
+            if vox == voxel:
+                t_window = (t0, t1)
+                break
+        if t_window is None:
+            return []
+    t0, t1 = t_window
+    rx, ry, rz = dims
+    span = 1 if params.neighbor_mode != "off" else 0
+    cand = []  # (segment index, home voxel, lid, attr) in gather order
+    for nz in range(voxel[2] - span, voxel[2] + span + 1):
+        for ny in range(voxel[1] - span, voxel[1] + span + 1):
+            for nx in range(voxel[0] - span, voxel[0] + span + 1):
+                if not (0 <= nx < rx and 0 <= ny < ry and 0 <= nz < rz):
+                    continue
+                lin = nx + rx * (ny + ry * nz)
+                base = int(model.offsets[lin])
+                for sgi in range(base, base + int(model.counts[lin])):
+                    lid = int(model.seg_lid[sgi])
+                    if seen is not None and (seen.get(lin, 0) >> lid) & 1:
+                        continue
+                    cand.append((sgi, (nx, ny, nz), lid, int(model.seg_attr[sgi])))
+    if not cand:
+        return []
+    idx = np.array([c[0] for c in cand])
+    a = model.seg_a[idx].astype(np.float64)
+    b = model.seg_b[idx].astype(np.float64)
+    rays = np.broadcast_to(np.concatenate([o, d]), (len(cand), 6))
+    r = float(params.tube_radius)
+    degenerate = np.linalg.norm(b - a, axis=1) < 1e-12
+    tube = probe_tubes(rays, a, b, r, f32_axis=False)
+    sph_a = probe_spheres(rays, a, r)
+    sph_b = probe_spheres(rays, b, r) if params.joint_spheres else None
+    hits = []
+    for k, (_, home, lid, attr) in enumerate(cand):
+        # a zero-length chord is tested as the sphere about its start point (raycast.py:193-194)
+        rows = [(sph_a[k], "joint-sphere") if degenerate[k] else (tube[k], "tube")]
+        if params.joint_spheres:
+            rows += [(sph_a[k], "joint-sphere"), (sph_b[k], "joint-sphere")]
+        for row, kind in rows:
+            if row[0] == 0.0 or not t0 <= row[1] < t1:
+                continue
+            hits.append(HitRecord(t_in=float(row[1]), t_out=float(row[2]), normal=row[3:6].copy(), voxel=home,
+                                  local_line_id=lid, attr_index=attr, kind=kind))
+    hits.sort(key=lambda h: _hit_sort_key(dims, h))
+    return hits
+
+
+def shade_local(hit, light, view, ambient=0.2, diffuse=0.7, specular=0.3, shininess=32.0) -> float:
+    """Local shading scale (raycast.py:286-294); `hit` may be a HitRecord or a bare normal."""
+    n = np.asarray(getattr(hit, "normal", hit), dtype=np.float64)
+    row = np.concatenate([n, np.asarray(light, dtype=np.float64), np.asarray(view, dtype=np.float64)])
+    return float(probe_shade(row[None], ambient, diffuse, specular, shininess)[0])
+
+
+def composite(hits, params: RenderParams, transfer_table, ray_dir=(0.0, 0.0, 1.0)) -> np.ndarray:
+    """Front-to-back blend of pre-sorted hits; returns premultiplied RGBA (raycast.py:297-332).
+    Stops once the accumulated alpha reaches tau, then blends the background underneath."""
+    table = np.asarray(transfer_table, dtype=np.float32)
+    d = np.asarray(ray_dir, dtype=np.float64)
+    d = d / np.linalg.norm(d)
+    view = -d
+    if params.light_dir is None:
+        light = view
+    else:
+        light = np.asarray(params.light_dir, dtype=np.float64)
+        light = light / np.linalg.norm(light)
+    hits = list(hits)
+    scales = np.zeros(0)
+    if hits:
+        nlv = np.stack([np.concatenate([np.asarray(h.normal, dtype=np.float64), light, view]) for h in hits])
+        scales = probe_shade(nlv, params.ambient, params.diffuse, params.specular, params.shininess)
+    mode = _OPACITY_MODES[params.opacity_mode]
+    acc = np.zeros(4, dtype=np.float64)
+    for h, scale in zip(hits, scales):
+        if mode == 0:
+            alpha = params.base_opacity
+        elif mode == 1:
+            alpha = float(table[h.attr_index, 3])
+        else:
+            alpha = 1.0 - (1.0 - params.base_opacity) ** max(0.0, h.t_out - h.t_in)
+        w = (1.0 - acc[3]) * alpha
+        acc[:3] += w * float(scale) * table[h.attr_index, :3].astype(np.float64)
+        acc[3] += w
+        if acc[3] >= params.tau:
+            break
+    bg = params.background
+    acc[:3] += (1.0 - acc[3]) * bg[3] * bg[:3]
+    acc[3] += (1.0 - acc[3]) * bg[3]
+    return acc
+
+
 # --- frame ---------------------------------------------------------------------------
 
 def default_camera(dims, width: int = 640, height: int = 360) -> Camera:
@@ -265,6 +388,16 @@ def ensure_lod(model: VoxelModel, octree: Optional[DensityOctree], replines, par
     if params.ao_mode == "precomputed" and model.ao is None:
         raise ValueError("the model carries no baked AO field; run `linevox precompute-ao` first")
     return octree, replines
+
+
+def _octree_args(octree: DensityOctree):
+    """The flat host layout the reference marshals for its kernels (raycast.py:369-388):
+    (flat f32, offsets i64[L+1], dims i64[L,3] as dx,dy,dz, L)."""
+    flat = np.concatenate([np.ascontiguousarray(l, dtype=np.float32).reshape(-1) for l in octree.levels])
+    off = np.zeros(octree.n_levels + 1, dtype=np.int64)
+    off[1:] = np.cumsum([l.size for l in octree.levels])
+    dims = np.asarray([octree.dims(l) for l in range(octree.n_levels)], dtype=np.int64)
+    return flat, off, dims, octree.n_levels
 
 
 def camera_struct(camera: Camera) -> "_lib.Camera":
@@ -394,6 +527,7 @@ class FramePlan:
         m.seg_rec_d, m.table_d = rec_d.data_ptr(), table_d.data_ptr()
         m.nsum_d = occ_d[0].data_ptr() if occ_d is not None else None
         m.nmask_d = occ_d[1].data_ptr() if occ_d is not None else None
+        m.ncell_d = occ_d[2].data_ptr() if occ_d is not None else None
         self.mdl = m
         ao_d = model.ao_device() if params.ao_mode == "precomputed" else None
         dirs_d = fibonacci_dirs_device(params.ao_rays, 1) \

@@ -15,12 +15,13 @@ those attributes replaces it and drops the stale device mirror; arrays mutated
 from __future__ import annotations
 
 import ctypes as C
-from typing import Optional
+from dataclasses import dataclass
+from typing import NamedTuple, Optional
 
 import numpy as np
 
 from . import _lib
-from .scene_io import CurveSet, GridSpec
+from .scene_io import Curve, CurveSet, GridSpec
 
 _FACE_BITS, _ATTR_BITS, _LID_BITS = 3, 8, 5
 
@@ -77,6 +78,142 @@ def unpack_records(packed: np.ndarray, n_bins: int) -> dict:
         "attr": field(6 + 2 * bb, 0xFF).astype(np.uint8),
         "lid": field(14 + 2 * bb, 0x1F).astype(np.uint8),
     }
+
+
+# --- the reference's small record / clipping operations (voxelizer.py:40-169, 273-287) -----------
+#
+# Same names, arguments and error behaviour, so the reference's tests/test_voxelizer.py can be
+# pointed at this package.  The integer packer and the bin snap are scalar host operations in
+# the reference too; `clip_curve_to_voxels` runs the device clipper (lvx_probe_clip).
+
+@dataclass(frozen=True)
+class QuantizedSegment:
+    """The six fields of one packed record (voxelizer.py:40-50)."""
+
+    face_in: int
+    bin_in: int
+    face_out: int
+    bin_out: int
+    attr_index: int
+    local_line_id: int
+
+
+class ClippedSegment(NamedTuple):
+    voxel: tuple
+    entry: np.ndarray
+    exit: np.ndarray
+    attr_entry: float
+    attr_exit: float
+
+
+def _bit_offsets(n: int):
+    """LSB-first layout face_in(3) bin_in(2 lb) face_out(3) bin_out(2 lb) attr(8) lid(5)
+    (voxelizer.py:79-89): (bin bits, bin_in, face_out, bin_out, attr, lid offsets)."""
+    bb = 2 * (n.bit_length() - 1)
+    return bb, _FACE_BITS, _FACE_BITS + bb, 2 * _FACE_BITS + bb, 2 * _FACE_BITS + 2 * bb, \
+        2 * _FACE_BITS + 2 * bb + _ATTR_BITS
+
+
+def pack_segment(seg: QuantizedSegment, n_bins: int) -> bytes:
+    """One record as `record_width(n_bins)` little-endian bytes (voxelizer.py:92-113)."""
+    n = _check_bins(n_bins)
+    if not (0 <= seg.face_in < 6 and 0 <= seg.face_out < 6):
+        raise ValueError(f"face IDs must be in [0,6), got {seg.face_in}/{seg.face_out}")
+    if not (0 <= seg.bin_in < n * n and 0 <= seg.bin_out < n * n):
+        raise ValueError(f"bin codes must be in [0,{n * n}), got {seg.bin_in}/{seg.bin_out}")
+    if not 0 <= seg.attr_index < 256:
+        raise ValueError(f"attr_index out of byte range: {seg.attr_index}")
+    if not 0 <= seg.local_line_id < 32:
+        raise ValueError(f"local_line_id needs 5 bits: {seg.local_line_id}")
+    _, o_bi, o_fo, o_bo, o_at, o_lid = _bit_offsets(n)
+    word = (int(seg.face_in) | (int(seg.bin_in) << o_bi) | (int(seg.face_out) << o_fo) | (int(seg.bin_out) << o_bo)
+            | (int(seg.attr_index) << o_at) | (int(seg.local_line_id) << o_lid))
+    return word.to_bytes(record_width(n), "little")
+
+
+def unpack_segment(data: bytes, n_bins: int) -> QuantizedSegment:
+    """Inverse of pack_segment (voxelizer.py:116-130)."""
+    n = _check_bins(n_bins)
+    w = record_width(n)
+    if len(data) != w:
+        raise ValueError(f"expected a {w}-byte record for N={n}, got {len(data)} bytes")
+    f = unpack_records(np.frombuffer(bytes(data), dtype=np.uint8), n)
+    return QuantizedSegment(face_in=int(f["face_in"][0]), bin_in=int(f["bin_in"][0]), face_out=int(f["face_out"][0]),
+                            bin_out=int(f["bin_out"][0]), attr_index=int(f["attr"][0]), local_line_id=int(f["lid"][0]))
+
+
+_ON_FACE_TOL = 1e-6  # voxelizer.py:36
+
+
+def quantize_point_on_face(p, face: int, n_bins: int, voxel=None):
+    """Snap a face point to the centre of its N x N bin (voxelizer.py:133-169): `p` is either the
+    two in-face coordinates or a 3-D grid point with its voxel.  Returns (bin code, snapped point)."""
+    n = _check_bins(n_bins)
+    if not 0 <= face < 6:
+        raise ValueError(f"face ID must be in [0,6), got {face}")
+    axis, side = face >> 1, float(face & 1)
+    ua, va = (1 if axis == 0 else 0), (1 if axis == 2 else 2)  # in-face axes, ascending
+    p = np.asarray(p, dtype=np.float64)
+    if p.shape == (2,):
+        u, v = p
+    elif p.shape == (3,):
+        if voxel is None:
+            raise ValueError("a 3D point needs its voxel")
+        local = p - np.asarray(voxel, dtype=np.float64)
+        if abs(local[axis] - side) > _ON_FACE_TOL:
+            raise ValueError(f"point {p.tolist()} is {abs(local[axis] - side):.2e} off face {face}")
+        if np.any(local < -_ON_FACE_TOL) or np.any(local > 1 + _ON_FACE_TOL):
+            raise ValueError(f"point {p.tolist()} lies outside voxel {voxel}")
+        u, v = local[ua], local[va]
+    else:
+        raise ValueError(f"expected a 2D in-face or 3D grid point, got shape {p.shape}")
+    bu = min(max(int(np.floor(u * n)), 0), n - 1)
+    bv = min(max(int(np.floor(v * n)), 0), n - 1)
+    cu, cv = (bu + 0.5) / n, (bv + 0.5) / n
+    if p.shape == (2,):
+        return bu + n * bv, np.array([cu, cv])
+    q = np.empty(3)
+    q[axis], q[ua], q[va] = side, cu, cv
+    return bu + n * bv, q + np.asarray(voxel, dtype=np.float64)
+
+
+def clip_batch_device(pts, attrs, off, dims):
+    """_clip_batch (voxelizer.py:213-263) on the device: (vox i64[n,3], p_in, p_out f64[n,3], a_in,
+    a_out f64[n], key u64[n]) in the reference's chord order."""
+    torch = _lib.require_device()
+    L, st = _lib.lib(), _lib.stream_ptr()
+    pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+    P = pts.shape[0]
+    pts_d, attrs_d = _lib.to_device(pts), _lib.to_device(np.ascontiguousarray(attrs, dtype=np.float64))
+    off = np.ascontiguousarray(off, dtype=np.int64)
+    first = torch.empty(max(P, 1), dtype=torch.uint8, device="cuda")
+    _lib.check(L.lvx_mark_curve_starts(_lib.ptr(_lib.to_device(off)), C.c_int64(off.size - 1), C.c_int64(P),
+                                       _lib.ptr(first), st))
+    bound = torch.zeros(1, dtype=torch.int64, device="cuda")
+    _lib.check(L.lvx_voxelize_bound(_lib.ptr(pts_d), _lib.ptr(first), C.c_int64(P), _lib.ptr(bound), st))
+    cap = max(int(bound.item()), 1)
+    vox = torch.empty((cap, 3), dtype=torch.int64, device="cuda")
+    p_in = torch.empty((cap, 3), dtype=torch.float64, device="cuda")
+    p_out = torch.empty((cap, 3), dtype=torch.float64, device="cuda")
+    att = torch.empty((cap, 2), dtype=torch.float64, device="cuda")
+    key = torch.empty(cap, dtype=torch.int64, device="cuda")
+    n_d = torch.zeros(1, dtype=torch.int64, device="cuda")
+    _lib.check(L.lvx_probe_clip(_lib.ptr(pts_d), _lib.ptr(attrs_d), _lib.ptr(first), C.c_int64(P),
+                                _lib.i32x3(dims), C.c_uint64(cap), _lib.ptr(vox), _lib.ptr(p_in), _lib.ptr(p_out),
+                                _lib.ptr(att), _lib.ptr(key), _lib.ptr(n_d), st))
+    n = int(n_d.item())
+    order = torch.argsort(key[:n])
+    g = lambda t: t[:n][order].cpu().numpy()
+    a = g(att)
+    return g(vox), g(p_in), g(p_out), a[:, 0].copy(), a[:, 1].copy(), g(key).view(np.uint64)
+
+
+def clip_curve_to_voxels(curve: Curve, spec: GridSpec) -> list:
+    """Split one curve into per-voxel chords between face crossings (voxelizer.py:273-287)."""
+    n = len(curve)
+    vox, p_in, p_out, a_in, a_out, _ = clip_batch_device(curve.points, curve.attrs, np.array([0, n], np.int64), spec.dims)
+    return [ClippedSegment(tuple(int(x) for x in vox[i]), p_in[i], p_out[i], float(a_in[i]), float(a_out[i]))
+            for i in range(vox.shape[0])]
 
 
 def default_transfer_table() -> np.ndarray:
@@ -301,7 +438,7 @@ class VoxelModel:
 
     # -- device-side render inputs --------------------------------------------------
     def device_view(self, need_occ: bool = True):
-        """(counts_d, offsets_d, seg_rec_d, table_d, (nsum_d, nmask_d)) -- the lvx_model
+        """(counts_d, offsets_d, seg_rec_d, table_d, (nsum_d, nmask_d, ncell_d)) -- the lvx_model
         fields.  The neighbour grids (27-neighbourhood segment counts / occupancy bits
         over the padded grid; nsum > 0 is the reference's dilated occupancy map) are
         only needed in neighbour mode."""
@@ -329,9 +466,10 @@ class VoxelModel:
             cells = (rx + 2) * (ry + 2) * (rz + 2)
             nsum = torch.empty(cells, dtype=torch.int16, device="cuda")
             nmask = torch.empty(cells, dtype=torch.int32, device="cuda")
+            ncell = torch.empty(cells, dtype=torch.int64, device="cuda")
             _lib.check(L.lvx_neighbor_sums(_lib.ptr(self.dev("counts")), _lib.i32x3(self.spec.dims),
-                                           _lib.ptr(nsum), _lib.ptr(nmask), st))
-            d["occ"] = (nsum, nmask)
+                                           _lib.ptr(nsum), _lib.ptr(nmask), _lib.ptr(ncell), st))
+            d["occ"] = (nsum, nmask, ncell)
         return (self.dev("counts"), self.dev("offsets"), d["seg_rec"], d["table"], d.get("occ"))
 
     def occupancy_dilated(self) -> np.ndarray:

@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol():
     L = ctypes.CDLL(_lib.LIB_PATH)
     for name in declared:
         assert hasattr(L, name), name
-    assert _lib.lib().lvx_abi_version() == 1
+    assert _lib.lib().lvx_abi_version() == 2
 
 
 def test_host_only_entry_points(lv):

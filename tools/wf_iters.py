@@ -1,5 +1,6 @@
 """Per-iteration counters of one wavefront frame (developer tool): LVX_WF_DEBUG=1 output."""
 import os, sys
+os.environ["LVX_WF_DEBUG"] = "1"  # (read once per process by the library)
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch
@@ -16,7 +17,6 @@ img = torch.empty((1080, 1920, 4), dtype=torch.float32, device="cuda")
 st = torch.zeros((1080, 3), dtype=torch.int64, device="cuda")
 plan.launch(img, st)
 torch.cuda.synchronize()
-os.environ["LVX_WF_DEBUG"] = "1"
 st.zero_()
 plan.launch(img, st)
 torch.cuda.synchronize()
