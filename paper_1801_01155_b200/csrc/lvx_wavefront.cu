@@ -67,24 +67,27 @@ struct __align__(16) WfWindow {
 static_assert(sizeof(WfWindow) == 16, "window record is 16 bytes");
 constexpr unsigned long long kBigBit = 1ull << 63;
 
-struct __align__(16) WfHit {
+// One hit = ONE 32-byte sector, written whole (no read-modify-write of a partly written sector on
+// its way to DRAM) and read whole.  The sphere centre of a joint hit lives in a 16-byte side record
+// that only joint hits write and only the de-duplication of joint hits reads.
+struct __align__(32) WfHit {
     double t_in;
     // the rest of the reference's order (home voxel, lid, kind, then gather order) and the
     // hit's small fields as one integer:
     //   lin << 24 | lid << 19 | (kind != tube) << 18 | index in voxel << 10 | kind3 << 8 | attr
+    // bit 63: dropped by the window cap (slow path only)
     unsigned long long key2;
     double scale, alpha;
-    float cx, cy, cz;  // sphere centre (joint hits)
-    u32 next;          // overflow list link; bit 31: dropped by the window cap
 };
-static_assert(sizeof(WfHit) == 48, "hit record is 48 bytes");
-constexpr u32 kDropped = 0x80000000u;
-__device__ __forceinline__ u32 hit_lin(unsigned long long k) { return (u32)(k >> 24); }
+static_assert(sizeof(WfHit) == 32, "hit record is one sector");
+constexpr unsigned long long kDroppedBit = 1ull << 63;
+__device__ __forceinline__ u32 hit_lin(unsigned long long k) { return (u32)(k >> 24) & 0x7FFFFFFFu; }
 __device__ __forceinline__ u32 hit_lid(unsigned long long k) { return (u32)(k >> 19) & 31u; }
 __device__ __forceinline__ u32 hit_kind3(unsigned long long k) { return (u32)(k >> 8) & 3u; }
 __device__ __forceinline__ u32 hit_attr(unsigned long long k) { return (u32)k & 0xFFu; }
 // gather order inside a window: (voxel scan order, index in voxel, primitive)
 __device__ __forceinline__ unsigned long long hit_gather(unsigned long long k) {
+    k &= ~kDroppedBit;
     return ((k >> 24) << 10) | (((k >> 10) & 255ull) << 2) | ((k >> 8) & 3ull);
 }
 
@@ -115,14 +118,14 @@ struct __align__(16) WfRayWalk {   // owned by the walk
 };
 static_assert(sizeof(WfRayWalk) == 96, "walk state is 96 bytes");
 
-struct __align__(16) WfRayPix {    // owned by the compositor
+struct __align__(32) WfRayPix {    // owned by the compositor: two sectors, read and written whole
     double acc[4];
     unsigned long long seen_bloom, sph_bloom;
     unsigned long long over;
-    u32 n_seen, n_sph;
-    u32 ovf, pix, out_off, pad;
+    u16 n_seen, n_sph;
+    u32 ovf;
 };
-static_assert(sizeof(WfRayPix) == 80, "pixel state is 80 bytes");
+static_assert(sizeof(WfRayPix) == 64, "pixel state is 64 bytes");
 
 // control block in device memory
 // windows a ray may record in the first iteration (doubling per iteration after that); also
@@ -173,11 +176,13 @@ struct WfArgs {
     WfCtl *ctl;
     WfRayWalk *rw;  // [R]
     WfRayPix *rp;   // [R]
+    uint2 *rpix;    // [R] constants of the ray: x | y << 16, offset of its pixel in the output
     u32 *head;      // [R] overflow hit list
-    u32 *tab_key, *tab_mask;   // [kInline][R]
-    float *tab_sph;            // [3][kInline][R]
-    u32 *pool_key, *pool_mask; // [pool_cap][LVX_MAX_SEEN - kInline]
-    float *pool_sph;           // [pool_cap][LVX_MAX_SEEN - kInline][3]
+    // de-duplication tables, contiguous per ray: a search walks ONE ray's sectors back to front
+    uint2 *tab_seen;           // [R][kInline] (home voxel, lid mask)
+    float4 *tab_sph;           // [R][kInline] joint-sphere centres
+    uint2 *pool_seen;          // [pool_cap][LVX_MAX_SEEN - kInline]
+    float4 *pool_sph;          // [pool_cap][LVX_MAX_SEEN - kInline]
     u32 pool_cap;
     u32 *live[2];
     WfWindow *win;
@@ -191,9 +196,12 @@ struct WfArgs {
     WfRayDir *rdir;              // [R] float64 direction + start of the walked range, by place (exact kernels)
     WfEntry *tube, *sph;
     u32 capq_surv;
-    WfHit *hit;       // overflow pool (linked lists)
+    WfHit *hit;       // overflow pool (linked lists through hit_next)
+    float4 *hit_c;    // [capq_hit * kNQ] sphere centres of the pool's joint hits
+    u32 *hit_next;    // [capq_hit * kNQ]
     u32 capq_hit;
     WfHit *hit_slot;  // [kHitSlots][R], indexed by the ray's position in the live list
+    float4 *slot_c;   // [kHitSlots][R] sphere centres of the joint hits
     u32 *hcnt;        // hits of the ray this iteration, by place
     u32 *win_over;  // [cap_win] overflow of a window (slow path only)
     int wn_sched, cand_budget, grow_from, grow_bits, wn_shift_max, tail_rays, tail_bits, tail_mode, tail_from;
@@ -422,10 +430,8 @@ __global__ void __launch_bounds__(kThreadsWf) wf_init_kernel(const WfArgs A) {
             rp.over = 0;
             rp.n_seen = rp.n_sph = 0;
             rp.ovf = kNil;
-            rp.pix = (u32)x | ((u32)y << 16);
-            rp.out_off = (u32)o;
-            rp.pad = 0;
             A.rp[slot] = rp;
+            A.rpix[slot] = make_uint2((u32)x | ((u32)y << 16), (u32)o);
             live = true;
         } else {
             write_pixel(A, (u32)o, 0.0, 0.0, 0.0, 0.0);
@@ -895,6 +901,22 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_CAND_MINB) wf_cand_kernel(c
     cand_flush(A, S, warp, lane, q);
 }
 
+// one 256-bit store / load per hit record (st/ld.global.v4.b64: whole-sector accesses)
+__device__ __forceinline__ void wf_store_hit(WfHit *p, const WfHit &h) {
+    lvx_st256(p, (u64)__double_as_longlong(h.t_in), h.key2, (u64)__double_as_longlong(h.scale),
+              (u64)__double_as_longlong(h.alpha));
+}
+__device__ __forceinline__ WfHit wf_load_hit(const WfHit *p) {
+    u64 a, b, c, d;
+    lvx_ld256(p, a, b, c, d);
+    WfHit h;
+    h.t_in = __longlong_as_double((long long)a);
+    h.key2 = b;
+    h.scale = __longlong_as_double((long long)c);
+    h.alpha = __longlong_as_double((long long)d);
+    return h;
+}
+
 // ---------------------------------------------------------------------------------------
 // exact: one thread per surviving primitive (KIND 0: tubes, 1: joint spheres)
 // ---------------------------------------------------------------------------------------
@@ -961,18 +983,16 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_EXACT_MINB) wf_exact_kernel
                    ((unsigned long long)(rank & 255u) << 10) | ((unsigned long long)kind3 << 8) | attr;
         rec.scale = scale;
         rec.alpha = alpha;
-        rec.cx = ccx;
-        rec.cy = ccy;
-        rec.cz = ccz;
-        rec.next = kNil & ~kDropped;
         const u32 j = atomicAdd(&A.hcnt[place], 1u);
         if (j < (u32)kHitSlots) {
-            A.hit_slot[(size_t)j * R + place] = rec;
+            wf_store_hit(A.hit_slot + ((size_t)j * R + place), rec);
+            if (KIND != 0) A.slot_c[(size_t)j * R + place] = make_float4(ccx, ccy, ccz, 0.0f);
         } else {
             const u32 e = queue_alloc_bits(A.ctl->hit_cnt, q, A.capq_hit, true, false, &A.ctl->err, 4u);
             if (e == kNil) continue;
-            rec.next = atomicExch(&A.head[place], e) & ~kDropped;
-            A.hit[e] = rec;
+            A.hit_next[e] = atomicExch(&A.head[place], e);
+            wf_store_hit(A.hit + e, rec);
+            if (KIND != 0) A.hit_c[e] = make_float4(ccx, ccy, ccz, 0.0f);
         }
     }
 }
@@ -991,17 +1011,13 @@ struct WfTables {
     const WfArgs &A;
     u32 slot;
     u32 ovf;
-    __device__ __forceinline__ u32 *key(u32 i) const {
-        return i < (u32)kInline ? A.tab_key + (size_t)i * A.R + slot
-                                : A.pool_key + (size_t)ovf * (LVX_MAX_SEEN - kInline) + (i - kInline);
+    __device__ __forceinline__ uint2 *seen(u32 i) const {
+        return i < (u32)kInline ? A.tab_seen + (size_t)slot * kInline + i
+                                : A.pool_seen + (size_t)ovf * (LVX_MAX_SEEN - kInline) + (i - kInline);
     }
-    __device__ __forceinline__ u32 *mask(u32 i) const {
-        return i < (u32)kInline ? A.tab_mask + (size_t)i * A.R + slot
-                                : A.pool_mask + (size_t)ovf * (LVX_MAX_SEEN - kInline) + (i - kInline);
-    }
-    __device__ __forceinline__ float *sph(u32 i, int c) const {
-        return i < (u32)kInline ? A.tab_sph + ((size_t)c * kInline + i) * A.R + slot
-                                : A.pool_sph + ((size_t)ovf * (LVX_MAX_SEEN - kInline) + (i - kInline)) * 3 + c;
+    __device__ __forceinline__ float4 *sph(u32 i) const {
+        return i < (u32)kInline ? A.tab_sph + (size_t)slot * kInline + i
+                                : A.pool_sph + (size_t)ovf * (LVX_MAX_SEEN - kInline) + (i - kInline);
     }
 };
 
@@ -1022,8 +1038,10 @@ __device__ __forceinline__ void wf_accumulate(const WfArgs &A, WfTables &T, WfPi
                         (__float_as_uint(cz) * 0xC2B2AE3Du);
         sph_bit = 1ull << (hsh >> 26);
         if (S.sph_bloom & sph_bit) {
-            for (int i = (int)S.n_sph - 1; i >= 0; --i)
-                if (*T.sph(i, 0) == cx && *T.sph(i, 1) == cy && *T.sph(i, 2) == cz) return;
+            for (int i = (int)S.n_sph - 1; i >= 0; --i) {
+                const float4 c = *T.sph(i);
+                if (c.x == cx && c.y == cy && c.z == cz) return;
+            }
         }
     }
     const bool need_pool = (S.n_seen == (u32)kInline || (is_sphere && S.n_sph == (u32)kInline)) && T.ovf == kNil;
@@ -1041,19 +1059,18 @@ __device__ __forceinline__ void wf_accumulate(const WfArgs &A, WfTables &T, WfPi
         bool found = false;
         if (S.seen_bloom & kb) {
             for (int i = (int)S.n_seen - 1; i >= 0; --i) {
-                if (*T.key(i) == lin) {
-                    u32 *mp = T.mask(i);
-                    const u32 mv = *mp;
-                    if (mv & bit) return;
-                    *mp = mv | bit;
+                uint2 *ep = T.seen(i);
+                const uint2 e = *ep;
+                if (e.x == lin) {
+                    if (e.y & bit) return;
+                    ep->y = e.y | bit;
                     found = true;
                     break;
                 }
             }
         }
         if (!found && S.n_seen < (u32)LVX_MAX_SEEN) {
-            *T.key(S.n_seen) = lin;
-            *T.mask(S.n_seen) = bit;
+            *T.seen(S.n_seen) = make_uint2(lin, bit);
             S.n_seen += 1;
             S.seen_bloom |= kb;
         }
@@ -1066,9 +1083,7 @@ __device__ __forceinline__ void wf_accumulate(const WfArgs &A, WfTables &T, WfPi
     S.acc[2] += w * scale * (double)col.z;
     S.acc[3] += w;
     if (is_sphere && S.n_sph < (u32)LVX_MAX_SEEN) {
-        *T.sph(S.n_sph, 0) = cx;
-        *T.sph(S.n_sph, 1) = cy;
-        *T.sph(S.n_sph, 2) = cz;
+        *T.sph(S.n_sph) = make_float4(cx, cy, cz, 0.0f);
         S.n_sph += 1;
         S.sph_bloom |= sph_bit;
     }
@@ -1084,6 +1099,9 @@ struct WfRayHits {
     __device__ __forceinline__ WfHit *at(u32 ref) const {
         return ref < (u32)kHitSlots ? A.hit_slot + (size_t)ref * A.R + place : A.hit + (ref - kHitSlots);
     }
+    __device__ __forceinline__ float4 centre(u32 ref) const {
+        return ref < (u32)kHitSlots ? A.slot_c[(size_t)ref * A.R + place] : A.hit_c[ref - kHitSlots];
+    }
     // iteration: ref = first(); while (ref != kNil) { ...; ref = next(ref); }
     __device__ __forceinline__ u32 first() const {
         return nslot ? 0u : (head == kNil ? kNil : head + kHitSlots);
@@ -1093,8 +1111,8 @@ struct WfRayHits {
             if (ref + 1 < nslot) return ref + 1;
             return head == kNil ? kNil : head + kHitSlots;
         }
-        const u32 e = A.hit[ref - kHitSlots].next & ~kDropped;
-        return e == (kNil & ~kDropped) ? kNil : e + kHitSlots;
+        const u32 e = A.hit_next[ref - kHitSlots];
+        return e == kNil ? kNil : e + kHitSlots;
     }
 };
 
@@ -1135,17 +1153,22 @@ __device__ void wf_apply_window_cap(const WfArgs &A, const WfRayHits &H, const W
             if (hit_gather(hb->key2) < ga) rank += 1;
         }
         if (rank >= (u32)LVX_MAX_WINDOW_HITS) {
-            ha->next |= kDropped;
+            ha->key2 |= kDroppedBit;
             A.win_over[w0 + k] += 1;
         }
     }
 }
 
-__device__ __forceinline__ bool wf_composite_one(const WfArgs &A, WfTables &T, WfPixel &S, const WfHit &h,
-                                                 double tau) {
+__device__ __forceinline__ bool wf_composite_one(const WfArgs &A, WfTables &T, WfPixel &S, const WfRayHits &H,
+                                                 u32 ref, double tau, double &t_in) {
     WF_STAT(1, 1);
-    wf_accumulate(A, T, S, h.scale, h.alpha, hit_lin(h.key2), hit_lid(h.key2), hit_attr(h.key2),
-                  hit_kind3(h.key2) != 0, h.cx, h.cy, h.cz);
+    const WfHit h = wf_load_hit(H.at(ref));
+    t_in = h.t_in;
+    const bool is_sphere = hit_kind3(h.key2) != 0;
+    float4 c = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    if (is_sphere) c = H.centre(ref);
+    wf_accumulate(A, T, S, h.scale, h.alpha, hit_lin(h.key2), hit_lid(h.key2), hit_attr(h.key2), is_sphere, c.x, c.y,
+                  c.z);
     return S.acc[3] >= tau;
 }
 
@@ -1217,7 +1240,7 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_ker
             unsigned long long s_k[kLight];
             for (u32 ref = H.first(); ref != kNil; ref = H.next(ref)) {
                 const WfHit *hp = H.at(ref);
-                if (big && (hp->next & kDropped)) continue;  // dropped by the window cap
+                if (big && (hp->key2 & kDroppedBit)) continue;  // dropped by the window cap
                 const double2 v = *reinterpret_cast<const double2 *>(hp);
                 const double t = v.x;
                 const unsigned long long k2 = (unsigned long long)__double_as_longlong(v.y);
@@ -1242,7 +1265,7 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_ker
             if (lane == L) {
                 u32 m = 0;
                 for (u32 ref = H.first(); ref != kNil; ref = H.next(ref)) {
-                    if (big && (H.at(ref)->next & kDropped)) continue;
+                    if (big && (H.at(ref)->key2 & kDroppedBit)) continue;
                     Q.ref[warp][m++] = ref;
                 }
                 Q.n[warp] = m;
@@ -1289,10 +1312,10 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_ker
             double term_t = 0.0;
             if (nhit <= (u32)kSortCap) {
                 for (int j = 0; j < n; ++j) {
-                    const WfHit h = *H.at(order[j]);
-                    if (wf_composite_one(A, T, S, h, tau)) {
+                    double t_hit;
+                    if (wf_composite_one(A, T, S, H, order[j], tau, t_hit)) {
                         terminated = true;
-                        term_t = h.t_in;
+                        term_t = t_hit;
                         break;
                     }
                 }
@@ -1308,7 +1331,7 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_ker
                     unsigned long long bk = 0;
                     for (u32 ref = H.first(); ref != kNil; ref = H.next(ref)) {
                         const WfHit *hp = H.at(ref);
-                        if (hp->next & kDropped) continue;
+                        if (hp->key2 & kDroppedBit) continue;
                         const double t = hp->t_in;
                         const unsigned long long k2 = hp->key2;
                         if (have_last && !wf_before(lt, lk, t, k2)) continue;
@@ -1319,10 +1342,10 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_ker
                         }
                     }
                     if (best == kNil) break;
-                    const WfHit h = *H.at(best);
-                    if (wf_composite_one(A, T, S, h, tau)) {
+                    double t_hit;
+                    if (wf_composite_one(A, T, S, H, best, tau, t_hit)) {
                         terminated = true;
-                        term_t = h.t_in;
+                        term_t = t_hit;
                         break;
                     }
                     have_last = true;
@@ -1334,8 +1357,8 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_ker
             rp.acc[1] = S.acc[1];
             rp.acc[2] = S.acc[2];
             rp.acc[3] = S.acc[3];
-            rp.n_seen = S.n_seen;
-            rp.n_sph = S.n_sph;
+            rp.n_seen = (u16)S.n_seen;
+            rp.n_sph = (u16)S.n_sph;
             rp.seen_bloom = S.seen_bloom;
             rp.sph_bloom = S.sph_bloom;
             rp.ovf = T.ovf;
@@ -1363,8 +1386,9 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_ker
         if (finished) {
             if (!terminated) tests = A.rw[slot].tests;
             over = rp.over;
-            write_pixel(A, rp.out_off, rp.acc[0], rp.acc[1], rp.acc[2], rp.acc[3]);
-            const u32 y = rp.pix >> 16;
+            const uint2 px = A.rpix[slot];
+            write_pixel(A, px.y, rp.acc[0], rp.acc[1], rp.acc[2], rp.acc[3]);
+            const u32 y = px.x >> 16;
             if (tests) atomicAdd(A.row_stats + 3 * (i64)y + 1, tests);
             if (over) atomicAdd(A.row_stats + 3 * (i64)y + 2, over);
         } else if (valid) {
@@ -1447,8 +1471,9 @@ __global__ void wf_begin_kernel(const WfArgs A) {
 // scratch layout ------------------------------------------------------------------------
 struct WfLayout {
     size_t total;
-    size_t ctl, rw, rp, head, tab_key, tab_mask, tab_sph, pool_key, pool_mask, pool_sph, live0, live1, win,
-        win_over, item_place, item_lin, item_q, item_t, fdir, span, rdir, tube, sph, hit, hit_slot, hcnt;
+    size_t ctl, rw, rp, rpix, head, tab_seen, tab_sph, pool_seen, pool_sph, live0, live1, win,
+        win_over, item_place, item_lin, item_q, item_t, fdir, span, rdir, tube, sph, hit, hit_c, hit_next, hit_slot,
+        slot_c, hcnt;
     u32 R, pool_cap, cap_win, capq_item, capq_surv, capq_hit;
 };
 
@@ -1474,12 +1499,11 @@ WfLayout wf_layout(i64 R, double scale) {
     L.rw = take(c, r * sizeof(WfRayWalk));
     L.rp = take(c, r * sizeof(WfRayPix));
     L.head = take(c, r * 4);
-    L.tab_key = take(c, r * 4 * kInline);
-    L.tab_mask = take(c, r * 4 * kInline);
-    L.tab_sph = take(c, r * 12 * kInline);
-    L.pool_key = take(c, po * 4);
-    L.pool_mask = take(c, po * 4);
-    L.pool_sph = take(c, po * 12);
+    L.rpix = take(c, r * 8);
+    L.tab_seen = take(c, r * 8 * kInline);
+    L.tab_sph = take(c, r * 16 * kInline);
+    L.pool_seen = take(c, po * 8);
+    L.pool_sph = take(c, po * 16);
     L.live0 = take(c, r * 4);
     L.live1 = take(c, r * 4);
     L.win = take(c, (size_t)L.cap_win * sizeof(WfWindow));
@@ -1494,7 +1518,10 @@ WfLayout wf_layout(i64 R, double scale) {
     L.tube = take(c, (size_t)L.capq_surv * kNQ * sizeof(WfEntry));
     L.sph = take(c, (size_t)L.capq_surv * kNQ * sizeof(WfEntry));
     L.hit = take(c, (size_t)L.capq_hit * kNQ * sizeof(WfHit));
+    L.hit_c = take(c, (size_t)L.capq_hit * kNQ * 16);
+    L.hit_next = take(c, (size_t)L.capq_hit * kNQ * 4);
     L.hit_slot = take(c, r * kHitSlots * sizeof(WfHit));
+    L.slot_c = take(c, r * kHitSlots * 16);
     L.hcnt = take(c, r * 4);
     L.total = take(c, 0);
     return L;
@@ -1652,12 +1679,11 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     A.rw = (WfRayWalk *)(base + L.rw);
     A.rp = (WfRayPix *)(base + L.rp);
     A.head = (u32 *)(base + L.head);
-    A.tab_key = (u32 *)(base + L.tab_key);
-    A.tab_mask = (u32 *)(base + L.tab_mask);
-    A.tab_sph = (float *)(base + L.tab_sph);
-    A.pool_key = (u32 *)(base + L.pool_key);
-    A.pool_mask = (u32 *)(base + L.pool_mask);
-    A.pool_sph = (float *)(base + L.pool_sph);
+    A.rpix = (uint2 *)(base + L.rpix);
+    A.tab_seen = (uint2 *)(base + L.tab_seen);
+    A.tab_sph = (float4 *)(base + L.tab_sph);
+    A.pool_seen = (uint2 *)(base + L.pool_seen);
+    A.pool_sph = (float4 *)(base + L.pool_sph);
     A.pool_cap = L.pool_cap;
     A.live[0] = (u32 *)(base + L.live0);
     A.live[1] = (u32 *)(base + L.live1);
@@ -1676,8 +1702,11 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     A.sph = (WfEntry *)(base + L.sph);
     A.capq_surv = L.capq_surv;
     A.hit = (WfHit *)(base + L.hit);
+    A.hit_c = (float4 *)(base + L.hit_c);
+    A.hit_next = (u32 *)(base + L.hit_next);
     A.capq_hit = L.capq_hit;
     A.hit_slot = (WfHit *)(base + L.hit_slot);
+    A.slot_c = (float4 *)(base + L.slot_c);
     A.hcnt = (u32 *)(base + L.hcnt);
     // schedule constants; the LVX_WF_* developer overrides are read ONCE per process
     const WfTuning &tune = wf_tuning();
