@@ -91,7 +91,10 @@ __device__ __forceinline__ unsigned long long hit_gather(unsigned long long k) {
     return ((k >> 24) << 10) | (((k >> 10) & 255ull) << 2) | ((k >> 8) & 3ull);
 }
 
-constexpr int kHitSlots = 12;      // hits per ray and iteration stored ray-parallel (the rest is listed)
+#ifndef LVX_WF_HITSLOTS
+#define LVX_WF_HITSLOTS 24
+#endif
+constexpr int kHitSlots = LVX_WF_HITSLOTS;  // hits per ray and iteration stored ray-parallel (the rest is listed)
 
 // what an exact test needs of its ray, by place: one 32-byte sector, two hops from the queue
 // entry (entry -> item_place -> here) instead of three (-> live -> the ray's state record)
@@ -131,7 +134,10 @@ static_assert(sizeof(WfRayPix) == 64, "pixel state is 64 bytes");
 // windows a ray may record in the first iteration (doubling per iteration after that); also
 // what the window arrays are sized for.  Swept with the spread / tail rules in place: 8 -> 12 is
 // worth 0.05-0.15 ms on C2, C3 and the 1M-line scene.
-constexpr int kWinFirst = 12;
+#ifndef LVX_WF_WINFIRST
+#define LVX_WF_WINFIRST 12
+#endif
+constexpr int kWinFirst = LVX_WF_WINFIRST;
 
 struct WfCtl {
     u32 n_live[2];
