@@ -4,6 +4,7 @@
 //   probes: traverse_voxels raycast.py:170-181, intersect_ray_tube/sphere :184-213,
 //           cone_soft_shadow / ao_density_rays / sample_ao illumination.py:142-225
 #include <math_constants.h>
+#include <stdlib.h>
 
 #include "lvx_geom.cuh"
 
@@ -142,6 +143,172 @@ ao_bake_brick_kernel(const u8 *__restrict__ counts, int rx, int ry, int rz, int 
         }
         __syncwarp();
     }
+}
+
+// Batched brick bake (the default).  Same staging as above; what changes is how the work is dealt:
+//  * the (voxel, ray) pairs of up to kBakeBatch occupied voxels are flattened over ALL threads of the
+//    block, so every lane marches a ray whatever n_rays and the occupancy pattern are (one warp per
+//    voxel left 28 of 32 lanes idle in the last of its four rounds at 100 rays);
+//  * the per-ray results of the batch sit in shared memory and ONE THREAD PER VOXEL adds them up in
+//    lattice order -- the reference's float64 summation order (_kernels.py:592-605) -- so up to 32 of
+//    these 100-step dependent chains run side by side instead of one at a time;
+//  * a brick whose halo lies inside the grid (INTERIOR) needs neither the grid-exit test nor the
+//    clamp-to-edge of sample_field_trilinear: no sample can leave the staged block;
+//  * cell indices are integers from one float64 -> int floor conversion per axis (the reference's
+//    floor / clip / int chain is the same integer), the eight corners are one base address plus
+//    constant offsets.
+// Arithmetic per sample is the reference's, operation for operation; the field is bit-identical.
+#ifndef LVX_AO_BATCH
+#define LVX_AO_BATCH 32
+#endif
+#ifndef LVX_AO_F64
+#define LVX_AO_F64 0
+#endif
+constexpr int kBakeBatch = LVX_AO_BATCH;
+constexpr int kBakeThreads = 256;
+// the staged density: float32 as stored (widened per corner load), or widened once at staging
+#if LVX_AO_F64
+typedef double bake_t;
+#else
+typedef float bake_t;
+#endif
+
+template <bool INTERIOR>
+__device__ __forceinline__ double bake_sample(const bake_t *__restrict__ s, int E, int lox, int loy, int loz, int rx,
+                                              int ry, int rz, double x, double y, double z) {
+    // sample_field_trilinear (_kernels.py:346-383) at scale 1: x / 1.0 - 0.5 == x - 0.5
+    const double qx = x / 1.0 - 0.5, qy = y / 1.0 - 0.5, qz = z / 1.0 - 0.5;
+    const int ix = __double2int_rd(qx), iy = __double2int_rd(qy), iz = __double2int_rd(qz);  // floor
+    const double fx = qx - (double)ix, fy = qy - (double)iy, fz = qz - (double)iz;
+    int o000, dx1, dy1, dz1;
+    if (INTERIOR) {
+        o000 = ((iz - loz) * E + (iy - loy)) * E + (ix - lox);
+        dx1 = 1;
+        dy1 = E;
+        dz1 = E * E;
+    } else {
+        const int x0 = min(max(ix, 0), rx - 1), x1 = min(max(ix + 1, 0), rx - 1);
+        const int y0 = min(max(iy, 0), ry - 1), y1 = min(max(iy + 1, 0), ry - 1);
+        const int z0 = min(max(iz, 0), rz - 1), z1 = min(max(iz + 1, 0), rz - 1);
+        o000 = ((z0 - loz) * E + (y0 - loy)) * E + (x0 - lox);
+        dx1 = x1 - x0;
+        dy1 = (y1 - y0) * E;
+        dz1 = (z1 - z0) * E * E;
+    }
+    const bake_t *c = s + o000;
+    const double v000 = (double)c[0], v001 = (double)c[dx1];
+    const double v010 = (double)c[dy1], v011 = (double)c[dy1 + dx1];
+    const double v100 = (double)c[dz1], v101 = (double)c[dz1 + dx1];
+    const double v110 = (double)c[dz1 + dy1], v111 = (double)c[dz1 + dy1 + dx1];
+    const double gx_ = 1.0 - fx, gy_ = 1.0 - fy, gz_ = 1.0 - fz;
+    const double c00 = v000 * gx_ + v001 * fx;
+    const double c01 = v010 * gx_ + v011 * fx;
+    const double c10 = v100 * gx_ + v101 * fx;
+    const double c11 = v110 * gx_ + v111 * fx;
+    const double c0 = c00 * gy_ + c01 * fy;
+    const double c1 = c10 * gy_ + c11 * fy;
+    return c0 * gz_ + c1 * fz;
+}
+
+template <bool INTERIOR>
+__device__ __forceinline__ void bake_batches(const bake_t *__restrict__ s_l0, const double *__restrict__ s_d,
+                                             double *__restrict__ s_res, const unsigned short *__restrict__ s_list,
+                                             int n_occ, int batch, int row, int E, int lox, int loy, int loz, int bx, int by,
+                                             int bz, int rx, int ry, int rz, int n_rays, double radius, double step,
+                                             float *__restrict__ out) {
+    const int tid = threadIdx.x;
+    const double gx = (double)rx, gy = (double)ry, gz = (double)rz;
+    for (int e0 = 0; e0 < n_occ; e0 += batch) {
+        const int nb = min(batch, n_occ - e0);
+        const int items = nb * n_rays;
+        for (int w = tid; w < items; w += kBakeThreads) {
+            const int v = w / n_rays, r = w - v * n_rays;
+            const int k = s_list[e0 + v];
+            const double px = (double)(bx + (k & 7)) + 0.5, py = (double)(by + ((k >> 3) & 7)) + 0.5,
+                         pz = (double)(bz + (k >> 6)) + 0.5;
+            const double dx = s_d[3 * r], dy = s_d[3 * r + 1], dz = s_d[3 * r + 2];
+            // density_ray_blocking, _kernels.py:425-445
+            double acc = 0.0, t_cur = step;
+            bool sat = false;
+            while (t_cur <= radius) {
+                const double sx = px + t_cur * dx, sy_ = py + t_cur * dy, sz_ = pz + t_cur * dz;
+                if (!INTERIOR && (sx < 0.0 || sy_ < 0.0 || sz_ < 0.0 || sx > gx || sy_ > gy || sz_ > gz)) break;
+                acc += bake_sample<INTERIOR>(s_l0, E, lox, loy, loz, rx, ry, rz, sx, sy_, sz_) * step;
+                if (acc >= 1.0) {
+                    sat = true;
+                    break;
+                }
+                t_cur += step;
+            }
+            s_res[v * row + r] = sat ? 1.0 : (acc < 1.0 ? acc : 1.0);
+        }
+        __syncthreads();
+        if (tid < nb) {
+            const double *mine = s_res + tid * row;
+            double total = 0.0;
+            for (int r = 0; r < n_rays; ++r) total += mine[r];
+            double v = total / (double)n_rays;
+            v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+            const int k = s_list[e0 + tid];
+            out[(bx + (k & 7)) + (i64)rx * ((by + ((k >> 3) & 7)) + (i64)ry * (bz + (k >> 6)))] = (float)v;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kBakeThreads)
+ao_bake_batch_kernel(const u8 *__restrict__ counts, int rx, int ry, int rz, int n_rays, double radius, double step,
+                     const double *__restrict__ dirs, const float *__restrict__ l0, int H, int batch, int row,
+                     float *__restrict__ out) {
+    extern __shared__ double s_mem[];
+    const int E = kBrick + 2 * H;
+    double *s_d = s_mem;                  // [3 * n_rays] ray directions in grid space
+    double *s_res = s_d + 3 * n_rays;     // [batch][row] per-ray results of the current batch
+    bake_t *s_l0 = reinterpret_cast<bake_t *>(s_res + (size_t)batch * row);  // [E^3]
+    __shared__ unsigned short s_list[kBrick * kBrick * kBrick];
+    __shared__ int s_n;
+    const int tid = threadIdx.x;
+    const int bx = blockIdx.x * kBrick, by = blockIdx.y * kBrick, bz = blockIdx.z * kBrick;
+    const int lox = bx - H, loy = by - H, loz = bz - H;
+    if (tid == 0) s_n = 0;
+    __syncthreads();
+    // occupied voxels first: an empty brick is done after writing its zeros
+    for (int k = tid; k < kBrick * kBrick * kBrick; k += kBakeThreads) {
+        const int x = bx + (k & 7), y = by + ((k >> 3) & 7), z = bz + (k >> 6);
+        if (x >= rx || y >= ry || z >= rz) continue;
+        const i64 lin = x + (i64)rx * (y + (i64)ry * z);
+        if (counts[lin] != 0) s_list[atomicAdd(&s_n, 1)] = (unsigned short)k;
+        else out[lin] = 0.0f;
+    }
+    __syncthreads();
+    const int n_occ = s_n;
+    if (n_occ == 0) return;
+    {
+        // ray directions: the lattice in the frame of the normal (0,0,1) (orient_frame, _kernels.py:555-569)
+        double tf[3], bf[3];
+        lvx_orient_frame(0.0, 0.0, 1.0, tf, bf);
+        for (int r = tid; r < n_rays; r += kBakeThreads) {
+            const double lx = dirs[3 * r], ly = dirs[3 * r + 1], lz = dirs[3 * r + 2];
+            s_d[3 * r] = lx * tf[0] + ly * bf[0] + lz * 0.0;
+            s_d[3 * r + 1] = lx * tf[1] + ly * bf[1] + lz * 0.0;
+            s_d[3 * r + 2] = lx * tf[2] + ly * bf[2] + lz * 1.0;
+        }
+    }
+    for (int k = tid; k < E * E * E; k += kBakeThreads) {
+        const int ix = k % E, iy = (k / E) % E, iz = k / (E * E);
+        const int gx_ = min(max(lox + ix, 0), rx - 1), gy_ = min(max(loy + iy, 0), ry - 1),
+                  gz_ = min(max(loz + iz, 0), rz - 1);
+        s_l0[k] = (bake_t)__ldg(l0 + ((i64)gz_ * ry + gy_) * rx + gx_);
+    }
+    __syncthreads();
+    // the warp order of the list is arbitrary (atomics); the result per voxel does not depend on it
+    const bool interior = lox >= 0 && loy >= 0 && loz >= 0 && lox + E <= rx && loy + E <= ry && loz + E <= rz;
+    if (interior)
+        bake_batches<true>(s_l0, s_d, s_res, s_list, n_occ, batch, row, E, lox, loy, loz, bx, by, bz, rx, ry, rz, n_rays,
+                           radius, step, out);
+    else
+        bake_batches<false>(s_l0, s_d, s_res, s_list, n_occ, batch, row, E, lox, loy, loz, bx, by, bz, rx, ry, rz, n_rays,
+                            radius, step, out);
 }
 
 __global__ void probe_dda_kernel(double ox, double oy, double oz, double dx, double dy, double dz,
@@ -296,13 +463,30 @@ int lvx_ao_bake(const uint8_t *counts_d, const int32_t dims[3], int32_t n_rays, 
     LVX_REQUIRE(n_rays >= 1 && n_rays <= 8192, "n_rays must be in [1, 8192], got %d", n_rays);
     LVX_REQUIRE(radius > 0.0 && step > 0.0, "radius and step must be positive");
     {
-        // brick kernel when the halo of the radius of influence fits in shared memory
+        // brick kernels when the halo of the radius of influence fits in shared memory
         const int H = (int)ceil(radius) + 1;
         const size_t E = (size_t)kBrick + 2 * (size_t)H;
+        dim3 bgrid((unsigned)lvx_ceil_div(dims[0], kBrick), (unsigned)lvx_ceil_div(dims[1], kBrick),
+                   (unsigned)lvx_ceil_div(dims[2], kBrick));
+        // batched kernel: as many voxels per batch as 64 KB of per-ray results hold (rows padded to an odd
+        // number of doubles: the per-voxel sums then read conflict-free)
+        const int row = n_rays | 1;
+        int batch = (int)((64 * 1024) / ((size_t)row * sizeof(double)));
+        batch = batch > kBakeBatch ? kBakeBatch : batch;
+        const size_t need_b = ((size_t)n_rays * 3 + (size_t)(batch > 0 ? batch : 1) * row) * sizeof(double) +
+                              E * E * E * sizeof(bake_t);
+        static const bool legacy = getenv("LVX_AO_LEGACY") != nullptr;  // developer A/B switch
+        if (!legacy && radius < 64.0 && batch >= 1 && need_b <= 200 * 1024) {
+            if (need_b > 48 * 1024)
+                LVX_CUDA_CHECK(cudaFuncSetAttribute(ao_bake_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    (int)need_b));
+            ao_bake_batch_kernel<<<bgrid, kBakeThreads, need_b, (cudaStream_t)stream>>>(
+                counts_d, dims[0], dims[1], dims[2], n_rays, radius, step, dirs_d, level0_d, H, batch, row, ao_d);
+            LVX_LAUNCH_CHECK();
+            return LVX_OK;
+        }
         const size_t need = ((size_t)n_rays * 3 + (size_t)kBakeWarps * n_rays) * sizeof(double) + E * E * E * sizeof(float);
         if (radius < 64.0 && need <= 160 * 1024) {
-            dim3 bgrid((unsigned)lvx_ceil_div(dims[0], kBrick), (unsigned)lvx_ceil_div(dims[1], kBrick),
-                       (unsigned)lvx_ceil_div(dims[2], kBrick));
             if (need > 48 * 1024)
                 LVX_CUDA_CHECK(cudaFuncSetAttribute(ao_bake_brick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     (int)need));
