@@ -570,7 +570,7 @@ def run_ours(args, wl):
 
     # ---- roofline of the frame kernel (rank 0, single GPU view) -----------------------------
     bits = torch.zeros((V + 31) // 32, dtype=torch.int32, device="cuda")
-    plan1 = FramePlan(cam, model, octree, params, nb)
+    plan1 = FramePlan(cam, model, octree, params, nb, records="rec")
     img1 = torch.empty((H, W, 4), dtype=torch.float32, device="cuda")
     st1 = torch.zeros((H, 3), dtype=torch.int64, device="cuda")
     plan1.launch_footprint(img1, st1, bits)

@@ -126,7 +126,10 @@ int lvx_raw_regroup(const uint64_t *in_key_d, const uint64_t *in_q_d, const uint
 
 /* Order every voxel's group by key (= the reference's stable argsort by voxel,
  * voxelizer.py:435-438), keep the first 255, lid = rank % 32, decode bin centres, pack
- * (voxelizer.py:439-488, 383-394).  Optional outputs may be NULL. */
+ * (voxelizer.py:439-488, 383-394).  Optional outputs may be NULL.
+ * Alignment: grouped_d (lvx_raw_regroup, lvx_voxelize_compact) and seg_rec_d (lvx_voxelize_compact,
+ * lvx_decode_packed, lvx_build_seg_records) are accessed with 256-bit loads / stores and must be
+ * 32-byte aligned; the calls return LVX_E_INVALID otherwise. */
 int lvx_voxelize_compact(const lvx_raw_record *grouped_d, int64_t n_raw, const uint32_t *vox_cnt_d,
                          const uint32_t *cursor_end_d, const uint32_t *offsets_d,
                          const int32_t dims[3], int32_t n_bins, uint8_t *packed_d, float *seg_a_d,

@@ -8,6 +8,67 @@ struct LvxHit {
     double t_in, t_out, nx, ny, nz;
 };
 
+// ---------------------------------------------------------------------------
+// The encoded segment records (voxelizer.py:79-89, model_io.py:151-179): `width` bytes per
+// record, LSB first  face_in(3) bin_in(2 lb) face_out(3) bin_out(2 lb) attr(8) lid(5).
+// A frame can be rendered straight from them: 5 bytes per segment at N = 32
+// instead of the 32-byte render record, so the whole model stays in L2.
+// ---------------------------------------------------------------------------
+struct LvxPacked {
+    const u8 *bytes;  // 8-byte aligned, readable up to the next multiple of 8 bytes
+    int width, lb, n;
+    float inv_n;      // 1 / n: n is a power of two, so x * inv_n == x / n exactly (float32 and float64)
+};
+
+__device__ __forceinline__ u64 lvx_packed_word(const LvxPacked &P, u32 seg) {
+    const size_t off = (size_t)seg * (size_t)P.width;
+    const u64 *p = reinterpret_cast<const u64 *>(P.bytes) + (off >> 3);
+    const int sh = (int)(off & 7) * 8;
+    u64 v = __ldg(p) >> sh;
+    if (sh + 8 * P.width > 64) v |= __ldg(p + 1) << (64 - sh);
+    return v;
+}
+
+struct LvxPackedFields {
+    u32 face_in, bin_in, face_out, bin_out, attr, lid;
+};
+__device__ __forceinline__ LvxPackedFields lvx_packed_fields(const LvxPacked &P, u64 v) {
+    const int bb = 2 * P.lb;
+    const u64 bmask = ((u64)1 << bb) - 1;
+    LvxPackedFields f;
+    f.face_in = (u32)(v & 7u);
+    f.bin_in = (u32)((v >> 3) & bmask);
+    f.face_out = (u32)((v >> (3 + bb)) & 7u);
+    f.bin_out = (u32)((v >> (6 + bb)) & bmask);
+    f.attr = (u32)((v >> (6 + 2 * bb)) & 0xFFu);
+    f.lid = (u32)((v >> (14 + 2 * bb)) & 31u);
+    return f;
+}
+
+// bin centre of (face, code) in the unit cube of its voxel: exact in float32 (dyadic, <= 9 fraction bits)
+__device__ __forceinline__ void lvx_packed_local(u32 face, u32 code, const LvxPacked &P, float out[3]) {
+    const int bu = (int)(code & (u32)(P.n - 1)), bv = (int)(code >> P.lb);
+    const float cu = ((float)bu + 0.5f) * P.inv_n, cv = ((float)bv + 0.5f) * P.inv_n;
+    const int axis = (int)(face >> 1);
+    const float side = (float)(face & 1);
+    out[0] = axis == 0 ? side : cu;
+    out[1] = axis == 1 ? side : (axis == 0 ? cu : cv);
+    out[2] = axis == 2 ? side : cv;
+}
+
+// the reference's reconstructed endpoint: bin centre + voxel in float64, cast to float32
+// (voxelizer.py:376-380, 477-478; model_io.py:169-179) -- the value the render records hold
+__device__ __forceinline__ void lvx_packed_point(u32 face, u32 code, const LvxPacked &P, int vx, int vy, int vz,
+                                                 float out[3]) {
+    const int bu = (int)(code & (u32)(P.n - 1)), bv = (int)(code >> P.lb);
+    const double cu = ((double)bu + 0.5) * (double)P.inv_n, cv = ((double)bv + 0.5) * (double)P.inv_n;
+    const int axis = (int)(face >> 1);
+    const double side = (double)(face & 1);
+    out[0] = (float)((axis == 0 ? side : cu) + (double)vx);
+    out[1] = (float)((axis == 1 ? side : (axis == 0 ? cu : cv)) + (double)vy);
+    out[2] = (float)((axis == 2 ? side : cv) + (double)vz);
+}
+
 // intersect_tube_raw, _kernels.py:76-134, in the specialisation the frame kernels
 // compile to: the endpoints arrive as float32, numba's float(f32) does not widen,
 // so axis, length and normalisation run in float32.

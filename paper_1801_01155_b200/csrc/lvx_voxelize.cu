@@ -662,7 +662,9 @@ compact_kernel(const lvx_raw_record *__restrict__ grouped, i64 n_raw, const u32 
     u32 rank = 0;
     if (n > 1) {
         const u32 end = cursor_end[lin];
-        for (u32 k = end - n; k < end; ++k) rank += grouped[k].key < key ? 1u : 0u;
+        // (a record that already has 255 predecessors is dropped whatever the rest of its group
+        // holds: the scan of a crowded voxel -- thousands of chords on a coarse grid -- stops there)
+        for (u32 k = end - n; k < end && rank < 255u; ++k) rank += grouped[k].key < key ? 1u : 0u;
     }
     if (rank >= 255u) return;  // voxelizer.py:442-448 keep the first 255 in curve order
     const i64 dst = (i64)offsets[lin] + rank;
@@ -918,6 +920,8 @@ int lvx_voxelize_compact(const lvx_raw_record *grouped_d, int64_t n_raw, const u
     LVX_REQUIRE(n_raw >= 0, "bad arguments");
     if (n_raw == 0) return LVX_OK;
     LVX_REQUIRE(grouped_d && vox_cnt_d && cursor_end_d && offsets_d && packed_d, "null input");
+    LVX_REQUIRE(((uintptr_t)grouped_d & 31) == 0 && ((uintptr_t)seg_rec_d & 31) == 0,
+                "grouped_d and seg_rec_d must be 32-byte aligned (256-bit accesses)");
     const int lb = ilog2i(n_bins);
     const int width = (2 * (3 + 2 * lb) + 8 + 5 + 7) / 8;  // record_width, voxelizer.py:70-76
     CompactOut o = {packed_d,      seg_a_d,        seg_b_d,      seg_attr_d, seg_lid_d, seg_voxel_d,
@@ -933,6 +937,7 @@ int lvx_raw_regroup(const uint64_t *in_key_d, const uint64_t *in_q_d, const uint
     LVX_REQUIRE(n_slots >= 0, "bad arguments");
     if (n_slots == 0) return LVX_OK;
     LVX_REQUIRE(in_key_d && in_q_d && in_lin_d && cursor_d && grouped_d, "null input");
+    LVX_REQUIRE(((uintptr_t)grouped_d & 31) == 0, "grouped_d must be 32-byte aligned (256-bit stores)");
     regroup_kernel<<<(unsigned)lvx_ceil_div(n_slots, 256), 256, 0, (cudaStream_t)stream>>>(
         in_key_d, in_q_d, in_lin_d, n_slots, cursor_d, grouped_d);
     LVX_LAUNCH_CHECK();
@@ -1024,6 +1029,7 @@ int lvx_decode_packed(const uint8_t *packed_d, const uint8_t *counts_d, const ui
     if (int rc = check_dims(dims)) return rc;
     if (int rc = check_bins(n_bins)) return rc;
     LVX_REQUIRE(packed_d && counts_d && offsets_d && err_d, "null input");
+    LVX_REQUIRE(((uintptr_t)seg_rec_d & 31) == 0, "seg_rec_d must be 32-byte aligned (256-bit stores)");
     const i64 V = (i64)dims[0] * dims[1] * dims[2];
     const int lb = ilog2i(n_bins);
     const int width = (2 * (3 + 2 * lb) + 8 + 5 + 7) / 8;  // record_width, voxelizer.py:70-76

@@ -164,6 +164,7 @@ struct WfArgs {
     const u8 *counts;
     const u32 *offsets;
     const lvx_seg_record *rec;
+    LvxPacked pk;  // the encoded records (frames rendered straight from them: rec may then be null)
     const float *table;
     const u16 *nsum;
     const u32 *nmask;
@@ -758,14 +759,14 @@ __device__ __forceinline__ void cand_flush(const WfArgs &A, CandStage &S, int wa
     __syncwarp();
 }
 
+// (ax..bz: the segment's endpoints in the frame of its voxel; half_len: bounding-sphere radius)
 __device__ __forceinline__ void cand_segment(const WfArgs &A, CandStage &S, int warp, const CandItem &I, u32 seg,
-                                             const float4 ra, const float4 rb, bool joints, float reach_pt, int q) {
-    const float ax = ra.x - I.fhx, ay = ra.y - I.fhy, az = ra.z - I.fhz;
-    const float bx = rb.x - I.fhx, by = rb.y - I.fhy, bz = rb.z - I.fhz;
+                                             float ax, float ay, float az, float bx, float by, float bz, float half_len,
+                                             bool joints, float reach_pt, int q) {
     u32 mk = 0;
     // the tube AND both joint spheres lie inside the segment's bounding sphere
     if (wf_near_line(0.5f * (ax + bx), 0.5f * (ay + by), 0.5f * (az + bz), I.q0x, I.q0y, I.q0z, I.fdx, I.fdy, I.fdz,
-                     rb.w + reach_pt)) {
+                     half_len + reach_pt)) {
         // the tube's entry point lies on the ray within tube_r of the segment's axis line:
         // |w . (d x u)| <= reach |d x u|  (absolute slack >> float32 rounding)
         const float ux = bx - ax, uy = by - ay, uz = bz - az;
@@ -827,6 +828,29 @@ __device__ __forceinline__ void cand_segment(const WfArgs &A, CandStage &S, int 
 #ifndef LVX_WF_CAND_MINB
 #define LVX_WF_CAND_MINB 4
 #endif
+// segment `seg` of an item: endpoints in the voxel's frame, from the render record or the encoded one
+template <bool PACKED>
+__device__ __forceinline__ void cand_fetch(const WfArgs &A, const CandItem &I, u32 seg, float a[3], float b[3],
+                                           float &half_len) {
+    if (PACKED) {
+        const LvxPackedFields f = lvx_packed_fields(A.pk, lvx_packed_word(A.pk, seg));
+        lvx_packed_local(f.face_in, f.bin_in, A.pk, a);
+        lvx_packed_local(f.face_out, f.bin_out, A.pk, b);
+        half_len = lvx_half_len(a[0], a[1], a[2], b[0], b[1], b[2]);
+    } else {
+        const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + seg));
+        const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + seg) + 1);
+        a[0] = ra.x - I.fhx;
+        a[1] = ra.y - I.fhy;
+        a[2] = ra.z - I.fhz;
+        b[0] = rb.x - I.fhx;
+        b[1] = rb.y - I.fhy;
+        b[2] = rb.z - I.fhz;
+        half_len = rb.w;
+    }
+}
+
+template <bool PACKED>
 __global__ void __launch_bounds__(kThreadsWf, LVX_WF_CAND_MINB) wf_cand_kernel(const WfArgs A) {
     __shared__ QueueView V;
     __shared__ CandStage S;
@@ -877,12 +901,9 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_CAND_MINB) wf_cand_kernel(c
             I[k].aux0 = nbr ? 0u : I[k].it;
             I[k].aux_step = nbr ? 1u : 0u;
         }
-        float4 ra[2], rb[2];
+        float ea[2][3], eb[2][3], hl[2];
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-            // (a listed voxel holds at least one record)
-            ra[k] = __ldg(reinterpret_cast<const float4 *>(A.rec + I[k].base));
-            rb[k] = __ldg(reinterpret_cast<const float4 *>(A.rec + I[k].base) + 1);
             const u32 hz = lin[k] / plane, hy = (lin[k] - hz * plane) / (u32)A.rx, hx = lin[k] - hz * plane - hy * (u32)A.rx;
             I[k].fhx = (float)hx;
             I[k].fhy = (float)hy;
@@ -890,16 +911,19 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_CAND_MINB) wf_cand_kernel(c
             I[k].q0x = q0[k].x;
             I[k].q0y = q0[k].y;
             I[k].q0z = q0[k].z;
+            // (a listed voxel holds at least one record)
+            cand_fetch<PACKED>(A, I[k], I[k].base, ea[k], eb[k], hl[k]);
         }
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
             if (I[k].cnt == 0) continue;
-            cand_segment(A, S, warp, I[k], I[k].base, ra[k], rb[k], joints, reach_pt, q);
+            cand_segment(A, S, warp, I[k], I[k].base, ea[k][0], ea[k][1], ea[k][2], eb[k][0], eb[k][1], eb[k][2], hl[k],
+                         joints, reach_pt, q);
             for (u32 sg = 1; sg < I[k].cnt; ++sg) {
                 const u32 seg = I[k].base + sg;
-                const float4 a4 = __ldg(reinterpret_cast<const float4 *>(A.rec + seg));
-                const float4 b4 = __ldg(reinterpret_cast<const float4 *>(A.rec + seg) + 1);
-                cand_segment(A, S, warp, I[k], seg, a4, b4, joints, reach_pt, q);
+                float a3[3], b3[3], h1;
+                cand_fetch<PACKED>(A, I[k], seg, a3, b3, h1);
+                cand_segment(A, S, warp, I[k], seg, a3[0], a3[1], a3[2], b3[0], b3[1], b3[2], h1, joints, reach_pt, q);
             }
         }
         __syncwarp();
@@ -929,7 +953,7 @@ __device__ __forceinline__ WfHit wf_load_hit(const WfHit *p) {
 #ifndef LVX_WF_EXACT_MINB
 #define LVX_WF_EXACT_MINB 4
 #endif
-template <int KIND, bool GEOM>
+template <int KIND, bool GEOM, bool PACKED>
 __global__ void __launch_bounds__(kThreadsWf, LVX_WF_EXACT_MINB) wf_exact_kernel(const WfArgs A, int par) {
     __shared__ QueueView V;
     queue_view_load(V, KIND == 0 ? A.ctl->tube_cnt : A.ctl->sph_cnt, A.capq_surv, A.ctl->err);
@@ -946,26 +970,45 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_EXACT_MINB) wf_exact_kernel
         const u32 place = c.place;
         const WfRayDir rd = A.rdir[place];
         const double rdx = rd.dx, rdy = rd.dy, rdz = rd.dz;
-        const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + seg));
+        // the segment's endpoints as the reference's float32 arrays hold them, + attr | lid << 8
+        float pa[3], pb[3];
+        u32 rmeta;
+        if (PACKED) {
+            const LvxPackedFields f = lvx_packed_fields(A.pk, lvx_packed_word(A.pk, seg));
+            const u32 plane = (u32)A.rx * (u32)A.ry;
+            const u32 vz = c.lin / plane, vy = (c.lin - vz * plane) / (u32)A.rx, vx = c.lin - vz * plane - vy * (u32)A.rx;
+            if (KIND == 0 || !(c.seg & 0x80000000u))
+                lvx_packed_point(f.face_in, f.bin_in, A.pk, (int)vx, (int)vy, (int)vz, pa);
+            if (KIND == 0 || (c.seg & 0x80000000u))
+                lvx_packed_point(f.face_out, f.bin_out, A.pk, (int)vx, (int)vy, (int)vz, pb);
+            rmeta = f.attr | (f.lid << 8);
+        } else {
+            const float4 ra = __ldg(reinterpret_cast<const float4 *>(A.rec + seg));
+            pa[0] = ra.x;
+            pa[1] = ra.y;
+            pa[2] = ra.z;
+            rmeta = __float_as_uint(ra.w);
+            if (KIND == 0 || (c.seg & 0x80000000u)) {
+                const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + seg) + 1);
+                pb[0] = rb.x;
+                pb[1] = rb.y;
+                pb[2] = rb.z;
+            }
+        }
         LvxHit h;
         bool hit;
         u32 kind3;
         float ccx = 0.0f, ccy = 0.0f, ccz = 0.0f;
         if (KIND == 0) {
-            const float4 rb = __ldg(reinterpret_cast<const float4 *>(A.rec + seg) + 1);
-            hit = lvx_tube_f32axis(ox, oy, oz, rdx, rdy, rdz, ra.x, ra.y, ra.z, rb.x, rb.y, rb.z, tube_r, h);
+            hit = lvx_tube_f32axis(ox, oy, oz, rdx, rdy, rdz, pa[0], pa[1], pa[2], pb[0], pb[1], pb[2], tube_r, h);
             kind3 = 0;
         } else {
-            float4 cc = ra;
-            kind3 = 1;
-            if (c.seg & 0x80000000u) {
-                cc = __ldg(reinterpret_cast<const float4 *>(A.rec + seg) + 1);
-                kind3 = 2;
-            }
-            hit = lvx_sphere<true>(ox, oy, oz, rdx, rdy, rdz, (double)cc.x, (double)cc.y, (double)cc.z, tube_r, h);
-            ccx = cc.x;
-            ccy = cc.y;
-            ccz = cc.z;
+            const bool end_b = (c.seg & 0x80000000u) != 0;
+            kind3 = end_b ? 2 : 1;
+            ccx = end_b ? pb[0] : pa[0];
+            ccy = end_b ? pb[1] : pa[1];
+            ccz = end_b ? pb[2] : pa[2];
+            hit = lvx_sphere<true>(ox, oy, oz, rdx, rdy, rdz, (double)ccx, (double)ccy, (double)ccz, tube_r, h);
         }
         // ownership (:838, :858, :878): a hit belongs to the window whose range holds its entry
         // parameter; the windows tile the walked range, so every hit entered inside the range
@@ -977,7 +1020,6 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_EXACT_MINB) wf_exact_kernel
             const double2 tr = A.item_t[c.aux];
             if (!(tr.x <= h.t_in && h.t_in < tr.y)) continue;
         }
-        const u32 rmeta = __float_as_uint(ra.w);
         const u32 attr = rmeta & 0xFFu, lid = (rmeta >> 8) & 31u;
         double scale, alpha;
         lvx_shade_hit<GEOM>(A, ox, oy, oz, rdx, rdy, rdz, h, attr, scale, alpha);
@@ -1729,6 +1771,23 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     const bool debug = tune.debug;
     const bool geom = params->shadow_mode == LVX_SHADOW_HARD || params->shadow_mode == LVX_SHADOW_REPLINES ||
                       params->ao_mode == LVX_AO_HEMISPHERE;
+    // straight from the encoded records when the caller passes no render records (the geometry
+    // secondary rays walk the render records themselves)
+    const bool packed = model->seg_rec_d == nullptr;
+    LVX_REQUIRE(!packed || (model->packed_d && !geom), "no render records: the encoded records are needed, and frames "
+                "with geometry secondary rays (hard / replines shadows, hemisphere AO) need lvx_seg_record");
+    if (packed) {
+        LVX_REQUIRE(model->n_bins >= 2 && model->n_bins <= 256 && (model->n_bins & (model->n_bins - 1)) == 0,
+                    "bad bin resolution %d of the encoded records", model->n_bins);
+        LVX_REQUIRE(((uintptr_t)model->packed_d & 7) == 0, "packed_d must be 8-byte aligned");
+        int lb = 0;
+        while ((1 << (lb + 1)) <= model->n_bins) ++lb;
+        A.pk.bytes = model->packed_d;
+        A.pk.lb = lb;
+        A.pk.n = model->n_bins;
+        A.pk.inv_n = 1.0f / (float)model->n_bins;
+        A.pk.width = (2 * (3 + 2 * lb) + 8 + 5 + 7) / 8;  // record_width, voxelizer.py:70-76
+    }
     cudaStream_t st = (cudaStream_t)stream;
     const int sms = lvx_sm_count();
     const int rays_mult = tune.rays_mult;
@@ -1754,13 +1813,16 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     }
             wf_walk_kernel<<<grid_rays, kThreadsWf, 0, st>>>(A, par);
             WF_DEBUG_SYNC("walk");
-            wf_cand_kernel<<<grid_q, kThreadsWf, 0, st>>>(A);
+            if (packed) wf_cand_kernel<true><<<grid_q, kThreadsWf, 0, st>>>(A);
+            else wf_cand_kernel<false><<<grid_q, kThreadsWf, 0, st>>>(A);
             WF_DEBUG_SYNC("candidates");
-            if (geom) wf_exact_kernel<0, true><<<grid_q, kThreadsWf, 0, st>>>(A, par);
-            else wf_exact_kernel<0, false><<<grid_q, kThreadsWf, 0, st>>>(A, par);
+            if (geom) wf_exact_kernel<0, true, false><<<grid_q, kThreadsWf, 0, st>>>(A, par);
+            else if (packed) wf_exact_kernel<0, false, true><<<grid_q, kThreadsWf, 0, st>>>(A, par);
+            else wf_exact_kernel<0, false, false><<<grid_q, kThreadsWf, 0, st>>>(A, par);
             WF_DEBUG_SYNC("exact<tube>");
-            if (params->joints && geom) wf_exact_kernel<1, true><<<grid_q, kThreadsWf, 0, st>>>(A, par);
-            else if (params->joints) wf_exact_kernel<1, false><<<grid_q, kThreadsWf, 0, st>>>(A, par);
+            if (params->joints && geom) wf_exact_kernel<1, true, false><<<grid_q, kThreadsWf, 0, st>>>(A, par);
+            else if (params->joints && packed) wf_exact_kernel<1, false, true><<<grid_q, kThreadsWf, 0, st>>>(A, par);
+            else if (params->joints) wf_exact_kernel<1, false, false><<<grid_q, kThreadsWf, 0, st>>>(A, par);
             WF_DEBUG_SYNC("exact<sphere>");
             wf_composite_kernel<<<grid_rays, kThreadsWf, 0, st>>>(A, par);
             WF_DEBUG_SYNC("composite");

@@ -464,6 +464,17 @@ def check_modes(params: RenderParams, model: VoxelModel, octree, replines=None):
         raise ValueError("precomputed AO requested but the model carries none")
 
 
+def default_records() -> str:
+    """What the wavefront engine reads segments from: LVX_RECORDS=auto|packed|rec.
+
+    "rec": the 32-byte render records (float32 endpoints, built by the voxelizer or decoded from
+    the encoded records).  "packed": the encoded records themselves (5 bytes per segment at N = 32,
+    decoded in the kernels -- SURVEY.md 8f row 1); the frame is byte-identical.  "auto": packed for a
+    model that carries only the encoded arrays (a .vxl file renders without any expansion), rec
+    otherwise.  Frames with geometry secondary rays and the tile engine always use "rec"."""
+    return os.environ.get("LVX_RECORDS", "auto")
+
+
 def default_engine() -> str:
     """Frame engine used when none is named: LVX_ENGINE=auto|tile|wavefront.
 
@@ -503,7 +514,7 @@ class FramePlan:
     def __init__(self, camera: Camera, model: VoxelModel, octree: Optional[DensityOctree],
                  params: RenderParams, neighbor: int, tile_first: int = 0, tile_step: int = 1,
                  compact: bool = False, tile_w: int = TILE_W, tile_h: int = TILE_H,
-                 engine: Optional[str] = None, replines=None):
+                 engine: Optional[str] = None, replines=None, records: Optional[str] = None):
         from .illumination import fibonacci_dirs_device
         check_modes(params, model, octree, replines)
         self.engine = engine or default_engine()
@@ -520,11 +531,23 @@ class FramePlan:
         self.par = params_struct(params, neighbor)
         geometry_rays = params.shadow_mode == "hard" or params.ao_mode == "hemisphere-geometry"
         self._rep = None
-        counts_d, offsets_d, rec_d, table_d, occ_d = model.device_view(need_occ=bool(neighbor) or geometry_rays)
+        records = records or default_records()
+        if records not in ("auto", "packed", "rec"):
+            raise ValueError(f"unknown record source {records!r}")
+        can_pack = self.engine == "wavefront" and not geometry_rays and params.shadow_mode != "replines" \
+            and model._has("packed")
+        self.records = "packed" if can_pack and (records == "packed" or
+                                                 (records == "auto" and not model.has_render_caches())) else "rec"
+        counts_d, offsets_d, rec_d, table_d, occ_d = model.device_view(
+            need_occ=bool(neighbor) or geometry_rays, need_rec=self.records == "rec")
+        packed_d = model.dev("packed") if self.records == "packed" else None
         m = _lib.Model()
         m.rx, m.ry, m.rz = model.spec.dims
+        m.n_bins = int(model.spec.bins_per_axis)
         m.counts_d, m.offsets_d = counts_d.data_ptr(), offsets_d.data_ptr()
-        m.seg_rec_d, m.table_d = rec_d.data_ptr(), table_d.data_ptr()
+        m.seg_rec_d = rec_d.data_ptr() if rec_d is not None else None
+        m.packed_d = packed_d.data_ptr() if packed_d is not None else None
+        m.table_d = table_d.data_ptr()
         m.nsum_d = occ_d[0].data_ptr() if occ_d is not None else None
         m.nmask_d = occ_d[1].data_ptr() if occ_d is not None else None
         m.ncell_d = occ_d[2].data_ptr() if occ_d is not None else None
@@ -547,7 +570,7 @@ class FramePlan:
         t.tile_w, t.tile_h = tile_w, tile_h
         t.tile_first, t.tile_step, t.compact = int(tile_first), int(tile_step), 1 if compact else 0
         self.til = t
-        self._keep = (counts_d, offsets_d, rec_d, table_d, occ_d, ao_d, dirs_d, octree, model)
+        self._keep = (counts_d, offsets_d, rec_d, packed_d, table_d, occ_d, ao_d, dirs_d, octree, model)
         self.width, self.height = int(camera.width), int(camera.height)
 
     def n_my_tiles(self) -> int:
@@ -589,6 +612,8 @@ class FramePlan:
 
     def launch_footprint(self, img_d, row_stats_d, voxel_bits_d):
         """Instrumented frame (bench.py): also marks every voxel whose header is read."""
+        if self.records != "rec":
+            raise ValueError("the footprint pass walks the render records: build the plan with records='rec'")
         _lib.check(_lib.lib().lvx_render_footprint(
             C.byref(self.cam), C.byref(self.mdl), C.byref(self.par), C.byref(self.lod),
             C.byref(self.til), _lib.ptr(img_d), _lib.ptr(row_stats_d), _lib.ptr(voxel_bits_d),

@@ -437,9 +437,16 @@ class VoxelModel:
         return int(voxel[0] + dx * (voxel[1] + dy * voxel[2]))
 
     # -- device-side render inputs --------------------------------------------------
-    def device_view(self, need_occ: bool = True):
+    def has_render_caches(self) -> bool:
+        """True when the per-segment arrays the 32-byte render records are built from are there
+        (a model built here, or one whose caches were decoded); False for a model that so far
+        carries only the encoded arrays (counts, offsets, packed), e.g. read from a .vxl file."""
+        return "seg_rec" in self._derived or all(self._has(k) for k in ("seg_a", "seg_b", "seg_attr", "seg_lid"))
+
+    def device_view(self, need_occ: bool = True, need_rec: bool = True):
         """(counts_d, offsets_d, seg_rec_d, table_d, (nsum_d, nmask_d, ncell_d)) -- the lvx_model
-        fields.  The neighbour grids (27-neighbourhood segment counts / occupancy bits
+        fields.  need_rec=False: the frame is rendered straight from the encoded records
+        (`dev("packed")`), seg_rec_d comes back None and nothing is expanded.  The neighbour grids (27-neighbourhood segment counts / occupancy bits
         over the padded grid; nsum > 0 is the reference's dilated occupancy map) are
         only needed in neighbour mode."""
         torch = _lib.require_device()
@@ -447,10 +454,10 @@ class VoxelModel:
         st = _lib.stream_ptr()
         d = self._derived
         S = self.segment_count
-        if "seg_rec" not in d and not all(self._has(k) for k in ("seg_a", "seg_b", "seg_attr", "seg_lid")):
-            # only the encoded arrays are there (e.g. a .vxl file): render straight from them
+        if need_rec and "seg_rec" not in d and not all(self._has(k) for k in ("seg_a", "seg_b", "seg_attr", "seg_lid")):
+            # only the encoded arrays are there (e.g. a .vxl file) and this caller walks render records
             d["seg_rec"] = self._decode_packed(caches=False)
-        if "seg_rec" not in d:
+        if need_rec and "seg_rec" not in d:
             rec = torch.empty((max(S, 1), 8), dtype=torch.float32, device="cuda")
             if S:
                 _lib.check(L.lvx_build_seg_records(
@@ -470,7 +477,7 @@ class VoxelModel:
             _lib.check(L.lvx_neighbor_sums(_lib.ptr(self.dev("counts")), _lib.i32x3(self.spec.dims),
                                            _lib.ptr(nsum), _lib.ptr(nmask), _lib.ptr(ncell), st))
             d["occ"] = (nsum, nmask, ncell)
-        return (self.dev("counts"), self.dev("offsets"), d["seg_rec"], d["table"], d.get("occ"))
+        return (self.dev("counts"), self.dev("offsets"), d.get("seg_rec") if need_rec else None, d["table"], d.get("occ"))
 
     def occupancy_dilated(self) -> np.ndarray:
         """The reference's `_occupancy_dilated` map (raycast.py:351-366): flat u8 over the

@@ -144,6 +144,35 @@ def test_c3_1080p_engines_are_byte_identical(lv, c3, kw):
     assert np.array_equal(sa, sb)
 
 
+def test_c3_rendered_straight_from_the_encoded_records(lv, c3):
+    """the wavefront engine decoding the 5-byte records in its kernels gives the
+    frame of the 32-byte render records, byte for byte (image and per-row counters), at full size;
+    and a model that carries only (counts, offsets, packed) renders WITHOUT being expanded."""
+    import torch
+    from paper_1801_01155_b200.raycast import FramePlan
+    _, m, oc = c3
+    cam = lv.default_camera(C3_DIMS, 1920, 1080)
+    for kw in (C3_KW, dict(C3_KW, shadow_mode="cone", light_dir=(0.3, 0.2, 1.0))):
+        p = lv.RenderParams(**kw)
+        out = {}
+        for rec in ("rec", "packed"):
+            plan = FramePlan(cam, m, oc, p, 1, engine="wavefront", records=rec)
+            assert plan.records == rec
+            img = torch.empty((1080, 1920, 4), dtype=torch.float32, device="cuda")
+            st = torch.zeros((1080, 3), dtype=torch.int64, device="cuda")
+            plan.launch(img, st)
+            torch.cuda.synchronize()
+            out[rec] = (img.cpu().numpy(), st.cpu().numpy())
+        assert np.array_equal(out["rec"][0], out["packed"][0]) and np.array_equal(out["rec"][1], out["packed"][1])
+    enc = lv.VoxelModel(spec=m.spec, counts=m.dev("counts"), offsets=m.dev("offsets"), packed=m.dev("packed"),
+                        transfer_table=m.transfer_table)
+    enc.ao = m.ao
+    fr = lv.render_frame(cam, enc, oc, None, lv.RenderParams(**C3_KW))
+    ref = lv.render_frame(cam, m, oc, None, lv.RenderParams(**C3_KW))
+    assert np.array_equal(fr.image, ref.image) and fr.stats["intersection_tests"] == ref.stats["intersection_tests"]
+    assert "seg_rec" not in enc._derived and not enc._has("seg_a")  # nothing was expanded
+
+
 def test_c3_own_voxel_vs_oracle_rows(lv, oracle, c3, c3_oracle):
     _, m, oc = c3
     ref, levels = c3_oracle

@@ -285,6 +285,40 @@ def test_model_from_encoded_arrays_only(lv, synth):
                       transfer_table=m.transfer_table).seg_a
 
 
+@pytest.mark.parametrize("n_bins", [4, 32, 128, 256])
+def test_packed_records_render_identically(lv, synth, n_bins):
+    """Every record width (4, 5, 6, 7 bytes): wavefront frames decoded from the encoded records in
+    the kernels == frames from the 32-byte render records, image and counters, in both modes."""
+    import torch
+    from paper_1801_01155_b200.raycast import FramePlan
+    dims = (14, 11, 9)
+    m = lv.build_voxel_model(lv.CurveSet.from_flat(*synth.turbulence(260, 50, dims)), lv.GridSpec(dims, n_bins))
+    oc = lv.build_lod(m)
+    m.ao = lv.precompute_voxel_ao(m, oc, lv.AOParams(n_rays=12, radius=3.0, step=1.0))
+    cam = lv.default_camera(dims, 160, 90)
+    for kw in (dict(base_opacity=0.3, neighbor_mode="on", ao_mode="precomputed"),
+               dict(base_opacity=0.3, neighbor_mode="off", joint_spheres=False),
+               dict(neighbor_mode="on", opacity_mode="distance-scaled", base_opacity=0.4, shadow_mode="cone",
+                    light_dir=(0.2, 0.4, 1.0))):
+        p = lv.RenderParams(**kw)
+        nb = 1 if kw["neighbor_mode"] == "on" else 0
+        res = []
+        for rec in ("rec", "packed"):
+            plan = FramePlan(cam, m, oc, p, nb, engine="wavefront", records=rec)
+            assert plan.records == rec
+            img = torch.empty((90, 160, 4), dtype=torch.float32, device="cuda")
+            st = torch.zeros((90, 3), dtype=torch.int64, device="cuda")
+            plan.launch(img, st)
+            torch.cuda.synchronize()
+            res.append((img.cpu().numpy(), st.cpu().numpy()))
+        assert np.array_equal(res[0][0], res[1][0]), kw
+        assert np.array_equal(res[0][1], res[1][1]), kw
+    # geometry secondary rays walk the render records: the plan falls back to them
+    plan = FramePlan(cam, m, oc, lv.RenderParams(shadow_mode="hard", light_dir=(0, 0, 1)), 1, engine="wavefront",
+                     records="packed")
+    assert plan.records == "rec"
+
+
 # --- error behaviour (SURVEY.md 8b) ------------------------------------------------------
 
 def test_error_conventions(lv, synth):

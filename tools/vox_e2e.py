@@ -34,3 +34,25 @@ for rep in range(3):
     out = vz.voxelize_device(pts_d, attrs_d, off_d, nc, spec)
     m = T("model_from_device", lambda: vz.model_from_device(out, spec, vz.default_transfer_table()))
     T("stage_clip", lambda: vz.stage_clip(pts_d, attrs_d, off_d, nc, spec, True))
+
+# --- where the time inside build_voxel_model goes: wrap its steps ---------------------------
+import time as _t
+acc = {}
+def wrap(mod, name):
+    f = getattr(mod, name)
+    def g(*a, **k):
+        torch.cuda.synchronize(); t0 = _t.perf_counter(); r = f(*a, **k); torch.cuda.synchronize()
+        acc[name] = acc.get(name, 0.0) + (_t.perf_counter() - t0) * 1e3
+        return r
+    setattr(mod, name, g)
+for n in ("stage_clip", "stage_scan", "stage_regroup", "stage_compact", "stage_provenance", "model_from_device", "voxelize_device"):
+    wrap(vz, n)
+wrap(_lib, "to_device")
+cs = lv.CurveSet.from_flat(pts, attrs, off)
+for rep in range(2):
+    acc.clear()
+    torch.cuda.synchronize(); t0 = _t.perf_counter()
+    m = lv.build_voxel_model(cs, spec)
+    torch.cuda.synchronize()
+    print("build_voxel_model %.2f ms:" % ((_t.perf_counter() - t0) * 1e3), {k: round(v, 2) for k, v in acc.items()})
+    del m
