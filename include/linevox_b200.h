@@ -171,6 +171,13 @@ int lvx_density_l0(const uint8_t *counts_d, const uint32_t *offsets_d,
                    const lvx_seg_record *seg_rec_d, const float *table_d, int64_t n_voxels,
                    float *level0_d, void *stream);
 
+/* The same for a grouping that is not the model's headers: uncapped u32 counts / offsets over records
+ * gathered into voxel order.  compute_density_level0 (lod.py:82-94) bins by `seg_voxel`, so a
+ * hand-assembled model whose seg_voxel disagrees with its headers (the reference's tests build
+ * such models, tests/test_lod.py:14-37) is binned the same way: stable sort by voxel, then this. */
+int lvx_density_l0_u32(const uint32_t *counts_d, const uint32_t *offsets_d, const lvx_seg_record *seg_rec_d,
+                       const float *table_d, int64_t n_voxels, float *level0_d, void *stream);
+
 /* Host helper: level offsets/dims of the flat octree buffer (_octree_args,
  * raycast.py:369-388).  off[n_levels+1], ldims[n_levels*3] as (dx,dy,dz). */
 int lvx_octree_layout(const int32_t dims[3], int64_t *off, int64_t *ldims, int32_t *n_levels);

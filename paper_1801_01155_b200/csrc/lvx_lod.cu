@@ -30,8 +30,9 @@ __device__ __forceinline__ double density_weight(const float4 a, const float4 b,
     return len * (double)s_sigma[__float_as_uint(a.w) & 0xFFu];
 }
 
+template <typename CountT>
 __global__ void __launch_bounds__(kDlThreads)
-density_l0_kernel(const u8 *__restrict__ counts, const u32 *__restrict__ offsets,
+density_l0_kernel(const CountT *__restrict__ counts, const u32 *__restrict__ offsets,
                   const lvx_seg_record *__restrict__ rec, const float *__restrict__ table,
                   i64 n_voxels, float *__restrict__ out) {
     constexpr unsigned FULL = 0xFFFFFFFFu;
@@ -43,7 +44,7 @@ density_l0_kernel(const u8 *__restrict__ counts, const u32 *__restrict__ offsets
     const i64 n_warps = ((i64)gridDim.x * blockDim.x) >> 5;
     for (i64 w = (((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5); w * 32 < n_voxels; w += n_warps) {
         const i64 v = w * 32 + lane;
-        const u32 n = v < n_voxels ? counts[v] : 0u;
+        const u32 n = v < n_voxels ? (u32)counts[v] : 0u;
         const unsigned occ = __ballot_sync(FULL, n != 0);
         if (occ == 0) {
             if (v < n_voxels) out[v] = 0.0f;
@@ -265,7 +266,20 @@ int lvx_density_l0(const uint8_t *counts_d, const uint32_t *offsets_d,
     const i64 warps = lvx_ceil_div(n_voxels, 32);
     const i64 blocks = lvx_ceil_div(warps, kDlThreads / 32);
     const i64 cap = (i64)lvx_sm_count() * 64;
-    density_l0_kernel<<<(unsigned)(blocks < cap ? blocks : cap), kDlThreads, 0, (cudaStream_t)stream>>>(
+    density_l0_kernel<u8><<<(unsigned)(blocks < cap ? blocks : cap), kDlThreads, 0, (cudaStream_t)stream>>>(
+        counts_d, offsets_d, seg_rec_d, table_d, n_voxels, level0_d);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_density_l0_u32(const uint32_t *counts_d, const uint32_t *offsets_d, const lvx_seg_record *seg_rec_d,
+                       const float *table_d, int64_t n_voxels, float *level0_d, void *stream) {
+    LVX_REQUIRE(counts_d && offsets_d && table_d && level0_d && n_voxels > 0, "bad arguments");
+    LVX_REQUIRE(((uintptr_t)seg_rec_d & 15) == 0, "seg_rec_d must be 16-byte aligned");
+    const i64 warps = lvx_ceil_div(n_voxels, 32);
+    const i64 blocks = lvx_ceil_div(warps, kDlThreads / 32);
+    const i64 cap = (i64)lvx_sm_count() * 64;
+    density_l0_kernel<u32><<<(unsigned)(blocks < cap ? blocks : cap), kDlThreads, 0, (cudaStream_t)stream>>>(
         counts_d, offsets_d, seg_rec_d, table_d, n_voxels, level0_d);
     LVX_LAUNCH_CHECK();
     return LVX_OK;

@@ -1773,9 +1773,10 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
                       params->ao_mode == LVX_AO_HEMISPHERE;
     // straight from the encoded records when the caller passes no render records (the geometry
     // secondary rays walk the render records themselves)
-    const bool packed = model->seg_rec_d == nullptr;
-    LVX_REQUIRE(!packed || (model->packed_d && !geom), "no render records: the encoded records are needed, and frames "
-                "with geometry secondary rays (hard / replines shadows, hemisphere AO) need lvx_seg_record");
+    // (a model without segments may pass neither: nothing is dereferenced)
+    const bool packed = model->seg_rec_d == nullptr && model->packed_d != nullptr;
+    LVX_REQUIRE(!packed || !geom, "frames with geometry secondary rays (hard / replines shadows, hemisphere AO) walk "
+                "the render records: pass lvx_seg_record");
     if (packed) {
         LVX_REQUIRE(model->n_bins >= 2 && model->n_bins <= 256 && (model->n_bins & (model->n_bins - 1)) == 0,
                     "bad bin resolution %d of the encoded records", model->n_bins);

@@ -98,13 +98,41 @@ def density_level0_device(model: VoxelModel, out=None):
     """Level-0 density as a device tensor f32[V] (no host copy); `out` may be the front of an
     octree buffer, so the mip chain reads it in place."""
     torch = _lib.require_device()
-    counts_d, offsets_d, rec_d, table_d, _ = model.device_view(need_occ=False)
     V = model.voxel_count
     if out is None:
         out = torch.empty(V, dtype=torch.float32, device="cuda")
+    if model.voxel_binning_is_external():
+        return _density_by_seg_voxel(model, out)
+    counts_d, offsets_d, rec_d, table_d, _ = model.device_view(need_occ=False)
     _lib.check(_lib.lib().lvx_density_l0(_lib.ptr(counts_d), _lib.ptr(offsets_d), _lib.ptr(rec_d),
                                          _lib.ptr(table_d), C.c_int64(V), _lib.ptr(out),
                                          _lib.stream_ptr()))
+    return out
+
+
+def _density_by_seg_voxel(model: VoxelModel, out):
+    """compute_density_level0 bins by `seg_voxel` (lod.py:90-93), not by the headers.  For a model
+    whose per-segment arrays were supplied by the caller the two need not agree, so the records are
+    put into voxel order with a STABLE sort (bincount adds a voxel's weights in segment order) and
+    summed by the same kernel over uncapped counts."""
+    torch = _lib.require_device()
+    V = model.voxel_count
+    dx, dy, _ = model.spec.dims
+    vox = model.dev("seg_voxel").to(torch.int64)
+    lin = vox[:, 0] + dx * (vox[:, 1] + dy * vox[:, 2])
+    order = torch.argsort(lin, stable=True)
+    S = int(lin.shape[0])
+    rec = torch.empty((max(S, 1), 8), dtype=torch.float32, device="cuda")
+    a, b = model.dev("seg_a")[order].contiguous(), model.dev("seg_b")[order].contiguous()
+    at, li = model.dev("seg_attr")[order].contiguous(), model.dev("seg_lid")[order].contiguous()
+    L, st = _lib.lib(), _lib.stream_ptr()
+    _lib.check(L.lvx_build_seg_records(_lib.ptr(a), _lib.ptr(b), _lib.ptr(at), _lib.ptr(li), C.c_int64(S),
+                                       _lib.ptr(rec), st))
+    counts = torch.bincount(lin, minlength=V)
+    offsets = (torch.cumsum(counts, 0) - counts).to(torch.int32)
+    table = _lib.to_device(np.ascontiguousarray(model.transfer_table, dtype=np.float32))
+    _lib.check(L.lvx_density_l0_u32(_lib.ptr(counts.to(torch.int32)), _lib.ptr(offsets), _lib.ptr(rec),
+                                    _lib.ptr(table), C.c_int64(V), _lib.ptr(out), st))
     return out
 
 

@@ -263,6 +263,7 @@ class VoxelModel:
         self._dev = {}
         self._derived = {}  # seg_rec, occ, table: device-only render inputs
         self._decoded = set()  # per-segment fields produced by _decode_packed (not user-supplied)
+        self._from_pipeline = False  # set by model_from_device: every array came out of the voxelizer
         self._ao = None
         for name, value in (("counts", counts), ("offsets", offsets), ("packed", packed),
                             ("seg_voxel", seg_voxel), ("seg_a", seg_a), ("seg_b", seg_b),
@@ -290,6 +291,8 @@ class VoxelModel:
             self._dev[name] = value
             self._host.pop(name, None)
         self._decoded.discard(name)  # now user-supplied
+        if name == "seg_voxel":
+            self._from_pipeline = False
         if name in _RENDER_INPUTS:
             self._derived.clear()
             self.__dict__.pop("_occ_dilated", None)
@@ -437,6 +440,13 @@ class VoxelModel:
         return int(voxel[0] + dx * (voxel[1] + dy * voxel[2]))
 
     # -- device-side render inputs --------------------------------------------------
+    def voxel_binning_is_external(self) -> bool:
+        """True when `seg_voxel` was handed in by the caller (not produced by the voxelizer or by
+        decoding `packed`): such a model's per-voxel grouping is whatever seg_voxel says, which is
+        what the reference's compute_density_level0 bins by (lod.py:90-93)."""
+        return (not self._from_pipeline) and self._has("seg_voxel") and "seg_voxel" not in self._decoded \
+            and self.segment_count > 0
+
     def has_render_caches(self) -> bool:
         """True when the per-segment arrays the 32-byte render records are built from are there
         (a model built here, or one whose caches were decoded); False for a model that so far
@@ -671,6 +681,7 @@ def model_from_device(out: dict, spec: GridSpec, transfer_table) -> "VoxelModel"
         seg_face_out=g("seg_face_out"), seg_bin_out=g("seg_bin_out"),
         dropped_overflow=out["dropped"], seg_curve=g("seg_curve"), seg_order=g("seg_order"))
     model._derived["seg_rec"] = out["seg_rec"]
+    model._from_pipeline = True
     return model
 
 

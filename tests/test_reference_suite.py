@@ -32,7 +32,8 @@ KNOWN = {
     # a numba-jitted helper of the TEST calls linevox._kernels.intersect_tube_raw from compiled code;
     # numba cannot call a Python-level stand-in (the same 100 000-pair comparison runs on the device
     # in tests/test_gpu_golden.py::test_tube_and_sphere_primitives against the reference's outputs)
-    "test_raycast.py::test_tube_matches_sampled_oracle": "numba-jitted test helper calls _kernels from compiled code",
+    "test_raycast.py::test_tube_against_sampled_bisection_oracle":
+        "numba-jitted test helper calls _kernels.intersect_tube_raw from compiled code",
 }
 
 CONFTEST = '''
