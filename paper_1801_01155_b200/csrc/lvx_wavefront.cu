@@ -242,30 +242,6 @@ __device__ __forceinline__ u32 queue_alloc(u32 *cnt, int q, u32 capq, u32 n, u32
     return (u32)q * capq + base;
 }
 
-// Allocate `n` consecutive entries for every lane that is converged here (any subset of the
-// warp): the lanes of the subset pass their counts round in lane order, one atomic per
-// subset.  `q` must be uniform over the subset.
-__device__ __forceinline__ u32 queue_alloc_n(u32 *cnt, int q, u32 capq, u32 n, u32 *err, u32 err_bit) {
-    const unsigned mask = __activemask();
-    const int lane = (int)(threadIdx.x & 31);
-    u32 pre = 0, total = 0;
-    for (unsigned m = mask; m; m &= m - 1) {
-        const int src = __ffs((int)m) - 1;
-        const u32 v = __shfl_sync(mask, n, src);
-        if (src < lane) pre += v;
-        total += v;
-    }
-    const int leader = __ffs((int)mask) - 1;
-    u32 base = 0;
-    if (lane == leader) base = atomicAdd(&cnt[q], total);
-    base = __shfl_sync(mask, base, leader);
-    if (base + pre + n > capq) {
-        atomicOr(err, err_bit);
-        return kNil;
-    }
-    return (u32)q * capq + base + pre;
-}
-
 // Allocate a + b entries (a, b in {0, 1}) for every lane that is converged here; one atomic
 // per warp.  `q` must be warp-uniform.  Returns the index of the lane's first entry or kNil.
 __device__ __forceinline__ u32 queue_alloc_bits(u32 *cnt, int q, u32 capq, bool a, bool b, u32 *err, u32 err_bit) {
@@ -476,11 +452,16 @@ struct WalkStage {
     u16 pre[kThreadsWf / 32][kWalkStage];  // items before record r (exclusive prefix of popc(fresh))
     u32 n[kThreadsWf / 32];
 };
+// own-voxel mode: the parameter range of the staged window (its one item is owned by that window alone)
+struct WalkStageT {
+    double2 t[kThreadsWf / 32][kWalkStage];
+};
 
 // all 32 lanes of the warp.  The staged windows are expanded to items so that CONSECUTIVE LANES
 // WRITE CONSECUTIVE ITEMS: every store instruction fills whole sectors (a lane that wrote the
 // items of "its" window one after the other touched a different sector per lane and store).
-__device__ __forceinline__ void walk_flush(const WfArgs &A, WalkStage &S, int warp, int lane, int q) {
+__device__ __forceinline__ void walk_flush(const WfArgs &A, WalkStage &S, const WalkStageT *ST, int warp, int lane,
+                                           int q) {
     constexpr unsigned FULL = 0xFFFFFFFFu;
     __syncwarp();
     const u32 n = min(S.n[warp], (u32)kWalkStage);
@@ -525,6 +506,8 @@ __device__ __forceinline__ void walk_flush(const WfArgs &A, WalkStage &S, int wa
                 A.item_lin[out0 + j] = (u32)((wx + bx_ - 1) + A.rx * ((wy + by_ - 1) + A.ry * (wz + bz_ - 1)));
                 // voxel-local float32 frame for the (conservative) pre-reject
                 A.item_q[out0 + j] = make_float4(w.qx - (float)(bx_ - 1), w.qy - (float)(by_ - 1), w.qz - (float)(bz_ - 1), 0.0f);
+                // own-voxel mode: only the window of the voxel itself gathers it (:797-799)
+                if (ST) A.item_t[out0 + j] = ST->t[warp][lo];
             }
         }
     }
@@ -549,7 +532,10 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_WALK_MINB) wf_walk_kernel(c
     const double cull = p.tube_r + kCullMarginWf;
     const double ox = A.cam.o[0], oy = A.cam.o[1], oz = A.cam.o[2];
     const size_t R = A.R;
-    __shared__ WalkStage S;
+    extern __shared__ __align__(16) unsigned char wf_walk_smem[];
+    WalkStage &S = *reinterpret_cast<WalkStage *>(wf_walk_smem);
+    // (the window ranges are staged only in own-voxel mode: the launch sizes the shared memory)
+    WalkStageT *ST = neighbor ? nullptr : reinterpret_cast<WalkStageT *>(wf_walk_smem + sizeof(WalkStage));
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (lane == 0) S.n[warp] = 0;
     __syncwarp();
@@ -642,7 +628,7 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_WALK_MINB) wf_walk_kernel(c
                             kw += 1;
                             const u32 fresh = nm & ~listed;
                             listed |= nm;
-                            if (fresh != 0 && neighbor) {
+                            if (fresh != 0) {
                                 const u32 pos = atomicAdd(&S.n[warp], 1u);  // (< kWalkStage: flushed below)
                                 WalkRec wr;
                                 wr.place = i;
@@ -654,18 +640,7 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_WALK_MINB) wf_walk_kernel(c
                                 wr.qz = (float)(p0z - (double)wz);
                                 wr.pad = 0.0f;
                                 S.rec[warp][pos] = wr;
-                            } else if (fresh != 0) {
-                                // own-voxel mode: one item, reserved in the global queue directly
-                                const u32 ib = queue_alloc_n(A.ctl->item_cnt, q, A.capq_item, 1u, &A.ctl->err, 1u);
-                                if (ib != kNil) {
-                                    A.item_place[ib] = i;
-                                    A.item_lin[ib] = (u32)(wx + rx * (wy + ry * wz));
-                                    // voxel-local float32 frame for the pre-reject
-                                    A.item_q[ib] = make_float4((float)(p0x - (double)wx), (float)(p0y - (double)wy),
-                                                               (float)(p0z - (double)wz), 0.0f);
-                                    // only the window of the voxel itself gathers it (:797-799)
-                                    A.item_t[ib] = make_double2(t0, t1);
-                                }
+                                if (ST) ST->t[warp][pos] = make_double2(t0, t1);
                             }
                         }
                     }
@@ -673,7 +648,7 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_WALK_MINB) wf_walk_kernel(c
             }
             __syncwarp();
             // every round adds at most one record per lane
-            if (S.n[warp] + 32u > (u32)kWalkStage) walk_flush(A, S, warp, lane, q);
+            if (S.n[warp] + 32u > (u32)kWalkStage) walk_flush(A, S, ST, warp, lane, q);
         }
         if (mine) {
             dda_store(rw, dda);
@@ -691,7 +666,7 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_WALK_MINB) wf_walk_kernel(c
             rd.t_lo = span0;
             A.rdir[i] = rd;
         }
-        walk_flush(A, S, warp, lane, q);
+        walk_flush(A, S, ST, warp, lane, q);
     }
 }
 
@@ -1794,6 +1769,15 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     const int rays_mult = tune.rays_mult;
     const unsigned grid_rays = (unsigned)(sms * rays_mult), grid_q = (unsigned)(sms * 8);
     A.ray_threads = grid_rays * (unsigned)kThreadsWf;
+    const size_t walk_smem = sizeof(WalkStage) + (params->neighbor ? 0 : sizeof(WalkStageT));
+    {
+        static bool attr_set = false;  // (more than 48 KB of dynamic shared memory is opt-in, once per process)
+        if (!attr_set) {
+            LVX_CUDA_CHECK(cudaFuncSetAttribute(wf_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)(sizeof(WalkStage) + sizeof(WalkStageT))));
+            attr_set = true;
+        }
+    }
     wf_begin_kernel<<<1, 64, 0, st>>>(A);
     wf_init_kernel<<<(unsigned)lvx_ceil_div(R, kThreadsWf), kThreadsWf, 0, st>>>(A);
     LVX_LAUNCH_CHECK();
@@ -1812,7 +1796,7 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
             return LVX_E_CUDA;                                                                \
         }                                                                                     \
     }
-            wf_walk_kernel<<<grid_rays, kThreadsWf, 0, st>>>(A, par);
+            wf_walk_kernel<<<grid_rays, kThreadsWf, walk_smem, st>>>(A, par);
             WF_DEBUG_SYNC("walk");
             if (packed) wf_cand_kernel<true><<<grid_q, kThreadsWf, 0, st>>>(A);
             else wf_cand_kernel<false><<<grid_q, kThreadsWf, 0, st>>>(A);

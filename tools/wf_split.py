@@ -14,7 +14,9 @@ for r in rows[hi + 1:]:
         cur = []
     cur.append((name, v))
 frames.append(cur)
-f = frames[1] if len(frames) > 1 else frames[0]
+fi = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+f = frames[fi] if len(frames) > fi else frames[0]
+print("frames:", len(frames), "showing", fi)
 tot = collections.OrderedDict(); it = 0; line = []
 for name, v in f:
     tot[name] = tot.get(name, 0) + v
