@@ -81,6 +81,7 @@ struct __align__(32) WfHit {
 };
 static_assert(sizeof(WfHit) == 32, "hit record is one sector");
 constexpr unsigned long long kDroppedBit = 1ull << 63;
+constexpr u32 kJointRef = 0x80000000u;  // flag on a sorted hit reference: the hit is a joint sphere
 __device__ __forceinline__ u32 hit_lin(unsigned long long k) { return (u32)(k >> 24) & 0x7FFFFFFFu; }
 __device__ __forceinline__ u32 hit_lid(unsigned long long k) { return (u32)(k >> 19) & 31u; }
 __device__ __forceinline__ u32 hit_kind3(unsigned long long k) { return (u32)(k >> 8) & 3u; }
@@ -1044,6 +1045,9 @@ struct WfTables {
     }
 };
 
+#ifndef LVX_WF_COMP_PIPE
+#define LVX_WF_COMP_PIPE 1
+#endif
 struct WfPixel {
     double acc[4];
     u32 n_seen, n_sph;
@@ -1080,6 +1084,8 @@ __device__ __forceinline__ void wf_accumulate(const WfArgs &A, WfTables &T, WfPi
         const u32 bit = 1u << lid;
         const unsigned long long kb = 1ull << ((lin * 0x9E3779B1u) >> 26);
         bool found = false;
+        // (measured and dropped: keeping the entry touched last in registers -- the three primitives of
+        // a segment ask for the same one -- costs more in register pressure than the loads it saves)
         if (S.seen_bloom & kb) {
             for (int i = (int)S.n_seen - 1; i >= 0; --i) {
                 uint2 *ep = T.seen(i);
@@ -1182,17 +1188,20 @@ __device__ void wf_apply_window_cap(const WfArgs &A, const WfRayHits &H, const W
     }
 }
 
+__device__ __forceinline__ bool wf_composite_hit(const WfArgs &A, WfTables &T, WfPixel &S, const WfHit &h,
+                                                 const float4 c, double tau) {
+    WF_STAT(1, 1);
+    wf_accumulate(A, T, S, h.scale, h.alpha, hit_lin(h.key2), hit_lid(h.key2), hit_attr(h.key2),
+                  hit_kind3(h.key2) != 0, c.x, c.y, c.z);
+    return S.acc[3] >= tau;
+}
 __device__ __forceinline__ bool wf_composite_one(const WfArgs &A, WfTables &T, WfPixel &S, const WfRayHits &H,
                                                  u32 ref, double tau, double &t_in) {
-    WF_STAT(1, 1);
     const WfHit h = wf_load_hit(H.at(ref));
     t_in = h.t_in;
-    const bool is_sphere = hit_kind3(h.key2) != 0;
     float4 c = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-    if (is_sphere) c = H.centre(ref);
-    wf_accumulate(A, T, S, h.scale, h.alpha, hit_lin(h.key2), hit_lid(h.key2), hit_attr(h.key2), is_sphere, c.x, c.y,
-                  c.z);
-    return S.acc[3] >= tau;
+    if (hit_kind3(h.key2) != 0) c = H.centre(ref);
+    return wf_composite_hit(A, T, S, h, c, tau);
 }
 
 #ifndef LVX_WF_LIGHT
@@ -1276,7 +1285,7 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_ker
                 }
                 s_t[pos] = t;
                 s_k[pos] = k2;
-                order[pos] = ref;
+                order[pos] = ref | (((k2 >> 18) & 1ull) ? kJointRef : 0u);
             }
         }
         __syncwarp();
@@ -1309,7 +1318,8 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_ker
                 const unsigned long long k2 = Q.k[warp][j];
                 u32 rank = 0;
                 for (u32 q = 0; q < m; ++q) rank += wf_before(Q.t[warp][q], Q.k[warp][q], t, k2) ? 1u : 0u;
-                Q.out[warp][rank] = Q.ref[warp][j];  // (keys are unique: a permutation)
+                // (keys are unique: a permutation)
+                Q.out[warp][rank] = Q.ref[warp][j] | (((k2 >> 18) & 1ull) ? kJointRef : 0u);
             }
             __syncwarp();
             if (lane == L) {
@@ -1334,14 +1344,41 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_ker
             WfTables T = {A, slot, rp.ovf};
             double term_t = 0.0;
             if (nhit <= (u32)kSortCap) {
+#if LVX_WF_COMP_PIPE
+                // the record (and joint centre) of hit j + 1 is in flight while hit j is composited
+                WfHit hc;
+                float4 cc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                if (n > 0) {
+                    const u32 r0 = order[0];
+                    hc = wf_load_hit(H.at(r0 & ~kJointRef));
+                    if (r0 & kJointRef) cc = H.centre(r0 & ~kJointRef);
+                }
+                for (int j = 0; j < n; ++j) {
+                    WfHit hn = hc;
+                    float4 cn = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                    if (j + 1 < n) {
+                        const u32 r1 = order[j + 1];
+                        hn = wf_load_hit(H.at(r1 & ~kJointRef));
+                        if (r1 & kJointRef) cn = H.centre(r1 & ~kJointRef);
+                    }
+                    if (wf_composite_hit(A, T, S, hc, cc, tau)) {
+                        terminated = true;
+                        term_t = hc.t_in;
+                        break;
+                    }
+                    hc = hn;
+                    cc = cn;
+                }
+#else
                 for (int j = 0; j < n; ++j) {
                     double t_hit;
-                    if (wf_composite_one(A, T, S, H, order[j], tau, t_hit)) {
+                    if (wf_composite_one(A, T, S, H, order[j] & ~kJointRef, tau, t_hit)) {
                         terminated = true;
                         term_t = t_hit;
                         break;
                     }
                 }
+#endif
             } else {
                 // more hits than the buffers hold: selection instead of sorting --
                 // repeatedly take the smallest key after the last composited one
@@ -1515,7 +1552,7 @@ WfLayout wf_layout(i64 R, double scale) {
     L.cap_win = (u32)fmin(4.0e9, (double)R * (double)kWinFirst);  // every ray may record kWinFirst windows in iteration 0
     L.capq_item = (u32)fmin(4.0e9 / kNQ, ((double)R * 24.0 * f + 65536.0) / kNQ);
     L.capq_surv = (u32)fmin(4.0e9 / kNQ, ((double)R * 10.0 * f + 65536.0) / kNQ);
-    L.capq_hit = (u32)fmin(4.0e9 / kNQ, ((double)R * 2.0 * f + 65536.0) / kNQ);
+    L.capq_hit = (u32)fmin(2.0e9 / kNQ, ((double)R * 2.0 * f + 65536.0) / kNQ);  // (references keep bit 31 free)
     size_t c = 0;
     const size_t r = (size_t)R, po = (size_t)L.pool_cap * (LVX_MAX_SEEN - kInline);
     L.ctl = take(c, sizeof(WfCtl));
