@@ -236,3 +236,91 @@ def test_density_probes(lv):
     from paper_1801_01155_b200 import _lib
     assert np.array_equal(_lib.fibonacci_dirs(25, 1), g["fib25_hemi"])
     assert np.array_equal(_lib.fibonacci_dirs(100, 0), g["fib100_sphere"])
+
+
+# --- the reference's small operations over the device probes (round 2) -------------------------------
+
+def test_clip_batch_device_matches_reference():
+    """_clip_batch (voxelizer.py:213-263) on the device, float64 outputs and all: the adversarial
+    lattice fixture (exact plane hits, reversals, corner crossings, out-of-grid excursions)."""
+    from paper_1801_01155_b200.voxelizer import clip_batch_device
+    g = golden("clip_lattice")
+    vox, p_in, p_out, a_in, a_out, key = clip_batch_device(g["pts"], g["attrs"], g["off"], tuple(int(d) for d in g["dims"]))
+    assert np.array_equal(vox, g["vox"]) and np.array_equal(p_in, g["p_in"]) and np.array_equal(p_out, g["p_out"])
+    assert np.array_equal(a_in, g["a_in"]) and np.array_equal(a_out, g["a_out"])
+    assert np.all(np.diff(key.astype(np.int64)) > 0)  # (edge, ordinal) keys strictly increase in reference order
+
+
+def test_clip_curve_to_voxels_kats():
+    """reference tests/test_voxelizer.py:209-235: axis-aligned chord, same-voxel curve, bridged vertices."""
+    import paper_1801_01155_b200 as lv
+    spec = lv.GridSpec((4, 4, 4), 8)
+    segs = lv.clip_curve_to_voxels(lv.Curve(points=np.array([[0.5, 0.5, 0.5], [2.5, 0.5, 0.5]]), attrs=np.array([0.0, 1.0])), spec)
+    assert len(segs) == 1 and segs[0].voxel == (1, 0, 0)
+    assert np.array_equal(segs[0].entry, [1.0, 0.5, 0.5]) and np.array_equal(segs[0].exit, [2.0, 0.5, 0.5])
+    assert segs[0].attr_entry == 0.25 and segs[0].attr_exit == 0.75
+    assert lv.clip_curve_to_voxels(lv.Curve(points=np.array([[1.2, 1.2, 1.2], [1.7, 1.4, 1.9]]), attrs=np.array([0.0, 1.0])), spec) == []
+    segs = lv.clip_curve_to_voxels(lv.Curve(points=np.array([[0.5, 0.5, 0.5], [1.3, 0.6, 0.5], [1.6, 0.4, 0.5], [2.5, 0.5, 0.5]]),
+                                            attrs=np.linspace(0, 1, 4)), spec)
+    assert len(segs) == 1 and segs[0].voxel == (1, 0, 0)  # interior vertices inside one voxel are bridged
+
+
+def test_shade_local_matches_reference():
+    """shade_scalar (_kernels.py:316-329): CUDA's pow is within 2 ulp of glibc's."""
+    from paper_1801_01155_b200.raycast import probe_shade
+    import paper_1801_01155_b200 as lv
+    g = golden("prim_shade")
+    got = probe_shade(np.concatenate([g["n"], g["l"], g["v"]], axis=1), 0.2, 0.7, 0.3, 32.0)
+    assert np.allclose(got, g["shade"], rtol=1e-14, atol=0.0)
+    assert (got != g["shade"]).mean() < 0.2
+    assert lv.shade_local(g["n"][0], g["l"][0], g["v"][0]) == got[0]
+
+
+def test_composite_and_gather_reference_ops():
+    """reference tests/test_raycast.py:283-288, 324-388: white/black at alpha .5; hits of a voxel in order."""
+    import paper_1801_01155_b200 as lv
+    p = lv.RenderParams(base_opacity=0.5, tau=1.0, ambient=1.0, diffuse=0.0, specular=0.0, background=(0, 0, 0, 1))
+    table = np.ones((256, 4), np.float32)
+    table[0, :3] = 0.0
+    hits = [lv.HitRecord(t_in=1.0, t_out=2.0, normal=np.array([0.0, 0.0, -1.0]), attr_index=255),
+            lv.HitRecord(t_in=3.0, t_out=4.0, normal=np.array([0.0, 0.0, -1.0]), attr_index=0)]
+    assert np.allclose(lv.composite(hits, p, table), [0.5, 0.5, 0.5, 1.0])
+    dims = (4, 4, 4)
+    cs = lv.CurveSet.from_curves([lv.Curve(points=np.array([[0.2, 1.5, 1.5], [3.8, 1.5, 1.5]]), attrs=np.array([0.0, 1.0]))])
+    m = lv.build_voxel_model(cs, lv.GridSpec(dims, 32))
+    ray = (np.array([1.5, 1.5, -2.0]), np.array([0.0, 0.0, 1.0]))
+    got = lv.gather_voxel_hits(ray, (1, 1, 1), m, lv.RenderParams(neighbor_mode="on"))
+    assert [h.kind for h in got] == ["tube"] and got[0].voxel == (1, 1, 1) and abs(got[0].t_in - 3.2) < 1e-6
+    assert lv.gather_voxel_hits(ray, (1, 1, 1), m, lv.RenderParams(neighbor_mode="on"), seen={21: 1}) == []
+
+
+def test_representative_line_probe_equals_level_kernel():
+    """representative_line (lod.py:141-169) through its probe == what the level kernel computed for
+    the same members (children in z,y,x order, each child's segments in stored order)."""
+    import paper_1801_01155_b200 as lv
+    v = golden("vox_turbulence")
+    dims = tuple(int(d) for d in v["dims"])
+    m = lv.build_voxel_model(lv.CurveSet.from_flat(v["pts"], v["attrs"], v["off"]), lv.GridSpec(dims, int(v["n_bins"])))
+    rep = lv.build_rep_lines(m, lv.build_lod(m), adjacency=False)
+    lvl = rep.levels[1]
+    pdx, pdy, pdz = lvl.dims
+    checked = 0
+    for plin in np.nonzero(lvl.valid)[0][:12]:
+        px, py, pz = plin % pdx, (plin // pdx) % pdy, plin // (pdx * pdy)
+        a, b = [], []
+        for dz in range(2):
+            for dy in range(2):
+                for dx in range(2):
+                    x, y, z = 2 * px + dx, 2 * py + dy, 2 * pz + dz
+                    if x >= dims[0] or y >= dims[1] or z >= dims[2]:
+                        continue
+                    lin = x + dims[0] * (y + dims[1] * z)
+                    o, c = int(m.offsets[lin]), int(m.counts[lin])
+                    a += [m.seg_a[o:o + c]]
+                    b += [m.seg_b[o:o + c]]
+        qa, qb, w = lv.representative_line(np.concatenate(a), np.concatenate(b), (2.0 * px, 2.0 * py, 2.0 * pz), 2.0,
+                                           int(v["n_bins"]))
+        assert np.array_equal(qa.astype(np.float32), lvl.a[plin]) and np.array_equal(qb.astype(np.float32), lvl.b[plin])
+        assert np.float32(w) == lvl.weight[plin]
+        checked += 1
+    assert checked > 0
