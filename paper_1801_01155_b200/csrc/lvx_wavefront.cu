@@ -929,8 +929,12 @@ __device__ __forceinline__ WfHit wf_load_hit(const WfHit *p) {
 #ifndef LVX_WF_EXACT_MINB
 #define LVX_WF_EXACT_MINB 4
 #endif
+#ifndef LVX_WF_EXACT_THREADS
+#define LVX_WF_EXACT_THREADS 256
+#endif
+constexpr int kThreadsExact = LVX_WF_EXACT_THREADS;
 template <int KIND, bool GEOM, bool PACKED>
-__global__ void __launch_bounds__(kThreadsWf, LVX_WF_EXACT_MINB) wf_exact_kernel(const WfArgs A, int par) {
+__global__ void __launch_bounds__(kThreadsExact, LVX_WF_EXACT_MINB) wf_exact_kernel(const WfArgs A, int par) {
     __shared__ QueueView V;
     queue_view_load(V, KIND == 0 ? A.ctl->tube_cnt : A.ctl->sph_cnt, A.capq_surv, A.ctl->err);
     const u32 total = V.pre[kNQ];
@@ -1208,6 +1212,7 @@ __device__ __forceinline__ bool wf_composite_one(const WfArgs &A, WfTables &T, W
 #define LVX_WF_LIGHT 8
 #endif
 constexpr int kLight = LVX_WF_LIGHT;  // up to this many hits a ray orders by itself; more are ranked by its warp
+static_assert(kLight <= kHitSlots && kHitSlots <= 255, "a light ray's hits are all in slots, and a slot index fits 8 bits");
 
 struct SortStage {
     double t[kThreadsWf / 32][kSortCap];
@@ -1222,6 +1227,12 @@ struct SortStage {
 __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_kernel(const WfArgs A, int par) {
     constexpr unsigned FULL = 0xFFFFFFFFu;
     __shared__ SortStage Q;
+    // sort buffers of the rays with few hits, one column per thread ([entry][thread]: conflict-free).
+    // In shared memory because thread-local arrays indexed at run time live in local memory, and
+    // the insertion sort's stores were a third of this kernel's L2 write traffic.
+    __shared__ double L_t[kLight][kThreadsWf];
+    __shared__ unsigned long long L_k[kLight][kThreadsWf];  // key2 with the hit's slot in its low 8 bits
+    const int tid = threadIdx.x;
     const u32 n_live = A.ctl->err ? 0u : A.ctl->n_live[par];
     const u32 wn = A.ctl->wn;
     const size_t R = A.R;
@@ -1266,26 +1277,24 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_ker
         // ---- order the hits: (t_in, key2) ---------------------------------------------------
         u32 order[kSortCap];
         int n = 0;
-        if (nhit && nhit <= (u32)kLight) {
-            // few hits: insertion sort by the ray's own thread
-            double s_t[kLight];
-            unsigned long long s_k[kLight];
+        const bool light = nhit <= (u32)kLight;
+        if (nhit && light) {
+            // few hits (all of them in slots: kLight <= kHitSlots): insertion sort by the ray's own thread
             for (u32 ref = H.first(); ref != kNil; ref = H.next(ref)) {
                 const WfHit *hp = H.at(ref);
                 if (big && (hp->key2 & kDroppedBit)) continue;  // dropped by the window cap
                 const double2 v = *reinterpret_cast<const double2 *>(hp);
                 const double t = v.x;
-                const unsigned long long k2 = (unsigned long long)__double_as_longlong(v.y);
+                // (the low 8 bits -- attr -- are not part of the order: they carry the slot here)
+                const unsigned long long k2 = ((unsigned long long)__double_as_longlong(v.y) & ~0xFFull) | ref;
                 int pos = n++;
-                while (pos > 0 && wf_before(t, k2, s_t[pos - 1], s_k[pos - 1])) {
-                    s_t[pos] = s_t[pos - 1];
-                    s_k[pos] = s_k[pos - 1];
-                    order[pos] = order[pos - 1];
+                while (pos > 0 && wf_before(t, k2, L_t[pos - 1][tid], L_k[pos - 1][tid])) {
+                    L_t[pos][tid] = L_t[pos - 1][tid];
+                    L_k[pos][tid] = L_k[pos - 1][tid];
                     --pos;
                 }
-                s_t[pos] = t;
-                s_k[pos] = k2;
-                order[pos] = ref | (((k2 >> 18) & 1ull) ? kJointRef : 0u);
+                L_t[pos][tid] = t;
+                L_k[pos][tid] = k2;
             }
         }
         __syncwarp();
@@ -1328,6 +1337,12 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_ker
             }
             __syncwarp();
         }
+        // reference (slot or pool entry, | kJointRef for a joint sphere) of the j-th hit in order
+        auto sorted_ref = [&](int j) -> u32 {
+            if (!light) return order[j];
+            const unsigned long long k2 = L_k[j][tid];
+            return (u32)(k2 & 0xFFull) | (((k2 >> 18) & 1ull) ? kJointRef : 0u);
+        };
         // ---- composite ----------------------------------------------------------------------
         WfRayPix rp;
         if (nhit) {
@@ -1349,7 +1364,7 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_ker
                 WfHit hc;
                 float4 cc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
                 if (n > 0) {
-                    const u32 r0 = order[0];
+                    const u32 r0 = sorted_ref(0);
                     hc = wf_load_hit(H.at(r0 & ~kJointRef));
                     if (r0 & kJointRef) cc = H.centre(r0 & ~kJointRef);
                 }
@@ -1357,7 +1372,7 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_ker
                     WfHit hn = hc;
                     float4 cn = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
                     if (j + 1 < n) {
-                        const u32 r1 = order[j + 1];
+                        const u32 r1 = sorted_ref(j + 1);
                         hn = wf_load_hit(H.at(r1 & ~kJointRef));
                         if (r1 & kJointRef) cn = H.centre(r1 & ~kJointRef);
                     }
@@ -1372,7 +1387,7 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_ker
 #else
                 for (int j = 0; j < n; ++j) {
                     double t_hit;
-                    if (wf_composite_one(A, T, S, H, order[j] & ~kJointRef, tau, t_hit)) {
+                    if (wf_composite_one(A, T, S, H, sorted_ref(j) & ~kJointRef, tau, t_hit)) {
                         terminated = true;
                         term_t = t_hit;
                         break;
@@ -1822,7 +1837,9 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     int it = 0;
     g_last_launches = 2;
     for (;;) {
-        const int burst = it == 0 ? 6 : 3;
+        // bursts of six iterations between looks at the live-ray count: a frame like C3 (10 iterations)
+        // costs one host read-back instead of three; an iteration without rays is six empty launches
+        const int burst = 6;
         for (int b = 0; b < burst; ++b, ++it) {
             const int par = it & 1;
 #define WF_DEBUG_SYNC(name)                                                                   \
@@ -1838,13 +1855,13 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
             if (packed) wf_cand_kernel<true><<<grid_q, kThreadsWf, 0, st>>>(A);
             else wf_cand_kernel<false><<<grid_q, kThreadsWf, 0, st>>>(A);
             WF_DEBUG_SYNC("candidates");
-            if (geom) wf_exact_kernel<0, true, false><<<grid_q, kThreadsWf, 0, st>>>(A, par);
-            else if (packed) wf_exact_kernel<0, false, true><<<grid_q, kThreadsWf, 0, st>>>(A, par);
-            else wf_exact_kernel<0, false, false><<<grid_q, kThreadsWf, 0, st>>>(A, par);
+            if (geom) wf_exact_kernel<0, true, false><<<grid_q, kThreadsExact, 0, st>>>(A, par);
+            else if (packed) wf_exact_kernel<0, false, true><<<grid_q, kThreadsExact, 0, st>>>(A, par);
+            else wf_exact_kernel<0, false, false><<<grid_q, kThreadsExact, 0, st>>>(A, par);
             WF_DEBUG_SYNC("exact<tube>");
-            if (params->joints && geom) wf_exact_kernel<1, true, false><<<grid_q, kThreadsWf, 0, st>>>(A, par);
-            else if (params->joints && packed) wf_exact_kernel<1, false, true><<<grid_q, kThreadsWf, 0, st>>>(A, par);
-            else if (params->joints) wf_exact_kernel<1, false, false><<<grid_q, kThreadsWf, 0, st>>>(A, par);
+            if (params->joints && geom) wf_exact_kernel<1, true, false><<<grid_q, kThreadsExact, 0, st>>>(A, par);
+            else if (params->joints && packed) wf_exact_kernel<1, false, true><<<grid_q, kThreadsExact, 0, st>>>(A, par);
+            else if (params->joints) wf_exact_kernel<1, false, false><<<grid_q, kThreadsExact, 0, st>>>(A, par);
             WF_DEBUG_SYNC("exact<sphere>");
             wf_composite_kernel<<<grid_rays, kThreadsWf, 0, st>>>(A, par);
             WF_DEBUG_SYNC("composite");
