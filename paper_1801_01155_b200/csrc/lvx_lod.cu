@@ -11,7 +11,8 @@ namespace {
 // Level-0 density.  np.bincount with weights is a sequential float64 accumulation of the
 // per-segment products length * sigma in stored order, one cast to float32 (lod.py:87-94).
 //
-// A warp owns 32 consecutive voxels.  Their records are one contiguous span of the record array
+// A warp owns 128 consecutive voxels per round (four per lane, interleaved so that the header loads
+// coalesce).  Their records are one contiguous span of the record array
 // (headers are exclusive prefix sums in voxel scan order), so the lanes load the span together --
 // one 32-byte record per lane and round, every sector used once, all loads independent -- and
 // leave the float64 products in shared memory; each lane then adds up the products of ITS voxel in
@@ -30,6 +31,8 @@ __device__ __forceinline__ double density_weight(const float4 a, const float4 b,
     return len * (double)s_sigma[__float_as_uint(a.w) & 0xFFu];
 }
 
+constexpr int kDlVox = 4;  // voxels per lane and round: amortises the per-round scan over 128 voxels
+
 template <typename CountT>
 __global__ void __launch_bounds__(kDlThreads)
 density_l0_kernel(const CountT *__restrict__ counts, const u32 *__restrict__ offsets,
@@ -42,44 +45,97 @@ density_l0_kernel(const CountT *__restrict__ counts, const u32 *__restrict__ off
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const i64 n_warps = ((i64)gridDim.x * blockDim.x) >> 5;
-    for (i64 w = (((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5); w * 32 < n_voxels; w += n_warps) {
-        const i64 v = w * 32 + lane;
-        const u32 n = v < n_voxels ? (u32)counts[v] : 0u;
-        const unsigned occ = __ballot_sync(FULL, n != 0);
-        if (occ == 0) {
-            if (v < n_voxels) out[v] = 0.0f;
+    const i64 per_round = 32 * kDlVox;
+    const bool aligned32 = (reinterpret_cast<uintptr_t>(rec) & 31) == 0;
+    for (i64 w = (((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5); w * per_round < n_voxels; w += n_warps) {
+        // lane owns voxels v0 + k * 32 + lane, k = 0 .. kDlVox - 1 (every load below is coalesced)
+        const i64 v0 = w * per_round + lane;
+        u32 n[kDlVox], off[kDlVox], first[kDlVox];
+        unsigned any = 0;
+        // counts AND offsets in one round trip (the offsets of empty voxels are loaded and ignored:
+        // their sectors are fetched for the occupied neighbours anyway); the headers of the warp's
+        // next round are requested now
+#pragma unroll
+        for (int k = 0; k < kDlVox; ++k) {
+            const i64 v = v0 + 32 * k;
+            n[k] = v < n_voxels ? (u32)counts[v] : 0u;
+            off[k] = v < n_voxels ? offsets[v] : 0u;
+            any |= n[k];
+            const i64 vn = v + n_warps * per_round;
+            if (vn < n_voxels && (lane & 7) == 0) {
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(offsets + vn));
+                if (lane == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(counts + vn));
+            }
+        }
+        if (!__any_sync(FULL, any != 0)) {
+#pragma unroll
+            for (int k = 0; k < kDlVox; ++k)
+                if (v0 + 32 * k < n_voxels) out[v0 + 32 * k] = 0.0f;
             continue;
         }
-        const u32 off = n ? offsets[v] : 0u;
-        u32 inc = n;
+        u32 total = 0, base = 0;
+        bool have_base = false;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const u32 t = __shfl_up_sync(FULL, inc, o);
-            if (lane >= o) inc += t;
+        for (int k = 0; k < kDlVox; ++k) {
+            u32 inc = n[k];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const u32 t = __shfl_up_sync(FULL, inc, o);
+                if (lane >= o) inc += t;
+            }
+            first[k] = total + inc - n[k];  // my records of voxel k are [first, first + n) of the span
+            total += __shfl_sync(FULL, inc, 31);
+            const unsigned occ = __ballot_sync(FULL, n[k] != 0);
+            if (!have_base && occ) {
+                base = __shfl_sync(FULL, off[k], __ffs((int)occ) - 1);
+                have_base = true;
+            }
         }
-        const u32 total = __shfl_sync(FULL, inc, 31);
-        const u32 first = inc - n;  // my records are [first, first + n) of the span
-        const u32 base = __shfl_sync(FULL, off, __ffs((int)occ) - 1);
-        const bool contiguous = __all_sync(FULL, n == 0 || off == base + first);
-        double acc = 0.0;
+        bool mine_ok = true;
+#pragma unroll
+        for (int k = 0; k < kDlVox; ++k) mine_ok = mine_ok && (n[k] == 0 || off[k] == base + first[k]);
+        const bool contiguous = __all_sync(FULL, mine_ok);
+        double acc[kDlVox];
+#pragma unroll
+        for (int k = 0; k < kDlVox; ++k) acc[k] = 0.0;
         if (contiguous) {
             const float4 *r = reinterpret_cast<const float4 *>(rec + base);
             for (u32 j0 = 0; j0 < total; j0 += kDlChunk) {
                 const u32 m = min((u32)kDlChunk, total - j0);
                 for (u32 j = lane; j < m; j += 32) {
-                    const float4 a = __ldg(r + 2 * (size_t)(j0 + j)), b = __ldg(r + 2 * (size_t)(j0 + j) + 1);
+                    float4 a, b;
+                    if (aligned32) {
+                        // one 256-bit load per record: every sector of the span is requested once
+                        u64 q0, q1, q2, q3;
+                        lvx_ld256(r + 2 * (size_t)(j0 + j), q0, q1, q2, q3);
+                        a = make_float4(__uint_as_float((u32)q0), __uint_as_float((u32)(q0 >> 32)), __uint_as_float((u32)q1),
+                                        __uint_as_float((u32)(q1 >> 32)));
+                        b = make_float4(__uint_as_float((u32)q2), __uint_as_float((u32)(q2 >> 32)), __uint_as_float((u32)q3),
+                                        __uint_as_float((u32)(q3 >> 32)));
+                    } else {
+                        a = __ldg(r + 2 * (size_t)(j0 + j));
+                        b = __ldg(r + 2 * (size_t)(j0 + j) + 1);
+                    }
                     s_w[warp][j] = density_weight(a, b, s_sigma);
                 }
                 __syncwarp();
-                const u32 lo = max(first, j0), hi = min(first + n, j0 + m);
-                for (u32 k = lo; k < hi; ++k) acc += s_w[warp][k - j0];
+#pragma unroll
+                for (int k = 0; k < kDlVox; ++k) {
+                    const u32 lo = max(first[k], j0), hi = min(first[k] + n[k], j0 + m);
+                    for (u32 q = lo; q < hi; ++q) acc[k] += s_w[warp][q - j0];
+                }
                 __syncwarp();
             }
-        } else if (n) {
-            const float4 *r = reinterpret_cast<const float4 *>(rec + off);
-            for (u32 k = 0; k < n; ++k) acc += density_weight(__ldg(r + 2 * k), __ldg(r + 2 * k + 1), s_sigma);
+        } else {
+#pragma unroll
+            for (int k = 0; k < kDlVox; ++k) {
+                const float4 *r = reinterpret_cast<const float4 *>(rec + off[k]);
+                for (u32 q = 0; q < n[k]; ++q) acc[k] += density_weight(__ldg(r + 2 * q), __ldg(r + 2 * q + 1), s_sigma);
+            }
         }
-        if (v < n_voxels) out[v] = (float)acc;
+#pragma unroll
+        for (int k = 0; k < kDlVox; ++k)
+            if (v0 + 32 * k < n_voxels) out[v0 + 32 * k] = (float)acc[k];
     }
 }
 
@@ -263,7 +319,7 @@ int lvx_density_l0(const uint8_t *counts_d, const uint32_t *offsets_d,
     LVX_REQUIRE(counts_d && offsets_d && table_d && level0_d && n_voxels > 0, "bad arguments");
     LVX_REQUIRE(((uintptr_t)seg_rec_d & 15) == 0, "seg_rec_d must be 16-byte aligned");
     // a few warps' worth of voxels per warp keeps the grid at some waves of the 148 SMs
-    const i64 warps = lvx_ceil_div(n_voxels, 32);
+    const i64 warps = lvx_ceil_div(n_voxels, 32 * kDlVox);
     const i64 blocks = lvx_ceil_div(warps, kDlThreads / 32);
     const i64 cap = (i64)lvx_sm_count() * 64;
     density_l0_kernel<u8><<<(unsigned)(blocks < cap ? blocks : cap), kDlThreads, 0, (cudaStream_t)stream>>>(
@@ -276,7 +332,7 @@ int lvx_density_l0_u32(const uint32_t *counts_d, const uint32_t *offsets_d, cons
                        const float *table_d, int64_t n_voxels, float *level0_d, void *stream) {
     LVX_REQUIRE(counts_d && offsets_d && table_d && level0_d && n_voxels > 0, "bad arguments");
     LVX_REQUIRE(((uintptr_t)seg_rec_d & 15) == 0, "seg_rec_d must be 16-byte aligned");
-    const i64 warps = lvx_ceil_div(n_voxels, 32);
+    const i64 warps = lvx_ceil_div(n_voxels, 32 * kDlVox);
     const i64 blocks = lvx_ceil_div(warps, kDlThreads / 32);
     const i64 cap = (i64)lvx_sm_count() * 64;
     density_l0_kernel<u32><<<(unsigned)(blocks < cap ? blocks : cap), kDlThreads, 0, (cudaStream_t)stream>>>(
