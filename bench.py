@@ -468,8 +468,16 @@ def run_ours(args, wl):
             t_ao = min(ev_ms(lambda: ao_bake_device(model, octree, aop)) for _ in range(2))
             occupied = int((model.dev("counts") > 0).sum().item())
             samples = occupied * ao[0] * int(ao[1] / ao[2])
+            # bound: the FP64 pipe (cache-resident, no FMA): ~58 float64-pipe instructions per trilinear
+            # sample in the interior path (SASS count); peak = SMs x 64 lanes x clock
+            fp64_peak = 148 * 64 * 1.965e9
             st["ao_bake"] = {"ms": t_ao, "occupied_voxels": occupied, "gsamples_per_s": samples / t_ao / 1e6,
-                             "requested_gbs": samples * 32 / t_ao / 1e6}
+                             "samples_upper_bound": samples, "requested_gbs": samples * 32 / t_ao / 1e6,
+                             "bound": "fp64 pipe", "fp64_ops_per_sample": 58,
+                             "frac_of_fp64_pipe_peak_upper_bound": samples * 58 / (t_ao * 1e-3) / fp64_peak,
+                             "note": "samples = occupied x rays x floor(R/step) is an upper bound (rays stop at "
+                                     "saturation or the grid border); ncu: sm__inst_executed_pipe_fp64 53 % "
+                                     "(profiles/r2_stage_kernels.txt)"}
             model.ao = lv.precompute_voxel_ao(model, octree, aop)
         return octree, st
 

@@ -58,6 +58,15 @@ constexpr int kSortCap = 48;       // hits per ray and iteration sorted in local
 constexpr u32 kNil = 0xFFFFFFFFu;
 constexpr double kCullMarginWf = 1e-4;
 constexpr float kRejectMarginWf = 2e-3f;
+// the ray point of an item in the frame of its voxel lies in [-1, 2]: 13 fraction bits (step 1.2e-4);
+// the pre-reject is conservative, its reach grows by the rounding (<= 1.06e-4 as a distance)
+constexpr float kItemQScale = 8192.0f;
+constexpr float kItemQSlack = 1.5e-4f;
+__device__ __forceinline__ u32 item_q16(float v) {
+    const float s = fminf(fmaxf(v * kItemQScale, -32768.0f), 32767.0f);
+    return (u32)(unsigned short)(short)__float2int_rn(s);
+}
+__device__ __forceinline__ float item_unq16(u32 h) { return (float)(short)(unsigned short)(h & 0xFFFFu) * (1.0f / kItemQScale); }
 
 // one record per window that can own hits (per-ray stride layout: ray place * wn + k)
 struct __align__(16) WfWindow {
@@ -195,8 +204,9 @@ struct WfArgs {
     u32 *live[2];
     WfWindow *win;
     u32 cap_win;
-    u32 *item_place, *item_lin;  // (ray place in the live list, home voxel)
-    float4 *item_q;              // ray point near the voxel, relative to the voxel's corner (float32)
+    // one 16-byte record per (ray, voxel) item: ray place in the live list, home voxel, and the ray
+    // point near the voxel relative to the voxel's corner as 3 x int16 fixed point (kItemQScale)
+    uint4 *item;
     double2 *item_t;             // own-voxel mode: parameter range of the item's window
     u32 capq_item;
     float4 *fdir;                // [R] float32 ray direction by place (one sector per item in the pre-reject)
@@ -503,10 +513,11 @@ __device__ __forceinline__ void walk_flush(const WfArgs &A, WalkStage &S, const 
                 const int wx = (int)(w.cell & 0xFFFFFu) - 1, wy = (int)((w.cell >> 20) & 0xFFFFFu) - 1,
                           wz = (int)(w.cell >> 40) - 1;
                 const int bz_ = b / 9, by_ = (b - 9 * bz_) / 3, bx_ = b - 9 * bz_ - 3 * by_;
-                A.item_place[out0 + j] = w.place;
-                A.item_lin[out0 + j] = (u32)((wx + bx_ - 1) + A.rx * ((wy + by_ - 1) + A.ry * (wz + bz_ - 1)));
-                // voxel-local float32 frame for the (conservative) pre-reject
-                A.item_q[out0 + j] = make_float4(w.qx - (float)(bx_ - 1), w.qy - (float)(by_ - 1), w.qz - (float)(bz_ - 1), 0.0f);
+                // (voxel-local frame for the conservative pre-reject)
+                A.item[out0 + j] = make_uint4(
+                    w.place, (u32)((wx + bx_ - 1) + A.rx * ((wy + by_ - 1) + A.ry * (wz + bz_ - 1))),
+                    item_q16(w.qx - (float)(bx_ - 1)) | (item_q16(w.qy - (float)(by_ - 1)) << 16),
+                    item_q16(w.qz - (float)(bz_ - 1)));
                 // own-voxel mode: only the window of the voxel itself gathers it (:797-799)
                 if (ST) A.item_t[out0 + j] = ST->t[warp][lo];
             }
@@ -834,7 +845,7 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_CAND_MINB) wf_cand_kernel(c
     const u32 total = V.pre[kNQ];
     const bool joints = A.p.joints != 0;
     const bool nbr = A.p.neighbor != 0;
-    const float reach_pt = (float)A.p.tube_r + kRejectMarginWf;
+    const float reach_pt = (float)A.p.tube_r + kRejectMarginWf + kItemQSlack;
     const u32 stride = gridDim.x * blockDim.x;
     const u32 plane = (u32)A.rx * (u32)A.ry;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -859,10 +870,11 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_CAND_MINB) wf_cand_kernel(c
             const u32 fk = f + (u32)k * stride;
             have[k] = fk < total;
             I[k].it = queue_view_index(V, have[k] ? fk : 0u, A.capq_item);
-            place[k] = A.item_place[I[k].it];
+            const uint4 itm = A.item[I[k].it];
+            place[k] = itm.x;
             I[k].place = place[k];
-            lin[k] = A.item_lin[I[k].it];
-            q0[k] = A.item_q[I[k].it];
+            lin[k] = itm.y;
+            q0[k] = make_float4(item_unq16(itm.z), item_unq16(itm.z >> 16), item_unq16(itm.w), 0.0f);
         }
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
@@ -1547,7 +1559,7 @@ __global__ void wf_begin_kernel(const WfArgs A) {
 struct WfLayout {
     size_t total;
     size_t ctl, rw, rp, rpix, head, tab_seen, tab_sph, pool_seen, pool_sph, live0, live1, win,
-        win_over, item_place, item_lin, item_q, item_t, fdir, span, rdir, tube, sph, hit, hit_c, hit_next, hit_slot,
+        win_over, item, item_t, fdir, span, rdir, tube, sph, hit, hit_c, hit_next, hit_slot,
         slot_c, hcnt;
     u32 R, pool_cap, cap_win, capq_item, capq_surv, capq_hit;
 };
@@ -1583,9 +1595,7 @@ WfLayout wf_layout(i64 R, double scale) {
     L.live1 = take(c, r * 4);
     L.win = take(c, (size_t)L.cap_win * sizeof(WfWindow));
     L.win_over = take(c, (size_t)L.cap_win * 4);
-    L.item_place = take(c, (size_t)L.capq_item * kNQ * 4);
-    L.item_lin = take(c, (size_t)L.capq_item * kNQ * 4);
-    L.item_q = take(c, (size_t)L.capq_item * kNQ * 16);
+    L.item = take(c, (size_t)L.capq_item * kNQ * 16);
     L.item_t = take(c, (size_t)L.capq_item * kNQ * 16);
     L.fdir = take(c, r * 16);
     L.span = take(c, r * 16);
@@ -1765,9 +1775,7 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     A.win = (WfWindow *)(base + L.win);
     A.cap_win = L.cap_win;
     A.win_over = (u32 *)(base + L.win_over);
-    A.item_place = (u32 *)(base + L.item_place);
-    A.item_lin = (u32 *)(base + L.item_lin);
-    A.item_q = (float4 *)(base + L.item_q);
+    A.item = (uint4 *)(base + L.item);
     A.item_t = (double2 *)(base + L.item_t);
     A.fdir = (float4 *)(base + L.fdir);
     A.span = (double *)(base + L.span);
