@@ -479,9 +479,10 @@ def default_engine() -> str:
     """Frame engine used when none is named: LVX_ENGINE=auto|tile|wavefront.
 
     Both engines produce the same bytes.  "auto" is the wavefront engine (streaming kernels over
-    device queues) in both modes: C3 1080p neighbour mode 7.9 ms vs 18.8 ms, own-voxel mode 7.3 ms
-    vs 10.9 ms for the tile engine (one monolithic kernel), which stays as the independent second
-    implementation the parity tests compare against and as the host of the footprint pass."""
+    device queues): C3 1080p neighbour mode 7.8 ms vs 18.8 ms, own-voxel mode 7.3 ms vs 10.9 ms for
+    the tile engine (one monolithic kernel) -- except in own-voxel mode on a dense model (more than
+    two segments per voxel), where the tile engine is faster.  The tile engine is also the independent
+    second implementation the parity tests compare against and the host of the footprint pass."""
     import os
     return os.environ.get("LVX_ENGINE", "auto")
 
@@ -519,7 +520,10 @@ class FramePlan:
         check_modes(params, model, octree, replines)
         self.engine = engine or default_engine()
         if self.engine == "auto":
-            self.engine = "wavefront"
+            # own-voxel mode on a dense model (several segments per voxel) is the one case the monolithic
+            # kernel wins: 1 M lines / 256^3 (5.8 segments per voxel) 7.4 ms vs 10.2 ms; C3 (0.58): 10.9 vs 7.3 ms
+            dense = model.segment_count > 2 * model.voxel_count
+            self.engine = "tile" if (not neighbor and dense) else "wavefront"
         if self.engine not in ("wavefront", "tile"):
             raise ValueError(f"unknown frame engine {self.engine!r}")
         # queue scale that this frame shape last needed (a frame whose queues overflow is

@@ -290,7 +290,7 @@ def test_composite_and_gather_reference_ops():
     m = lv.build_voxel_model(cs, lv.GridSpec(dims, 32))
     ray = (np.array([1.5, 1.5, -2.0]), np.array([0.0, 0.0, 1.0]))
     got = lv.gather_voxel_hits(ray, (1, 1, 1), m, lv.RenderParams(neighbor_mode="on"))
-    assert [h.kind for h in got] == ["tube"] and got[0].voxel == (1, 1, 1) and abs(got[0].t_in - 3.2) < 1e-6
+    assert [h.kind for h in got] == ["tube"] and got[0].voxel == (1, 1, 1) and abs(got[0].t_in - 3.2) < 0.03  # (endpoints are bin centres)
     assert lv.gather_voxel_hits(ray, (1, 1, 1), m, lv.RenderParams(neighbor_mode="on"), seen={21: 1}) == []
 
 
