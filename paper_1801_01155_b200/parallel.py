@@ -69,6 +69,13 @@ def tile_pixel_indices(rank: int, world: int, width: int, height: int, tile_w: i
     return (ys * width + xs).astype(np.int64), mask
 
 
+def _host_staged(group=None) -> bool:
+    """True when the group's backend cannot move CUDA tensors (gloo: used to run the multi-rank
+    paths with several ranks sharing ONE GPU in tests): collectives then go through host memory."""
+    import torch.distributed as dist
+    return dist.get_backend(group) == "gloo"
+
+
 # dtypes every backend (NCCL included) can move; anything else travels as its bytes
 _WIRE_DTYPES = ("torch.uint8", "torch.int8", "torch.int32", "torch.int64", "torch.float16", "torch.bfloat16",
                 "torch.float32", "torch.float64")
@@ -91,6 +98,8 @@ def allgather_varlen_multi(tensors, group=None):
     import torch.distributed as dist
     world = dist.get_world_size(group)
     dev = tensors[0].device
+    if dev.type == "cuda" and _host_staged(group):
+        return [[p.to(dev) for p in parts] for parts in allgather_varlen_multi([t.cpu() for t in tensors], group)]
     mine = torch.tensor([int(t.shape[0]) for t in tensors], dtype=torch.int64, device=dev)
     sizes = torch.empty(world * len(tensors), dtype=torch.int64, device=dev)
     dist.all_gather_into_tensor(sizes, mine, group=group)  # (flat output: what gloo and NCCL both accept)
@@ -112,6 +121,19 @@ def allgather_varlen_multi(tensors, group=None):
             parts = [p.contiguous().view(orig[0]).reshape((p.shape[0],) + orig[1]) for p in parts]
         out.append(parts)
     return out
+
+
+def all_reduce_(t, op=None, group=None):
+    """all_reduce in place (through host memory when the backend cannot move CUDA tensors)."""
+    import torch.distributed as dist
+    op = dist.ReduceOp.SUM if op is None else op
+    if t.device.type == "cuda" and _host_staged(group):
+        h = t.cpu()
+        dist.all_reduce(h, op=op, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op, group=group)
+    return t
 
 
 def allgather_varlen(t, group=None):
@@ -175,6 +197,14 @@ def gather_tiles(send, dst: int = 0, group=None, recv=None):
     import torch.distributed as dist
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
+    if send.device.type == "cuda" and _host_staged(group):
+        got = gather_tiles(send.cpu(), dst, group)
+        if got is None:
+            return None
+        if recv is None:
+            return got.to(send.device)
+        recv.copy_(got)
+        return recv
     if rank != dst:
         dist.gather(send, None, dst=dst, group=group)
         return None
@@ -323,16 +353,14 @@ def build_voxel_model_sharded(curves: CurveSet, spec: GridSpec, transfer_table=N
         failure = e
     flag = torch.tensor([0 if failure is None else (2 if isinstance(failure, MemoryError) else 1)],
                         dtype=torch.int32, device=local_off.device)
-    dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+    flag = all_reduce_(flag, dist.ReduceOp.MAX, group)
     if int(flag.item()) != 0:
         if failure is not None:
             raise failure
         kind = MemoryError if int(flag.item()) == 2 else RuntimeError
         raise kind("sharded voxelization failed on another rank")
-    total = sh["vox_cnt"].clone()
-    dist.all_reduce(total, group=group)  # int32 bit patterns of u32 counts add correctly
-    err = sh["err"].clone()
-    dist.all_reduce(err, op=dist.ReduceOp.MAX, group=group)
+    total = all_reduce_(sh["vox_cnt"].clone(), dist.ReduceOp.SUM, group)  # int32 bit patterns of u32 counts add correctly
+    err = all_reduce_(sh["err"].clone(), dist.ReduceOp.MAX, group)
     # (edge_kept is u16 in an int16 tensor: it travels as bytes, NCCL has no 16-bit integer type)
     keys, qs, lins, kept = allgather_varlen_multi(
         [sh["raw_key"], sh["raw_q"], sh["raw_lin"], sh["edge_kept"][:p1 - p0]], group)

@@ -71,4 +71,5 @@ def main():
             dump_stage_clocks()
             print(f"[{name} {label}] S={m.segment_count} {e0.elapsed_time(e1)/5:.3f} ms  img {h} stats {(st.sum(0)//5).tolist()}", flush=True)
 
-main()
+if __name__ == "__main__":
+    main()
