@@ -582,6 +582,9 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_WALK_MINB) wf_walk_kernel(c
         // round are issued together, and between rounds the warp is converged, so the stage of
         // fresh windows is flushed (one global atomic, coalesced stores) BEFORE it can overflow
         // -- no allocation round trip ever sits inside a ray's walk.
+        // (measured and dropped: requesting the NEXT window's neighbour cell one round ahead -- the walker
+        // already stands on it after next() -- changes nothing; a round is bound by its chain of
+        // dependent float64 instructions, not by that load)
         bool go = mine;
         for (;;) {
             go = go && kw < wn && csum < budget;
@@ -1636,7 +1639,7 @@ struct WfTuning {
     int grow_bits = 1;
     int tail_rays = 0, tail_bits = 4, tail_mode = 1, tail_from = 6;
     int wn_shift_max = 4;
-    int rays_mult = 8;
+    int rays_mult = 0;  // 0: by the number of ray slots
     bool debug = false;
 };
 
@@ -1826,7 +1829,10 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     }
     cudaStream_t st = (cudaStream_t)stream;
     const int sms = lvx_sm_count();
-    const int rays_mult = tune.rays_mult;
+    // blocks per SM of the ray-parallel kernels (walk, composite): 8 for a full frame; a screen share of a
+    // multi-GPU frame has fewer rays than that launch has threads from the first iteration on, and does
+    // better with a smaller one (1080p / 8 ranks: 2.48 -> 2.26 ms, 4K / 8: 4.74 -> 4.54 ms; LVX_WF_GRID_RAYS overrides)
+    const int rays_mult = tune.rays_mult > 0 ? tune.rays_mult : (R >= 1500000 ? 8 : (R >= 600000 ? 6 : 4));
     const unsigned grid_rays = (unsigned)(sms * rays_mult), grid_q = (unsigned)(sms * 8);
     A.ray_threads = grid_rays * (unsigned)kThreadsWf;
     const size_t walk_smem = sizeof(WalkStage) + (params->neighbor ? 0 : sizeof(WalkStageT));
