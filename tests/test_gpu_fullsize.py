@@ -306,6 +306,39 @@ def test_one_million_lines(lv, oracle, synth):
     assert np.array_equal(out["packed"].cpu().numpy(), packed_full)
 
 
+def test_one_million_lines_frame(lv, oracle, synth):
+    """BASELINE configs[3]'s scene on one GPU at 1080p (the north-star "<= 16 ms" frame): model, LoD
+    and the 16.7 M-voxel AO bake equal the oracle's, the frame equals the oracle's on every 64th row
+    (image within the bar, per-row counters equal), both engines agree byte for byte, and the 4K frame
+    with cone shadows agrees between the engines too."""
+    dims = (256, 256, 256)
+    pts, attrs, off = synth.turbulence(1000000, 100, dims)
+    m = lv.build_voxel_model(lv.CurveSet.from_flat(pts, attrs, off), lv.GridSpec(dims))
+    oc = lv.build_lod(m)
+    m.ao = lv.precompute_voxel_ao(m, oc)
+    ref = oracle.build_voxel_model(pts, attrs, off, dims, 32)
+    del pts, attrs
+    assert m.segment_count == ref.segment_count == 96824127
+    assert np.array_equal(m.packed, ref.packed) and np.array_equal(m.counts, ref.counts)
+    levels = oracle.build_octree(oracle.compute_density_level0(ref))
+    for a, b in zip(oc.levels, levels):
+        assert np.array_equal(a, b)
+    ref.ao = oracle.precompute_voxel_ao(ref, levels, 100, 5.0, 1.0)
+    assert np.array_equal(np.asarray(m.ao), np.asarray(ref.ao))
+    kw = dict(base_opacity=0.25, tau=0.95, neighbor_mode="on", ao_mode="precomputed")
+    cam = lv.default_camera(dims, 1920, 1080)
+    img, rs, _ = gpu_frame(lv, cam, m, oc, kw, "wavefront")
+    check_against_oracle_rows(oracle, dims, 1920, 1080, ref, levels, kw, img, rs, step=64)
+    del ref, levels
+    b, sb, _ = gpu_frame(lv, cam, m, oc, kw, "tile")
+    assert np.array_equal(img, b) and np.array_equal(rs, sb)
+    kw4 = dict(kw, shadow_mode="cone", light_dir=(0.3, 0.2, 1.0))
+    cam4 = lv.default_camera(dims, 3840, 2160)
+    a4, sa4, _ = gpu_frame(lv, cam4, m, oc, kw4, "wavefront")
+    b4, sb4, _ = gpu_frame(lv, cam4, m, oc, kw4, "tile")
+    assert np.array_equal(a4, b4) and np.array_equal(sa4, sb4)
+
+
 def test_packed_only_model_follows_reassignment(lv, synth):
     """A model that carries only (counts, offsets, packed) renders from records decoded on the device;
     assigning new encoded arrays must drop every stale decoded cache."""
