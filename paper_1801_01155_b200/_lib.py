@@ -190,7 +190,13 @@ def to_device(a: np.ndarray, dtype=None):
         a = a.view(np.int16)
     elif a.dtype == np.uint64:
         a = a.view(np.int64)
-    t = torch.from_numpy(a)
+    if not a.flags.writeable:
+        import warnings
+        with warnings.catch_warnings():  # (the tensor is only read: it is copied to the device right away)
+            warnings.simplefilter("ignore", UserWarning)
+            t = torch.from_numpy(a)
+    else:
+        t = torch.from_numpy(a)
     if a.nbytes < _STAGE_MIN or os.environ.get("LVX_H2D") == "pageable":
         return t.to("cuda", non_blocking=False)
     out = torch.empty(t.shape, dtype=t.dtype, device="cuda")
