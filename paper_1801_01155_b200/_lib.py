@@ -65,7 +65,7 @@ SYMBOLS = [
     "lvx_abi_version", "lvx_last_error", "lvx_device_check",
     "lvx_mark_curve_starts", "lvx_scan_scratch_bytes", "lvx_voxel_scan",
     "lvx_voxelize_bound", "lvx_voxelize_clip", "lvx_voxelize_compact", "lvx_raw_regroup", "lvx_scan_u16", "lvx_provenance",
-    "lvx_build_seg_records", "lvx_decode_packed", "lvx_density_l0", "lvx_density_l0_u32", "lvx_octree_layout", "lvx_build_octree",
+    "lvx_build_seg_records", "lvx_decode_packed", "lvx_density_l0", "lvx_density_l0_u32", "lvx_density_l0_packed", "lvx_octree_layout", "lvx_build_octree",
     "lvx_occupancy_dilate", "lvx_neighbor_sums", "lvx_render_scratch_bytes", "lvx_render", "lvx_render_wf_scratch_bytes", "lvx_render_wf", "lvx_render_wf_last_launches",
     "lvx_render_footprint", "lvx_untile", "lvx_untile_all",
     "lvx_fibonacci_dirs", "lvx_ao_bake", "lvx_probe_dda", "lvx_probe_tube", "lvx_probe_sphere",

@@ -4,14 +4,18 @@
 //   compute_density_level0   lod.py:82-94
 //   _coarsen / build_octree  lod.py:97-119
 //   _occupancy_dilated       raycast.py:351-366
-#include "lvx_common.cuh"
+#include <math_constants.h>
+
+#include <cstdlib>
+
+#include "lvx_geom.cuh"
 
 namespace {
 
 // Level-0 density.  np.bincount with weights is a sequential float64 accumulation of the
 // per-segment products length * sigma in stored order, one cast to float32 (lod.py:87-94).
 //
-// A warp owns 128 consecutive voxels per round (four per lane, interleaved so that the header loads
+// A warp owns 64 consecutive voxels per round (two per lane, interleaved so that the header loads
 // coalesce).  Their records are one contiguous span of the record array
 // (headers are exclusive prefix sums in voxel scan order), so the lanes load the span together --
 // one 32-byte record per lane and round, every sector used once, all loads independent -- and
@@ -31,12 +35,33 @@ __device__ __forceinline__ double density_weight(const float4 a, const float4 b,
     return len * (double)s_sigma[__float_as_uint(a.w) & 0xFFu];
 }
 
-constexpr int kDlVox = 4;  // voxels per lane and round: amortises the per-round scan over 128 voxels
+#ifndef LVX_DL_CAP
+#define LVX_DL_CAP 64
+#endif
+#ifndef LVX_DL_U1
+#define LVX_DL_U1 1
+#endif
+#ifndef LVX_DL_VOX
+#define LVX_DL_VOX 2
+#endif
+constexpr int kDlVox = LVX_DL_VOX;  // voxels per lane and round
 
-template <typename CountT>
+// One encoded record's product.  Used only while every global coordinate (voxel + bin centre) is exact
+// in float32 -- then b - a in float64 is the difference of the voxel-local bin centres, whichever voxel
+// the record sits in, and the voxel need not be known here.
+__device__ __forceinline__ double density_weight_packed(const LvxPacked &P, size_t s, const float *s_sigma) {
+    const LvxPackedFields f = lvx_packed_fields(P, lvx_packed_word(P, s));
+    float a[3], b[3];
+    lvx_packed_point(f.face_in, f.bin_in, P, 0, 0, 0, a);
+    lvx_packed_point(f.face_out, f.bin_out, P, 0, 0, 0, b);
+    const double ex = (double)b[0] - (double)a[0], ey = (double)b[1] - (double)a[1], ez = (double)b[2] - (double)a[2];
+    return sqrt(ex * ex + ey * ey + ez * ez) * (double)s_sigma[f.attr];
+}
+
+template <typename CountT, bool PACKED>
 __global__ void __launch_bounds__(kDlThreads)
 density_l0_kernel(const CountT *__restrict__ counts, const u32 *__restrict__ offsets,
-                  const lvx_seg_record *__restrict__ rec, const float *__restrict__ table,
+                  const lvx_seg_record *__restrict__ rec, const LvxPacked P, const float *__restrict__ table,
                   i64 n_voxels, float *__restrict__ out) {
     constexpr unsigned FULL = 0xFFFFFFFFu;
     __shared__ float s_sigma[256];
@@ -45,56 +70,55 @@ density_l0_kernel(const CountT *__restrict__ counts, const u32 *__restrict__ off
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const i64 n_warps = ((i64)gridDim.x * blockDim.x) >> 5;
-    const i64 per_round = 32 * kDlVox;
+    constexpr int per_round = 32 * kDlVox;
     const bool aligned32 = (reinterpret_cast<uintptr_t>(rec) & 31) == 0;
     for (i64 w = (((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5); w * per_round < n_voxels; w += n_warps) {
-        // lane owns voxels v0 + k * 32 + lane, k = 0 .. kDlVox - 1 (every load below is coalesced)
-        const i64 v0 = w * per_round + lane;
+        // lane owns voxels vbase + k * 32 + lane, k = 0 .. kDlVox - 1 (every load below is coalesced)
+        const i64 vbase = w * per_round;
+        const CountT *c = counts + vbase;
+        const u32 *o = offsets + vbase;
+        float *dst = out + vbase;
+        const int nv = (int)(n_voxels - vbase < per_round ? n_voxels - vbase : per_round);
         u32 n[kDlVox], off[kDlVox], first[kDlVox];
         unsigned any = 0;
-        // counts AND offsets in one round trip (the offsets of empty voxels are loaded and ignored:
-        // their sectors are fetched for the occupied neighbours anyway); the headers of the warp's
-        // next round are requested now
+        // counts AND offsets in one round trip (the offsets of empty voxels are part of the prefix
+        // sums and are used below); the headers of the warp's next round are requested now
 #pragma unroll
         for (int k = 0; k < kDlVox; ++k) {
-            const i64 v = v0 + 32 * k;
-            n[k] = v < n_voxels ? (u32)counts[v] : 0u;
-            off[k] = v < n_voxels ? offsets[v] : 0u;
+            const int i = 32 * k + lane;
+            n[k] = i < nv ? (u32)c[i] : 0u;
+            off[k] = i < nv ? o[i] : 0u;
             any |= n[k];
-            const i64 vn = v + n_warps * per_round;
-            if (vn < n_voxels && (lane & 7) == 0) {
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(offsets + vn));
-                if (lane == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(counts + vn));
-            }
+        }
+        if (vbase + n_warps * per_round + per_round <= n_voxels) {
+            const size_t ahead = (size_t)(n_warps * per_round);
+            if (lane < 4 * kDlVox) asm volatile("prefetch.global.L2 [%0];" ::"l"(o + ahead + 8 * lane));
+            if (lane == 31) asm volatile("prefetch.global.L2 [%0];" ::"l"(c + ahead));
         }
         if (!__any_sync(FULL, any != 0)) {
 #pragma unroll
             for (int k = 0; k < kDlVox; ++k)
-                if (v0 + 32 * k < n_voxels) out[v0 + 32 * k] = 0.0f;
+                if (32 * k + lane < nv) dst[32 * k + lane] = 0.0f;
             continue;
         }
-        u32 total = 0, base = 0;
-        bool have_base = false;
+        // The headers of a whole round are exclusive prefix sums exactly when every voxel's offset is
+        // its predecessor's offset + count: one shuffle per voxel checks that, and then the span, each
+        // voxel's place in it and its length follow from the offsets alone (no scan).
+        bool chain = nv == per_round;
 #pragma unroll
         for (int k = 0; k < kDlVox; ++k) {
-            u32 inc = n[k];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const u32 t = __shfl_up_sync(FULL, inc, o);
-                if (lane >= o) inc += t;
+            u32 next = __shfl_down_sync(FULL, off[k], 1);
+            if (k + 1 < kDlVox) {
+                const u32 wrap = __shfl_sync(FULL, off[k + 1], 0);
+                if (lane == 31) next = wrap;
             }
-            first[k] = total + inc - n[k];  // my records of voxel k are [first, first + n) of the span
-            total += __shfl_sync(FULL, inc, 31);
-            const unsigned occ = __ballot_sync(FULL, n[k] != 0);
-            if (!have_base && occ) {
-                base = __shfl_sync(FULL, off[k], __ffs((int)occ) - 1);
-                have_base = true;
-            }
+            if (k + 1 < kDlVox || lane < 31) chain = chain && next == off[k] + n[k];
         }
-        bool mine_ok = true;
+        const bool contiguous = __all_sync(FULL, chain);
+        const u32 base = __shfl_sync(FULL, off[0], 0);
+        const u32 total = __shfl_sync(FULL, off[kDlVox - 1] + n[kDlVox - 1], 31) - base;
 #pragma unroll
-        for (int k = 0; k < kDlVox; ++k) mine_ok = mine_ok && (n[k] == 0 || off[k] == base + first[k]);
-        const bool contiguous = __all_sync(FULL, mine_ok);
+        for (int k = 0; k < kDlVox; ++k) first[k] = off[k] - base;
         double acc[kDlVox];
 #pragma unroll
         for (int k = 0; k < kDlVox; ++k) acc[k] = 0.0;
@@ -103,6 +127,10 @@ density_l0_kernel(const CountT *__restrict__ counts, const u32 *__restrict__ off
             for (u32 j0 = 0; j0 < total; j0 += kDlChunk) {
                 const u32 m = min((u32)kDlChunk, total - j0);
                 for (u32 j = lane; j < m; j += 32) {
+                    if constexpr (PACKED) {
+                        s_w[warp][j] = density_weight_packed(P, (size_t)base + j0 + j, s_sigma);
+                        continue;
+                    }
                     float4 a, b;
                     if (aligned32) {
                         // one 256-bit load per record: every sector of the span is requested once
@@ -119,23 +147,72 @@ density_l0_kernel(const CountT *__restrict__ counts, const u32 *__restrict__ off
                     s_w[warp][j] = density_weight(a, b, s_sigma);
                 }
                 __syncwarp();
+                if (total <= (u32)kDlChunk) {  // the whole span is in shared memory (the usual round)
 #pragma unroll
-                for (int k = 0; k < kDlVox; ++k) {
-                    const u32 lo = max(first[k], j0), hi = min(first[k] + n[k], j0 + m);
-                    for (u32 q = lo; q < hi; ++q) acc[k] += s_w[warp][q - j0];
+                    for (int k = 0; k < kDlVox; ++k) {
+                        const double *p = &s_w[warp][first[k]];
+#if LVX_DL_U1
+#pragma unroll 1
+#endif
+                        for (u32 q = 0; q < n[k]; ++q) acc[k] += p[q];
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < kDlVox; ++k) {
+                        const u32 lo = max(first[k], j0), hi = min(first[k] + n[k], j0 + m);
+                        for (u32 q = lo; q < hi; ++q) acc[k] += s_w[warp][q - j0];
+                    }
                 }
                 __syncwarp();
             }
         } else {
 #pragma unroll
             for (int k = 0; k < kDlVox; ++k) {
-                const float4 *r = reinterpret_cast<const float4 *>(rec + off[k]);
-                for (u32 q = 0; q < n[k]; ++q) acc[k] += density_weight(__ldg(r + 2 * q), __ldg(r + 2 * q + 1), s_sigma);
+                if constexpr (PACKED) {
+                    for (u32 q = 0; q < n[k]; ++q) acc[k] += density_weight_packed(P, (size_t)off[k] + q, s_sigma);
+                } else {
+                    const float4 *r = reinterpret_cast<const float4 *>(rec + off[k]);
+                    for (u32 q = 0; q < n[k]; ++q)
+                        acc[k] += density_weight(__ldg(r + 2 * q), __ldg(r + 2 * q + 1), s_sigma);
+                }
             }
         }
 #pragma unroll
         for (int k = 0; k < kDlVox; ++k)
-            if (v0 + 32 * k < n_voxels) out[v0 + 32 * k] = (float)acc[k];
+            if (32 * k + lane < nv) dst[32 * k + lane] = (float)acc[k];
+    }
+}
+
+// The same sums from the ENCODED records (5 bytes per segment at N = 32 instead of the 32-byte render
+// record: 2.3x less traffic for the whole kernel at C3).  A lane adds up the records of its own voxels
+// in stored order; neighbouring lanes own neighbouring voxels, whose records are neighbours in memory,
+// so the 8-byte loads of a warp fall into a handful of sectors.  The endpoints are reconstructed exactly
+// as the voxelizer does (bin centre + voxel in float64, cast to float32), so the products are bit-identical.
+__global__ void __launch_bounds__(kDlThreads)
+density_l0_packed_kernel(const u8 *__restrict__ counts, const u32 *__restrict__ offsets, const LvxPacked P,
+                         const float *__restrict__ table, int rx, int ry, i64 n_voxels, float *__restrict__ out) {
+    __shared__ float s_sigma[256];
+    s_sigma[threadIdx.x] = table[4 * threadIdx.x + 3];
+    __syncthreads();
+    const i64 stride = (i64)gridDim.x * blockDim.x;
+    for (i64 v = (i64)blockIdx.x * blockDim.x + threadIdx.x; v < n_voxels; v += stride) {
+        const u32 n = counts[v];
+        double acc = 0.0;
+        if (n) {
+            const u32 base = offsets[v];
+            const int vx = (int)(v % rx), vy = (int)((v / rx) % ry), vz = (int)(v / ((i64)rx * ry));
+            for (u32 q = 0; q < n; ++q) {
+                const LvxPackedFields f = lvx_packed_fields(P, lvx_packed_word(P, base + q));
+                float a[3], b[3];
+                lvx_packed_point(f.face_in, f.bin_in, P, vx, vy, vz, a);
+                lvx_packed_point(f.face_out, f.bin_out, P, vx, vy, vz, b);
+                // endpoints are widened BEFORE the subtraction (lod.py:87-89)
+                const double ex = (double)b[0] - (double)a[0], ey = (double)b[1] - (double)a[1],
+                             ez = (double)b[2] - (double)a[2];
+                acc += sqrt(ex * ex + ey * ey + ez * ez) * (double)s_sigma[f.attr];
+            }
+        }
+        out[v] = (float)acc;
     }
 }
 
@@ -173,11 +250,26 @@ __device__ __forceinline__ float mip_reduce(const float *s, int pitch_y, int pit
 
 __global__ void __launch_bounds__(kMipP *kMipP *kMipP)
 mip3_kernel(const float *__restrict__ src, MipDims d0, float *__restrict__ dst1, MipDims d1,
-            float *__restrict__ dst2, MipDims d2, float *__restrict__ dst3, MipDims d3, int n_out) {
+            float *__restrict__ dst2, MipDims d2, float *__restrict__ dst3, MipDims d3, int n_out, bool vec4) {
     __shared__ float s0[kMipC * kMipC * (kMipC + 1)];
     __shared__ float s1[kMipP * kMipP * (kMipP + 1)];
     __shared__ float s2[4 * 4 * 5];
     const int bx = blockIdx.x * kMipP, by = blockIdx.y * kMipP, bz = blockIdx.z * kMipP;
+    if (vec4 && 2 * bx + kMipC <= d0.x) {
+        // rows of the child brick as four 16-byte loads (the row starts are 64-byte aligned here)
+        for (int idx = threadIdx.x; idx < kMipC * kMipC * kMipC / 4; idx += blockDim.x) {
+            const int q = idx % (kMipC / 4), ly = (idx / (kMipC / 4)) % kMipC, lz = idx / (kMipC * kMipC / 4);
+            const int gy = 2 * by + ly, gz = 2 * bz + lz;
+            float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            if (gy < d0.y && gz < d0.z)
+                v = __ldg(reinterpret_cast<const float4 *>(src + ((i64)gz * d0.y + gy) * d0.x + 2 * bx) + q);
+            float *row = &s0[(lz * kMipC + ly) * (kMipC + 1) + 4 * q];
+            row[0] = v.x;
+            row[1] = v.y;
+            row[2] = v.z;
+            row[3] = v.w;
+        }
+    } else
     for (int idx = threadIdx.x; idx < kMipC * kMipC * kMipC; idx += blockDim.x) {
         const int lx = idx % kMipC, ly = (idx / kMipC) % kMipC, lz = idx / (kMipC * kMipC);
         const int gx = 2 * bx + lx, gy = 2 * by + ly, gz = 2 * bz + lz;
@@ -321,9 +413,43 @@ int lvx_density_l0(const uint8_t *counts_d, const uint32_t *offsets_d,
     // a few warps' worth of voxels per warp keeps the grid at some waves of the 148 SMs
     const i64 warps = lvx_ceil_div(n_voxels, 32 * kDlVox);
     const i64 blocks = lvx_ceil_div(warps, kDlThreads / 32);
-    const i64 cap = (i64)lvx_sm_count() * 64;
-    density_l0_kernel<u8><<<(unsigned)(blocks < cap ? blocks : cap), kDlThreads, 0, (cudaStream_t)stream>>>(
-        counts_d, offsets_d, seg_rec_d, table_d, n_voxels, level0_d);
+    const i64 cap = (i64)lvx_sm_count() * LVX_DL_CAP;
+    density_l0_kernel<u8, false><<<(unsigned)(blocks < cap ? blocks : cap), kDlThreads, 0, (cudaStream_t)stream>>>(
+        counts_d, offsets_d, seg_rec_d, LvxPacked{}, table_d, n_voxels, level0_d);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_density_l0_packed(const uint8_t *counts_d, const uint32_t *offsets_d, const uint8_t *packed_d,
+                          const int32_t dims[3], int32_t n_bins, const float *table_d, float *level0_d, void *stream) {
+    LVX_REQUIRE(counts_d && offsets_d && table_d && level0_d && dims && dims[0] >= 1 && dims[1] >= 1 && dims[2] >= 1,
+                "bad arguments");
+    LVX_REQUIRE(n_bins >= 2 && n_bins <= 256 && (n_bins & (n_bins - 1)) == 0, "bad bin resolution %d", n_bins);
+    LVX_REQUIRE(((uintptr_t)packed_d & 7) == 0, "packed_d must be 8-byte aligned");
+    LvxPacked P;
+    int lb = 0;
+    while ((1 << (lb + 1)) <= n_bins) ++lb;
+    P.bytes = packed_d;
+    P.lb = lb;
+    P.n = n_bins;
+    P.inv_n = 1.0f / (float)n_bins;
+    P.width = (2 * (3 + 2 * lb) + 8 + 5 + 7) / 8;  // record_width, voxelizer.py:70-76
+    const i64 V = (i64)dims[0] * dims[1] * dims[2];
+    const int dmax = dims[0] > dims[1] ? (dims[0] > dims[2] ? dims[0] : dims[2]) : (dims[1] > dims[2] ? dims[1] : dims[2]);
+    static const bool force_general = getenv("LVX_DENSITY_GENERAL") != nullptr;  // tests reach the fallback with it
+    if (!force_general && (i64)dmax * 2 * n_bins <= (i64)1 << 24) {
+        // voxel + bin centre is exact in float32: the warp-cooperative kernel, without the voxel
+        const i64 blocks = lvx_ceil_div(lvx_ceil_div(V, (i64)kDlVox), kDlThreads);
+        const i64 cap = (i64)lvx_sm_count() * LVX_DL_CAP;
+        density_l0_kernel<u8, true><<<(unsigned)(blocks < cap ? blocks : cap), kDlThreads, 0, (cudaStream_t)stream>>>(
+            counts_d, offsets_d, nullptr, P, table_d, V, level0_d);
+        LVX_LAUNCH_CHECK();
+        return LVX_OK;
+    }
+    const i64 blocks = lvx_ceil_div(V, kDlThreads);
+    const i64 cap = (i64)lvx_sm_count() * 256;
+    density_l0_packed_kernel<<<(unsigned)(blocks < cap ? blocks : cap), kDlThreads, 0, (cudaStream_t)stream>>>(
+        counts_d, offsets_d, P, table_d, dims[0], dims[1], V, level0_d);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }
@@ -334,9 +460,9 @@ int lvx_density_l0_u32(const uint32_t *counts_d, const uint32_t *offsets_d, cons
     LVX_REQUIRE(((uintptr_t)seg_rec_d & 15) == 0, "seg_rec_d must be 16-byte aligned");
     const i64 warps = lvx_ceil_div(n_voxels, 32 * kDlVox);
     const i64 blocks = lvx_ceil_div(warps, kDlThreads / 32);
-    const i64 cap = (i64)lvx_sm_count() * 64;
-    density_l0_kernel<u32><<<(unsigned)(blocks < cap ? blocks : cap), kDlThreads, 0, (cudaStream_t)stream>>>(
-        counts_d, offsets_d, seg_rec_d, table_d, n_voxels, level0_d);
+    const i64 cap = (i64)lvx_sm_count() * LVX_DL_CAP;
+    density_l0_kernel<u32, false><<<(unsigned)(blocks < cap ? blocks : cap), kDlThreads, 0, (cudaStream_t)stream>>>(
+        counts_d, offsets_d, seg_rec_d, LvxPacked{}, table_d, n_voxels, level0_d);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }
@@ -380,7 +506,8 @@ int lvx_build_octree(float *flat_d, const int32_t dims[3], void *stream) {
                   (unsigned)lvx_ceil_div(d1.z, kMipP));
         mip3_kernel<<<grid, kMipP * kMipP * kMipP, 0, (cudaStream_t)stream>>>(
             flat_d + off[l], d0, flat_d + off[l + 1], d1, n_out >= 2 ? flat_d + off[l + 2] : nullptr, d2,
-            n_out >= 3 ? flat_d + off[l + 3] : nullptr, d3, n_out);
+            n_out >= 3 ? flat_d + off[l + 3] : nullptr, d3, n_out,
+            d0.x % 4 == 0 && ((uintptr_t)(flat_d + off[l]) & 15) == 0);
         LVX_LAUNCH_CHECK();
         l += n_out;
     }

@@ -12,6 +12,7 @@ kernel); `levels` are numpy views downloaded on first access.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 
@@ -103,6 +104,17 @@ def density_level0_device(model: VoxelModel, out=None):
         out = torch.empty(V, dtype=torch.float32, device="cuda")
     if model.voxel_binning_is_external():
         return _density_by_seg_voxel(model, out)
+    mode = os.environ.get("LVX_DENSITY", "auto")
+    if model.records_match_packed() and (mode == "packed" or (mode == "auto" and not model.has_render_caches())):
+        # a model that carries only the encoded arrays (a .vxl file): the sum is taken from them,
+        # nothing is expanded (bit-identical; with the render records at hand those are faster,
+        # the decode costs more issue slots than the 27 bytes per segment it saves)
+        table = _lib.to_device(np.ascontiguousarray(model.transfer_table, dtype=np.float32))
+        _lib.check(_lib.lib().lvx_density_l0_packed(
+            _lib.ptr(model.dev("counts")), _lib.ptr(model.dev("offsets")), _lib.ptr(model.dev("packed")),
+            _lib.i32x3(model.spec.dims), C.c_int32(int(model.spec.bins_per_axis)), _lib.ptr(table), _lib.ptr(out),
+            _lib.stream_ptr()))
+        return out
     counts_d, offsets_d, rec_d, table_d, _ = model.device_view(need_occ=False)
     _lib.check(_lib.lib().lvx_density_l0(_lib.ptr(counts_d), _lib.ptr(offsets_d), _lib.ptr(rec_d),
                                          _lib.ptr(table_d), C.c_int64(V), _lib.ptr(out),

@@ -291,7 +291,7 @@ class VoxelModel:
             self._dev[name] = value
             self._host.pop(name, None)
         self._decoded.discard(name)  # now user-supplied
-        if name == "seg_voxel":
+        if name.startswith("seg_") or name in ("counts", "offsets", "packed"):
             self._from_pipeline = False
         if name in _RENDER_INPUTS:
             self._derived.clear()
@@ -446,6 +446,17 @@ class VoxelModel:
         what the reference's compute_density_level0 bins by (lod.py:90-93)."""
         return (not self._from_pipeline) and self._has("seg_voxel") and "seg_voxel" not in self._decoded \
             and self.segment_count > 0
+
+    def records_match_packed(self) -> bool:
+        """True when the per-segment arrays are known to be what `packed` decodes to: the model came
+        out of the voxelizer, or it carries only the encoded arrays (anything else was decoded from
+        them).  False once a caller has supplied per-segment arrays of their own."""
+        if not self._has("packed") or self.segment_count == 0:
+            return False
+        if self._from_pipeline:
+            return True
+        return all((not self._has(k)) or k in self._decoded
+                   for k in ("seg_a", "seg_b", "seg_attr", "seg_lid", "seg_voxel"))
 
     def has_render_caches(self) -> bool:
         """True when the per-segment arrays the 32-byte render records are built from are there

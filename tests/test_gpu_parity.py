@@ -285,6 +285,51 @@ def test_model_from_encoded_arrays_only(lv, synth):
                       transfer_table=m.transfer_table).seg_a
 
 
+_DENSITY_SNIPPET = """
+import sys, hashlib, numpy as np
+sys.path.insert(0, {root!r})
+import paper_1801_01155_b200 as lv
+from paper_1801_01155_b200 import synth
+for dims, nb in (((23, 17, 40), 32), ((9, 30, 11), 256), ((16, 16, 16), 4)):
+    m = lv.build_voxel_model(lv.CurveSet.from_flat(*synth.turbulence(900, 40, dims)), lv.GridSpec(dims, nb))
+    enc = lv.VoxelModel(spec=m.spec, counts=m.counts.copy(), offsets=m.offsets.copy(), packed=m.packed.copy(),
+                        transfer_table=m.transfer_table)
+    d = lv.compute_density_level0(enc)
+    assert not enc.has_render_caches()
+    print(hashlib.sha256(np.ascontiguousarray(d).tobytes()).hexdigest())
+"""
+
+
+def test_density_from_encoded_records(lv, synth):
+    """An encoded-only model gets its level-0 density from the packed records without any expansion
+    (lvx_density_l0_packed): both kernels behind it -- the warp-cooperative one for grids whose
+    coordinates are exact in float32, and the voxel-aware general one (forced here through
+    LVX_DENSITY_GENERAL) -- give the render-record sums bit for bit (lod.py:82-94)."""
+    import hashlib, os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    want = []
+    for dims, nb in (((23, 17, 40), 32), ((9, 30, 11), 256), ((16, 16, 16), 4)):
+        m = lv.build_voxel_model(lv.CurveSet.from_flat(*synth.turbulence(900, 40, dims)), lv.GridSpec(dims, nb))
+        assert m.has_render_caches()
+        d = lv.compute_density_level0(m)  # render records
+        want.append(hashlib.sha256(np.ascontiguousarray(d).tobytes()).hexdigest())
+        enc = lv.VoxelModel(spec=m.spec, counts=m.counts.copy(), offsets=m.offsets.copy(), packed=m.packed.copy(),
+                            transfer_table=m.transfer_table)
+        assert np.array_equal(lv.compute_density_level0(enc), d)
+        assert not enc.has_render_caches()  # nothing was expanded for it
+        # caller-supplied segment arrays win over the encoded ones (the reference sums seg_a / seg_b)
+        enc.seg_a = m.seg_a * np.float32(0.5)
+        enc.seg_b = m.seg_b * np.float32(0.5)
+        enc.seg_attr, enc.seg_lid, enc.seg_voxel = m.seg_attr, m.seg_lid, m.seg_voxel
+        got = lv.compute_density_level0(enc)
+        assert not np.array_equal(got, d) and np.allclose(got, 0.5 * d, rtol=1e-6)
+    for env in ({}, {"LVX_DENSITY_GENERAL": "1"}):
+        out = subprocess.run([sys.executable, "-c", _DENSITY_SNIPPET.format(root=root)], capture_output=True, text=True,
+                             env={**os.environ, **env}, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        assert out.stdout.split() == want, env
+
+
 @pytest.mark.parametrize("n_bins", [4, 32, 128, 256])
 def test_packed_records_render_identically(lv, synth, n_bins):
     """Every record width (4, 5, 6, 7 bytes): wavefront frames decoded from the encoded records in
