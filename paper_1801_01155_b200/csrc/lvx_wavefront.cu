@@ -1227,7 +1227,7 @@ __device__ __forceinline__ bool wf_composite_one(const WfArgs &A, WfTables &T, W
 #define LVX_WF_LIGHT 8
 #endif
 constexpr int kLight = LVX_WF_LIGHT;  // up to this many hits a ray orders by itself; more are ranked by its warp
-static_assert(kLight <= kHitSlots && kHitSlots <= 255, "a light ray's hits are all in slots, and a slot index fits 8 bits");
+static_assert(kLight <= kHitSlots && kHitSlots <= 127 && kHitSlots <= kSortCap, "a light ray's hits are all in slots, and a slot index fits 8 bits");
 
 struct SortStage {
     double t[kThreadsWf / 32][kSortCap];
@@ -1247,6 +1247,7 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_ker
     // the insertion sort's stores were a third of this kernel's L2 write traffic.
     __shared__ double L_t[kLight][kThreadsWf];
     __shared__ unsigned long long L_k[kLight][kThreadsWf];  // key2 with the hit's slot in its low 8 bits
+    __shared__ unsigned char O8[kHitSlots][kThreadsWf];      // order of a heavier ray's slots (| 0x80: joint sphere)
     const int tid = threadIdx.x;
     const u32 n_live = A.ctl->err ? 0u : A.ctl->n_live[par];
     const u32 wn = A.ctl->wn;
@@ -1293,6 +1294,8 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_ker
         u32 order[kSortCap];
         int n = 0;
         const bool light = nhit <= (u32)kLight;
+        // more than a light ray's hits, all of them in slots, none dropped: ranked by the warp into O8
+        const bool in_slots = !light && nhit <= (u32)kHitSlots && !big;
         if (nhit && light) {
             // few hits (all of them in slots: kLight <= kHitSlots): insertion sort by the ray's own thread
             for (u32 ref = H.first(); ref != kNil; ref = H.next(ref)) {
@@ -1318,6 +1321,30 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_ker
         while (hm) {
             const int L = __ffs((int)hm) - 1;
             hm &= hm - 1;
+            const u32 placeL = __shfl_sync(FULL, i, L);
+            const u32 nhL = __shfl_sync(FULL, nhit, L);
+            if (__shfl_sync(FULL, (int)in_slots, L)) {
+                // the usual heavy ray: every hit sits in a slot and none is dropped, so hit j IS slot j --
+                // nothing is listed by the ray's own lane, the ranks go straight into the ray's
+                // byte column (no copy into its local array either)
+                for (u32 j = lane; j < nhL; j += 32) {
+                    const double2 v = *reinterpret_cast<const double2 *>(A.hit_slot + (size_t)j * R + placeL);
+                    Q.t[warp][j] = v.x;
+                    Q.k[warp][j] = (unsigned long long)__double_as_longlong(v.y);
+                }
+                __syncwarp();
+                for (u32 j = lane; j < nhL; j += 32) {
+                    const double t = Q.t[warp][j];
+                    const unsigned long long k2 = Q.k[warp][j];
+                    u32 rank = 0;
+                    for (u32 q = 0; q < nhL; ++q) rank += wf_before(Q.t[warp][q], Q.k[warp][q], t, k2) ? 1u : 0u;
+                    // (keys are unique: a permutation)
+                    O8[rank][(warp << 5) + L] = (unsigned char)(j | (((k2 >> 18) & 1ull) ? 0x80u : 0u));
+                }
+                if (lane == L) n = (int)nhL;
+                __syncwarp();
+                continue;
+            }
             if (lane == L) {
                 u32 m = 0;
                 for (u32 ref = H.first(); ref != kNil; ref = H.next(ref)) {
@@ -1328,7 +1355,6 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_ker
             }
             __syncwarp();
             const u32 m = Q.n[warp];
-            const u32 placeL = __shfl_sync(FULL, i, L);
             for (u32 j = lane; j < m; j += 32) {
                 const u32 ref = Q.ref[warp][j];
                 const WfHit *hp = ref < (u32)kHitSlots ? A.hit_slot + (size_t)ref * R + placeL : A.hit + (ref - kHitSlots);
@@ -1354,6 +1380,10 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_ker
         }
         // reference (slot or pool entry, | kJointRef for a joint sphere) of the j-th hit in order
         auto sorted_ref = [&](int j) -> u32 {
+            if (in_slots) {
+                const u32 b = O8[j][tid];
+                return (b & 0x7Fu) | ((b & 0x80u) ? kJointRef : 0u);
+            }
             if (!light) return order[j];
             const unsigned long long k2 = L_k[j][tid];
             return (u32)(k2 & 0xFFull) | (((k2 >> 18) & 1ull) ? kJointRef : 0u);
