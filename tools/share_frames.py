@@ -18,3 +18,10 @@ st = torch.zeros((H, 3), dtype=torch.int64, device="cuda")
 for _ in range(4):
     plan.launch(img, st)
 torch.cuda.synchronize()
+import time
+ts = []
+for _ in range(10):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(); t0 = time.perf_counter(); e0.record(); plan.launch(img, st); e1.record(); torch.cuda.synchronize()
+    ts.append((e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3))
+print("share 1/%d %dx%d: events min %.3f ms median %.3f ms; wall min %.3f ms" % (N, W, H, min(t[0] for t in ts), sorted(t[0] for t in ts)[5], min(t[1] for t in ts)))
