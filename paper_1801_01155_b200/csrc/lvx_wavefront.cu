@@ -51,6 +51,31 @@ namespace cg = cooperative_groups;
 
 namespace {
 
+// Programmatic dependent launch: every kernel of the frame is launched with the stream-serialisation
+// attribute, so its launch is set up while the previous kernel of the chain drains; the first
+// statement of every kernel waits for that kernel's completion and memory flush.  The ~74 launches of a frame are all dependent
+// and short -- in a multi-GPU share they last 10-100 us each -- so the launch gaps are worth hiding.
+#define WF_PDL_ENTER() asm volatile("griddepcontrol.wait;" ::: "memory")
+// (letting the dependents in EARLY -- griddepcontrol.launch_dependents at the top of every kernel -- was
+// measured and dropped: their waiting blocks take the place of the running kernel's later waves, C3
+// 7.42 -> 7.79 ms; in the one-block bookkeeping kernels alone it changes nothing)
+
+template <typename... KArgs, typename... Args>
+cudaError_t wf_launch(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                      Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, KArgs(args)...);
+}
+
 constexpr int kNQ = 64;            // sub-queues per queue (spreads the allocation atomics)
 constexpr int kInline = 16;        // de-duplication table entries kept inline per ray
 constexpr int kThreadsWf = 256;
@@ -368,6 +393,7 @@ __device__ __forceinline__ void dda_load(const WfArgs &A, const WfRayWalk &r, in
 // init: one thread per pixel (8x4 tiles per warp, the tile kernel's mapping)
 // ---------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreadsWf) wf_init_kernel(const WfArgs A) {
+    WF_PDL_ENTER();
     constexpr unsigned FULL = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31;
     const i64 gw = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -533,6 +559,7 @@ __device__ __forceinline__ void walk_flush(const WfArgs &A, WalkStage &S, const 
 #define LVX_WF_WALK_MINB 3
 #endif
 __global__ void __launch_bounds__(kThreadsWf, LVX_WF_WALK_MINB) wf_walk_kernel(const WfArgs A, int par) {
+    WF_PDL_ENTER();
     constexpr unsigned FULL = 0xFFFFFFFFu;
     const u32 n_live = A.ctl->err ? 0u : A.ctl->n_live[par];
     const u32 wn = A.ctl->wn;
@@ -842,6 +869,7 @@ __device__ __forceinline__ void cand_fetch(const WfArgs &A, const CandItem &I, u
 
 template <bool PACKED>
 __global__ void __launch_bounds__(kThreadsWf, LVX_WF_CAND_MINB) wf_cand_kernel(const WfArgs A) {
+    WF_PDL_ENTER();
     __shared__ QueueView V;
     __shared__ CandStage S;
     queue_view_load(V, A.ctl->item_cnt, A.capq_item, A.ctl->err);
@@ -950,6 +978,7 @@ __device__ __forceinline__ WfHit wf_load_hit(const WfHit *p) {
 constexpr int kThreadsExact = LVX_WF_EXACT_THREADS;
 template <int KIND, bool GEOM, bool PACKED>
 __global__ void __launch_bounds__(kThreadsExact, LVX_WF_EXACT_MINB) wf_exact_kernel(const WfArgs A, int par) {
+    WF_PDL_ENTER();
     __shared__ QueueView V;
     queue_view_load(V, KIND == 0 ? A.ctl->tube_cnt : A.ctl->sph_cnt, A.capq_surv, A.ctl->err);
     const u32 total = V.pre[kNQ];
@@ -1240,6 +1269,7 @@ struct SortStage {
 #define LVX_WF_COMP_MINB 4
 #endif
 __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_kernel(const WfArgs A, int par) {
+    WF_PDL_ENTER();
     constexpr unsigned FULL = 0xFFFFFFFFu;
     __shared__ SortStage Q;
     // sort buffers of the rays with few hits, one column per thread ([entry][thread]: conflict-free).
@@ -1525,6 +1555,7 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_ker
 
 // between iterations: clear the queues, retire the consumed live list, set the next budget
 __global__ void wf_next_kernel(const WfArgs A, int par, int it_next) {
+    WF_PDL_ENTER();
     const int t = threadIdx.x;
     if (t < kNQ) {
         A.ctl->item_cnt[t] = 0;
@@ -1566,6 +1597,7 @@ __global__ void wf_next_kernel(const WfArgs A, int par, int it_next) {
 }
 
 __global__ void wf_begin_kernel(const WfArgs A) {
+    WF_PDL_ENTER();
     const int t = threadIdx.x;
     if (t < kNQ) {
         A.ctl->item_cnt[t] = 0;
@@ -1671,6 +1703,7 @@ struct WfTuning {
     int wn_shift_max = 4;
     int rays_mult = 0;  // 0: by the number of ray slots
     bool debug = false;
+    bool pdl = true;  // programmatic dependent launch of the frame's kernels (LVX_WF_PDL=0: plain launches)
 };
 
 int env_int(const char *name, int dflt, bool positive_only = false) {
@@ -1694,6 +1727,7 @@ const WfTuning &wf_tuning() {
         t.wn_sched = env_int("LVX_WF_WN", t.wn_sched, true);
         t.rays_mult = env_int("LVX_WF_GRID_RAYS", t.rays_mult, true);
         t.debug = getenv("LVX_WF_DEBUG") != nullptr;
+        t.pdl = env_int("LVX_WF_PDL", 1) != 0;
         return t;
     }();
     return T;
@@ -1837,6 +1871,7 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     A.wn_shift_max = tune.wn_shift_max;
 
     const bool debug = tune.debug;
+    const bool pdl = tune.pdl && !debug;
     const bool geom = params->shadow_mode == LVX_SHADOW_HARD || params->shadow_mode == LVX_SHADOW_REPLINES ||
                       params->ao_mode == LVX_AO_HEMISPHERE;
     // straight from the encoded records when the caller passes no render records (the geometry
@@ -1874,8 +1909,8 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
             attr_set = true;
         }
     }
-    wf_begin_kernel<<<1, 64, 0, st>>>(A);
-    wf_init_kernel<<<(unsigned)lvx_ceil_div(R, kThreadsWf), kThreadsWf, 0, st>>>(A);
+    LVX_CUDA_CHECK(wf_launch(pdl, wf_begin_kernel, 1, 64, 0, st, A));
+    LVX_CUDA_CHECK(wf_launch(pdl, wf_init_kernel, (unsigned)lvx_ceil_div(R, kThreadsWf), kThreadsWf, 0, st, A));
     LVX_LAUNCH_CHECK();
     u32 host[4] = {0, 0, 0, 0};
     int it = 0;
@@ -1894,20 +1929,20 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
             return LVX_E_CUDA;                                                                \
         }                                                                                     \
     }
-            wf_walk_kernel<<<grid_rays, kThreadsWf, walk_smem, st>>>(A, par);
+            LVX_CUDA_CHECK(wf_launch(pdl, wf_walk_kernel, grid_rays, kThreadsWf, walk_smem, st, A, par));
             WF_DEBUG_SYNC("walk");
-            if (packed) wf_cand_kernel<true><<<grid_q, kThreadsWf, 0, st>>>(A);
-            else wf_cand_kernel<false><<<grid_q, kThreadsWf, 0, st>>>(A);
+            if (packed) LVX_CUDA_CHECK(wf_launch(pdl, wf_cand_kernel<true>, grid_q, kThreadsWf, 0, st, A));
+            else LVX_CUDA_CHECK(wf_launch(pdl, wf_cand_kernel<false>, grid_q, kThreadsWf, 0, st, A));
             WF_DEBUG_SYNC("candidates");
-            if (geom) wf_exact_kernel<0, true, false><<<grid_q, kThreadsExact, 0, st>>>(A, par);
-            else if (packed) wf_exact_kernel<0, false, true><<<grid_q, kThreadsExact, 0, st>>>(A, par);
-            else wf_exact_kernel<0, false, false><<<grid_q, kThreadsExact, 0, st>>>(A, par);
+            if (geom) LVX_CUDA_CHECK(wf_launch(pdl, wf_exact_kernel<0, true, false>, grid_q, kThreadsExact, 0, st, A, par));
+            else if (packed) LVX_CUDA_CHECK(wf_launch(pdl, wf_exact_kernel<0, false, true>, grid_q, kThreadsExact, 0, st, A, par));
+            else LVX_CUDA_CHECK(wf_launch(pdl, wf_exact_kernel<0, false, false>, grid_q, kThreadsExact, 0, st, A, par));
             WF_DEBUG_SYNC("exact<tube>");
-            if (params->joints && geom) wf_exact_kernel<1, true, false><<<grid_q, kThreadsExact, 0, st>>>(A, par);
-            else if (params->joints && packed) wf_exact_kernel<1, false, true><<<grid_q, kThreadsExact, 0, st>>>(A, par);
-            else if (params->joints) wf_exact_kernel<1, false, false><<<grid_q, kThreadsExact, 0, st>>>(A, par);
+            if (params->joints && geom) LVX_CUDA_CHECK(wf_launch(pdl, wf_exact_kernel<1, true, false>, grid_q, kThreadsExact, 0, st, A, par));
+            else if (params->joints && packed) LVX_CUDA_CHECK(wf_launch(pdl, wf_exact_kernel<1, false, true>, grid_q, kThreadsExact, 0, st, A, par));
+            else if (params->joints) LVX_CUDA_CHECK(wf_launch(pdl, wf_exact_kernel<1, false, false>, grid_q, kThreadsExact, 0, st, A, par));
             WF_DEBUG_SYNC("exact<sphere>");
-            wf_composite_kernel<<<grid_rays, kThreadsWf, 0, st>>>(A, par);
+            LVX_CUDA_CHECK(wf_launch(pdl, wf_composite_kernel, grid_rays, kThreadsWf, 0, st, A, par));
             WF_DEBUG_SYNC("composite");
             if (debug) {
                 WfCtl c;
@@ -1928,7 +1963,7 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
                         "sum n_seen %llu  sum n_sph %llu\n", c.dbg[0], c.dbg[1], c.dbg[3], c.dbg[4], c.dbg[5], c.dbg[6]);
 #endif
             }
-            wf_next_kernel<<<1, 64, 0, st>>>(A, par, it + 1);
+            LVX_CUDA_CHECK(wf_launch(pdl, wf_next_kernel, 1, 64, 0, st, A, par, it + 1));
         }
         LVX_LAUNCH_CHECK();
         // rays left?  (n_live of the list the next iteration reads, and the error bits)
