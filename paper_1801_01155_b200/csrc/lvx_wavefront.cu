@@ -302,17 +302,26 @@ struct QueueView {
     u32 pre[kNQ + 1];
 };
 __device__ __forceinline__ void queue_view_load(QueueView &v, const u32 *cnt, u32 capq, u32 err) {
-    // (called by all threads of the block; v lives in shared memory)
-    if (threadIdx.x == 0) {
-        u32 run = 0;
-        for (int q = 0; q < kNQ; ++q) {
-            v.pre[q] = run;
-            const u32 c = cnt[q];
-            run += c < capq ? c : capq;
+    // (called by all threads of the block; v lives in shared memory.  The first warp scans the kNQ
+    // counters, two per lane: one memory round trip instead of a serial loop at the top of every block)
+    static_assert(kNQ == 64, "two counters per lane of one warp");
+    if (threadIdx.x < 32) {
+        const int lane = (int)threadIdx.x;
+        u32 c0 = cnt[2 * lane], c1 = cnt[2 * lane + 1];
+        c0 = c0 < capq ? c0 : capq;
+        c1 = c1 < capq ? c1 : capq;
+        u32 inc = c0 + c1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+            if (lane >= o) inc += t;
         }
+        const u32 ex = inc - (c0 + c1);
+        v.pre[2 * lane] = ex;
+        v.pre[2 * lane + 1] = ex + c0;
         // an overflowed queue holds unwritten entries: the frame is void (the host retries
         // with larger queues), nothing downstream may touch it
-        v.pre[kNQ] = err ? 0u : run;
+        if (lane == 31) v.pre[kNQ] = err ? 0u : inc;
     }
     __syncthreads();
 }
@@ -977,9 +986,7 @@ __device__ __forceinline__ WfHit wf_load_hit(const WfHit *p) {
 #endif
 constexpr int kThreadsExact = LVX_WF_EXACT_THREADS;
 template <int KIND, bool GEOM, bool PACKED>
-__global__ void __launch_bounds__(kThreadsExact, LVX_WF_EXACT_MINB) wf_exact_kernel(const WfArgs A, int par) {
-    WF_PDL_ENTER();
-    __shared__ QueueView V;
+__device__ __forceinline__ void wf_exact_body(const WfArgs &A, int par, QueueView &V, u32 block, u32 n_blocks) {
     queue_view_load(V, KIND == 0 ? A.ctl->tube_cnt : A.ctl->sph_cnt, A.capq_surv, A.ctl->err);
     const u32 total = V.pre[kNQ];
     const double ox = A.cam.o[0], oy = A.cam.o[1], oz = A.cam.o[2];
@@ -987,7 +994,7 @@ __global__ void __launch_bounds__(kThreadsExact, LVX_WF_EXACT_MINB) wf_exact_ker
     const size_t R = A.R;
     const WfEntry *queue = KIND == 0 ? A.tube : A.sph;
     const bool neighbor = A.p.neighbor != 0;
-    for (u32 f = blockIdx.x * blockDim.x + threadIdx.x; f < total; f += gridDim.x * blockDim.x) {
+    for (u32 f = block * blockDim.x + threadIdx.x; f < total; f += n_blocks * blockDim.x) {
         const int q = warp_queue(f);
         const WfEntry c = queue[queue_view_index(V, f, A.capq_surv)];
         const u32 seg = c.seg & 0x7FFFFFFFu;
@@ -1067,6 +1074,41 @@ __global__ void __launch_bounds__(kThreadsExact, LVX_WF_EXACT_MINB) wf_exact_ker
             if (KIND != 0) A.hit_c[e] = make_float4(ccx, ccy, ccz, 0.0f);
         }
     }
+}
+
+// Tubes and joint spheres in ONE launch: the blocks of the grid are divided between the two queues in
+// proportion to their lengths (a sphere entry weighs 5/4 of a tube entry: more of them are hits and
+// get shaded), so neither half waits for the other and the frame has one launch, one ramp-up and one
+// drain less per iteration.
+template <bool GEOM, bool PACKED>
+__global__ void __launch_bounds__(kThreadsExact, LVX_WF_EXACT_MINB) wf_exact_kernel(const WfArgs A, int par) {
+    WF_PDL_ENTER();
+    __shared__ QueueView V;
+    __shared__ u32 s_split;
+    if (threadIdx.x < 32) {
+        unsigned long long t = 0, sp = 0;
+        if (A.p.joints != 0) sp = (unsigned long long)A.ctl->sph_cnt[threadIdx.x] + A.ctl->sph_cnt[threadIdx.x + 32];
+        t = (unsigned long long)A.ctl->tube_cnt[threadIdx.x] + A.ctl->tube_cnt[threadIdx.x + 32];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            t += __shfl_xor_sync(0xFFFFFFFFu, t, o);
+            sp += __shfl_xor_sync(0xFFFFFFFFu, sp, o);
+        }
+        if (threadIdx.x == 0) {
+            const unsigned long long ws = sp * 5ull, wt = t * 4ull;
+            u32 nt = gridDim.x;  // blocks on the tube queue
+            if (sp != 0) {
+                nt = t == 0 ? 0u : (u32)((wt * gridDim.x + (ws + wt) / 2) / (ws + wt));
+                if (t != 0 && nt == 0) nt = 1;
+                if (nt >= gridDim.x && gridDim.x > 1) nt = gridDim.x - 1;
+            }
+            s_split = nt;
+        }
+    }
+    __syncthreads();
+    const u32 nt = s_split;
+    if (blockIdx.x < nt) wf_exact_body<0, GEOM, PACKED>(A, par, V, blockIdx.x, nt);
+    else wf_exact_body<1, GEOM, PACKED>(A, par, V, blockIdx.x - nt, gridDim.x - nt);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1934,14 +1976,10 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
             if (packed) LVX_CUDA_CHECK(wf_launch(pdl, wf_cand_kernel<true>, grid_q, kThreadsWf, 0, st, A));
             else LVX_CUDA_CHECK(wf_launch(pdl, wf_cand_kernel<false>, grid_q, kThreadsWf, 0, st, A));
             WF_DEBUG_SYNC("candidates");
-            if (geom) LVX_CUDA_CHECK(wf_launch(pdl, wf_exact_kernel<0, true, false>, grid_q, kThreadsExact, 0, st, A, par));
-            else if (packed) LVX_CUDA_CHECK(wf_launch(pdl, wf_exact_kernel<0, false, true>, grid_q, kThreadsExact, 0, st, A, par));
-            else LVX_CUDA_CHECK(wf_launch(pdl, wf_exact_kernel<0, false, false>, grid_q, kThreadsExact, 0, st, A, par));
-            WF_DEBUG_SYNC("exact<tube>");
-            if (params->joints && geom) LVX_CUDA_CHECK(wf_launch(pdl, wf_exact_kernel<1, true, false>, grid_q, kThreadsExact, 0, st, A, par));
-            else if (params->joints && packed) LVX_CUDA_CHECK(wf_launch(pdl, wf_exact_kernel<1, false, true>, grid_q, kThreadsExact, 0, st, A, par));
-            else if (params->joints) LVX_CUDA_CHECK(wf_launch(pdl, wf_exact_kernel<1, false, false>, grid_q, kThreadsExact, 0, st, A, par));
-            WF_DEBUG_SYNC("exact<sphere>");
+            if (geom) LVX_CUDA_CHECK(wf_launch(pdl, wf_exact_kernel<true, false>, grid_q, kThreadsExact, 0, st, A, par));
+            else if (packed) LVX_CUDA_CHECK(wf_launch(pdl, wf_exact_kernel<false, true>, grid_q, kThreadsExact, 0, st, A, par));
+            else LVX_CUDA_CHECK(wf_launch(pdl, wf_exact_kernel<false, false>, grid_q, kThreadsExact, 0, st, A, par));
+            WF_DEBUG_SYNC("exact");
             LVX_CUDA_CHECK(wf_launch(pdl, wf_composite_kernel, grid_rays, kThreadsWf, 0, st, A, par));
             WF_DEBUG_SYNC("composite");
             if (debug) {
