@@ -600,7 +600,7 @@ def run_ours(args, wl):
     del bits, b8, touched
     k1 = kern_ms if world == 1 else min(ev_ms(lambda: plan1.launch(img1, st1)) for _ in range(2))
     kname = "render_kernel" if plan.engine == "tile" else \
-        "wavefront frame: wf_init + N x (wf_walk, wf_cand, wf_exact<tube>, wf_exact<sphere>, wf_composite)"
+        "wavefront frame: wf_init + N x (wf_walk, wf_cand, wf_exact, wf_composite, wf_next)"
     roofline = {"bound": "hbm", "kernel": kname, "engine": plan.engine, "achieved": alg_bytes / k1 / 1e6, "peak": peak,
                 "unit": "GB/s", "frac": alg_bytes / k1 / 1e6 / peak, "traffic": None,
                 "peak_source": peak_src, "alg_bytes_per_launch": alg_bytes, "voxels_touched": n_vox,

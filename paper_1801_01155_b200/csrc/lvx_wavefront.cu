@@ -487,6 +487,9 @@ __global__ void __launch_bounds__(kThreadsWf) wf_init_kernel(const WfArgs A) {
 // items when the warp is converged again (end of the rays' batches): one global atomic and
 // one scan per warp instead of an allocation round trip inside the walk (neighbour mode).
 constexpr int kWalkStage = 176;
+#ifndef LVX_WF_FLUSH_SCAN
+#define LVX_WF_FLUSH_SCAN 1
+#endif
 struct __align__(16) WalkRec {
     u32 place, fresh;
     unsigned long long cell;  // (x + 1) | (y + 1) << 20 | (z + 1) << 40
@@ -533,6 +536,25 @@ __device__ __forceinline__ void walk_flush(const WfArgs &A, WalkStage &S, const 
             if (lane == 0) atomicOr(&A.ctl->err, 1u);
         } else {
             const u32 out0 = (u32)q * A.capq_item + base;
+#if LVX_WF_FLUSH_SCAN
+            // Items are expanded 32 at a time; the record that holds item j is found from the START FLAGS
+            // of the records in the batch (one warp reduction + a population count) instead of a binary
+            // search over the prefix array per item -- those eight dependent shared-memory loads were a
+            // fifth of this kernel's stall samples (profiles/r2_wavefront_hot_lines.txt, before).
+            u32 r_lo = 0;  // first record with items at or after the batch start (warp-uniform)
+            for (u32 b0 = 0; b0 < total; b0 += 32) {
+                // records whose first item lies in [b0, b0 + 32): at most 32 of them, starting at r_lo
+                const u32 r = r_lo + (u32)lane;
+                const u32 pr = r < n ? (u32)S.pre[warp][r] : 0xFFFFFFFFu;
+                const bool in_batch = pr >= b0 && pr < b0 + 32u;  // (pr < b0 only for r_lo itself, handled below)
+                const unsigned starts = __reduce_or_sync(FULL, in_batch ? 1u << (pr - b0) : 0u);
+                const u32 j = b0 + (u32)lane;
+                // item j belongs to the last record that starts at or before it: r_lo - 1 if none in the batch does
+                const u32 ahead = (u32)__popc(starts & (0xFFFFFFFFu >> (31 - lane)));
+                const u32 lo = r_lo + ahead - 1u;
+                r_lo += (u32)__popc(starts);
+                if (j >= total) continue;
+#else
             for (u32 j = (u32)lane; j < total; j += 32) {
                 // the record that holds item j: the last r with pre[r] <= j
                 u32 lo = 0, hi = n;
@@ -541,6 +563,7 @@ __device__ __forceinline__ void walk_flush(const WfArgs &A, WalkStage &S, const 
                     if ((u32)S.pre[warp][mid] <= j) lo = mid;
                     else hi = mid;
                 }
+#endif
                 const WalkRec w = S.rec[warp][lo];
                 u32 mm = w.fresh;
                 for (u32 k = j - (u32)S.pre[warp][lo]; k; --k) mm &= mm - 1;  // its k-th fresh voxel
@@ -2013,7 +2036,7 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
             return LVX_E_RANGE;
         }
         g_last_iterations = it;
-        g_last_launches = 2 + it * (params->joints ? 6 : 5);
+        g_last_launches = 2 + it * 5;  // begin, init + (walk, candidates, exact, composite, next) per iteration
         if (host[0] == 0) break;
         LVX_REQUIRE(it < 100000, "wavefront did not converge");
     }

@@ -42,8 +42,9 @@ def short(name):
         n = name.split("(")[0].split("::")[-1]
     n = n.replace("void ", "").replace("_kernel", "")
     if "wf_exact" in name:
-        t = name.split("wf_exact_kernel<")[1].split(">")[0].replace(" ", "")
-        n = "wf_exact<%s>" % {"0,0": "tube", "1,0": "sphere", "0,1": "tube,geom", "1,1": "sphere,geom"}.get(t, t)
+        t = name.split("wf_exact_kernel<")[1].split(">")[0].replace(" ", "").replace("(bool)", "")
+        # one launch for tubes and joint spheres since round 2; template arguments: geometry rays, packed records
+        n = "wf_exact" + {"0,0": "", "1,0": "<geom>", "0,1": "<packed>"}.get(t, "<%s>" % t)
     return n[:26]
 
 agg = collections.OrderedDict()

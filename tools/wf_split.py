@@ -7,7 +7,7 @@ frames = []; cur = []
 for r in rows[hi + 1:]:
     if len(r) <= vi: continue
     name = r[ki].split('(')[0].split('::')[-1].replace('wf_', '').replace('_kernel', '')
-    if 'wf_exact' in r[ki]: name = 'exact_t' if 'wf_exact_kernel<0' in r[ki] else 'exact_s'
+    if 'wf_exact' in r[ki]: name = 'exact'
     v = float(r[vi].replace(',', '')); v = v / 1e3 if r[ui] == 'ns' else (v * 1e3 if r[ui] == 'ms' else v)
     if name == 'begin':
         if cur: frames.append(cur)
