@@ -1023,6 +1023,16 @@ __device__ __forceinline__ void wf_exact_body(const WfArgs &A, int par, QueueVie
         const u32 seg = c.seg & 0x7FFFFFFFu;
         const u32 place = c.place;
         const WfRayDir rd = A.rdir[place];
+        // (the end of the walked range / the item's window are requested NOW, with the ray record: loaded
+        // where they are used they cost a second memory round trip after the intersection test)
+        double own_lo = 0.0, own_hi = 0.0;
+        if (neighbor) {
+            own_hi = A.span[R + place];
+        } else {
+            const double2 tr = A.item_t[c.aux];
+            own_lo = tr.x;
+            own_hi = tr.y;
+        }
         const double rdx = rd.dx, rdy = rd.dy, rdz = rd.dz;
         // the segment's endpoints as the reference's float32 arrays hold them, + attr | lid << 8
         float pa[3], pb[3];
@@ -1068,12 +1078,8 @@ __device__ __forceinline__ void wf_exact_body(const WfArgs &A, int par, QueueVie
         // parameter; the windows tile the walked range, so every hit entered inside the range
         // walked this iteration is owned by exactly one of this iteration's windows
         if (!hit) continue;
-        if (neighbor) {
-            if (!(rd.t_lo <= h.t_in && h.t_in < A.span[R + place])) continue;
-        } else {
-            const double2 tr = A.item_t[c.aux];
-            if (!(tr.x <= h.t_in && h.t_in < tr.y)) continue;
-        }
+        if (neighbor) own_lo = rd.t_lo;
+        if (!(own_lo <= h.t_in && h.t_in < own_hi)) continue;
         const u32 attr = rmeta & 0xFFu, lid = (rmeta >> 8) & 31u;
         double scale, alpha;
         lvx_shade_hit<GEOM>(A, ox, oy, oz, rdx, rdy, rdz, h, attr, scale, alpha);
