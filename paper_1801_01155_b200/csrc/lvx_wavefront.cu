@@ -325,14 +325,17 @@ __device__ __forceinline__ void queue_view_load(QueueView &v, const u32 *cnt, u3
     }
     __syncthreads();
 }
-__device__ __forceinline__ u32 queue_view_index(const QueueView &v, u32 f, u32 capq) {
-    int lo = 0, hi = kNQ;  // pre[lo] <= f < pre[hi]
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (v.pre[mid] <= f) lo = mid;
-        else hi = mid;
-    }
-    return (u32)lo * capq + (f - v.pre[lo]);
+// Global entry index of the 32 consecutive flat indices f0 + lane of a converged warp (f0 a multiple
+// of 32): the sub-queue of f0 is the number of boundaries at or below it -- two ballots instead of a
+// six-step binary search per lane -- and a lane steps on only when the warp's range runs into the
+// next sub-queue.  (Lanes past the end of the queue get an index they must not use.)
+__device__ __forceinline__ u32 queue_view_index_warp(const QueueView &v, u32 f0, int lane, u32 capq) {
+    const unsigned b1 = __ballot_sync(0xFFFFFFFFu, v.pre[lane + 1] <= f0);                 // boundaries 1 .. 32
+    const unsigned b2 = __ballot_sync(0xFFFFFFFFu, lane < 31 && v.pre[lane + 33] <= f0);   // 33 .. 63
+    u32 lo = (u32)(__popc(b1) + __popc(b2));
+    const u32 f = f0 + (u32)lane;
+    while (lo + 1 < (u32)kNQ && v.pre[lo + 1] <= f) ++lo;
+    return lo * capq + (f - v.pre[lo]);
 }
 
 __device__ __forceinline__ void ray_dir(const lvx_camera &cam, int x, int y, double &ddx, double &ddy,
@@ -572,10 +575,12 @@ __device__ __forceinline__ void walk_flush(const WfArgs &A, WalkStage &S, const 
                           wz = (int)(w.cell >> 40) - 1;
                 const int bz_ = b / 9, by_ = (b - 9 * bz_) / 3, bx_ = b - 9 * bz_ - 3 * by_;
                 // (voxel-local frame for the conservative pre-reject)
+                // {place, x | y << 16, z | qx << 16, qy | qz << 16}: the voxel's coordinates rather than its
+                // linear index (the pre-reject wants both; two multiplies there instead of two divisions)
                 A.item[out0 + j] = make_uint4(
-                    w.place, (u32)((wx + bx_ - 1) + A.rx * ((wy + by_ - 1) + A.ry * (wz + bz_ - 1))),
-                    item_q16(w.qx - (float)(bx_ - 1)) | (item_q16(w.qy - (float)(by_ - 1)) << 16),
-                    item_q16(w.qz - (float)(bz_ - 1)));
+                    w.place, (u32)(wx + bx_ - 1) | ((u32)(wy + by_ - 1) << 16),
+                    (u32)(wz + bz_ - 1) | (item_q16(w.qx - (float)(bx_ - 1)) << 16),
+                    item_q16(w.qy - (float)(by_ - 1)) | (item_q16(w.qz - (float)(bz_ - 1)) << 16));
                 // own-voxel mode: only the window of the voxel itself gathers it (:797-799)
                 if (ST) A.item_t[out0 + j] = ST->t[warp][lo];
             }
@@ -910,7 +915,6 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_CAND_MINB) wf_cand_kernel(c
     const bool nbr = A.p.neighbor != 0;
     const float reach_pt = (float)A.p.tube_r + kRejectMarginWf + kItemQSlack;
     const u32 stride = gridDim.x * blockDim.x;
-    const u32 plane = (u32)A.rx * (u32)A.ry;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (lane == 0) {
         S.n_tube[warp] = 0;
@@ -925,19 +929,24 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_CAND_MINB) wf_cand_kernel(c
         if (S.n_tube[warp] > (u32)kStageTube / 2 || S.n_sph[warp] > (u32)kStageSph / 2) cand_flush(A, S, warp, lane, q);
         const u32 f = f0 + (u32)lane;
         CandItem I[2];
-        u32 lin[2], place[2];
+        u32 lin[2], place[2], hx[2], hy[2], hz[2];
         float4 q0[2];
         bool have[2];
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
             const u32 fk = f + (u32)k * stride;
             have[k] = fk < total;
-            I[k].it = queue_view_index(V, have[k] ? fk : 0u, A.capq_item);
+            const u32 it_w = queue_view_index_warp(V, f0 + (u32)k * stride, lane, A.capq_item);
+            I[k].it = have[k] ? it_w : 0u;
             const uint4 itm = A.item[I[k].it];
             place[k] = itm.x;
             I[k].place = place[k];
-            lin[k] = itm.y;
-            q0[k] = make_float4(item_unq16(itm.z), item_unq16(itm.z >> 16), item_unq16(itm.w), 0.0f);
+            // voxel coordinates (16 bits each) and the ray point in the voxel's frame (wf_item)
+            hx[k] = itm.y & 0xFFFFu;
+            hy[k] = itm.y >> 16;
+            hz[k] = itm.z & 0xFFFFu;
+            lin[k] = hx[k] + (u32)A.rx * (hy[k] + (u32)A.ry * hz[k]);
+            q0[k] = make_float4(item_unq16(itm.z >> 16), item_unq16(itm.w), item_unq16(itm.w >> 16), 0.0f);
         }
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
@@ -955,10 +964,9 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_CAND_MINB) wf_cand_kernel(c
         float ea[2][3], eb[2][3], hl[2];
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-            const u32 hz = lin[k] / plane, hy = (lin[k] - hz * plane) / (u32)A.rx, hx = lin[k] - hz * plane - hy * (u32)A.rx;
-            I[k].fhx = (float)hx;
-            I[k].fhy = (float)hy;
-            I[k].fhz = (float)hz;
+            I[k].fhx = (float)hx[k];
+            I[k].fhy = (float)hy[k];
+            I[k].fhz = (float)hz[k];
             I[k].q0x = q0[k].x;
             I[k].q0y = q0[k].y;
             I[k].q0z = q0[k].z;
@@ -1017,9 +1025,14 @@ __device__ __forceinline__ void wf_exact_body(const WfArgs &A, int par, QueueVie
     const size_t R = A.R;
     const WfEntry *queue = KIND == 0 ? A.tube : A.sph;
     const bool neighbor = A.p.neighbor != 0;
-    for (u32 f = block * blockDim.x + threadIdx.x; f < total; f += n_blocks * blockDim.x) {
+    // (the loop bound is warp-uniform: the queue index is found by the converged warp)
+    for (u32 f0 = block * blockDim.x + (threadIdx.x & ~31u); f0 < total; f0 += n_blocks * blockDim.x) {
+        __syncwarp();
+        const u32 f = f0 + (threadIdx.x & 31u);
+        const u32 qi = queue_view_index_warp(V, f0, (int)(threadIdx.x & 31u), A.capq_surv);
+        if (f >= total) continue;
         const int q = warp_queue(f);
-        const WfEntry c = queue[queue_view_index(V, f, A.capq_surv)];
+        const WfEntry c = queue[qi];
         const u32 seg = c.seg & 0x7FFFFFFFu;
         const u32 place = c.place;
         const WfRayDir rd = A.rdir[place];
@@ -1428,19 +1441,26 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_COMP_MINB) wf_composite_ker
                 // the usual heavy ray: every hit sits in a slot and none is dropped, so hit j IS slot j --
                 // nothing is listed by the ray's own lane, the ranks go straight into the ray's
                 // byte column (no copy into its local array either)
+                // (t_in >= 0, and + 0.0 makes a -0.0 a +0.0: the order of the doubles is the order of their
+                // bit patterns, so (t_in, key >> 8) is ONE 128-bit unsigned comparison -- no FP64-pipe
+                // compares in the m x m loop)
                 for (u32 j = lane; j < nhL; j += 32) {
                     const double2 v = *reinterpret_cast<const double2 *>(A.hit_slot + (size_t)j * R + placeL);
-                    Q.t[warp][j] = v.x;
-                    Q.k[warp][j] = (unsigned long long)__double_as_longlong(v.y);
+                    Q.t[warp][j] = v.x + 0.0;
+                    Q.k[warp][j] = (unsigned long long)__double_as_longlong(v.y) >> 8;
                 }
                 __syncwarp();
                 for (u32 j = lane; j < nhL; j += 32) {
-                    const double t = Q.t[warp][j];
-                    const unsigned long long k2 = Q.k[warp][j];
+                    const unsigned __int128 mine = ((unsigned __int128)(unsigned long long)__double_as_longlong(Q.t[warp][j]) << 64) |
+                                                   Q.k[warp][j];
                     u32 rank = 0;
-                    for (u32 q = 0; q < nhL; ++q) rank += wf_before(Q.t[warp][q], Q.k[warp][q], t, k2) ? 1u : 0u;
-                    // (keys are unique: a permutation)
-                    O8[rank][(warp << 5) + L] = (unsigned char)(j | (((k2 >> 18) & 1ull) ? 0x80u : 0u));
+                    for (u32 q = 0; q < nhL; ++q) {
+                        const unsigned __int128 other =
+                            ((unsigned __int128)(unsigned long long)__double_as_longlong(Q.t[warp][q]) << 64) | Q.k[warp][q];
+                        rank += other < mine ? 1u : 0u;
+                    }
+                    // (keys are unique: a permutation; bit 18 of the key -- joint sphere -- is bit 10 here)
+                    O8[rank][(warp << 5) + L] = (unsigned char)(j | (((Q.k[warp][j] >> 10) & 1ull) ? 0x80u : 0u));
                 }
                 if (lane == L) n = (int)nhL;
                 __syncwarp();
@@ -1831,7 +1851,8 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     LVX_REQUIRE(model->rx >= 1 && model->ry >= 1 && model->rz >= 1 && model->counts_d && model->offsets_d &&
                     model->table_d,
                 "bad model");
-    LVX_REQUIRE(model->rx < 65535 && model->ry < 65535 && (i64)model->rx * model->ry * model->rz < ((i64)1 << 31),
+    LVX_REQUIRE(model->rx < 65535 && model->ry < 65535 && model->rz < 65535 &&
+                    (i64)model->rx * model->ry * model->rz < ((i64)1 << 31),
                 "grid too large to render");
     LVX_REQUIRE(!params->neighbor || (model->nsum_d && model->nmask_d && model->ncell_d),
                 "neighbour mode needs the neighbour grids (lvx_neighbor_sums, with the merged cells)");
