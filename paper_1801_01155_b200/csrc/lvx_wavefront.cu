@@ -833,6 +833,7 @@ __device__ __forceinline__ void cand_segment(const WfArgs &A, CandStage &S, int 
         }
     }
     const unsigned act = __activemask();
+    if (!__any_sync(act, mk != 0)) return;  // (the usual case: one vote instead of three ballots)
     const unsigned bt = __ballot_sync(act, (mk & 1u) != 0);
     const unsigned ba = __ballot_sync(act, (mk & 2u) != 0), bb = __ballot_sync(act, (mk & 4u) != 0);
     if ((bt | ba | bb) == 0) return;
