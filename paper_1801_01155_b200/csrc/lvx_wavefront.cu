@@ -939,7 +939,10 @@ __global__ void __launch_bounds__(kThreadsWf, LVX_WF_CAND_MINB) wf_cand_kernel(c
             have[k] = fk < total;
             const u32 it_w = queue_view_index_warp(V, f0 + (u32)k * stride, lane, A.capq_item);
             I[k].it = have[k] ? it_w : 0u;
-            const uint4 itm = A.item[I[k].it];
+            // (a lane past the end of the queue reads item 0, which may be stale: its fields are not used
+            // as addresses)
+            uint4 itm = A.item[I[k].it];
+            if (!have[k]) itm = make_uint4(0u, 0u, 0u, 0u);
             place[k] = itm.x;
             I[k].place = place[k];
             // voxel coordinates (16 bits each) and the ray point in the voxel's frame (wf_item)
