@@ -179,9 +179,12 @@ def _staged_upload(torch, src, dst):
     evs[1].synchronize()
 
 
-def to_device(a: np.ndarray, dtype=None):
+def to_device(a: np.ndarray, dtype=None, pad: int = 0):
     """Host numpy -> device tensor on the current stream.  numpy memory is pageable: large arrays
-    go through cached pinned staging buffers, small ones through the driver's pageable path."""
+    go through cached pinned staging buffers, small ones through the driver's pageable path.
+    pad > 0 (1-D arrays): the device buffer is `pad` zeroed elements longer than the array and a view
+    of the array's part is returned -- for arrays the kernels read in aligned words past their end
+    (the encoded records: include/linevox_b200.h)."""
     torch = require_device()
     a = np.ascontiguousarray(a, dtype=dtype)
     if a.dtype == np.uint32:  # torch's unsigned support is partial: ship the bit pattern
@@ -197,6 +200,17 @@ def to_device(a: np.ndarray, dtype=None):
             t = torch.from_numpy(a)
     else:
         t = torch.from_numpy(a)
+    if pad:
+        if t.dim() != 1:
+            raise ValueError("padding is for 1-D arrays")
+        buf = torch.empty(t.numel() + int(pad), dtype=t.dtype, device="cuda")
+        buf[t.numel():].zero_()
+        out = buf[:t.numel()]
+        if a.nbytes < _STAGE_MIN or os.environ.get("LVX_H2D") == "pageable":
+            out.copy_(t)
+        else:
+            _staged_upload(torch, t, out)
+        return out
     if a.nbytes < _STAGE_MIN or os.environ.get("LVX_H2D") == "pageable":
         return t.to("cuda", non_blocking=False)
     out = torch.empty(t.shape, dtype=t.dtype, device="cuda")

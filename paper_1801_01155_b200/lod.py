@@ -143,7 +143,8 @@ def _density_by_seg_voxel(model: VoxelModel, out):
     counts = torch.bincount(lin, minlength=V)
     offsets = (torch.cumsum(counts, 0) - counts).to(torch.int32)
     table = _lib.to_device(np.ascontiguousarray(model.transfer_table, dtype=np.float32))
-    _lib.check(L.lvx_density_l0_u32(_lib.ptr(counts.to(torch.int32)), _lib.ptr(offsets), _lib.ptr(rec),
+    counts32 = counts.to(torch.int32)  # (held until the call is queued: a temporary is freed before the launch)
+    _lib.check(L.lvx_density_l0_u32(_lib.ptr(counts32), _lib.ptr(offsets), _lib.ptr(rec),
                                     _lib.ptr(table), C.c_int64(V), _lib.ptr(out), st))
     return out
 

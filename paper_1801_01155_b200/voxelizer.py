@@ -187,7 +187,8 @@ def clip_batch_device(pts, attrs, off, dims):
     pts_d, attrs_d = _lib.to_device(pts), _lib.to_device(np.ascontiguousarray(attrs, dtype=np.float64))
     off = np.ascontiguousarray(off, dtype=np.int64)
     first = torch.empty(max(P, 1), dtype=torch.uint8, device="cuda")
-    _lib.check(L.lvx_mark_curve_starts(_lib.ptr(_lib.to_device(off)), C.c_int64(off.size - 1), C.c_int64(P),
+    off_dev = _lib.to_device(off)  # (held until the call is queued: a temporary is freed before the launch)
+    _lib.check(L.lvx_mark_curve_starts(_lib.ptr(off_dev), C.c_int64(off.size - 1), C.c_int64(P),
                                        _lib.ptr(first), st))
     bound = torch.zeros(1, dtype=torch.int64, device="cuda")
     _lib.check(L.lvx_voxelize_bound(_lib.ptr(pts_d), _lib.ptr(first), C.c_int64(P), _lib.ptr(bound), st))
@@ -288,6 +289,8 @@ class VoxelModel:
             self._host[name] = arr
             self._dev.pop(name, None)
         else:
+            if name == "packed":
+                value = _padded_device_bytes(value)
             self._dev[name] = value
             self._host.pop(name, None)
         self._decoded.discard(name)  # now user-supplied
@@ -407,7 +410,8 @@ class VoxelModel:
         """Device tensor of one array field (uploaded from the host copy if needed)."""
         d = self._dev.get(name)
         if d is None:
-            d = _lib.to_device(self._get_array(name))
+            # (the kernels read the encoded records in aligned 8-byte words: up to 7 bytes past the end)
+            d = _lib.to_device(self._get_array(name), pad=8 if name == "packed" else 0)
             self._dev[name] = d
         return d
 
@@ -525,6 +529,23 @@ class VoxelModel:
 
 # ---------------------------------------------------------------------------------
 
+def _padded_device_bytes(t, spare: int = 8):
+    """A device byte tensor whose storage extends at least `spare` bytes past its end (the kernels
+    that decode the encoded records read aligned 8-byte words): the tensor itself when its storage
+    already does, else a copy into a longer buffer."""
+    import torch
+    t = t.reshape(-1)
+    if not t.is_contiguous():
+        t = t.contiguous()
+    end = (t.storage_offset() + t.numel()) * t.element_size()
+    if t.untyped_storage().nbytes() - end >= spare:
+        return t
+    buf = torch.empty(t.numel() + spare, dtype=t.dtype, device=t.device)
+    buf[t.numel():].zero_()
+    buf[:t.numel()].copy_(t)
+    return buf[:t.numel()]
+
+
 def _scratch(n):
     import torch
     nbytes = int(_lib.lib().lvx_scan_scratch_bytes(C.c_int64(max(int(n), 1))))
@@ -582,9 +603,10 @@ def stage_scan(vox_cnt):
     offsets = torch.empty(V, dtype=torch.int32, device="cuda")  # u32 bit pattern
     counts = torch.empty(V, dtype=torch.uint8, device="cuda")
     totals = torch.zeros(2, dtype=torch.int64, device="cuda")
+    scratch = _scratch(V)  # (held until the call is queued: a temporary is freed before the launch)
     _lib.check(_lib.lib().lvx_voxel_scan(_lib.ptr(vox_cnt), C.c_int64(V), _lib.ptr(cursor),
                                          _lib.ptr(offsets), _lib.ptr(counts), _lib.ptr(totals),
-                                         _lib.ptr(_scratch(V)), _lib.stream_ptr()))
+                                         _lib.ptr(scratch), _lib.stream_ptr()))
     n_raw, S = (int(x) for x in totals.cpu().tolist())
     if n_raw >= 2 ** 32:
         raise MemoryError(f"{n_raw} chords exceed the 32-bit offsets of the voxel headers")
@@ -600,7 +622,8 @@ def stage_compact(grouped, n_raw: int, vox_cnt, cursor_end, offsets, counts,
     dev = "cuda"
     out = {
         "counts": counts, "offsets": offsets,
-        "packed": torch.empty(m * w, dtype=torch.uint8, device=dev),
+        # (+ 8: the kernels that decode the records read aligned 8-byte words, up to 7 bytes past the end)
+        "packed": torch.empty(m * w + 8, dtype=torch.uint8, device=dev)[:m * w],
         "seg_rec": torch.empty((m, 8), dtype=torch.float32, device=dev),
     }
     if caches:
@@ -639,8 +662,9 @@ def stage_provenance(seg_key, S: int, edge_kept, off_d, n_curves: int):
         P = int(edge_kept.shape[0])
         edge_base = torch.empty(P, dtype=torch.int32, device="cuda")
         L, st = _lib.lib(), _lib.stream_ptr()
+        scratch = _scratch(P)
         _lib.check(L.lvx_scan_u16(_lib.ptr(edge_kept), C.c_int64(P), _lib.ptr(edge_base),
-                                  _lib.ptr(_scratch(P)), st))
+                                  _lib.ptr(scratch), st))
         _lib.check(L.lvx_provenance(_lib.ptr(seg_key), C.c_int64(S), _lib.ptr(edge_base),
                                     _lib.ptr(off_d), C.c_int64(n_curves), _lib.ptr(seg_curve),
                                     _lib.ptr(seg_order), st))
