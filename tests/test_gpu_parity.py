@@ -178,6 +178,30 @@ def test_odd_image_sizes_and_determinism(lv, oracle, synth):
         assert fr.stats["intersection_tests"] == st["intersection_tests"]
 
 
+def test_small_frames_after_a_frame_on_a_larger_grid(lv, oracle, synth):
+    """The frame scratch (queues, per-ray state) is reused between frames: a tiny frame on a small grid
+    right after a frame on a larger one must not pick up anything of it -- lanes past the end of a queue
+    once used a stale item's voxel as an address.  Both record sources, both modes."""
+    big = (96, 96, 96)
+    mb = lv.build_voxel_model(lv.CurveSet.from_flat(*synth.turbulence(3000, 60, big)), lv.GridSpec(big))
+    dims = (10, 9, 7)
+    m, ref = both(lv, oracle, synth.wiggles(120, 30, dims), dims)
+    enc = lv.VoxelModel(spec=m.spec, counts=m.counts.copy(), offsets=m.offsets.copy(), packed=m.packed.copy(),
+                        transfer_table=m.transfer_table)
+    levels = oracle.build_octree(oracle.compute_density_level0(ref))
+    for nb in (True, False):
+        mode = "on" if nb else "off"
+        for (W, H) in ((1, 1), (7, 5), (130, 3)):
+            lv.render_frame(lv.default_camera(big, 320, 200), mb, None, None, lv.RenderParams(base_opacity=0.3, neighbor_mode=mode))
+            img, st = oracle.render(oracle.default_camera(dims, W, H), ref, levels, base_opacity=0.5, neighbor=nb)
+            for model in (m, enc):
+                fr = lv.render_frame(lv.default_camera(dims, W, H), model, None, None,
+                                     lv.RenderParams(base_opacity=0.5, neighbor_mode=mode))
+                assert np.abs(fr.image - img).max() <= MAX_ERR
+                assert fr.stats["voxel_steps"] == st["voxel_steps"]
+                assert fr.stats["intersection_tests"] == st["intersection_tests"]
+
+
 def test_camera_inside_grid_and_auto_neighbor(lv, oracle, synth):
     dims = (12, 12, 12)
     m, ref = both(lv, oracle, synth.turbulence(200, 60, dims), dims)

@@ -20,4 +20,4 @@ pr = cProfile.Profile(); pr.enable()
 for _ in range(20):
     fr = lv.render_frame(cam, m, oc, None, p)
 pr.disable()
-pstats.Stats(pr).sort_stats("cumulative").print_stats(18)
+pstats.Stats(pr).sort_stats("tottime").print_stats(40)
