@@ -182,6 +182,7 @@ struct WfCtl {
     u32 wn;    // windows per ray of the current iteration
     u32 budget;  // candidate budget per ray of the current iteration (neighbour-sum units)
     u32 live0;   // rays alive after the first iteration (what "few rays left" is measured against)
+    u32 done_it;  // the iteration count the frame needed (set once, when the live list first comes up empty)
 #ifdef LVX_WF_STATS
     unsigned long long dbg[8];  // developer counters: owned hits, composited, suppressed, rays with hits, terminated
 #endif
@@ -1661,6 +1662,7 @@ __global__ void wf_next_kernel(const WfArgs A, int par, int it_next) {
     if (t == 0) {
         A.ctl->n_live[par] = 0;
         const u32 live = A.ctl->n_live[par ^ 1];
+        if (live == 0 && A.ctl->done_it == 0) A.ctl->done_it = (u32)it_next;
         u32 wn = (u32)A.wn_sched << (it_next < A.wn_shift_max ? it_next : A.wn_shift_max);
         const u32 fit = live ? A.cap_win / live : A.cap_win;
         if (wn > fit) wn = fit;
@@ -1705,6 +1707,7 @@ __global__ void wf_begin_kernel(const WfArgs A) {
         A.ctl->n_live[1] = 0;
         A.ctl->pool_cnt = 0;
         A.ctl->err = 0;
+        A.ctl->done_it = 0;
 #ifdef LVX_WF_STATS
         for (int k = 0; k < 8; ++k) A.ctl->dbg[k] = 0;
 #endif
@@ -1799,6 +1802,7 @@ struct WfTuning {
     int rays_mult = 0;  // 0: by the number of ray slots
     bool debug = false;
     bool pdl = true;  // programmatic dependent launch of the frame's kernels (LVX_WF_PDL=0: plain launches)
+    bool adaptive_burst = true;  // first burst sized by the previous frame's iteration count (LVX_WF_ADAPT=0: always six)
 };
 
 int env_int(const char *name, int dflt, bool positive_only = false) {
@@ -1823,6 +1827,7 @@ const WfTuning &wf_tuning() {
         t.rays_mult = env_int("LVX_WF_GRID_RAYS", t.rays_mult, true);
         t.debug = getenv("LVX_WF_DEBUG") != nullptr;
         t.pdl = env_int("LVX_WF_PDL", 1) != 0;
+        t.adaptive_burst = env_int("LVX_WF_ADAPT", 1) != 0;
         return t;
     }();
     return T;
@@ -1831,6 +1836,7 @@ const WfTuning &wf_tuning() {
 }  // namespace
 
 static thread_local int g_last_launches = 0, g_last_iterations = 0;
+static thread_local int g_needed_iterations = 0;  // of this thread's previous frame (sizes the next frame's first burst)
 
 extern "C" {
 
@@ -2010,11 +2016,16 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     LVX_LAUNCH_CHECK();
     u32 host[4] = {0, 0, 0, 0};
     int it = 0;
+    const int first_burst = tune.adaptive_burst ? (g_needed_iterations < 48 ? g_needed_iterations : 48) : 0;
     g_last_launches = 2;
     for (;;) {
-        // bursts of six iterations between looks at the live-ray count: a frame like C3 (10 iterations)
-        // costs one host read-back instead of three; an iteration without rays is six empty launches
-        const int burst = 6;
+        // bursts of iterations between looks at the live-ray count: six at a time (a frame like C3, 10
+        // iterations, costs two host read-backs instead of ten; an iteration without rays is five empty
+        // launches).  The FIRST burst is as long as the previous frame of this thread turned out to be --
+        // consecutive frames of an interactive session need the same number of iterations give or take
+        // one --, so a steady sequence of frames reads the count back once, at the end, and launches
+        // nothing in vain; a wrong guess costs a few empty launches or one more burst, never a result.
+        const int burst = it == 0 && first_burst > 6 ? first_burst : 6;
         for (int b = 0; b < burst; ++b, ++it) {
             const int par = it & 1;
 #define WF_DEBUG_SYNC(name)                                                                   \
@@ -2061,12 +2072,14 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
         // rays left?  (n_live of the list the next iteration reads, and the error bits)
         LVX_CUDA_CHECK(cudaMemcpyAsync(&host[0], &A.ctl->n_live[it & 1], 4, cudaMemcpyDeviceToHost, st));
         LVX_CUDA_CHECK(cudaMemcpyAsync(&host[1], &A.ctl->err, 4, cudaMemcpyDeviceToHost, st));
+        LVX_CUDA_CHECK(cudaMemcpyAsync(&host[2], &A.ctl->done_it, 4, cudaMemcpyDeviceToHost, st));
         LVX_CUDA_CHECK(cudaStreamSynchronize(st));
         if (host[1]) {
             lvx_set_error("wavefront queues overflowed (bits %u): retry with a larger scratch scale", host[1]);
             return LVX_E_RANGE;
         }
         g_last_iterations = it;
+        g_needed_iterations = host[2] ? (int)host[2] : it;
         g_last_launches = 2 + it * 5;  // begin, init + (walk, candidates, exact, composite, next) per iteration
         if (host[0] == 0) break;
         LVX_REQUIRE(it < 100000, "wavefront did not converge");
