@@ -21,6 +21,9 @@ constexpr double kFaceEps = 1e-9;   // voxelizer.py:361
 #define LVX_CLIP_THREADS 128
 #endif
 constexpr int kClipThreads = LVX_CLIP_THREADS;
+#ifndef LVX_CLIP_TILE
+#define LVX_CLIP_TILE 1  // chords built crossing-parallel from a shared-memory tile of events (0: edge-parallel)
+#endif
 
 struct Event {
     double pos[3];
@@ -89,16 +92,13 @@ __device__ __forceinline__ i64 chord_voxel(const Event &a, const Event &b, int r
         double dd = fabs(b.pos[c] - a.pos[c]);
         m = dd > m ? dd : m;
     }
-    long long vo = (long long)(b.up ? b.k - 1.0 : b.k);
-    long long vi = (long long)(a.up ? a.k : a.k - 1.0);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        if (c == b.ax) vox[c] = vo;
-    }
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        if (c == a.ax) vox[c] = vi;
-    }
+    const long long vo = (long long)(b.up ? b.k - 1.0 : b.k);
+    const long long vi = (long long)(a.up ? a.k : a.k - 1.0);
+    // (selects on the three components, the entry event's axis last: indexing vox[] by a run-time axis
+    // puts the array in local memory)
+    vox[0] = a.ax == 0 ? vi : (b.ax == 0 ? vo : vox[0]);
+    vox[1] = a.ax == 1 ? vi : (b.ax == 1 ? vo : vox[1]);
+    vox[2] = a.ax == 2 ? vi : (b.ax == 2 ? vo : vox[2]);
     if (!(m > kMinChord)) return -1;
     if (vox[0] < 0 || vox[0] >= rx || vox[1] < 0 || vox[1] >= ry || vox[2] < 0 || vox[2] >= rz)
         return -1;
@@ -274,15 +274,69 @@ __device__ __forceinline__ int clip_edge(const ClipView &V, i64 i, const EdgeAxe
     return kept;
 }
 
+// The edge-parallel path as a call of its own (a block with more than kTileEvents crossings: rare): it
+// takes scalars only and rebuilds the edge from the staged vertices, so nothing of the caller's state has
+// to live in local memory for it.
+__device__ __noinline__ int clip_edge_call(const ClipStage *S, const double *pts, const double *attrs, const u8 *first,
+                                           i64 base, i64 hi, i64 i, int rx, int ry, int rz, int n_bins,
+                                           u32 *__restrict__ vox_cnt, u64 *__restrict__ raw_key,
+                                           u64 *__restrict__ raw_q, u32 *__restrict__ raw_lin, u64 slot0,
+                                           int *__restrict__ err) {
+    const ClipView V = {*S, pts, attrs, first, base, hi};
+    double a0[3], a1[3];
+    V.vertex(i, a0);
+    V.vertex(i + 1, a1);
+    EdgeAxes E;
+    E.init(a0, a1);
+    return clip_edge(V, i, E, a0, rx, ry, rz, n_bins, vox_cnt, raw_key, raw_q, raw_lin, slot0, err);
+}
+
 #ifndef LVX_CLIP_MINB
 #define LVX_CLIP_MINB 8
 #endif
+// The plane-crossing events of a block's edges, in the reference's order (slot order = edge order, then
+// the merged (s, axis) order inside an edge), staged in shared memory: every event is computed ONCE, by
+// its edge, and every chord -- the pair (event e-1, event e) of one curve -- is then built by its own
+// thread, so the chord half of the work (voxel, keep test, two face/bin quantisations, attribute, the
+// three stores and the counter) runs with all lanes busy however the crossings are spread over the
+// edges (0-3 per edge on the bench scenes: the edge-parallel version ran at 15.8 of 32 lanes and
+// computed the last event of every edge twice, once more by the look-back of its successor).
+#ifndef LVX_CLIP_TILE_EVENTS
+#define LVX_CLIP_TILE_EVENTS 512
+#endif
+constexpr int kTileEvents = LVX_CLIP_TILE_EVENTS;  // a block whose edges cross more planes takes the edge-parallel path
+static_assert(kClipThreads <= 128, "block-local edge and curve-start indices are bytes with 0xFF reserved");
+struct ClipTile {
+    // (slot kTileEvents: the predecessor of the block's first event when it lies in an earlier block)
+    double x[kTileEvents + 1], y[kTileEvents + 1], z[kTileEvents + 1], a[kTileEvents + 1];
+    u16 meta[kTileEvents + 1];    // edge (block-local) | axis << 8 | up << 10
+    u8 kept[kTileEvents];
+    u16 slot0[kClipThreads];      // first event slot of edge t (exclusive prefix of the crossing counts)
+    u8 cstart[kClipThreads];      // block-local index of the first point of edge t's curve; 0xFF: before the block
+};
+
+__device__ __forceinline__ void tile_event(const ClipTile &T, int e, Event &ev) {
+    const u32 m = T.meta[e];
+    ev.pos[0] = T.x[e];
+    ev.pos[1] = T.y[e];
+    ev.pos[2] = T.z[e];
+    ev.attr = T.a[e];
+    ev.ax = (int)((m >> 8) & 3u);
+    ev.up = ((m >> 10) & 1u) != 0;
+    ev.k = ev.ax == 0 ? ev.pos[0] : (ev.ax == 1 ? ev.pos[1] : ev.pos[2]);  // make_event: pos[ax] = k
+}
+
 __global__ void __launch_bounds__(kClipThreads, LVX_CLIP_MINB)
 clip_once_kernel(const double *__restrict__ pts, const double *__restrict__ attrs, const u8 *__restrict__ first,
                  i64 n_points, int rx, int ry, int rz, int n_bins, u64 capacity, u32 *__restrict__ vox_cnt,
                  u64 *__restrict__ raw_key, u64 *__restrict__ raw_q, u32 *__restrict__ raw_lin,
                  unsigned long long *__restrict__ n_slots, u16 *__restrict__ edge_kept, int *__restrict__ err) {
     __shared__ ClipStage S;
+#if LVX_CLIP_TILE
+    __shared__ ClipTile T;
+    __shared__ int s_cw[kClipThreads / 32];  // last curve start seen by each warp
+    __shared__ int s_prev0;                  // the block's first event has a predecessor outside the block
+#endif
     __shared__ u32 s_warp[kClipThreads / 32];
     __shared__ unsigned long long s_base;
     const i64 base = (i64)blockIdx.x * kClipThreads;
@@ -296,18 +350,20 @@ clip_once_kernel(const double *__restrict__ pts, const double *__restrict__ attr
     const ClipView V = {S, pts, attrs, first, base, hi};
     const i64 i = base + threadIdx.x;
     const bool edge = i + 1 < n_points && !S.first[threadIdx.x + 1];
-    double a0[3] = {0.0, 0.0, 0.0};
-    EdgeAxes E;
+    // (only the crossing count is carried over the block scan: the edge is set up again from the staged
+    // vertices where its events are listed -- six shared-memory loads and floors against ~25 registers
+    // held across two barriers)
     int crossings = 0;
     if (edge) {
-        double a1[3];
+        double a0[3], a1[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             a0[c] = S.pts[3 * threadIdx.x + c];
             a1[c] = S.pts[3 * (threadIdx.x + 1) + c];
         }
-        E.init(a0, a1);
-        crossings = E.total();
+        EdgeAxes E0;
+        E0.init(a0, a1);
+        crossings = E0.total();
     }
     // reserve one slot per plane crossing of the block (every chord ends at a crossing)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -318,6 +374,16 @@ clip_once_kernel(const double *__restrict__ pts, const double *__restrict__ attr
         if (lane >= o) inc += t;
     }
     if (lane == 31) s_warp[warp] = inc;
+#if LVX_CLIP_TILE
+    // the curve of edge t starts at the last first-point at or before t (running maximum over the block)
+    int cs = (i < n_points && S.first[threadIdx.x]) ? (int)threadIdx.x : -1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xFFFFFFFFu, cs, o);
+        if (lane >= o) cs = max(cs, t);
+    }
+    if (lane == 31) s_cw[warp] = cs;
+#endif
     __syncthreads();
     u32 before = 0, total = 0;
 #pragma unroll
@@ -327,12 +393,147 @@ clip_once_kernel(const double *__restrict__ pts, const double *__restrict__ attr
         total += t;
     }
     if (threadIdx.x == 0) s_base = total ? atomicAdd(n_slots, (unsigned long long)total) : 0ull;
+#if LVX_CLIP_TILE
+    if (total != 0 && total <= (u32)kTileEvents) {
+#pragma unroll
+        for (int w = 0; w < kClipThreads / 32; ++w) {
+            if (w < warp) cs = max(cs, s_cw[w]);
+        }
+        const u32 my0 = before + inc - (u32)crossings;
+        T.slot0[threadIdx.x] = (u16)my0;
+        T.cstart[threadIdx.x] = cs < 0 ? (u8)0xFF : (u8)cs;
+        if (threadIdx.x == 0) s_prev0 = 0;
+        __syncthreads();
+        const u64 blk0 = s_base;
+        if (blk0 + (u64)total > capacity) {  // the caller's bound was wrong
+            if (threadIdx.x == 0) *err = 2;
+            if (i < n_points && edge_kept) edge_kept[i] = 0;
+            return;
+        }
+        // A: every edge lists its own events in merged (s, axis) order (voxelizer.py:224)
+        if (crossings > 0) {
+            const double att0 = S.attr[threadIdx.x], att1 = S.attr[threadIdx.x + 1];
+            EdgeAxes E;
+            {
+                double a0[3], a1[3];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    a0[c] = S.pts[3 * threadIdx.x + c];
+                    a1[c] = S.pts[3 * (threadIdx.x + 1) + c];
+                }
+                E.init(a0, a1);
+            }
+            // (the plane of the next crossing is recomputed from its ordinal instead of being carried: the
+            // kernel is short of registers, not of integer-to-double conversions)
+            int j[3] = {0, 0, 0};
+            double s_next[3];
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) s_next[ax] = E.cnt[ax] > 0 ? E.param(ax, E.plane(ax, 0)) : 2.0;
+            Event ev;
+            for (int n = 0; n < crossings; ++n) {
+                int best = 0;
+                double bs = s_next[0];
+                if (s_next[1] < bs) {
+                    best = 1;
+                    bs = s_next[1];
+                }
+                if (s_next[2] < bs) {
+                    best = 2;
+                    bs = s_next[2];
+                }
+                const double bk = best == 0 ? E.plane(0, j[0]) : (best == 1 ? E.plane(1, j[1]) : E.plane(2, j[2]));
+                make_event(ev, E, E.x0, att0, att1, true, best, bk, bs);
+                const u32 e = my0 + (u32)n;
+                T.x[e] = ev.pos[0];
+                T.y[e] = ev.pos[1];
+                T.z[e] = ev.pos[2];
+                T.a[e] = ev.attr;
+                T.meta[e] = (u16)(threadIdx.x | ((u32)best << 8) | ((ev.up ? 1u : 0u) << 10));
+#pragma unroll
+                for (int ax = 0; ax < 3; ++ax) {
+                    if (ax == best) {
+                        j[ax] += 1;
+                        s_next[ax] = j[ax] < E.cnt[ax] ? E.param(ax, E.plane(ax, j[ax])) : 2.0;  // (valid s are <= 1)
+                    }
+                }
+            }
+        }
+        // the one event that may pair with an event of an earlier block: the block's first, when its curve
+        // began before the block (the look-back from the block's first point; the edges between that
+        // point and the event's own edge cross nothing)
+        if (crossings > 0 && my0 == 0 && cs < 0) {
+            Event p0;
+            if (lookback_event_v<true>(V, base, p0)) {
+                T.x[kTileEvents] = p0.pos[0];
+                T.y[kTileEvents] = p0.pos[1];
+                T.z[kTileEvents] = p0.pos[2];
+                T.a[kTileEvents] = p0.attr;
+                T.meta[kTileEvents] = (u16)(((u32)p0.ax << 8) | ((p0.up ? 1u : 0u) << 10));
+                s_prev0 = 1;
+            }
+        }
+        __syncthreads();
+        // B: one thread per chord
+        for (u32 e = threadIdx.x; e < total; e += kClipThreads) {
+            Event ev, prev;
+            tile_event(T, (int)e, ev);
+            const u32 il = T.meta[e] & 0xFFu;
+            bool have_prev;
+            if (e > 0) {
+                tile_event(T, (int)e - 1, prev);
+                have_prev = T.cstart[T.meta[e - 1] & 0xFFu] == T.cstart[il];  // same curve
+            } else {
+                have_prev = s_prev0 != 0;
+                if (have_prev) tile_event(T, kTileEvents, prev);
+            }
+            u32 out_lin = kNoVoxel;
+            u8 kept = 0;
+            if (have_prev) {
+                long long vox[3];
+                const i64 lin = chord_voxel(prev, ev, rx, ry, rz, vox);
+                if (lin >= 0) {
+                    // voxelizer.py:439 -- rint is round-half-even
+                    double av = rint(255.0 * 0.5 * (prev.attr + ev.attr));
+                    av = av < 0.0 ? 0.0 : (av > 255.0 ? 255.0 : av);
+                    u32 fin = face_and_bin(prev.pos, vox, n_bins);
+                    u32 fout = face_and_bin(ev.pos, vox, n_bins);
+                    if (fin == 0xFFFFFFFFu || fout == 0xFFFFFFFFu) {
+                        *err = 1;
+                        fin = fout = 0;
+                    }
+                    raw_q[blk0 + e] = (u64)fin | ((u64)fout << 19) | ((u64)(u32)av << 38);
+                    out_lin = (u32)lin;
+                    atomicAdd(&vox_cnt[lin], 1u);  // result unused: compiles to a reduction
+                    kept = 1;
+                }
+            }
+            raw_lin[blk0 + e] = out_lin;
+            T.kept[e] = kept;
+        }
+        __syncthreads();
+        // C: the key of a kept chord carries its ordinal among the kept chords of its edge
+        for (u32 e = threadIdx.x; e < total; e += kClipThreads) {
+            if (!T.kept[e]) continue;
+            const u32 il = T.meta[e] & 0xFFu;
+            u32 ord = 0;
+            for (u32 k = T.slot0[il]; k < e; ++k) ord += T.kept[k];
+            raw_key[blk0 + e] = ((u64)(base + il) << 16) | (u64)ord;
+        }
+        if (i < n_points && edge_kept) {
+            u32 kept = 0;
+            for (u32 k = 0; k < (u32)crossings; ++k) kept += T.kept[my0 + k];
+            edge_kept[i] = (u16)kept;
+        }
+        return;
+    }
+#endif
     __syncthreads();
     int kept = 0;
     if (crossings > 0) {
         const u64 slot0 = s_base + before + inc - (u32)crossings;
         if (slot0 + (u64)crossings > capacity) *err = 2;  // the caller's bound was wrong
-        else kept = clip_edge(V, i, E, a0, rx, ry, rz, n_bins, vox_cnt, raw_key, raw_q, raw_lin, slot0, err);
+        else kept = clip_edge_call(&S, pts, attrs, first, base, hi, i, rx, ry, rz, n_bins, vox_cnt, raw_key, raw_q,
+                                   raw_lin, slot0, err);
     }
     if (i < n_points && edge_kept) edge_kept[i] = (u16)kept;
 }

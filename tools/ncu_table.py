@@ -2,7 +2,7 @@
 
     python tools/ncu_table.py <raw.csv> [--by-launch] [--title "..."] [--out profiles/x.txt]
 Aggregates launches by kernel name (time-weighted means) and prints: launches, total ms, share,
-dram GB (read+write), dram GB/s and % of HBM peak, L2 GB (lts__t_bytes) and lts %, issue %, achieved
+dram GB (read+write), dram GB/s and % of HBM peak, L2 GB (lts__t_bytes, or lts__t_sectors x 32 B) and lts %, issue %, achieved
 warps %, lanes per instruction, fp64 / fma / alu / lsu pipe %, registers, top stall reasons.
 """
 import argparse, collections, csv, json, os, sys
@@ -24,7 +24,7 @@ def scale(name):
     return {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "tbyte": 1e12, "ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3,
             "ms": 1.0, "msecond": 1.0, "second": 1e3, "s": 1e3}.get(u, 1)
 
-M = {"ms": "gpu__time_duration.sum", "rd": "dram__bytes_read.sum", "wr": "dram__bytes_write.sum", "l2": "lts__t_bytes.sum",
+M = {"ms": "gpu__time_duration.sum", "rd": "dram__bytes_read.sum", "wr": "dram__bytes_write.sum", "l2": "lts__t_bytes.sum", "l2s": "lts__t_sectors.sum",
      "lts": "lts__throughput.avg.pct_of_peak_sustained_elapsed", "issue": "smsp__issue_active.avg.pct_of_peak_sustained_active",
      "warps": "sm__warps_active.avg.pct_of_peak_sustained_active", "lanes": "smsp__thread_inst_executed_per_inst_executed.ratio",
      "regs": "launch__registers_per_thread", "fp64": "sm__inst_executed_pipe_fp64.sum.pct_of_peak_sustained_active",
@@ -57,6 +57,9 @@ for i, r in enumerate(rows[2:]):
     for k in ("rd", "wr", "l2"):
         if k in M and d[M[k]] not in ("", "n/a"):
             e[k] += float(d[M[k]]) * scale(M[k])
+    # (--set full carries the L2 traffic as sectors, not bytes: 32 bytes each)
+    if "l2" not in M and "l2s" in M and d[M["l2s"]] not in ("", "n/a"):
+        e["l2"] += float(d[M["l2s"]].replace(",", "")) * 32.0
     for k in ("lts", "issue", "warps", "lanes", "fp64", "fp64b", "fma", "alu", "lsu", "l1hit", "l2hit"):
         if k in M and d[M[k]] not in ("", "n/a"):
             e[k] += float(d[M[k]]) * t
