@@ -145,6 +145,43 @@ def test_ragged_and_degenerate_inputs(lv, oracle):
     assert_model_equal(m, as_dict(ref))
 
 
+@pytest.mark.parametrize("seed", [0, 1])
+def test_clip_paths_long_edges_and_block_boundaries(lv, oracle, seed):
+    """The clip kernel builds chords from a shared-memory tile of a block's events (128 edges) and
+    falls back to the edge-parallel path when a block crosses more than 512 planes: mix curves of
+    2-5 vertices spanning the whole grid (hundreds of crossings per edge), dense short-edged curves,
+    two-vertex curves and curves without any crossing, at lengths that put curve ends on, next to
+    and far from the 128-edge block boundaries; provenance (edge, ordinal) included."""
+    rng = np.random.default_rng(100 + seed)
+    dims = (48, 40, 56)
+    hi = np.array(dims, dtype=np.float64)
+    curves = []
+    for k in range(220):
+        kind = rng.integers(0, 6)
+        if kind == 0:      # long edges: a few vertices anywhere in (and slightly outside) the grid
+            c = rng.uniform(-2.0, hi + 2.0, (int(rng.integers(2, 6)), 3))
+        elif kind == 1:    # short steps: a random walk of 100-300 vertices
+            n = int(rng.integers(100, 300))
+            c = rng.uniform(2.0, hi - 2.0, (1, 3)) + np.cumsum(rng.normal(0.0, 0.45, (n, 3)), axis=0)
+        elif kind == 2:    # exactly one block of edges / one less / one more
+            n = int(rng.choice([128, 129, 130, 127, 256, 257]))
+            c = rng.uniform(2.0, hi - 2.0, (1, 3)) + np.cumsum(rng.normal(0.0, 0.3, (n, 3)), axis=0)
+        elif kind == 3:    # the shortest curve the API accepts: two vertices (one edge, zero to a few crossings)
+            c = rng.uniform(0.0, hi, (1, 3)) + rng.normal(0.0, 0.8, (2, 3))
+        elif kind == 4:    # many vertices inside one voxel: no crossing at all
+            c = np.floor(rng.uniform(1.0, hi - 1.0, (1, 3))) + rng.uniform(0.05, 0.95, (int(rng.integers(2, 200)), 3))
+        else:              # lattice-aligned vertices (ties between axes)
+            c = np.round(rng.uniform(0.0, hi, (int(rng.integers(2, 40)), 3)) * 2.0) / 2.0
+        curves.append(np.ascontiguousarray(c, dtype=np.float64))
+    pts = np.concatenate(curves)
+    off = np.concatenate([[0], np.cumsum([len(c) for c in curves])]).astype(np.int64)
+    attrs = rng.uniform(0.0, 1.0, len(pts))
+    m, ref = both(lv, oracle, (pts, attrs, off), dims, 16)
+    assert_model_equal(m, as_dict(ref))
+    assert m.dropped_overflow == ref.dropped_overflow
+    assert m.segment_count > 20000
+
+
 def test_empty_model(lv, oracle):
     dims = (4, 4, 4)
     pts = np.array([[1.1, 1.1, 1.1], [1.2, 1.3, 1.4]])
