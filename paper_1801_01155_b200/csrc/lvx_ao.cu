@@ -164,6 +164,13 @@ ao_bake_brick_kernel(const u8 *__restrict__ counts, int rx, int ry, int rz, int 
 #ifndef LVX_AO_F64
 #define LVX_AO_F64 0
 #endif
+#ifndef LVX_AO_TABLE
+#define LVX_AO_TABLE 1
+#endif
+#ifndef LVX_AO_STEPS
+#define LVX_AO_STEPS 6
+#endif
+constexpr int kBakeSteps = LVX_AO_STEPS;  // march steps whose parameters a thread keeps in registers
 constexpr int kBakeBatch = LVX_AO_BATCH;
 constexpr int kBakeThreads = 256;
 // the staged density: float32 as stored (widened per corner load), or widened once at staging
@@ -210,7 +217,7 @@ __device__ __forceinline__ double bake_sample(const bake_t *__restrict__ s, int 
     return c0 * gz_ + c1 * fz;
 }
 
-template <bool INTERIOR>
+template <bool INTERIOR, bool TABLE>
 __device__ __forceinline__ void bake_batches(const bake_t *__restrict__ s_l0, const double *__restrict__ s_d,
                                              double *__restrict__ s_res, const unsigned short *__restrict__ s_list,
                                              int n_occ, int batch, int row, int E, int lox, int loy, int loz, int bx, int by,
@@ -218,9 +225,51 @@ __device__ __forceinline__ void bake_batches(const bake_t *__restrict__ s_l0, co
                                              float *__restrict__ out) {
     const int tid = threadIdx.x;
     const double gx = (double)rx, gy = (double)ry, gz = (double)rz;
+    // The march parameters t_1 = step, t_{k+1} = t_k + step (while t_k <= radius) are the same for every
+    // ray: up to kBakeSteps of them are computed ONCE per thread, by the reference's own additions, and
+    // kept in registers (the loop below is fully unrolled, so the indices are static).  Per sample that
+    // takes the float64 add and compare of the loop control off the FP64 pipe, the kernel's bound; so do
+    // multiplying by a step of exactly 1 (x * 1.0 == x) and testing acc >= 1 on the high word (for any
+    // acc the final result is the same: a NaN ends as 1.0 either way).
+    // (TABLE is the host's decision, lvx_ao_bake: the march has 4 .. kBakeSteps steps; a kernel of its
+    // own, so that the plain loop keeps its 60 registers -- 4 blocks per SM at small radii)
+    double tk[kBakeSteps];
+    int n_steps = 0;
+    if (TABLE) {
+        double t = step;
+#pragma unroll
+        for (int k = 0; k < kBakeSteps; ++k) {
+            tk[k] = t;
+            if (t <= radius) n_steps = k + 1;  // (t grows: the steps that qualify are the leading ones)
+            t += step;
+        }
+    }
+    const bool unit_step = step == 1.0;
     for (int e0 = 0; e0 < n_occ; e0 += batch) {
         const int nb = min(batch, n_occ - e0);
         const int items = nb * n_rays;
+        if (TABLE) {
+            for (int w = tid; w < items; w += kBakeThreads) {
+                const int v = w / n_rays, r = w - v * n_rays;
+                const int k = s_list[e0 + v];
+                const double px = (double)(bx + (k & 7)) + 0.5, py = (double)(by + ((k >> 3) & 7)) + 0.5,
+                             pz = (double)(bz + (k >> 6)) + 0.5;
+                const double dx = s_d[3 * r], dy = s_d[3 * r + 1], dz = s_d[3 * r + 2];
+                // density_ray_blocking, _kernels.py:425-445
+                double acc = 0.0;
+#pragma unroll
+                for (int q = 0; q < kBakeSteps; ++q) {
+                    if (q >= n_steps) break;
+                    const double t_cur = tk[q];
+                    const double sx = px + t_cur * dx, sy_ = py + t_cur * dy, sz_ = pz + t_cur * dz;
+                    if (!INTERIOR && (sx < 0.0 || sy_ < 0.0 || sz_ < 0.0 || sx > gx || sy_ > gy || sz_ > gz)) break;
+                    const double smp = bake_sample<INTERIOR>(s_l0, E, lox, loy, loz, rx, ry, rz, sx, sy_, sz_);
+                    acc += unit_step ? smp : smp * step;
+                    if (__double2hiint(acc) >= 0x3FF00000) break;  // acc >= 1.0
+                }
+                s_res[v * row + r] = acc < 1.0 ? acc : 1.0;  // (a saturated ray has acc >= 1)
+            }
+        } else
         for (int w = tid; w < items; w += kBakeThreads) {
             const int v = w / n_rays, r = w - v * n_rays;
             const int k = s_list[e0 + v];
@@ -256,7 +305,10 @@ __device__ __forceinline__ void bake_batches(const bake_t *__restrict__ s_l0, co
     }
 }
 
-__global__ void __launch_bounds__(kBakeThreads)
+// (the table kernel is given the registers of three blocks per SM -- what its shared memory allows at
+// R = 5 anyway; left to itself ptxas stops at 64 and spills: 15.4 instead of 14.9 ms)
+template <bool TABLE>
+__global__ void __launch_bounds__(kBakeThreads, TABLE ? 3 : 4)
 ao_bake_batch_kernel(const u8 *__restrict__ counts, int rx, int ry, int rz, int n_rays, double radius, double step,
                      const double *__restrict__ dirs, const float *__restrict__ l0, int H, int batch, int row,
                      float *__restrict__ out) {
@@ -304,10 +356,10 @@ ao_bake_batch_kernel(const u8 *__restrict__ counts, int rx, int ry, int rz, int 
     // the warp order of the list is arbitrary (atomics); the result per voxel does not depend on it
     const bool interior = lox >= 0 && loy >= 0 && loz >= 0 && lox + E <= rx && loy + E <= ry && loz + E <= rz;
     if (interior)
-        bake_batches<true>(s_l0, s_d, s_res, s_list, n_occ, batch, row, E, lox, loy, loz, bx, by, bz, rx, ry, rz, n_rays,
+        bake_batches<true, TABLE>(s_l0, s_d, s_res, s_list, n_occ, batch, row, E, lox, loy, loz, bx, by, bz, rx, ry, rz, n_rays,
                            radius, step, out);
     else
-        bake_batches<false>(s_l0, s_d, s_res, s_list, n_occ, batch, row, E, lox, loy, loz, bx, by, bz, rx, ry, rz, n_rays,
+        bake_batches<false, TABLE>(s_l0, s_d, s_res, s_list, n_occ, batch, row, E, lox, loy, loz, bx, by, bz, rx, ry, rz, n_rays,
                             radius, step, out);
 }
 
@@ -477,10 +529,21 @@ int lvx_ao_bake(const uint8_t *counts_d, const int32_t dims[3], int32_t n_rays, 
                               E * E * E * sizeof(bake_t);
         static const bool legacy = getenv("LVX_AO_LEGACY") != nullptr;  // developer A/B switch
         if (!legacy && radius < 64.0 && batch >= 1 && need_b <= 200 * 1024) {
+            // the march parameters in registers when there are 4 .. kBakeSteps of them (the same float64
+            // additions the kernels make; see bake_batches)
+            int n_steps = 0;
+            {
+                double t = step;
+                while (t <= radius && n_steps <= kBakeSteps) {
+                    n_steps += 1;
+                    t += step;
+                }
+            }
+            const bool table = LVX_AO_TABLE && n_steps >= 4 && n_steps <= kBakeSteps;
+            auto kernel = table ? ao_bake_batch_kernel<true> : ao_bake_batch_kernel<false>;
             if (need_b > 48 * 1024)
-                LVX_CUDA_CHECK(cudaFuncSetAttribute(ao_bake_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                    (int)need_b));
-            ao_bake_batch_kernel<<<bgrid, kBakeThreads, need_b, (cudaStream_t)stream>>>(
+                LVX_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need_b));
+            kernel<<<bgrid, kBakeThreads, need_b, (cudaStream_t)stream>>>(
                 counts_d, dims[0], dims[1], dims[2], n_rays, radius, step, dirs_d, level0_d, H, batch, row, ao_d);
             LVX_LAUNCH_CHECK();
             return LVX_OK;
