@@ -279,7 +279,10 @@ typedef struct {
  * hitbuf_d: per-thread hit scratch, lvx_render_scratch_bytes() bytes.
  * Every pixel of the image is written exactly once and never read, so img_d may also be
  * pinned host memory mapped into the device's address space (cudaHostAlloc under unified
- * addressing): the image then reaches the host while the frame is still being computed. */
+ * addressing): the image then reaches the host while the frame is still being computed.
+ * lvx_render_wf recognises such a pointer (cudaPointerGetAttributes) and lets a copy engine lay
+ * the pixels of the rays that miss the grid (a constant) from a second stream of its own, joined
+ * inside the call. */
 size_t lvx_render_scratch_bytes(const lvx_camera *cam, const lvx_tiling *tiling);
 int lvx_render(const lvx_camera *cam, const lvx_model *model, const lvx_params *params,
                const lvx_lod *lod, const lvx_tiling *tiling, float *img_d,

@@ -212,6 +212,7 @@ struct WfArgs {
     double rep_radius_base;   // tube_radius * 2^level (raycast.py:425)
     lvx_tiling tl;
     int tiles_x, n_my_tiles;
+    int skip_miss;  // the pixels of rays that miss the grid are written by a copy engine (host image), not by wf_init
     float *img;
     unsigned long long *row_stats;
     // scratch
@@ -366,6 +367,18 @@ __device__ __forceinline__ void write_pixel(const WfArgs &A, u32 o, double a0, d
     reinterpret_cast<float4 *>(A.img)[o] = outp;
 }
 
+// The pixel of a ray that misses the grid, repeated n times: the source of the copy-engine transfers
+// that lay the background of a HOST image (see lvx_render_wf).
+__global__ void __launch_bounds__(256) wf_bgfill_kernel(const WfArgs A, float4 *__restrict__ buf, u32 n) {
+    const lvx_params &p = A.p;
+    float4 outp;  // write_pixel with nothing accumulated (_kernels.py:916-920)
+    outp.x = (float)(0.0 + (1.0 - 0.0) * p.bg[3] * p.bg[0]);
+    outp.y = (float)(0.0 + (1.0 - 0.0) * p.bg[3] * p.bg[1]);
+    outp.z = (float)(0.0 + (1.0 - 0.0) * p.bg[3] * p.bg[2]);
+    outp.w = (float)(0.0 + (1.0 - 0.0) * p.bg[3]);
+    for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) buf[i] = outp;
+}
+
 __device__ __forceinline__ void dda_store(WfRayWalk &r, const LvxDda &d) {
     r.t_cur = d.t_cur;
     r.t_exit = d.t_exit;
@@ -466,7 +479,7 @@ __global__ void __launch_bounds__(kThreadsWf) wf_init_kernel(const WfArgs A) {
             A.rp[slot] = rp;
             A.rpix[slot] = make_uint2((u32)x | ((u32)y << 16), (u32)o);
             live = true;
-        } else {
+        } else if (!A.skip_miss) {
             write_pixel(A, (u32)o, 0.0, 0.0, 0.0, 0.0);
         }
     }
@@ -1723,9 +1736,11 @@ struct WfLayout {
     size_t total;
     size_t ctl, rw, rp, rpix, head, tab_seen, tab_sph, pool_seen, pool_sph, live0, live1, win,
         win_over, item, item_t, fdir, span, rdir, tube, sph, hit, hit_c, hit_next, hit_slot,
-        slot_c, hcnt;
+        slot_c, hcnt, bgfill;
     u32 R, pool_cap, cap_win, capq_item, capq_surv, capq_hit;
 };
+
+constexpr size_t kBgChunk = (size_t)8 << 20;  // background pattern the copy engine repeats over a host image
 
 size_t take(size_t &cur, size_t bytes) {
     const size_t at = (cur + 255) & ~(size_t)255;
@@ -1771,6 +1786,7 @@ WfLayout wf_layout(i64 R, double scale) {
     L.hit_slot = take(c, r * kHitSlots * sizeof(WfHit));
     L.slot_c = take(c, r * kHitSlots * 16);
     L.hcnt = take(c, r * 4);
+    L.bgfill = take(c, kBgChunk);
     L.total = take(c, 0);
     return L;
 }
@@ -1802,6 +1818,7 @@ struct WfTuning {
     int rays_mult = 0;  // 0: by the number of ray slots
     bool debug = false;
     bool pdl = true;  // programmatic dependent launch of the frame's kernels (LVX_WF_PDL=0: plain launches)
+    bool bg_copy = true;  // background of a host image by the copy engine (LVX_WF_BGCOPY=0: by wf_init)
     bool adaptive_burst = true;  // first burst sized by the previous frame's iteration count (LVX_WF_ADAPT=0: always six)
 };
 
@@ -1828,9 +1845,42 @@ const WfTuning &wf_tuning() {
         t.debug = getenv("LVX_WF_DEBUG") != nullptr;
         t.pdl = env_int("LVX_WF_PDL", 1) != 0;
         t.adaptive_burst = env_int("LVX_WF_ADAPT", 1) != 0;
+        t.bg_copy = env_int("LVX_WF_BGCOPY", 1) != 0;
         return t;
     }();
     return T;
+}
+
+// a second stream of the calling thread on the current device, for the copy-engine transfers that run
+// next to a frame (created once)
+struct WfSide {
+    int device = -1;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+WfSide *wf_side() {
+    static thread_local WfSide sides[16];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
+    WfSide &s = sides[dev];
+    if (s.device != dev) {
+        if (cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        if (cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming) != cudaSuccess)
+            return nullptr;
+        s.device = dev;
+    }
+    return &s;
+}
+
+// is p pinned host memory (mapped into the device's address space)?
+bool wf_is_host_pointer(const void *p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
 }
 
 }  // namespace
@@ -2011,6 +2061,29 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
             attr_set = true;
         }
     }
+    // A HOST image (pinned memory the kernels write through its device mapping): two thirds of a frame
+    // like C3 are rays that miss the grid, 22 MB of identical pixels that wf_init would push over PCIe
+    // store by store.  A copy engine lays them instead -- the miss pixel repeated over the WHOLE image,
+    // from an 8 MB pattern in the scratch buffer, on a second stream while init / walk / candidates /
+    // exact run -- and is joined before the first kernel that writes finished pixels (composite).
+    WfSide *side = nullptr;
+    if (tune.bg_copy && !debug && !tiling->compact && wf_is_host_pointer(img_d)) side = wf_side();
+    bool side_joined = true;
+    if (side) {
+        float4 *pat = (float4 *)(base + L.bgfill);
+        const size_t img_bytes = (size_t)cam->width * cam->height * 16;
+        const size_t chunk = img_bytes < kBgChunk ? img_bytes : kBgChunk;
+        wf_bgfill_kernel<<<(unsigned)sms, 256, 0, st>>>(A, pat, (u32)(chunk / 16));
+        LVX_CUDA_CHECK(cudaEventRecord(side->fork, st));
+        LVX_CUDA_CHECK(cudaStreamWaitEvent(side->stream, side->fork, 0));
+        for (size_t off = 0; off < img_bytes; off += chunk) {
+            const size_t n = img_bytes - off < chunk ? img_bytes - off : chunk;
+            LVX_CUDA_CHECK(cudaMemcpyAsync((char *)img_d + off, pat, n, cudaMemcpyDeviceToHost, side->stream));
+        }
+        LVX_CUDA_CHECK(cudaEventRecord(side->join, side->stream));
+        A.skip_miss = 1;
+        side_joined = false;
+    }
     LVX_CUDA_CHECK(wf_launch(pdl, wf_begin_kernel, 1, 64, 0, st, A));
     LVX_CUDA_CHECK(wf_launch(pdl, wf_init_kernel, (unsigned)lvx_ceil_div(R, kThreadsWf), kThreadsWf, 0, st, A));
     LVX_LAUNCH_CHECK();
@@ -2045,6 +2118,10 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
             else if (packed) LVX_CUDA_CHECK(wf_launch(pdl, wf_exact_kernel<false, true>, grid_q, kThreadsExact, 0, st, A, par));
             else LVX_CUDA_CHECK(wf_launch(pdl, wf_exact_kernel<false, false>, grid_q, kThreadsExact, 0, st, A, par));
             WF_DEBUG_SYNC("exact");
+            if (!side_joined) {  // (the background is down before any finished pixel is written)
+                LVX_CUDA_CHECK(cudaStreamWaitEvent(st, side->join, 0));
+                side_joined = true;
+            }
             LVX_CUDA_CHECK(wf_launch(pdl, wf_composite_kernel, grid_rays, kThreadsWf, 0, st, A, par));
             WF_DEBUG_SYNC("composite");
             if (debug) {
@@ -2080,7 +2157,8 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
         }
         g_last_iterations = it;
         g_needed_iterations = host[2] ? (int)host[2] : it;
-        g_last_launches = 2 + it * 5;  // begin, init + (walk, candidates, exact, composite, next) per iteration
+        // begin, init (+ the background pattern) + (walk, candidates, exact, composite, next) per iteration
+        g_last_launches = 2 + (side ? 1 : 0) + it * 5;
         if (host[0] == 0) break;
         LVX_REQUIRE(it < 100000, "wavefront did not converge");
     }
