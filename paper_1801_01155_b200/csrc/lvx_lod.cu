@@ -223,6 +223,9 @@ density_l0_packed_kernel(const u8 *__restrict__ counts, const u32 *__restrict__ 
 // l with coalesced row loads and reduces it three times in shared memory, writing its 8^3 / 4^3 /
 // 2^3 share of levels l+1, l+2, l+3 (as many of them as exist).  One pass over level l, no re-read of
 // the levels in between.
+#ifndef LVX_MIP_DIRECT
+#define LVX_MIP_DIRECT 1
+#endif
 constexpr int kMipP = 8;             // brick edge at the first output level
 constexpr int kMipC = 2 * kMipP;     // child brick edge
 
@@ -255,6 +258,47 @@ mip3_kernel(const float *__restrict__ src, MipDims d0, float *__restrict__ dst1,
     __shared__ float s1[kMipP * kMipP * (kMipP + 1)];
     __shared__ float s2[4 * 4 * 5];
     const int bx = blockIdx.x * kMipP, by = blockIdx.y * kMipP, bz = blockIdx.z * kMipP;
+#if LVX_MIP_DIRECT
+    // The first level straight from global memory: a thread's eight children are four aligned pairs
+    // (x, x+1) -- four 8-byte loads in flight at once, added in the reference's (oz, oy, ox) order in
+    // registers; no staging of the 16^3 child brick, no barrier before the first output.  (The staged
+    // path ran at a third of the HBM peak on its instruction count: index arithmetic, four scalar
+    // shared-memory stores per 16-byte load, eight shared-memory loads per parent.)
+    if (vec4) {  // (rows of an even length, 16-byte aligned base: every pair is 8-byte aligned and in range together)
+        const int tx = threadIdx.x % kMipP, ty = (threadIdx.x / kMipP) % kMipP, tz = threadIdx.x / (kMipP * kMipP);
+        const int x = bx + tx, y = by + ty, z = bz + tz;
+        float v = 0.0f;
+        if (x < d1.x && y < d1.y && z < d1.z) {
+            float2 c[2][2];
+            bool in[2][2];
+#pragma unroll
+            for (int oz = 0; oz < 2; ++oz)
+#pragma unroll
+                for (int oy = 0; oy < 2; ++oy) {
+                    in[oz][oy] = 2 * z + oz < d0.z && 2 * y + oy < d0.y;
+                    c[oz][oy] = make_float2(0.0f, 0.0f);
+                    if (in[oz][oy])
+                        c[oz][oy] = __ldg(reinterpret_cast<const float2 *>(
+                            src + ((i64)(2 * z + oz) * d0.y + (2 * y + oy)) * d0.x + 2 * x));
+                }
+            float acc = 0.0f, cnt = 0.0f;
+#pragma unroll
+            for (int oz = 0; oz < 2; ++oz)
+#pragma unroll
+                for (int oy = 0; oy < 2; ++oy) {
+                    if (in[oz][oy]) {  // (d0.x is even here: both x children exist)
+                        acc = acc + c[oz][oy].x;
+                        cnt = cnt + 1.0f;
+                        acc = acc + c[oz][oy].y;
+                        cnt = cnt + 1.0f;
+                    }
+                }
+            v = acc / cnt;
+            dst1[((i64)z * d1.y + y) * d1.x + x] = v;
+        }
+        s1[(tz * kMipP + ty) * (kMipP + 1) + tx] = v;
+    } else {
+#endif
     if (vec4 && 2 * bx + kMipC <= d0.x) {
         // rows of the child brick as four 16-byte loads (the row starts are 64-byte aligned here)
         for (int idx = threadIdx.x; idx < kMipC * kMipC * kMipC / 4; idx += blockDim.x) {
@@ -288,6 +332,9 @@ mip3_kernel(const float *__restrict__ src, MipDims d0, float *__restrict__ dst1,
         }
         s1[(tz * kMipP + ty) * (kMipP + 1) + tx] = v;
     }
+#if LVX_MIP_DIRECT
+    }
+#endif
     if (n_out < 2) return;
     __syncthreads();
     if (threadIdx.x < 64) {
