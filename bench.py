@@ -484,7 +484,7 @@ def run_ours(args, wl):
                              "frac_of_fp64_pipe_peak_upper_bound": samples * 58 / (t_ao * 1e-3) / fp64_peak,
                              "note": "samples = occupied x rays x floor(R/step) is an upper bound (rays stop at "
                                      "saturation or the grid border); ncu: sm__inst_executed_pipe_fp64 53 % "
-                                     "(profiles/r2p_stage_kernels.txt)"}
+                                     "(profiles/r2q_stage_kernels.txt)"}
             model.ao = lv.precompute_voxel_ao(model, octree, aop)
         return octree, st
 
