@@ -2067,7 +2067,11 @@ int lvx_render_wf(const lvx_camera *cam, const lvx_model *model, const lvx_param
     // from an 8 MB pattern in the scratch buffer, on a second stream while init / walk / candidates /
     // exact run -- and is joined before the first kernel that writes finished pixels (composite).
     WfSide *side = nullptr;
-    if (tune.bg_copy && !debug && !tiling->compact && wf_is_host_pointer(img_d)) side = wf_side();
+    // (only when this call renders the WHOLE image: a share of an in-place tiled frame must not touch
+    // the other shares' pixels)
+    if (tune.bg_copy && !debug && !tiling->compact && tiling->tile_step == 1 && tiling->tile_first == 0 &&
+        wf_is_host_pointer(img_d))
+        side = wf_side();
     bool side_joined = true;
     if (side) {
         float4 *pat = (float4 *)(base + L.bgfill);

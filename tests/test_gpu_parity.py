@@ -321,6 +321,38 @@ def test_frame_written_to_pinned_host_memory_equals_device_frame(lv, synth, monk
         assert out["host"][1] == out["device"][1], kw
 
 
+def test_shares_of_a_frame_rendered_in_place_into_one_host_image(lv, synth):
+    """A host image gets the pixels of the rays that miss the grid from a copy engine -- but only when
+    the call renders the WHOLE image: the shares of an in-place tiled frame (tile k of every 3, not
+    compact) written one after the other into one pinned image must add up to the full frame, each
+    share leaving the others' pixels alone; and a frame larger than the 8 MB pattern the copy engine
+    repeats equals the frame rendered into device memory."""
+    import torch
+    from paper_1801_01155_b200.raycast import FramePlan
+    dims = (24, 24, 24)
+    m = lv.build_voxel_model(lv.CurveSet.from_flat(*synth.turbulence(1500, 50, dims)), lv.GridSpec(dims))
+    oc = lv.build_lod(m)
+    p = lv.RenderParams(base_opacity=0.2, neighbor_mode="on", background=(0.2, 0.4, 0.6, 0.5))
+    for W, H in ((203, 117), (1100, 700)):   # 0.4 MB; 12.3 MB = one and a half patterns
+        cam = lv.default_camera(dims, W, H)
+        full_d = torch.empty((H, W, 4), dtype=torch.float32, device="cuda")
+        st = torch.zeros((H, 3), dtype=torch.int64, device="cuda")
+        FramePlan(cam, m, oc, p, 1, engine="wavefront").launch(full_d, st)
+        whole = torch.full((H, W, 4), -1.0, dtype=torch.float32).pin_memory()
+        st1 = torch.zeros((H, 3), dtype=torch.int64, device="cuda")
+        FramePlan(cam, m, oc, p, 1, engine="wavefront").launch(whole, st1)
+        torch.cuda.synchronize()
+        assert np.array_equal(whole.numpy(), full_d.cpu().numpy()), (W, H)
+        assert torch.equal(st, st1)
+        img = torch.full((H, W, 4), -1.0, dtype=torch.float32).pin_memory()
+        st2 = torch.zeros((H, 3), dtype=torch.int64, device="cuda")
+        for k in (2, 0, 1):
+            FramePlan(cam, m, oc, p, 1, tile_first=k, tile_step=3, engine="wavefront").launch(img, st2)
+        torch.cuda.synchronize()
+        assert np.array_equal(img.numpy(), full_d.cpu().numpy()), (W, H)
+        assert torch.equal(st, st2)
+
+
 def test_model_from_encoded_arrays_only(lv, synth):
     """a model that arrives as (counts, offsets, packed) only -- what a .vxl
     file holds -- is decoded on the device (lvx_decode_packed, model_io.py:151-179): caches
